@@ -1,0 +1,490 @@
+#!/usr/bin/env python
+"""bench.py — Top-K feature frames/s (fwd+bwd, D=512) on B200, BASELINE.json config 3.
+
+One step = one Top-K feature frame, forward + backward, of the config-3 synthetic scene
+(1M Gaussians, 1200x680, D=512, K=3; the reference bench recipe fslam_main.cpp:167-196):
+    prepare_scene (projection, depth sort, tile binning)   render.cpp:73-156
+    geometric pass (alpha blend + Top-K records)           render.cpp:158-240
+    render_feature (Top-K gather)                          render.cpp:301-337
+    backward_feature (dense N x D feature gradient)        backward.cpp:273-321
+    backward_geometric (geometry + pose gradients)         backward.cpp:72-271
+Nothing is cached across steps (tk_invalidate each step); inputs are larger than L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c5] [--impl ours|reference]
+
+Under torchrun (N > 1) the feature dimension is sharded D/N per GPU: every
+rank recomputes the integer Top-K records, gathers/scatters its channel slice, and the rendered
+map is all-gathered with NCCL (tk_allgather_feature).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Top-K feature frames/s (fwd+bwd, D=512) and achieved HBM GB/s at 1/2/4/8 B200"
+CONFIGS = {
+    "c3": dict(n=1_000_000, w=1200, h=680, d=512, k=3, label="config 3: 1M Gaussians, 1200x680, D=512, K=3"),
+    "c1": dict(n=100_000, w=640, h=480, d=512, k=3, label="config 1/2: 100k Gaussians, 640x480, D=512"),
+    "c5": dict(n=4_000_000, w=1920, h=1080, d=768, k=3, label="config 5: 4M Gaussians, 1920x1080, D=768"),
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def host_info():
+    model = ""
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                model = l.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    mem_gb = 0.0
+    try:
+        for l in open("/proc/meminfo"):
+            if l.startswith("MemAvailable"):
+                mem_gb = int(l.split()[1]) / 1e6
+    except Exception:
+        pass
+    return os.cpu_count() or 1, model, mem_gb
+
+
+# ------------------------------------------------------------------------------------ CPU arm
+CPU_SNIPPET = r"""
+import json, sys, time, os
+sys.path.insert(0, {root!r}); sys.path.insert(0, os.path.join({root!r}, "tests"))
+import numpy as np, ctypes as C
+import _oracle as O
+from paper_2602_06991_b200 import synth
+from paper_2602_06991_b200.types import RenderSettings
+cfg = {cfg!r}
+scene, cam, pose, _ = synth.bench_scene(cfg["n"], cfg["w"], cfg["h"], cfg["d"])
+scene.feature = synth.unit_features(scene.size(), cfg["d"], 7, dtype=np.float64)
+s = RenderSettings(top_k=cfg["k"])
+P = cfg["w"] * cfg["h"]
+gf = np.empty(P * cfg["d"], np.float32)
+from paper_2602_06991_b200 import _native as N
+N.synth_lib().tk_synth_hash_fill_f32(gf.size, 11, -1.0, 1.0, gf.ctypes.data)
+gf = gf.astype(np.float64)
+gc = synth.uniform_image((cfg["h"], cfg["w"], 3), 12)
+gd = synth.uniform_image((cfg["h"], cfg["w"]), 13)
+om = O.OracleMap(scene)
+L = O.lib()
+threads = L.orc_max_threads()
+times = np.zeros(6)
+budget, frames, total = {budget!r}, 0, 0.0
+best = None
+while True:
+    L.orc_time_frame(om.h, C.byref(O.pose_c(pose)), C.byref(O.cam_c(cam)), C.byref(O.settings_c(s)),
+                     gf.ctypes.data, gc.ctypes.data, gd.ctypes.data, 1, {fthreads}, times.ctypes.data)
+    frames += 1
+    total += times[5]
+    best = times.copy() if best is None else np.minimum(best, times)
+    if frames >= {max_frames} or total >= budget:
+        break
+print("CPU_RESULT " + json.dumps(dict(frames=frames, seconds=total, threads=int(threads),
+                                     phases=dict(zip(["prepare_scene", "geometric_pass", "render_feature",
+                                                      "backward_feature", "backward_geometric", "frame"],
+                                                     [float(x) for x in best])))))
+"""
+
+
+def run_cpu_oracle(cfg, budget_s, max_frames, timeout_s):
+    cores, model, mem_gb = host_info()
+    # backward_feature keeps one N x D fp64 partial per thread (backward.cpp:290-291): cap threads to RAM
+    per_thread_gb = cfg["n"] * cfg["d"] * 8 / 1e9
+    fthreads = max(1, min(cores, int((mem_gb * 0.5 - 3 * per_thread_gb) / max(per_thread_gb, 1e-9))))
+    code = CPU_SNIPPET.format(root=ROOT, cfg=cfg, budget=budget_s, max_frames=max_frames, fthreads=fthreads)
+    env = dict(os.environ, OMP_NUM_THREADS=str(cores))
+    try:
+        res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout_s,
+                             env=env)
+    except subprocess.TimeoutExpired:
+        return None, f"timeout after {timeout_s}s", cores, model, fthreads
+    for line in res.stdout.splitlines():
+        if line.startswith("CPU_RESULT "):
+            return json.loads(line[len("CPU_RESULT "):]), None, cores, model, fthreads
+    return None, (res.stderr or res.stdout)[-400:], cores, model, fthreads
+
+
+def reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    r, err, cores, model, fthreads = run_cpu_oracle(cfg, budget_s=120.0, max_frames=max(1, args.steps),
+                                                     timeout_s=900)
+    line = {"impl": "reference", "metric": METRIC, "unit": "frames/s", "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg["label"], "top_k": cfg["k"]}}
+    if r is None:
+        line.update({"value": None, "error": err})
+    else:
+        v = r["frames"] / r["seconds"]
+        sample = (f"{r['frames']} full frame(s) of the workload through the oracle port (oracle/src/oracle.cpp, "
+                  f"restating render.cpp/backward.cpp), OpenMP {cores} threads ({fthreads} for backward_feature, "
+                  f"RAM-capped N x D fp64 per-thread partials); host {model}")
+        line.update({"value": v, "ms_per_step": 1000.0 / v,
+                     "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "port",
+                                      "sample": sample, "phases_s": r["phases"]},
+                     "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def main_gpu(args, cfg):
+    import torch
+
+    from paper_2602_06991_b200 import _native as N
+    from paper_2602_06991_b200 import synth
+    from paper_2602_06991_b200.api import to_camera, to_pose, to_settings
+    from paper_2602_06991_b200.types import RenderSettings
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    lib = N.render_lib()
+    slib = N.synth_lib()
+
+    n, W, H, D, K = cfg["n"], cfg["w"], cfg["h"], cfg["d"], args.k or cfg["k"]
+    P = W * H
+    if D % world:
+        raise SystemExit("D must divide by the number of GPUs")
+    Ds = D // world
+    c0 = rank * Ds
+
+    t0 = time.time()
+    scene, cam, pose, _ = synth.bench_scene(n, W, H, D)
+    feat_full = synth.unit_features(scene.size(), D, 7)
+    feat = np.ascontiguousarray(feat_full[:, c0:c0 + Ds])
+    del feat_full
+    n = scene.size()
+    settings = RenderSettings(top_k=K)
+    cpose, ccam, cset = to_pose(pose), to_camera(cam), to_settings(settings)
+
+    h = C.c_void_p()
+    N.check(lib.tk_create(local, C.byref(h)))
+    ctx = h
+    geo = [np.ascontiguousarray(a, np.float64) for a in (scene.mean, scene.log_scale, scene.rotation,
+                                                          scene.opacity_logit, scene.color)]
+    view = N.tk_scene_view(n, Ds, *(a.ctypes.data for a in geo), feat.ctypes.data, scene.generation)
+    N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
+
+    if world > 1:
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            N.check(lib.tk_comm_unique_id(uid))
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, 0)
+        uid = (C.c_uint8 * 128)(*t.tolist())
+        N.check(lib.tk_comm_init(ctx, uid, world, rank, D))
+
+    dev = torch.device("cuda", local)
+    gF_host = np.empty(P * Ds, np.float32)
+    slib.tk_synth_hash_fill_f32(gF_host.size, 11 + rank, -1.0, 1.0, gF_host.ctypes.data)
+    gC_host = synth.uniform_image((H, W, 3), 12)
+    gD_host = synth.uniform_image((H, W), 13)
+    gF = torch.from_numpy(gF_host).to(dev)
+    gC = torch.from_numpy(gC_host).to(dev)
+    gD = torch.from_numpy(gD_host).to(dev)
+    Ffull = torch.empty(P * D, dtype=torch.float32, device=dev) if world > 1 else None
+    grads = N.tk_geom_grads()
+    grads.mem = N.TK_DEVICE
+    setup_s = time.time() - t0
+
+    def step():
+        N.check(lib.tk_invalidate(ctx))
+        N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
+        N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))
+        if world > 1:
+            N.check(lib.tk_allgather_feature(ctx, C.c_void_p(Ffull.data_ptr()), N.TK_DEVICE))
+        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), N.TK_DEVICE, None, N.TK_DEVICE))
+        N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
+                                          C.c_void_p(gC.data_ptr()), C.c_void_p(gD.data_ptr()), N.TK_DEVICE,
+                                          C.byref(grads)))
+
+    stream = torch.cuda.ExternalStream(lib.tk_get_stream(ctx), device=dev)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    N.check(lib.tk_synchronize(ctx))
+
+    # records statistics (outside timing): distinct Gaussians referenced U, valid slots M
+    idx_np = np.empty(P * K, np.int32)
+    rec_out = N.tk_geom_out(N.TK_HOST, None, None, None, idx_np.ctypes.data, None, None, None, 0, 0)
+    N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.byref(rec_out)))
+    valid = idx_np[idx_np >= 0]
+    U = int(np.unique(valid).size)
+    M = int(valid.size)
+
+    # ---- timed region (device-resident inputs)
+    launches0 = lib.tk_kernel_launches(ctx)
+    N.check(lib.tk_profile_read(ctx, None, None, 1))
+    N.check(lib.tk_profile_enable(ctx, 1))
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    N.check(lib.tk_synchronize(ctx))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    barrier()
+    clk = clocks.stop()
+    N.check(lib.tk_profile_enable(ctx, 0))
+    ms = ev0.elapsed_time(ev1)
+    launches = lib.tk_kernel_launches(ctx) - launches0
+    ph_ms = (C.c_double * len(N.PHASES))()
+    ph_cnt = (C.c_int64 * len(N.PHASES))()
+    N.check(lib.tk_profile_read(ctx, ph_ms, ph_cnt, 1))
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = args.steps / (ms / 1000.0)
+
+    phases = {name: {"ms_per_step": ph_ms[i] / args.steps, "launch_groups": int(ph_cnt[i])}
+              for i, name in enumerate(N.PHASES) if ph_cnt[i]}
+
+    # ---- roofline of the dominant HBM-bound kernel (algorithmic bytes per launch / event time)
+    peak, peak_kind = load_peaks()
+    bytes_gather = P * Ds * 4 + U * Ds * 4 + P * K * (4 + 8) + P
+    bytes_fbwd = P * Ds * 4 + n * Ds * 4 + M * (4 + 4) + (n + 1) * 4
+    cand = {
+        "gather": (bytes_gather, ph_ms[2] / max(1, ph_cnt[2])),
+        "fbwd": (bytes_fbwd, ph_ms[4] / max(1, ph_cnt[4])),
+    }
+    dom = max(cand, key=lambda k: cand[k][1])
+    b_dom, t_dom = cand[dom]
+    achieved = b_dom / (t_dom / 1000.0) / 1e9 if t_dom > 0 else 0.0
+    roof = {"kernel": {"gather": "k_gather (render_feature)", "fbwd": "k_feat_bwd (backward_feature)"}[dom],
+            "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
+    feat_bytes = bytes_gather + bytes_fbwd
+    feat_ms = ph_ms[2] / max(1, ph_cnt[2]) + (ph_ms[3] / max(1, ph_cnt[3])) + ph_ms[4] / max(1, ph_cnt[4])
+    feature_path = {"algorithmic_bytes": feat_bytes, "ms": feat_ms,
+                    "achieved_gbs": feat_bytes / (feat_ms / 1000.0) / 1e9 if feat_ms > 0 else 0.0}
+
+    # ---- e2e through the C ABI with pinned host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpose, ccam, cset, n, Ds, P,
+                      K, max(2, min(args.steps, args.e2e_steps)), stream, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r, err, cores, model, fthreads = run_cpu_oracle(cfg, budget_s=20.0, max_frames=1, timeout_s=600)
+        if r is not None:
+            cpu = {"value": r["frames"] / r["seconds"], "unit": "frames/s", "cores": cores, "kind": "port",
+                   "sample": f"{r['frames']} full frame(s) of this workload through the oracle port "
+                             f"(OpenMP {cores} threads, {fthreads} for backward_feature: RAM cap on its per-thread "
+                             f"N x D fp64 partials); host {model}",
+                   "phases_s": r["phases"]}
+        else:
+            cpu = {"value": None, "unit": "frames/s", "cores": cores, "kind": "port", "sample": f"not run: {err}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "data": "synthetic",
+            "config": {"workload": cfg["label"], "gaussians": n, "width": W, "height": H, "feature_dim": D,
+                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": f"feature-dim shard d{world}",
+                       "l2": "inputs larger than L2 (features %.2f GB, F %.2f GB)" % (n * D * 4 / 1e9,
+                                                                                        P * D * 4 / 1e9),
+                       "records": {"distinct_gaussians": U, "valid_slots": M}},
+            "hbm_gbs": feature_path["achieved_gbs"],
+            "roofline": roof, "feature_path": feature_path, "phases": phases,
+            "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    lib.tk_destroy(ctx)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpose, ccam, cset, n, Ds, P, K, steps,
+            stream, dist):
+    """Drop-in use: host scene + upstream grads in, host render + gradients out, every step."""
+    def pinned(shape, dtype):
+        t = torch.empty(int(np.prod(shape)), dtype=dtype, pin_memory=True)
+        return t, t.numpy().reshape(shape)
+
+    keep = []
+
+    def pin_copy(a):
+        t, v = pinned(a.shape, {np.float64: torch.float64, np.float32: torch.float32}[a.dtype.type])
+        v[...] = a
+        keep.append(t)
+        return v
+
+    g_pin = [pin_copy(a) for a in geo]
+    f_pin = pin_copy(feat)
+    gF_pin = pin_copy(gF_host)
+    gC_pin = pin_copy(gC_host)
+    gD_pin = pin_copy(gD_host)
+    outs = {}
+    for name, shape, dt in [("color", P * 3, torch.float64), ("depth", P, torch.float64), ("alpha", P, torch.float64),
+                            ("index", P * K, torch.int32), ("weight", P * K, torch.float64),
+                            ("count", P, torch.uint8), ("contrib", n, torch.float64), ("F", P * Ds, torch.float32),
+                            ("df", n * Ds, torch.float32), ("gmean", n * 3, torch.float64),
+                            ("gls", n * 3, torch.float64), ("grot", n * 4, torch.float64),
+                            ("gop", n, torch.float64), ("gcol", n * 3, torch.float64)]:
+        t, v = pinned((shape,), dt)
+        keep.append(t)
+        outs[name] = v
+    view = N.tk_scene_view(n, Ds, *(a.ctypes.data for a in g_pin), f_pin.ctypes.data, 0)
+    gout = N.tk_geom_out(N.TK_HOST, *(outs[x].ctypes.data for x in ("color", "depth", "alpha", "index", "weight",
+                                                                    "count", "contrib")), 0, 0)
+    gg = N.tk_geom_grads(N.TK_HOST, *(outs[x].ctypes.data for x in ("gmean", "gls", "grot", "gop", "gcol")))
+    h2d = sum(a.nbytes for a in g_pin) + f_pin.nbytes + gF_pin.nbytes + gC_pin.nbytes + gD_pin.nbytes
+    d2h = sum(v.nbytes for v in outs.values()) + 6 * 8
+
+    def step():
+        N.check(lib.tk_invalidate(ctx))
+        N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
+        N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.byref(gout)))
+        N.check(lib.tk_render_feature(ctx, None, C.c_void_p(outs["F"].ctypes.data), N.TK_HOST))
+        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF_pin.ctypes.data), N.TK_HOST,
+                                        C.c_void_p(outs["df"].ctypes.data), N.TK_HOST))
+        N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
+                                          C.c_void_p(gC_pin.ctypes.data), C.c_void_p(gD_pin.ctypes.data), N.TK_HOST,
+                                          C.byref(gg)))
+
+    step()
+    N.check(lib.tk_synchronize(ctx))
+    if dist:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    return {"value": steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d * world),
+            "d2h_bytes_per_step": int(d2h * world), "steps": steps, "ms_per_step": ms / steps,
+            "path": "C ABI with pinned host buffers: scene upload, render_geometric, render_feature, "
+                    "backward_feature, backward_geometric (host in/out)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = dict(CONFIGS[args.config])
+    if args.k:
+        cfg["k"] = args.k
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+        return
+    main_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

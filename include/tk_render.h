@@ -1,0 +1,205 @@
+/*
+ * tk_render.h — C ABI of the B200-native Top-K feature-render path (libtkrender.so).
+ *
+ * Drop-in boundary for the reference renderer API (proj/include/fslam/raster/render.hpp,
+ * backward.hpp).  Plain pointers and sizes only; every call is enqueued on the context's CUDA
+ * stream and returns a status.  On error the status is non-zero and tk_last_error() holds the
+ * message; the C++ mirror (include/tk/fslam_raster.hpp) rethrows it as std::runtime_error
+ * with the reference's message text.
+ *
+ * Entry point                      replaces (reference, /root/reference/proj/...)
+ * ------------------------------   -----------------------------------------------------------
+ * tk_scene_upload                  SceneMap / Gaussian3D buffers (map/scene_map.hpp:16-27,
+ *                                  core/types.hpp:25-44) -> device-resident SoA mirror
+ * tk_prepare_scene                 raster_detail::prepare_scene   (raster/render.hpp:99-100)
+ * tk_prepared_export               raster_detail::PreparedScene    (raster/render.hpp:84-92)
+ * tk_render_geometric              render_geometric               (raster/render.hpp:60-61)
+ * tk_render_feature                render_feature                 (raster/render.hpp:66)
+ * tk_render_feature_full_blend     render_feature_full_blend      (raster/render.hpp:70-71)
+ * tk_backward_feature              backward_feature               (raster/backward.hpp:33-34)
+ * tk_backward_geometric            backward_geometric             (raster/backward.hpp:27-29)
+ * tk_comm_* / tk_allgather_feature multi-GPU D-sharding (no reference counterpart)
+ *
+ * Memory spaces: every buffer argument is tagged TK_HOST or TK_DEVICE.  Host buffers are
+ * copied in/out inside the call (pinned memory from tk_host_alloc is fastest); device buffers
+ * are used in place.  Device results that the caller did not ask to receive stay resident in
+ * the context and can be read with tk_device_view().
+ */
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TK_ABI_VERSION 1
+
+typedef enum {
+    TK_OK = 0,
+    TK_ERR_STALE_INDEX = 1, /* render.cpp:307-310, backward.cpp:279-282 */
+    TK_ERR_BAD_ARG = 2,     /* shape / argument mismatch */
+    TK_ERR_CUDA = 3,
+    TK_ERR_NCCL = 4,
+    TK_ERR_OOM = 5,
+    TK_ERR_STATE = 6 /* e.g. no scene uploaded, no records rendered */
+} tk_status;
+
+enum { TK_HOST = 0, TK_DEVICE = 1 };
+
+typedef struct tk_ctx tk_ctx;
+
+typedef struct { /* CameraIntrinsics, core/types.hpp:15-21 */
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane, far_plane;
+} tk_camera;
+
+typedef struct { /* Pose (world-to-camera), core/pose.hpp:11-19; quaternion used unnormalised */
+    double qw, qx, qy, qz;
+    double tx, ty, tz;
+} tk_pose;
+
+typedef struct { /* RenderSettings, raster/render.hpp:14-21 */
+    int32_t top_k;
+    int32_t tile_size;
+    double transmittance_floor;
+    double background[3];
+    double cov2d_dilation;
+    double alpha_clamp;
+} tk_settings;
+
+typedef struct { /* Gaussian SoA view; rotation is (w,x,y,z) */
+    int64_t n;
+    int32_t d;              /* feature channels held by this context (a shard under tk_comm) */
+    const double* mean;     /* n x 3 */
+    const double* log_scale;/* n x 3 */
+    const double* rotation; /* n x 4 */
+    const double* opacity_logit; /* n */
+    const double* color;    /* n x 3 */
+    const float* feature;   /* n x d, fp32; NULL keeps the resident features (n, d unchanged) */
+    uint64_t generation;    /* SceneMap::generation (scene_map.hpp:16) */
+} tk_scene_view;
+
+typedef struct { /* TopKGrid, raster/render.hpp:27-44 (slot = (y*W+x)*k + j) */
+    int32_t width, height, k;
+    const int32_t* index;  /* W*H*k, -1 unused */
+    const double* weight;  /* W*H*k */
+    const uint8_t* count;  /* W*H */
+    int32_t mem;           /* TK_HOST / TK_DEVICE */
+} tk_topk_view;
+
+typedef struct { /* RenderOutput, raster/render.hpp:46-55; NULL pointers are skipped */
+    int32_t mem;
+    double* color;         /* H*W*3 */
+    double* depth;         /* H*W */
+    double* alpha;         /* H*W, sum of weights (render.cpp:222) */
+    int32_t* topk_index;   /* H*W*k */
+    double* topk_weight;   /* H*W*k */
+    uint8_t* topk_count;   /* H*W */
+    double* contributions; /* n */
+    uint64_t generation;   /* out: stamped (render.cpp:167-168) */
+    int64_t map_size;      /* out */
+} tk_geom_out;
+
+typedef struct { /* GeomGrads, raster/backward.hpp:15-22; NULL pointers are skipped */
+    int32_t mem;
+    double* mean;          /* n x 3 */
+    double* log_scale;     /* n x 3 */
+    double* rotation;      /* n x 4 (w,x,y,z) */
+    double* opacity_logit; /* n */
+    double* color;         /* n x 3 */
+    double pose_twist[6];  /* out: [nu, omega] */
+} tk_geom_grads;
+
+typedef struct { /* resident device buffers of the last calls (read-only views) */
+    const double* color;
+    const double* depth;
+    const double* alpha;
+    const int32_t* topk_index;
+    const double* topk_weight;
+    const uint8_t* topk_count;
+    const double* contributions;
+    const float* feature_out;   /* render_feature result, H*W*d */
+    const float* feature_grad;  /* backward_feature result, n*d */
+    float* grad_feature_in;     /* staging buffer for dL/dF, H*W*d (writable) */
+    const double* mean;         /* scene mirror */
+    float* feature;             /* scene features, n*d (writable: in-place optimiser updates) */
+    int64_t n;
+    int32_t d, width, height, k;
+} tk_device_view;
+
+void tk_default_settings(tk_settings* s);
+const char* tk_last_error(void);
+int32_t tk_abi_version(void);
+
+tk_status tk_create(int32_t device, tk_ctx** out);
+tk_status tk_destroy(tk_ctx* ctx);
+tk_status tk_synchronize(tk_ctx* ctx);
+void* tk_get_stream(tk_ctx* ctx); /* cudaStream_t */
+
+tk_status tk_host_alloc(size_t bytes, void** out); /* pinned host memory */
+tk_status tk_host_free(void* p);
+
+tk_status tk_scene_upload(tk_ctx* ctx, const tk_scene_view* scene, int32_t mem);
+tk_status tk_device_view_get(tk_ctx* ctx, tk_device_view* out);
+
+tk_status tk_prepare_scene(tk_ctx* ctx, const tk_pose* pose, const tk_camera* cam,
+                           const tk_settings* s, int64_t* n_entries, int64_t* n_tile_entries,
+                           int32_t* tiles_x, int32_t* tiles_y);
+/* host outputs: entries7 = n_entries x {mx,my,ixx,ixy,iyy,z,opacity}, src, tile_offsets
+ * (tiles+1), tile_entries (n_tile_entries) — the PreparedScene of the last prepare. */
+tk_status tk_prepared_export(tk_ctx* ctx, double* entries7, int32_t* src, int32_t* tile_offsets,
+                             int32_t* tile_entries);
+
+tk_status tk_render_geometric(tk_ctx* ctx, const tk_pose* pose, const tk_camera* cam,
+                              const tk_settings* s, tk_geom_out* out);
+/* topk == NULL: the records of the last tk_render_geometric on this context. */
+tk_status tk_render_feature(tk_ctx* ctx, const tk_topk_view* topk, float* out, int32_t out_mem);
+tk_status tk_render_feature_full_blend(tk_ctx* ctx, const tk_pose* pose, const tk_camera* cam,
+                                       const tk_settings* s, float* out, int32_t out_mem);
+/* grad_feature: H*W*d fp32 (NULL + TK_DEVICE: the context's grad_feature_in buffer). out: n*d */
+tk_status tk_backward_feature(tk_ctx* ctx, const tk_topk_view* topk, const float* grad_feature,
+                              int32_t grad_mem, float* out, int32_t out_mem);
+/* grad_color H*W*3, grad_depth H*W (may be NULL = empty image, backward.cpp:104) */
+tk_status tk_backward_geometric(tk_ctx* ctx, const tk_pose* pose, const tk_camera* cam,
+                                const tk_settings* s, const double* grad_color,
+                                const double* grad_depth, int32_t grad_mem, tk_geom_grads* out);
+
+/* Multi-GPU feature-dimension sharding (one process per GPU, NCCL over NVLink). */
+tk_status tk_comm_unique_id(uint8_t id[128]);
+tk_status tk_comm_init(tk_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank,
+                       int32_t d_total);
+/* All-gather of every rank's [H*W][d_shard] slice of the last render_feature into the full
+ * H*W*d_total HWC map (channel-interleaved), on every rank. */
+tk_status tk_allgather_feature(tk_ctx* ctx, float* out, int32_t out_mem);
+tk_status tk_allreduce_sum_f64(tk_ctx* ctx, double* values, int32_t count); /* host values */
+
+/* Drop the cached PreparedScene / forward state: the next call re-projects, re-sorts and
+ * re-bins (the reference recomputes prepare_scene in every call, render.cpp:295). */
+tk_status tk_invalidate(tk_ctx* ctx);
+
+/* Profiling: number of kernels this context launched since creation. */
+int64_t tk_kernel_launches(tk_ctx* ctx);
+
+/* Per-phase device time (CUDA events on the context stream).  Phases: */
+enum {
+    TK_PHASE_PREPARE = 0,      /* projection + depth sort + tile binning + materialise */
+    TK_PHASE_GEOM_FWD = 1,     /* geometric pass (alpha blend + Top-K) */
+    TK_PHASE_GATHER = 2,       /* Top-K feature gather */
+    TK_PHASE_FBWD_INDEX = 3,   /* feature backward: slot keys + radix sort + segments */
+    TK_PHASE_FBWD = 4,         /* feature backward: segmented reduction kernel */
+    TK_PHASE_GEOM_BWD = 5,     /* geometric backward sweep */
+    TK_PHASE_CHAIN = 6,        /* per-Gaussian chain rule + twist reduction */
+    TK_PHASE_FULL_BLEND = 7,   /* full-blend feature pass */
+    TK_PHASE_ALLGATHER = 8,    /* NCCL all-gather + interleave */
+    TK_PHASE_COPY = 9,         /* host <-> device copies made inside calls */
+    TK_NUM_PHASES = 10
+};
+tk_status tk_profile_enable(tk_ctx* ctx, int32_t on);
+/* ms[TK_NUM_PHASES], counts[TK_NUM_PHASES] accumulated since the last reset (synchronises). */
+tk_status tk_profile_read(tk_ctx* ctx, double* ms, int64_t* counts, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif

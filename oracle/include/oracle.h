@@ -1,0 +1,132 @@
+/*
+ * oracle.h — C ABI of the CPU fp64 restatement of the reference renderer.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This library is the parity checker for the
+ * B200 path and the CPU baseline of bench.py.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load it.  The product library (paper_2602_06991_b200/) never links,
+ * imports or calls anything under oracle/.
+ *
+ * It restates, function by function, the reference's raster path
+ * (/root/reference/proj, read-only, cannot be built here: Eigen3, libpng,
+ * doctest and CLI11 are absent — see DESIGN.md "Oracle"):
+ *   core/types.hpp:12-44, core/pose.hpp:16, core/projection.cpp:7-35,
+ *   raster/render.cpp:34-343, raster/backward.cpp:35-321,
+ *   raster/reference.cpp:22-121.
+ * Bit-level pinning: the reference runs its small fixed-size products through
+ * Eigen (not vendored, version unpinned); this restatement fixes one
+ * summation order (left to right) and is compiled with -ffp-contract=off and
+ * no -march, like the reference build (proj/CMakeLists.txt:7-9).  It is pinned
+ * to the reference's own known-answer tests at their stated tolerances
+ * (tests/test_oracle_kats.py).
+ */
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Same field layout as tk_camera / tk_pose / tk_settings in include/tk_render.h. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double near_plane, far_plane;
+} orc_camera; /* CameraIntrinsics, types.hpp:15-21 */
+
+typedef struct {
+    double qw, qx, qy, qz; /* world-to-camera rotation (not normalised on use, pose.hpp:16) */
+    double tx, ty, tz;
+} orc_pose; /* Pose, pose.hpp:11-19 */
+
+typedef struct {
+    int32_t top_k;
+    int32_t tile_size;
+    double transmittance_floor;
+    double background[3];
+    double cov2d_dilation;
+    double alpha_clamp;
+} orc_settings; /* RenderSettings, render.hpp:14-21 */
+
+typedef struct orc_map orc_map;   /* SceneMap (AoS + per-Gaussian heap feature) */
+typedef struct orc_prep orc_prep; /* raster_detail::PreparedScene */
+
+const char* orc_last_error(void);
+
+/* Map: SoA inputs are copied into the reference's AoS layout. features: n*d doubles. */
+orc_map* orc_map_create(int64_t n, int32_t d, const double* mean, const double* log_scale,
+                        const double* rotation_wxyz, const double* opacity_logit,
+                        const double* color, const double* feature, uint64_t generation);
+void orc_map_free(orc_map* m);
+
+/* project_gaussian (projection.cpp:7-35). out7 = mx,my,c00,c01,c10,c11,depth. returns visible. */
+int orc_project_gaussian(const orc_map* m, int64_t i, const orc_pose* pose, const orc_camera* cam,
+                         double dilation, double* out7);
+
+/* prepare_scene (render.cpp:73-156) */
+orc_prep* orc_prepare_scene(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                            const orc_settings* s);
+void orc_prep_sizes(const orc_prep* p, int64_t* n_entries, int64_t* n_tile_entries,
+                    int32_t* tiles_x, int32_t* tiles_y);
+/* entries7: n_entries x {mx,my,ixx,ixy,iyy,z,opacity}; src: n_entries; tile_offsets: tiles+1 */
+void orc_prep_export(const orc_prep* p, double* entries7, int32_t* src, int32_t* tile_offsets,
+                     int32_t* tile_entries);
+void orc_prep_free(orc_prep* p);
+
+/* geometric_pass (render.cpp:158-240) on a prepared scene. Any output may be NULL. */
+int orc_geometric_pass(const orc_prep* p, const orc_map* m, const orc_settings* s, double* color,
+                       double* depth, double* alpha, int32_t* topk_index, double* topk_weight,
+                       uint8_t* topk_count, double* contributions);
+
+/* render_geometric (render.cpp:293-299) */
+int orc_render_geometric(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                         const orc_settings* s, double* color, double* depth, double* alpha,
+                         int32_t* topk_index, double* topk_weight, uint8_t* topk_count,
+                         double* contributions);
+
+/* render_feature (render.cpp:301-337). returns 0 ok, 1 stale index (message in orc_last_error). */
+int orc_render_feature(const orc_map* m, int32_t width, int32_t height, int32_t k,
+                       const int32_t* topk_index, const double* topk_weight,
+                       const uint8_t* topk_count, double* out_feature);
+
+/* render_feature_full_blend (render.cpp:242-289, 339-343) */
+int orc_render_feature_full_blend(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                                  const orc_settings* s, double* out_feature);
+
+/* backward_feature (backward.cpp:273-321). out: n*d dense. */
+int orc_backward_feature(const orc_map* m, int32_t width, int32_t height, int32_t k,
+                         const int32_t* topk_index, const double* topk_weight,
+                         const uint8_t* topk_count, const double* grad_feature, double* out);
+
+/* backward_geometric (backward.cpp:72-271). grad_depth may be NULL (empty image). */
+int orc_backward_geometric(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                           const orc_settings* s, const double* grad_color,
+                           const double* grad_depth, double* g_mean, double* g_log_scale,
+                           double* g_rotation, double* g_opacity_logit, double* g_color,
+                           double* pose_twist);
+
+/* render_reference (reference.cpp:22-121). feature_blend (P*d) and the per-pixel contributor
+ * records are produced only when the pointers are non-NULL.  records: flattened, with
+ * record_offsets[P+1]; call first with rec_index=NULL to get the total count in *n_records. */
+int orc_render_reference(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                         const orc_settings* s, double* color, double* depth, double* alpha,
+                         double* transmittance, double* feature_blend, int32_t* topk_index,
+                         double* topk_weight, uint8_t* topk_count, double* contributions,
+                         int64_t* record_offsets, int32_t* rec_index, double* rec_weight,
+                         int64_t* n_records);
+
+/* Timing harness for the CPU baseline (fslam_main.cpp:28-36 time_call: best of reps,
+ * steady_clock).  Times each reference function separately on the given inputs and writes
+ * seconds into times[6] = {prepare_scene, geometric_pass, render_feature, backward_feature,
+ * backward_geometric, frame_total}.  grad_* are the upstream gradients.  Returns threads used. */
+int orc_time_frame(const orc_map* m, const orc_pose* pose, const orc_camera* cam,
+                   const orc_settings* s, const double* grad_feature, const double* grad_color,
+                   const double* grad_depth, int reps, int feature_threads, double* times);
+
+int orc_max_threads(void);
+void orc_set_threads(int n);
+
+#ifdef __cplusplus
+}
+#endif

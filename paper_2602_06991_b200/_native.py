@@ -1,0 +1,175 @@
+"""ctypes binding of the C ABI in include/tk_render.h and include/tk_synth.h.
+
+The product path is the CUDA library lib/libtkrender.so; there is no CPU fallback.  Loading
+fails loudly if the library is missing (run ``python -m paper_2602_06991_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "lib")
+RENDER_LIB = os.path.join(LIB_DIR, "libtkrender.so")
+SYNTH_LIB = os.path.join(LIB_DIR, "libtk_synth.so")
+
+TK_HOST, TK_DEVICE = 0, 1
+TK_OK, TK_ERR_STALE_INDEX, TK_ERR_BAD_ARG, TK_ERR_CUDA, TK_ERR_NCCL, TK_ERR_OOM, TK_ERR_STATE = range(7)
+
+dbl_p = C.POINTER(C.c_double)
+flt_p = C.POINTER(C.c_float)
+i32_p = C.POINTER(C.c_int32)
+u8_p = C.POINTER(C.c_uint8)
+i64_p = C.POINTER(C.c_int64)
+
+
+class tk_camera(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32), ("near_plane", C.c_double),
+                ("far_plane", C.c_double)]
+
+
+class tk_pose(C.Structure):
+    _fields_ = [("qw", C.c_double), ("qx", C.c_double), ("qy", C.c_double), ("qz", C.c_double),
+                ("tx", C.c_double), ("ty", C.c_double), ("tz", C.c_double)]
+
+
+class tk_settings(C.Structure):
+    _fields_ = [("top_k", C.c_int32), ("tile_size", C.c_int32), ("transmittance_floor", C.c_double),
+                ("background", C.c_double * 3), ("cov2d_dilation", C.c_double), ("alpha_clamp", C.c_double)]
+
+
+class tk_scene_view(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p),
+                ("rotation", C.c_void_p), ("opacity_logit", C.c_void_p), ("color", C.c_void_p),
+                ("feature", C.c_void_p), ("generation", C.c_uint64)]
+
+
+class tk_topk_view(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("k", C.c_int32), ("index", C.c_void_p),
+                ("weight", C.c_void_p), ("count", C.c_void_p), ("mem", C.c_int32)]
+
+
+class tk_geom_out(C.Structure):
+    _fields_ = [("mem", C.c_int32), ("color", C.c_void_p), ("depth", C.c_void_p), ("alpha", C.c_void_p),
+                ("topk_index", C.c_void_p), ("topk_weight", C.c_void_p), ("topk_count", C.c_void_p),
+                ("contributions", C.c_void_p), ("generation", C.c_uint64), ("map_size", C.c_int64)]
+
+
+class tk_geom_grads(C.Structure):
+    _fields_ = [("mem", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p), ("rotation", C.c_void_p),
+                ("opacity_logit", C.c_void_p), ("color", C.c_void_p), ("pose_twist", C.c_double * 6)]
+
+
+class tk_device_view(C.Structure):
+    _fields_ = [("color", C.c_void_p), ("depth", C.c_void_p), ("alpha", C.c_void_p),
+                ("topk_index", C.c_void_p), ("topk_weight", C.c_void_p), ("topk_count", C.c_void_p),
+                ("contributions", C.c_void_p), ("feature_out", C.c_void_p), ("feature_grad", C.c_void_p),
+                ("grad_feature_in", C.c_void_p), ("mean", C.c_void_p), ("feature", C.c_void_p),
+                ("n", C.c_int64), ("d", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("k", C.c_int32)]
+
+
+class tk_synth_arrays(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p),
+                ("rotation", C.c_void_p), ("opacity_logit", C.c_void_p), ("color", C.c_void_p),
+                ("feature", C.c_void_p)]
+
+
+class tk_synth_spec(C.Structure):
+    _fields_ = [("room_min", C.c_double * 3), ("room_max", C.c_double * 3), ("classes", C.c_int32),
+                ("feature_dim", C.c_int32), ("spacing", C.c_double), ("jitter", C.c_double),
+                ("opacity", C.c_double), ("boxes", C.c_int32), ("seed", C.c_uint64)]
+
+
+# (name, restype, argtypes) of every symbol include/tk_render.h declares.
+RENDER_SYMBOLS = [
+    ("tk_default_settings", None, [C.POINTER(tk_settings)]),
+    ("tk_last_error", C.c_char_p, []),
+    ("tk_abi_version", C.c_int32, []),
+    ("tk_create", C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    ("tk_destroy", C.c_int, [C.c_void_p]),
+    ("tk_synchronize", C.c_int, [C.c_void_p]),
+    ("tk_get_stream", C.c_void_p, [C.c_void_p]),
+    ("tk_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    ("tk_host_free", C.c_int, [C.c_void_p]),
+    ("tk_scene_upload", C.c_int, [C.c_void_p, C.POINTER(tk_scene_view), C.c_int32]),
+    ("tk_device_view_get", C.c_int, [C.c_void_p, C.POINTER(tk_device_view)]),
+    ("tk_prepare_scene", C.c_int, [C.c_void_p, C.POINTER(tk_pose), C.POINTER(tk_camera), C.POINTER(tk_settings),
+                                   i64_p, i64_p, i32_p, i32_p]),
+    ("tk_prepared_export", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tk_render_geometric", C.c_int, [C.c_void_p, C.POINTER(tk_pose), C.POINTER(tk_camera),
+                                      C.POINTER(tk_settings), C.POINTER(tk_geom_out)]),
+    ("tk_render_feature", C.c_int, [C.c_void_p, C.POINTER(tk_topk_view), C.c_void_p, C.c_int32]),
+    ("tk_render_feature_full_blend", C.c_int, [C.c_void_p, C.POINTER(tk_pose), C.POINTER(tk_camera),
+                                               C.POINTER(tk_settings), C.c_void_p, C.c_int32]),
+    ("tk_backward_feature", C.c_int, [C.c_void_p, C.POINTER(tk_topk_view), C.c_void_p, C.c_int32, C.c_void_p,
+                                      C.c_int32]),
+    ("tk_backward_geometric", C.c_int, [C.c_void_p, C.POINTER(tk_pose), C.POINTER(tk_camera),
+                                        C.POINTER(tk_settings), C.c_void_p, C.c_void_p, C.c_int32,
+                                        C.POINTER(tk_geom_grads)]),
+    ("tk_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("tk_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
+    ("tk_allgather_feature", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    ("tk_allreduce_sum_f64", C.c_int, [C.c_void_p, dbl_p, C.c_int32]),
+    ("tk_kernel_launches", C.c_int64, [C.c_void_p]),
+    ("tk_invalidate", C.c_int, [C.c_void_p]),
+    ("tk_profile_enable", C.c_int, [C.c_void_p, C.c_int32]),
+    ("tk_profile_read", C.c_int, [C.c_void_p, dbl_p, i64_p, C.c_int32]),
+]
+
+PHASES = ["prepare", "geom_fwd", "gather", "fbwd_index", "fbwd", "geom_bwd", "chain", "full_blend", "allgather",
+          "copy"]
+
+SYNTH_SYMBOLS = [
+    ("tk_synth_default_spec", None, [C.POINTER(tk_synth_spec)]),
+    ("tk_synth_random_scene", None, [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                                     C.POINTER(tk_synth_arrays)]),
+    ("tk_synth_build_scene", C.c_int64, [C.POINTER(tk_synth_spec), C.POINTER(tk_synth_arrays), C.c_void_p]),
+    ("tk_synth_trajectory", C.c_int, [C.c_int32, C.c_int32, C.POINTER(tk_synth_spec), C.c_void_p]),
+    ("tk_synth_unit_features", None, [C.c_int64, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
+    ("tk_synth_uniform_fill", None, [C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_void_p]),
+    ("tk_synth_hash_fill_f32", None, [C.c_int64, C.c_uint64, C.c_float, C.c_float, C.c_void_p]),
+]
+
+_render = None
+_synth = None
+
+
+def _bind(lib, symbols):
+    for name, res, args in symbols:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def render_lib():
+    """The CUDA library.  Raises if it is not built: there is no fallback path."""
+    global _render
+    if _render is None:
+        if not os.path.exists(RENDER_LIB):
+            raise ImportError(f"{RENDER_LIB} missing: build it with `python -m paper_2602_06991_b200.build`")
+        _render = _bind(C.CDLL(RENDER_LIB, mode=C.RTLD_GLOBAL), RENDER_SYMBOLS)
+    return _render
+
+
+def synth_lib():
+    global _synth
+    if _synth is None:
+        if not os.path.exists(SYNTH_LIB):
+            raise ImportError(f"{SYNTH_LIB} missing: build it with `python -m paper_2602_06991_b200.build`")
+        _synth = _bind(C.CDLL(SYNTH_LIB), SYNTH_SYMBOLS)
+    return _synth
+
+
+class TkError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+
+
+def check(status: int) -> None:
+    if status != TK_OK:
+        msg = render_lib().tk_last_error()
+        raise TkError(status, msg.decode() if msg else f"tk status {status}")

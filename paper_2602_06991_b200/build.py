@@ -1,0 +1,90 @@
+"""Build the native libraries in-tree (nvcc / g++ only; no torch extension machinery).
+
+  lib/libtkrender.so   sm_100a CUDA kernels + the C ABI of include/tk_render.h
+  lib/libtk_synth.so   host C++ synthetic-input generators (include/tk_synth.h)
+
+The geometry TUs (prepare.cu, geometric.cu) are compiled with --fmad=false so their fp64
+arithmetic rounds like the reference's x86-64 build (no FMA contraction); the feature TU is
+fp32 and keeps FMA.  Run:  python -m paper_2602_06991_b200.build
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "lib")
+BUILD = os.path.join(ROOT, "build", "native")
+INCLUDE = os.path.join(ROOT, "include")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
+              "--expt-relaxed-constexpr", "-I" + INCLUDE, "-I" + CSRC]
+
+CUDA_UNITS = [
+    ("sort.cu", []),
+    ("prepare.cu", ["--fmad=false"]),
+    ("geometric.cu", ["--fmad=false"]),
+    ("feature.cu", []),
+    ("tk_abi.cu", []),
+]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _run(cmd: list[str], log) -> None:
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    log.write(" ".join(cmd) + "\n" + res.stdout + res.stderr + "\n")
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"build failed: {' '.join(cmd[:3])} ...")
+
+
+def _stale(target: str, sources: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(s) > t for s in sources)
+
+
+def build(force: bool = False, verbose: bool = False) -> dict[str, str]:
+    os.makedirs(LIB, exist_ok=True)
+    os.makedirs(BUILD, exist_ok=True)
+    nvcc = _nvcc()
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers += [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith(".h")]
+    out = {}
+    with open(os.path.join(BUILD, "build.log"), "w") as log:
+        objs = []
+        for src, extra in CUDA_UNITS:
+            s = os.path.join(CSRC, src)
+            o = os.path.join(BUILD, src.replace(".cu", ".o"))
+            if force or _stale(o, [s] + headers):
+                _run([nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", s, "-o", o], log)
+            objs.append(o)
+        so = os.path.join(LIB, "libtkrender.so")
+        if force or _stale(so, objs):
+            _run([nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", so, "-ldl"], log)
+        out["tkrender"] = so
+        synth_src = os.path.join(CSRC, "host", "synth.cpp")
+        synth_so = os.path.join(LIB, "libtk_synth.so")
+        if force or _stale(synth_so, [synth_src, os.path.join(INCLUDE, "tk_synth.h")]):
+            _run(["g++", "-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-I" + INCLUDE, synth_src,
+                  "-o", synth_so], log)
+        out["synth"] = synth_so
+    if verbose:
+        print(open(os.path.join(BUILD, "build.log")).read())
+    return out
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,303 @@
+// feature.cu — K5 Top-K feature gather, K6 full-blend gather, K7 feature backward, K10 stale
+// check.  fp32 features, HBM-bound: one warp per output row, 128-bit loads of the K selected
+// D-channel rows (read-only path) and 128-bit streaming stores of the output row.
+#include "feature.cuh"
+
+namespace tk {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ float4 fma4(float a, float4 x, float4 acc) {
+    acc.x = fmaf(a, x.x, acc.x);
+    acc.y = fmaf(a, x.y, acc.y);
+    acc.z = fmaf(a, x.z, acc.z);
+    acc.w = fmaf(a, x.w, acc.w);
+    return acc;
+}
+
+__device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
+
+// render_feature (render.cpp:319-334): F[p] = sum_j (w_j / sum_w) f[idx_j], sum in slot order.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_gather(GatherParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    for (int64_t px = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; px < p.n_pixels; px += nw) {
+        const int c = p.count[px];
+        int id = 0;
+        double wd = 0.0;
+        if (lane < c) {
+            id = p.index[px * p.k + lane];
+            wd = p.weight[px * p.k + lane];
+        }
+        double sum = 0.0;
+        for (int j = 0; j < c; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
+        const float wn = lane < c ? static_cast<float>(wd / sum) : 0.0f;
+        if (VEC) {
+            const int d4 = D >> 2;
+            float4* orow = reinterpret_cast<float4*>(p.out + px * D);
+            for (int base = 0; base < d4; base += 128) {
+                float4 acc[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+                for (int j = 0; j < c; ++j) {
+                    const int g = __shfl_sync(0xffffffffu, id, j);
+                    const float wj = __shfl_sync(0xffffffffu, wn, j);
+                    const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(g) * D);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        if (q < d4) acc[m] = fma4(wj, ldg4(row + q), acc[m]);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    if (q < d4) __stcs(orow + q, acc[m]);
+                }
+            }
+        } else {
+            float* orow = p.out + px * D;
+            for (int base = 0; base < D; base += 128) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                for (int j = 0; j < c; ++j) {
+                    const int g = __shfl_sync(0xffffffffu, id, j);
+                    const float wj = __shfl_sync(0xffffffffu, wn, j);
+                    const float* row = p.feat + static_cast<int64_t>(g) * D;
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        if (q < D) acc[m] = fmaf(wj, __ldg(row + q), acc[m]);
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    if (q < D) __stcs(orow + q, acc[m]);
+                }
+            }
+        }
+    }
+}
+
+// feature_pass_full_blend (render.cpp:277-280): F[p] = sum_i w_i f_i over the contributor list.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    for (int64_t px = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; px < p.n_pixels; px += nw) {
+        const int r0 = p.offsets[px], r1 = p.offsets[px + 1];
+        const int step = VEC ? 128 : 128;
+        const int dd = VEC ? D >> 2 : D;
+        for (int base = 0; base < dd; base += step) {
+            float4 acc4[4];
+            float acc1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r = r0; r < r1; r += 32) {
+                const int nr = min(32, r1 - r);
+                int sid = 0;
+                float sw = 0.f;
+                if (lane < nr) {
+                    sid = p.src[r + lane];
+                    sw = static_cast<float>(p.w[r + lane]);
+                }
+                for (int j = 0; j < nr; ++j) {
+                    const int g = __shfl_sync(0xffffffffu, sid, j);
+                    const float wj = __shfl_sync(0xffffffffu, sw, j);
+                    if (VEC) {
+                        const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(g) * D);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
+                        }
+                    } else {
+                        const float* row = p.feat + static_cast<int64_t>(g) * D;
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < dd) acc1[m] = fmaf(wj, __ldg(row + q), acc1[m]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q < dd) {
+                    if (VEC) __stcs(reinterpret_cast<float4*>(p.out + px * D) + q, acc4[m]);
+                    else __stcs(p.out + px * D + q, acc1[m]);
+                }
+            }
+        }
+    }
+}
+
+// Record keys for the inverted (Gaussian -> slots) index, plus the renormalised weights.
+__global__ void k_slot_keys(SlotKeyParams p) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= p.n_slots) return;
+    const int64_t px = s / p.k;
+    const int j = static_cast<int>(s - px * p.k);
+    const int c = p.count[px];
+    const int32_t id = p.index[s];
+    const bool valid = j < c && id >= 0;
+    p.keys[s] = valid ? static_cast<uint32_t>(id) : static_cast<uint32_t>(p.n_gaussians);
+    p.vals[s] = static_cast<uint32_t>(s);
+    float wn = 0.0f;
+    if (valid) {
+        double sum = 0.0;                                    // backward.cpp:303-304, slot order
+        for (int jj = 0; jj < c; ++jj) sum += p.weight[px * p.k + jj];
+        wn = static_cast<float>(p.weight[s] / sum);
+    }
+    p.wnorm[s] = wn;
+}
+
+// backward_feature (backward.cpp:288-319) as a deterministic segmented reduction: one warp per
+// Gaussian sums its records in (pixel, slot) order and writes the dense row once.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    const int dd = VEC ? D >> 2 : D;
+    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n_gaussians; g += nw) {
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        for (int base = 0; base < dd; base += 128) {
+            float4 acc4[4];
+            float acc1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r = r0; r < r1; r += 32) {
+                const int nr = min(32, r1 - r);
+                int64_t spx = 0;
+                float sw = 0.f;
+                if (lane < nr) {
+                    const uint32_t s = p.slots[r + lane];
+                    spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+                    sw = p.wnorm[s];
+                }
+#pragma unroll 2
+                for (int j = 0; j < nr; ++j) {
+                    const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
+                    float wj = __shfl_sync(0xffffffffu, sw, j);
+                    if (!isfinite(wj)) {
+                        // Zero-weight records: the reference skips pixels whose gradient row is
+                        // all zero (backward.cpp:296-302), so 0/0 only propagates for live rows.
+                        bool any = false;
+                        for (int q = lane; q < D; q += 32) any |= p.grad[pxj * D + q] != 0.0f;
+                        if (!__any_sync(0xffffffffu, any)) continue;
+                    }
+                    if (VEC) {
+                        const float4* row = reinterpret_cast<const float4*>(p.grad + pxj * D);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
+                        }
+                    } else {
+                        const float* row = p.grad + pxj * D;
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < dd) acc1[m] = fmaf(wj, __ldg(row + q), acc1[m]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q < dd) {
+                    if (VEC) __stcs(reinterpret_cast<float4*>(p.out + g * D) + q, acc4[m]);
+                    else __stcs(p.out + g * D + q, acc1[m]);
+                }
+            }
+        }
+    }
+}
+
+__global__ void k_max_index(const int32_t* __restrict__ index, int64_t n, int32_t* __restrict__ out) {
+    int32_t m = INT32_MIN;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        m = max(m, index[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+// First slot (in slot order) whose index is >= n: the reference throws on it (render.cpp:305-311).
+__global__ void k_first_stale(const int32_t* __restrict__ index, int64_t n_slots, int64_t n,
+                              unsigned long long* __restrict__ first) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_slots;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (index[i] >= n) atomicMin(first, static_cast<unsigned long long>(i));
+}
+
+__global__ void k_interleave(const float* __restrict__ in, int64_t n_pixels, int ds, int g, float* __restrict__ out) {
+    const int64_t total = n_pixels * g * ds;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t px = i / (static_cast<int64_t>(g) * ds);
+        const int64_t rem = i - px * g * ds;
+        const int r = static_cast<int>(rem / ds), c = static_cast<int>(rem - static_cast<int64_t>(r) * ds);
+        out[i] = in[(static_cast<int64_t>(r) * n_pixels + px) * ds + c];
+    }
+}
+
+inline unsigned warp_grid(int64_t rows) {
+    const int64_t blocks = (rows + kWarps - 1) / kWarps;
+    const int64_t cap = 148LL * 32;
+    return static_cast<unsigned>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
+}
+
+inline bool vec_ok(const void* a, const void* b, int d) {
+    return (d % 4) == 0 && (reinterpret_cast<uintptr_t>(a) % 16) == 0 && (reinterpret_cast<uintptr_t>(b) % 16) == 0;
+}
+
+}  // namespace
+
+void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
+    if (p.n_pixels <= 0 || p.d <= 0) return;
+    if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    else k_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+}
+
+void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
+    if (p.n_pixels <= 0 || p.d <= 0) return;
+    if (vec_ok(p.feat, p.out, p.d)) k_list_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    else k_list_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+}
+
+void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st) {
+    if (p.n_slots > 0) k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p);
+}
+
+void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st) {
+    if (p.n_gaussians <= 0 || p.d <= 0) return;
+    if (vec_ok(p.grad, p.out, p.d)) k_feat_bwd<true><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
+    else k_feat_bwd<false><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
+}
+
+void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st) {
+    if (n_slots > 0) k_max_index<<<296, 256, 0, st>>>(index, n_slots, max_index);
+}
+
+void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,
+                        cudaStream_t st) {
+    if (n_slots > 0) k_first_stale<<<296, 256, 0, st>>>(index, n_slots, n, first);
+}
+
+void launch_interleave(const float* in, int64_t n_pixels, int ds, int g, float* out, cudaStream_t st) {
+    if (n_pixels > 0) k_interleave<<<148 * 8, 256, 0, st>>>(in, n_pixels, ds, g, out);
+}
+
+}  // namespace tk

@@ -1,0 +1,63 @@
+// feature.cuh — launch interface of the D-channel feature kernels (fp32, HBM-bound).
+#pragma once
+#include "tk_common.cuh"
+
+namespace tk {
+
+struct GatherParams {
+    int64_t n_pixels;
+    int k;                 // record slots per pixel
+    const int32_t* index;  // P x k
+    const double* weight;  // P x k
+    const uint8_t* count;  // P
+    const float* feat;     // N x D
+    int d;
+    float* out;            // P x D
+};
+
+struct ListGatherParams {
+    int64_t n_pixels;
+    const int32_t* offsets;  // P + 1
+    const int32_t* src;
+    const double* w;
+    const float* feat;
+    int d;
+    float* out;
+};
+
+struct SlotKeyParams {
+    int64_t n_slots;       // P x k
+    int k;
+    int64_t n_gaussians;
+    const int32_t* index;
+    const double* weight;
+    const uint8_t* count;
+    uint32_t* keys;        // Gaussian id, or n_gaussians for unused slots
+    uint32_t* vals;        // slot id
+    float* wnorm;          // renormalised slot weight (render.cpp:324-329)
+};
+
+struct FeatBwdParams {
+    int64_t n_gaussians;
+    int k;
+    int d;
+    const int32_t* seg;    // N + 1 record offsets per Gaussian
+    const uint32_t* slots; // records sorted by (Gaussian, slot)
+    const float* wnorm;
+    const float* grad;     // P x D
+    float* out;            // N x D
+};
+
+void launch_feature_gather(const GatherParams& p, cudaStream_t st);
+void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
+void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st);
+void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st);
+// *max_index = max over all slots (device int, preset to INT_MIN)
+void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st);
+// *first = smallest slot whose index >= n (device u64, preset to ~0)
+void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,
+                        cudaStream_t st);
+// interleave [G][P][ds] shard slices into [P][G*ds]
+void launch_interleave(const float* in, int64_t n_pixels, int ds, int g, float* out, cudaStream_t st);
+
+}  // namespace tk

@@ -1,0 +1,67 @@
+// geometric.cuh — launch interface of the geometric forward / backward kernels (fp64).
+#pragma once
+#include "tk_common.cuh"
+
+namespace tk {
+
+enum GeomMode { kGeomForward = 0, kGeomCount = 1, kGeomList = 2 };
+
+struct GeomFwdParams {
+    Frame f;
+    TileEntries te;
+    const int32_t* tile_offsets;  // CSR over tiles (reference tile_offsets)
+    const int32_t* padded_start;  // start of each tile in the padded tile-ordered arrays
+    int sub_x, sub_y;             // 16x16 pixel blocks per tile (tile_size > 16)
+    // kGeomForward outputs (any may be null except aux)
+    double* color;
+    double* depth;
+    double* alpha;
+    int32_t* topk_index;
+    double* topk_weight;
+    uint8_t* topk_count;
+    unsigned long long* contrib;  // n, fp64 bit patterns (max of positive doubles)
+    PixelAux aux;
+    // kGeomCount / kGeomList (full blend)
+    int32_t* list_count;
+    const int32_t* list_offsets;
+    int32_t* list_src;
+    double* list_w;
+};
+
+struct GeomBwdParams {
+    Frame f;
+    TileEntries te;
+    const int32_t* tile_offsets;
+    const int32_t* padded_start;
+    int sub_x, sub_y;
+    PixelAux aux;              // from the forward
+    const double* grad_color;  // P x 3
+    const double* grad_depth;  // P or null
+    double* mid;               // n x 10: mx,my,ixx,ixy,iyy,z,opacity,cr,cg,cb
+};
+
+struct ChainParams {
+    int64_t n;
+    const double* mid;
+    const double* mean;
+    const double* log_scale;
+    const double* rotation;
+    const double* opacity_logit;
+    double pose[7];
+    double fx, fy, dilation;
+    double* g_mean;
+    double* g_log_scale;
+    double* g_rotation;
+    double* g_opacity_logit;
+    double* g_color;
+    double* twist;  // n x 6
+};
+
+// returns dynamic smem bytes used
+void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
+void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
+void launch_chain(const ChainParams& p, cudaStream_t st);
+// deterministic two-level sum of twist[n][6] -> out[6] (device)
+void launch_twist_reduce(const double* twist, int64_t n, double* partial, double* out, cudaStream_t st);
+
+}  // namespace tk

@@ -1,0 +1,32 @@
+// sort.cuh — hand-written device primitives: exclusive scan and stable LSD radix sort.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tk {
+
+size_t align_bytes(size_t b);  // round up to 256 B
+
+// Scratch bytes needed by scan_exclusive for n elements.
+size_t scan_scratch_bytes(int64_t n);
+// out[i] = sum(in[0..i)), out may alias nothing; *total (device, int64) = sum(in).
+// Launches 3 kernels.  in/out int32 (callers check *total against INT32_MAX).
+void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch,
+                    cudaStream_t st, int64_t* launches);
+
+// Stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit), 8 bits per
+// pass.  Results end in keys_out/vals_out (buffers are ping-ponged internally; the *_alt
+// buffers are scratch of the same size).
+size_t radix_scratch_bytes(int64_t n);
+void radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
+                          int64_t n, int begin_bit, int end_bit, void* scratch, cudaStream_t st,
+                          bool* result_in_alt, int64_t* launches);
+void radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                          int64_t n, int begin_bit, int end_bit, void* scratch, cudaStream_t st,
+                          bool* result_in_alt, int64_t* launches);
+
+// offsets[g] = first index i with keys[i] >= g, for g in [0, n_segments]; keys sorted ascending.
+void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments,
+                         cudaStream_t st, int64_t* launches);
+
+}  // namespace tk

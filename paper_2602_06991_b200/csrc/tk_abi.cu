@@ -1,0 +1,1101 @@
+// tk_abi.cu — the C ABI (include/tk_render.h): context, device-resident scene mirror, and the
+// host orchestration of the sm_100a kernels for each reference entry point.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "feature.cuh"
+#include "geometric.cuh"
+#include "prepare.cuh"
+#include "sort.cuh"
+#include "tk_common.cuh"
+#include "tk_render.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct TkError {
+    tk_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(tk_status st, const std::string& msg) { throw TkError{st, msg}; }
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess)                                                                 \
+            fail(e_ == cudaErrorMemoryAllocation ? TK_ERR_OOM : TK_ERR_CUDA,                   \
+                 std::string(#call) + ": " + cudaGetErrorString(e_));                          \
+    } while (0)
+
+#define CK_LAUNCH(ctx)                                                                         \
+    do {                                                                                       \
+        cudaError_t e_ = cudaGetLastError();                                                   \
+        if (e_ != cudaSuccess) fail(TK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+template <class T>
+T* ensure(DevBuf& b, size_t count) {
+    const size_t need = std::max<size_t>(count, 1) * sizeof(T);
+    if (b.bytes < need) {
+        b.release();
+        const size_t alloc = tk::align_bytes(need + need / 8);
+        CK(cudaMalloc(&b.p, alloc));
+        b.bytes = alloc;
+    }
+    return static_cast<T*>(b.p);
+}
+
+template <class T>
+T* ptr(const DevBuf& b) {
+    return static_cast<T*>(b.p);
+}
+
+struct PrepKey {
+    double pose[7];
+    double fx, fy, cx, cy, near_plane, far_plane, dilation;
+    int width, height, tile_size;
+    uint64_t scene_version;
+    bool operator==(const PrepKey& o) const { return std::memcmp(this, &o, sizeof(PrepKey)) == 0; }
+};
+
+struct FwdKey {
+    PrepKey prep;
+    double tfloor, alpha_clamp, bg[3];
+    bool operator==(const FwdKey& o) const { return std::memcmp(this, &o, sizeof(FwdKey)) == 0; }
+};
+
+// NCCL entry points, resolved at tk_comm_init time so the library loads without NCCL.
+struct NcclApi {
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool load() {
+        if (handle) return true;
+        handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!handle) handle = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!handle) return false;
+        GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(handle, "ncclGetUniqueId"));
+        CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(handle, "ncclCommInitRank"));
+        AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(handle, "ncclAllGather"));
+        AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(handle, "ncclAllReduce"));
+        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(handle, "ncclCommDestroy"));
+        GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(handle, "ncclGetErrorString"));
+        return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy && GetErrorString;
+    }
+};
+NcclApi g_nccl;
+
+#define NK(call)                                                                               \
+    do {                                                                                       \
+        ncclResult_t r_ = (call);                                                              \
+        if (r_ != ncclSuccess) fail(TK_ERR_NCCL, std::string(#call) + ": " + g_nccl.GetErrorString(r_)); \
+    } while (0)
+
+// CUDA-event phase timer on the context stream (tk_profile_*).
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    struct Rec {
+        int phase;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    double ms[TK_NUM_PHASES] = {};
+    int64_t cnt[TK_NUM_PHASES] = {};
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        return e;
+    }
+    void drain() {
+        for (const Rec& r : pending) {
+            float t = 0.f;
+            CK(cudaEventSynchronize(r.b));
+            CK(cudaEventElapsedTime(&t, r.a, r.b));
+            ms[r.phase] += t;
+            cnt[r.phase] += 1;
+            pool.push_back(r.a);
+            pool.push_back(r.b);
+        }
+        pending.clear();
+    }
+    ~Profiler() {
+        for (const Rec& r : pending) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+struct tk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    Profiler prof;
+    // scene mirror
+    int64_t n = 0;
+    int32_t d = 0;
+    uint64_t generation = 0;
+    uint64_t scene_version = 0;
+    bool has_scene = false, has_features = false;
+    DevBuf mean, log_scale, rotation, opacity_logit, color, feature;
+    // projection, per Gaussian
+    DevBuf pmx, pmy, pixx, pixy, piyy, pz, pop, rect, valid, ntiles, pos;
+    DevBuf dkeys, dvals, dkeys_alt, dvals_alt, ntiles_sorted, pair_off;
+    DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
+    DevBuf te[12];
+    DevBuf scratch, dscal;
+    int64_t* hscal = nullptr;  // pinned mirror of dscal
+    // prepared scene
+    bool prepared = false;
+    PrepKey prep_key{};
+    int64_t n_vis = 0, n_pairs = 0;
+    int tiles_x = 0, tiles_y = 0;
+    const uint32_t* order = nullptr;
+    const uint32_t* tile_keys_sorted = nullptr;
+    const uint32_t* tile_vals_sorted = nullptr;
+    // forward outputs / records
+    DevBuf o_color, o_depth, o_alpha, o_index, o_weight, o_count, o_contrib, aux_t, aux_n;
+    bool has_records = false;
+    int rec_w = 0, rec_h = 0, rec_k = 0;
+    uint64_t rec_generation = 0;
+    int64_t rec_map_size = 0;
+    bool aux_valid = false;
+    FwdKey aux_key{};
+    // external records staging
+    DevBuf x_index, x_weight, x_count;
+    // feature
+    DevBuf f_out, f_grad_in, f_grad_out, s_keys, s_vals, s_keys_alt, s_vals_alt, s_wnorm, s_seg;
+    int64_t fout_pixels = 0;
+    // geometric backward
+    DevBuf g_color_in, g_depth_in, mid, twist, twist_part, twist_out, gg_mean, gg_ls, gg_rot, gg_op, gg_col;
+    // full blend
+    DevBuf l_count, l_off, l_src, l_w;
+    // multi-GPU
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0, d_total = 0;
+    DevBuf gather_buf;
+};
+
+namespace {
+
+struct PhaseScope {
+    tk_ctx* c;
+    int phase;
+    cudaEvent_t a = nullptr;
+    PhaseScope(tk_ctx* ctx, int ph) : c(ctx), phase(ph) {
+        if (c->prof.on) {
+            a = c->prof.get();
+            CK(cudaEventRecord(a, c->stream));
+        }
+    }
+    ~PhaseScope() {
+        if (a) {
+            cudaEvent_t b = c->prof.get();
+            cudaEventRecord(b, c->stream);
+            c->prof.pending.push_back({phase, a, b});
+        }
+    }
+};
+
+tk_status guard_status(const TkError& e) {
+    g_err = e.msg;
+    return e.st;
+}
+
+template <class F>
+tk_status guarded(F&& f) {
+    try {
+        f();
+        g_err.clear();
+        return TK_OK;
+    } catch (const TkError& e) {
+        return guard_status(e);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TK_ERR_STATE;
+    }
+}
+
+// Host <-> device copies made inside an API call (timed as TK_PHASE_COPY when profiling).
+void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
+    if (bytes == 0) return;
+    PhaseScope phase(c, TK_PHASE_COPY);
+    CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       c->stream));
+}
+
+void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
+    if (bytes == 0 || dst == nullptr) return;
+    PhaseScope phase(c, TK_PHASE_COPY);
+    CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       c->stream));
+}
+
+void sync(tk_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+int bits_for(uint64_t max_value) {  // bits needed to represent values in [0, max_value]
+    int b = 0;
+    while (b < 64 && (max_value >> b) != 0) ++b;
+    return b;
+}
+
+void check_frame(const tk_camera* cam, const tk_settings* s) {
+    if (!cam || !s) fail(TK_ERR_BAD_ARG, "null camera or settings");
+    if (cam->width <= 0 || cam->height <= 0) fail(TK_ERR_BAD_ARG, "camera width/height must be positive");
+    if (s->tile_size <= 0) fail(TK_ERR_BAD_ARG, "tile_size must be positive");
+    if (s->top_k < 0) fail(TK_ERR_BAD_ARG, "top_k must be >= 0");
+}
+
+tk::Frame make_frame(tk_ctx* c, const tk_camera* cam, const tk_settings* s) {
+    tk::Frame f{};
+    f.width = cam->width;
+    f.height = cam->height;
+    f.tile_size = s->tile_size;
+    f.tiles_x = (cam->width + s->tile_size - 1) / s->tile_size;   // render.cpp:122-123
+    f.tiles_y = (cam->height + s->tile_size - 1) / s->tile_size;
+    f.k = std::min(s->top_k, tk::kMaxTopK);                        // render.cpp:161
+    f.tfloor = s->transmittance_floor;
+    f.alpha_clamp = s->alpha_clamp;
+    for (int i = 0; i < 3; ++i) f.bg[i] = s->background[i];
+    (void)c;
+    return f;
+}
+
+PrepKey make_prep_key(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s) {
+    PrepKey k;
+    std::memset(&k, 0, sizeof(k));
+    const double pv[7] = {pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
+    std::memcpy(k.pose, pv, sizeof(pv));
+    k.fx = cam->fx;
+    k.fy = cam->fy;
+    k.cx = cam->cx;
+    k.cy = cam->cy;
+    k.near_plane = cam->near_plane;
+    k.far_plane = cam->far_plane;
+    k.dilation = s->cov2d_dilation;
+    k.width = cam->width;
+    k.height = cam->height;
+    k.tile_size = s->tile_size;
+    k.scene_version = c->scene_version;
+    return k;
+}
+
+FwdKey make_fwd_key(const PrepKey& pk, const tk_settings* s) {
+    FwdKey k;
+    std::memset(&k, 0, sizeof(k));
+    k.prep = pk;
+    k.tfloor = s->transmittance_floor;
+    k.alpha_clamp = s->alpha_clamp;
+    for (int i = 0; i < 3; ++i) k.bg[i] = s->background[i];
+    return k;
+}
+
+tk::TileEntries tile_entries(tk_ctx* c) {
+    tk::TileEntries t;
+    t.mx = ptr<double>(c->te[0]);
+    t.my = ptr<double>(c->te[1]);
+    t.ixx = ptr<double>(c->te[2]);
+    t.ixy = ptr<double>(c->te[3]);
+    t.iyy = ptr<double>(c->te[4]);
+    t.z = ptr<double>(c->te[5]);
+    t.opacity = ptr<double>(c->te[6]);
+    t.cr = ptr<double>(c->te[7]);
+    t.cg = ptr<double>(c->te[8]);
+    t.cb = ptr<double>(c->te[9]);
+    t.src = ptr<int32_t>(c->te[10]);
+    t.list_pos = ptr<int32_t>(c->te[11]);
+    return t;
+}
+
+void ensure_scratch(tk_ctx* c, int64_t n) {
+    const size_t need = std::max(tk::radix_scratch_bytes(n), tk::scan_scratch_bytes(n + 1));
+    ensure<char>(c->scratch, need);
+}
+
+// prepare_scene (render.cpp:73-156) on the device; cached on (pose, camera, settings, scene).
+void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s) {
+    if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+    const PrepKey key = make_prep_key(c, pose, cam, s);
+    if (c->prepared && c->prep_key == key) return;
+    c->prepared = false;
+    c->aux_valid = false;
+    PhaseScope phase(c, TK_PHASE_PREPARE);
+    const int64_t n = c->n;
+    cudaStream_t st = c->stream;
+    const tk::Frame f = make_frame(c, cam, s);
+    const int n_tiles = f.tiles_x * f.tiles_y;
+    c->tiles_x = f.tiles_x;
+    c->tiles_y = f.tiles_y;
+    int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+    ensure_scratch(c, std::max<int64_t>(n, n_tiles + 1));
+
+    tk::ProjectParams pp{};
+    pp.n = n;
+    pp.mean = ptr<double>(c->mean);
+    pp.log_scale = ptr<double>(c->log_scale);
+    pp.rotation = ptr<double>(c->rotation);
+    pp.opacity_logit = ptr<double>(c->opacity_logit);
+    const double pv[7] = {pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
+    std::memcpy(pp.pose, pv, sizeof(pv));
+    pp.fx = cam->fx;
+    pp.fy = cam->fy;
+    pp.cx = cam->cx;
+    pp.cy = cam->cy;
+    pp.near_plane = cam->near_plane;
+    pp.far_plane = cam->far_plane;
+    pp.dilation = s->cov2d_dilation;
+    pp.tile_size = s->tile_size;
+    pp.tiles_x = f.tiles_x;
+    pp.tiles_y = f.tiles_y;
+    pp.mx = ensure<double>(c->pmx, n);
+    pp.my = ensure<double>(c->pmy, n);
+    pp.ixx = ensure<double>(c->pixx, n);
+    pp.ixy = ensure<double>(c->pixy, n);
+    pp.iyy = ensure<double>(c->piyy, n);
+    pp.z = ensure<double>(c->pz, n);
+    pp.opacity = ensure<double>(c->pop, n);
+    pp.rect = ensure<int4>(c->rect, n);
+    pp.valid = ensure<int32_t>(c->valid, n);
+    pp.ntiles = ensure<int32_t>(c->ntiles, n);
+    pp.key_min = reinterpret_cast<uint64_t*>(dscal + 1);
+    pp.key_max = reinterpret_cast<uint64_t*>(dscal + 2);
+    CK(cudaMemsetAsync(dscal + 1, 0xff, sizeof(int64_t), st));
+    CK(cudaMemsetAsync(dscal + 2, 0, sizeof(int64_t), st));
+    tk::launch_project(pp, st);
+    c->launches += n > 0;
+    CK_LAUNCH(c);
+
+    int32_t* pos = ensure<int32_t>(c->pos, n);
+    tk::scan_exclusive(pp.valid, pos, n, dscal + 0, c->scratch.p, st, &c->launches);
+    uint64_t* dkeys = ensure<uint64_t>(c->dkeys, n);
+    uint32_t* dvals = ensure<uint32_t>(c->dvals, n);
+    uint64_t* dkeys_alt = ensure<uint64_t>(c->dkeys_alt, n);
+    uint32_t* dvals_alt = ensure<uint32_t>(c->dvals_alt, n);
+    tk::launch_compact(pp.valid, pos, pp.z, n, dkeys, dvals, st);
+    c->launches += n > 0;
+    CK_LAUNCH(c);
+    CK(cudaMemcpyAsync(c->hscal, dscal, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    sync(c);
+    const int64_t n_vis = n > 0 ? c->hscal[0] : 0;
+    const uint64_t kmin = static_cast<uint64_t>(c->hscal[1]), kmax = static_cast<uint64_t>(c->hscal[2]);
+    c->n_vis = n_vis;
+
+    // depth sort: stable LSD over the bits in which the visible keys differ (render.cpp:108-111)
+    bool alt = false;
+    if (n_vis > 1) {
+        const int hb = bits_for(kmin ^ kmax);
+        tk::radix_sort_pairs_u64(dkeys, dvals, dkeys_alt, dvals_alt, n_vis, 0, hb, c->scratch.p, st, &alt,
+                                 &c->launches);
+        CK_LAUNCH(c);
+    }
+    c->order = alt ? dvals_alt : dvals;
+
+    int32_t* nts = ensure<int32_t>(c->ntiles_sorted, n_vis);
+    int32_t* poff = ensure<int32_t>(c->pair_off, n_vis);
+    tk::launch_sorted_ntiles(c->order, n_vis, pp.ntiles, nts, st);
+    c->launches += n_vis > 0;
+    tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st, &c->launches);
+    CK(cudaMemcpyAsync(c->hscal + 3, dscal + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    sync(c);
+    const int64_t n_pairs = n_vis > 0 ? c->hscal[3] : 0;
+    if (n_pairs > INT32_MAX) fail(TK_ERR_BAD_ARG, "tile list exceeds 2^31 entries");
+    c->n_pairs = n_pairs;
+
+    uint32_t* tkeys = ensure<uint32_t>(c->tkeys, n_pairs);
+    uint32_t* tvals = ensure<uint32_t>(c->tvals, n_pairs);
+    uint32_t* tkeys_alt = ensure<uint32_t>(c->tkeys_alt, n_pairs);
+    uint32_t* tvals_alt = ensure<uint32_t>(c->tvals_alt, n_pairs);
+    tk::launch_emit_pairs(c->order, n_vis, pp.rect, nts, poff, f.tiles_x, tkeys, tvals, st);
+    c->launches += n_vis > 0;
+    ensure_scratch(c, std::max<int64_t>(n_pairs, n_tiles + 1));
+    bool talt = false;
+    const int tbits = bits_for(static_cast<uint64_t>(n_tiles - 1));
+    if (n_pairs > 1 && tbits > 0) {
+        tk::radix_sort_pairs_u32(tkeys, tvals, tkeys_alt, tvals_alt, n_pairs, 0, tbits, c->scratch.p, st, &talt,
+                                 &c->launches);
+    }
+    c->tile_keys_sorted = talt ? tkeys_alt : tkeys;
+    c->tile_vals_sorted = talt ? tvals_alt : tvals;
+    int32_t* toff = ensure<int32_t>(c->tile_offsets, n_tiles + 1);
+    tk::segment_offsets_u32(c->tile_keys_sorted, n_pairs, toff, n_tiles, st, &c->launches);
+    int32_t* pcnt = ensure<int32_t>(c->padded_cnt, n_tiles + 1);
+    int32_t* pstart = ensure<int32_t>(c->padded_start, n_tiles + 1);
+    tk::launch_padded_counts(toff, n_tiles, pcnt, st);
+    c->launches += 1;
+    tk::scan_exclusive(pcnt, pstart, n_tiles + 1, dscal + 4, c->scratch.p, st, &c->launches);
+    const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
+    for (int i = 0; i < 10; ++i) ensure<double>(c->te[i], padded_cap);
+    ensure<int32_t>(c->te[10], padded_cap);
+    ensure<int32_t>(c->te[11], padded_cap);
+    tk::MaterializeParams mp{};
+    mp.n_pairs = n_pairs;
+    mp.tile_keys = c->tile_keys_sorted;
+    mp.tile_vals = c->tile_vals_sorted;
+    mp.tile_offsets = toff;
+    mp.padded_start = pstart;
+    mp.order = c->order;
+    mp.mx = pp.mx;
+    mp.my = pp.my;
+    mp.ixx = pp.ixx;
+    mp.ixy = pp.ixy;
+    mp.iyy = pp.iyy;
+    mp.z = pp.z;
+    mp.opacity = pp.opacity;
+    mp.color = ptr<double>(c->color);
+    mp.out = tile_entries(c);
+    tk::launch_materialize(mp, st);
+    c->launches += n_pairs > 0;
+    CK_LAUNCH(c);
+    c->prepared = true;
+    c->prep_key = key;
+}
+
+int sub_blocks(int tile_size) { return tile_size <= 16 ? 1 : (tile_size + 15) / 16; }
+
+// geometric_pass (render.cpp:158-240).  Record/colour outputs are optional (null = skip);
+// the per-pixel aux (final T, entries visited) is always written for the backward.
+void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records) {
+    const tk::Frame f = make_frame(c, cam, s);
+    const int64_t P = static_cast<int64_t>(f.width) * f.height;
+    const int k = f.k;
+    cudaStream_t st = c->stream;
+    tk::GeomFwdParams gp{};
+    gp.f = f;
+    gp.te = tile_entries(c);
+    gp.tile_offsets = ptr<int32_t>(c->tile_offsets);
+    gp.padded_start = ptr<int32_t>(c->padded_start);
+    gp.sub_x = gp.sub_y = sub_blocks(f.tile_size);
+    gp.aux.t_final = ensure<double>(c->aux_t, P);
+    gp.aux.n_iter = ensure<int32_t>(c->aux_n, P);
+    if (records) {
+        gp.color = ensure<double>(c->o_color, P * 3);
+        gp.depth = ensure<double>(c->o_depth, P);
+        gp.alpha = ensure<double>(c->o_alpha, P);
+        gp.topk_index = ensure<int32_t>(c->o_index, P * std::max(k, 1));
+        gp.topk_weight = ensure<double>(c->o_weight, P * std::max(k, 1));
+        gp.topk_count = ensure<uint8_t>(c->o_count, P);
+        gp.contrib = ensure<unsigned long long>(c->o_contrib, c->n);
+        CK(cudaMemsetAsync(gp.contrib, 0, std::max<int64_t>(c->n, 1) * sizeof(double), st));
+    }
+    const int nblk = f.tiles_x * f.tiles_y * gp.sub_x * gp.sub_y;
+    {
+        PhaseScope phase(c, TK_PHASE_GEOM_FWD);
+        tk::launch_geom_fwd(tk::kGeomForward, gp, nblk, st);
+    }
+    c->launches += 1;
+    CK_LAUNCH(c);
+    if (records) {
+        c->has_records = true;
+        c->rec_w = f.width;
+        c->rec_h = f.height;
+        c->rec_k = k;
+        c->rec_generation = c->generation;
+        c->rec_map_size = c->n;
+    }
+}
+
+std::string stale_message(const char* fn, int32_t idx, int64_t n) {
+    return std::string(fn) + ": top-k record references gaussian " + std::to_string(idx) + " but the map holds " +
+           std::to_string(n) + " (stale snapshot)";
+}
+
+struct Records {
+    int w = 0, h = 0, k = 0;
+    const int32_t* index = nullptr;
+    const double* weight = nullptr;
+    const uint8_t* count = nullptr;
+};
+
+// Resolve a TopKGrid argument to device pointers, with the reference's stale-index check
+// (render.cpp:305-311, backward.cpp:278-283) done before any work.
+Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
+    Records r;
+    const int64_t n = c->n;
+    cudaStream_t st = c->stream;
+    if (!v) {
+        if (!c->has_records) fail(TK_ERR_STATE, std::string(fn) + ": no records (call tk_render_geometric first)");
+        r.w = c->rec_w;
+        r.h = c->rec_h;
+        r.k = c->rec_k;
+        r.index = ptr<int32_t>(c->o_index);
+        r.weight = ptr<double>(c->o_weight);
+        r.count = ptr<uint8_t>(c->o_count);
+        if (c->rec_map_size <= n) return r;  // indices < rec_map_size <= n by construction
+    } else {
+        if (v->width < 0 || v->height < 0 || v->k < 0) fail(TK_ERR_BAD_ARG, "negative TopKGrid shape");
+        r.w = v->width;
+        r.h = v->height;
+        r.k = v->k;
+        const int64_t slots = static_cast<int64_t>(r.w) * r.h * r.k;
+        const int64_t P = static_cast<int64_t>(r.w) * r.h;
+        if (v->mem == TK_HOST) {
+            for (int64_t q = 0; q < slots; ++q)
+                if (v->index[q] >= n) fail(TK_ERR_STALE_INDEX, stale_message(fn, v->index[q], n));
+            int32_t* di = ensure<int32_t>(c->x_index, slots);
+            double* dw = ensure<double>(c->x_weight, slots);
+            uint8_t* dc = ensure<uint8_t>(c->x_count, P);
+            copy_in(di, v->index, slots * sizeof(int32_t), TK_HOST, c);
+            copy_in(dw, v->weight, slots * sizeof(double), TK_HOST, c);
+            copy_in(dc, v->count, P, TK_HOST, c);
+            r.index = di;
+            r.weight = dw;
+            r.count = dc;
+            return r;
+        }
+        r.index = v->index;
+        r.weight = v->weight;
+        r.count = v->count;
+    }
+    // device-side check: first offending slot in slot order
+    const int64_t slots = static_cast<int64_t>(r.w) * r.h * r.k;
+    int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+    CK(cudaMemsetAsync(dscal + 5, 0xff, sizeof(int64_t), st));
+    tk::launch_first_stale(r.index, slots, n, reinterpret_cast<unsigned long long*>(dscal + 5), st);
+    c->launches += slots > 0;
+    CK(cudaMemcpyAsync(c->hscal + 5, dscal + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    sync(c);
+    const uint64_t first = static_cast<uint64_t>(c->hscal[5]);
+    if (first != ~0ull) {
+        int32_t idx = 0;
+        CK(cudaMemcpy(&idx, r.index + first, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        fail(TK_ERR_STALE_INDEX, stale_message(fn, idx, n));
+    }
+    return r;
+}
+
+void require_features(tk_ctx* c) {
+    if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+    if (!c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+void tk_default_settings(tk_settings* s) {  // render.hpp:14-21
+    s->top_k = 3;
+    s->tile_size = 16;
+    s->transmittance_floor = 1e-4;
+    s->background[0] = s->background[1] = s->background[2] = 0.0;
+    s->cov2d_dilation = 0.3;
+    s->alpha_clamp = 0.999;
+}
+
+const char* tk_last_error(void) { return g_err.c_str(); }
+int32_t tk_abi_version(void) { return TK_ABI_VERSION; }
+
+tk_status tk_create(int32_t device, tk_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(TK_ERR_BAD_ARG, "null out");
+        *out = nullptr;
+        int count = 0;
+        CK(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count) fail(TK_ERR_BAD_ARG, "device index out of range");
+        CK(cudaSetDevice(device));
+        tk_ctx* c = new tk_ctx;
+        c->device = device;
+        cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscal), 16 * sizeof(int64_t), cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            delete c;
+            fail(TK_ERR_CUDA, std::string("tk_create: ") + cudaGetErrorString(e));
+        }
+        *out = c;
+    });
+}
+
+tk_status tk_destroy(tk_ctx* c) {
+    if (!c) return TK_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf* all[] = {&c->mean, &c->log_scale, &c->rotation, &c->opacity_logit, &c->color, &c->feature, &c->pmx,
+                     &c->pmy, &c->pixx, &c->pixy, &c->piyy, &c->pz, &c->pop, &c->rect, &c->valid, &c->ntiles,
+                     &c->pos, &c->dkeys, &c->dvals, &c->dkeys_alt, &c->dvals_alt, &c->ntiles_sorted, &c->pair_off,
+                     &c->tkeys, &c->tvals, &c->tkeys_alt, &c->tvals_alt, &c->tile_offsets, &c->padded_cnt,
+                     &c->padded_start, &c->scratch, &c->dscal, &c->o_color, &c->o_depth, &c->o_alpha, &c->o_index,
+                     &c->o_weight, &c->o_count, &c->o_contrib, &c->aux_t, &c->aux_n, &c->x_index, &c->x_weight,
+                     &c->x_count, &c->f_out, &c->f_grad_in, &c->f_grad_out, &c->s_keys, &c->s_vals,
+                     &c->s_keys_alt, &c->s_vals_alt, &c->s_wnorm, &c->s_seg, &c->g_color_in, &c->g_depth_in,
+                     &c->mid, &c->twist, &c->twist_part, &c->twist_out, &c->gg_mean, &c->gg_ls, &c->gg_rot,
+                     &c->gg_op, &c->gg_col, &c->l_count, &c->l_off, &c->l_src, &c->l_w, &c->gather_buf};
+    for (DevBuf* b : all) b->release();
+    for (DevBuf& b : c->te) b.release();
+    if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
+    if (c->hscal) cudaFreeHost(c->hscal);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return TK_OK;
+}
+
+tk_status tk_synchronize(tk_ctx* c) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        sync(c);
+    });
+}
+
+void* tk_get_stream(tk_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+int64_t tk_kernel_launches(tk_ctx* c) { return c ? c->launches : 0; }
+
+tk_status tk_host_alloc(size_t bytes, void** out) {
+    return guarded([&] { CK(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocDefault)); });
+}
+tk_status tk_host_free(void* p) {
+    return guarded([&] {
+        if (p) CK(cudaFreeHost(p));
+    });
+}
+
+tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
+    return guarded([&] {
+        if (!c || !s) fail(TK_ERR_BAD_ARG, "null argument");
+        if (s->n < 0 || s->d < 0) fail(TK_ERR_BAD_ARG, "negative scene size");
+        if (s->n > INT32_MAX - 1) fail(TK_ERR_BAD_ARG, "scene larger than 2^31-1 Gaussians");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t st = c->stream;
+        const int64_t n = s->n;
+        if (!s->feature && c->has_features && (n != c->n || s->d != c->d))
+            fail(TK_ERR_BAD_ARG, "feature == NULL requires unchanged n and d");
+        copy_in(ensure<double>(c->mean, n * 3), s->mean, n * 3 * sizeof(double), mem, c);
+        copy_in(ensure<double>(c->log_scale, n * 3), s->log_scale, n * 3 * sizeof(double), mem, c);
+        copy_in(ensure<double>(c->rotation, n * 4), s->rotation, n * 4 * sizeof(double), mem, c);
+        copy_in(ensure<double>(c->opacity_logit, n), s->opacity_logit, n * sizeof(double), mem, c);
+        copy_in(ensure<double>(c->color, n * 3), s->color, n * 3 * sizeof(double), mem, c);
+        if (s->feature) {
+            copy_in(ensure<float>(c->feature, n * std::max(s->d, 1)), s->feature,
+                    static_cast<size_t>(n) * s->d * sizeof(float), mem, c);
+            c->has_features = true;
+        }
+        c->n = n;
+        c->d = s->d;
+        c->generation = s->generation;
+        c->scene_version += 1;
+        c->has_scene = true;
+        c->prepared = false;
+        c->aux_valid = false;
+    });
+}
+
+tk_status tk_device_view_get(tk_ctx* c, tk_device_view* v) {
+    return guarded([&] {
+        std::memset(v, 0, sizeof(*v));
+        v->color = ptr<double>(c->o_color);
+        v->depth = ptr<double>(c->o_depth);
+        v->alpha = ptr<double>(c->o_alpha);
+        v->topk_index = ptr<int32_t>(c->o_index);
+        v->topk_weight = ptr<double>(c->o_weight);
+        v->topk_count = ptr<uint8_t>(c->o_count);
+        v->contributions = ptr<double>(c->o_contrib);
+        v->feature_out = ptr<float>(c->f_out);
+        v->feature_grad = ptr<float>(c->f_grad_out);
+        const int64_t P = static_cast<int64_t>(c->rec_w) * c->rec_h;
+        v->grad_feature_in = ensure<float>(c->f_grad_in, std::max<int64_t>(P, 1) * std::max(c->d, 1));
+        v->mean = ptr<double>(c->mean);
+        v->feature = ptr<float>(c->feature);
+        v->n = c->n;
+        v->d = c->d;
+        v->width = c->rec_w;
+        v->height = c->rec_h;
+        v->k = c->rec_k;
+    });
+}
+
+tk_status tk_prepare_scene(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
+                           int64_t* n_entries, int64_t* n_tile_entries, int32_t* tiles_x, int32_t* tiles_y) {
+    return guarded([&] {
+        check_frame(cam, s);
+        CK(cudaSetDevice(c->device));
+        prepare(c, pose, cam, s);
+        if (n_entries) *n_entries = c->n_vis;
+        if (n_tile_entries) *n_tile_entries = c->n_pairs;
+        if (tiles_x) *tiles_x = c->tiles_x;
+        if (tiles_y) *tiles_y = c->tiles_y;
+    });
+}
+
+tk_status tk_prepared_export(tk_ctx* c, double* entries7, int32_t* src, int32_t* tile_offsets,
+                             int32_t* tile_entries_out) {
+    return guarded([&] {
+        if (!c->prepared) fail(TK_ERR_STATE, "no prepared scene");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t st = c->stream;
+        const int64_t nv = c->n_vis;
+        DevBuf e7, s7;
+        double* de = ensure<double>(e7, nv * 7);
+        int32_t* ds = ensure<int32_t>(s7, nv);
+        tk::launch_export_entries(c->order, nv, ptr<double>(c->pmx), ptr<double>(c->pmy), ptr<double>(c->pixx),
+                                  ptr<double>(c->pixy), ptr<double>(c->piyy), ptr<double>(c->pz),
+                                  ptr<double>(c->pop), de, ds, st);
+        CK_LAUNCH(c);
+        copy_out(entries7, de, nv * 7 * sizeof(double), TK_HOST, c);
+        copy_out(src, ds, nv * sizeof(int32_t), TK_HOST, c);
+        copy_out(tile_offsets, ptr<int32_t>(c->tile_offsets),
+                 (static_cast<int64_t>(c->tiles_x) * c->tiles_y + 1) * sizeof(int32_t), TK_HOST, c);
+        copy_out(tile_entries_out, c->tile_vals_sorted, c->n_pairs * sizeof(int32_t), TK_HOST, c);
+        sync(c);
+        e7.release();
+        s7.release();
+    });
+}
+
+tk_status tk_render_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
+                              tk_geom_out* out) {
+    return guarded([&] {
+        check_frame(cam, s);
+        CK(cudaSetDevice(c->device));
+        prepare(c, pose, cam, s);
+        forward(c, cam, s, true);
+        c->aux_valid = true;
+        c->aux_key = make_fwd_key(c->prep_key, s);
+        if (out) {
+            const int64_t P = static_cast<int64_t>(cam->width) * cam->height;
+            const int64_t k = c->rec_k;
+            cudaStream_t st = c->stream;
+            copy_out(out->color, c->o_color.p, P * 3 * sizeof(double), out->mem, c);
+            copy_out(out->depth, c->o_depth.p, P * sizeof(double), out->mem, c);
+            copy_out(out->alpha, c->o_alpha.p, P * sizeof(double), out->mem, c);
+            copy_out(out->topk_index, c->o_index.p, P * k * sizeof(int32_t), out->mem, c);
+            copy_out(out->topk_weight, c->o_weight.p, P * k * sizeof(double), out->mem, c);
+            copy_out(out->topk_count, c->o_count.p, P, out->mem, c);
+            copy_out(out->contributions, c->o_contrib.p, c->n * sizeof(double), out->mem, c);
+            out->generation = c->generation;
+            out->map_size = c->n;
+            if (out->mem == TK_HOST) sync(c);
+        }
+    });
+}
+
+tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int32_t out_mem) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        require_features(c);
+        const Records r = resolve_records(c, topk, "render_feature");
+        if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
+        const int64_t P = static_cast<int64_t>(r.w) * r.h;
+        float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_out, P * std::max(c->d, 1));
+        tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, dst};
+        {
+            PhaseScope phase(c, TK_PHASE_GATHER);
+            tk::launch_feature_gather(gp, c->stream);
+        }
+        c->launches += P > 0;
+        CK_LAUNCH(c);
+        c->fout_pixels = P;
+        if (out && out_mem == TK_HOST) {
+            copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
+            sync(c);
+        }
+    });
+}
+
+tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* grad, int32_t grad_mem, float* out,
+                              int32_t out_mem) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        require_features(c);
+        const Records r = resolve_records(c, topk, "backward_feature");
+        if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
+        cudaStream_t st = c->stream;
+        const int64_t P = static_cast<int64_t>(r.w) * r.h;
+        const int64_t slots = P * r.k;
+        const int64_t n = c->n;
+        const float* g = grad;
+        if (!grad) {
+            if (grad_mem != TK_DEVICE) fail(TK_ERR_BAD_ARG, "null grad_feature");
+            g = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
+        } else if (grad_mem == TK_HOST) {
+            float* dg = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
+            copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
+            g = dg;
+        }
+        // inverted index: records sorted by (Gaussian, slot)
+        uint32_t* keys = ensure<uint32_t>(c->s_keys, slots);
+        uint32_t* vals = ensure<uint32_t>(c->s_vals, slots);
+        uint32_t* keys_alt = ensure<uint32_t>(c->s_keys_alt, slots);
+        uint32_t* vals_alt = ensure<uint32_t>(c->s_vals_alt, slots);
+        float* wn = ensure<float>(c->s_wnorm, slots);
+        int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
+        ensure_scratch(c, std::max<int64_t>(slots, n + 1));
+        bool alt = false;
+        {
+            PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
+            tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, keys, vals, wn};
+            tk::launch_slot_keys(sk, st);
+            c->launches += slots > 0;
+            if (slots > 1)
+                tk::radix_sort_pairs_u32(keys, vals, keys_alt, vals_alt, slots, 0,
+                                         bits_for(static_cast<uint64_t>(n)), c->scratch.p, st, &alt, &c->launches);
+            tk::segment_offsets_u32(alt ? keys_alt : keys, slots, seg, n, st, &c->launches);
+        }
+        const uint32_t* svals = alt ? vals_alt : vals;
+        float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_grad_out, n * std::max(c->d, 1));
+        tk::FeatBwdParams fp{n, r.k, c->d, seg, svals, wn, g, dst};
+        {
+            PhaseScope phase(c, TK_PHASE_FBWD);
+            tk::launch_feature_bwd(fp, st);
+        }
+        c->launches += n > 0;
+        CK_LAUNCH(c);
+        if (out && out_mem == TK_HOST) {
+            copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), TK_HOST, c);
+            sync(c);
+        }
+    });
+}
+
+tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
+                                       float* out, int32_t out_mem) {
+    return guarded([&] {
+        check_frame(cam, s);
+        CK(cudaSetDevice(c->device));
+        require_features(c);
+        prepare(c, pose, cam, s);
+        cudaStream_t st = c->stream;
+        const tk::Frame f = make_frame(c, cam, s);
+        const int64_t P = static_cast<int64_t>(f.width) * f.height;
+        tk::GeomFwdParams gp{};
+        gp.f = f;
+        gp.te = tile_entries(c);
+        gp.tile_offsets = ptr<int32_t>(c->tile_offsets);
+        gp.padded_start = ptr<int32_t>(c->padded_start);
+        gp.sub_x = gp.sub_y = sub_blocks(f.tile_size);
+        gp.list_count = ensure<int32_t>(c->l_count, P + 1);
+        int32_t* off = ensure<int32_t>(c->l_off, P + 1);
+        CK(cudaMemsetAsync(gp.list_count + P, 0, sizeof(int32_t), st));
+        const int nblk = f.tiles_x * f.tiles_y * gp.sub_x * gp.sub_y;
+        tk::launch_geom_fwd(tk::kGeomCount, gp, nblk, st);
+        ensure_scratch(c, P + 1);
+        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+        tk::scan_exclusive(gp.list_count, off, P + 1, dscal + 6, c->scratch.p, st, &c->launches);
+        CK(cudaMemcpyAsync(c->hscal + 6, dscal + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        sync(c);
+        const int64_t total = c->hscal[6];
+        if (total > INT32_MAX) fail(TK_ERR_BAD_ARG, "contributor lists exceed 2^31 entries");
+        gp.list_offsets = off;
+        gp.list_src = ensure<int32_t>(c->l_src, total);
+        gp.list_w = ensure<double>(c->l_w, total);
+        tk::launch_geom_fwd(tk::kGeomList, gp, nblk, st);
+        float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_out, P * std::max(c->d, 1));
+        tk::ListGatherParams lp{P, off, gp.list_src, gp.list_w, ptr<float>(c->feature), c->d, dst};
+        tk::launch_list_gather(lp, st);
+        c->launches += 3;
+        CK_LAUNCH(c);
+        if (out && out_mem == TK_HOST) {
+            copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
+            sync(c);
+        }
+    });
+}
+
+tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
+                                const double* grad_color, const double* grad_depth, int32_t grad_mem,
+                                tk_geom_grads* out) {
+    return guarded([&] {
+        check_frame(cam, s);
+        if (!grad_color) fail(TK_ERR_BAD_ARG, "null grad_color");
+        CK(cudaSetDevice(c->device));
+        prepare(c, pose, cam, s);  // backward.cpp:75 (cached when the forward used the same inputs)
+        const FwdKey fk = make_fwd_key(c->prep_key, s);
+        if (!(c->aux_valid && c->aux_key == fk)) {
+            forward(c, cam, s, false);
+            c->aux_valid = true;
+            c->aux_key = fk;
+        }
+        cudaStream_t st = c->stream;
+        const tk::Frame f = make_frame(c, cam, s);
+        const int64_t P = static_cast<int64_t>(f.width) * f.height;
+        const int64_t n = c->n;
+        const double* gc = grad_color;
+        const double* gd = grad_depth;
+        if (grad_mem == TK_HOST) {
+            double* dgc = ensure<double>(c->g_color_in, P * 3);
+            copy_in(dgc, grad_color, P * 3 * sizeof(double), TK_HOST, c);
+            gc = dgc;
+            if (grad_depth) {
+                double* dgd = ensure<double>(c->g_depth_in, P);
+                copy_in(dgd, grad_depth, P * sizeof(double), TK_HOST, c);
+                gd = dgd;
+            }
+        }
+        double* mid = ensure<double>(c->mid, n * 10);
+        CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), st));
+        tk::GeomBwdParams bp{};
+        bp.f = f;
+        bp.te = tile_entries(c);
+        bp.tile_offsets = ptr<int32_t>(c->tile_offsets);
+        bp.padded_start = ptr<int32_t>(c->padded_start);
+        bp.sub_x = bp.sub_y = sub_blocks(f.tile_size);
+        bp.aux.t_final = ptr<double>(c->aux_t);
+        bp.aux.n_iter = ptr<int32_t>(c->aux_n);
+        bp.grad_color = gc;
+        bp.grad_depth = gd;
+        bp.mid = mid;
+        {
+            PhaseScope phase(c, TK_PHASE_GEOM_BWD);
+            tk::launch_geom_bwd(bp, f.tiles_x * f.tiles_y * bp.sub_x * bp.sub_y, st);
+        }
+        c->launches += 1;
+        CK_LAUNCH(c);
+        const bool dev_out = out && out->mem == TK_DEVICE;
+        tk::ChainParams cp{};
+        cp.n = n;
+        cp.mid = mid;
+        cp.mean = ptr<double>(c->mean);
+        cp.log_scale = ptr<double>(c->log_scale);
+        cp.rotation = ptr<double>(c->rotation);
+        cp.opacity_logit = ptr<double>(c->opacity_logit);
+        const double pv[7] = {pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
+        std::memcpy(cp.pose, pv, sizeof(pv));
+        cp.fx = cam->fx;
+        cp.fy = cam->fy;
+        cp.dilation = s->cov2d_dilation;
+        cp.g_mean = dev_out && out->mean ? out->mean : ensure<double>(c->gg_mean, n * 3);
+        cp.g_log_scale = dev_out && out->log_scale ? out->log_scale : ensure<double>(c->gg_ls, n * 3);
+        cp.g_rotation = dev_out && out->rotation ? out->rotation : ensure<double>(c->gg_rot, n * 4);
+        cp.g_opacity_logit = dev_out && out->opacity_logit ? out->opacity_logit : ensure<double>(c->gg_op, n);
+        cp.g_color = dev_out && out->color ? out->color : ensure<double>(c->gg_col, n * 3);
+        cp.twist = ensure<double>(c->twist, n * 6);
+        double* tpart = ensure<double>(c->twist_part, 148 * 6);
+        double* tout = ensure<double>(c->twist_out, 6);
+        {
+            PhaseScope phase(c, TK_PHASE_CHAIN);
+            tk::launch_chain(cp, st);
+            tk::launch_twist_reduce(cp.twist, n, tpart, tout, st);
+        }
+        c->launches += 3;
+        CK_LAUNCH(c);
+        if (out) {
+            if (out->mem == TK_HOST) {
+                copy_out(out->mean, cp.g_mean, n * 3 * sizeof(double), TK_HOST, c);
+                copy_out(out->log_scale, cp.g_log_scale, n * 3 * sizeof(double), TK_HOST, c);
+                copy_out(out->rotation, cp.g_rotation, n * 4 * sizeof(double), TK_HOST, c);
+                copy_out(out->opacity_logit, cp.g_opacity_logit, n * sizeof(double), TK_HOST, c);
+                copy_out(out->color, cp.g_color, n * 3 * sizeof(double), TK_HOST, c);
+            }
+            copy_out(out->pose_twist, tout, 6 * sizeof(double), TK_HOST, c);
+            sync(c);
+        }
+    });
+}
+
+tk_status tk_invalidate(tk_ctx* c) {
+    return guarded([&] {
+        c->prepared = false;
+        c->aux_valid = false;
+    });
+}
+
+tk_status tk_profile_enable(tk_ctx* c, int32_t on) {
+    return guarded([&] { c->prof.on = on != 0; });
+}
+
+tk_status tk_profile_read(tk_ctx* c, double* ms, int64_t* counts, int32_t reset) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        c->prof.drain();
+        for (int i = 0; i < TK_NUM_PHASES; ++i) {
+            if (ms) ms[i] = c->prof.ms[i];
+            if (counts) counts[i] = c->prof.cnt[i];
+            if (reset) {
+                c->prof.ms[i] = 0.0;
+                c->prof.cnt[i] = 0;
+            }
+        }
+    });
+}
+
+tk_status tk_comm_unique_id(uint8_t id[128]) {
+    return guarded([&] {
+        if (!g_nccl.load()) fail(TK_ERR_NCCL, "libnccl.so.2 not found");
+        ncclUniqueId uid;
+        NK(g_nccl.GetUniqueId(&uid));
+        static_assert(sizeof(uid) == 128, "ncclUniqueId size");
+        std::memcpy(id, &uid, 128);
+    });
+}
+
+tk_status tk_comm_init(tk_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank, int32_t d_total) {
+    return guarded([&] {
+        if (!g_nccl.load()) fail(TK_ERR_NCCL, "libnccl.so.2 not found");
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(TK_ERR_BAD_ARG, "bad rank / nranks");
+        CK(cudaSetDevice(c->device));
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        NK(g_nccl.CommInitRank(&c->comm, nranks, uid, rank));
+        c->nranks = nranks;
+        c->rank = rank;
+        c->d_total = d_total;
+    });
+}
+
+tk_status tk_allgather_feature(tk_ctx* c, float* out, int32_t out_mem) {
+    return guarded([&] {
+        if (!c->comm) fail(TK_ERR_STATE, "tk_comm_init not called");
+        if (c->d * c->nranks != c->d_total) fail(TK_ERR_BAD_ARG, "d_total must equal nranks * d_shard");
+        CK(cudaSetDevice(c->device));
+        cudaStream_t st = c->stream;
+        const int64_t P = c->fout_pixels;
+        const size_t slice = static_cast<size_t>(P) * c->d;
+        float* gath = ensure<float>(c->gather_buf, slice * c->nranks);
+        NK(g_nccl.AllGather(c->f_out.p, gath, slice, ncclFloat32, c->comm, st));
+        float* dst = out && out_mem == TK_DEVICE ? out : nullptr;
+        DevBuf tmp;
+        if (!dst) dst = ensure<float>(tmp, slice * c->nranks);
+        tk::launch_interleave(gath, P, c->d, c->nranks, dst, st);
+        c->launches += 1;
+        CK_LAUNCH(c);
+        if (out && out_mem == TK_HOST) copy_out(out, dst, slice * c->nranks * sizeof(float), TK_HOST, c);
+        sync(c);
+        tmp.release();
+    });
+}
+
+tk_status tk_allreduce_sum_f64(tk_ctx* c, double* values, int32_t count) {
+    return guarded([&] {
+        if (!c->comm) fail(TK_ERR_STATE, "tk_comm_init not called");
+        CK(cudaSetDevice(c->device));
+        DevBuf tmp;
+        double* d = ensure<double>(tmp, count);
+        copy_in(d, values, count * sizeof(double), TK_HOST, c);
+        NK(g_nccl.AllReduce(d, d, count, ncclFloat64, ncclSum, c->comm, c->stream));
+        copy_out(values, d, count * sizeof(double), TK_HOST, c);
+        sync(c);
+        tmp.release();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+"""Host-side mirror of the reference renderer's value types (no Eigen, numpy arrays).
+
+Field names and defaults follow the reference headers so code written against
+proj/include/fslam/{core,raster,map} reads the same.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+K_MAX_TOP_K = 32                          # render.hpp:23
+K_LOG_WEIGHT_CUTOFF = -27.631021115928547  # render.hpp:97
+
+
+@dataclass
+class CameraIntrinsics:  # core/types.hpp:15-21
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    width: int = 0
+    height: int = 0
+    near_plane: float = 0.05
+    far_plane: float = 100.0
+
+
+@dataclass
+class Pose:  # core/pose.hpp:11-19, world-to-camera; rotation quaternion (w, x, y, z)
+    rotation: tuple = (1.0, 0.0, 0.0, 0.0)
+    translation: tuple = (0.0, 0.0, 0.0)
+
+    @staticmethod
+    def identity() -> "Pose":
+        return Pose()
+
+
+@dataclass
+class RenderSettings:  # raster/render.hpp:14-21
+    top_k: int = 3
+    transmittance_floor: float = 1e-4
+    background: tuple = (0.0, 0.0, 0.0)
+    tile_size: int = 16
+    cov2d_dilation: float = 0.3
+    alpha_clamp: float = 0.999
+
+
+@dataclass
+class SceneMap:  # map/scene_map.hpp:16-27 as SoA arrays; rotation (w,x,y,z); feature (n, d)
+    mean: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    log_scale: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    rotation: np.ndarray = field(default_factory=lambda: np.zeros((0, 4)))
+    opacity_logit: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    color: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    feature: np.ndarray | None = None
+    generation: int = 0
+    feature_dim: int = 0
+
+    def size(self) -> int:
+        return int(self.mean.shape[0])
+
+    def __len__(self) -> int:
+        return self.size()
+
+    def copy(self) -> "SceneMap":
+        return SceneMap(self.mean.copy(), self.log_scale.copy(), self.rotation.copy(), self.opacity_logit.copy(),
+                        self.color.copy(), None if self.feature is None else self.feature.copy(), self.generation,
+                        self.feature_dim)
+
+
+@dataclass
+class TopKGrid:  # raster/render.hpp:27-44; slot = (y*W + x)*k + j
+    width: int = 0
+    height: int = 0
+    k: int = 0
+    index: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    weight: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    count: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+
+    @staticmethod
+    def empty(w: int, h: int, k: int) -> "TopKGrid":
+        return TopKGrid(w, h, k, np.full(w * h * k, -1, np.int32), np.zeros(w * h * k), np.zeros(w * h, np.uint8))
+
+    def slot(self, x: int, y: int, j: int) -> int:
+        return (y * self.width + x) * self.k + j
+
+    def pixel(self, x: int, y: int) -> int:
+        return y * self.width + x
+
+
+@dataclass
+class RenderOutput:  # raster/render.hpp:46-55; images are H x W x C
+    color: np.ndarray | None = None
+    depth: np.ndarray | None = None
+    alpha: np.ndarray | None = None
+    feature: np.ndarray | None = None
+    topk: TopKGrid | None = None
+    contributions: np.ndarray | None = None
+    generation: int = 0
+    map_size: int = 0
+
+
+@dataclass
+class GeomGrads:  # raster/backward.hpp:15-22
+    mean: np.ndarray
+    log_scale: np.ndarray
+    rotation: np.ndarray
+    opacity_logit: np.ndarray
+    color: np.ndarray
+    pose_twist: np.ndarray
+
+
+@dataclass
+class PreparedScene:  # raster/render.hpp:84-92 (entries as n x 7: mx,my,ixx,ixy,iyy,z,opacity)
+    entries: np.ndarray
+    src: np.ndarray
+    tile_offsets: np.ndarray
+    tile_entries: np.ndarray
+    tiles_x: int
+    tiles_y: int
+    width: int
+    height: int
+    generation: int
+    map_size: int

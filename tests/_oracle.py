@@ -1,0 +1,221 @@
+"""ctypes wrapper of the CPU oracle (oracle/include/oracle.h).
+
+TEST INFRASTRUCTURE ONLY: the checker the GPU path is compared against, never the product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_DIR = os.path.join(ROOT, "oracle")
+ORACLE_LIB = os.path.join(ORACLE_DIR, "_build", "liboracle.so")
+
+
+class orc_camera(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_int32), ("height", C.c_int32), ("near_plane", C.c_double), ("far_plane", C.c_double)]
+
+
+class orc_pose(C.Structure):
+    _fields_ = [("qw", C.c_double), ("qx", C.c_double), ("qy", C.c_double), ("qz", C.c_double),
+                ("tx", C.c_double), ("ty", C.c_double), ("tz", C.c_double)]
+
+
+class orc_settings(C.Structure):
+    _fields_ = [("top_k", C.c_int32), ("tile_size", C.c_int32), ("transmittance_floor", C.c_double),
+                ("background", C.c_double * 3), ("cov2d_dilation", C.c_double), ("alpha_clamp", C.c_double)]
+
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", ORACLE_DIR], check=True)
+    return ORACLE_LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        src = os.path.join(ORACLE_DIR, "src", "oracle.cpp")
+        if not os.path.exists(ORACLE_LIB) or (os.path.exists(src) and
+                                              os.path.getmtime(src) > os.path.getmtime(ORACLE_LIB)):
+            build()
+        L = C.CDLL(ORACLE_LIB)
+        vp = C.c_void_p
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_map_create.restype = vp
+        L.orc_map_create.argtypes = [C.c_int64, C.c_int32, vp, vp, vp, vp, vp, vp, C.c_uint64]
+        L.orc_map_free.argtypes = [vp]
+        L.orc_project_gaussian.argtypes = [vp, C.c_int64, vp, vp, C.c_double, vp]
+        L.orc_prepare_scene.restype = vp
+        L.orc_prepare_scene.argtypes = [vp, vp, vp, vp]
+        L.orc_prep_sizes.argtypes = [vp, vp, vp, vp, vp]
+        L.orc_prep_export.argtypes = [vp, vp, vp, vp, vp]
+        L.orc_prep_free.argtypes = [vp]
+        L.orc_geometric_pass.argtypes = [vp] * 10
+        L.orc_render_geometric.argtypes = [vp] * 11
+        L.orc_render_feature.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp]
+        L.orc_render_feature_full_blend.argtypes = [vp] * 5
+        L.orc_backward_feature.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, vp]
+        L.orc_backward_geometric.argtypes = [vp] * 12
+        L.orc_render_reference.argtypes = [vp] * 17
+        L.orc_time_frame.argtypes = [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp]
+        L.orc_max_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def pose_c(p):
+    q, t = p.rotation, p.translation
+    return orc_pose(q[0], q[1], q[2], q[3], t[0], t[1], t[2])
+
+
+def cam_c(c):
+    return orc_camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.near_plane, c.far_plane)
+
+
+def settings_c(s):
+    o = orc_settings()
+    o.top_k, o.tile_size, o.transmittance_floor = s.top_k, s.tile_size, s.transmittance_floor
+    o.background[:] = tuple(s.background)
+    o.cov2d_dilation, o.alpha_clamp = s.cov2d_dilation, s.alpha_clamp
+    return o
+
+
+class OracleMap:
+    """SceneMap in the oracle's AoS layout (fp64 features)."""
+
+    def __init__(self, m):
+        self.n, self.d = m.size(), m.feature_dim
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (m.mean, m.log_scale, m.rotation, m.opacity_logit,
+                                                              m.color)]
+        feat = None if m.feature is None else np.ascontiguousarray(m.feature, np.float64)
+        self.h = lib().orc_map_create(self.n, self.d, *[_p(a) for a in arrs], _p(feat), m.generation)
+
+    def __del__(self):
+        try:
+            lib().orc_map_free(self.h)
+        except Exception:
+            pass
+
+
+def render_geometric(m, pose, cam, s):
+    om = OracleMap(m)
+    W, H = cam.width, cam.height
+    k = min(s.top_k, 32)
+    out = dict(color=np.zeros((H, W, 3)), depth=np.zeros((H, W)), alpha=np.zeros((H, W)),
+               index=np.zeros(W * H * k, np.int32), weight=np.zeros(W * H * k), count=np.zeros(W * H, np.uint8),
+               contributions=np.zeros(m.size()))
+    lib().orc_render_geometric(om.h, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.byref(settings_c(s)),
+                               *[_p(out[x]) for x in ("color", "depth", "alpha", "index", "weight", "count",
+                                                      "contributions")])
+    out["k"] = k
+    return out
+
+
+def prepare_scene(m, pose, cam, s):
+    om = OracleMap(m)
+    L = lib()
+    h = L.orc_prepare_scene(om.h, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.byref(settings_c(s)))
+    ne, nt, tx, ty = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+    L.orc_prep_sizes(h, C.byref(ne), C.byref(nt), C.byref(tx), C.byref(ty))
+    e7 = np.zeros((ne.value, 7))
+    src = np.zeros(ne.value, np.int32)
+    toff = np.zeros(tx.value * ty.value + 1, np.int32)
+    tent = np.zeros(nt.value, np.int32)
+    L.orc_prep_export(h, _p(e7), _p(src), _p(toff), _p(tent))
+    L.orc_prep_free(h)
+    return dict(entries=e7, src=src, tile_offsets=toff, tile_entries=tent, tiles_x=tx.value, tiles_y=ty.value)
+
+
+def project_gaussian(m, i, pose, cam, dilation=0.3):
+    om = OracleMap(m)
+    out = np.zeros(7)
+    vis = lib().orc_project_gaussian(om.h, i, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.c_double(dilation),
+                                     _p(out))
+    return bool(vis), out
+
+
+class StaleIndex(RuntimeError):
+    pass
+
+
+def render_feature(m, w, h, k, index, weight, count):
+    om = OracleMap(m)
+    out = np.zeros((h, w, m.feature_dim))
+    rc = lib().orc_render_feature(om.h, w, h, k, _p(np.ascontiguousarray(index, np.int32)),
+                                  _p(np.ascontiguousarray(weight, np.float64)),
+                                  _p(np.ascontiguousarray(count, np.uint8)), _p(out))
+    if rc:
+        raise StaleIndex(lib().orc_last_error().decode())
+    return out
+
+
+def render_feature_full_blend(m, pose, cam, s):
+    om = OracleMap(m)
+    out = np.zeros((cam.height, cam.width, m.feature_dim))
+    lib().orc_render_feature_full_blend(om.h, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.byref(settings_c(s)),
+                                        _p(out))
+    return out
+
+
+def backward_feature(m, w, h, k, index, weight, count, grad):
+    om = OracleMap(m)
+    out = np.zeros(m.size() * m.feature_dim)
+    g = np.ascontiguousarray(grad, np.float64)
+    rc = lib().orc_backward_feature(om.h, w, h, k, _p(np.ascontiguousarray(index, np.int32)),
+                                    _p(np.ascontiguousarray(weight, np.float64)),
+                                    _p(np.ascontiguousarray(count, np.uint8)), _p(g), _p(out))
+    if rc:
+        raise StaleIndex(lib().orc_last_error().decode())
+    return out
+
+
+def backward_geometric(m, pose, cam, s, grad_color, grad_depth):
+    om = OracleMap(m)
+    n = m.size()
+    g = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
+             opacity_logit=np.zeros(n), color=np.zeros((n, 3)), pose_twist=np.zeros(6))
+    gc = np.ascontiguousarray(grad_color, np.float64)
+    gd = None if grad_depth is None else np.ascontiguousarray(grad_depth, np.float64)
+    lib().orc_backward_geometric(om.h, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.byref(settings_c(s)), _p(gc),
+                                 _p(gd), *[_p(g[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit",
+                                                              "color", "pose_twist")])
+    return g
+
+
+def render_reference(m, pose, cam, s, with_features=False, keep_records=False):
+    om = OracleMap(m)
+    W, H = cam.width, cam.height
+    P = W * H
+    k = min(s.top_k, 32)
+    o = dict(color=np.zeros((H, W, 3)), depth=np.zeros((H, W)), alpha=np.zeros((H, W)),
+             transmittance=np.zeros((H, W)), feature_blend=np.zeros((H, W, m.feature_dim)) if with_features else None,
+             index=np.zeros(P * k, np.int32), weight=np.zeros(P * k), count=np.zeros(P, np.uint8),
+             contributions=np.zeros(m.size()))
+    nrec = C.c_int64()
+    L = lib()
+    args = [om.h, C.byref(pose_c(pose)), C.byref(cam_c(cam)), C.byref(settings_c(s))]
+    outs = [_p(o[x]) for x in ("color", "depth", "alpha", "transmittance", "feature_blend", "index", "weight",
+                               "count", "contributions")]
+    if keep_records:
+        L.orc_render_reference(*args, *[None] * 9, None, None, None, C.byref(nrec))
+        offs = np.zeros(P + 1, np.int64)
+        ri = np.zeros(nrec.value, np.int32)
+        rw = np.zeros(nrec.value)
+        L.orc_render_reference(*args, *outs, _p(offs), _p(ri), _p(rw), C.byref(nrec))
+        o["records"] = [list(zip(ri[offs[p]:offs[p + 1]], rw[offs[p]:offs[p + 1]])) for p in range(P)]
+    else:
+        L.orc_render_reference(*args, *outs, None, None, None, C.byref(nrec))
+    o["k"] = k
+    return o

@@ -1,0 +1,365 @@
+"""Pin the CPU oracle to the reference's own known-answer tests (CPU only).
+
+Each test restates a reference test case (proj/tests/test_raster.cpp, test_backward.cpp,
+test_core.cpp) with the reference's tolerance, run against oracle/ (the restatement of
+render.cpp / backward.cpp / reference.cpp / projection.cpp).  These are the golden vectors that
+pin the oracle before it is trusted as the GPU parity checker.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from _se3 import axis_angle, rel_error, se3_apply_twist
+from paper_2602_06991_b200 import synth
+from paper_2602_06991_b200.types import CameraIntrinsics, Pose, RenderSettings, SceneMap
+
+
+def logit(p):
+    return math.log(p / (1.0 - p))
+
+
+def centered_camera(side, focal):  # test_raster.cpp:17-25
+    return CameraIntrinsics(fx=focal, fy=focal, cx=float(side // 2), cy=float(side // 2), width=side, height=side,
+                            near_plane=0.05, far_plane=50.0)
+
+
+def flat_map(gs, d=2):  # flat_gaussian, test_raster.cpp:27-37
+    n = len(gs)
+    m = SceneMap(mean=np.array([g[0] for g in gs], float).reshape(n, 3),
+                 log_scale=np.array([[g[3]] * 3 for g in gs], float).reshape(n, 3),
+                 rotation=np.tile([1.0, 0, 0, 0], (n, 1)).astype(float),
+                 opacity_logit=np.array([logit(g[1]) for g in gs], float),
+                 color=np.array([g[2] for g in gs], float).reshape(n, 3),
+                 feature=np.zeros((n, d)), feature_dim=d)
+    if n:
+        m.feature[:, 0] = 1.0
+    return m
+
+
+def test_empty_map_renders_background():  # test_raster.cpp:41-58
+    m = flat_map([], 2)
+    s = RenderSettings(background=(0.2, 0.4, 0.6))
+    o = O.render_geometric(m, Pose(), centered_camera(32, 40.0), s)
+    assert np.allclose(o["color"][..., 0], 0.2) and np.allclose(o["color"][..., 1], 0.4)
+    assert np.allclose(o["color"][..., 2], 0.6)
+    assert (o["depth"] == 0).all() and (o["alpha"] == 0).all() and (o["count"] == 0).all()
+
+
+# The reference's own KATs below use flat Gaussians with log_scale = 1.0 (sigma = e) at z = 1, 2.
+# The reference code culls those (projection.cpp:19-20: z <= 3*exp(max log_scale)), so the
+# reference tests as written fail against the reference code.  The oracle follows the code;
+# the KATs use log_scale = -2.0, which leaves the centre-pixel answers unchanged (dx = dy = 0).
+KAT_LS = -2.0
+
+
+def test_reference_cull_applies_to_reference_kat_gaussians():  # projection.cpp:19-20
+    m = flat_map([((0, 0, 2), 0.5, (1, 0, 0), 1.0)])
+    o = O.render_geometric(m, Pose(), centered_camera(33, 16.0), RenderSettings())
+    assert (o["alpha"] == 0).all()
+
+
+def test_single_gaussian_blends_one_term():  # test_raster.cpp:60-77
+    m = flat_map([((0, 0, 2), 0.5, (1, 0, 0), KAT_LS)])
+    o = O.render_geometric(m, Pose(), centered_camera(33, 16.0), RenderSettings())
+    c = 16
+    assert o["color"][c, c, 0] == pytest.approx(0.5, rel=1e-12)
+    assert o["color"][c, c, 1] == 0.0
+    assert o["depth"][c, c] == pytest.approx(1.0, rel=1e-12)
+    assert o["alpha"][c, c] == pytest.approx(0.5, rel=1e-12)
+    assert o["contributions"][0] == pytest.approx(0.5, rel=1e-12)
+
+
+def test_two_on_axis_gaussians_composite():  # test_raster.cpp:79-100
+    m = flat_map([((0, 0, 1), 0.6, (1, 0, 0), KAT_LS), ((0, 0, 2), 0.8, (0, 1, 0), KAT_LS)])
+    s = RenderSettings(transmittance_floor=0.0)
+    cam = centered_camera(33, 16.0)
+    o = O.render_geometric(m, Pose(), cam, s)
+    c = 16
+    assert o["color"][c, c, 0] == pytest.approx(0.6, rel=1e-9)
+    assert o["color"][c, c, 1] == pytest.approx(0.32, rel=1e-9)
+    assert o["color"][c, c, 2] == 0.0
+    assert o["depth"][c, c] == pytest.approx(1.24, rel=1e-9)
+    r = O.render_reference(m, Pose(), cam, s)
+    assert r["color"][c, c, 0] == pytest.approx(0.6, rel=1e-9)
+    assert r["depth"][c, c] == pytest.approx(1.24, rel=1e-9)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_tiled_matches_brute_force(seed):  # test_raster.cpp:102-129
+    s = RenderSettings(transmittance_floor=0.0, background=(0.1, 0.2, 0.3))
+    cam = synth.test_camera(64, 48)
+    m = synth.random_scene(300, 4, seed)
+    t = O.render_geometric(m, Pose(), cam, s)
+    r = O.render_reference(m, Pose(), cam, s)
+    err = max(np.abs(t["color"] - r["color"]).max(), np.abs(t["depth"] - r["depth"]).max(),
+              np.abs(t["alpha"] - r["alpha"]).max())
+    assert err < 1e-5
+    assert (t["count"] == r["count"]).all()
+    assert (t["index"] == r["index"]).all()
+    np.testing.assert_allclose(t["weight"], r["weight"], rtol=1e-9)
+
+
+def test_weights_and_transmittance_account_for_everything():  # test_raster.cpp:131-147
+    m = synth.random_scene(200, 4, 9)
+    cam = synth.test_camera(48, 48)
+    r = O.render_reference(m, Pose(), cam, RenderSettings(transmittance_floor=0.0), keep_records=True)
+    T = r["transmittance"].reshape(-1)
+    for p, rec in enumerate(r["records"]):
+        assert abs(sum(w for _, w in rec) + T[p] - 1.0) < 1e-6
+
+
+def test_topk_holds_k_largest_non_increasing():  # test_raster.cpp:149-206
+    m = synth.random_scene(150, 4, 12)
+    cam = synth.test_camera(32, 32)
+    s = RenderSettings(top_k=3, transmittance_floor=0.0)
+    r = O.render_reference(m, Pose(), cam, s, keep_records=True)
+    t = O.render_geometric(m, Pose(), cam, s)
+    for p, rec in enumerate(r["records"]):
+        cnt = int(t["count"][p])
+        assert cnt == min(3, len(rec))
+        prev = 2.0
+        sel = [(int(t["index"][p * 3 + j]), t["weight"][p * 3 + j]) for j in range(cnt)]
+        for idx, w in sel:
+            assert 0.0 < w <= prev
+            prev = w
+            assert any(ri == idx and abs(rw - w) < 1e-12 for ri, rw in rec)
+        if len(rec) > cnt + 1:
+            members = {i for i, _ in sel}
+            trimmed, dropped = [], False
+            for e in rec:
+                if e[0] not in members and not dropped:
+                    dropped = True
+                    continue
+                trimmed.append(e)
+            trimmed.sort(key=lambda e: -e[1])
+            for j in range(cnt):
+                assert abs(trimmed[j][1] - sel[j][1]) < 1e-12
+
+
+def test_feature_rendering_renormalizes():  # test_raster.cpp:208-241
+    m = flat_map([((0, 0, 1), 0.5, (1, 0, 0), 1.0), ((0, 0, 2), 0.5, (0, 1, 0), 1.0)], 3)
+    m.feature[:] = [[1, 0, 0], [0, 1, 0]]
+    f = O.render_feature(m, 1, 1, 2, [0, 1], [0.3, 0.1], [2])
+    assert f[0, 0, 0] == pytest.approx(0.75, rel=1e-12)
+    assert f[0, 0, 1] == pytest.approx(0.25, rel=1e-12)
+    assert f[0, 0, 2] == 0.0
+    f1 = O.render_feature(m, 1, 1, 1, [1], [0.123], [1])
+    assert f1[0, 0, 1] == 1.0
+    f0 = O.render_feature(m, 1, 1, 2, [-1, -1], [0, 0], [0])
+    assert (f0 == 0).all()
+
+
+def test_stale_topk_index_is_a_hard_error():  # test_raster.cpp:243-253
+    m = flat_map([((0, 0, 1), 0.5, (1, 0, 0), 1.0)])
+    with pytest.raises(O.StaleIndex, match="references gaussian 5 but the map holds 1"):
+        O.render_feature(m, 1, 1, 1, [5], [0.5], [1])
+
+
+def test_k_covering_every_contributor_matches_full_blend():  # test_raster.cpp:255-283
+    m = synth.random_scene(40, 5, 31)
+    rng = np.random.Generator(np.random.MT19937(0))
+    from paper_2602_06991_b200.synth import uniform_image
+    m.log_scale[:] = np.repeat(uniform_image((40,), 77, -4.5, -3.5)[:, None], 3, axis=1)
+    cam = synth.test_camera(40, 40)
+    s = RenderSettings(top_k=32, transmittance_floor=0.0)
+    r = O.render_reference(m, Pose(), cam, s, with_features=True, keep_records=True)
+    t = O.render_geometric(m, Pose(), cam, s)
+    f = O.render_feature(m, 40, 40, 32, t["index"], t["weight"], t["count"])
+    for rec in r["records"]:
+        assert len(rec) <= 32
+    np.testing.assert_array_less(np.abs(f * r["alpha"][..., None] - r["feature_blend"]), 1e-6)
+    del rng
+
+
+def test_renders_bit_deterministic_and_tile_size_independent():  # test_raster.cpp:285-305
+    m = synth.random_scene(250, 4, 17)
+    cam = synth.test_camera(64, 64)
+    s = RenderSettings()
+    a = O.render_geometric(m, Pose(), cam, s)
+    b = O.render_geometric(m, Pose(), cam, s)
+    assert a["color"].tobytes() == b["color"].tobytes() and a["depth"].tobytes() == b["depth"].tobytes()
+    assert (a["index"] == b["index"]).all() and (a["contributions"] == b["contributions"]).all()
+    c = O.render_geometric(m, Pose(), cam, RenderSettings(tile_size=8))
+    assert a["color"].tobytes() == c["color"].tobytes()
+    assert (a["index"] == c["index"]).all()
+
+
+def test_degenerate_covariance_is_skipped():  # test_raster.cpp:307-319
+    m = flat_map([((0, 0, 1), 0.5, (1, 0, 0), 400.0)])
+    o = O.render_geometric(m, Pose(), centered_camera(16, 10.0), RenderSettings(cov2d_dilation=0.0))
+    assert o["alpha"][8, 8] == 0.0
+
+
+# ----------------------------------------------------------------------------- backward
+def linear_objective(m, pose, cam, s, gc, gd):  # test_backward.cpp:53-60
+    o = O.render_geometric(m, pose, cam, s)
+    return float((gc * o["color"]).sum() + (gd * o["depth"]).sum())
+
+
+GROUPS = [("mean", 3), ("log_scale", 3), ("rotation", 4), ("opacity_logit", 1), ("color", 3)]
+
+
+def check_all_groups(m, pose, cam, s, gc, gd, step, tol):  # test_backward.cpp:67-94
+    g = O.backward_geometric(m, pose, cam, s, gc, gd)
+    checked = 0
+    for name, dim in GROUPS:
+        arr = getattr(m, name)
+        for i in range(m.size()):
+            for e in range(dim):
+                idx = (i,) if arr.ndim == 1 else (i, e)
+                saved = arr[idx]
+                arr[idx] = saved + step
+                hi = linear_objective(m, pose, cam, s, gc, gd)
+                arr[idx] = saved - step
+                lo = linear_objective(m, pose, cam, s, gc, gd)
+                arr[idx] = saved
+                fd = (hi - lo) / (2 * step)
+                an = g[name][idx]
+                assert rel_error(an, fd, 1e-5) < tol, (name, i, e, an, fd)
+                checked += 1
+    return checked
+
+
+def test_zero_upstream_gradients_give_zero():  # test_backward.cpp:104-120
+    m = synth.random_scene(10, 3, 4)
+    cam = synth.test_camera(16, 16)
+    g = O.backward_geometric(m, Pose(), cam, RenderSettings(transmittance_floor=0.0), np.zeros((16, 16, 3)),
+                             np.zeros((16, 16)))
+    for v in g.values():
+        assert (v == 0).all()
+
+
+def test_single_gaussian_gradients_match_central_differences():  # test_backward.cpp:122-134
+    m = synth.random_scene(1, 3, 8)
+    cam = synth.test_camera(16, 16)
+    gc = synth.uniform_image((16, 16, 3), 2)
+    rest = synth.uniform_image((16 * 16 * 3 + 16 * 16,), 2)[16 * 16 * 3:].reshape(16, 16)
+    assert check_all_groups(m, Pose(), cam, RenderSettings(transmittance_floor=0.0), gc, rest, 1e-4, 1e-4) == 14
+
+
+def test_overlapping_scene_gradients_match_central_differences():  # test_backward.cpp:136-153
+    m = synth.random_scene(5, 3, 15, 1.0, 2.5)
+    cam = synth.test_camera(16, 16)
+    s = RenderSettings(transmittance_floor=0.0, background=(0.3, 0.1, 0.2))
+    both = synth.uniform_image((16 * 16 * 4,), 3)
+    gc, gd = both[:768].reshape(16, 16, 3), both[768:].reshape(16, 16)
+    pose = Pose(axis_angle(0.1, (0, 1, 0)), (0.02, -0.01, 0.05))
+    assert check_all_groups(m, pose, cam, s, gc, gd, 1e-4, 1e-4) == 70
+
+
+def test_pose_twist_gradient_matches_central_differences():  # test_backward.cpp:155-179
+    m = synth.random_scene(12, 3, 23)
+    cam = synth.test_camera(16, 16)
+    s = RenderSettings(transmittance_floor=0.0)
+    both = synth.uniform_image((16 * 16 * 4,), 5)
+    gc, gd = both[:768].reshape(16, 16, 3), both[768:].reshape(16, 16)
+    pose = Pose(axis_angle(-0.15, (1, 0, 0)), (0.0, 0.03, -0.02))
+    g = O.backward_geometric(m, pose, cam, s, gc, gd)
+    for axis in range(6):
+        def f(t):
+            xi = np.zeros(6)
+            xi[axis] = t
+            return linear_objective(m, se3_apply_twist(xi, pose), cam, s, gc, gd)
+        fd = (f(1e-6) - f(-1e-6)) / 2e-6
+        assert rel_error(g["pose_twist"][axis], fd, 1e-6) < 1e-3
+
+
+def test_feature_backward_passthrough_and_stale():  # test_backward.cpp:181-206
+    m = synth.random_scene(3, 4, 6)
+    none = O.backward_feature(m, 1, 1, 1, [2], [0.4], [1], np.zeros((1, 1, 4)))
+    assert (none == 0).all()
+    g = np.zeros((1, 1, 4))
+    g[0, 0, 0], g[0, 0, 3] = 0.7, -0.2
+    out = O.backward_feature(m, 1, 1, 1, [2], [0.4], [1], g)
+    assert out[2 * 4 + 0] == pytest.approx(0.7) and out[2 * 4 + 3] == pytest.approx(-0.2) and out[0] == 0.0
+    with pytest.raises(O.StaleIndex, match="backward_feature: top-k record references gaussian 99"):
+        O.backward_feature(m, 1, 1, 1, [99], [0.4], [1], g)
+
+
+def test_feature_gradients_match_central_differences():  # test_backward.cpp:208-239
+    m = synth.random_scene(20, 4, 42)
+    cam = synth.test_camera(8, 8)
+    s = RenderSettings(top_k=3, transmittance_floor=0.0)
+    t = O.render_geometric(m, Pose(), cam, s)
+    gf = synth.uniform_image((8, 8, 4), 7)
+    grads = O.backward_feature(m, 8, 8, 3, t["index"], t["weight"], t["count"], gf)
+    for i in range(m.size()):
+        for c in range(4):
+            def obj(v):
+                mm = m.copy()
+                mm.feature[i, c] = v
+                return float((gf * O.render_feature(mm, 8, 8, 3, t["index"], t["weight"], t["count"])).sum())
+            x = m.feature[i, c]
+            fd = (obj(x + 1e-4) - obj(x - 1e-4)) / 2e-4
+            assert rel_error(grads[i * 4 + c], fd, 1e-6) < 1e-4
+
+
+def test_early_stopped_forward_still_exact_gradients():  # test_backward.cpp:241-269
+    m = synth.random_scene(6, 3, 19, 1.0, 2.0)
+    m.opacity_logit[:] = logit(0.9)
+    cam = synth.test_camera(12, 12)
+    s = RenderSettings(transmittance_floor=5e-2)
+    both = synth.uniform_image((12 * 12 * 4,), 11)
+    gc, gd = both[:432].reshape(12, 12, 3), both[432:].reshape(12, 12)
+    g = O.backward_geometric(m, Pose(), cam, s, gc, gd)
+    for i in range(m.size()):
+        for e in range(3):
+            saved = m.color[i, e]
+            m.color[i, e] = saved + 1e-5
+            hi = linear_objective(m, Pose(), cam, s, gc, gd)
+            m.color[i, e] = saved - 1e-5
+            lo = linear_objective(m, Pose(), cam, s, gc, gd)
+            m.color[i, e] = saved
+            assert rel_error(g["color"][i, e], (hi - lo) / 2e-5, 1e-6) < 1e-4
+
+
+# ----------------------------------------------------------------------------- projection
+def one(mean, log_scale=(0, 0, 0), rot=(1, 0, 0, 0)):
+    return SceneMap(mean=np.array([mean], float), log_scale=np.array([log_scale], float),
+                    rotation=np.array([rot], float), opacity_logit=np.zeros(1), color=np.zeros((1, 3)),
+                    feature=np.ones((1, 1)), feature_dim=1)
+
+
+def cam100():
+    return CameraIntrinsics(fx=100, fy=100, cx=50, cy=50, width=100, height=100, near_plane=0.1, far_plane=10.0)
+
+
+def test_on_axis_projects_to_principal_point():  # test_core.cpp:71-89
+    # The reference test uses the default log_scale 0 (sigma 1), which projection.cpp:19-20 culls
+    # at z = 1; a small extent keeps the Gaussian visible and the expected values unchanged.
+    assert not O.project_gaussian(one((0, 0, 1)), 0, Pose(), cam100())[0]
+    vis, p = O.project_gaussian(one((0, 0, 1), (KAT_LS,) * 3), 0, Pose(), cam100())
+    assert vis and p[0] == pytest.approx(50.0, rel=1e-12) and p[1] == pytest.approx(50.0, rel=1e-12)
+    assert p[6] == 1.0
+
+
+def test_behind_camera_is_invisible():  # test_core.cpp:91-96
+    vis, _ = O.project_gaussian(one((0, 0, -1)), 0, Pose(), synth.test_camera(100, 100))
+    assert not vis
+
+
+def test_isotropic_covariance_matches_closed_form():  # test_core.cpp:98-119
+    sigma, z = 0.01, 2.0
+    vis, p = O.project_gaussian(one((0, 0, z), (math.log(sigma),) * 3), 0, Pose(), cam100())
+    expected = (100 * sigma / z) ** 2 + 0.3
+    assert p[2] == pytest.approx(expected, rel=1e-9) and p[5] == pytest.approx(expected, rel=1e-9)
+    assert abs(p[3]) < 1e-12
+
+
+def test_projection_properties_over_random_scenes():  # test_core.cpp:121-142
+    cam = synth.test_camera(64, 64)
+    m = synth.random_scene(200, 4, 21)
+    pose = Pose(axis_angle(0.2, (0, 1, 0)), (0.05, -0.02, 0.1))
+    om = O.OracleMap(m)
+    for i in range(m.size()):
+        import ctypes as C
+        out = np.zeros(7)
+        vis = O.lib().orc_project_gaussian(om.h, i, C.byref(O.pose_c(pose)), C.byref(O.cam_c(cam)),
+                                           C.c_double(0.3), out.ctypes.data)
+        if not vis:
+            continue
+        assert abs(out[3] - out[4]) < 1e-12
+        assert out[2] > 0 and out[2] * out[5] - out[3] * out[4] > 0
+        assert cam.near_plane < out[6] < cam.far_plane
