@@ -60,9 +60,10 @@ def test_prepared_scene_exact(R, name, mk, cam, pose, tile):
     assert (g.src == o["src"]).all(), "depth order differs"
     assert (g.tile_offsets == o["tile_offsets"]).all(), "tile CSR offsets differ"
     assert (g.tile_entries == o["tile_entries"]).all(), "tile lists differ"
-    # geometry is bit-identical except opacity (exp in logistic may differ by an ulp)
-    assert (g.entries[:, :6] == o["entries"][:, :6]).all()
-    np.testing.assert_allclose(g.entries[:, 6], o["entries"][:, 6], rtol=1e-15)
+    # mean2d and depth are bit-identical (mul/add/div only); the inverse covariance and opacity
+    # go through exp() (CUDA libdevice vs glibc), which may differ in the last ulp
+    assert (g.entries[:, [0, 1, 5]] == o["entries"][:, [0, 1, 5]]).all()
+    np.testing.assert_allclose(g.entries[:, [2, 3, 4, 6]], o["entries"][:, [2, 3, 4, 6]], rtol=1e-13)
 
 
 @pytest.mark.parametrize("name,mk,cam,pose", SCENES, ids=[s[0] for s in SCENES])
