@@ -114,9 +114,19 @@ __global__ void __launch_bounds__(256) k_project(ProjectParams p) {
         smax = 0ull;
     }
     __syncthreads();
-    if (ok) {
-        atomicMin(&smin, static_cast<unsigned long long>(key));
-        atomicMax(&smax, static_cast<unsigned long long>(key));
+    {
+        unsigned long long lo = ok ? key : ~0ull, hi = ok ? key : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+            const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+            lo = a < lo ? a : lo;
+            hi = b > hi ? b : hi;
+        }
+        if ((threadIdx.x & 31) == 0 && hi >= lo) {
+            atomicMin(&smin, lo);
+            atomicMax(&smax, hi);
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0 && smax >= smin) {
