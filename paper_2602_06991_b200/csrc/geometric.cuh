@@ -11,7 +11,6 @@ struct GeomFwdParams {
     TileEntries te;
     const int32_t* tile_offsets;  // CSR over tiles (reference tile_offsets)
     const int32_t* padded_start;  // start of each tile in the padded tile-ordered arrays
-    int sub_x, sub_y;             // 16x16 pixel blocks per tile (tile_size > 16)
     // kGeomForward outputs (any may be null except aux)
     double* color;
     double* depth;
@@ -33,7 +32,6 @@ struct GeomBwdParams {
     TileEntries te;
     const int32_t* tile_offsets;
     const int32_t* padded_start;
-    int sub_x, sub_y;
     PixelAux aux;              // from the forward
     const double* grad_color;  // P x 3
     const double* grad_depth;  // P or null
@@ -57,7 +55,8 @@ struct ChainParams {
     double* twist;  // n x 6
 };
 
-// returns dynamic smem bytes used
+// number of one-warp CTAs covering the frame (8x4 pixel blocks per tile)
+int geom_blocks(const Frame& f);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
 void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);

@@ -483,7 +483,6 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     c->prep_key = key;
 }
 
-int sub_blocks(int tile_size) { return tile_size <= 16 ? 1 : (tile_size + 15) / 16; }
 
 // geometric_pass (render.cpp:158-240).  Record/colour outputs are optional (null = skip);
 // the per-pixel aux (final T, entries visited) is always written for the backward.
@@ -497,7 +496,6 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
     gp.te = tile_entries(c);
     gp.tile_offsets = ptr<int32_t>(c->tile_offsets);
     gp.padded_start = ptr<int32_t>(c->padded_start);
-    gp.sub_x = gp.sub_y = sub_blocks(f.tile_size);
     gp.aux.t_final = ensure<double>(c->aux_t, P);
     gp.aux.n_iter = ensure<int32_t>(c->aux_n, P);
     if (records) {
@@ -510,7 +508,7 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
         gp.contrib = ensure<unsigned long long>(c->o_contrib, c->n);
         CK(cudaMemsetAsync(gp.contrib, 0, std::max<int64_t>(c->n, 1) * sizeof(double), st));
     }
-    const int nblk = f.tiles_x * f.tiles_y * gp.sub_x * gp.sub_y;
+    const int nblk = tk::geom_blocks(f);
     {
         PhaseScope phase(c, TK_PHASE_GEOM_FWD);
         tk::launch_geom_fwd(tk::kGeomForward, gp, nblk, st);
@@ -892,11 +890,10 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
         gp.te = tile_entries(c);
         gp.tile_offsets = ptr<int32_t>(c->tile_offsets);
         gp.padded_start = ptr<int32_t>(c->padded_start);
-        gp.sub_x = gp.sub_y = sub_blocks(f.tile_size);
-        gp.list_count = ensure<int32_t>(c->l_count, P + 1);
+            gp.list_count = ensure<int32_t>(c->l_count, P + 1);
         int32_t* off = ensure<int32_t>(c->l_off, P + 1);
         CK(cudaMemsetAsync(gp.list_count + P, 0, sizeof(int32_t), st));
-        const int nblk = f.tiles_x * f.tiles_y * gp.sub_x * gp.sub_y;
+        const int nblk = tk::geom_blocks(f);
         tk::launch_geom_fwd(tk::kGeomCount, gp, nblk, st);
         ensure_scratch(c, P + 1);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
@@ -958,7 +955,6 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         bp.te = tile_entries(c);
         bp.tile_offsets = ptr<int32_t>(c->tile_offsets);
         bp.padded_start = ptr<int32_t>(c->padded_start);
-        bp.sub_x = bp.sub_y = sub_blocks(f.tile_size);
         bp.aux.t_final = ptr<double>(c->aux_t);
         bp.aux.n_iter = ptr<int32_t>(c->aux_n);
         bp.grad_color = gc;
@@ -966,7 +962,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         bp.mid = mid;
         {
             PhaseScope phase(c, TK_PHASE_GEOM_BWD);
-            tk::launch_geom_bwd(bp, f.tiles_x * f.tiles_y * bp.sub_x * bp.sub_y, st);
+            tk::launch_geom_bwd(bp, tk::geom_blocks(f), st);
         }
         c->launches += 1;
         CK_LAUNCH(c);
