@@ -57,6 +57,7 @@ struct ChainParams {
 
 // number of one-warp CTAs covering the frame (8x4 pixel blocks per tile)
 int geom_blocks(const Frame& f);
+int geom_blocks_per_tile(int tile_size);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
 void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);

@@ -193,7 +193,15 @@ __global__ void k_materialize(MaterializeParams p) {
     p.out.cg[dst] = p.color[i * 3 + 1];
     p.out.cb[dst] = p.color[i * 3 + 2];
     p.out.src[dst] = static_cast<int32_t>(i);
-    p.out.list_pos[dst] = static_cast<int32_t>(s);
+    // Bounding box of {d : -0.5 d^T A d >= cutoff}, A = (ixx, ixy; ixy, iyy): |d_x| <= sqrt(R Sxx)
+    // with R = -2 cutoff and S = A^-1.  Inflated (1e-6 relative + 1e-3 px) so that rounding can
+    // never cull an entry that contributes to a pixel of the block (culling only skips work).
+    const double ixx = p.ixx[i], ixy = p.ixy[i], iyy = p.iyy[i];
+    const double det = ixx * iyy - ixy * ixy;
+    const double r2 = -2.0 * kLogWeightCutoff;
+    const double hx = sqrt(r2 * (iyy / det)), hy = sqrt(r2 * (ixx / det));
+    p.out.hx[dst] = det > 0.0 ? static_cast<float>(hx * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
+    p.out.hy[dst] = det > 0.0 ? static_cast<float>(hy * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
 }
 
 __global__ void k_export_entries(const uint32_t* __restrict__ order, int64_t nv, const double* __restrict__ mx,

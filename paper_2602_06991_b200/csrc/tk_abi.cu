@@ -175,7 +175,8 @@ struct tk_ctx {
     DevBuf pmx, pmy, pixx, pixy, piyy, pz, pop, rect, valid, ntiles, pos;
     DevBuf dkeys, dvals, dkeys_alt, dvals_alt, ntiles_sorted, pair_off;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
-    DevBuf te[12];
+    DevBuf te[13];
+    DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
     DevBuf scratch, dscal;
     int64_t* hscal = nullptr;  // pinned mirror of dscal
     // prepared scene
@@ -336,7 +337,8 @@ tk::TileEntries tile_entries(tk_ctx* c) {
     t.cg = ptr<double>(c->te[8]);
     t.cb = ptr<double>(c->te[9]);
     t.src = ptr<int32_t>(c->te[10]);
-    t.list_pos = ptr<int32_t>(c->te[11]);
+    t.hx = ptr<float>(c->te[11]);
+    t.hy = ptr<float>(c->te[12]);
     return t;
 }
 
@@ -459,7 +461,9 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
     for (int i = 0; i < 10; ++i) ensure<double>(c->te[i], padded_cap);
     ensure<int32_t>(c->te[10], padded_cap);
-    ensure<int32_t>(c->te[11], padded_cap);
+    ensure<float>(c->te[11], padded_cap);
+    ensure<float>(c->te[12], padded_cap);
+    ensure<int32_t>(c->wl, padded_cap * tk::geom_blocks_per_tile(s->tile_size));
     tk::MaterializeParams mp{};
     mp.n_pairs = n_pairs;
     mp.tile_keys = c->tile_keys_sorted;
@@ -498,6 +502,8 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
     gp.padded_start = ptr<int32_t>(c->padded_start);
     gp.aux.t_final = ensure<double>(c->aux_t, P);
     gp.aux.n_iter = ensure<int32_t>(c->aux_n, P);
+    gp.aux.wl = ptr<int32_t>(c->wl);
+    gp.aux.wl_count = ensure<int32_t>(c->wl_count, tk::geom_blocks(f));
     if (records) {
         gp.color = ensure<double>(c->o_color, P * 3);
         gp.depth = ensure<double>(c->o_depth, P);
@@ -649,7 +655,8 @@ tk_status tk_destroy(tk_ctx* c) {
                      &c->x_count, &c->f_out, &c->f_grad_in, &c->f_grad_out, &c->s_keys, &c->s_vals,
                      &c->s_keys_alt, &c->s_vals_alt, &c->s_wnorm, &c->s_seg, &c->g_color_in, &c->g_depth_in,
                      &c->mid, &c->twist, &c->twist_part, &c->twist_out, &c->gg_mean, &c->gg_ls, &c->gg_rot,
-                     &c->gg_op, &c->gg_col, &c->l_count, &c->l_off, &c->l_src, &c->l_w, &c->gather_buf};
+                     &c->gg_op, &c->gg_col, &c->l_count, &c->l_off, &c->l_src, &c->l_w, &c->gather_buf,
+                     &c->wl, &c->wl_count};
     for (DevBuf* b : all) b->release();
     for (DevBuf& b : c->te) b.release();
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -957,6 +964,8 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         bp.padded_start = ptr<int32_t>(c->padded_start);
         bp.aux.t_final = ptr<double>(c->aux_t);
         bp.aux.n_iter = ptr<int32_t>(c->aux_n);
+        bp.aux.wl = ptr<int32_t>(c->wl);
+        bp.aux.wl_count = ptr<int32_t>(c->wl_count);
         bp.grad_color = gc;
         bp.grad_depth = gd;
         bp.mid = mid;
