@@ -269,35 +269,42 @@ void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
     if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
     else k_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    dbg_launch("k_gather", st);
 }
 
 void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
     if (vec_ok(p.feat, p.out, p.d)) k_list_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
     else k_list_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    dbg_launch("k_list_gather", st);
 }
 
 void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st) {
     if (p.n_slots > 0) k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p);
+    dbg_launch("k_slot_keys", st);
 }
 
 void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st) {
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     if (vec_ok(p.grad, p.out, p.d)) k_feat_bwd<true><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
     else k_feat_bwd<false><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
+    dbg_launch("k_feat_bwd", st);
 }
 
 void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st) {
     if (n_slots > 0) k_max_index<<<296, 256, 0, st>>>(index, n_slots, max_index);
+    dbg_launch("k_max_index", st);
 }
 
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,
                         cudaStream_t st) {
     if (n_slots > 0) k_first_stale<<<296, 256, 0, st>>>(index, n_slots, n, first);
+    dbg_launch("k_first_stale", st);
 }
 
 void launch_interleave(const float* in, int64_t n_pixels, int ds, int g, float* out, cudaStream_t st) {
     if (n_pixels > 0) k_interleave<<<148 * 8, 256, 0, st>>>(in, n_pixels, ds, g, out);
+    dbg_launch("k_interleave", st);
 }
 
 }  // namespace tk

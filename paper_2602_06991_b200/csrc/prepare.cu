@@ -135,13 +135,15 @@ __global__ void __launch_bounds__(256) k_project(ProjectParams p) {
     }
 }
 
+// Sort keys: fp64 bit pattern of z minus the smallest visible one (positive doubles order like
+// their bits, so this is monotone and packs the key range into the low bits).
 __global__ void k_compact(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
-                          const double* __restrict__ z, int64_t n, uint64_t* __restrict__ keys,
-                          uint32_t* __restrict__ vals) {
+                          const double* __restrict__ z, int64_t n, const uint64_t* __restrict__ key_min,
+                          uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n || !valid[i]) return;
     const int32_t q = pos[i];
-    keys[q] = static_cast<uint64_t>(__double_as_longlong(z[i]));
+    keys[q] = static_cast<uint64_t>(__double_as_longlong(z[i])) - *key_min;
     vals[q] = static_cast<uint32_t>(i);
 }
 
@@ -229,16 +231,19 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 
 void launch_project(const ProjectParams& p, cudaStream_t st) {
     if (p.n > 0) k_project<<<blocks_for(p.n, 256), 256, 0, st>>>(p);
+    dbg_launch("k_project", st);
 }
 
-void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, int64_t n, uint64_t* keys,
-                    uint32_t* vals, cudaStream_t st) {
-    if (n > 0) k_compact<<<blocks_for(n, 256), 256, 0, st>>>(valid, pos, z, n, keys, vals);
+void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, int64_t n, const uint64_t* key_min,
+                    uint64_t* keys, uint32_t* vals, cudaStream_t st) {
+    if (n > 0) k_compact<<<blocks_for(n, 256), 256, 0, st>>>(valid, pos, z, n, key_min, keys, vals);
+    dbg_launch("k_compact", st);
 }
 
 void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntiles, int32_t* ntiles_sorted,
                           cudaStream_t st) {
     if (nv > 0) k_sorted_ntiles<<<blocks_for(nv, 256), 256, 0, st>>>(order, nv, ntiles, ntiles_sorted);
+    dbg_launch("k_sorted_ntiles", st);
 }
 
 void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, const int32_t* ntiles_sorted,
@@ -250,10 +255,12 @@ void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, cons
 
 void launch_padded_counts(const int32_t* tile_offsets, int n_tiles, int32_t* padded, cudaStream_t st) {
     k_padded_counts<<<blocks_for(n_tiles + 1, 256), 256, 0, st>>>(tile_offsets, n_tiles, padded);
+    dbg_launch("k_padded_counts", st);
 }
 
 void launch_materialize(const MaterializeParams& p, cudaStream_t st) {
     if (p.n_pairs > 0) k_materialize<<<blocks_for(p.n_pairs, 256), 256, 0, st>>>(p);
+    dbg_launch("k_materialize", st);
 }
 
 void launch_export_entries(const uint32_t* order, int64_t nv, const double* mx, const double* my, const double* ixx,

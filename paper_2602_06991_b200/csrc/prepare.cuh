@@ -34,8 +34,8 @@ struct MaterializeParams {
 };
 
 void launch_project(const ProjectParams& p, cudaStream_t st);
-void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, int64_t n, uint64_t* keys,
-                    uint32_t* vals, cudaStream_t st);
+void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, int64_t n, const uint64_t* key_min,
+                    uint64_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntiles, int32_t* ntiles_sorted,
                           cudaStream_t st);
 void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, const int32_t* ntiles_sorted,

@@ -8,10 +8,25 @@
 #include "sort.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tk_common.cuh"
 
 namespace tk {
 
 size_t align_bytes(size_t b) { return (b + 255) / 256 * 256; }
+
+void dbg_launch(const char* name, cudaStream_t st) {
+    static const int on = [] {
+        const char* e = std::getenv("TK_SYNC_CHECK");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) std::fprintf(stderr, "[tk] kernel %s failed: %s\n", name, cudaGetErrorString(e));
+}
 
 namespace {
 
@@ -96,12 +111,33 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const int32_t* __re
     }
 }
 
+// Whole scan in one launch for small inputs (radix histograms, tile counts).
+constexpr int64_t kSmallScan = 1024 * 64;
+__global__ void __launch_bounds__(1024) k_scan_single(const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                                                      int64_t n, int64_t* __restrict__ total) {
+    const int64_t per = (n + 1023) / 1024;
+    const int64_t b = static_cast<int64_t>(threadIdx.x) * per;
+    const int64_t e = b + per < n ? b + per : n;
+    int64_t s = 0;
+    for (int64_t i = b; i < e; ++i) s += in[i];
+    int64_t tot;
+    int64_t run = block_excl_scan<1024>(s, &tot);
+    for (int64_t i = b; i < e; ++i) {
+        const int32_t v = in[i];
+        out[i] = static_cast<int32_t>(run);
+        run += v;
+    }
+    if (threadIdx.x == 0) *total = tot;
+}
+
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ROUNDS = 16;
+constexpr int RS_ROUNDS = 8;
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;
 constexpr int RS_RADIX = 256;
 
+// Per-block digit histogram.  Warp-aggregated (match_any) so runs of equal digits -- tile ids,
+// Gaussian ids -- cost one shared atomic per distinct digit per warp.
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, int64_t n, int shift,
                                                         int32_t* __restrict__ hist, int nb) {
@@ -109,66 +145,109 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
     cnt[threadIdx.x] = 0;
     __syncthreads();
     const int64_t base = static_cast<int64_t>(blockIdx.x) * RS_TILE;
+    const unsigned lane = threadIdx.x & 31;
 #pragma unroll 4
     for (int r = 0; r < RS_ROUNDS; ++r) {
         const int64_t idx = base + r * RS_THREADS + threadIdx.x;
-        if (idx < n) atomicAdd(&cnt[static_cast<unsigned>(keys[idx] >> shift) & 0xffu], 1);
+        const unsigned d = idx < n ? static_cast<unsigned>(keys[idx] >> shift) & 0xffu : RS_RADIX;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        if (d < RS_RADIX && lane == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&cnt[d], __popc(peers));
     }
     __syncthreads();
     hist[static_cast<int64_t>(threadIdx.x) * nb + blockIdx.x] = cnt[threadIdx.x];
 }
 
+// Stable scatter: rank every key of the block's tile (match_any within warps, prefix across
+// warps and rounds), place it digit-sorted in shared memory, then write each digit's run to
+// its global offset with consecutive threads on consecutive addresses.
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            int64_t n, int shift, const int32_t* __restrict__ offs,
                                                            int nb) {
-    __shared__ int32_t base[RS_RADIX];
-    __shared__ int32_t wc[RS_WARPS][RS_RADIX + 1];
+    __shared__ int32_t gbase[RS_RADIX];
+    __shared__ int32_t lstart[RS_RADIX];
+    __shared__ int32_t run[RS_RADIX];
+    __shared__ int32_t wc[RS_WARPS][RS_RADIX];
+    __shared__ K skey[RS_TILE];
+    __shared__ uint32_t sval[RS_TILE];
+    __shared__ int32_t wsum[RS_WARPS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    base[tid] = offs[static_cast<int64_t>(tid) * nb + blockIdx.x];
-#pragma unroll
-    for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * RS_TILE;
+    const int tile_n = static_cast<int>(n - tile0 < RS_TILE ? n - tile0 : RS_TILE);
+    gbase[tid] = offs[static_cast<int64_t>(tid) * nb + blockIdx.x];
+    run[tid] = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
+    // local digit counts of the tile -> lstart (exclusive prefix over digits)
+    K key[RS_ROUNDS];
+    uint32_t val[RS_ROUNDS];
+    unsigned dig[RS_ROUNDS];
     __syncthreads();
+#pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
-        const int64_t idx = tile0 + r * RS_THREADS + tid;
-        const bool valid = idx < n;
-        K key = 0;
-        uint32_t val = 0;
-        unsigned digit = RS_RADIX;  // invalid lanes group together and are never written
-        if (valid) {
-            key = kin[idx];
-            val = vin[idx];
-            digit = static_cast<unsigned>(key >> shift) & 0xffu;
+        const int li = r * RS_THREADS + tid;
+        dig[r] = RS_RADIX;
+        if (li < tile_n) {
+            key[r] = kin[tile0 + li];
+            val[r] = vin[tile0 + li];
+            dig[r] = static_cast<unsigned>(key[r] >> shift) & 0xffu;
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, digit);
-        const int rank = __popc(peers & lt);
-        const bool leader = rank == 0;
-        if (leader && valid) wc[warp][digit] = __popc(peers);
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
+        if (dig[r] < RS_RADIX && lane == __ffs(peers) - 1) atomicAdd(&run[dig[r]], __popc(peers));
+    }
+    __syncthreads();
+    {  // block exclusive scan of run[] (256 digits, one per thread) into lstart
+        const int v = run[tid];
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) wsum[warp] = incl;
         __syncthreads();
-        {  // thread d: exclusive prefix over warps of digit d, then advance the running base
-            int32_t run = base[tid];
+        int woff = 0;
+        for (int w = 0; w < warp; ++w) woff += wsum[w];
+        lstart[tid] = woff + incl - v;
+        run[tid] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        const unsigned d = dig[r];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int rank = __popc(peers & lt);
+        if (d < RS_RADIX && rank == 0) wc[warp][d] = __popc(peers);
+        __syncthreads();
+        {  // thread d: prefix over warps, continuing this digit's running count
+            int32_t acc = run[tid];
 #pragma unroll
             for (int w = 0; w < RS_WARPS; ++w) {
                 const int32_t c = wc[w][tid];
-                wc[w][tid] = run;
-                run += c;
+                wc[w][tid] = acc;
+                acc += c;
             }
-            base[tid] = run;
+            run[tid] = acc;
         }
         __syncthreads();
-        if (valid) {
-            const int32_t pos = wc[warp][digit] + rank;
-            kout[pos] = key;
-            vout[pos] = val;
+        if (d < RS_RADIX) {
+            const int lpos = lstart[d] + wc[warp][d] + rank;
+            skey[lpos] = key[r];
+            sval[lpos] = val[r];
         }
         __syncthreads();
 #pragma unroll
         for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
         __syncthreads();
-        if (tile0 + (r + 1) * RS_THREADS >= n) break;  // uniform across the block
+    }
+    for (int j = tid; j < tile_n; j += RS_THREADS) {
+        const K kj = skey[j];
+        const unsigned d = static_cast<unsigned>(kj >> shift) & 0xffu;
+        const int32_t gpos = gbase[d] + (j - lstart[d]);
+        kout[gpos] = kj;
+        vout[gpos] = sval[j];
     }
 }
 
@@ -192,14 +271,46 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
     bool in_alt = false;
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         k_rs_hist<K><<<nb, RS_THREADS, 0, st>>>(kin, n, shift, hist, nb);
+        dbg_launch("k_rs_hist", st);
         scan_exclusive(hist, hist, hn, total, scan_scratch, st, launches);
         k_rs_scatter<K><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb);
+        dbg_launch("k_rs_scatter", st);
         *launches += 2;
         std::swap(kin, kout);
         std::swap(vin, vout);
         in_alt = !in_alt;
     }
     *result_in_alt = in_alt;
+}
+
+// Finish a radix sort that only ordered key bits >= lo_bit: sort each run of equal high bits by
+// (full key, value).  Runs longer than 64 set *overflow (the caller redoes a full sort).
+__global__ void k_fixup_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n, int lo_bit,
+                             int32_t* __restrict__ overflow) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t c = keys[i] >> lo_bit;
+    if (i > 0 && (keys[i - 1] >> lo_bit) == c) return;
+    int64_t j = i + 1;
+    while (j < n && (keys[j] >> lo_bit) == c) {
+        ++j;
+        if (j - i > 64) {
+            *overflow = 1;
+            return;
+        }
+    }
+    for (int64_t a = i + 1; a < j; ++a) {  // insertion sort by (key, val)
+        const uint64_t k = keys[a];
+        const uint32_t v = vals[a];
+        int64_t b = a - 1;
+        while (b >= i && (keys[b] > k || (keys[b] == k && vals[b] > v))) {
+            keys[b + 1] = keys[b];
+            vals[b + 1] = vals[b];
+            --b;
+        }
+        keys[b + 1] = k;
+        vals[b + 1] = v;
+    }
 }
 
 __global__ void k_segment_offsets(const uint32_t* __restrict__ keys, int64_t n, int32_t* __restrict__ offsets,
@@ -224,11 +335,20 @@ size_t scan_scratch_bytes(int64_t n) {
 
 void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch, cudaStream_t st,
                     int64_t* launches) {
+    if (n <= kSmallScan) {
+        k_scan_single<<<1, 1024, 0, st>>>(in, out, n, total);
+        dbg_launch("k_scan_single", st);
+        *launches += 1;
+        return;
+    }
     const int64_t nb = std::max<int64_t>(1, (n + SCAN_TILE - 1) / SCAN_TILE);
     int64_t* bsum = static_cast<int64_t*>(scratch);
     k_scan_reduce<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, n, bsum);
+    dbg_launch("k_scan_reduce", st);
     k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, total);
+    dbg_launch("k_scan_blocks", st);
     k_scan_apply<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, bsum);
+    dbg_launch("k_scan_apply", st);
     *launches += 3;
 }
 
@@ -252,10 +372,19 @@ void radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, ui
                               launches);
 }
 
+void fixup_runs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int lo_bit, int32_t* overflow, cudaStream_t st,
+                    int64_t* launches) {
+    if (n <= 1 || lo_bit <= 0) return;
+    k_fixup_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, vals, n, lo_bit, overflow);
+    dbg_launch("k_fixup_runs", st);
+    *launches += 1;
+}
+
 void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments, cudaStream_t st,
                          int64_t* launches) {
     const int64_t total = n_segments + 1;
     k_segment_offsets<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(keys, n, offsets, n_segments);
+    dbg_launch("k_segment_offsets", st);
     *launches += 1;
 }
 

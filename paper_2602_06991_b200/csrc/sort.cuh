@@ -25,6 +25,11 @@ void radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, ui
                           int64_t n, int begin_bit, int end_bit, void* scratch, cudaStream_t st,
                           bool* result_in_alt, int64_t* launches);
 
+// After sorting bits >= lo_bit only: order runs of equal high bits by (key, value).  Sets
+// *overflow (device int) when a run exceeds 64 keys; the caller then sorts all bits.
+void fixup_runs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int lo_bit, int32_t* overflow, cudaStream_t st,
+                    int64_t* launches);
+
 // offsets[g] = first index i with keys[i] >= g, for g in [0, n_segments]; keys sorted ascending.
 void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments,
                          cudaStream_t st, int64_t* launches);

@@ -406,7 +406,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     uint32_t* dvals = ensure<uint32_t>(c->dvals, n);
     uint64_t* dkeys_alt = ensure<uint64_t>(c->dkeys_alt, n);
     uint32_t* dvals_alt = ensure<uint32_t>(c->dvals_alt, n);
-    tk::launch_compact(pp.valid, pos, pp.z, n, dkeys, dvals, st);
+    tk::launch_compact(pp.valid, pos, pp.z, n, pp.key_min, dkeys, dvals, st);
     c->launches += n > 0;
     CK_LAUNCH(c);
     CK(cudaMemcpyAsync(c->hscal, dscal, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -415,23 +415,35 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     const uint64_t kmin = static_cast<uint64_t>(c->hscal[1]), kmax = static_cast<uint64_t>(c->hscal[2]);
     c->n_vis = n_vis;
 
-    // depth sort: stable LSD over the bits in which the visible keys differ (render.cpp:108-111)
-    bool alt = false;
-    if (n_vis > 1) {
-        const int hb = bits_for(kmin ^ kmax);
-        tk::radix_sort_pairs_u64(dkeys, dvals, dkeys_alt, dvals_alt, n_vis, 0, hb, c->scratch.p, st, &alt,
-                                 &c->launches);
-        CK_LAUNCH(c);
-    }
-    c->order = alt ? dvals_alt : dvals;
-
+    // Depth sort (render.cpp:108-111): stable LSD radix over the top 24 bits in which the visible
+    // fp64 depth keys differ (values start in src order), then every run of equal high bits is
+    // ordered by (full key, src).  A run longer than 64 keys triggers a full-width sort instead.
+    const int hb = n_vis > 1 ? bits_for(kmax - kmin) : 0;
     int32_t* nts = ensure<int32_t>(c->ntiles_sorted, n_vis);
     int32_t* poff = ensure<int32_t>(c->pair_off, n_vis);
-    tk::launch_sorted_ntiles(c->order, n_vis, pp.ntiles, nts, st);
-    c->launches += n_vis > 0;
-    tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st, &c->launches);
-    CK(cudaMemcpyAsync(c->hscal + 3, dscal + 3, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    sync(c);
+    auto depth_sort = [&](int lo_bit) {
+        bool alt = false;
+        CK(cudaMemsetAsync(dscal + 7, 0, sizeof(int64_t), st));
+        if (n_vis > 1) {
+            tk::radix_sort_pairs_u64(dkeys, dvals, dkeys_alt, dvals_alt, n_vis, lo_bit, hb, c->scratch.p, st, &alt,
+                                     &c->launches);
+            tk::fixup_runs_u64(alt ? dkeys_alt : dkeys, alt ? dvals_alt : dvals, n_vis, lo_bit,
+                               reinterpret_cast<int32_t*>(dscal + 7), st, &c->launches);
+            CK_LAUNCH(c);
+        }
+        c->order = alt ? dvals_alt : dvals;
+        tk::launch_sorted_ntiles(c->order, n_vis, pp.ntiles, nts, st);
+        c->launches += n_vis > 0;
+        tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st, &c->launches);
+        CK(cudaMemcpyAsync(c->hscal + 3, dscal + 3, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        sync(c);
+    };
+    const int lo = hb > 24 ? hb - 24 : 0;
+    depth_sort(lo);
+    if (lo > 0 && c->hscal[7] != 0) {  // pathological run of near-equal depths: sort every bit
+        tk::launch_compact(pp.valid, pos, pp.z, n, pp.key_min, dkeys, dvals, st);
+        depth_sort(0);
+    }
     const int64_t n_pairs = n_vis > 0 ? c->hscal[3] : 0;
     if (n_pairs > INT32_MAX) fail(TK_ERR_BAD_ARG, "tile list exceeds 2^31 entries");
     c->n_pairs = n_pairs;
