@@ -314,6 +314,7 @@ def main_gpu(args, cfg):
     ev0.record(stream)
     for _ in range(args.steps):
         step()
+    N.check(lib.tk_join(ctx))  # the main stream now follows the side streams' work
     ev1.record(stream)
     N.check(lib.tk_synchronize(ctx))
     barrier()
@@ -450,6 +451,7 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
     ev0.record(stream)
     for _ in range(steps):
         step()
+    N.check(lib.tk_join(ctx))
     ev1.record(stream)
     N.check(lib.tk_synchronize(ctx))
     ms = ev0.elapsed_time(ev1)

@@ -136,7 +136,10 @@ int32_t tk_abi_version(void);
 tk_status tk_create(int32_t device, tk_ctx** out);
 tk_status tk_destroy(tk_ctx* ctx);
 tk_status tk_synchronize(tk_ctx* ctx);
-void* tk_get_stream(tk_ctx* ctx); /* cudaStream_t */
+/* The context runs the feature calls and the geometry backward on two side streams so they
+ * overlap; tk_join orders the main stream (tk_get_stream) after all of them, device-side. */
+tk_status tk_join(tk_ctx* ctx);
+void* tk_get_stream(tk_ctx* ctx); /* cudaStream_t of the main stream */
 
 tk_status tk_host_alloc(size_t bytes, void** out); /* pinned host memory */
 tk_status tk_host_free(void* p);

@@ -90,6 +90,7 @@ RENDER_SYMBOLS = [
     ("tk_create", C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     ("tk_destroy", C.c_int, [C.c_void_p]),
     ("tk_synchronize", C.c_int, [C.c_void_p]),
+    ("tk_join", C.c_int, [C.c_void_p]),
     ("tk_get_stream", C.c_void_p, [C.c_void_p]),
     ("tk_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     ("tk_host_free", C.c_int, [C.c_void_p]),

@@ -2,6 +2,7 @@
 // check.  fp32 features, HBM-bound: one warp per output row, 128-bit loads of the K selected
 // D-channel rows (read-only path) and 128-bit streaming stores of the output row.
 #include "feature.cuh"
+#include "sort.cuh"
 
 namespace tk {
 
@@ -160,6 +161,59 @@ __global__ void k_slot_keys(SlotKeyParams p) {
     p.wnorm[s] = wn;
 }
 
+// Inverted index (Gaussian -> record slots) by counting: count, scan, fill, then sort every
+// segment by slot so the reduction order never depends on the atomic fill order.
+__global__ void k_slot_count(SlotKeyParams p, int32_t* __restrict__ cnt) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= p.n_slots) return;
+    const int64_t px = s / p.k;
+    const int j = static_cast<int>(s - px * p.k);
+    const int c = p.count[px];
+    const int32_t id = p.index[s];
+    float wn = 0.0f;
+    if (j < c && id >= 0) {
+        atomicAdd(&cnt[id], 1);
+        double sum = 0.0;                                    // backward.cpp:303-304, slot order
+        for (int jj = 0; jj < c; ++jj) sum += p.weight[px * p.k + jj];
+        wn = static_cast<float>(p.weight[s] / sum);
+    }
+    p.wnorm[s] = wn;
+}
+
+__global__ void k_slot_fill(SlotKeyParams p, const int32_t* __restrict__ seg, int32_t* __restrict__ cursor,
+                            uint32_t* __restrict__ recs) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= p.n_slots) return;
+    const int64_t px = s / p.k;
+    const int j = static_cast<int>(s - px * p.k);
+    const int32_t id = p.index[s];
+    if (j < p.count[px] && id >= 0) recs[seg[id] + atomicAdd(&cursor[id], 1)] = static_cast<uint32_t>(s);
+}
+
+// One warp per Gaussian: rank of each record among its segment (slots are unique).
+__global__ void __launch_bounds__(kThreads) k_seg_sort(const int32_t* __restrict__ seg, int64_t n,
+                                                       const uint32_t* __restrict__ recs,
+                                                       uint32_t* __restrict__ sorted) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < n; g += nw) {
+        const int r0 = seg[g], L = seg[g + 1] - r0;
+        if (L <= 32) {
+            const uint32_t v = lane < L ? recs[r0 + lane] : 0xffffffffu;
+            int rank = 0;
+            for (int q = 0; q < L; ++q) rank += __shfl_sync(0xffffffffu, v, q) < v ? 1 : 0;
+            if (lane < L) sorted[r0 + rank] = v;
+        } else {
+            for (int i = lane; i < L; i += 32) {
+                const uint32_t v = recs[r0 + i];
+                int rank = 0;
+                for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
+                sorted[r0 + rank] = v;
+            }
+        }
+    }
+}
+
 // backward_feature (backward.cpp:288-319) as a deterministic segmented reduction: one warp per
 // Gaussian sums its records in (pixel, slot) order and writes the dense row once.
 template <bool VEC>
@@ -282,6 +336,21 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
 void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st) {
     if (p.n_slots > 0) k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p);
     dbg_launch("k_slot_keys", st);
+}
+
+void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
+                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches) {
+    const unsigned g = static_cast<unsigned>((p.n_slots + 255) / 256);
+    cudaMemsetAsync(cnt_seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
+    cudaMemsetAsync(cursor, 0, (n_gaussians + 1) * sizeof(int32_t), st);
+    if (p.n_slots > 0) k_slot_count<<<g, 256, 0, st>>>(p, cnt_seg);
+    dbg_launch("k_slot_count", st);
+    scan_exclusive(cnt_seg, cnt_seg, n_gaussians + 1, total, scan_scratch, st, launches);
+    if (p.n_slots > 0) k_slot_fill<<<g, 256, 0, st>>>(p, cnt_seg, cursor, recs);
+    dbg_launch("k_slot_fill", st);
+    if (n_gaussians > 0) k_seg_sort<<<warp_grid(n_gaussians), kThreads, 0, st>>>(cnt_seg, n_gaussians, recs, sorted);
+    dbg_launch("k_seg_sort", st);
+    *launches += 3;
 }
 
 void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st) {

@@ -111,6 +111,62 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const int32_t* __re
     }
 }
 
+// Single-pass scan with decoupled look-back: each block publishes its aggregate, then its
+// inclusive prefix once the predecessor's prefix is known (status word: 2-bit flag | 62-bit sum).
+// Block order comes from a ticket so a block only ever waits on blocks already running.
+constexpr unsigned long long kFlagAgg = 1ull << 62, kFlagPrefix = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const int32_t* __restrict__ in,
+                                                                int32_t* __restrict__ out, int64_t n,
+                                                                unsigned long long* __restrict__ status,
+                                                                int* __restrict__ ticket, int64_t* __restrict__ total,
+                                                                int nb) {
+    __shared__ int bid_s;
+    __shared__ int64_t excl_s;
+    if (threadIdx.x == 0) bid_s = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int bid = bid_s;
+    const int64_t base = static_cast<int64_t>(bid) * SCAN_TILE + static_cast<int64_t>(threadIdx.x) * SCAN_ITEMS;
+    int32_t v[SCAN_ITEMS];
+    int64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        v[i] = base + i < n ? in[base + i] : 0;
+        s += v[i];
+    }
+    int64_t tot;
+    const int64_t local = block_excl_scan<SCAN_THREADS>(s, &tot);
+    if (threadIdx.x == 0) {
+        volatile unsigned long long* vs = status;
+        int64_t excl = 0;
+        if (bid == 0) {
+            vs[0] = kFlagPrefix | static_cast<unsigned long long>(tot);
+        } else {
+            vs[bid] = kFlagAgg | static_cast<unsigned long long>(tot);
+            __threadfence();
+            for (int p = bid - 1;;) {
+                const unsigned long long w = vs[p];
+                const unsigned long long flag = w & ~kValMask;
+                if (flag == 0) continue;
+                excl += static_cast<int64_t>(w & kValMask);
+                if (flag == kFlagPrefix) break;
+                --p;
+            }
+            __threadfence();
+            vs[bid] = kFlagPrefix | static_cast<unsigned long long>(excl + tot);
+        }
+        excl_s = excl;
+        if (bid == nb - 1) *total = excl + tot;
+    }
+    __syncthreads();
+    int64_t run = excl_s + local;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; ++i) {
+        if (base + i < n) out[base + i] = static_cast<int32_t>(run);
+        run += v[i];
+    }
+}
+
 // Whole scan in one launch for small inputs (radix histograms, tile counts).
 constexpr int64_t kSmallScan = 1024 * 64;
 __global__ void __launch_bounds__(1024) k_scan_single(const int32_t* __restrict__ in, int32_t* __restrict__ out,
@@ -330,7 +386,7 @@ __global__ void k_segment_offsets(const uint32_t* __restrict__ keys, int64_t n, 
 
 size_t scan_scratch_bytes(int64_t n) {
     const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    return align_bytes(static_cast<size_t>(nb + 1) * sizeof(int64_t));
+    return align_bytes(static_cast<size_t>(nb + 2) * sizeof(int64_t));
 }
 
 void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch, cudaStream_t st,
@@ -342,6 +398,16 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
         return;
     }
     const int64_t nb = std::max<int64_t>(1, (n + SCAN_TILE - 1) / SCAN_TILE);
+    {  // single pass: a block reads its whole tile before writing it, so in-place is safe
+        unsigned long long* status = static_cast<unsigned long long*>(scratch);
+        int* ticket = reinterpret_cast<int*>(status + nb);
+        cudaMemsetAsync(status, 0, (nb + 1) * sizeof(unsigned long long), st);
+        k_scan_lookback<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, status, ticket, total,
+                                                                          static_cast<int>(nb));
+        dbg_launch("k_scan_lookback", st);
+        *launches += 1;
+        return;
+    }
     int64_t* bsum = static_cast<int64_t*>(scratch);
     k_scan_reduce<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, n, bsum);
     dbg_launch("k_scan_reduce", st);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -161,7 +162,11 @@ struct Profiler {
 
 struct tk_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;                    // main stream (tk_get_stream)
+    cudaStream_t s_feat = nullptr, s_geo = nullptr;  // side streams: feature path, geometry backward
+    cudaStream_t cur = nullptr;                       // stream the current call enqueues on
+    cudaEvent_t ev_main = nullptr, ev_feat = nullptr, ev_geo = nullptr;
+    bool feat_pending = false, geo_pending = false;
     int64_t launches = 0;
     Profiler prof;
     // scene mirror
@@ -177,7 +182,7 @@ struct tk_ctx {
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
     DevBuf te[13];
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
-    DevBuf scratch, dscal;
+    DevBuf scratch, scratch_feat, dscal;
     int64_t* hscal = nullptr;  // pinned mirror of dscal
     // prepared scene
     bool prepared = false;
@@ -219,13 +224,13 @@ struct PhaseScope {
     PhaseScope(tk_ctx* ctx, int ph) : c(ctx), phase(ph) {
         if (c->prof.on) {
             a = c->prof.get();
-            CK(cudaEventRecord(a, c->stream));
+            CK(cudaEventRecord(a, c->cur));
         }
     }
     ~PhaseScope() {
         if (a) {
             cudaEvent_t b = c->prof.get();
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, c->cur);
             c->prof.pending.push_back({phase, a, b});
         }
     }
@@ -255,17 +260,44 @@ void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
     if (bytes == 0) return;
     PhaseScope phase(c, TK_PHASE_COPY);
     CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       c->stream));
+                       c->cur));
 }
 
 void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
     if (bytes == 0 || dst == nullptr) return;
     PhaseScope phase(c, TK_PHASE_COPY);
     CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                       c->stream));
+                       c->cur));
 }
 
-void sync(tk_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+void sync(tk_ctx* c) { CK(cudaStreamSynchronize(c->cur)); }
+
+// Stream discipline.  The main stream owns everything that (re)writes the scene mirror, the
+// PreparedScene and the forward records; the feature calls run on s_feat and the geometry
+// backward on s_geo, each ordered after the main stream's latest work (ev_main), so the
+// HBM-bound feature kernels and the fp64-bound geometry backward overlap.  Main-stream work
+// first waits for outstanding side-stream work that still reads those buffers.
+void on_main(tk_ctx* c) {
+    c->cur = c->stream;
+    if (c->feat_pending) {
+        CK(cudaStreamWaitEvent(c->stream, c->ev_feat, 0));
+        c->feat_pending = false;
+    }
+    if (c->geo_pending) {
+        CK(cudaStreamWaitEvent(c->stream, c->ev_geo, 0));
+        c->geo_pending = false;
+    }
+}
+void main_done(tk_ctx* c) { CK(cudaEventRecord(c->ev_main, c->stream)); }
+void on_side(tk_ctx* c, bool feat) {
+    c->cur = feat ? c->s_feat : c->s_geo;
+    CK(cudaStreamWaitEvent(c->cur, c->ev_main, 0));
+}
+void side_done(tk_ctx* c, bool feat) {
+    CK(cudaEventRecord(feat ? c->ev_feat : c->ev_geo, c->cur));
+    if (feat) c->feat_pending = true;
+    else c->geo_pending = true;
+}
 
 int bits_for(uint64_t max_value) {  // bits needed to represent values in [0, max_value]
     int b = 0;
@@ -342,9 +374,9 @@ tk::TileEntries tile_entries(tk_ctx* c) {
     return t;
 }
 
-void ensure_scratch(tk_ctx* c, int64_t n) {
+void ensure_scratch(tk_ctx* c, int64_t n, bool feat = false) {
     const size_t need = std::max(tk::radix_scratch_bytes(n), tk::scan_scratch_bytes(n + 1));
-    ensure<char>(c->scratch, need);
+    ensure<char>(feat ? c->scratch_feat : c->scratch, need);
 }
 
 // prepare_scene (render.cpp:73-156) on the device; cached on (pose, camera, settings, scene).
@@ -356,7 +388,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     c->aux_valid = false;
     PhaseScope phase(c, TK_PHASE_PREPARE);
     const int64_t n = c->n;
-    cudaStream_t st = c->stream;
+    cudaStream_t st = c->cur;
     const tk::Frame f = make_frame(c, cam, s);
     const int n_tiles = f.tiles_x * f.tiles_y;
     c->tiles_x = f.tiles_x;
@@ -506,7 +538,7 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
     const tk::Frame f = make_frame(c, cam, s);
     const int64_t P = static_cast<int64_t>(f.width) * f.height;
     const int k = f.k;
-    cudaStream_t st = c->stream;
+    cudaStream_t st = c->cur;
     tk::GeomFwdParams gp{};
     gp.f = f;
     gp.te = tile_entries(c);
@@ -560,7 +592,7 @@ struct Records {
 Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
     Records r;
     const int64_t n = c->n;
-    cudaStream_t st = c->stream;
+    cudaStream_t st = c->cur;
     if (!v) {
         if (!c->has_records) fail(TK_ERR_STATE, std::string(fn) + ": no records (call tk_render_geometric first)");
         r.w = c->rec_w;
@@ -645,6 +677,27 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         tk_ctx* c = new tk_ctx;
         c->device = device;
         cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+        // The HBM-bound feature chain (short dependent launches) gets the highest priority so its
+        // blocks are scheduled as soon as the long fp64 geometry-backward grid frees SM slots.
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        const char* serial = std::getenv("TK_SERIAL");  // profiling aid: one stream, no overlap
+        if (serial && serial[0] == '1') {
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_feat, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_geo, cudaStreamNonBlocking);
+            if (e == cudaSuccess) {  // alias the side streams to the main stream
+                cudaStreamDestroy(c->s_feat);
+                cudaStreamDestroy(c->s_geo);
+                c->s_feat = c->s_geo = c->stream;
+            }
+        } else {
+            if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->s_feat, cudaStreamNonBlocking, prio_hi);
+            if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->s_geo, cudaStreamNonBlocking, prio_lo);
+        }
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_feat, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_geo, cudaEventDisableTiming);
+        c->cur = c->stream;
         if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscal), 16 * sizeof(int64_t), cudaHostAllocDefault);
         if (e != cudaSuccess) {
             delete c;
@@ -658,11 +711,13 @@ tk_status tk_destroy(tk_ctx* c) {
     if (!c) return TK_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->s_feat) cudaStreamSynchronize(c->s_feat);
+    if (c->s_geo) cudaStreamSynchronize(c->s_geo);
     DevBuf* all[] = {&c->mean, &c->log_scale, &c->rotation, &c->opacity_logit, &c->color, &c->feature, &c->pmx,
                      &c->pmy, &c->pixx, &c->pixy, &c->piyy, &c->pz, &c->pop, &c->rect, &c->valid, &c->ntiles,
                      &c->pos, &c->dkeys, &c->dvals, &c->dkeys_alt, &c->dvals_alt, &c->ntiles_sorted, &c->pair_off,
                      &c->tkeys, &c->tvals, &c->tkeys_alt, &c->tvals_alt, &c->tile_offsets, &c->padded_cnt,
-                     &c->padded_start, &c->scratch, &c->dscal, &c->o_color, &c->o_depth, &c->o_alpha, &c->o_index,
+                     &c->padded_start, &c->scratch, &c->scratch_feat, &c->dscal, &c->o_color, &c->o_depth, &c->o_alpha, &c->o_index,
                      &c->o_weight, &c->o_count, &c->o_contrib, &c->aux_t, &c->aux_n, &c->x_index, &c->x_weight,
                      &c->x_count, &c->f_out, &c->f_grad_in, &c->f_grad_out, &c->s_keys, &c->s_vals,
                      &c->s_keys_alt, &c->s_vals_alt, &c->s_wnorm, &c->s_seg, &c->g_color_in, &c->g_depth_in,
@@ -674,6 +729,10 @@ tk_status tk_destroy(tk_ctx* c) {
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     if (c->hscal) cudaFreeHost(c->hscal);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->s_feat && c->s_feat != c->stream) cudaStreamDestroy(c->s_feat);
+    if (c->s_geo && c->s_geo != c->stream) cudaStreamDestroy(c->s_geo);
+    for (cudaEvent_t e : {c->ev_main, c->ev_feat, c->ev_geo})
+        if (e) cudaEventDestroy(e);
     delete c;
     return TK_OK;
 }
@@ -681,7 +740,17 @@ tk_status tk_destroy(tk_ctx* c) {
 tk_status tk_synchronize(tk_ctx* c) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));
-        sync(c);
+        CK(cudaStreamSynchronize(c->s_feat));
+        CK(cudaStreamSynchronize(c->s_geo));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+tk_status tk_join(tk_ctx* c) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        main_done(c);
     });
 }
 
@@ -703,7 +772,8 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
         if (s->n < 0 || s->d < 0) fail(TK_ERR_BAD_ARG, "negative scene size");
         if (s->n > INT32_MAX - 1) fail(TK_ERR_BAD_ARG, "scene larger than 2^31-1 Gaussians");
         CK(cudaSetDevice(c->device));
-        cudaStream_t st = c->stream;
+        on_main(c);
+        cudaStream_t st = c->cur;
         const int64_t n = s->n;
         if (!s->feature && c->has_features && (n != c->n || s->d != c->d))
             fail(TK_ERR_BAD_ARG, "feature == NULL requires unchanged n and d");
@@ -724,6 +794,7 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
         c->has_scene = true;
         c->prepared = false;
         c->aux_valid = false;
+        main_done(c);
     });
 }
 
@@ -756,11 +827,13 @@ tk_status tk_prepare_scene(tk_ctx* c, const tk_pose* pose, const tk_camera* cam,
     return guarded([&] {
         check_frame(cam, s);
         CK(cudaSetDevice(c->device));
+        on_main(c);
         prepare(c, pose, cam, s);
         if (n_entries) *n_entries = c->n_vis;
         if (n_tile_entries) *n_tile_entries = c->n_pairs;
         if (tiles_x) *tiles_x = c->tiles_x;
         if (tiles_y) *tiles_y = c->tiles_y;
+        main_done(c);
     });
 }
 
@@ -769,7 +842,8 @@ tk_status tk_prepared_export(tk_ctx* c, double* entries7, int32_t* src, int32_t*
     return guarded([&] {
         if (!c->prepared) fail(TK_ERR_STATE, "no prepared scene");
         CK(cudaSetDevice(c->device));
-        cudaStream_t st = c->stream;
+        on_main(c);
+        cudaStream_t st = c->cur;
         const int64_t nv = c->n_vis;
         DevBuf e7, s7;
         double* de = ensure<double>(e7, nv * 7);
@@ -786,6 +860,7 @@ tk_status tk_prepared_export(tk_ctx* c, double* entries7, int32_t* src, int32_t*
         sync(c);
         e7.release();
         s7.release();
+        main_done(c);
     });
 }
 
@@ -794,6 +869,7 @@ tk_status tk_render_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* c
     return guarded([&] {
         check_frame(cam, s);
         CK(cudaSetDevice(c->device));
+        on_main(c);
         prepare(c, pose, cam, s);
         forward(c, cam, s, true);
         c->aux_valid = true;
@@ -801,7 +877,7 @@ tk_status tk_render_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* c
         if (out) {
             const int64_t P = static_cast<int64_t>(cam->width) * cam->height;
             const int64_t k = c->rec_k;
-            cudaStream_t st = c->stream;
+            cudaStream_t st = c->cur;
             copy_out(out->color, c->o_color.p, P * 3 * sizeof(double), out->mem, c);
             copy_out(out->depth, c->o_depth.p, P * sizeof(double), out->mem, c);
             copy_out(out->alpha, c->o_alpha.p, P * sizeof(double), out->mem, c);
@@ -813,12 +889,14 @@ tk_status tk_render_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* c
             out->map_size = c->n;
             if (out->mem == TK_HOST) sync(c);
         }
+        main_done(c);
     });
 }
 
 tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int32_t out_mem) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));
+        on_side(c, true);
         require_features(c);
         const Records r = resolve_records(c, topk, "render_feature");
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
@@ -827,7 +905,7 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
         tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, dst};
         {
             PhaseScope phase(c, TK_PHASE_GATHER);
-            tk::launch_feature_gather(gp, c->stream);
+            tk::launch_feature_gather(gp, c->cur);
         }
         c->launches += P > 0;
         CK_LAUNCH(c);
@@ -836,6 +914,7 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
             copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
             sync(c);
         }
+        side_done(c, true);
     });
 }
 
@@ -843,10 +922,11 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
                               int32_t out_mem) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));
+        on_side(c, true);
         require_features(c);
         const Records r = resolve_records(c, topk, "backward_feature");
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
-        cudaStream_t st = c->stream;
+        cudaStream_t st = c->cur;
         const int64_t P = static_cast<int64_t>(r.w) * r.h;
         const int64_t slots = P * r.k;
         const int64_t n = c->n;
@@ -859,26 +939,19 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
             copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
             g = dg;
         }
-        // inverted index: records sorted by (Gaussian, slot)
-        uint32_t* keys = ensure<uint32_t>(c->s_keys, slots);
-        uint32_t* vals = ensure<uint32_t>(c->s_vals, slots);
-        uint32_t* keys_alt = ensure<uint32_t>(c->s_keys_alt, slots);
-        uint32_t* vals_alt = ensure<uint32_t>(c->s_vals_alt, slots);
+        // inverted index (Gaussian -> slots, ascending within each Gaussian) by counting
+        uint32_t* recs = ensure<uint32_t>(c->s_keys, slots);
+        uint32_t* svals = ensure<uint32_t>(c->s_vals, slots);
+        int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 1);
         float* wn = ensure<float>(c->s_wnorm, slots);
         int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
-        ensure_scratch(c, std::max<int64_t>(slots, n + 1));
-        bool alt = false;
+        ensure_scratch(c, std::max<int64_t>(slots, n + 1), true);
         {
             PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
-            tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, keys, vals, wn};
-            tk::launch_slot_keys(sk, st);
-            c->launches += slots > 0;
-            if (slots > 1)
-                tk::radix_sort_pairs_u32(keys, vals, keys_alt, vals_alt, slots, 0,
-                                         bits_for(static_cast<uint64_t>(n)), c->scratch.p, st, &alt, &c->launches);
-            tk::segment_offsets_u32(alt ? keys_alt : keys, slots, seg, n, st, &c->launches);
+            tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
+            int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+            tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, st, &c->launches);
         }
-        const uint32_t* svals = alt ? vals_alt : vals;
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_grad_out, n * std::max(c->d, 1));
         tk::FeatBwdParams fp{n, r.k, c->d, seg, svals, wn, g, dst};
         {
@@ -891,6 +964,7 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
             copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), TK_HOST, c);
             sync(c);
         }
+        side_done(c, true);
     });
 }
 
@@ -899,9 +973,10 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
     return guarded([&] {
         check_frame(cam, s);
         CK(cudaSetDevice(c->device));
+        on_main(c);
         require_features(c);
         prepare(c, pose, cam, s);
-        cudaStream_t st = c->stream;
+        cudaStream_t st = c->cur;
         const tk::Frame f = make_frame(c, cam, s);
         const int64_t P = static_cast<int64_t>(f.width) * f.height;
         tk::GeomFwdParams gp{};
@@ -934,6 +1009,7 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
             copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
             sync(c);
         }
+        main_done(c);
     });
 }
 
@@ -944,14 +1020,19 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         check_frame(cam, s);
         if (!grad_color) fail(TK_ERR_BAD_ARG, "null grad_color");
         CK(cudaSetDevice(c->device));
-        prepare(c, pose, cam, s);  // backward.cpp:75 (cached when the forward used the same inputs)
-        const FwdKey fk = make_fwd_key(c->prep_key, s);
-        if (!(c->aux_valid && c->aux_key == fk)) {
+        // backward.cpp:75 recomputes prepare_scene; it is reused when the forward of this context
+        // ran on the same inputs, and only then does the call stay off the main stream.
+        const FwdKey fk = make_fwd_key(make_prep_key(c, pose, cam, s), s);
+        if (!(c->prepared && c->aux_valid && c->aux_key == fk)) {
+            on_main(c);
+            prepare(c, pose, cam, s);
             forward(c, cam, s, false);
             c->aux_valid = true;
             c->aux_key = fk;
+            main_done(c);
         }
-        cudaStream_t st = c->stream;
+        on_side(c, false);  // the sweep overlaps the feature path (s_feat)
+        cudaStream_t st = c->cur;
         const tk::Frame f = make_frame(c, cam, s);
         const int64_t P = static_cast<int64_t>(f.width) * f.height;
         const int64_t n = c->n;
@@ -1026,6 +1107,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
             copy_out(out->pose_twist, tout, 6 * sizeof(double), TK_HOST, c);
             sync(c);
         }
+        side_done(c, false);
     });
 }
 
@@ -1084,7 +1166,8 @@ tk_status tk_allgather_feature(tk_ctx* c, float* out, int32_t out_mem) {
         if (!c->comm) fail(TK_ERR_STATE, "tk_comm_init not called");
         if (c->d * c->nranks != c->d_total) fail(TK_ERR_BAD_ARG, "d_total must equal nranks * d_shard");
         CK(cudaSetDevice(c->device));
-        cudaStream_t st = c->stream;
+        on_side(c, true);
+        cudaStream_t st = c->cur;
         const int64_t P = c->fout_pixels;
         const size_t slice = static_cast<size_t>(P) * c->d;
         float* gath = ensure<float>(c->gather_buf, slice * c->nranks);
@@ -1098,6 +1181,7 @@ tk_status tk_allgather_feature(tk_ctx* c, float* out, int32_t out_mem) {
         if (out && out_mem == TK_HOST) copy_out(out, dst, slice * c->nranks * sizeof(float), TK_HOST, c);
         sync(c);
         tmp.release();
+        side_done(c, true);
     });
 }
 
@@ -1105,13 +1189,15 @@ tk_status tk_allreduce_sum_f64(tk_ctx* c, double* values, int32_t count) {
     return guarded([&] {
         if (!c->comm) fail(TK_ERR_STATE, "tk_comm_init not called");
         CK(cudaSetDevice(c->device));
+        on_main(c);
         DevBuf tmp;
         double* d = ensure<double>(tmp, count);
         copy_in(d, values, count * sizeof(double), TK_HOST, c);
-        NK(g_nccl.AllReduce(d, d, count, ncclFloat64, ncclSum, c->comm, c->stream));
+        NK(g_nccl.AllReduce(d, d, count, ncclFloat64, ncclSum, c->comm, c->cur));
         copy_out(values, d, count * sizeof(double), TK_HOST, c);
         sync(c);
         tmp.release();
+        main_done(c);
     });
 }
 
