@@ -184,17 +184,19 @@ __global__ void k_materialize(MaterializeParams p) {
     const uint32_t s = p.tile_vals[j];
     const int64_t dst = static_cast<int64_t>(p.padded_start[t]) + (j - p.tile_offsets[t]);
     const uint32_t i = p.order[s];
-    p.out.mx[dst] = p.mx[i];
-    p.out.my[dst] = p.my[i];
-    p.out.ixx[dst] = p.ixx[i];
-    p.out.ixy[dst] = p.ixy[i];
-    p.out.iyy[dst] = p.iyy[i];
-    p.out.z[dst] = p.z[i];
-    p.out.opacity[dst] = p.opacity[i];
-    p.out.cr[dst] = p.color[i * 3 + 0];
-    p.out.cg[dst] = p.color[i * 3 + 1];
-    p.out.cb[dst] = p.color[i * 3 + 2];
-    p.out.src[dst] = static_cast<int32_t>(i);
+    EntryChunk& ch = p.out.chunks[dst / kChunk];
+    const int l = static_cast<int>(dst % kChunk);
+    ch.f[0][l] = p.mx[i];
+    ch.f[1][l] = p.my[i];
+    ch.f[2][l] = p.ixx[i];
+    ch.f[3][l] = p.ixy[i];
+    ch.f[4][l] = p.iyy[i];
+    ch.f[5][l] = p.z[i];
+    ch.f[6][l] = p.opacity[i];
+    ch.f[7][l] = p.color[i * 3 + 0];
+    ch.f[8][l] = p.color[i * 3 + 1];
+    ch.f[9][l] = p.color[i * 3 + 2];
+    ch.src[l] = static_cast<int32_t>(i);
     // Bounding box of {d : -0.5 d^T A d >= cutoff}, A = (ixx, ixy; ixy, iyy): |d_x| <= sqrt(R Sxx)
     // with R = -2 cutoff and S = A^-1.  Inflated (1e-6 relative + 1e-3 px) so that rounding can
     // never cull an entry that contributes to a pixel of the block (culling only skips work).
@@ -202,8 +204,8 @@ __global__ void k_materialize(MaterializeParams p) {
     const double det = ixx * iyy - ixy * ixy;
     const double r2 = -2.0 * kLogWeightCutoff;
     const double hx = sqrt(r2 * (iyy / det)), hy = sqrt(r2 * (ixx / det));
-    p.out.hx[dst] = det > 0.0 ? static_cast<float>(hx * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
-    p.out.hy[dst] = det > 0.0 ? static_cast<float>(hy * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
+    ch.hx[l] = det > 0.0 ? static_cast<float>(hx * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
+    ch.hy[l] = det > 0.0 ? static_cast<float>(hy * (1.0 + 1e-6) + 1e-3) : 3.0e38f;
 }
 
 __global__ void k_export_entries(const uint32_t* __restrict__ order, int64_t nv, const double* __restrict__ mx,

@@ -358,19 +358,7 @@ FwdKey make_fwd_key(const PrepKey& pk, const tk_settings* s) {
 
 tk::TileEntries tile_entries(tk_ctx* c) {
     tk::TileEntries t;
-    t.mx = ptr<double>(c->te[0]);
-    t.my = ptr<double>(c->te[1]);
-    t.ixx = ptr<double>(c->te[2]);
-    t.ixy = ptr<double>(c->te[3]);
-    t.iyy = ptr<double>(c->te[4]);
-    t.z = ptr<double>(c->te[5]);
-    t.opacity = ptr<double>(c->te[6]);
-    t.cr = ptr<double>(c->te[7]);
-    t.cg = ptr<double>(c->te[8]);
-    t.cb = ptr<double>(c->te[9]);
-    t.src = ptr<int32_t>(c->te[10]);
-    t.hx = ptr<float>(c->te[11]);
-    t.hy = ptr<float>(c->te[12]);
+    t.chunks = ptr<tk::EntryChunk>(c->te[0]);
     return t;
 }
 
@@ -503,10 +491,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     c->launches += 1;
     tk::scan_exclusive(pcnt, pstart, n_tiles + 1, dscal + 4, c->scratch.p, st, &c->launches);
     const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
-    for (int i = 0; i < 10; ++i) ensure<double>(c->te[i], padded_cap);
-    ensure<int32_t>(c->te[10], padded_cap);
-    ensure<float>(c->te[11], padded_cap);
-    ensure<float>(c->te[12], padded_cap);
+    ensure<tk::EntryChunk>(c->te[0], padded_cap / tk::kChunk + 1);
     ensure<int32_t>(c->wl, padded_cap * tk::geom_blocks_per_tile(s->tile_size));
     tk::MaterializeParams mp{};
     mp.n_pairs = n_pairs;
