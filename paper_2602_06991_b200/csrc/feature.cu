@@ -21,6 +21,81 @@ __device__ __forceinline__ float4 fma4(float a, float4 x, float4 acc) {
 
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
+// Pixel of virtual index v when the image is walked in 16x16 tiles (neighbouring pixels share
+// most of their Top-K Gaussians, so tile order keeps those feature rows L2-resident).
+__device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height, int tiles_x, bool* valid) {
+    const int64_t t = v >> 8;
+    const int l = static_cast<int>(v & 255);
+    const int x = static_cast<int>(t % tiles_x) * 16 + (l & 15), y = static_cast<int>(t / tiles_x) * 16 + (l >> 4);
+    *valid = x < width && y < height;
+    return static_cast<int64_t>(y) * width + x;
+}
+
+// render_feature (render.cpp:319-334) for D % 4 == 0: one warp per pixel, two pixels in flight
+// per warp (all 2*K*D/128 row loads issued before the FMAs), pixels visited in tile order,
+// 128-bit read-only loads of the selected rows and 128-bit streaming stores of the output row.
+__global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2;
+    const int tiles_x = (p.width + 15) / 16, tiles_y = (p.height + 15) / 16;
+    const int64_t nv = static_cast<int64_t>(tiles_x) * tiles_y * 256;
+    for (int64_t v0 = ((static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5) * 2; v0 < nv; v0 += nw * 2) {
+        int64_t px[2];
+        int c[2], id[2];
+        float wn[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            bool valid;
+            px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &valid);
+            c[u] = valid ? p.count[px[u]] : 0;
+            double wd = 0.0;
+            id[u] = 0;
+            if (lane < c[u]) {
+                id[u] = p.index[px[u] * p.k + lane];
+                wd = p.weight[px[u] * p.k + lane];
+            }
+            double sum = 0.0;
+            for (int j = 0; j < c[u]; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
+            wn[u] = lane < c[u] ? static_cast<float>(wd / sum) : 0.0f;
+            c[u] = valid ? c[u] : -1;  // -1: outside the image, nothing to write
+        }
+        const int cmax = max(c[0], c[1]);
+        for (int base = 0; base < d4; base += 128) {
+            float4 acc[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) acc[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < cmax; ++j) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int g = __shfl_sync(0xffffffffu, id[u], j);
+                    const float wj = __shfl_sync(0xffffffffu, wn[u], j);
+                    if (j < c[u]) {
+                        const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(g) * D);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < d4) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (c[u] < 0) continue;
+                float4* orow = reinterpret_cast<float4*>(p.out + px[u] * D);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    if (q < d4) __stcs(orow + q, acc[u][m]);
+                }
+            }
+        }
+    }
+}
+
 // render_feature (render.cpp:319-334): F[p] = sum_j (w_j / sum_w) f[idx_j], sum in slot order.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_gather(GatherParams p) {
@@ -321,7 +396,9 @@ inline bool vec_ok(const void* a, const void* b, int d) {
 
 void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
-    if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    if (vec_ok(p.feat, p.out, p.d) && p.width > 0 && static_cast<int64_t>(p.width) * p.height == p.n_pixels)
+        k_gather_tiled<<<warp_grid((p.n_pixels + 1) / 2), kThreads, 0, st>>>(p);
+    else if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
     else k_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
     dbg_launch("k_gather", st);
 }

@@ -13,6 +13,7 @@ struct GatherParams {
     const float* feat;     // N x D
     int d;
     float* out;            // P x D
+    int width, height;     // image shape (0: plain pixel order)
 };
 
 struct ListGatherParams {

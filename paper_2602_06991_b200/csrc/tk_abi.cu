@@ -887,7 +887,7 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
         const int64_t P = static_cast<int64_t>(r.w) * r.h;
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_out, P * std::max(c->d, 1));
-        tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, dst};
+        tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, dst, r.w, r.h};
         {
             PhaseScope phase(c, TK_PHASE_GATHER);
             tk::launch_feature_gather(gp, c->cur);
