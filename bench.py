@@ -251,12 +251,11 @@ def main_gpu(args, cfg):
     N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
 
     if world > 1:
+        from paper_2602_06991_b200 import dist as tkdist
         uid = (C.c_uint8 * 128)()
         if rank == 0:
             N.check(lib.tk_comm_unique_id(uid))
-        t = torch.tensor(list(uid), dtype=torch.uint8)
-        dist.broadcast(t, 0)
-        uid = (C.c_uint8 * 128)(*t.tolist())
+        uid = (C.c_uint8 * 128)(*tkdist.broadcast_bytes(dist, bytes(uid) if rank == 0 else None, 128))
         N.check(lib.tk_comm_init(ctx, uid, world, rank, D))
 
     dev = torch.device("cuda", local)

@@ -1,0 +1,362 @@
+// fslam_raster.hpp — C++ mirror of the reference renderer API over the C ABI (tk_render.h).
+//
+// Drop-in for proj/include/fslam/raster/render.hpp + backward.hpp: the same type names, field
+// names, defaults and function signatures (Eigen replaced by small POD vectors), the same
+// pure-function semantics (every call sees the map as passed) and the same error behaviour (a
+// stale Top-K record throws std::runtime_error with the reference's message).  All work runs in
+// libtkrender.so on the GPU; there is no CPU fallback.
+//
+// Reference interface -> this header
+//   render.hpp:14-21   RenderSettings            render.hpp:27-44  TopKGrid
+//   render.hpp:46-55   RenderOutput              render.hpp:60-71  render_geometric /
+//   render.hpp:84-92   raster_detail::PreparedScene                 render_feature /
+//   backward.hpp:15-22 GeomGrads                                    render_feature_full_blend
+//   backward.hpp:27-34 backward_geometric / backward_feature
+//   core/types.hpp     CameraIntrinsics, Gaussian3D   core/image.hpp Image<T>   core/pose.hpp Pose
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tk_render.h"
+
+namespace tk {
+namespace fslam {
+
+struct Vec3 {
+    double x = 0, y = 0, z = 0;
+};
+struct Quat {  // (w, x, y, z)
+    double w = 1, x = 0, y = 0, z = 0;
+};
+
+inline double logistic(double x) { return 1.0 / (1.0 + std::exp(-x)); }  // types.hpp:12
+inline double logit(double p) { return std::log(p / (1.0 - p)); }
+
+struct CameraIntrinsics {  // types.hpp:15-21
+    double fx = 0, fy = 0;
+    double cx = 0, cy = 0;
+    int width = 0, height = 0;
+    double near_plane = 0.05;
+    double far_plane = 100.0;
+};
+
+struct Pose {  // pose.hpp:11-19 (world-to-camera)
+    Quat rotation;
+    Vec3 translation;
+    static Pose identity() { return {}; }
+};
+
+struct Gaussian3D {  // types.hpp:25-44
+    Vec3 mean;
+    Vec3 log_scale;
+    Quat rotation;
+    double opacity_logit = 0.0;
+    Vec3 color;
+    std::vector<double> feature;  // unit L2 norm
+    int topk_count = 0;
+    double max_contribution = 0.0;
+    double opacity() const { return logistic(opacity_logit); }
+};
+
+struct SceneMap {  // scene_map.hpp:16-27
+    std::vector<Gaussian3D> gaussians;
+    std::uint64_t generation = 0;
+    int feature_dim = 0;
+    std::size_t size() const { return gaussians.size(); }
+    bool empty() const { return gaussians.empty(); }
+};
+
+template <typename T>
+struct Image {  // image.hpp:10-34, H x W x C, channel fastest
+    int width = 0, height = 0, channels = 1;
+    std::vector<T> data;
+    Image() = default;
+    Image(int w, int h, int c, T fill = T{})
+        : width(w), height(h), channels(c), data(static_cast<std::size_t>(w) * h * c, fill) {}
+    bool empty() const { return data.empty(); }
+    std::size_t pixel_count() const { return static_cast<std::size_t>(width) * height; }
+    std::size_t offset(int x, int y, int c = 0) const {
+        return (static_cast<std::size_t>(y) * width + x) * channels + c;
+    }
+    T& at(int x, int y, int c = 0) { return data[offset(x, y, c)]; }
+    const T& at(int x, int y, int c = 0) const { return data[offset(x, y, c)]; }
+};
+using ImageD = Image<double>;
+using ImageF = Image<float>;
+
+struct RenderSettings {  // render.hpp:14-21
+    int top_k = 3;
+    double transmittance_floor = 1e-4;
+    Vec3 background;
+    int tile_size = 16;
+    double cov2d_dilation = 0.3;
+    double alpha_clamp = 0.999;
+};
+
+inline constexpr int kMaxTopK = 32;  // render.hpp:23
+
+struct TopKGrid {  // render.hpp:27-44
+    int width = 0, height = 0, k = 0;
+    std::vector<std::int32_t> index;
+    std::vector<double> weight;
+    std::vector<std::uint8_t> count;
+    TopKGrid() = default;
+    TopKGrid(int w, int h, int kk)
+        : width(w), height(h), k(kk), index(static_cast<std::size_t>(w) * h * kk, -1),
+          weight(static_cast<std::size_t>(w) * h * kk, 0.0), count(static_cast<std::size_t>(w) * h, 0) {}
+    std::size_t slot(int x, int y, int j) const { return (static_cast<std::size_t>(y) * width + x) * k + j; }
+    std::size_t pixel(int x, int y) const { return static_cast<std::size_t>(y) * width + x; }
+};
+
+struct RenderOutput {  // render.hpp:46-55
+    ImageD color, depth, alpha, feature;
+    TopKGrid topk;
+    std::vector<double> contributions;
+    std::uint64_t generation = 0;
+    std::size_t map_size = 0;
+};
+
+struct GeomGrads {  // backward.hpp:15-22; rotation gradient order (w, x, y, z)
+    std::vector<Vec3> mean, log_scale;
+    std::vector<Quat> rotation;
+    std::vector<double> opacity_logit;
+    std::vector<Vec3> color;
+    double pose_twist[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace raster_detail {
+struct ProjEntry {  // render.hpp:75-81
+    double mx, my, ixx, ixy, iyy, z, opacity;
+    std::int32_t src;
+};
+struct PreparedScene {  // render.hpp:84-92
+    std::vector<ProjEntry> entries;
+    std::vector<std::int32_t> tile_offsets;
+    std::vector<std::int32_t> tile_entries;
+    int tiles_x = 0, tiles_y = 0, width = 0, height = 0;
+    std::uint64_t generation = 0;
+    std::size_t map_size = 0;
+};
+inline constexpr double kLogWeightCutoff = -27.631021115928547;  // render.hpp:97
+}  // namespace raster_detail
+
+namespace detail {
+inline void check(tk_status s) {
+    if (s != TK_OK) throw std::runtime_error(tk_last_error());
+}
+inline tk_pose to_c(const Pose& p) {
+    return {p.rotation.w, p.rotation.x, p.rotation.y, p.rotation.z,
+            p.translation.x, p.translation.y, p.translation.z};
+}
+inline tk_camera to_c(const CameraIntrinsics& c) {
+    return {c.fx, c.fy, c.cx, c.cy, c.width, c.height, c.near_plane, c.far_plane};
+}
+inline tk_settings to_c(const RenderSettings& s) {
+    tk_settings o;
+    o.top_k = s.top_k;
+    o.tile_size = s.tile_size;
+    o.transmittance_floor = s.transmittance_floor;
+    o.background[0] = s.background.x;
+    o.background[1] = s.background.y;
+    o.background[2] = s.background.z;
+    o.cov2d_dilation = s.cov2d_dilation;
+    o.alpha_clamp = s.alpha_clamp;
+    return o;
+}
+}  // namespace detail
+
+// One device context.  Every entry point uploads the map it is given (the reference takes the
+// map by const reference on every call, so in-place edits between calls are always seen).
+class Renderer {
+public:
+    explicit Renderer(int device = 0) { detail::check(tk_create(device, &ctx_)); }
+    ~Renderer() { tk_destroy(ctx_); }
+    Renderer(const Renderer&) = delete;
+    Renderer& operator=(const Renderer&) = delete;
+    tk_ctx* context() const { return ctx_; }
+
+    void upload(const SceneMap& m) {
+        const std::size_t n = m.size();
+        const int d = m.feature_dim;
+        mean_.resize(n * 3);
+        ls_.resize(n * 3);
+        rot_.resize(n * 4);
+        op_.resize(n);
+        col_.resize(n * 3);
+        feat_.assign(n * static_cast<std::size_t>(d), 0.0f);
+        for (std::size_t i = 0; i < n; ++i) {
+            const Gaussian3D& g = m.gaussians[i];
+            const double mv[3] = {g.mean.x, g.mean.y, g.mean.z}, lv[3] = {g.log_scale.x, g.log_scale.y, g.log_scale.z};
+            const double cv[3] = {g.color.x, g.color.y, g.color.z};
+            for (int a = 0; a < 3; ++a) {
+                mean_[i * 3 + a] = mv[a];
+                ls_[i * 3 + a] = lv[a];
+                col_[i * 3 + a] = cv[a];
+            }
+            rot_[i * 4 + 0] = g.rotation.w;
+            rot_[i * 4 + 1] = g.rotation.x;
+            rot_[i * 4 + 2] = g.rotation.y;
+            rot_[i * 4 + 3] = g.rotation.z;
+            op_[i] = g.opacity_logit;
+            for (int c = 0; c < d && c < static_cast<int>(g.feature.size()); ++c)
+                feat_[i * d + c] = static_cast<float>(g.feature[c]);
+        }
+        tk_scene_view v{static_cast<int64_t>(n), d, mean_.data(), ls_.data(), rot_.data(), op_.data(), col_.data(),
+                        feat_.data(), m.generation};
+        detail::check(tk_scene_upload(ctx_, &v, TK_HOST));
+    }
+
+    raster_detail::PreparedScene prepare_scene(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
+                                               const RenderSettings& s) {
+        upload(m);
+        const tk_pose p = detail::to_c(pose);
+        const tk_camera c = detail::to_c(cam);
+        const tk_settings st = detail::to_c(s);
+        int64_t ne = 0, nt = 0;
+        int32_t tx = 0, ty = 0;
+        detail::check(tk_prepare_scene(ctx_, &p, &c, &st, &ne, &nt, &tx, &ty));
+        std::vector<double> e7(static_cast<std::size_t>(ne) * 7);
+        std::vector<int32_t> src(static_cast<std::size_t>(ne));
+        raster_detail::PreparedScene out;
+        out.tile_offsets.resize(static_cast<std::size_t>(tx) * ty + 1);
+        out.tile_entries.resize(static_cast<std::size_t>(nt));
+        detail::check(tk_prepared_export(ctx_, e7.data(), src.data(), out.tile_offsets.data(), out.tile_entries.data()));
+        out.entries.resize(static_cast<std::size_t>(ne));
+        for (int64_t q = 0; q < ne; ++q)
+            out.entries[q] = {e7[q * 7 + 0], e7[q * 7 + 1], e7[q * 7 + 2], e7[q * 7 + 3],
+                              e7[q * 7 + 4], e7[q * 7 + 5], e7[q * 7 + 6], src[q]};
+        out.tiles_x = tx;
+        out.tiles_y = ty;
+        out.width = cam.width;
+        out.height = cam.height;
+        out.generation = m.generation;
+        out.map_size = m.size();
+        return out;
+    }
+
+    RenderOutput render_geometric(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
+                                  const RenderSettings& s) {  // render.cpp:293-299
+        upload(m);
+        const int w = cam.width, h = cam.height, k = std::min(std::max(s.top_k, 0), kMaxTopK);
+        RenderOutput out;
+        out.color = ImageD(w, h, 3);
+        out.depth = ImageD(w, h, 1);
+        out.alpha = ImageD(w, h, 1);
+        out.topk = TopKGrid(w, h, k);
+        out.contributions.assign(m.size(), 0.0);
+        tk_geom_out g{TK_HOST, out.color.data.data(), out.depth.data.data(), out.alpha.data.data(),
+                      out.topk.index.data(), out.topk.weight.data(), out.topk.count.data(),
+                      out.contributions.data(), 0, 0};
+        const tk_pose p = detail::to_c(pose);
+        const tk_camera c = detail::to_c(cam);
+        const tk_settings st = detail::to_c(s);
+        detail::check(tk_render_geometric(ctx_, &p, &c, &st, &g));
+        out.generation = g.generation;
+        out.map_size = static_cast<std::size_t>(g.map_size);
+        return out;
+    }
+
+    ImageD render_feature(const SceneMap& m, const TopKGrid& t) {  // render.cpp:301-337
+        upload(m);
+        std::vector<float> f(static_cast<std::size_t>(t.width) * t.height * m.feature_dim);
+        tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
+        detail::check(tk_render_feature(ctx_, &v, f.data(), TK_HOST));
+        ImageD out(t.width, t.height, m.feature_dim);
+        for (std::size_t i = 0; i < f.size(); ++i) out.data[i] = f[i];
+        return out;
+    }
+
+    ImageD render_feature_full_blend(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
+                                     const RenderSettings& s) {  // render.cpp:339-343
+        upload(m);
+        std::vector<float> f(static_cast<std::size_t>(cam.width) * cam.height * m.feature_dim);
+        const tk_pose p = detail::to_c(pose);
+        const tk_camera c = detail::to_c(cam);
+        const tk_settings st = detail::to_c(s);
+        detail::check(tk_render_feature_full_blend(ctx_, &p, &c, &st, f.data(), TK_HOST));
+        ImageD out(cam.width, cam.height, m.feature_dim);
+        for (std::size_t i = 0; i < f.size(); ++i) out.data[i] = f[i];
+        return out;
+    }
+
+    std::vector<double> backward_feature(const SceneMap& m, const TopKGrid& t,
+                                         const ImageD& grad_feature) {  // backward.cpp:273-321
+        upload(m);
+        std::vector<float> g(grad_feature.data.begin(), grad_feature.data.end());
+        std::vector<float> o(m.size() * static_cast<std::size_t>(m.feature_dim));
+        tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
+        detail::check(tk_backward_feature(ctx_, &v, g.data(), TK_HOST, o.data(), TK_HOST));
+        return std::vector<double>(o.begin(), o.end());
+    }
+
+    GeomGrads backward_geometric(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
+                                 const RenderSettings& s, const ImageD& grad_color,
+                                 const ImageD& grad_depth) {  // backward.cpp:72-271
+        upload(m);
+        const std::size_t n = m.size();
+        std::vector<double> gm(n * 3), gl(n * 3), gr(n * 4), go(n), gc(n * 3);
+        tk_geom_grads out{TK_HOST, gm.data(), gl.data(), gr.data(), go.data(), gc.data(), {0, 0, 0, 0, 0, 0}};
+        const tk_pose p = detail::to_c(pose);
+        const tk_camera c = detail::to_c(cam);
+        const tk_settings st = detail::to_c(s);
+        detail::check(tk_backward_geometric(ctx_, &p, &c, &st, grad_color.data.data(),
+                                            grad_depth.empty() ? nullptr : grad_depth.data.data(), TK_HOST, &out));
+        GeomGrads g;
+        g.mean.resize(n);
+        g.log_scale.resize(n);
+        g.rotation.resize(n);
+        g.opacity_logit = go;
+        g.color.resize(n);
+        for (std::size_t i = 0; i < n; ++i) {
+            g.mean[i] = {gm[i * 3], gm[i * 3 + 1], gm[i * 3 + 2]};
+            g.log_scale[i] = {gl[i * 3], gl[i * 3 + 1], gl[i * 3 + 2]};
+            g.rotation[i] = {gr[i * 4], gr[i * 4 + 1], gr[i * 4 + 2], gr[i * 4 + 3]};
+            g.color[i] = {gc[i * 3], gc[i * 3 + 1], gc[i * 3 + 2]};
+        }
+        for (int a = 0; a < 6; ++a) g.pose_twist[a] = out.pose_twist[a];
+        return g;
+    }
+
+private:
+    tk_ctx* ctx_ = nullptr;
+    std::vector<double> mean_, ls_, rot_, op_, col_;
+    std::vector<float> feat_;
+};
+
+// Free functions with the reference signatures, on a per-thread default context (device 0).
+inline Renderer& default_renderer() {
+    thread_local std::unique_ptr<Renderer> r;
+    if (!r) r = std::make_unique<Renderer>(0);
+    return *r;
+}
+inline RenderOutput render_geometric(const SceneMap& m, const Pose& p, const CameraIntrinsics& c,
+                                     const RenderSettings& s) {
+    return default_renderer().render_geometric(m, p, c, s);
+}
+inline ImageD render_feature(const SceneMap& m, const TopKGrid& t) { return default_renderer().render_feature(m, t); }
+inline ImageD render_feature_full_blend(const SceneMap& m, const Pose& p, const CameraIntrinsics& c,
+                                       const RenderSettings& s) {
+    return default_renderer().render_feature_full_blend(m, p, c, s);
+}
+inline std::vector<double> backward_feature(const SceneMap& m, const TopKGrid& t, const ImageD& g) {
+    return default_renderer().backward_feature(m, t, g);
+}
+inline GeomGrads backward_geometric(const SceneMap& m, const Pose& p, const CameraIntrinsics& c,
+                                    const RenderSettings& s, const ImageD& gc, const ImageD& gd) {
+    return default_renderer().backward_geometric(m, p, c, s, gc, gd);
+}
+namespace raster_detail {
+inline PreparedScene prepare_scene(const SceneMap& m, const Pose& p, const CameraIntrinsics& c,
+                                   const RenderSettings& s) {
+    return default_renderer().prepare_scene(m, p, c, s);
+}
+}  // namespace raster_detail
+
+}  // namespace fslam
+}  // namespace tk

@@ -269,3 +269,28 @@ def test_bench_recipe_scene_parity(R):
     p = R.prepare_scene(m, pose, cam, s)
     po = O.prepare_scene(m, pose, cam, s)
     assert (p.tile_entries == po["tile_entries"]).all() and (p.src == po["src"]).all()
+
+
+def test_nccl_single_rank_allgather_equals_render(R):
+    """tk_comm_* with one rank: the all-gather + interleave path returns the rendered map."""
+    import ctypes as C
+    from paper_2602_06991_b200 import _native as N
+    m, c = synth.random_scene(500, 16, 2), synth.test_camera(48, 32)
+    g = R.render_geometric(m, Pose(), c, RenderSettings())
+    f = R.render_feature(m, g.topk)
+    uid = (C.c_uint8 * 128)()
+    N.check(R.lib.tk_comm_unique_id(uid))
+    N.check(R.lib.tk_comm_init(R.ctx, uid, 1, 0, 16))
+    N.check(R.lib.tk_render_feature(R.ctx, None, None, N.TK_DEVICE))
+    full = np.zeros((32, 48, 16), np.float32)
+    N.check(R.lib.tk_allgather_feature(R.ctx, full.ctypes.data, N.TK_HOST))
+    assert (full == f).all()
+
+
+def test_backward_feature_bit_deterministic(R):
+    m, c = synth.random_scene(2000, 64, 12), synth.test_camera(96, 64)
+    g = R.render_geometric(m, Pose(), c, RenderSettings(top_k=4))
+    gf = synth.uniform_image((64, 96, 64), 3).astype(np.float32)
+    a = R.backward_feature(m, g.topk, gf)
+    b = R.backward_feature(m, g.topk, gf)
+    assert a.tobytes() == b.tobytes()

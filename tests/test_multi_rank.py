@@ -1,0 +1,82 @@
+"""Multi-rank host logic of the D-sharded path on CPU: world_size 2, gloo, 127.0.0.1.
+
+Each rank gathers its channel slice of the Top-K feature map (host statement of the gather), the
+slices are all-gathered over gloo and interleaved exactly as tk_allgather_feature does on the
+device, and the result must equal the unsharded gather bit for bit (channels never mix).  The
+unique-id broadcast and max-over-ranks timing helpers used by bench.py are exercised too.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2602_06991_b200 import dist as tkdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _records(P=48, N=40, K=3, seed=0):
+    rng = np.random.default_rng(seed)
+    count = rng.integers(0, K + 1, size=P).astype(np.uint8)
+    index = np.full(P * K, -1, np.int32)
+    weight = np.zeros(P * K)
+    for p in range(P):
+        c = int(count[p])
+        index[p * K:p * K + c] = rng.choice(N, size=c, replace=False)
+        weight[p * K:p * K + c] = np.sort(rng.uniform(0.01, 1.0, size=c))[::-1]
+    feat = rng.standard_normal((N, 12))
+    return feat, index, weight, count, K
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        feat, index, weight, count, K = _records()
+        mine = tkdist.shard_features(feat, world, rank)
+        part = tkdist.gather_reference(mine, index, weight, count, K)
+        parts = [torch.zeros_like(torch.from_numpy(part)) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(part))
+        full = tkdist.interleave([p.numpy() for p in parts])
+        ref = tkdist.gather_reference(feat, index, weight, count, K)
+        uid = tkdist.broadcast_bytes(dist, bytes(range(128)) if rank == 0 else None, 128)
+        tmax = tkdist.max_over_ranks(dist, 1.0 + rank)
+        q.put((rank, bool(np.array_equal(full, ref)), uid == bytes(range(128)), tmax))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_range():
+    assert tkdist.shard_range(512, 8, 3) == (192, 256)
+    assert tkdist.shard_range(768, 2, 1) == (384, 768)
+    with pytest.raises(ValueError):
+        tkdist.shard_range(10, 3, 0)
+
+
+def test_two_rank_feature_shard_allgather_matches_full_render():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, equal, uid_ok, tmax in res:
+        assert equal, f"rank {rank}: sharded gather != full gather"
+        assert uid_ok
+        assert tmax == 2.0
