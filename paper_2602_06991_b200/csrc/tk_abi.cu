@@ -666,8 +666,11 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         // blocks are scheduled as soon as the long fp64 geometry-backward grid frees SM slots.
         int prio_lo = 0, prio_hi = 0;
         cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-        const char* serial = std::getenv("TK_SERIAL");  // profiling aid: one stream, no overlap
-        if (serial && serial[0] == '1') {
+        // Side streams only with TK_OVERLAP=1: on B200 the fp64 geometry backward and the feature
+        // kernels each fill the SMs' register files, so overlapping them measured no gain; the
+        // default aliases every stream to the main one (per-kernel times stay unambiguous).
+        const char* overlap = std::getenv("TK_OVERLAP");
+        if (!(overlap && overlap[0] == '1')) {
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_feat, cudaStreamNonBlocking);
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_geo, cudaStreamNonBlocking);
             if (e == cudaSuccess) {  // alias the side streams to the main stream
