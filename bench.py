@@ -51,6 +51,22 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel_prefix: str):
+    """DRAM bytes (read + write) per launch of a kernel from the latest committed ncu --set full
+    capture (profiles/*_ncu_traffic.json, written by scripts/profile_summary.py), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")), key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            t = json.load(open(f))
+        except Exception:
+            continue
+        for k, v in t.items():
+            if k.startswith(kernel_prefix):
+                return {"bytes": v, "source": os.path.basename(f), "kernel": k}
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -228,13 +244,20 @@ def main_gpu(args, cfg):
 
     n, W, H, D, K = cfg["n"], cfg["w"], cfg["h"], cfg["d"], args.k or cfg["k"]
     P = W * H
-    if D % world:
+    # keyframe mode (default): rank r renders keyframe r of the config-4 orbit batch with all D
+    # channels -- independent views, no data-path collective (weak scaling).  dshard mode: every
+    # rank renders the same view for its D/G channel slice and NCCL all-gathers the map.
+    dshard = world > 1 and args.mode == "dshard"
+    shards = world if dshard else 1
+    if D % shards:
         raise SystemExit("D must divide by the number of GPUs")
-    Ds = D // world
-    c0 = rank * Ds
+    Ds = D // shards
+    c0 = (rank * Ds) if dshard else 0
 
     t0 = time.time()
-    scene, cam, pose, _ = synth.bench_scene(n, W, H, D)
+    scene, cam, pose, spec = synth.bench_scene(n, W, H, D)
+    if not dshard:
+        pose = synth.generate_trajectory("orbit", 8, spec)[rank % 8]
     feat_full = synth.unit_features(scene.size(), D, 7)
     feat = np.ascontiguousarray(feat_full[:, c0:c0 + Ds])
     del feat_full
@@ -250,7 +273,7 @@ def main_gpu(args, cfg):
     view = N.tk_scene_view(n, Ds, *(a.ctypes.data for a in geo), feat.ctypes.data, scene.generation)
     N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
 
-    if world > 1:
+    if dshard:
         from paper_2602_06991_b200 import dist as tkdist
         uid = (C.c_uint8 * 128)()
         if rank == 0:
@@ -266,7 +289,7 @@ def main_gpu(args, cfg):
     gF = torch.from_numpy(gF_host).to(dev)
     gC = torch.from_numpy(gC_host).to(dev)
     gD = torch.from_numpy(gD_host).to(dev)
-    Ffull = torch.empty(P * D, dtype=torch.float32, device=dev) if world > 1 else None
+    Ffull = torch.empty(P * D, dtype=torch.float32, device=dev) if dshard else None
     grads = N.tk_geom_grads()
     grads.mem = N.TK_DEVICE
     setup_s = time.time() - t0
@@ -275,7 +298,7 @@ def main_gpu(args, cfg):
         N.check(lib.tk_invalidate(ctx))
         N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
         N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))
-        if world > 1:
+        if dshard:
             N.check(lib.tk_allgather_feature(ctx, C.c_void_p(Ffull.data_ptr()), N.TK_DEVICE))
         N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), N.TK_DEVICE, None, N.TK_DEVICE))
         N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
@@ -347,7 +370,8 @@ def main_gpu(args, cfg):
     achieved = b_dom / (t_dom / 1000.0) / 1e9 if t_dom > 0 else 0.0
     roof = {"kernel": {"gather": "k_gather (render_feature)", "fbwd": "k_feat_bwd (backward_feature)"}[dom],
             "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
+            "frac": achieved / peak, "traffic": ncu_traffic({"gather": "k_gather", "fbwd": "k_feat_bwd"}[dom]),
+            "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
     feat_bytes = bytes_gather + bytes_fbwd
     feat_ms = ph_ms[2] / max(1, ph_cnt[2]) + (ph_ms[3] / max(1, ph_cnt[3])) + ph_ms[4] / max(1, ph_cnt[4])
     feature_path = {"algorithmic_bytes": feat_bytes, "ms": feat_ms,
@@ -375,10 +399,11 @@ def main_gpu(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
             "config": {"workload": cfg["label"], "gaussians": n, "width": W, "height": H, "feature_dim": D,
-                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": f"feature-dim shard d{world}",
+                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": (f"feature-dim shard d{world} + NCCL all-gather" if dshard else
+                                       f"keyframe-parallel x{world}: rank r renders orbit keyframe r, all D"),
                        "l2": "inputs larger than L2 (features %.2f GB, F %.2f GB)" % (n * D * 4 / 1e9,
                                                                                         P * D * 4 / 1e9),
                        "records": {"distinct_gaussians": U, "valid_slots": M}},
@@ -476,6 +501,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--mode", default="keyframe", choices=["keyframe", "dshard"],
+                    help="multi-GPU decomposition (N > 1)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])
