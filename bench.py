@@ -370,8 +370,11 @@ def main_gpu(args, cfg):
     achieved = b_dom / (t_dom / 1000.0) / 1e9 if t_dom > 0 else 0.0
     roof = {"kernel": {"gather": "k_gather (render_feature)", "fbwd": "k_feat_bwd (backward_feature)"}[dom],
             "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic({"gather": "k_gather", "fbwd": "k_feat_bwd"}[dom]),
-            "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
+            "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
+    tr = ncu_traffic({"gather": "k_gather", "fbwd": "k_feat_bwd"}[dom])
+    if tr:
+        roof["traffic"] = tr["bytes"]
+        roof["traffic_source"] = f"profiles/{tr['source']} ({tr['kernel']}, dram read+write per launch)"
     feat_bytes = bytes_gather + bytes_fbwd
     feat_ms = ph_ms[2] / max(1, ph_cnt[2]) + (ph_ms[3] / max(1, ph_cnt[3])) + ph_ms[4] / max(1, ph_cnt[4])
     feature_path = {"algorithmic_bytes": feat_bytes, "ms": feat_ms,

@@ -127,6 +127,51 @@ int orc_time_frame(const orc_map* m, const orc_pose* pose, const orc_camera* cam
 int orc_max_threads(void);
 void orc_set_threads(int n);
 
+/* ---- one mapping iteration (map/losses.cpp, core/ssim.cpp, map/optimizer.cpp, map/mapper.cpp) ----
+ * Same field layout as tk_mapper_config in include/tk_render.h.  Flattens MapperConfig's
+ * LossWeights (losses.hpp:9-21), GroupLearningRates / AdamParams (optimizer.hpp:9-23),
+ * Schedule::feature_update_period (mapper.hpp:16) and the log-scale clamps (mapper.hpp:31-32). */
+typedef struct {
+    double lambda_geo, lambda_feat, lambda1, lambda2;
+    int32_t color_secondary;        /* 0 = D-SSIM, 1 = duplicated L1 (ColorSecondaryTerm) */
+    int32_t feature_update_period;
+    double l1_deadband;
+    double lr_mean, lr_log_scale, lr_rotation, lr_opacity, lr_color, lr_feature;
+    double beta1, beta2, eps;
+    double min_log_scale, max_log_scale;
+} orc_mapper_config;
+
+typedef struct orc_opt orc_opt; /* OptimizerState (optimizer.hpp:25-53) */
+orc_opt* orc_opt_create(int64_t n, int32_t d);
+void orc_opt_free(orc_opt* o);
+
+/* ssim_with_grad (ssim.cpp:110-158); images h x w x c, channel fastest. */
+double orc_ssim_with_grad(int32_t w, int32_t h, int32_t c, const double* a, const double* b, double* grad);
+
+/* compute_losses (losses.cpp:22-133). values[3] = {map, geo, feat}; grad_feature may be NULL. */
+int orc_compute_losses(int32_t w, int32_t h, int32_t d, const double* color, const double* depth,
+                       const uint8_t* topk_count, const double* feature, const float* gt_color,
+                       const float* gt_depth, const float* gt_feature, const orc_mapper_config* cfg,
+                       int32_t include_feature, double* values, double* grad_color, double* grad_depth,
+                       double* grad_feature);
+
+/* optimize_step (mapper.cpp:162-255) on a caller-chosen keyframe, without the prune branch.
+ * Updates the map and optimizer state in place; values[3] as above. */
+int orc_optimize_step(orc_map* m, orc_opt* o, const orc_mapper_config* cfg, const orc_camera* cam,
+                      const orc_settings* s, const orc_pose* kf_pose, const float* gt_color,
+                      const float* gt_depth, const float* gt_feature, int64_t iteration, double* values,
+                      int32_t* feature_step);
+
+/* update_contribution_stats (mapper.cpp:62-78); 1 = generation / size mismatch (orc_last_error). */
+int orc_update_contribution_stats(orc_map* m, uint64_t generation, int64_t map_size, int32_t w, int32_t h,
+                                  int32_t k, const int32_t* index, const uint8_t* count,
+                                  const double* contributions);
+
+/* Map parameters and selection statistics back out in SoA form (any pointer may be NULL). */
+void orc_map_export(const orc_map* m, double* mean, double* log_scale, double* rotation,
+                    double* opacity_logit, double* color, double* feature, int32_t* topk_count,
+                    double* max_contribution);
+
 #ifdef __cplusplus
 }
 #endif

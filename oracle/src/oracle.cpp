@@ -49,6 +49,8 @@ struct Gaussian {                      // Gaussian3D, types.hpp:25-44
     double opacity_logit;
     double color[3];
     std::vector<double> feature;       // heap VectorXd per Gaussian (types.hpp:31)
+    int topk_count = 0;                // selection statistics (types.hpp:34-35)
+    double max_contribution = 0.0;
 };
 
 }  // namespace
@@ -1022,3 +1024,7 @@ int orc_time_frame(const orc_map* m, const orc_pose* pose, const orc_camera* cam
 }
 
 }  // extern "C"
+
+// Mapping iteration (losses, SSIM, Adam, optimize_step): map/losses.cpp, core/ssim.cpp,
+// map/optimizer.cpp, map/mapper.cpp.
+#include "oracle_mapping.inc"

@@ -122,3 +122,42 @@ class PreparedScene:  # raster/render.hpp:84-92 (entries as n x 7: mx,my,ixx,ixy
     height: int
     generation: int
     map_size: int
+
+
+@dataclass
+class Frame:  # map/scene_map.hpp Keyframe::frame: color H x W x 3, depth H x W, feature H x W x d (fp32)
+    color: np.ndarray
+    depth: np.ndarray
+    feature: np.ndarray | None = None
+
+
+@dataclass
+class MapperConfig:
+    """The mapping-iteration knobs of MapperConfig (map/mapper.hpp:23-35) flattened: LossWeights
+    (losses.hpp:9-21), GroupLearningRates and AdamParams (optimizer.hpp:9-23),
+    Schedule::feature_update_period (mapper.hpp:16) and the log-scale clamps (mapper.hpp:31-32)."""
+    lambda_geo: float = 1.0
+    lambda_feat: float = 1.0
+    lambda1: float = 0.2
+    lambda2: float = 1.0
+    color_secondary: int = 0  # 0 = D-SSIM (kDssim), 1 = duplicated L1 (kL1Duplicate)
+    feature_update_period: int = 5
+    l1_deadband: float = 0.0
+    lr_mean: float = 2e-3
+    lr_log_scale: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_opacity: float = 5e-2
+    lr_color: float = 2e-2
+    lr_feature: float = 1e-2
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    min_log_scale: float = -10.0
+    max_log_scale: float = 1.0
+
+
+@dataclass
+class LossValues:  # map/losses.hpp:23-27
+    map: float = 0.0
+    geo: float = 0.0
+    feat: float = 0.0

@@ -41,9 +41,10 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        src = os.path.join(ORACLE_DIR, "src", "oracle.cpp")
-        if not os.path.exists(ORACLE_LIB) or (os.path.exists(src) and
-                                              os.path.getmtime(src) > os.path.getmtime(ORACLE_LIB)):
+        srcs = [os.path.join(ORACLE_DIR, "src", f) for f in ("oracle.cpp", "oracle_mapping.inc")]
+        srcs.append(os.path.join(ORACLE_DIR, "include", "oracle.h"))
+        if not os.path.exists(ORACLE_LIB) or any(
+                os.path.exists(f) and os.path.getmtime(f) > os.path.getmtime(ORACLE_LIB) for f in srcs):
             build()
         L = C.CDLL(ORACLE_LIB)
         vp = C.c_void_p
@@ -67,6 +68,16 @@ def lib():
         L.orc_time_frame.argtypes = [vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp]
         L.orc_max_threads.restype = C.c_int
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_opt_create.restype = vp
+        L.orc_opt_create.argtypes = [C.c_int64, C.c_int32]
+        L.orc_opt_free.argtypes = [vp]
+        L.orc_ssim_with_grad.restype = C.c_double
+        L.orc_ssim_with_grad.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, vp]
+        L.orc_compute_losses.argtypes = [C.c_int32, C.c_int32, C.c_int32] + [vp] * 8 + [C.c_int32] + [vp] * 4
+        L.orc_optimize_step.argtypes = [vp] * 9 + [C.c_int64, vp, vp]
+        L.orc_map_export.argtypes = [vp] * 9
+        L.orc_update_contribution_stats.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                                    vp, vp, vp]
         _lib = L
     return _lib
 
@@ -219,3 +230,87 @@ def render_reference(m, pose, cam, s, with_features=False, keep_records=False):
         L.orc_render_reference(*args, *outs, None, None, None, C.byref(nrec))
     o["k"] = k
     return o
+
+
+class orc_mapper_config(C.Structure):
+    _fields_ = [("lambda_geo", C.c_double), ("lambda_feat", C.c_double), ("lambda1", C.c_double),
+                ("lambda2", C.c_double), ("color_secondary", C.c_int32), ("feature_update_period", C.c_int32),
+                ("l1_deadband", C.c_double), ("lr_mean", C.c_double), ("lr_log_scale", C.c_double),
+                ("lr_rotation", C.c_double), ("lr_opacity", C.c_double), ("lr_color", C.c_double),
+                ("lr_feature", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("min_log_scale", C.c_double), ("max_log_scale", C.c_double)]
+
+
+def mapper_config_c(cfg):
+    o = orc_mapper_config()
+    for name, _ in orc_mapper_config._fields_:
+        setattr(o, name, getattr(cfg, name))
+    return o
+
+
+def ssim_with_grad(a, b):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    h, w, c = a.shape
+    g = np.zeros_like(a)
+    return lib().orc_ssim_with_grad(w, h, c, _p(a), _p(b), _p(g)), g
+
+
+def compute_losses(color, depth, count, feature, gt_color, gt_depth, gt_feature, cfg, include_feature):
+    """compute_losses (losses.cpp:22-133) -> (values{map,geo,feat}, grad_color, grad_depth, grad_feature)."""
+    h, w = depth.shape
+    d = 0 if gt_feature is None else gt_feature.shape[-1]
+    vals = np.zeros(3)
+    gc, gd = np.zeros((h, w, 3)), np.zeros((h, w))
+    gf = np.zeros((h, w, d)) if include_feature else None
+    f = None if feature is None else np.ascontiguousarray(feature, np.float64)
+    gtf = None if gt_feature is None else np.ascontiguousarray(gt_feature, np.float32)
+    lib().orc_compute_losses(w, h, d, _p(np.ascontiguousarray(color, np.float64)),
+                             _p(np.ascontiguousarray(depth, np.float64)), _p(np.ascontiguousarray(count, np.uint8)),
+                             _p(f), _p(np.ascontiguousarray(gt_color, np.float32)),
+                             _p(np.ascontiguousarray(gt_depth, np.float32)), _p(gtf),
+                             C.byref(mapper_config_c(cfg)), int(include_feature), _p(vals), _p(gc), _p(gd), _p(gf))
+    return dict(map=vals[0], geo=vals[1], feat=vals[2]), gc, gd, gf
+
+
+class OracleMapper:
+    """SceneMap + OptimizerState driven through optimize_step (mapper.cpp:162-255, no pruning)."""
+
+    def __init__(self, m, cfg):
+        self.map = OracleMap(m)
+        self.n, self.d = self.map.n, self.map.d
+        self.opt = lib().orc_opt_create(self.n, self.d)
+        self.cfg = mapper_config_c(cfg)
+
+    def __del__(self):
+        try:
+            lib().orc_opt_free(self.opt)
+        except Exception:
+            pass
+
+    def step(self, pose, cam, s, gt_color, gt_depth, gt_feature, iteration):
+        vals = np.zeros(3)
+        fs = C.c_int32()
+        gtf = None if gt_feature is None else np.ascontiguousarray(gt_feature, np.float32)
+        lib().orc_optimize_step(self.map.h, self.opt, C.byref(self.cfg), C.byref(cam_c(cam)), C.byref(settings_c(s)),
+                                C.byref(pose_c(pose)), _p(np.ascontiguousarray(gt_color, np.float32)),
+                                _p(np.ascontiguousarray(gt_depth, np.float32)), _p(gtf), int(iteration), _p(vals),
+                                C.byref(fs))
+        return dict(map=vals[0], geo=vals[1], feat=vals[2]), bool(fs.value)
+
+    def update_contribution_stats(self, generation, map_size, w, h, k, index, count, contributions):
+        rc = lib().orc_update_contribution_stats(self.map.h, generation, map_size, w, h, k,
+                                                 _p(np.ascontiguousarray(index, np.int32)),
+                                                 _p(np.ascontiguousarray(count, np.uint8)),
+                                                 _p(np.ascontiguousarray(contributions, np.float64)))
+        if rc:
+            raise RuntimeError(lib().orc_last_error().decode())
+
+    def export(self):
+        n, d = self.n, self.d
+        o = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
+                 opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d)),
+                 topk_count=np.zeros(n, np.int32), max_contribution=np.zeros(n))
+        lib().orc_map_export(self.map.h, *[_p(o[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit",
+                                                              "color", "feature", "topk_count", "max_contribution")])
+        return o

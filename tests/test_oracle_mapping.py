@@ -1,0 +1,180 @@
+"""Pin the mapping-iteration oracle (oracle/src/oracle_mapping.inc) to the reference's own tests.
+
+Restates, at the reference's tolerances, proj/tests/test_core.cpp:187-240 (SSIM), and
+proj/tests/test_mapper.cpp:124-158 (contribution statistics), :270-311 (loss mix) and
+:313-415 (the single-Gaussian optimize_step problem: schedule, period one, fit).  CPU only.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from paper_2602_06991_b200 import synth
+from paper_2602_06991_b200.types import MapperConfig, Pose, RenderSettings, SceneMap
+
+
+def logit(p):
+    return math.log(p / (1.0 - p))
+
+
+def ssim_value(a, b):
+    return O.ssim_with_grad(a, b)[0]
+
+
+def test_ssim_basics_and_fd_gradient():  # test_core.cpp:187-240
+    rng = np.random.default_rng(9)
+    a = rng.uniform(0, 1, (16, 16, 1))
+    b = rng.uniform(0, 1, (16, 16, 1))
+    assert ssim_value(a, a) == pytest.approx(1.0, rel=1e-12)
+    assert ssim_value(a, 1.0 - a) < 0.0
+    base, grad = O.ssim_with_grad(a, b)
+    direction = rng.uniform(-1, 1, a.shape)
+    analytic = float((grad * direction).sum())
+    h = 1e-6
+    fd = (ssim_value(a + h * direction, b) - ssim_value(a - h * direction, b)) / (2 * h)
+    assert abs(analytic - fd) / max(abs(fd), 1e-9) < 1e-6
+    for idx in (8 * 16 + 8, 5 * 16 + 9):
+        y, x = divmod(idx, 16)
+        hp = 1e-5
+        ap, am = a.copy(), a.copy()
+        ap[y, x, 0] += hp
+        am[y, x, 0] -= hp
+        fd1 = (ssim_value(ap, b) - ssim_value(am, b)) / (2 * hp)
+        assert abs(grad[y, x, 0] - fd1) / max(abs(fd1), 1e-3) < 1e-4
+
+
+def test_ssim_multichannel_mean_over_channels():  # ssim.cpp:90-108: mean over every channel's windows
+    rng = np.random.default_rng(3)
+    a = rng.uniform(0, 1, (14, 17, 3))
+    b = rng.uniform(0, 1, (14, 17, 3))
+    per = [ssim_value(a[..., c:c + 1], b[..., c:c + 1]) for c in range(3)]
+    assert ssim_value(a, b) == pytest.approx(np.mean(per), rel=1e-12)
+
+
+def stats_map(n, d=2):  # test_mapper.cpp:67-80
+    return SceneMap(mean=np.array([[i, 0, 1] for i in range(n)], float), log_scale=np.zeros((n, 3)),
+                    rotation=np.tile([1.0, 0, 0, 0], (n, 1)), opacity_logit=np.zeros(n), color=np.zeros((n, 3)),
+                    feature=np.eye(n, d), feature_dim=d)
+
+
+def test_contribution_statistics_accumulate():  # test_mapper.cpp:124-158
+    m = stats_map(3)
+    om = O.OracleMapper(m, MapperConfig())
+    w, h, k = 4, 3, 2
+    index = np.zeros(w * h * k, np.int32)
+    count = np.ones(w * h, np.uint8)
+    count[0] = 2
+    index[1] = 1
+    om.update_contribution_stats(0, 3, w, h, k, index, count, np.array([0.4, 0.25, 0.0]))
+    e = om.export()
+    assert list(e["topk_count"]) == [12, 1, 0]
+    assert e["max_contribution"][0] == 0.4 and e["max_contribution"][2] == 0.0
+    om.update_contribution_stats(0, 3, w, h, k, index, count, np.array([0.7, 0.1, 0.0]))
+    e = om.export()
+    assert e["topk_count"][0] == 24
+    assert e["max_contribution"][0] == 0.7 and e["max_contribution"][1] == 0.25
+    with pytest.raises(RuntimeError, match="does not match map generation"):
+        om.update_contribution_stats(99, 3, w, h, k, index, count, np.zeros(3))
+
+
+@pytest.fixture(scope="module")
+def loss_setup():  # test_mapper.cpp:270-281
+    cam = synth.test_camera(16, 16)
+    m = synth.random_scene(5, 4, 3)
+    r = O.render_geometric(m, Pose(), cam, RenderSettings())
+    gt_color = r["color"].astype(np.float32)
+    gt_depth = r["depth"].astype(np.float32)
+    gt_feature = np.zeros((16, 16, 4), np.float32)
+    return r, gt_color, gt_depth, gt_feature
+
+
+def test_identical_render_gives_zero_loss(loss_setup):
+    r, gc, gd, gf = loss_setup
+    v, *_ = O.compute_losses(r["color"], r["depth"], r["count"], None, gc, gd, gf, MapperConfig(), False)
+    assert v["geo"] < 1e-7 and v["map"] < 1e-7
+
+
+def test_uniform_color_offset_plain_l1(loss_setup):
+    r, gc, gd, gf = loss_setup
+    cfg = MapperConfig(lambda1=0.0, lambda2=0.0, lambda_feat=0.0)
+    v, *_ = O.compute_losses(r["color"] + 0.1, r["depth"], r["count"], None, gc, gd, gf, cfg, False)
+    assert v["map"] == pytest.approx(0.1, rel=1e-6)
+
+
+def test_invalid_depth_pixels_carry_no_depth_loss(loss_setup):
+    r, gc, gd, gf = loss_setup
+    v, _, g_depth, _ = O.compute_losses(r["color"], r["depth"] + 123.0, r["count"], None, gc, np.zeros_like(gd), gf,
+                                        MapperConfig(lambda1=0.0), False)
+    assert v["geo"] < 1e-7 and (g_depth == 0).all()
+
+
+def test_feature_term_masks_uncovered_and_invalid_pixels():  # losses.cpp:88-118
+    rng = np.random.default_rng(5)
+    h, w, d = 12, 13, 3
+    feat = rng.normal(size=(h, w, d))
+    gt = rng.normal(size=(h, w, d)).astype(np.float32)
+    gt[:3] = 0.0
+    count = rng.integers(0, 3, (h, w)).astype(np.uint8)
+    cfg = MapperConfig(lambda_feat=0.7)
+    v, _, _, gf = O.compute_losses(np.zeros((h, w, 3)), np.zeros((h, w)), count, feat, np.zeros((h, w, 3), np.float32),
+                                   np.zeros((h, w), np.float32), gt, cfg, True)
+    mask = (count > 0) & (np.abs(gt).sum(-1) > 0)
+    diff = feat - gt.astype(np.float64)
+    assert v["feat"] == pytest.approx(np.abs(diff[mask]).sum() / (mask.sum() * d), rel=1e-12)
+    assert v["map"] == pytest.approx(1.0 * v["geo"] + 0.7 * v["feat"], rel=1e-12)
+    assert (gf[~mask] == 0).all()
+    assert np.allclose(gf[mask], 0.7 * np.sign(diff[mask]) / (mask.sum() * d), rtol=0, atol=0)
+
+
+def single_gaussian_problem():  # test_mapper.cpp:313-357
+    cam = synth.test_camera(24, 24)
+    s = RenderSettings(transmittance_floor=0.0)
+    truth = SceneMap(mean=np.array([[0.05, -0.03, 1.5]]), log_scale=np.full((1, 3), math.log(0.12)),
+                     rotation=np.array([[1.0, 0, 0, 0]]), opacity_logit=np.array([logit(0.8)]),
+                     color=np.array([[0.8, 0.3, 0.2]]), feature=np.array([[1.0, 0.0]]), feature_dim=2)
+    gt = O.render_geometric(truth, Pose(), cam, s)
+    gt_color = gt["color"].astype(np.float32)
+    gt_depth = gt["depth"].astype(np.float32)
+    gt_feature = np.zeros((24, 24, 2), np.float32)
+    gt_feature[gt["alpha"] > 0.3, 0] = 1.0
+    start = SceneMap(mean=truth.mean + [0.06, -0.04, 0.08], log_scale=truth.log_scale.copy(),
+                     rotation=truth.rotation.copy(), opacity_logit=np.array([logit(0.5)]),
+                     color=np.array([[0.5, 0.5, 0.5]]), feature=np.array([[0.0, 1.0]]), feature_dim=2)
+    return start, cam, s, gt_color, gt_depth, gt_feature
+
+
+def test_hybrid_schedule_touches_features_only_on_period():  # test_mapper.cpp:360-376
+    start, cam, s, gc, gd, gf = single_gaussian_problem()
+    om = O.OracleMapper(start, MapperConfig(feature_update_period=5))
+    for it in range(1, 13):
+        before = om.export()["feature"].copy()
+        v, fstep = om.step(Pose(), cam, s, gc, gd, gf, it)
+        changed = np.linalg.norm(om.export()["feature"] - before) > 0
+        assert fstep == (it % 5 == 0) and changed == fstep
+        if not fstep:
+            assert v["feat"] == 0.0
+
+
+def test_every_step_carries_feature_term_with_period_one():  # test_mapper.cpp:378-391
+    start, cam, s, gc, gd, gf = single_gaussian_problem()
+    om = O.OracleMapper(start, MapperConfig(feature_update_period=1))
+    for it in range(1, 6):
+        v, fstep = om.step(Pose(), cam, s, gc, gd, gf, it)
+        assert fstep and v["feat"] > 0.0
+
+
+def test_single_gaussian_fits_its_keyframe():  # test_mapper.cpp:393-415
+    start, cam, s, gc, gd, gf = single_gaussian_problem()
+    om = O.OracleMapper(start, MapperConfig(feature_update_period=1))
+    first = last = None
+    for it in range(1, 201):
+        v, _ = om.step(Pose(), cam, s, gc, gd, gf, it)
+        first = v["geo"] if first is None else first
+        last = v["geo"]
+    assert last < first / 10.0
+    e = om.export()
+    assert e["feature"][0, 0] > 0.9
+    assert abs(np.linalg.norm(e["feature"][0]) - 1.0) < 1e-6
+    assert np.linalg.norm(e["rotation"][0]) == pytest.approx(1.0, rel=1e-9)
+    assert e["color"].max() <= 1.0 and e["color"].min() >= 0.0
