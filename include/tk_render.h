@@ -19,6 +19,12 @@
  * tk_backward_feature              backward_feature               (raster/backward.hpp:33-34)
  * tk_backward_geometric            backward_geometric             (raster/backward.hpp:27-29)
  * tk_comm_* / tk_allgather_feature multi-GPU D-sharding (no reference counterpart)
+ * tk_keyframe_set                  SceneMap::keyframes entry (map/scene_map.hpp, Keyframe)
+ * tk_optimizer_reset               OptimizerState (map/optimizer.hpp:25-53), zeroed
+ * tk_optimize_step                 optimize_step without pruning (map/mapper.hpp:72-73,
+ *                                  mapper.cpp:162-255): compute_losses (losses.hpp:42-43),
+ *                                  adam_step (optimizer.hpp:58-59), update_contribution_stats
+ * tk_scene_download                SceneMap parameters + Gaussian3D statistics back to the host
  *
  * Memory spaces: every buffer argument is tagged TK_HOST or TK_DEVICE.  Host buffers are
  * copied in/out inside the call (pinned memory from tk_host_alloc is fastest); device buffers
@@ -178,6 +184,54 @@ tk_status tk_comm_init(tk_ctx* ctx, const uint8_t id[128], int32_t nranks, int32
 tk_status tk_allgather_feature(tk_ctx* ctx, float* out, int32_t out_mem);
 tk_status tk_allreduce_sum_f64(tk_ctx* ctx, double* values, int32_t count); /* host values */
 
+/* ---- one mapping iteration on the device (map/mapper.cpp:162-255) ---- */
+typedef struct { /* MapperConfig knobs of one iteration; same layout as the oracle's orc_mapper_config */
+    double lambda_geo, lambda_feat, lambda1, lambda2; /* LossWeights, losses.hpp:9-21 */
+    int32_t color_secondary;        /* 0 = D-SSIM, 1 = duplicated L1 (ColorSecondaryTerm) */
+    int32_t feature_update_period;  /* Schedule, mapper.hpp:16 */
+    double l1_deadband;
+    double lr_mean, lr_log_scale, lr_rotation, lr_opacity, lr_color, lr_feature; /* optimizer.hpp:15-22 */
+    double beta1, beta2, eps;       /* AdamParams, optimizer.hpp:9-13 */
+    double min_log_scale, max_log_scale; /* mapper.hpp:31-32 */
+} tk_mapper_config;
+
+typedef struct { /* Frame (ground truth of one keyframe): fp32 images, HWC */
+    int32_t width, height, d;
+    const float* color;   /* H*W*3 */
+    const float* depth;   /* H*W; <= 0 marks invalid depth */
+    const float* feature; /* H*W*d, or NULL (then d must be 0) */
+    int32_t mem;
+} tk_frame_view;
+
+typedef struct { /* SceneMap parameters + statistics out; NULL pointers are skipped */
+    int32_t mem;
+    double* mean;             /* n x 3 */
+    double* log_scale;        /* n x 3 */
+    double* rotation;         /* n x 4 */
+    double* opacity_logit;    /* n */
+    double* color;            /* n x 3 */
+    float* feature;           /* n x d */
+    int32_t* topk_count;      /* n, Gaussian3D::topk_count */
+    double* max_contribution; /* n, Gaussian3D::max_contribution */
+} tk_scene_out;
+
+void tk_default_mapper_config(tk_mapper_config* cfg); /* the reference's defaults */
+/* Store keyframe `slot` (0-based; slots grow on demand) device-resident: pose + frame. */
+tk_status tk_keyframe_set(tk_ctx* ctx, int32_t slot, const tk_pose* pose, const tk_frame_view* frame);
+/* Zero the Adam state of every group for the resident scene (n, d) and, when reset_stats,
+ * the selection statistics (topk_count, max_contribution). */
+tk_status tk_optimizer_reset(tk_ctx* ctx, int32_t reset_stats);
+/* One optimisation step on keyframe `slot` (the caller samples it; mapper.cpp:167-168):
+ * render, losses, backward, Adam per group (features on iteration % feature_update_period
+ * == 0), renormalisation, statistics.  values_out (host, may be NULL = stay on the device,
+ * no synchronisation) receives {map, geo, feat} (LossValues, losses.hpp:23-27). */
+tk_status tk_optimize_step(tk_ctx* ctx, const tk_mapper_config* cfg, const tk_camera* cam,
+                           const tk_settings* s, int32_t slot, int64_t iteration, double* values_out,
+                           int32_t* feature_step_out);
+/* Loss values of the last tk_optimize_step (synchronises). */
+tk_status tk_loss_values(tk_ctx* ctx, double values[3]);
+tk_status tk_scene_download(tk_ctx* ctx, const tk_scene_out* out);
+
 /* Drop the cached PreparedScene / forward state: the next call re-projects, re-sorts and
  * re-bins (the reference recomputes prepare_scene in every call, render.cpp:295). */
 tk_status tk_invalidate(tk_ctx* ctx);
@@ -197,7 +251,9 @@ enum {
     TK_PHASE_FULL_BLEND = 7,   /* full-blend feature pass */
     TK_PHASE_ALLGATHER = 8,    /* NCCL all-gather + interleave */
     TK_PHASE_COPY = 9,         /* host <-> device copies made inside calls */
-    TK_NUM_PHASES = 10
+    TK_PHASE_LOSS = 10,        /* compute_losses: colour/depth L1, D-SSIM, fused feature L1 */
+    TK_PHASE_ADAM = 11,        /* chain rule + geometry Adam, feature backward + Adam */
+    TK_NUM_PHASES = 12
 };
 tk_status tk_profile_enable(tk_ctx* ctx, int32_t on);
 /* ms[TK_NUM_PHASES], counts[TK_NUM_PHASES] accumulated since the last reset (synchronises). */

@@ -70,6 +70,26 @@ class tk_device_view(C.Structure):
                 ("k", C.c_int32)]
 
 
+class tk_mapper_config(C.Structure):
+    _fields_ = [("lambda_geo", C.c_double), ("lambda_feat", C.c_double), ("lambda1", C.c_double),
+                ("lambda2", C.c_double), ("color_secondary", C.c_int32), ("feature_update_period", C.c_int32),
+                ("l1_deadband", C.c_double), ("lr_mean", C.c_double), ("lr_log_scale", C.c_double),
+                ("lr_rotation", C.c_double), ("lr_opacity", C.c_double), ("lr_color", C.c_double),
+                ("lr_feature", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("min_log_scale", C.c_double), ("max_log_scale", C.c_double)]
+
+
+class tk_frame_view(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("d", C.c_int32), ("color", C.c_void_p),
+                ("depth", C.c_void_p), ("feature", C.c_void_p), ("mem", C.c_int32)]
+
+
+class tk_scene_out(C.Structure):
+    _fields_ = [("mem", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p), ("rotation", C.c_void_p),
+                ("opacity_logit", C.c_void_p), ("color", C.c_void_p), ("feature", C.c_void_p),
+                ("topk_count", C.c_void_p), ("max_contribution", C.c_void_p)]
+
+
 class tk_synth_arrays(C.Structure):
     _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p),
                 ("rotation", C.c_void_p), ("opacity_logit", C.c_void_p), ("color", C.c_void_p),
@@ -117,10 +137,17 @@ RENDER_SYMBOLS = [
     ("tk_invalidate", C.c_int, [C.c_void_p]),
     ("tk_profile_enable", C.c_int, [C.c_void_p, C.c_int32]),
     ("tk_profile_read", C.c_int, [C.c_void_p, dbl_p, i64_p, C.c_int32]),
+    ("tk_default_mapper_config", None, [C.POINTER(tk_mapper_config)]),
+    ("tk_keyframe_set", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(tk_pose), C.POINTER(tk_frame_view)]),
+    ("tk_optimizer_reset", C.c_int, [C.c_void_p, C.c_int32]),
+    ("tk_optimize_step", C.c_int, [C.c_void_p, C.POINTER(tk_mapper_config), C.POINTER(tk_camera),
+                                   C.POINTER(tk_settings), C.c_int32, C.c_int64, dbl_p, i32_p]),
+    ("tk_loss_values", C.c_int, [C.c_void_p, dbl_p]),
+    ("tk_scene_download", C.c_int, [C.c_void_p, C.POINTER(tk_scene_out)]),
 ]
 
 PHASES = ["prepare", "geom_fwd", "gather", "fbwd_index", "fbwd", "geom_bwd", "chain", "full_blend", "allgather",
-          "copy"]
+          "copy", "loss", "adam"]
 
 SYNTH_SYMBOLS = [
     ("tk_synth_default_spec", None, [C.POINTER(tk_synth_spec)]),

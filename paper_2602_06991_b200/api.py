@@ -15,8 +15,8 @@ import ctypes as C
 import numpy as np
 
 from . import _native as N
-from .types import (CameraIntrinsics, GeomGrads, Pose, PreparedScene, RenderOutput, RenderSettings, SceneMap,
-                    TopKGrid, K_MAX_TOP_K)
+from .types import (CameraIntrinsics, Frame, GeomGrads, LossValues, MapperConfig, Pose, PreparedScene,
+                    RenderOutput, RenderSettings, SceneMap, TopKGrid, K_MAX_TOP_K)
 
 
 def _c(a: np.ndarray | None, dtype) -> np.ndarray | None:
@@ -46,6 +46,13 @@ def to_settings(s: RenderSettings) -> N.tk_settings:
     out.background[:] = tuple(s.background)
     out.cov2d_dilation = s.cov2d_dilation
     out.alpha_clamp = s.alpha_clamp
+    return out
+
+
+def to_mapper_config(cfg: MapperConfig) -> N.tk_mapper_config:
+    out = N.tk_mapper_config()
+    for name, _ in N.tk_mapper_config._fields_:
+        setattr(out, name, getattr(cfg, name))
     return out
 
 
@@ -180,6 +187,115 @@ class Renderer:
                                                C.byref(to_settings(s)), _p(gc), _p(gd), N.TK_HOST, C.byref(out)))
         g.pose_twist[:] = list(out.pose_twist)
         return g
+
+    # ---------------------------------------------------------------- mapping iteration
+    def keyframe_set(self, slot: int, pose: Pose, frame: Frame) -> None:
+        """Store a keyframe (SceneMap::keyframes entry) device-resident."""
+        col = _c(frame.color, np.float32)
+        dep = _c(frame.depth, np.float32)
+        feat = None if frame.feature is None else _c(frame.feature, np.float32)
+        h, w = dep.shape[:2]
+        d = 0 if feat is None else int(feat.shape[-1])
+        if col.size != w * h * 3 or (feat is not None and feat.size != w * h * d):
+            raise ValueError("keyframe_set: frame images disagree in shape")
+        view = N.tk_frame_view(w, h, d, _p(col), _p(dep), _p(feat), N.TK_HOST)
+        N.check(self.lib.tk_keyframe_set(self.ctx, slot, C.byref(to_pose(pose)), C.byref(view)))
+
+    def optimizer_reset(self, reset_stats: bool = True) -> None:
+        """A zeroed OptimizerState (optimizer.hpp:25-53) for the resident map."""
+        N.check(self.lib.tk_optimizer_reset(self.ctx, int(reset_stats)))
+
+    def optimize_step(self, cfg: MapperConfig, cam: CameraIntrinsics, s: RenderSettings, slot: int,
+                      iteration: int, fetch: bool = True) -> tuple[LossValues | None, bool]:
+        """optimize_step on keyframe `slot` (mapper.cpp:162-255 without pruning).  With fetch=False the
+        loss values stay on the device (no synchronisation); read them with loss_values()."""
+        vals = (C.c_double * 3)()
+        fs = C.c_int32()
+        N.check(self.lib.tk_optimize_step(self.ctx, C.byref(to_mapper_config(cfg)), C.byref(to_camera(cam)),
+                                          C.byref(to_settings(s)), slot, iteration,
+                                          vals if fetch else None, C.byref(fs)))
+        return (LossValues(vals[0], vals[1], vals[2]) if fetch else None), bool(fs.value)
+
+    def loss_values(self) -> LossValues:
+        vals = (C.c_double * 3)()
+        N.check(self.lib.tk_loss_values(self.ctx, vals))
+        return LossValues(vals[0], vals[1], vals[2])
+
+    def scene_download(self, n: int, d: int) -> dict:
+        """The resident map's parameters and selection statistics."""
+        o = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
+                 opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d), np.float32),
+                 topk_count=np.zeros(n, np.int32), max_contribution=np.zeros(n))
+        out = N.tk_scene_out(N.TK_HOST, *[_p(o[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit",
+                                                              "color", "feature", "topk_count",
+                                                              "max_contribution")])
+        N.check(self.lib.tk_scene_download(self.ctx, C.byref(out)))
+        return o
+
+
+class MT19937_64:
+    """std::mt19937_64 (the reference mapper's keyframe sampler, mapper.cpp:167)."""
+
+    _MASK = (1 << 64) - 1
+
+    def __init__(self, seed: int = 5489):
+        self.mt = [0] * 312
+        self.mt[0] = seed & self._MASK
+        for i in range(1, 312):
+            self.mt[i] = (6364136223846793005 * (self.mt[i - 1] ^ (self.mt[i - 1] >> 62)) + i) & self._MASK
+        self.idx = 312
+
+    def _twist(self) -> None:
+        mt = self.mt
+        for i in range(312):
+            x = (mt[i] & 0xFFFFFFFF80000000) | (mt[(i + 1) % 312] & 0x7FFFFFFF)
+            xa = x >> 1
+            if x & 1:
+                xa ^= 0xB5026F5AA96619E9
+            mt[i] = mt[(i + 156) % 312] ^ xa
+        self.idx = 0
+
+    def __call__(self) -> int:
+        if self.idx >= 312:
+            self._twist()
+        y = self.mt[self.idx]
+        self.idx += 1
+        y ^= (y >> 29) & 0x5555555555555555
+        y ^= (y << 17) & 0x71D67FFFEB880000
+        y ^= (y << 37) & 0xFFF7EEE000000000
+        y ^= y >> 43
+        return y & self._MASK
+
+
+class Mapper:
+    """The mapping loop of map/mapper.cpp over a device-resident map: keyframes live in HBM, each
+    optimize_step samples one with ``rng() % len(keyframes)`` (mapper.cpp:167) and runs render,
+    losses, backward and Adam on the GPU.  Pruning / insertion stay with the caller."""
+
+    def __init__(self, renderer: Renderer, m: SceneMap, cfg: MapperConfig, cam: CameraIntrinsics,
+                 settings: RenderSettings | None = None):
+        self.r, self.cfg, self.cam = renderer, cfg, cam
+        self.settings = settings or RenderSettings()
+        self.n, self.d = m.size(), m.feature_dim
+        renderer.upload(m)
+        renderer.optimizer_reset(True)
+        self.n_keyframes = 0
+
+    def add_keyframe(self, pose: Pose, frame: Frame) -> int:
+        self.r.keyframe_set(self.n_keyframes, pose, frame)
+        self.n_keyframes += 1
+        return self.n_keyframes - 1
+
+    def optimize_step(self, iteration: int, rng: MT19937_64, fetch: bool = True):
+        if self.n_keyframes == 0:
+            raise RuntimeError("optimize_step: no keyframes")
+        slot = rng() % self.n_keyframes
+        vals, fstep = self.r.optimize_step(self.cfg, self.cam, self.settings, slot, iteration, fetch)
+        return dict(iteration=iteration, losses=vals, feature_step=fstep, keyframe=slot, pruned=0,
+                    gaussian_count=self.n)
+
+    def export(self) -> dict:
+        return self.r.scene_download(self.n, self.d)
 
 
 _default: Renderer | None = None

@@ -3,7 +3,7 @@
   lib/libtkrender.so   sm_100a CUDA kernels + the C ABI of include/tk_render.h
   lib/libtk_synth.so   host C++ synthetic-input generators (include/tk_synth.h)
 
-The geometry TUs (prepare.cu, geometric.cu) are compiled with --fmad=false so their fp64
+The geometry TUs (prepare.cu, geometric.cu) and the loss / optimiser TU (mapping.cu) are compiled with --fmad=false so their fp64
 arithmetic rounds like the reference's x86-64 build (no FMA contraction); the feature TU is
 fp32 and keeps FMA.  Run:  python -m paper_2602_06991_b200.build
 """
@@ -30,6 +30,7 @@ CUDA_UNITS = [
     ("prepare.cu", ["--fmad=false"]),
     ("geometric.cu", ["--fmad=false"]),
     ("feature.cu", []),
+    ("mapping.cu", ["--fmad=false"]),
     ("tk_abi.cu", []),
 ]
 

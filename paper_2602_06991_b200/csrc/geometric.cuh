@@ -55,12 +55,31 @@ struct ChainParams {
     double* twist;  // n x 6
 };
 
+// In-place Adam over the five geometry groups (optimizer.hpp:25-53 layout: one m / v array per
+// group, strided like the parameters).  Group order: mean, log_scale, rotation, opacity, color.
+struct GeoAdamParams {
+    double* mean;
+    double* log_scale;
+    double* rotation;
+    double* opacity_logit;
+    double* color;
+    double* m[5];
+    double* v[5];
+    double lr[5];
+    double beta1, beta2, eps, bc1, bc2;
+    double min_log_scale, max_log_scale;
+    const unsigned long long* contrib;  // forward peak weights (fp64 bits), or null
+    double* max_contrib;
+};
+
 // number of one-warp CTAs covering the frame (8x4 pixel blocks per tile)
 int geom_blocks(const Frame& f);
 int geom_blocks_per_tile(int tile_size);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
 void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);
+// chain rule + Adam + clamps + renormalisation in one pass (no gradient arrays, no twist)
+void launch_chain_adam(const ChainParams& p, const GeoAdamParams& a, cudaStream_t st);
 // deterministic two-level sum of twist[n][6] -> out[6] (device)
 void launch_twist_reduce(const double* twist, int64_t n, double* partial, double* out, cudaStream_t st);
 

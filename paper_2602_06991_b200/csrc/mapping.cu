@@ -1,0 +1,619 @@
+// mapping.cu — the per-iteration loss and optimiser kernels of one mapping step
+// (map/mapper.cpp:162-255).  Compiled with --fmad=false: the colour/depth L1 and the D-SSIM
+// gradient follow ssim.cpp / losses.cpp operation by operation, so grad_color is bit-identical
+// to the fp64 oracle; the feature kernels use explicit fmaf (fp32, stated tolerance).
+//
+// Data per step (config 3: 1200x680, D = 512, 1M Gaussians):
+//   colour loss + SSIM: fp64 image maps, ~40 B/pixel/channel of map traffic (L2-resident tiles);
+//   feature loss: reads the K selected feature rows (as render_feature) and the keyframe's
+//     D-channel row, writes 2 sign bits per channel instead of the fp32 dL/dF image;
+//   feature Adam: per Gaussian reads the sign words of its records, then f, m, v (fp32) once.
+#include "mapping.cuh"
+#include "sort.cuh"
+
+namespace tk {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr double kC1 = 0.01 * 0.01;  // ssim.cpp:15-16
+constexpr double kC2 = 0.03 * 0.03;
+constexpr int kHalo = kSsimWin - 1;
+constexpr int kTile = 16;
+constexpr int kWinTile = kTile + kHalo;
+
+__device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+// Deterministic block sum of NV doubles (fixed shuffle tree, then warps in order).
+template <int NV>
+__device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restrict__ dst) {
+    __shared__ double sh[NV][kWarps];
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(0xffffffffu, v[a], o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+#pragma unroll
+        for (int a = 0; a < NV; ++a) sh[a][warp] = v[a];
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int w = 0; w < kWarps; ++w) s += sh[threadIdx.x][w];
+        dst[threadIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------- keyframe preprocessing
+__global__ void __launch_bounds__(kThreads) k_gt_valid(const float* __restrict__ gt, int64_t pixels, int d,
+                                                       uint8_t* __restrict__ valid, const float* __restrict__ gt_depth,
+                                                       unsigned long long* __restrict__ depth_n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    unsigned long long cnt = 0;
+    for (int64_t px = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; px < pixels; px += nw) {
+        bool any = false;
+        if (gt)
+            for (int c = lane; c < d; c += 32) any |= gt[px * d + c] != 0.0f;  // losses.cpp:98-100
+        any = __any_sync(0xffffffffu, any);
+        if (lane == 0) {
+            valid[px] = any ? 1 : 0;
+            cnt += gt_depth[px] > 0.0f ? 1 : 0;                              // losses.cpp:68-71
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(depth_n, cnt);
+}
+
+// ---------------------------------------------------------------- colour / depth / SSIM
+// convolve_valid row pass (ssim.cpp:31-41) of the five planes a, b, aa, bb, ab, all channels.
+__global__ void __launch_bounds__(kThreads) k_ssim_rows(ColorLossParams p) {
+    const int ow = p.w - kHalo;
+    const int64_t total = 3LL * p.h * ow;
+    const int64_t plane = static_cast<int64_t>(p.h) * ow;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int c = static_cast<int>(t / plane);
+        const int64_t r = t - c * plane;
+        const int y = static_cast<int>(r / ow), x = static_cast<int>(r - static_cast<int64_t>(y) * ow);
+        double sa = 0.0, sb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
+#pragma unroll
+        for (int i = 0; i < kSsimWin; ++i) {
+            const int64_t q = (static_cast<int64_t>(y) * p.w + x + i) * 3 + c;
+            const double va = p.color[q], vb = static_cast<double>(p.gt_color[q]);
+            const double kw = p.kern[i];
+            sa += kw * va;
+            sb += kw * vb;
+            saa += kw * (va * va);
+            sbb += kw * (vb * vb);
+            sab += kw * (va * vb);
+        }
+        double* o = p.rows + c * plane + r;
+        o[0] = sa;
+        o[3 * plane] = sb;
+        o[6 * plane] = saa;
+        o[9 * plane] = sbb;
+        o[12 * plane] = sab;
+    }
+}
+
+// Column pass (ssim.cpp:42-48) and the per-window terms of ssim_with_grad (ssim.cpp:128-145).
+__global__ void __launch_bounds__(kThreads) k_ssim_windows(ColorLossParams p) {
+    const int ow = p.w - kHalo, oh = p.h - kHalo;
+    const int64_t plane_r = static_cast<int64_t>(p.h) * ow, plane_w = static_cast<int64_t>(oh) * ow;
+    const int64_t total = 3 * plane_w;
+    double v[1] = {0.0};
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < total;
+         t += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int c = static_cast<int>(t / plane_w);
+        const int64_t r = t - c * plane_w;
+        const int wy = static_cast<int>(r / ow), wx = static_cast<int>(r - static_cast<int64_t>(wy) * ow);
+        double s[5];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+            const double* src = p.rows + (m * 3 + c) * plane_r + wx;
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < kSsimWin; ++i) acc += p.kern[i] * src[static_cast<int64_t>(wy + i) * ow];
+            s[m] = acc;
+        }
+        const double mu_a = s[0], mu_b = s[1];
+        const double var_a = s[2] - mu_a * mu_a;
+        const double var_b = s[3] - mu_b * mu_b;
+        const double cov = s[4] - mu_a * mu_b;
+        const double a1 = 2.0 * mu_a * mu_b + kC1;
+        const double a2 = 2.0 * cov + kC2;
+        const double b1 = mu_a * mu_a + mu_b * mu_b + kC1;
+        const double b2 = var_a + var_b + kC2;
+        v[0] += (a1 * a2) / (b1 * b2);
+        const double d_mu = 2.0 * (mu_b * a2 * b1 - mu_a * a1 * a2) / (b1 * b1 * b2);
+        const double d_var = -a1 * a2 / (b1 * b2 * b2);
+        const double d_cov = 2.0 * a1 / (b1 * b2);
+        double* o = p.win + c * plane_w + r;
+        o[0] = mu_a;
+        o[3 * plane_w] = mu_b;
+        o[6 * plane_w] = d_mu;
+        o[9 * plane_w] = d_var;
+        o[12 * plane_w] = d_cov;
+    }
+    block_sum_store<1>(v, p.partial + blockIdx.x * kLossSlots + kSsimSum);
+}
+
+// Per pixel: colour L1 (losses.cpp:36-46), the D-SSIM gradient gathered over every window that
+// covers the pixel in the reference's (wy, wx) accumulation order (ssim.cpp:147-154), the
+// colour-gradient mix (losses.cpp:50-58), depth L1 (losses.cpp:64-80) and the lambda folds
+// (losses.cpp:128-130).  16x16 pixel tiles; the 26x26 windows they need are staged in smem.
+__global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
+    __shared__ double sw[5][kWinTile][kWinTile];
+    const int ow = p.w - kHalo, oh = p.h - kHalo;
+    const int64_t plane_w = static_cast<int64_t>(oh > 0 ? oh : 0) * (ow > 0 ? ow : 0);
+    const int tx = (p.w + kTile - 1) / kTile, ty = (p.h + kTile - 1) / kTile;
+    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
+    const double scale = -0.5 * p.lambda1;
+    const double fold_d = p.lambda_geo * p.lambda2;
+    double v[2] = {0.0, 0.0};
+    for (int tile = blockIdx.x; tile < tx * ty; tile += gridDim.x) {
+        const int x0 = (tile % tx) * kTile, y0 = (tile / tx) * kTile;
+        const int x = x0 + lx, y = y0 + ly;
+        const bool in = x < p.w && y < p.h;
+        const int64_t px = static_cast<int64_t>(y) * p.w + x;
+        double g[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c < 3; ++c) {
+            if (p.use_ssim) {
+                __syncthreads();
+                for (int e = threadIdx.x; e < kWinTile * kWinTile; e += kThreads) {
+                    const int ey = e / kWinTile, ex = e - ey * kWinTile;
+                    const int wy = y0 - kHalo + ey, wx = x0 - kHalo + ex;
+                    if (wy >= 0 && wy < oh && wx >= 0 && wx < ow) {
+                        const double* src = p.win + c * plane_w + static_cast<int64_t>(wy) * ow + wx;
+#pragma unroll
+                        for (int m = 0; m < 5; ++m) sw[m][ey][ex] = src[m * 3 * plane_w];
+                    }
+                }
+                __syncthreads();
+                if (in) {
+                    const double av = p.color[px * 3 + c], bv = static_cast<double>(p.gt_color[px * 3 + c]);
+                    const int wy_lo = max(0, y - kHalo), wy_hi = min(oh - 1, y);
+                    const int wx_lo = max(0, x - kHalo), wx_hi = min(ow - 1, x);
+                    double acc = 0.0;
+                    for (int wy = wy_lo; wy <= wy_hi; ++wy) {
+                        const int ey = wy - (y0 - kHalo);
+                        const double ky = p.kern[y - wy];
+                        for (int wx = wx_lo; wx <= wx_hi; ++wx) {
+                            const int ex = wx - (x0 - kHalo);
+                            const double wgt = ky * p.kern[x - wx];
+                            acc += p.inv_count * wgt *
+                                   (sw[2][ey][ex] + sw[3][ey][ex] * 2.0 * (av - sw[0][ey][ex]) +
+                                    sw[4][ey][ex] * (bv - sw[1][ey][ex]));
+                        }
+                    }
+                    g[c] = acc;
+                }
+            }
+        }
+        if (!in) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double diff = p.color[px * 3 + c] - static_cast<double>(p.gt_color[px * 3 + c]);
+            v[0] += fmax(fabs(diff) - p.deadband, 0.0);
+            double gc = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_color_n;
+            if (p.use_ssim) gc = (1.0 - p.lambda1) * gc + scale * g[c];
+            p.grad_color[px * 3 + c] = gc * p.lambda_geo;
+        }
+        double gd = 0.0;
+        if (p.use_depth) {
+            const float t = p.gt_depth[px];
+            if (t > 0.0f) {
+                const double diff = p.depth[px] - static_cast<double>(t);
+                v[1] += fmax(fabs(diff) - p.deadband, 0.0);
+                gd = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_depth_n;
+            }
+        }
+        p.grad_depth[px] = gd * fold_d;
+    }
+    block_sum_store<2>(v, p.partial + blockIdx.x * kLossSlots + kL1Color);
+}
+
+// ---------------------------------------------------------------- feature loss
+__device__ __forceinline__ float4 fma4(float a, float4 x, float4 acc) {
+    acc.x = fmaf(a, x.x, acc.x);
+    acc.y = fmaf(a, x.y, acc.y);
+    acc.z = fmaf(a, x.z, acc.z);
+    acc.w = fmaf(a, x.w, acc.w);
+    return acc;
+}
+
+__device__ __forceinline__ uint32_t sign_bits(float d) { return (d > 0.0f ? 1u : 0u) | (d < 0.0f ? 2u : 0u); }
+
+__device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height, int tiles_x, bool* valid) {
+    const int64_t t = v >> 8;
+    const int l = static_cast<int>(v & 255);
+    const int x = static_cast<int>(t % tiles_x) * 16 + (l & 15), y = static_cast<int>(t / tiles_x) * 16 + (l >> 4);
+    *valid = x < width && y < height;
+    return static_cast<int64_t>(y) * width + x;
+}
+
+// render_feature (render.cpp:319-334) fused with the masked feature L1 (losses.cpp:92-118):
+// the rendered row never leaves registers; per channel only sign(F - GT) is stored (the
+// gradient is lambda_feat * sign / (feat_n * D), with the scalar applied in the Adam kernel).
+// D % 4 == 0: two pixels per warp in 16x16 tile order, 128-bit loads.
+__global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
+    const int tiles_x = (p.width + 15) / 16, tiles_y = (p.height + 15) / 16;
+    const int64_t nv = static_cast<int64_t>(tiles_x) * tiles_y * 256;
+    double v[2] = {0.0, 0.0};
+    for (int64_t v0 = ((static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5) * 2; v0 < nv; v0 += nw * 2) {
+        int64_t px[2];
+        int c[2], id[2];
+        float wn[2];
+        bool in[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &in[u]);
+            const int cnt = in[u] ? p.count[px[u]] : 0;
+            const bool live = cnt > 0 && p.gt_valid[px[u]];
+            c[u] = live ? cnt : 0;
+            double wd = 0.0;
+            id[u] = 0;
+            if (lane < c[u]) {
+                id[u] = p.index[px[u] * p.k + lane];
+                wd = p.weight[px[u] * p.k + lane];
+            }
+            double sum = 0.0;
+            for (int j = 0; j < c[u]; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
+            wn[u] = lane < c[u] ? static_cast<float>(wd / sum) : 0.0f;
+            if (lane == 0 && live) v[1] += 1.0;
+        }
+        const int cmax = max(c[0], c[1]);
+        for (int base = 0; base < d4; base += 128) {
+            float4 acc[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) acc[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < cmax; ++j) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int g = __shfl_sync(0xffffffffu, id[u], j);
+                    const float wj = __shfl_sync(0xffffffffu, wn[u], j);
+                    if (j < c[u]) {
+                        const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(g) * D);
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) {
+                            const int q = base + m * 32 + lane;
+                            if (q < d4) acc[u][m] = fma4(wj, __ldg(row + q), acc[u][m]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                if (!in[u]) continue;
+                const float4* grow = reinterpret_cast<const float4*>(p.gt + px[u] * D);
+                uint32_t* srow = p.signs + px[u] * wpp;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    uint32_t byte = 0;
+                    if (c[u] > 0 && q < d4) {
+                        const float4 t = __ldcs(grow + q);
+                        const float dx = acc[u][m].x - t.x, dy = acc[u][m].y - t.y;
+                        const float dz = acc[u][m].z - t.z, dw = acc[u][m].w - t.w;
+                        v[0] += static_cast<double>(fabsf(dx)) + static_cast<double>(fabsf(dy)) +
+                                static_cast<double>(fabsf(dz)) + static_cast<double>(fabsf(dw));
+                        byte = sign_bits(dx) | (sign_bits(dy) << 2) | (sign_bits(dz) << 4) | (sign_bits(dw) << 6);
+                    }
+                    uint32_t word = byte << (8 * (lane & 3));
+                    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+                    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+                    if ((lane & 3) == 0 && q < d4) srow[q >> 2] = word;
+                }
+            }
+        }
+    }
+    block_sum_store<2>(v, p.partial + blockIdx.x * kLossSlots + kFeatAbs);
+}
+
+// Any D: one pixel per warp, scalar channels.
+__global__ void __launch_bounds__(kThreads) k_feature_loss_scalar(FeatLossParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, wpp = (D + 15) >> 4;
+    const int64_t P = static_cast<int64_t>(p.width) * p.height;
+    double v[2] = {0.0, 0.0};
+    for (int64_t px = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; px < P; px += nw) {
+        const int cnt = p.count[px];
+        const bool live = cnt > 0 && p.gt_valid[px];
+        const int c = live ? cnt : 0;
+        int id = 0;
+        double wd = 0.0;
+        if (lane < c) {
+            id = p.index[px * p.k + lane];
+            wd = p.weight[px * p.k + lane];
+        }
+        double sum = 0.0;
+        for (int j = 0; j < c; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
+        const float wn = lane < c ? static_cast<float>(wd / sum) : 0.0f;
+        if (lane == 0 && live) v[1] += 1.0;
+        for (int base = 0; base < D; base += 32) {
+            const int q = base + lane;
+            float acc = 0.0f;
+            for (int j = 0; j < c; ++j) {
+                const int g = __shfl_sync(0xffffffffu, id, j);
+                const float wj = __shfl_sync(0xffffffffu, wn, j);
+                if (q < D) acc = fmaf(wj, __ldg(p.feat + static_cast<int64_t>(g) * D + q), acc);
+            }
+            uint32_t bits = 0;
+            if (c > 0 && q < D) {
+                const float dq = acc - p.gt[px * D + q];
+                v[0] += static_cast<double>(fabsf(dq));
+                bits = sign_bits(dq);
+            }
+            uint32_t word = bits << (2 * (lane & 15));
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+            if ((lane & 15) == 0 && q < D) p.signs[px * wpp + (q >> 4)] = word;
+        }
+    }
+    block_sum_store<2>(v, p.partial + blockIdx.x * kLossSlots + kFeatAbs);
+}
+
+// Loss values (losses.cpp:84-126) from the per-block partials, summed in a fixed order.
+__global__ void __launch_bounds__(kThreads) k_loss_finalize(FinalizeParams p) {
+    __shared__ double tot[kLossSlots];
+    for (int s = 0; s < kLossSlots; ++s) {
+        double v[1] = {0.0};
+        for (int b = threadIdx.x; b < p.nparts; b += kThreads) v[0] += p.partial[b * kLossSlots + s];
+        block_sum_store<1>(v, &tot[s]);
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double l1_color = tot[kL1Color] * p.inv_color_n;
+    double secondary = 0.0;
+    if (p.use_ssim) secondary = 0.5 * (1.0 - tot[kSsimSum] * p.inv_count);
+    else if (p.secondary_l1) secondary = l1_color;
+    const double l1_depth = p.use_depth ? tot[kL1Depth] * p.inv_depth_n : 0.0;
+    const double geo = (1.0 - p.lambda1) * l1_color + p.lambda1 * secondary + p.lambda2 * l1_depth;
+    double feat = 0.0;
+    float fscale = 0.0f;
+    if (p.feature_step && tot[kFeatCount] > 0.0) {
+        const double inv = 1.0 / (tot[kFeatCount] * p.d);
+        feat = tot[kFeatAbs] * inv;
+        fscale = static_cast<float>(p.lambda_feat * inv);
+    }
+    const double lf = p.feature_step ? p.lambda_feat : 0.0;
+    p.values[0] = p.lambda_geo * geo + lf * feat;
+    p.values[1] = geo;
+    p.values[2] = feat;
+    if (p.feat_scale) *p.feat_scale = fscale;
+}
+
+// update_contribution_stats (mapper.cpp:68-73): Top-K selection counts (integer atomics).
+__global__ void k_topk_stats(const int32_t* __restrict__ index, const uint8_t* __restrict__ count, int64_t pixels,
+                             int k, int32_t* __restrict__ topk_count) {
+    for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < pixels;
+         px += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = count[px];
+        for (int j = 0; j < c; ++j) atomicAdd(topk_count + index[px * k + j], 1);
+    }
+}
+
+// ---------------------------------------------------------------- feature backward + Adam
+__device__ __forceinline__ float sgnbit(uint32_t bits, int sh) {
+    return static_cast<float>((bits >> sh) & 1u) - static_cast<float>((bits >> (sh + 1)) & 1u);
+}
+
+__device__ __forceinline__ float adam1(float g, float& m, float& v, float f, const FeatAdamParams& p) {
+    m = p.beta1 * m + (1.0f - p.beta1) * g;                                   // optimizer.cpp:57-61
+    v = p.beta2 * v + (1.0f - p.beta2) * g * g;
+    return f - p.lr * (m / p.bc1) / (sqrtf(v / p.bc2) + p.eps);
+}
+
+__device__ __forceinline__ float warp_sum(float s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// backward_feature (backward.cpp:288-319) over the sign image, fused with the feature Adam
+// step and the renormalisation of mapper.cpp:239-252.  One warp per Gaussian (all N: Adam
+// moves every row through its moments); records summed in (pixel, slot) order.
+__global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
+    const float scale = *p.scale;
+    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        float4* frow = reinterpret_cast<float4*>(p.feat + g * D);
+        float4* mrow = reinterpret_cast<float4*>(p.m + g * D);
+        float4* vrow = reinterpret_cast<float4*>(p.v + g * D);
+        float ss = 0.0f;
+        float4 keep[4];
+        for (int base = 0; base < d4; base += 128) {
+            float4 acc[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int r = r0; r < r1; r += 32) {
+                const int nr = min(32, r1 - r);
+                int64_t spx = 0;
+                float sw = 0.f;
+                if (lane < nr) {
+                    const uint32_t s = p.slots[r + lane];
+                    spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+                    sw = p.wnorm[s];
+                }
+                for (int j = 0; j < nr; ++j) {
+                    const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
+                    const float wj = __shfl_sync(0xffffffffu, sw, j);
+                    const uint32_t* srow = p.signs + pxj * wpp;
+                    if (!isfinite(wj)) {  // backward.cpp:296-302: all-zero gradient rows are skipped
+                        bool any = false;
+                        for (int q = lane; q < wpp; q += 32) any |= srow[q] != 0u;
+                        if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
+                    }
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        if (q < d4) {
+                            const uint32_t b = __ldg(srow + (q >> 2)) >> (8 * (q & 3));
+                            acc[m].x = fmaf(wj, sgnbit(b, 0), acc[m].x);
+                            acc[m].y = fmaf(wj, sgnbit(b, 2), acc[m].y);
+                            acc[m].z = fmaf(wj, sgnbit(b, 4), acc[m].z);
+                            acc[m].w = fmaf(wj, sgnbit(b, 6), acc[m].w);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q >= d4) continue;
+                float4 f = frow[q], mm = mrow[q], vv = vrow[q];
+                f.x = adam1(acc[m].x * scale, mm.x, vv.x, f.x, p);
+                f.y = adam1(acc[m].y * scale, mm.y, vv.y, f.y, p);
+                f.z = adam1(acc[m].z * scale, mm.z, vv.z, f.z, p);
+                f.w = adam1(acc[m].w * scale, mm.w, vv.w, f.w, p);
+                __stcs(mrow + q, mm);
+                __stcs(vrow + q, vv);
+                ss += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+                if (d4 <= 128) keep[m] = f;
+                else frow[q] = f;
+            }
+        }
+        const float norm = sqrtf(warp_sum(ss));
+        const float inv = norm > 1e-12f ? 1.0f / norm : 1.0f;
+        if (d4 <= 128) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = m * 32 + lane;
+                if (q < d4) {
+                    float4 f = keep[m];
+                    if (norm > 1e-12f) {
+                        f.x *= inv;
+                        f.y *= inv;
+                        f.z *= inv;
+                        f.w *= inv;
+                    }
+                    frow[q] = f;
+                }
+            }
+        } else if (norm > 1e-12f) {
+            for (int q = lane; q < d4; q += 32) {
+                float4 f = frow[q];
+                f.x *= inv;
+                f.y *= inv;
+                f.z *= inv;
+                f.w *= inv;
+                frow[q] = f;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, wpp = (D + 15) >> 4;
+    const float scale = *p.scale;
+    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        float* frow = p.feat + g * D;
+        float ss = 0.0f;
+        for (int base = 0; base < D; base += 32) {
+            const int q = base + lane;
+            float acc = 0.0f;
+            for (int r = r0; r < r1; ++r) {
+                const uint32_t s = p.slots[r];
+                const int64_t pxj = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+                const float wj = p.wnorm[s];
+                const uint32_t* srow = p.signs + pxj * wpp;
+                if (!isfinite(wj)) {
+                    bool any = false;
+                    for (int t = lane; t < wpp; t += 32) any |= srow[t] != 0u;
+                    if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
+                }
+                if (q < D) acc = fmaf(wj, sgnbit(srow[q >> 4], 2 * (q & 15)), acc);
+            }
+            if (q < D) {
+                float mm = p.m[g * D + q], vv = p.v[g * D + q];
+                const float f = adam1(acc * scale, mm, vv, frow[q], p);
+                p.m[g * D + q] = mm;
+                p.v[g * D + q] = vv;
+                frow[q] = f;
+                ss += f * f;
+            }
+        }
+        const float norm = sqrtf(warp_sum(ss));
+        if (norm > 1e-12f)
+            for (int q = lane; q < D; q += 32) frow[q] /= norm;
+    }
+}
+
+inline unsigned capped_grid(int64_t items, int per_block, int64_t cap) {
+    const int64_t b = (items + per_block - 1) / per_block;
+    return static_cast<unsigned>(b < 1 ? 1 : (b < cap ? b : cap));
+}
+
+}  // namespace
+
+void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int64_t* depth_n_out,
+                     const float* gt_depth, cudaStream_t st) {
+    cudaMemsetAsync(depth_n_out, 0, sizeof(int64_t), st);
+    if (pixels <= 0) return;
+    k_gt_valid<<<capped_grid(pixels, kWarps, 148 * 16), kThreads, 0, st>>>(
+        gt, pixels, d, valid, gt_depth, reinterpret_cast<unsigned long long*>(depth_n_out));
+    dbg_launch("k_gt_valid", st);
+}
+
+void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launches) {
+    const int64_t P = static_cast<int64_t>(p.w) * p.h;
+    if (P <= 0) return;
+    if (p.use_ssim) {
+        const int ow = p.w - kHalo, oh = p.h - kHalo;
+        k_ssim_rows<<<capped_grid(3LL * p.h * ow, kThreads, 148 * 16), kThreads, 0, st>>>(p);
+        dbg_launch("k_ssim_rows", st);
+        k_ssim_windows<<<capped_grid(3LL * oh * ow, kThreads, kLossBlocks), kThreads, 0, st>>>(p);
+        dbg_launch("k_ssim_windows", st);
+        *launches += 2;
+    }
+    const int64_t tiles = static_cast<int64_t>((p.w + kTile - 1) / kTile) * ((p.h + kTile - 1) / kTile);
+    k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st>>>(p);
+    dbg_launch("k_color_loss", st);
+    *launches += 1;
+}
+
+void launch_feature_loss(const FeatLossParams& p, cudaStream_t st) {
+    const int64_t P = static_cast<int64_t>(p.width) * p.height;
+    if (P <= 0 || p.d <= 0) return;
+    const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p.gt) % 16) == 0;
+    if (vec) k_feature_loss_vec<<<capped_grid((P + 1) / 2, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
+    else k_feature_loss_scalar<<<capped_grid(P, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
+    dbg_launch("k_feature_loss", st);
+}
+
+void launch_loss_finalize(const FinalizeParams& p, cudaStream_t st) {
+    k_loss_finalize<<<1, kThreads, 0, st>>>(p);
+    dbg_launch("k_loss_finalize", st);
+}
+
+void launch_topk_stats(const int32_t* index, const uint8_t* count, int64_t pixels, int k, int32_t* topk_count,
+                       cudaStream_t st) {
+    if (pixels <= 0 || k <= 0) return;
+    k_topk_stats<<<capped_grid(pixels, 256, 148 * 8), 256, 0, st>>>(index, count, pixels, k, topk_count);
+    dbg_launch("k_topk_stats", st);
+}
+
+void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
+    if (p.n <= 0 || p.d <= 0) return;
+    const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
+    if (vec) k_feature_adam_vec<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+    else k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+    dbg_launch("k_feature_adam", st);
+}
+
+}  // namespace tk

@@ -13,6 +13,7 @@
 
 #include "feature.cuh"
 #include "geometric.cuh"
+#include "mapping.cuh"
 #include "prepare.cuh"
 #include "sort.cuh"
 #include "tk_common.cuh"
@@ -158,6 +159,21 @@ struct Profiler {
     }
 };
 
+// One keyframe of SceneMap::keyframes, device-resident (ground-truth images + pose).
+struct Keyframe {
+    tk_pose pose{};
+    int w = 0, h = 0, d = 0;
+    bool has_feature = false;
+    int64_t depth_n = 0;  // pixels with valid ground-truth depth (losses.cpp:68-71)
+    DevBuf color, depth, feature, valid;
+    void release() {
+        color.release();
+        depth.release();
+        feature.release();
+        valid.release();
+    }
+};
+
 }  // namespace
 
 struct tk_ctx {
@@ -209,6 +225,15 @@ struct tk_ctx {
     DevBuf g_color_in, g_depth_in, mid, twist, twist_part, twist_out, gg_mean, gg_ls, gg_rot, gg_op, gg_col;
     // full blend
     DevBuf l_count, l_off, l_src, l_w;
+    // mapping iteration: keyframes, optimiser state (per group m / v), statistics, loss scratch
+    std::vector<Keyframe> kfs;
+    bool opt_ready = false;
+    int64_t opt_n = 0, stat_n = -1;
+    int32_t opt_d = 0;
+    int64_t step_geo = 0, step_feat = 0;
+    DevBuf am[5], av[5], fm, fv, stat_count, stat_maxc;
+    DevBuf ssim_rows, ssim_win, l_gc, l_gd, l_partial, l_values, l_fscale, l_signs;
+    double* hvals = nullptr;  // pinned {map, geo, feat} of the last optimize_step
     // multi-GPU
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;
@@ -629,6 +654,73 @@ Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
     return r;
 }
 
+struct SlotIndex {
+    const int32_t* seg;
+    const uint32_t* slots;
+    const float* wnorm;
+};
+
+// Inverted (Gaussian -> record slots) index of a TopKGrid, ascending slot order per Gaussian.
+SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
+    const int64_t slots = static_cast<int64_t>(r.w) * r.h * r.k;
+    const int64_t n = c->n;
+    uint32_t* recs = ensure<uint32_t>(c->s_keys, slots);
+    uint32_t* svals = ensure<uint32_t>(c->s_vals, slots);
+    int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 1);
+    float* wn = ensure<float>(c->s_wnorm, slots);
+    int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
+    ensure_scratch(c, std::max<int64_t>(slots, n + 1), true);
+    PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
+    tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
+    int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+    tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, c->cur, &c->launches);
+    return SlotIndex{seg, svals, wn};
+}
+
+// The backward sweep of backward_geometric (backward.cpp:106-188) into the per-Gaussian
+// projected-space gradients (n x 10), on the forward state of this context.
+double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double* gd) {
+    const int64_t n = c->n;
+    double* mid = ensure<double>(c->mid, n * 10);
+    CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), c->cur));
+    tk::GeomBwdParams bp{};
+    bp.f = f;
+    bp.te = tile_entries(c);
+    bp.tile_offsets = ptr<int32_t>(c->tile_offsets);
+    bp.padded_start = ptr<int32_t>(c->padded_start);
+    bp.aux.t_final = ptr<double>(c->aux_t);
+    bp.aux.n_iter = ptr<int32_t>(c->aux_n);
+    bp.aux.wl = ptr<int32_t>(c->wl);
+    bp.aux.wl_count = ptr<int32_t>(c->wl_count);
+    bp.grad_color = gc;
+    bp.grad_depth = gd;
+    bp.mid = mid;
+    {
+        PhaseScope phase(c, TK_PHASE_GEOM_BWD);
+        tk::launch_geom_bwd(bp, tk::geom_blocks(f), c->cur);
+    }
+    c->launches += 1;
+    CK_LAUNCH(c);
+    return mid;
+}
+
+tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
+                             const double* mid) {
+    tk::ChainParams cp{};
+    cp.n = c->n;
+    cp.mid = mid;
+    cp.mean = ptr<double>(c->mean);
+    cp.log_scale = ptr<double>(c->log_scale);
+    cp.rotation = ptr<double>(c->rotation);
+    cp.opacity_logit = ptr<double>(c->opacity_logit);
+    const double pv[7] = {pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
+    std::memcpy(cp.pose, pv, sizeof(pv));
+    cp.fx = cam->fx;
+    cp.fy = cam->fy;
+    cp.dilation = s->cov2d_dilation;
+    return cp;
+}
+
 void require_features(tk_ctx* c) {
     if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
     if (!c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
@@ -714,6 +806,15 @@ tk_status tk_destroy(tk_ctx* c) {
                      &c->wl, &c->wl_count};
     for (DevBuf* b : all) b->release();
     for (DevBuf& b : c->te) b.release();
+    for (Keyframe& k : c->kfs) k.release();
+    for (int g = 0; g < 5; ++g) {
+        c->am[g].release();
+        c->av[g].release();
+    }
+    DevBuf* mapping[] = {&c->fm, &c->fv, &c->stat_count, &c->stat_maxc, &c->ssim_rows, &c->ssim_win, &c->l_gc,
+                         &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs};
+    for (DevBuf* b : mapping) b->release();
+    if (c->hvals) cudaFreeHost(c->hvals);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     if (c->hscal) cudaFreeHost(c->hscal);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -927,21 +1028,9 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
             copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
             g = dg;
         }
-        // inverted index (Gaussian -> slots, ascending within each Gaussian) by counting
-        uint32_t* recs = ensure<uint32_t>(c->s_keys, slots);
-        uint32_t* svals = ensure<uint32_t>(c->s_vals, slots);
-        int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 1);
-        float* wn = ensure<float>(c->s_wnorm, slots);
-        int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
-        ensure_scratch(c, std::max<int64_t>(slots, n + 1), true);
-        {
-            PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
-            tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
-            int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-            tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, st, &c->launches);
-        }
+        const SlotIndex si = build_slot_index(c, r);
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_grad_out, n * std::max(c->d, 1));
-        tk::FeatBwdParams fp{n, r.k, c->d, seg, svals, wn, g, dst};
+        tk::FeatBwdParams fp{n, r.k, c->d, si.seg, si.slots, si.wnorm, g, dst};
         {
             PhaseScope phase(c, TK_PHASE_FBWD);
             tk::launch_feature_bwd(fp, st);
@@ -1036,39 +1125,9 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
                 gd = dgd;
             }
         }
-        double* mid = ensure<double>(c->mid, n * 10);
-        CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), st));
-        tk::GeomBwdParams bp{};
-        bp.f = f;
-        bp.te = tile_entries(c);
-        bp.tile_offsets = ptr<int32_t>(c->tile_offsets);
-        bp.padded_start = ptr<int32_t>(c->padded_start);
-        bp.aux.t_final = ptr<double>(c->aux_t);
-        bp.aux.n_iter = ptr<int32_t>(c->aux_n);
-        bp.aux.wl = ptr<int32_t>(c->wl);
-        bp.aux.wl_count = ptr<int32_t>(c->wl_count);
-        bp.grad_color = gc;
-        bp.grad_depth = gd;
-        bp.mid = mid;
-        {
-            PhaseScope phase(c, TK_PHASE_GEOM_BWD);
-            tk::launch_geom_bwd(bp, tk::geom_blocks(f), st);
-        }
-        c->launches += 1;
-        CK_LAUNCH(c);
+        double* mid = geom_sweep(c, f, gc, gd);
         const bool dev_out = out && out->mem == TK_DEVICE;
-        tk::ChainParams cp{};
-        cp.n = n;
-        cp.mid = mid;
-        cp.mean = ptr<double>(c->mean);
-        cp.log_scale = ptr<double>(c->log_scale);
-        cp.rotation = ptr<double>(c->rotation);
-        cp.opacity_logit = ptr<double>(c->opacity_logit);
-        const double pv[7] = {pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
-        std::memcpy(cp.pose, pv, sizeof(pv));
-        cp.fx = cam->fx;
-        cp.fy = cam->fy;
-        cp.dilation = s->cov2d_dilation;
+        tk::ChainParams cp = chain_params(c, pose, cam, s, mid);
         cp.g_mean = dev_out && out->mean ? out->mean : ensure<double>(c->gg_mean, n * 3);
         cp.g_log_scale = dev_out && out->log_scale ? out->log_scale : ensure<double>(c->gg_ls, n * 3);
         cp.g_rotation = dev_out && out->rotation ? out->rotation : ensure<double>(c->gg_rot, n * 4);
@@ -1185,6 +1244,327 @@ tk_status tk_allreduce_sum_f64(tk_ctx* c, double* values, int32_t count) {
         copy_out(values, d, count * sizeof(double), TK_HOST, c);
         sync(c);
         tmp.release();
+        main_done(c);
+    });
+}
+
+// ------------------------------------------------------------------ mapping iteration
+void tk_default_mapper_config(tk_mapper_config* cfg) {
+    cfg->lambda_geo = 1.0;  // losses.hpp:9-21
+    cfg->lambda_feat = 1.0;
+    cfg->lambda1 = 0.2;
+    cfg->lambda2 = 1.0;
+    cfg->color_secondary = 0;
+    cfg->feature_update_period = 5;  // mapper.hpp:16
+    cfg->l1_deadband = 0.0;
+    cfg->lr_mean = 2e-3;  // optimizer.hpp:15-22
+    cfg->lr_log_scale = 5e-3;
+    cfg->lr_rotation = 1e-3;
+    cfg->lr_opacity = 5e-2;
+    cfg->lr_color = 2e-2;
+    cfg->lr_feature = 1e-2;
+    cfg->beta1 = 0.9;  // optimizer.hpp:9-13
+    cfg->beta2 = 0.999;
+    cfg->eps = 1e-8;
+    cfg->min_log_scale = -10.0;  // mapper.hpp:31-32
+    cfg->max_log_scale = 1.0;
+}
+
+tk_status tk_keyframe_set(tk_ctx* c, int32_t slot, const tk_pose* pose, const tk_frame_view* fr) {
+    return guarded([&] {
+        if (!c || !pose || !fr) fail(TK_ERR_BAD_ARG, "null argument");
+        if (slot < 0 || slot > (1 << 20)) fail(TK_ERR_BAD_ARG, "keyframe slot out of range");
+        if (fr->width <= 0 || fr->height <= 0 || fr->d < 0) fail(TK_ERR_BAD_ARG, "bad frame shape");
+        if (!fr->color || !fr->depth) fail(TK_ERR_BAD_ARG, "frame needs color and depth");
+        if (fr->d > 0 && !fr->feature) fail(TK_ERR_BAD_ARG, "frame feature is NULL but d > 0");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        if (static_cast<size_t>(slot) >= c->kfs.size()) c->kfs.resize(slot + 1);
+        Keyframe& k = c->kfs[slot];
+        k.pose = *pose;
+        k.w = fr->width;
+        k.h = fr->height;
+        k.d = fr->d;
+        k.has_feature = fr->d > 0;
+        const int64_t P = static_cast<int64_t>(k.w) * k.h;
+        float* col = ensure<float>(k.color, P * 3);
+        float* dep = ensure<float>(k.depth, P);
+        copy_in(col, fr->color, P * 3 * sizeof(float), fr->mem, c);
+        copy_in(dep, fr->depth, P * sizeof(float), fr->mem, c);
+        float* feat = nullptr;
+        if (k.has_feature) {
+            feat = ensure<float>(k.feature, P * k.d);
+            copy_in(feat, fr->feature, static_cast<size_t>(P) * k.d * sizeof(float), fr->mem, c);
+        }
+        uint8_t* valid = ensure<uint8_t>(k.valid, P);
+        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+        tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, dep, c->cur);
+        c->launches += 1;
+        CK_LAUNCH(c);
+        CK(cudaMemcpyAsync(c->hscal + 9, dscal + 9, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cur));
+        sync(c);
+        k.depth_n = c->hscal[9];
+        main_done(c);
+    });
+}
+
+tk_status tk_optimizer_reset(tk_ctx* c, int32_t reset_stats) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        const int64_t n = c->n;
+        const int dims[5] = {3, 3, 4, 1, 3};
+        for (int g = 0; g < 5; ++g) {
+            CK(cudaMemsetAsync(ensure<double>(c->am[g], n * dims[g]), 0, std::max<int64_t>(n, 1) * dims[g] * 8, c->cur));
+            CK(cudaMemsetAsync(ensure<double>(c->av[g], n * dims[g]), 0, std::max<int64_t>(n, 1) * dims[g] * 8, c->cur));
+        }
+        const int64_t nd = n * std::max(c->d, 1);
+        CK(cudaMemsetAsync(ensure<float>(c->fm, nd), 0, std::max<int64_t>(nd, 1) * 4, c->cur));
+        CK(cudaMemsetAsync(ensure<float>(c->fv, nd), 0, std::max<int64_t>(nd, 1) * 4, c->cur));
+        if (reset_stats || c->stat_n != n) {
+            CK(cudaMemsetAsync(ensure<int32_t>(c->stat_count, n), 0, std::max<int64_t>(n, 1) * 4, c->cur));
+            CK(cudaMemsetAsync(ensure<double>(c->stat_maxc, n), 0, std::max<int64_t>(n, 1) * 8, c->cur));
+            c->stat_n = n;
+        }
+        c->step_geo = c->step_feat = 0;
+        c->opt_ready = true;
+        c->opt_n = n;
+        c->opt_d = c->d;
+        main_done(c);
+    });
+}
+
+tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_camera* cam, const tk_settings* s,
+                           int32_t slot, int64_t iteration, double* values_out, int32_t* feature_step_out) {
+    return guarded([&] {
+        check_frame(cam, s);
+        if (!cfg) fail(TK_ERR_BAD_ARG, "null mapper config");
+        if (slot < 0 || static_cast<size_t>(slot) >= c->kfs.size() || c->kfs[slot].w == 0)
+            fail(TK_ERR_BAD_ARG, "optimize_step: no keyframe in that slot");
+        if (cfg->feature_update_period <= 0) fail(TK_ERR_BAD_ARG, "feature_update_period must be positive");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        if (!c->opt_ready || c->opt_n != c->n || c->opt_d != c->d || c->stat_n != c->n)
+            fail(TK_ERR_STATE, "optimizer state does not match the scene (tk_optimizer_reset)");
+        const Keyframe& kf = c->kfs[slot];
+        if (kf.w != cam->width || kf.h != cam->height)
+            fail(TK_ERR_BAD_ARG, "compute_losses: render/frame shape mismatch");
+        const bool feature_step = (iteration % cfg->feature_update_period) == 0;  // mapper.cpp:171
+        const bool use_ssim = cfg->lambda1 != 0.0 && cfg->color_secondary == 0;
+        if (use_ssim && (cam->width < tk::kSsimWin || cam->height < tk::kSsimWin))
+            fail(TK_ERR_BAD_ARG, "ssim: image smaller than the 11x11 window");
+        if (feature_step) {
+            if (c->d <= 0 || !c->has_features)
+                fail(TK_ERR_BAD_ARG, "compute_losses: feature loss requested but render has no feature image");
+            if (kf.d != c->d) fail(TK_ERR_BAD_ARG, "compute_losses: feature shape mismatch");
+        }
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        cudaStream_t st = c->cur;
+        // render_geometric on the keyframe pose (mapper.cpp:173)
+        prepare(c, &kf.pose, cam, s);
+        forward(c, cam, s, true);
+        const tk::Frame f = make_frame(c, cam, s);
+        const int64_t P = static_cast<int64_t>(f.width) * f.height;
+        const int64_t n = c->n;
+        const int d = c->d;
+        double* gc = ensure<double>(c->l_gc, P * 3);
+        double* gd = ensure<double>(c->l_gd, P);
+        double* partial = ensure<double>(c->l_partial, tk::kLossBlocks * tk::kLossSlots);
+        double* values = ensure<double>(c->l_values, 4);
+        float* fscale = ensure<float>(c->l_fscale, 1);
+        const int wpp = (d + 15) / 16;
+        uint32_t* signs = feature_step ? ensure<uint32_t>(c->l_signs, P * std::max(wpp, 1)) : nullptr;
+        {
+            PhaseScope phase(c, TK_PHASE_LOSS);
+            CK(cudaMemsetAsync(partial, 0, tk::kLossBlocks * tk::kLossSlots * sizeof(double), st));
+            tk::launch_topk_stats(ptr<int32_t>(c->o_index), ptr<uint8_t>(c->o_count), P, f.k,
+                                  ptr<int32_t>(c->stat_count), st);
+            c->launches += 1;
+            // compute_losses (mapper.cpp:176, losses.cpp:22-133)
+            tk::ColorLossParams lp{};
+            lp.w = f.width;
+            lp.h = f.height;
+            lp.color = ptr<double>(c->o_color);
+            lp.depth = ptr<double>(c->o_depth);
+            lp.gt_color = ptr<float>(kf.color);
+            lp.gt_depth = ptr<float>(kf.depth);
+            lp.lambda_geo = cfg->lambda_geo;
+            lp.lambda1 = cfg->lambda1;
+            lp.lambda2 = cfg->lambda2;
+            lp.deadband = cfg->l1_deadband;
+            lp.use_ssim = use_ssim ? 1 : 0;
+            lp.use_depth = (kf.depth_n > 0 && cfg->lambda2 != 0.0) ? 1 : 0;
+            lp.inv_color_n = 1.0 / (static_cast<double>(f.width) * f.height * 3.0);
+            lp.inv_depth_n = kf.depth_n > 0 ? 1.0 / static_cast<double>(kf.depth_n) : 0.0;
+            {
+                const int ow = f.width - tk::kSsimWin + 1, oh = f.height - tk::kSsimWin + 1;
+                const size_t count = use_ssim ? static_cast<size_t>(ow) * oh * 3 : 1;  // ssim.cpp:119-123
+                lp.inv_count = 1.0 / static_cast<double>(count);
+                double sum = 0.0;  // gaussian_kernel(), ssim.cpp:18-28
+                for (int i = 0; i < tk::kSsimWin; ++i) {
+                    const double dd = i - tk::kSsimWin / 2;
+                    lp.kern[i] = std::exp(-0.5 * dd * dd / (1.5 * 1.5));
+                    sum += lp.kern[i];
+                }
+                for (double& v : lp.kern) v /= sum;
+                if (use_ssim) {
+                    lp.rows = ensure<double>(c->ssim_rows, 15LL * f.height * ow);
+                    lp.win = ensure<double>(c->ssim_win, 15LL * oh * ow);
+                }
+            }
+            lp.grad_color = gc;
+            lp.grad_depth = gd;
+            lp.partial = partial;
+            tk::launch_color_loss(lp, st, &c->launches);
+            if (feature_step) {
+                tk::FeatLossParams fl{};
+                fl.width = f.width;
+                fl.height = f.height;
+                fl.k = f.k;
+                fl.d = d;
+                fl.index = ptr<int32_t>(c->o_index);
+                fl.weight = ptr<double>(c->o_weight);
+                fl.count = ptr<uint8_t>(c->o_count);
+                fl.feat = ptr<float>(c->feature);
+                fl.gt = ptr<float>(kf.feature);
+                fl.gt_valid = ptr<uint8_t>(kf.valid);
+                fl.signs = signs;
+                fl.partial = partial;
+                tk::launch_feature_loss(fl, st);
+                c->launches += 1;
+            }
+            tk::FinalizeParams fp{};
+            fp.partial = partial;
+            fp.nparts = tk::kLossBlocks;
+            fp.lambda_geo = cfg->lambda_geo;
+            fp.lambda_feat = cfg->lambda_feat;
+            fp.lambda1 = cfg->lambda1;
+            fp.lambda2 = cfg->lambda2;
+            fp.use_ssim = lp.use_ssim;
+            fp.secondary_l1 = (cfg->lambda1 != 0.0 && cfg->color_secondary != 0) ? 1 : 0;
+            fp.use_depth = lp.use_depth;
+            fp.feature_step = feature_step ? 1 : 0;
+            fp.d = d;
+            fp.inv_color_n = lp.inv_color_n;
+            fp.inv_depth_n = lp.inv_depth_n;
+            fp.inv_count = lp.inv_count;
+            fp.values = values;
+            fp.feat_scale = fscale;
+            tk::launch_loss_finalize(fp, st);
+            c->launches += 1;
+            CK_LAUNCH(c);
+        }
+        if (!c->hvals) CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hvals), 4 * sizeof(double), cudaHostAllocDefault));
+        CK(cudaMemcpyAsync(c->hvals, values, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        // backward_geometric (mapper.cpp:179-180) on this forward
+        double* mid = geom_sweep(c, f, gc, gd);
+        {
+            PhaseScope phase(c, TK_PHASE_ADAM);
+            // geometry groups (mapper.cpp:183-236): five adam_step calls, one step counter each
+            c->step_geo += 1;
+            tk::GeoAdamParams ga{};
+            ga.mean = ptr<double>(c->mean);
+            ga.log_scale = ptr<double>(c->log_scale);
+            ga.rotation = ptr<double>(c->rotation);
+            ga.opacity_logit = ptr<double>(c->opacity_logit);
+            ga.color = ptr<double>(c->color);
+            for (int g = 0; g < 5; ++g) {
+                ga.m[g] = ptr<double>(c->am[g]);
+                ga.v[g] = ptr<double>(c->av[g]);
+            }
+            ga.lr[0] = cfg->lr_mean;
+            ga.lr[1] = cfg->lr_log_scale;
+            ga.lr[2] = cfg->lr_rotation;
+            ga.lr[3] = cfg->lr_opacity;
+            ga.lr[4] = cfg->lr_color;
+            ga.beta1 = cfg->beta1;
+            ga.beta2 = cfg->beta2;
+            ga.eps = cfg->eps;
+            ga.bc1 = 1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_geo));  // optimizer.cpp:52-53
+            ga.bc2 = 1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_geo));
+            ga.min_log_scale = cfg->min_log_scale;
+            ga.max_log_scale = cfg->max_log_scale;
+            ga.contrib = ptr<unsigned long long>(c->o_contrib);
+            ga.max_contrib = ptr<double>(c->stat_maxc);
+            tk::launch_chain_adam(chain_params(c, &kf.pose, cam, s, mid), ga, st);
+            c->launches += n > 0;
+            CK_LAUNCH(c);
+            if (feature_step && d > 0) {  // mapper.cpp:239-252
+                c->step_feat += 1;
+                Records r;
+                r.w = f.width;
+                r.h = f.height;
+                r.k = f.k;
+                r.index = ptr<int32_t>(c->o_index);
+                r.weight = ptr<double>(c->o_weight);
+                r.count = ptr<uint8_t>(c->o_count);
+                const SlotIndex si = build_slot_index(c, r);
+                tk::FeatAdamParams fa{};
+                fa.n = n;
+                fa.k = f.k;
+                fa.d = d;
+                fa.seg = si.seg;
+                fa.slots = si.slots;
+                fa.wnorm = si.wnorm;
+                fa.signs = signs;
+                fa.scale = fscale;
+                fa.feat = ptr<float>(c->feature);
+                fa.m = ptr<float>(c->fm);
+                fa.v = ptr<float>(c->fv);
+                fa.lr = static_cast<float>(cfg->lr_feature);
+                fa.beta1 = static_cast<float>(cfg->beta1);
+                fa.beta2 = static_cast<float>(cfg->beta2);
+                fa.eps = static_cast<float>(cfg->eps);
+                fa.bc1 = static_cast<float>(1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat)));
+                fa.bc2 = static_cast<float>(1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat)));
+                tk::launch_feature_adam(fa, st);
+                c->launches += n > 0;
+                CK_LAUNCH(c);
+            }
+        }
+        // the scene changed: the next render re-projects (records keep the pre-step snapshot)
+        c->scene_version += 1;
+        c->prepared = false;
+        c->aux_valid = false;
+        if (feature_step_out) *feature_step_out = feature_step ? 1 : 0;
+        if (values_out) {
+            sync(c);
+            std::memcpy(values_out, c->hvals, 3 * sizeof(double));
+        }
+        main_done(c);
+    });
+}
+
+tk_status tk_loss_values(tk_ctx* c, double values[3]) {
+    return guarded([&] {
+        if (!c->hvals) fail(TK_ERR_STATE, "no optimize_step has run");
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+        std::memcpy(values, c->hvals, 3 * sizeof(double));
+    });
+}
+
+tk_status tk_scene_download(tk_ctx* c, const tk_scene_out* o) {
+    return guarded([&] {
+        if (!c || !o) fail(TK_ERR_BAD_ARG, "null argument");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        if ((o->topk_count || o->max_contribution) && c->stat_n != c->n)
+            fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        const int64_t n = c->n;
+        copy_out(o->mean, c->mean.p, n * 3 * sizeof(double), o->mem, c);
+        copy_out(o->log_scale, c->log_scale.p, n * 3 * sizeof(double), o->mem, c);
+        copy_out(o->rotation, c->rotation.p, n * 4 * sizeof(double), o->mem, c);
+        copy_out(o->opacity_logit, c->opacity_logit.p, n * sizeof(double), o->mem, c);
+        copy_out(o->color, c->color.p, n * 3 * sizeof(double), o->mem, c);
+        if (o->feature && c->has_features)
+            copy_out(o->feature, c->feature.p, static_cast<size_t>(n) * c->d * sizeof(float), o->mem, c);
+        copy_out(o->topk_count, c->stat_count.p, n * sizeof(int32_t), o->mem, c);
+        copy_out(o->max_contribution, c->stat_maxc.p, n * sizeof(double), o->mem, c);
+        if (o->mem == TK_HOST) sync(c);
         main_done(c);
     });
 }

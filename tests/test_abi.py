@@ -42,7 +42,9 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"tk_camera": N.tk_camera, "tk_pose": N.tk_pose, "tk_settings": N.tk_settings,
                "tk_scene_view": N.tk_scene_view, "tk_topk_view": N.tk_topk_view, "tk_geom_out": N.tk_geom_out,
                "tk_geom_grads": N.tk_geom_grads, "tk_device_view": N.tk_device_view,
-               "tk_synth_arrays": N.tk_synth_arrays, "tk_synth_spec": N.tk_synth_spec}
+               "tk_synth_arrays": N.tk_synth_arrays, "tk_synth_spec": N.tk_synth_spec,
+               "tk_mapper_config": N.tk_mapper_config, "tk_frame_view": N.tk_frame_view,
+               "tk_scene_out": N.tk_scene_out}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tk_render.h"', '#include "tk_synth.h"',
              "int main(void) {"]
     for name, cls in structs.items():
@@ -67,6 +69,28 @@ def test_default_settings_match_reference():  # render.hpp:14-21
     N.render_lib().tk_default_settings(C.byref(s))
     assert (s.top_k, s.tile_size, s.transmittance_floor, tuple(s.background), s.cov2d_dilation, s.alpha_clamp) == \
         (3, 16, 1e-4, (0.0, 0.0, 0.0), 0.3, 0.999)
+
+
+def test_default_mapper_config_matches_reference_and_oracle_layout(tmp_path):
+    """tk_default_mapper_config == MapperConfig() (losses.hpp, optimizer.hpp, mapper.hpp defaults),
+    and tk_mapper_config has the oracle's orc_mapper_config layout field by field."""
+    from paper_2602_06991_b200.types import MapperConfig
+    import _oracle as O
+    cfg = N.tk_mapper_config()
+    N.render_lib().tk_default_mapper_config(C.byref(cfg))
+    ref = MapperConfig()
+    for name, _ in N.tk_mapper_config._fields_:
+        assert getattr(cfg, name) == getattr(ref, name), name
+    assert [f for f, _ in O.orc_mapper_config._fields_] == [f for f, _ in N.tk_mapper_config._fields_]
+    assert C.sizeof(O.orc_mapper_config) == C.sizeof(N.tk_mapper_config)
+
+
+def test_mt19937_64_matches_the_standard():  # [rand.predef]: 10000th output of default-seeded engine
+    from paper_2602_06991_b200.api import MT19937_64
+    r = MT19937_64()
+    for _ in range(9999):
+        r()
+    assert r() == 9981545732273789042
 
 
 def test_create_without_gpu_fails_cleanly():

@@ -1,0 +1,225 @@
+"""GPU parity of one mapping iteration (tk_optimize_step) against the CPU oracle's optimize_step.
+
+Contract:
+  * loss values: geo rel <= 1e-10 (fp64 both sides); feat rel <= 1e-5 (fp32 features on the GPU).
+  * geometry parameters after Adam: abs <= 1e-10 (fp64; gradients differ only by atomic order).
+  * features after Adam + renormalisation: abs <= 2e-5 (fp32 state).
+  * topk_count: exactly equal; max_contribution: rel <= 1e-9.
+Plus the reference's own mapper tests (test_mapper.cpp:360-415) run through the GPU Mapper.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import _oracle as O
+from _se3 import axis_angle
+from paper_2602_06991_b200 import _native as N
+from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200.types import Frame, MapperConfig, Pose, RenderSettings, SceneMap
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    r = api.Renderer(0)
+    yield r
+    r.close()
+
+
+def logit(p):
+    return math.log(p / (1.0 - p))
+
+
+def make_problem(n=300, d=8, w=64, h=48, seed=1, pose=None, depth_holes=True):
+    """A map, a perturbed 'truth' rendered by the oracle as the keyframe, and random GT features."""
+    m = synth.random_scene(n, d, seed)
+    truth = m.copy()
+    rng = np.random.default_rng(seed + 100)
+    truth.mean = truth.mean + rng.normal(0, 0.02, truth.mean.shape)
+    truth.color = np.clip(truth.color + rng.normal(0, 0.1, truth.color.shape), 0, 1)
+    cam = synth.test_camera(w, h)
+    pose = pose or Pose()
+    s = RenderSettings()
+    gt = O.render_geometric(truth, pose, cam, s)
+    depth = gt["depth"].astype(np.float32)
+    if depth_holes:
+        depth[: h // 6] = 0.0
+    feat = rng.normal(0, 1, (h, w, d)).astype(np.float32)
+    feat[gt["alpha"] < 0.3] = 0.0
+    frame = Frame(color=gt["color"].astype(np.float32), depth=depth, feature=feat)
+    return m, cam, s, pose, frame
+
+
+def run_both(R, m, cam, s, pose, frame, cfg, iterations):
+    om = O.OracleMapper(m, cfg)
+    R.upload(m)
+    R.optimizer_reset(True)
+    R.keyframe_set(0, pose, frame)
+    out = []
+    for it in iterations:
+        ov, ofs = om.step(pose, cam, s, frame.color, frame.depth, frame.feature, it)
+        gv, gfs = R.optimize_step(cfg, cam, s, 0, it)
+        assert gfs == ofs
+        out.append((it, ov, gv, ofs))
+    return om, out
+
+
+def compare_state(R, om, m, feat_tol=2e-5):
+    o = om.export()
+    g = R.scene_download(m.size(), m.feature_dim)
+    for key in ("mean", "log_scale", "rotation", "opacity_logit", "color"):
+        np.testing.assert_allclose(g[key], o[key], rtol=0, atol=1e-10, err_msg=key)
+    np.testing.assert_allclose(g["feature"], o["feature"], rtol=0, atol=feat_tol, err_msg="feature")
+    assert (g["topk_count"] == o["topk_count"]).all(), "topk_count differs"
+    np.testing.assert_allclose(g["max_contribution"], o["max_contribution"], rtol=1e-9, atol=0)
+
+
+CFGS = [
+    ("defaults", MapperConfig()),
+    ("l1dup_deadband", MapperConfig(color_secondary=1, l1_deadband=0.01, lambda_feat=0.5)),
+    ("no_depth_lambda1_0", MapperConfig(lambda1=0.0, lambda2=0.0, lambda_geo=2.0)),
+    ("period1", MapperConfig(feature_update_period=1, lr_feature=5e-2)),
+]
+
+
+@pytest.mark.parametrize("name,cfg", CFGS, ids=[c[0] for c in CFGS])
+def test_optimize_step_matches_oracle(R, name, cfg):
+    m, cam, s, pose, frame = make_problem()
+    om, steps = run_both(R, m, cam, s, pose, frame, cfg, [5, 6, 7])
+    for it, ov, gv, fs in steps:
+        assert gv.geo == pytest.approx(ov["geo"], rel=1e-10), (it, "geo")
+        assert gv.feat == pytest.approx(ov["feat"], rel=1e-5, abs=1e-12), (it, "feat")
+        assert gv.map == pytest.approx(ov["map"], rel=1e-5), (it, "map")
+        if not fs:
+            assert gv.feat == 0.0
+    compare_state(R, om, m)
+
+
+@pytest.mark.parametrize("k,tile", [(1, 16), (8, 8), (16, 32)])
+def test_optimize_step_topk_and_tile_variants(R, k, tile):
+    m, cam, s, pose, frame = make_problem(n=500, d=12, w=72, h=40, seed=4,
+                                          pose=Pose(axis_angle(0.15, (0, 1, 0)), (0.03, 0.0, 0.05)))
+    s = RenderSettings(top_k=k, tile_size=tile, background=(0.1, 0.0, 0.2))
+    om, steps = run_both(R, m, cam, s, pose, frame, MapperConfig(feature_update_period=2), [2, 3])
+    for it, ov, gv, fs in steps:
+        assert gv.geo == pytest.approx(ov["geo"], rel=1e-10)
+        assert gv.feat == pytest.approx(ov["feat"], rel=1e-5, abs=1e-12)
+    compare_state(R, om, m)
+
+
+def test_scalar_feature_path_odd_d(R):  # D % 4 != 0: scalar loss / Adam kernels
+    m, cam, s, pose, frame = make_problem(n=200, d=7, seed=11)
+    om, steps = run_both(R, m, cam, s, pose, frame, MapperConfig(feature_update_period=1), [1, 2])
+    for it, ov, gv, fs in steps:
+        assert gv.feat == pytest.approx(ov["feat"], rel=1e-5)
+    compare_state(R, om, m)
+
+
+def test_wide_feature_rows_two_pass_renormalise(R):  # D > 512: multi-chunk Adam + second norm pass
+    m, cam, s, pose, frame = make_problem(n=120, d=520, w=40, h=32, seed=3)
+    om, steps = run_both(R, m, cam, s, pose, frame, MapperConfig(feature_update_period=1), [1])
+    compare_state(R, om, m)
+
+
+def test_deferred_loss_values(R):
+    m, cam, s, pose, frame = make_problem(seed=8)
+    cfg = MapperConfig()
+    om = O.OracleMapper(m, cfg)
+    ov, _ = om.step(pose, cam, s, frame.color, frame.depth, frame.feature, 10)
+    R.upload(m)
+    R.optimizer_reset(True)
+    R.keyframe_set(0, pose, frame)
+    none, fs = R.optimize_step(cfg, cam, s, 0, 10, fetch=False)
+    assert none is None and fs
+    v = R.loss_values()
+    assert v.geo == pytest.approx(ov["geo"], rel=1e-10) and v.feat == pytest.approx(ov["feat"], rel=1e-5)
+
+
+def test_errors(R):
+    m, cam, s, pose, frame = make_problem(n=50, d=4, w=32, h=24)
+    r = api.Renderer(0)
+    try:
+        r.upload(m)
+        r.keyframe_set(0, pose, frame)
+        with pytest.raises(RuntimeError, match="tk_optimizer_reset"):
+            r.optimize_step(MapperConfig(), cam, s, 0, 1)
+        r.optimizer_reset()
+        with pytest.raises(RuntimeError, match="no keyframe"):
+            r.optimize_step(MapperConfig(), cam, s, 3, 1)
+        with pytest.raises(RuntimeError, match="shape mismatch"):
+            r.optimize_step(MapperConfig(), synth.test_camera(40, 24), s, 0, 1)
+        small = Frame(color=np.zeros((8, 8, 3), np.float32), depth=np.ones((8, 8), np.float32),
+                      feature=np.ones((8, 8, 4), np.float32))
+        r.keyframe_set(1, pose, small)
+        with pytest.raises(RuntimeError, match="11x11"):
+            r.optimize_step(MapperConfig(), synth.test_camera(8, 8), s, 1, 1)
+        r.optimize_step(MapperConfig(lambda1=0.0), synth.test_camera(8, 8), s, 1, 1)  # no SSIM: fine
+    finally:
+        r.close()
+
+
+# ---- the reference's mapper tests (test_mapper.cpp:313-415), on the GPU Mapper
+def single_gaussian_problem():
+    cam = synth.test_camera(24, 24)
+    s = RenderSettings(transmittance_floor=0.0)
+    truth = SceneMap(mean=np.array([[0.05, -0.03, 1.5]]), log_scale=np.full((1, 3), math.log(0.12)),
+                     rotation=np.array([[1.0, 0, 0, 0]]), opacity_logit=np.array([logit(0.8)]),
+                     color=np.array([[0.8, 0.3, 0.2]]), feature=np.array([[1.0, 0.0]]), feature_dim=2)
+    gt = O.render_geometric(truth, Pose(), cam, s)
+    feat = np.zeros((24, 24, 2), np.float32)
+    feat[gt["alpha"] > 0.3, 0] = 1.0
+    frame = Frame(color=gt["color"].astype(np.float32), depth=gt["depth"].astype(np.float32), feature=feat)
+    start = SceneMap(mean=truth.mean + [0.06, -0.04, 0.08], log_scale=truth.log_scale.copy(),
+                     rotation=truth.rotation.copy(), opacity_logit=np.array([logit(0.5)]),
+                     color=np.array([[0.5, 0.5, 0.5]]), feature=np.array([[0.0, 1.0]]), feature_dim=2)
+    return start, cam, s, frame
+
+
+def test_hybrid_schedule_touches_features_only_on_period(R):  # test_mapper.cpp:360-376
+    start, cam, s, frame = single_gaussian_problem()
+    mp = api.Mapper(R, start, MapperConfig(feature_update_period=5), cam, s)
+    mp.add_keyframe(Pose(), frame)
+    rng = api.MT19937_64(77)
+    for it in range(1, 13):
+        before = mp.export()["feature"].copy()
+        rec = mp.optimize_step(it, rng)
+        changed = np.linalg.norm(mp.export()["feature"] - before) > 0
+        assert rec["feature_step"] == (it % 5 == 0) and changed == rec["feature_step"]
+        if not rec["feature_step"]:
+            assert rec["losses"].feat == 0.0
+
+
+def test_every_step_carries_feature_term_with_period_one(R):  # test_mapper.cpp:378-391
+    start, cam, s, frame = single_gaussian_problem()
+    mp = api.Mapper(R, start, MapperConfig(feature_update_period=1), cam, s)
+    mp.add_keyframe(Pose(), frame)
+    rng = api.MT19937_64(78)
+    for it in range(1, 6):
+        rec = mp.optimize_step(it, rng)
+        assert rec["feature_step"] and rec["losses"].feat > 0.0
+
+
+def test_single_gaussian_fits_its_keyframe(R):  # test_mapper.cpp:393-415
+    start, cam, s, frame = single_gaussian_problem()
+    mp = api.Mapper(R, start, MapperConfig(feature_update_period=1), cam, s)
+    mp.add_keyframe(Pose(), frame)
+    rng = api.MT19937_64(79)
+    geo = [mp.optimize_step(it, rng)["losses"].geo for it in range(1, 201)]
+    assert geo[-1] < geo[0] / 10.0
+    e = mp.export()
+    assert e["feature"][0, 0] > 0.9
+    assert abs(np.linalg.norm(e["feature"][0]) - 1.0) < 1e-6
+    assert np.linalg.norm(e["rotation"][0]) == pytest.approx(1.0, rel=1e-9)
+    assert e["color"].max() <= 1.0 and e["color"].min() >= 0.0
+
+
+def test_mapper_samples_keyframes_like_the_reference(R):  # mapper.cpp:167: rng() % keyframes.size()
+    m, cam, s, pose, frame = make_problem(n=100, d=4, w=32, h=24)
+    mp = api.Mapper(R, m, MapperConfig(), cam, s)
+    for _ in range(3):
+        mp.add_keyframe(pose, frame)
+    rng, ref = api.MT19937_64(5), api.MT19937_64(5)
+    for it in range(1, 7):
+        assert mp.optimize_step(it, rng, fetch=False)["keyframe"] == ref() % 3
