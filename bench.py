@@ -12,9 +12,15 @@ Nothing is cached across steps (tk_invalidate each step); inputs are larger than
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c5] [--impl ours|reference]
 
-Under torchrun (N > 1) the feature dimension is sharded D/N per GPU: every
-rank recomputes the integer Top-K records, gathers/scatters its channel slice, and the rendered
-map is all-gathered with NCCL (tk_allgather_feature).  Rank 0 prints one JSON line.
+Under torchrun (N > 1) the default is keyframe-parallel weak scaling (config 4's 8-keyframe
+batch): rank r renders orbit keyframe r with all D channels, no data-path collective.  With
+--mode dshard the feature dimension is sharded D/N per GPU: every rank
+recomputes the integer Top-K records, gathers/scatters its channel slice, and the rendered map
+is all-gathered with NCCL (tk_allgather_feature).  Rank 0 prints one JSON line.
+
+The line also carries "mapping": one mapping iteration (tk_optimize_step: render, losses with
+D-SSIM and the masked feature L1, backward, Adam over every group, features on every 5th
+iteration) in iterations/s, device-resident and end to end (BASELINE north_star: >= 15 it/s).
 """
 from __future__ import annotations
 
@@ -386,6 +392,11 @@ def main_gpu(args, cfg):
         e2e = run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpose, ccam, cset, n, Ds, P,
                       K, max(2, min(args.steps, args.e2e_steps)), stream, dist)
 
+    mapping = None
+    if not dshard and not args.no_mapping:
+        mapping = run_mapping(lib, slib, N, torch, ctx, W, H, D, n, cpose, ccam, cset, args.steps, args.warmup,
+                              0 if args.no_e2e else args.e2e_steps, stream, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         r, err, cores, model, fthreads = run_cpu_oracle(cfg, budget_s=20.0, max_frames=1, timeout_s=600)
@@ -413,7 +424,7 @@ def main_gpu(args, cfg):
             "hbm_gbs": feature_path["achieved_gbs"],
             "roofline": roof, "feature_path": feature_path, "phases": phases,
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
-            "setup_s": setup_s,
+            "mapping": mapping, "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
     lib.tk_destroy(ctx)
@@ -493,6 +504,107 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
                     "backward_feature, backward_geometric (host in/out)"}
 
 
+def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, warmup, e2e_steps, stream, dist):
+    """Mapping iterations/s: tk_optimize_step (mapper.cpp:162-255 without pruning) on one keyframe of
+    the config-3 map: render_geometric, compute_losses (colour/depth L1 + D-SSIM + masked feature L1),
+    backward_geometric, Adam over every group, features on every 5th iteration, statistics."""
+    P = W * H
+
+    def pinned(count, dtype):
+        t = torch.empty(count, dtype=dtype, pin_memory=True)
+        return t, t.numpy()
+
+    keep = []
+    tc, col = pinned(P * 3, torch.float32)
+    td, dep = pinned(P, torch.float32)
+    tf, feat = pinned(P * D, torch.float32)
+    keep += [tc, td, tf]
+    slib.tk_synth_hash_fill_f32(col.size, 21, 0.0, 1.0, col.ctypes.data)
+    slib.tk_synth_hash_fill_f32(dep.size, 22, 0.5, 4.0, dep.ctypes.data)
+    slib.tk_synth_hash_fill_f32(feat.size, 23, -1.0, 1.0, feat.ctypes.data)
+    frame = N.tk_frame_view(W, H, D, col.ctypes.data, dep.ctypes.data, feat.ctypes.data, N.TK_HOST)
+    cfg = N.tk_mapper_config()
+    lib.tk_default_mapper_config(C.byref(cfg))
+    N.check(lib.tk_optimizer_reset(ctx, 1))
+    N.check(lib.tk_keyframe_set(ctx, 0, C.byref(kpose), C.byref(frame)))
+    it = [1]
+
+    def step(values=None):
+        N.check(lib.tk_optimize_step(ctx, C.byref(cfg), C.byref(ccam), C.byref(cset), 0, it[0], values, None))
+        it[0] += 1
+
+    for _ in range(warmup):
+        step()
+    N.check(lib.tk_synchronize(ctx))
+    steps = max(cfg.feature_update_period, (steps // cfg.feature_update_period) * cfg.feature_update_period)
+    N.check(lib.tk_profile_read(ctx, None, None, 1))
+    N.check(lib.tk_profile_enable(ctx, 1))
+    launches0 = lib.tk_kernel_launches(ctx)
+    if dist:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    N.check(lib.tk_profile_enable(ctx, 0))
+    ms = ev0.elapsed_time(ev1)
+    launches = lib.tk_kernel_launches(ctx) - launches0
+    ph_ms = (C.c_double * len(N.PHASES))()
+    ph_cnt = (C.c_int64 * len(N.PHASES))()
+    N.check(lib.tk_profile_read(ctx, ph_ms, ph_cnt, 1))
+    vals = (C.c_double * 3)()
+    N.check(lib.tk_loss_values(ctx, vals))
+
+    def ms_max(x):
+        if dist:
+            t = torch.tensor([x], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    ms = ms_max(ms)
+    world = dist.get_world_size() if dist else 1
+    out = {"metric": "mapping iterations/s (optimize_step fwd+losses+bwd+Adam, features every 5th iteration)",
+           "value": world * steps / (ms / 1000.0), "unit": "iterations/s", "ms_per_iteration": ms / steps,
+           "iterations": steps, "feature_update_period": cfg.feature_update_period, "gpu_launches": int(launches),
+           "last_losses": {"map": vals[0], "geo": vals[1], "feat": vals[2]},
+           "phases": {nm: {"ms_per_iteration": ph_ms[i] / steps, "launch_groups": int(ph_cnt[i])}
+                      for i, nm in enumerate(N.PHASES) if ph_cnt[i]},
+           "target": ">= 15 mapping iterations/s end to end (BASELINE.json north_star)"}
+    if e2e_steps <= 0:
+        return out
+    e2e_steps = max(2, e2e_steps)
+    hv = (C.c_double * 3)()
+    # (a) the keyframe's ground truth copied host -> device every iteration (worst case)
+    ev0.record(stream)
+    for _ in range(e2e_steps):
+        N.check(lib.tk_keyframe_set(ctx, 0, C.byref(kpose), C.byref(frame)))
+        step(hv)
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    ms_a = ms_max(ev0.elapsed_time(ev1))
+    # (b) keyframes resident in HBM (SceneMap::keyframes), loss values read back every iteration
+    ev0.record(stream)
+    for _ in range(e2e_steps):
+        step(hv)
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    ms_b = ms_max(ev0.elapsed_time(ev1))
+    out["e2e"] = {"value": world * e2e_steps / (ms_a / 1000.0), "unit": "iterations/s",
+                  "h2d_bytes_per_step": int(world * (col.nbytes + dep.nbytes + feat.nbytes)),
+                  "d2h_bytes_per_step": int(world * 24), "steps": e2e_steps,
+                  "path": "C ABI: tk_keyframe_set from pinned host (colour, depth, D-channel feature) + "
+                          "tk_optimize_step with the loss values read back, every iteration"}
+    out["e2e_resident_keyframes"] = {"value": world * e2e_steps / (ms_b / 1000.0), "unit": "iterations/s",
+                                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(world * 24),
+                                     "path": "keyframe uploaded once (device-resident keyframe store); "
+                                             "tk_optimize_step + loss values read back every iteration"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -504,6 +616,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-mapping", action="store_true", help="skip the mapping-iteration measurement")
     ap.add_argument("--mode", default="keyframe", choices=["keyframe", "dshard"],
                     help="multi-GPU decomposition (N > 1)")
     args = ap.parse_args()

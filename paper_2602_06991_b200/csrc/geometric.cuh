@@ -52,7 +52,7 @@ struct ChainParams {
     double* g_rotation;
     double* g_opacity_logit;
     double* g_color;
-    double* twist;  // n x 6
+    double* twist;  // n x 6, or null (mapping: no pose gradient)
 };
 
 // In-place Adam over the five geometry groups (optimizer.hpp:25-53 layout: one m / v array per
@@ -63,6 +63,7 @@ struct GeoAdamParams {
     double* rotation;
     double* opacity_logit;
     double* color;
+    const double* g[5];  // gradients (k_chain outputs)
     double* m[5];
     double* v[5];
     double lr[5];
@@ -78,8 +79,8 @@ int geom_blocks_per_tile(int tile_size);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
 void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);
-// chain rule + Adam + clamps + renormalisation in one pass (no gradient arrays, no twist)
-void launch_chain_adam(const ChainParams& p, const GeoAdamParams& a, cudaStream_t st);
+// Adam + clamps + renormalisation + peak statistic over every Gaussian (thread per Gaussian)
+void launch_geo_adam(const GeoAdamParams& a, int64_t n, cudaStream_t st);
 // deterministic two-level sum of twist[n][6] -> out[6] (device)
 void launch_twist_reduce(const double* twist, int64_t n, double* partial, double* out, cudaStream_t st);
 

@@ -20,8 +20,6 @@ constexpr int kWarps = kThreads / 32;
 constexpr double kC1 = 0.01 * 0.01;  // ssim.cpp:15-16
 constexpr double kC2 = 0.03 * 0.03;
 constexpr int kHalo = kSsimWin - 1;
-constexpr int kTile = 16;
-constexpr int kWinTile = kTile + kHalo;
 
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
@@ -66,61 +64,73 @@ __global__ void __launch_bounds__(kThreads) k_gt_valid(const float* __restrict__
 }
 
 // ---------------------------------------------------------------- colour / depth / SSIM
-// convolve_valid row pass (ssim.cpp:31-41) of the five planes a, b, aa, bb, ab, all channels.
-__global__ void __launch_bounds__(kThreads) k_ssim_rows(ColorLossParams p) {
-    const int ow = p.w - kHalo;
-    const int64_t total = 3LL * p.h * ow;
-    const int64_t plane = static_cast<int64_t>(p.h) * ow;
-    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * kThreads) {
-        const int c = static_cast<int>(t / plane);
-        const int64_t r = t - c * plane;
-        const int y = static_cast<int>(r / ow), x = static_cast<int>(r - static_cast<int64_t>(y) * ow);
-        double sa = 0.0, sb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
-#pragma unroll
-        for (int i = 0; i < kSsimWin; ++i) {
-            const int64_t q = (static_cast<int64_t>(y) * p.w + x + i) * 3 + c;
-            const double va = p.color[q], vb = static_cast<double>(p.gt_color[q]);
-            const double kw = p.kern[i];
-            sa += kw * va;
-            sb += kw * vb;
-            saa += kw * (va * va);
-            sbb += kw * (vb * vb);
-            sab += kw * (va * vb);
-        }
-        double* o = p.rows + c * plane + r;
-        o[0] = sa;
-        o[3 * plane] = sb;
-        o[6 * plane] = saa;
-        o[9 * plane] = sbb;
-        o[12 * plane] = sab;
-    }
-}
+// Window statistics of ssim_with_grad (ssim.cpp:31-50 convolve_valid, then :128-145) for a
+// 32 x 8 tile of windows of one channel: the (8+10) x (32+10) input patch of a and b is staged
+// in shared memory, the row pass goes to shared memory, the column pass runs per window.  Sums
+// run in the reference's tap order, so every statistic is bit-identical to the oracle's.
+constexpr int kSW = 32, kSH = 8;
+constexpr int kPW = kSW + kHalo, kPH = kSH + kHalo;
 
-// Column pass (ssim.cpp:42-48) and the per-window terms of ssim_with_grad (ssim.cpp:128-145).
-__global__ void __launch_bounds__(kThreads) k_ssim_windows(ColorLossParams p) {
+__global__ void __launch_bounds__(kThreads) k_ssim_stats(ColorLossParams p) {
+    __shared__ double pa[kPH][kPW], pb[kPH][kPW];
+    __shared__ double hs[5][kPH][kSW];
     const int ow = p.w - kHalo, oh = p.h - kHalo;
-    const int64_t plane_r = static_cast<int64_t>(p.h) * ow, plane_w = static_cast<int64_t>(oh) * ow;
-    const int64_t total = 3 * plane_w;
+    const int64_t plane_w = static_cast<int64_t>(oh) * ow;
+    const int tx = (ow + kSW - 1) / kSW, ty = (oh + kSH - 1) / kSH;
+    const int ntiles = 3 * tx * ty;
     double v[1] = {0.0};
-    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < total;
-         t += static_cast<int64_t>(gridDim.x) * kThreads) {
-        const int c = static_cast<int>(t / plane_w);
-        const int64_t r = t - c * plane_w;
-        const int wy = static_cast<int>(r / ow), wx = static_cast<int>(r - static_cast<int64_t>(wy) * ow);
-        double s[5];
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int c = tile / (tx * ty);
+        const int t2 = tile - c * tx * ty;
+        const int wx0 = (t2 % tx) * kSW, wy0 = (t2 / tx) * kSH;
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPH * kPW; e += kThreads) {
+            const int ey = e / kPW, ex = e - ey * kPW;
+            const int x = wx0 + ex, y = wy0 + ey;
+            double va = 0.0, vb = 0.0;
+            if (x < p.w && y < p.h) {
+                const int64_t q = (static_cast<int64_t>(y) * p.w + x) * 3 + c;
+                va = p.color[q];
+                vb = static_cast<double>(p.gt_color[q]);
+            }
+            pa[ey][ex] = va;
+            pb[ey][ex] = vb;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < kPH * kSW; e += kThreads) {  // row pass (ssim.cpp:36-41)
+            const int ey = e / kSW, ex = e - ey * kSW;
+            double sa = 0.0, sb = 0.0, saa = 0.0, sbb = 0.0, sab = 0.0;
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
-            const double* src = p.rows + (m * 3 + c) * plane_r + wx;
+            for (int i = 0; i < kSsimWin; ++i) {
+                const double va = pa[ey][ex + i], vb = pb[ey][ex + i], kw = p.kern[i];
+                sa += kw * va;
+                sb += kw * vb;
+                saa += kw * (va * va);
+                sbb += kw * (vb * vb);
+                sab += kw * (va * vb);
+            }
+            hs[0][ey][ex] = sa;
+            hs[1][ey][ex] = sb;
+            hs[2][ey][ex] = saa;
+            hs[3][ey][ex] = sbb;
+            hs[4][ey][ex] = sab;
+        }
+        __syncthreads();
+        const int lx = threadIdx.x % kSW, ly = threadIdx.x / kSW;
+        const int wx = wx0 + lx, wy = wy0 + ly;
+        if (wx >= ow || wy >= oh) continue;
+        double st[5];
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {  // column pass (ssim.cpp:42-48)
             double acc = 0.0;
 #pragma unroll
-            for (int i = 0; i < kSsimWin; ++i) acc += p.kern[i] * src[static_cast<int64_t>(wy + i) * ow];
-            s[m] = acc;
+            for (int i = 0; i < kSsimWin; ++i) acc += p.kern[i] * hs[m][ly + i][lx];
+            st[m] = acc;
         }
-        const double mu_a = s[0], mu_b = s[1];
-        const double var_a = s[2] - mu_a * mu_a;
-        const double var_b = s[3] - mu_b * mu_b;
-        const double cov = s[4] - mu_a * mu_b;
+        const double mu_a = st[0], mu_b = st[1];
+        const double var_a = st[2] - mu_a * mu_a;
+        const double var_b = st[3] - mu_b * mu_b;
+        const double cov = st[4] - mu_a * mu_b;
         const double a1 = 2.0 * mu_a * mu_b + kC1;
         const double a2 = 2.0 * cov + kC2;
         const double b1 = mu_a * mu_a + mu_b * mu_b + kC1;
@@ -129,11 +139,11 @@ __global__ void __launch_bounds__(kThreads) k_ssim_windows(ColorLossParams p) {
         const double d_mu = 2.0 * (mu_b * a2 * b1 - mu_a * a1 * a2) / (b1 * b1 * b2);
         const double d_var = -a1 * a2 / (b1 * b2 * b2);
         const double d_cov = 2.0 * a1 / (b1 * b2);
-        double* o = p.win + c * plane_w + r;
+        double* o = p.win + c * plane_w + static_cast<int64_t>(wy) * ow + wx;
         o[0] = mu_a;
         o[3 * plane_w] = mu_b;
         o[6 * plane_w] = d_mu;
-        o[9 * plane_w] = d_var;
+        o[9 * plane_w] = d_var * 2.0;  // the reference's (d_var * 2.0), exact
         o[12 * plane_w] = d_cov;
     }
     block_sum_store<1>(v, p.partial + blockIdx.x * kLossSlots + kSsimSum);
@@ -142,74 +152,102 @@ __global__ void __launch_bounds__(kThreads) k_ssim_windows(ColorLossParams p) {
 // Per pixel: colour L1 (losses.cpp:36-46), the D-SSIM gradient gathered over every window that
 // covers the pixel in the reference's (wy, wx) accumulation order (ssim.cpp:147-154), the
 // colour-gradient mix (losses.cpp:50-58), depth L1 (losses.cpp:64-80) and the lambda folds
-// (losses.cpp:128-130).  16x16 pixel tiles; the 26x26 windows they need are staged in smem.
+// (losses.cpp:128-130).  Each thread owns a 1 x 4 pixel column of a 16 x 64 tile, so one
+// shared-memory window read serves up to four pixels; (inv_count * wgt) comes from a 11 x 11
+// table computed like the reference's product.
+constexpr int kCX = 16, kCY = 64, kCR = 4;
+constexpr int kCWX = kCX + kHalo, kCWY = kCY + kHalo;
+constexpr size_t kColorSmem = (5 * kCWY * kCWX + kSsimWin * kSsimWin) * sizeof(double);
+
 __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
-    __shared__ double sw[5][kWinTile][kWinTile];
+    extern __shared__ double smem[];
+    double* sw = smem;                        // [5][kCWY][kCWX]
+    double* tw = smem + 5 * kCWY * kCWX;      // [11][11] inv_count * (kern[ky] * kern[kx])
     const int ow = p.w - kHalo, oh = p.h - kHalo;
     const int64_t plane_w = static_cast<int64_t>(oh > 0 ? oh : 0) * (ow > 0 ? ow : 0);
-    const int tx = (p.w + kTile - 1) / kTile, ty = (p.h + kTile - 1) / kTile;
-    const int lx = threadIdx.x & (kTile - 1), ly = threadIdx.x / kTile;
+    const int tx = (p.w + kCX - 1) / kCX, ty = (p.h + kCY - 1) / kCY;
+    const int lx = threadIdx.x % kCX, lr = threadIdx.x / kCX;
     const double scale = -0.5 * p.lambda1;
     const double fold_d = p.lambda_geo * p.lambda2;
+    for (int e = threadIdx.x; e < kSsimWin * kSsimWin; e += kThreads)
+        tw[e] = p.inv_count * (p.kern[e / kSsimWin] * p.kern[e % kSsimWin]);
     double v[2] = {0.0, 0.0};
     for (int tile = blockIdx.x; tile < tx * ty; tile += gridDim.x) {
-        const int x0 = (tile % tx) * kTile, y0 = (tile / tx) * kTile;
-        const int x = x0 + lx, y = y0 + ly;
-        const bool in = x < p.w && y < p.h;
-        const int64_t px = static_cast<int64_t>(y) * p.w + x;
-        double g[3] = {0.0, 0.0, 0.0};
-        for (int c = 0; c < 3; ++c) {
-            if (p.use_ssim) {
+        const int x0 = (tile % tx) * kCX, y0 = (tile / tx) * kCY;
+        const int x = x0 + lx, ys = y0 + lr * kCR;
+        double g[3][kCR];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int j = 0; j < kCR; ++j) g[c][j] = 0.0;
+        if (p.use_ssim) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
                 __syncthreads();
-                for (int e = threadIdx.x; e < kWinTile * kWinTile; e += kThreads) {
-                    const int ey = e / kWinTile, ex = e - ey * kWinTile;
+                for (int e = threadIdx.x; e < kCWY * kCWX; e += kThreads) {
+                    const int ey = e / kCWX, ex = e - ey * kCWX;
                     const int wy = y0 - kHalo + ey, wx = x0 - kHalo + ex;
                     if (wy >= 0 && wy < oh && wx >= 0 && wx < ow) {
                         const double* src = p.win + c * plane_w + static_cast<int64_t>(wy) * ow + wx;
 #pragma unroll
-                        for (int m = 0; m < 5; ++m) sw[m][ey][ex] = src[m * 3 * plane_w];
+                        for (int m = 0; m < 5; ++m) sw[(m * kCWY + ey) * kCWX + ex] = src[m * 3 * plane_w];
                     }
                 }
                 __syncthreads();
-                if (in) {
-                    const double av = p.color[px * 3 + c], bv = static_cast<double>(p.gt_color[px * 3 + c]);
-                    const int wy_lo = max(0, y - kHalo), wy_hi = min(oh - 1, y);
-                    const int wx_lo = max(0, x - kHalo), wx_hi = min(ow - 1, x);
-                    double acc = 0.0;
-                    for (int wy = wy_lo; wy <= wy_hi; ++wy) {
-                        const int ey = wy - (y0 - kHalo);
-                        const double ky = p.kern[y - wy];
-                        for (int wx = wx_lo; wx <= wx_hi; ++wx) {
-                            const int ex = wx - (x0 - kHalo);
-                            const double wgt = ky * p.kern[x - wx];
-                            acc += p.inv_count * wgt *
-                                   (sw[2][ey][ex] + sw[3][ey][ex] * 2.0 * (av - sw[0][ey][ex]) +
-                                    sw[4][ey][ex] * (bv - sw[1][ey][ex]));
+                if (x >= p.w) continue;
+                double av[kCR], bv[kCR];
+#pragma unroll
+                for (int j = 0; j < kCR; ++j) {
+                    const int y = min(ys + j, p.h - 1);
+                    const int64_t q = (static_cast<int64_t>(y) * p.w + x) * 3 + c;
+                    av[j] = p.color[q];
+                    bv[j] = static_cast<double>(p.gt_color[q]);
+                }
+                const int wy_lo = max(0, ys - kHalo), wy_hi = min(oh - 1, ys + kCR - 1);
+                for (int wy = wy_lo; wy <= wy_hi; ++wy) {
+                    const int ey = wy - (y0 - kHalo);
+                    for (int kx = kHalo; kx >= 0; --kx) {  // wx = x - kx ascending
+                        const int wx = x - kx;
+                        if (wx < 0 || wx >= ow) continue;
+                        const int ex = wx - (x0 - kHalo);
+                        const double* wp = sw + ey * kCWX + ex;
+                        const double mu_a = wp[0], mu_b = wp[kCWY * kCWX], d_mu = wp[2 * kCWY * kCWX];
+                        const double dv2 = wp[3 * kCWY * kCWX], d_cov = wp[4 * kCWY * kCWX];
+#pragma unroll
+                        for (int j = 0; j < kCR; ++j) {
+                            const int ky = ys + j - wy;
+                            if (ky < 0 || ky > kHalo) continue;
+                            g[c][j] += tw[ky * kSsimWin + kx] * (d_mu + dv2 * (av[j] - mu_a) + d_cov * (bv[j] - mu_b));
                         }
                     }
-                    g[c] = acc;
                 }
             }
         }
-        if (!in) continue;
+        if (x >= p.w) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double diff = p.color[px * 3 + c] - static_cast<double>(p.gt_color[px * 3 + c]);
-            v[0] += fmax(fabs(diff) - p.deadband, 0.0);
-            double gc = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_color_n;
-            if (p.use_ssim) gc = (1.0 - p.lambda1) * gc + scale * g[c];
-            p.grad_color[px * 3 + c] = gc * p.lambda_geo;
-        }
-        double gd = 0.0;
-        if (p.use_depth) {
-            const float t = p.gt_depth[px];
-            if (t > 0.0f) {
-                const double diff = p.depth[px] - static_cast<double>(t);
-                v[1] += fmax(fabs(diff) - p.deadband, 0.0);
-                gd = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_depth_n;
+        for (int j = 0; j < kCR; ++j) {
+            const int y = ys + j;
+            if (y >= p.h) break;
+            const int64_t px = static_cast<int64_t>(y) * p.w + x;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double diff = p.color[px * 3 + c] - static_cast<double>(p.gt_color[px * 3 + c]);
+                v[0] += fmax(fabs(diff) - p.deadband, 0.0);
+                double gc = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_color_n;
+                if (p.use_ssim) gc = (1.0 - p.lambda1) * gc + scale * g[c][j];
+                p.grad_color[px * 3 + c] = gc * p.lambda_geo;
             }
+            double gd = 0.0;
+            if (p.use_depth) {
+                const float t = p.gt_depth[px];
+                if (t > 0.0f) {
+                    const double diff = p.depth[px] - static_cast<double>(t);
+                    v[1] += fmax(fabs(diff) - p.deadband, 0.0);
+                    gd = (fabs(diff) > p.deadband ? sgn(diff) : 0.0) * p.inv_depth_n;
+                }
+            }
+            p.grad_depth[px] = gd * fold_d;
         }
-        p.grad_depth[px] = gd * fold_d;
     }
     block_sum_store<2>(v, p.partial + blockIdx.x * kLossSlots + kL1Color);
 }
@@ -268,6 +306,17 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
         }
         const int cmax = max(c[0], c[1]);
         for (int base = 0; base < d4; base += 128) {
+            // keyframe rows first: their loads overlap the Top-K row gather below
+            float4 gt[2][4];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float4* grow = reinterpret_cast<const float4*>(p.gt + px[u] * D);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    gt[u][m] = (c[u] > 0 && q < d4) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
             float4 acc[2][4];
 #pragma unroll
             for (int u = 0; u < 2; ++u)
@@ -291,18 +340,17 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (!in[u]) continue;
-                const float4* grow = reinterpret_cast<const float4*>(p.gt + px[u] * D);
                 uint32_t* srow = p.signs + px[u] * wpp;
+                float sabs = 0.0f;
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int q = base + m * 32 + lane;
                     uint32_t byte = 0;
                     if (c[u] > 0 && q < d4) {
-                        const float4 t = __ldcs(grow + q);
+                        const float4 t = gt[u][m];
                         const float dx = acc[u][m].x - t.x, dy = acc[u][m].y - t.y;
                         const float dz = acc[u][m].z - t.z, dw = acc[u][m].w - t.w;
-                        v[0] += static_cast<double>(fabsf(dx)) + static_cast<double>(fabsf(dy)) +
-                                static_cast<double>(fabsf(dz)) + static_cast<double>(fabsf(dw));
+                        sabs += (fabsf(dx) + fabsf(dy)) + (fabsf(dz) + fabsf(dw));
                         byte = sign_bits(dx) | (sign_bits(dy) << 2) | (sign_bits(dz) << 4) | (sign_bits(dw) << 6);
                     }
                     uint32_t word = byte << (8 * (lane & 3));
@@ -310,6 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
                     word |= __shfl_xor_sync(0xffffffffu, word, 2);
                     if ((lane & 3) == 0 && q < d4) srow[q >> 2] = word;
                 }
+                v[0] += static_cast<double>(sabs);
             }
         }
     }
@@ -401,14 +450,20 @@ __global__ void k_topk_stats(const int32_t* __restrict__ index, const uint8_t* _
 }
 
 // ---------------------------------------------------------------- feature backward + Adam
-__device__ __forceinline__ float sgnbit(uint32_t bits, int sh) {
-    return static_cast<float>((bits >> sh) & 1u) - static_cast<float>((bits >> (sh + 1)) & 1u);
+// w * sign for the 2-bit code at bit `sh` (01 = +1, 10 = -1, 00 = 0): selects, no conversions.
+__device__ __forceinline__ float signed_w(uint32_t bits, int sh, float w) {
+    float t = (bits >> sh) & 1u ? w : 0.0f;
+    return (bits >> (sh + 1)) & 1u ? -w : t;
 }
 
+// adam_step (optimizer.cpp:57-61) in fp32 with the bias corrections as host reciprocals and a
+// reciprocal-sqrt / fast-divide epilogue (the fp32 feature path's stated tolerance).
 __device__ __forceinline__ float adam1(float g, float& m, float& v, float f, const FeatAdamParams& p) {
-    m = p.beta1 * m + (1.0f - p.beta1) * g;                                   // optimizer.cpp:57-61
-    v = p.beta2 * v + (1.0f - p.beta2) * g * g;
-    return f - p.lr * (m / p.bc1) / (sqrtf(v / p.bc2) + p.eps);
+    m = fmaf(p.beta1, m, p.one_m_beta1 * g);
+    v = fmaf(p.beta2, v, p.one_m_beta2 * g * g);
+    const float mhat = m * p.inv_bc1, vhat = v * p.inv_bc2;
+    const float den = vhat * rsqrtf(fmaxf(vhat, 1e-30f)) + p.eps;
+    return f - __fdividef(p.lr * mhat, den);
 }
 
 __device__ __forceinline__ float warp_sum(float s) {
@@ -425,14 +480,25 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
     const float scale = *p.scale;
+    const uint32_t* __restrict__ signs = p.signs;
     for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
         const int r0 = p.seg[g], r1 = p.seg[g + 1];
-        float4* frow = reinterpret_cast<float4*>(p.feat + g * D);
-        float4* mrow = reinterpret_cast<float4*>(p.m + g * D);
-        float4* vrow = reinterpret_cast<float4*>(p.v + g * D);
+        float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
+        float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
+        float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
         float ss = 0.0f;
-        float4 keep[4];
+        float4 fk[4], mk[4], vk[4];
         for (int base = 0; base < d4; base += 128) {
+            // the row's parameter / moment loads go out first and overlap the record sweep
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q < d4) {
+                    fk[m] = __ldcs(frow + q);
+                    mk[m] = __ldcs(mrow + q);
+                    vk[m] = __ldcs(vrow + q);
+                }
+            }
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -448,7 +514,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
                 for (int j = 0; j < nr; ++j) {
                     const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
                     const float wj = __shfl_sync(0xffffffffu, sw, j);
-                    const uint32_t* srow = p.signs + pxj * wpp;
+                    const uint32_t* srow = signs + pxj * wpp;
                     if (!isfinite(wj)) {  // backward.cpp:296-302: all-zero gradient rows are skipped
                         bool any = false;
                         for (int q = lane; q < wpp; q += 32) any |= srow[q] != 0u;
@@ -459,10 +525,10 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
                         const int q = base + m * 32 + lane;
                         if (q < d4) {
                             const uint32_t b = __ldg(srow + (q >> 2)) >> (8 * (q & 3));
-                            acc[m].x = fmaf(wj, sgnbit(b, 0), acc[m].x);
-                            acc[m].y = fmaf(wj, sgnbit(b, 2), acc[m].y);
-                            acc[m].z = fmaf(wj, sgnbit(b, 4), acc[m].z);
-                            acc[m].w = fmaf(wj, sgnbit(b, 6), acc[m].w);
+                            acc[m].x += signed_w(b, 0, wj);
+                            acc[m].y += signed_w(b, 2, wj);
+                            acc[m].z += signed_w(b, 4, wj);
+                            acc[m].w += signed_w(b, 6, wj);
                         }
                     }
                 }
@@ -471,7 +537,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
             for (int m = 0; m < 4; ++m) {
                 const int q = base + m * 32 + lane;
                 if (q >= d4) continue;
-                float4 f = frow[q], mm = mrow[q], vv = vrow[q];
+                float4 f = fk[m], mm = mk[m], vv = vk[m];
                 f.x = adam1(acc[m].x * scale, mm.x, vv.x, f.x, p);
                 f.y = adam1(acc[m].y * scale, mm.y, vv.y, f.y, p);
                 f.z = adam1(acc[m].z * scale, mm.z, vv.z, f.z, p);
@@ -479,28 +545,29 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
                 __stcs(mrow + q, mm);
                 __stcs(vrow + q, vv);
                 ss += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
-                if (d4 <= 128) keep[m] = f;
-                else frow[q] = f;
+                fk[m] = f;
+                if (d4 > 128) frow[q] = f;
             }
         }
-        const float norm = sqrtf(warp_sum(ss));
-        const float inv = norm > 1e-12f ? 1.0f / norm : 1.0f;
+        const float ssum = warp_sum(ss);
+        const bool renorm = ssum > 1e-24f;  // norm > 1e-12 (mapper.cpp:249)
+        const float inv = renorm ? rsqrtf(ssum) : 1.0f;
         if (d4 <= 128) {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int q = m * 32 + lane;
                 if (q < d4) {
-                    float4 f = keep[m];
-                    if (norm > 1e-12f) {
+                    float4 f = fk[m];
+                    if (renorm) {
                         f.x *= inv;
                         f.y *= inv;
                         f.z *= inv;
                         f.w *= inv;
                     }
-                    frow[q] = f;
+                    __stcs(frow + q, f);
                 }
             }
-        } else if (norm > 1e-12f) {
+        } else if (renorm) {
             for (int q = lane; q < d4; q += 32) {
                 float4 f = frow[q];
                 f.x *= inv;
@@ -535,7 +602,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams
                     for (int t = lane; t < wpp; t += 32) any |= srow[t] != 0u;
                     if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
                 }
-                if (q < D) acc = fmaf(wj, sgnbit(srow[q >> 4], 2 * (q & 15)), acc);
+                if (q < D) acc += signed_w(srow[q >> 4], 2 * (q & 15), wj);
             }
             if (q < D) {
                 float mm = p.m[g * D + q], vv = p.v[g * D + q];
@@ -573,14 +640,18 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launc
     if (P <= 0) return;
     if (p.use_ssim) {
         const int ow = p.w - kHalo, oh = p.h - kHalo;
-        k_ssim_rows<<<capped_grid(3LL * p.h * ow, kThreads, 148 * 16), kThreads, 0, st>>>(p);
-        dbg_launch("k_ssim_rows", st);
-        k_ssim_windows<<<capped_grid(3LL * oh * ow, kThreads, kLossBlocks), kThreads, 0, st>>>(p);
-        dbg_launch("k_ssim_windows", st);
-        *launches += 2;
+        const int64_t tiles = 3LL * ((ow + kSW - 1) / kSW) * ((oh + kSH - 1) / kSH);
+        k_ssim_stats<<<capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st>>>(p);
+        dbg_launch("k_ssim_stats", st);
+        *launches += 1;
     }
-    const int64_t tiles = static_cast<int64_t>((p.w + kTile - 1) / kTile) * ((p.h + kTile - 1) / kTile);
-    k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st>>>(p);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_color_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kColorSmem));
+        configured = true;
+    }
+    const int64_t tiles = static_cast<int64_t>((p.w + kCX - 1) / kCX) * ((p.h + kCY - 1) / kCY);
+    k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, kColorSmem, st>>>(p);
     dbg_launch("k_color_loss", st);
     *launches += 1;
 }

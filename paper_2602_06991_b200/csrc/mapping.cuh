@@ -24,8 +24,7 @@ struct ColorLossParams {
     int use_depth;           // depth_n > 0 and lambda2 != 0
     double inv_color_n, inv_depth_n, inv_count;
     double kern[kSsimWin];   // gaussian_kernel() of ssim.cpp:18-28 (host-computed)
-    double* rows;            // 5 x 3 x H x OW   horizontal pass
-    double* win;             // 5 x 3 x OH x OW  per window: mu_a, mu_b, d_mu, d_var, d_cov
+    double* win;             // 5 x 3 x OH x OW  per window: mu_a, mu_b, d_mu, 2 d_var, d_cov
     double* grad_color;      // H x W x 3 (final, lambda_geo folded)
     double* grad_depth;      // H x W
     double* partial;         // kLossBlocks x kLossSlots
@@ -64,7 +63,7 @@ struct FeatAdamParams {
     float* feat;             // N x D, updated in place
     float* m;
     float* v;
-    float lr, beta1, beta2, eps, bc1, bc2;
+    float lr, beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bc1, inv_bc2;
 };
 
 void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int64_t* depth_n_out,

@@ -1410,7 +1410,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 }
                 for (double& v : lp.kern) v /= sum;
                 if (use_ssim) {
-                    lp.rows = ensure<double>(c->ssim_rows, 15LL * f.height * ow);
                     lp.win = ensure<double>(c->ssim_win, 15LL * oh * ow);
                 }
             }
@@ -1488,8 +1487,21 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ga.max_log_scale = cfg->max_log_scale;
             ga.contrib = ptr<unsigned long long>(c->o_contrib);
             ga.max_contrib = ptr<double>(c->stat_maxc);
-            tk::launch_chain_adam(chain_params(c, &kf.pose, cam, s, mid), ga, st);
-            c->launches += n > 0;
+            tk::ChainParams cp = chain_params(c, &kf.pose, cam, s, mid);
+            cp.g_mean = ensure<double>(c->gg_mean, n * 3);
+            cp.g_log_scale = ensure<double>(c->gg_ls, n * 3);
+            cp.g_rotation = ensure<double>(c->gg_rot, n * 4);
+            cp.g_opacity_logit = ensure<double>(c->gg_op, n);
+            cp.g_color = ensure<double>(c->gg_col, n * 3);
+            cp.twist = nullptr;
+            tk::launch_chain(cp, st);
+            ga.g[0] = cp.g_mean;
+            ga.g[1] = cp.g_log_scale;
+            ga.g[2] = cp.g_rotation;
+            ga.g[3] = cp.g_opacity_logit;
+            ga.g[4] = cp.g_color;
+            tk::launch_geo_adam(ga, n, st);
+            c->launches += n > 0 ? 2 : 0;
             CK_LAUNCH(c);
             if (feature_step && d > 0) {  // mapper.cpp:239-252
                 c->step_feat += 1;
@@ -1517,8 +1529,10 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fa.beta1 = static_cast<float>(cfg->beta1);
                 fa.beta2 = static_cast<float>(cfg->beta2);
                 fa.eps = static_cast<float>(cfg->eps);
-                fa.bc1 = static_cast<float>(1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat)));
-                fa.bc2 = static_cast<float>(1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat)));
+                fa.one_m_beta1 = static_cast<float>(1.0 - cfg->beta1);
+                fa.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
+                fa.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat))));
+                fa.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat))));
                 tk::launch_feature_adam(fa, st);
                 c->launches += n > 0;
                 CK_LAUNCH(c);
