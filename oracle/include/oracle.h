@@ -167,6 +167,19 @@ int orc_update_contribution_stats(orc_map* m, uint64_t generation, int64_t map_s
                                   int32_t k, const int32_t* index, const uint8_t* count,
                                   const double* contributions);
 
+/* insert_gaussians (mapper.cpp:19-60): SoA source points (feature n x d_src or NULL). */
+int orc_insert_gaussians(orc_map* m, orc_opt* o, int64_t n_src, const double* position, const double* color,
+                         const double* feature, int32_t d_src, const double* spacing, const double* distance,
+                         double tau, const orc_pose* world_to_camera);
+/* prune_map (mapper.cpp:80-160) + OptimizerState::compact; returns the number removed. */
+int64_t orc_prune_map(orc_map* m, orc_opt* o, double keep_ratio, uint64_t seed, int32_t threshold,
+                      int32_t* removed_out);
+int64_t orc_map_size(const orc_map* m);
+double* orc_opt_moments(orc_opt* o, int32_t group, int32_t which, int64_t* count);
+uint64_t orc_map_generation(const orc_map* m);
+int32_t orc_map_feature_dim(const orc_map* m);
+void orc_map_set_stats(orc_map* m, const int32_t* topk_count, const double* max_contribution);
+
 /* Map parameters and selection statistics back out in SoA form (any pointer may be NULL). */
 void orc_map_export(const orc_map* m, double* mean, double* log_scale, double* rotation,
                     double* opacity_logit, double* color, double* feature, int32_t* topk_count,

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>

@@ -76,6 +76,19 @@ def lib():
         L.orc_compute_losses.argtypes = [C.c_int32, C.c_int32, C.c_int32] + [vp] * 8 + [C.c_int32] + [vp] * 4
         L.orc_optimize_step.argtypes = [vp] * 9 + [C.c_int64, vp, vp]
         L.orc_map_export.argtypes = [vp] * 9
+        L.orc_insert_gaussians.restype = C.c_int
+        L.orc_insert_gaussians.argtypes = [vp, vp, C.c_int64, vp, vp, vp, C.c_int32, vp, vp, C.c_double, vp]
+        L.orc_prune_map.restype = C.c_int64
+        L.orc_prune_map.argtypes = [vp, vp, C.c_double, C.c_uint64, C.c_int32, vp]
+        L.orc_map_size.restype = C.c_int64
+        L.orc_map_size.argtypes = [vp]
+        L.orc_map_generation.restype = C.c_uint64
+        L.orc_map_generation.argtypes = [vp]
+        L.orc_map_feature_dim.restype = C.c_int32
+        L.orc_map_feature_dim.argtypes = [vp]
+        L.orc_map_set_stats.argtypes = [vp, vp, vp]
+        L.orc_opt_moments.restype = C.POINTER(C.c_double)
+        L.orc_opt_moments.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]
         L.orc_update_contribution_stats.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                                     vp, vp, vp]
         _lib = L
@@ -306,8 +319,43 @@ class OracleMapper:
         if rc:
             raise RuntimeError(lib().orc_last_error().decode())
 
+    def size(self):
+        return int(lib().orc_map_size(self.map.h))
+
+    def generation(self):
+        return int(lib().orc_map_generation(self.map.h))
+
+    def set_stats(self, topk_count, max_contribution):
+        lib().orc_map_set_stats(self.map.h, _p(np.ascontiguousarray(topk_count, np.int32)),
+                                _p(np.ascontiguousarray(max_contribution, np.float64)))
+
+    def moments(self, group, which=0):
+        cnt = C.c_int64()
+        ptr = lib().orc_opt_moments(self.opt, group, which, C.byref(cnt))
+        return np.ctypeslib.as_array(ptr, shape=(cnt.value,)) if cnt.value else np.zeros(0)
+
+    def insert(self, position, color, feature, spacing, distance, tau, pose):
+        """insert_gaussians (mapper.cpp:19-60); returns the number inserted."""
+        pos = np.ascontiguousarray(position, np.float64)
+        f = None if feature is None else np.ascontiguousarray(feature, np.float64)
+        d_src = 0 if f is None else f.shape[1]
+        n = lib().orc_insert_gaussians(self.map.h, self.opt, pos.shape[0], _p(pos),
+                                       _p(np.ascontiguousarray(color, np.float64)), _p(f), d_src,
+                                       _p(np.ascontiguousarray(spacing, np.float64)),
+                                       _p(np.ascontiguousarray(distance, np.float64)), tau, C.byref(pose_c(pose)))
+        self.n = self.size()
+        self.d = int(lib().orc_map_feature_dim(self.map.h))
+        return n
+
+    def prune(self, keep_ratio, seed, threshold):
+        """prune_map (mapper.cpp:80-160); returns the removed indices."""
+        out = np.zeros(max(1, self.size()), np.int32)
+        k = lib().orc_prune_map(self.map.h, self.opt, keep_ratio, seed, threshold, _p(out))
+        self.n = self.size()
+        return out[:k].copy()
+
     def export(self):
-        n, d = self.n, self.d
+        n, d = self.size(), self.d
         o = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
                  opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d)),
                  topk_count=np.zeros(n, np.int32), max_contribution=np.zeros(n))

@@ -178,3 +178,110 @@ def test_single_gaussian_fits_its_keyframe():  # test_mapper.cpp:393-415
     assert abs(np.linalg.norm(e["feature"][0]) - 1.0) < 1e-6
     assert np.linalg.norm(e["rotation"][0]) == pytest.approx(1.0, rel=1e-9)
     assert e["color"].max() <= 1.0 and e["color"].min() >= 0.0
+
+
+# ---- insertion and pruning (test_mapper.cpp:84-122, 160-268, 417-441)
+INF = float("inf")
+
+
+def simple_sources(n, d):  # test_mapper.cpp:17-27
+    pos = np.array([[0.1 * i, 0.0, 1.0 + 0.1 * i] for i in range(n)])
+    col = np.full((n, 3), 0.5)
+    feat = np.zeros((n, d))
+    feat[np.arange(n), np.arange(n) % d] = 1.0
+    return pos, col, feat, np.full(n, 0.05)
+
+
+def empty_mapper(d=0):
+    m = SceneMap(mean=np.zeros((0, 3)), log_scale=np.zeros((0, 3)), rotation=np.zeros((0, 4)),
+                 opacity_logit=np.zeros(0), color=np.zeros((0, 3)), feature=np.zeros((0, d)), feature_dim=d)
+    return O.OracleMapper(m, MapperConfig())
+
+
+def test_insertion_keeps_only_far_enough_points():
+    pos, col, feat, sp = simple_sources(3, 4)
+    om = empty_mapper()
+    assert om.insert(pos, col, feat, sp, [0.01, 0.02, 0.03], 0.05, Pose()) == 0
+    assert om.size() == 0 and om.generation() == 0
+    om = empty_mapper()
+    assert om.insert(pos, col, feat, sp, [INF] * 3, 0.05, Pose()) == 3
+    assert om.size() == 3 and om.generation() == 1 and om.moments(0).size == 9
+    e = om.export()
+    assert np.allclose(1.0 / (1.0 + np.exp(-e["opacity_logit"])), 0.5)
+    assert np.all(np.abs(np.linalg.norm(e["feature"], axis=1) - 1.0) < 1e-9)
+    om = empty_mapper()
+    assert om.insert(pos, col, feat, sp, [0.01, 0.2, 0.07], 0.05, Pose()) == 2
+    e = om.export()
+    assert np.linalg.norm(e["mean"][0] - pos[1]) < 1e-12 and np.linalg.norm(e["mean"][1] - pos[2]) < 1e-12
+    om = empty_mapper()
+    p1, c1, f1, s1 = simple_sources(1, 4)
+    assert om.insert(p1, c1, f1, s1, [INF], 0.05, Pose(translation=np.array([-1.0, 0.0, 0.0]))) == 1
+    assert np.linalg.norm(om.export()["mean"][0] - [1.0, 0.0, 1.0]) < 1e-12
+
+
+def prune_case(counts, maxc, keep, seed, thr=0):
+    om = O.OracleMapper(stats_map(len(counts)), MapperConfig())
+    om.set_stats(counts, maxc)
+    return om, om.prune(keep, seed, thr)
+
+
+def test_prune_keeps_non_candidates_untouched():
+    om, removed = prune_case([1, 2, 3, 4], [0.1, 0.2, 0.3, 0.4], 0.5, 7)
+    e = om.export()
+    assert removed.size == 0 and om.size() == 4
+    assert (e["topk_count"] == 0).all() and (e["max_contribution"] == 0).all()
+    om, removed = prune_case([0, 0, 5], [0.0, 0.0, 0.9], 0.5, 7)
+    assert removed.size == 0 and om.size() == 3
+    for seed in range(50):
+        om, removed = prune_case([5, 0, 3, 0], [0.1, 0.2, 0.3, 0.4], 0.5, seed)
+        assert set(removed.tolist()) <= {1, 3} and om.size() == 4 - removed.size
+        assert om.moments(0).size == 3 * om.size()
+
+
+def survival_oracle(scores, keep):  # test_mapper.cpp:32-65, the exact draw-tree marginals
+    n = len(scores)
+    marg = np.zeros(n)
+    stack = [(list(range(n)), 1.0, keep)]
+    while stack:
+        pool, prob, left = stack.pop()
+        if left == 0:
+            continue
+        mass = sum(scores[i] for i in pool)
+        for p, idx in enumerate(pool):
+            pick = scores[idx] / mass if mass > 0 else 1.0 / len(pool)
+            if pick <= 0:
+                continue
+            marg[idx] += prob * pick
+            stack.append((pool[:p] + pool[p + 1:], prob * pick, left - 1))
+    return marg
+
+
+@pytest.mark.parametrize("scores,trials,seed0,tol", [([0.25] * 4, 4000, 1000, 0.03),
+                                                     ([0.9, 0.1, 0.05, 0.0], 6000, 9000, 0.02),
+                                                     ([0.9, 0.0, 0.0, 0.0], 6000, 40000, 0.025)])
+def test_prune_survival_frequencies_match_draw_tree(scores, trials, seed0, tol):  # test_mapper.cpp:199-268
+    marg = survival_oracle(scores, 2)
+    survived = np.zeros(4)
+    for t in range(trials):
+        om, removed = prune_case([0, 0, 0, 0], scores, 0.5, seed0 + t)
+        alive = np.ones(4, bool)
+        alive[removed] = False
+        survived += alive
+    assert np.all(np.abs(survived / trials - marg) < tol)
+
+
+def test_optimizer_state_in_lockstep_through_insert_and_prune():  # test_mapper.cpp:417-441
+    pos, col, feat, sp = simple_sources(6, 4)
+    om = empty_mapper()
+    om.insert(pos, col, feat, sp, [INF] * 6, 0.05, Pose())
+    om.set_stats([3 if i % 2 == 0 else 0 for i in range(6)], [0.1 * (i + 1) for i in range(6)])
+    mom = om.moments(0)
+    for i in range(6):
+        mom[i * 3] = 100.0 + i
+    removed = om.prune(0.5, 5, 0)
+    assert removed.size == 1 and om.moments(0).size == 3 * om.size()
+    e = om.export()
+    mom = om.moments(0)
+    for i in range(om.size()):
+        tag = int(round(mom[i * 3] - 100.0))
+        assert np.linalg.norm(e["mean"][i] - pos[tag]) < 1e-12
