@@ -25,6 +25,9 @@
  *                                  mapper.cpp:162-255): compute_losses (losses.hpp:42-43),
  *                                  adam_step (optimizer.hpp:58-59), update_contribution_stats
  * tk_scene_download                SceneMap parameters + Gaussian3D statistics back to the host
+ * tk_insert_gaussians              insert_gaussians (map/mapper.hpp:41-43, mapper.cpp:19-60)
+ * tk_prune_map                     prune_map + OptimizerState::compact (mapper.hpp:53-54,
+ *                                  mapper.cpp:80-160, optimizer.cpp:9-47)
  *
  * Memory spaces: every buffer argument is tagged TK_HOST or TK_DEVICE.  Host buffers are
  * copied in/out inside the call (pinned memory from tk_host_alloc is fastest); device buffers
@@ -231,6 +234,30 @@ tk_status tk_optimize_step(tk_ctx* ctx, const tk_mapper_config* cfg, const tk_ca
 /* Loss values of the last tk_optimize_step (synchronises). */
 tk_status tk_loss_values(tk_ctx* ctx, double values[3]);
 tk_status tk_scene_download(tk_ctx* ctx, const tk_scene_out* out);
+
+/* ---- structural edits of the resident map (generation bumps, optimiser state in lockstep) ---- */
+typedef struct { /* SourcePoint batch (track/gicp.hpp:18-25), SoA */
+    int64_t n;
+    int32_t d;               /* feature channels of the source points (0: none) */
+    const double* position;  /* n x 3, camera frame */
+    const double* color;     /* n x 3 */
+    const float* feature;    /* n x d, or NULL */
+    const double* spacing;   /* n: local sample spacing (scene units) */
+    const double* distance;  /* n: correspondence distance to the map (inf: none) */
+    int32_t mem;
+} tk_source_view;
+
+tk_status tk_scene_info(tk_ctx* ctx, int64_t* n, int32_t* d, uint64_t* generation);
+/* Inserts one Gaussian per source point with distance >= tau (mapper.cpp:29-52), extends the
+ * optimiser state and statistics with zeros and bumps the generation when any is inserted. */
+tk_status tk_insert_gaussians(tk_ctx* ctx, const tk_source_view* src, double tau_insert,
+                              const tk_pose* world_to_camera, int32_t* inserted);
+/* Two-stage prune on the context's statistics: the draw runs on the host exactly as
+ * mapper.cpp:85-139 (std::mt19937_64(seed)); the map, features and every optimiser group are
+ * compacted in lockstep on the device; statistics restart at zero.  removed_out (host, capacity
+ * n, may be NULL) receives the removed indices in ascending order. */
+tk_status tk_prune_map(tk_ctx* ctx, double keep_ratio, uint64_t seed, int32_t topk_count_threshold,
+                       int32_t* removed_out, int64_t* n_removed);
 
 /* Drop the cached PreparedScene / forward state: the next call re-projects, re-sorts and
  * re-bins (the reference recomputes prepare_scene in every call, render.cpp:295). */

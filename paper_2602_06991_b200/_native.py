@@ -90,6 +90,11 @@ class tk_scene_out(C.Structure):
                 ("topk_count", C.c_void_p), ("max_contribution", C.c_void_p)]
 
 
+class tk_source_view(C.Structure):
+    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("position", C.c_void_p), ("color", C.c_void_p),
+                ("feature", C.c_void_p), ("spacing", C.c_void_p), ("distance", C.c_void_p), ("mem", C.c_int32)]
+
+
 class tk_synth_arrays(C.Structure):
     _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p),
                 ("rotation", C.c_void_p), ("opacity_logit", C.c_void_p), ("color", C.c_void_p),
@@ -144,6 +149,10 @@ RENDER_SYMBOLS = [
                                    C.POINTER(tk_settings), C.c_int32, C.c_int64, dbl_p, i32_p]),
     ("tk_loss_values", C.c_int, [C.c_void_p, dbl_p]),
     ("tk_scene_download", C.c_int, [C.c_void_p, C.POINTER(tk_scene_out)]),
+    ("tk_scene_info", C.c_int, [C.c_void_p, i64_p, i32_p, C.POINTER(C.c_uint64)]),
+    ("tk_insert_gaussians", C.c_int, [C.c_void_p, C.POINTER(tk_source_view), C.c_double, C.POINTER(tk_pose),
+                                      i32_p]),
+    ("tk_prune_map", C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_void_p, i64_p]),
 ]
 
 PHASES = ["prepare", "geom_fwd", "gather", "fbwd_index", "fbwd", "geom_bwd", "chain", "full_blend", "allgather",

@@ -233,6 +233,35 @@ class Renderer:
         return o
 
 
+    def scene_info(self) -> tuple[int, int, int]:
+        n, d, g = C.c_int64(), C.c_int32(), C.c_uint64()
+        N.check(self.lib.tk_scene_info(self.ctx, C.byref(n), C.byref(d), C.byref(g)))
+        return n.value, d.value, g.value
+
+    def insert_gaussians(self, position, color, feature, spacing, distance, tau: float, world_to_camera: Pose) -> int:
+        """insert_gaussians (mapper.cpp:19-60) on the resident map; returns the number inserted."""
+        pos = _c(position, np.float64).reshape(-1, 3)
+        n = pos.shape[0]
+        col = _c(color, np.float64).reshape(n, 3)
+        feat = None if feature is None else _c(feature, np.float32).reshape(n, -1)
+        d = 0 if feat is None else feat.shape[1]
+        sp = _c(spacing, np.float64).reshape(n)
+        dist = _c(distance, np.float64).reshape(n)
+        view = N.tk_source_view(n, d, _p(pos), _p(col), _p(feat), _p(sp), _p(dist), N.TK_HOST)
+        out = C.c_int32()
+        N.check(self.lib.tk_insert_gaussians(self.ctx, C.byref(view), tau, C.byref(to_pose(world_to_camera)),
+                                             C.byref(out)))
+        return out.value
+
+    def prune_map(self, keep_ratio: float, seed: int, threshold: int) -> np.ndarray:
+        """prune_map (mapper.cpp:80-160); returns the removed indices (ascending)."""
+        n = self.scene_info()[0]
+        out = np.zeros(max(n, 1), np.int32)
+        k = C.c_int64()
+        N.check(self.lib.tk_prune_map(self.ctx, keep_ratio, seed & ((1 << 64) - 1), threshold, _p(out), C.byref(k)))
+        return out[:k.value].copy()
+
+
 class MT19937_64:
     """std::mt19937_64 (the reference mapper's keyframe sampler, mapper.cpp:167)."""
 
@@ -269,8 +298,8 @@ class MT19937_64:
 
 class Mapper:
     """The mapping loop of map/mapper.cpp over a device-resident map: keyframes live in HBM, each
-    optimize_step samples one with ``rng() % len(keyframes)`` (mapper.cpp:167) and runs render,
-    losses, backward and Adam on the GPU.  Pruning / insertion stay with the caller."""
+    optimize_step samples one with ``rng() % len(keyframes)`` (mapper.cpp:167), runs render,
+    losses, backward and Adam on the GPU and prunes on schedule (mapper.cpp:256-260)."""
 
     def __init__(self, renderer: Renderer, m: SceneMap, cfg: MapperConfig, cam: CameraIntrinsics,
                  settings: RenderSettings | None = None):
@@ -291,8 +320,20 @@ class Mapper:
             raise RuntimeError("optimize_step: no keyframes")
         slot = rng() % self.n_keyframes
         vals, fstep = self.r.optimize_step(self.cfg, self.cam, self.settings, slot, iteration, fetch)
-        return dict(iteration=iteration, losses=vals, feature_step=fstep, keyframe=slot, pruned=0,
+        pruned = 0
+        c = self.cfg
+        if c.pruning and c.prune_period > 0 and iteration > 0 and iteration % c.prune_period == 0:
+            pruned = len(self.r.prune_map(c.prune_keep_ratio, rng(), c.topk_count_threshold))
+            self.n, self.d, _ = self.r.scene_info()
+        return dict(iteration=iteration, losses=vals, feature_step=fstep, keyframe=slot, pruned=pruned,
                     gaussian_count=self.n)
+
+    def insert(self, position, color, feature, spacing, distance, world_to_camera: Pose) -> int:
+        """insert_gaussians with the config's tau_insert; the optimiser state extends in lockstep."""
+        k = self.r.insert_gaussians(position, color, feature, spacing, distance, self.cfg.tau_insert,
+                                    world_to_camera)
+        self.n, self.d, _ = self.r.scene_info()
+        return k
 
     def export(self) -> dict:
         return self.r.scene_download(self.n, self.d)

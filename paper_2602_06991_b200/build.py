@@ -31,6 +31,7 @@ CUDA_UNITS = [
     ("geometric.cu", ["--fmad=false"]),
     ("feature.cu", []),
     ("mapping.cu", ["--fmad=false"]),
+    ("mapedit.cu", ["--fmad=false"]),
     ("tk_abi.cu", []),
 ]
 

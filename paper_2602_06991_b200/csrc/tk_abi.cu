@@ -8,11 +8,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
 #include "feature.cuh"
 #include "geometric.cuh"
+#include "mapedit.cuh"
 #include "mapping.cuh"
 #include "prepare.cuh"
 #include "sort.cuh"
@@ -719,6 +721,103 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     cp.fy = cam->fy;
     cp.dilation = s->cov2d_dilation;
     return cp;
+}
+
+// Grow a device array to new_count elements keeping the first old_count (structural edits).
+template <class T>
+T* grow_keep(tk_ctx* c, DevBuf& b, int64_t old_count, int64_t new_count, bool zero_tail) {
+    const size_t need = static_cast<size_t>(std::max<int64_t>(new_count, 1)) * sizeof(T);
+    if (b.bytes < need) {
+        DevBuf nb;
+        const size_t alloc = tk::align_bytes(need + need / 8);
+        CK(cudaMalloc(&nb.p, alloc));
+        nb.bytes = alloc;
+        if (old_count > 0 && b.p)
+            CK(cudaMemcpyAsync(nb.p, b.p, old_count * sizeof(T), cudaMemcpyDeviceToDevice, c->cur));
+        CK(cudaStreamSynchronize(c->cur));
+        b.release();
+        b = nb;
+    }
+    if (zero_tail && new_count > old_count)
+        CK(cudaMemsetAsync(ptr<T>(b) + old_count, 0, (new_count - old_count) * sizeof(T), c->cur));
+    return ptr<T>(b);
+}
+
+// Keep the rows flagged in keep (n rows of `width` elements) in order, into a fresh buffer.
+template <class T>
+void compact_rows(tk_ctx* c, DevBuf& b, int64_t n, int width, int64_t n_keep, const int32_t* keep,
+                  const int32_t* pos) {
+    if (!b.p || width <= 0) return;
+    DevBuf nb;
+    ensure<T>(nb, std::max<int64_t>(n_keep, 1) * width);
+    if (sizeof(T) == 8)
+        tk::launch_compact_f64(reinterpret_cast<const double*>(b.p), static_cast<double*>(nb.p), keep, pos, n, width,
+                               c->cur);
+    else
+        tk::launch_compact_f32(reinterpret_cast<const float*>(b.p), static_cast<float*>(nb.p), keep, pos, n, width,
+                               c->cur);
+    c->launches += n > 0;
+    CK_LAUNCH(c);
+    CK(cudaStreamSynchronize(c->cur));
+    b.release();
+    b = nb;
+}
+
+// prune_map's candidate draw (mapper.cpp:80-139), host side: candidates have topk_count <=
+// threshold; ceil(keep_ratio * candidates) survive, drawn without replacement proportionally to
+// max_contribution with std::mt19937_64(seed), uniformly once the mass is exhausted.
+std::vector<int32_t> prune_select(const std::vector<int32_t>& counts, const std::vector<double>& maxc,
+                                  double keep_ratio, uint64_t seed, int32_t threshold) {
+    std::vector<int32_t> cand;
+    for (size_t i = 0; i < counts.size(); ++i)
+        if (counts[i] <= threshold) cand.push_back(static_cast<int32_t>(i));
+    std::vector<int32_t> removed;
+    if (cand.empty()) return removed;
+    std::vector<double> score(cand.size());
+    double total = 0.0;
+    for (size_t i = 0; i < cand.size(); ++i) {
+        score[i] = maxc[cand[i]];
+        total += score[i];
+    }
+    if (!(total > 0.0)) return removed;  // survival weights undefined: keep every candidate
+    const size_t keep = static_cast<size_t>(std::ceil(keep_ratio * static_cast<double>(cand.size())));
+    if (keep >= cand.size()) return removed;
+    std::mt19937_64 rng(seed);
+    std::vector<uint8_t> kept(cand.size(), 0);
+    std::vector<size_t> pool(cand.size());
+    for (size_t i = 0; i < pool.size(); ++i) pool[i] = i;
+    double mass = total;
+    for (size_t draw = 0; draw < keep; ++draw) {
+        size_t pick = 0;
+        if (mass > 0.0) {
+            const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53 * mass;  // canonical_unit * mass
+            double acc = 0.0;
+            pick = pool.size() - 1;
+            for (size_t q = 0; q < pool.size(); ++q) {
+                acc += score[pool[q]];
+                if (u < acc) {
+                    pick = q;
+                    break;
+                }
+            }
+        } else {
+            pick = static_cast<size_t>(rng() % pool.size());
+        }
+        const size_t chosen = pool[pick];
+        kept[chosen] = 1;
+        mass -= score[chosen];
+        if (mass < 0.0) mass = 0.0;
+        pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(pick));
+    }
+    for (size_t i = 0; i < cand.size(); ++i)
+        if (!kept[i]) removed.push_back(cand[i]);
+    return removed;
+}
+
+void scene_changed(tk_ctx* c) {
+    c->scene_version += 1;
+    c->prepared = false;
+    c->aux_valid = false;
 }
 
 void require_features(tk_ctx* c) {
@@ -1579,6 +1678,191 @@ tk_status tk_scene_download(tk_ctx* c, const tk_scene_out* o) {
         copy_out(o->topk_count, c->stat_count.p, n * sizeof(int32_t), o->mem, c);
         copy_out(o->max_contribution, c->stat_maxc.p, n * sizeof(double), o->mem, c);
         if (o->mem == TK_HOST) sync(c);
+        main_done(c);
+    });
+}
+
+// ------------------------------------------------------------------ structural edits
+tk_status tk_scene_info(tk_ctx* c, int64_t* n, int32_t* d, uint64_t* generation) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (n) *n = c->n;
+        if (d) *d = c->d;
+        if (generation) *generation = c->generation;
+    });
+}
+
+tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, const tk_pose* w2c,
+                              int32_t* inserted) {
+    return guarded([&] {
+        if (!c || !src || !w2c) fail(TK_ERR_BAD_ARG, "null argument");
+        if (src->n < 0 || src->d < 0) fail(TK_ERR_BAD_ARG, "negative source size");
+        if (src->n > 0 && (!src->position || !src->color || !src->spacing || !src->distance))
+            fail(TK_ERR_BAD_ARG, "insert_gaussians: position, color, spacing and distance are required");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        cudaStream_t st = c->cur;
+        const int64_t ns = src->n;
+        if (inserted) *inserted = 0;
+        if (ns == 0) {
+            main_done(c);
+            return;
+        }
+        DevBuf bpos, bcol, bsp, bdist, bfeat, bflag, bflag32, bslot;
+        auto dev_in = [&](DevBuf& b, const void* p, size_t bytes) -> const void* {
+            if (src->mem == TK_DEVICE) return p;
+            ensure<char>(b, bytes);
+            copy_in(b.p, p, bytes, TK_HOST, c);
+            return b.p;
+        };
+        const double* pos = static_cast<const double*>(dev_in(bpos, src->position, ns * 3 * sizeof(double)));
+        const double* col = static_cast<const double*>(dev_in(bcol, src->color, ns * 3 * sizeof(double)));
+        const double* sp = static_cast<const double*>(dev_in(bsp, src->spacing, ns * sizeof(double)));
+        const double* dist = static_cast<const double*>(dev_in(bdist, src->distance, ns * sizeof(double)));
+        const float* feat = (src->feature && src->d > 0)
+                                ? static_cast<const float*>(dev_in(bfeat, src->feature, ns * src->d * sizeof(float)))
+                                : nullptr;
+        uint8_t* flag = ensure<uint8_t>(bflag, ns);
+        int32_t* flag32 = ensure<int32_t>(bflag32, ns);
+        int32_t* slot = ensure<int32_t>(bslot, ns);
+        tk::launch_insert_flags(dist, ns, tau, flag, flag32, st);
+        ensure_scratch(c, ns + 1);
+        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+        tk::scan_exclusive(flag32, slot, ns, dscal + 10, c->scratch.p, st, &c->launches);
+        CK(cudaMemcpyAsync(c->hscal + 10, dscal + 10, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        sync(c);
+        const int64_t total = c->hscal[10];
+        c->launches += 1;
+        if (total > 0) {
+            if (c->d == 0 && feat && (c->n == 0 || !c->has_features)) c->d = src->d;  // mapper.cpp:40-41
+            const int64_t n0 = c->n, n1 = n0 + total;
+            const int d = c->d;
+            tk::InsertParams ip{};
+            ip.n_src = ns;
+            ip.base = n0;
+            ip.position = pos;
+            ip.color = col;
+            ip.feature = feat;
+            ip.d_src = src->d;
+            ip.spacing = sp;
+            ip.slot = slot;
+            ip.flag = flag;
+            // se3_inverse (pose.cpp:14-19) and its normalised rotation (mapper.cpp:25-26)
+            const double qi[4] = {w2c->qw, -w2c->qx, -w2c->qy, -w2c->qz};
+            const double t[3] = {w2c->tx, w2c->ty, w2c->tz};
+            double ti[3];
+            tk::quat_rotate_eigen(qi, t, ti);
+            const double qn = std::sqrt(((qi[0] * qi[0] + qi[1] * qi[1]) + qi[2] * qi[2]) + qi[3] * qi[3]);
+            for (int a = 0; a < 4; ++a) {
+                ip.qi[a] = qi[a];
+                ip.rot[a] = qi[a] / qn;
+            }
+            for (int a = 0; a < 3; ++a) ip.ti[a] = -ti[a];
+            ip.opacity_logit = std::log(0.5 / (1.0 - 0.5));                     // logit(0.5)
+            ip.d = d;
+            ip.mean = grow_keep<double>(c, c->mean, n0 * 3, n1 * 3, false);
+            ip.log_scale = grow_keep<double>(c, c->log_scale, n0 * 3, n1 * 3, false);
+            ip.rotation = grow_keep<double>(c, c->rotation, n0 * 4, n1 * 4, false);
+            ip.opacity = grow_keep<double>(c, c->opacity_logit, n0, n1, false);
+            ip.color_out = grow_keep<double>(c, c->color, n0 * 3, n1 * 3, false);
+            if (d > 0) {
+                ip.feat = grow_keep<float>(c, c->feature, c->has_features ? n0 * d : 0, n1 * d, false);
+                c->has_features = true;
+            }
+            tk::launch_insert_fill(ip, st);
+            c->launches += 1;
+            CK_LAUNCH(c);
+            if (c->opt_ready && c->opt_n == n0) {  // OptimizerState::extend (optimizer.cpp:29-36)
+                const int dims[5] = {3, 3, 4, 1, 3};
+                for (int g = 0; g < 5; ++g) {
+                    grow_keep<double>(c, c->am[g], n0 * dims[g], n1 * dims[g], true);
+                    grow_keep<double>(c, c->av[g], n0 * dims[g], n1 * dims[g], true);
+                }
+                grow_keep<float>(c, c->fm, n0 * c->opt_d, n1 * d, true);
+                grow_keep<float>(c, c->fv, n0 * c->opt_d, n1 * d, true);
+                if (c->opt_d != d) {  // the feature group is sized now (mapper.cpp:54)
+                    CK(cudaMemsetAsync(c->fm.p, 0, n1 * d * sizeof(float), st));
+                    CK(cudaMemsetAsync(c->fv.p, 0, n1 * d * sizeof(float), st));
+                }
+                c->opt_n = n1;
+                c->opt_d = d;
+            }
+            if (c->stat_n == n0) {
+                grow_keep<int32_t>(c, c->stat_count, n0, n1, true);
+                grow_keep<double>(c, c->stat_maxc, n0, n1, true);
+                c->stat_n = n1;
+            }
+            c->n = n1;
+            c->generation += 1;                                                 // mapper.cpp:56
+            scene_changed(c);
+            if (inserted) *inserted = static_cast<int32_t>(total);
+        }
+        sync(c);
+        for (DevBuf* b : {&bpos, &bcol, &bsp, &bdist, &bfeat, &bflag, &bflag32, &bslot}) b->release();
+        main_done(c);
+    });
+}
+
+tk_status tk_prune_map(tk_ctx* c, double keep_ratio, uint64_t seed, int32_t threshold, int32_t* removed_out,
+                       int64_t* n_removed) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        if (c->stat_n != c->n) fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        cudaStream_t st = c->cur;
+        const int64_t n = c->n;
+        std::vector<int32_t> counts(n);
+        std::vector<double> maxc(n);
+        copy_out(counts.data(), c->stat_count.p, n * sizeof(int32_t), TK_HOST, c);
+        copy_out(maxc.data(), c->stat_maxc.p, n * sizeof(double), TK_HOST, c);
+        sync(c);
+        const std::vector<int32_t> removed = prune_select(counts, maxc, keep_ratio, seed, threshold);
+        const int64_t nr = static_cast<int64_t>(removed.size());
+        if (nr > 0) {  // mapper.cpp:141-154 + OptimizerState::compact
+            DevBuf brem, bkeep, bpos;
+            int32_t* drem = ensure<int32_t>(brem, nr);
+            copy_in(drem, removed.data(), nr * sizeof(int32_t), TK_HOST, c);
+            int32_t* keep = ensure<int32_t>(bkeep, n);
+            int32_t* pos = ensure<int32_t>(bpos, n);
+            tk::launch_keep_flags(drem, nr, n, keep, st);
+            ensure_scratch(c, n + 1);
+            int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+            tk::scan_exclusive(keep, pos, n, dscal + 11, c->scratch.p, st, &c->launches);
+            c->launches += 2;
+            const int64_t nk = n - nr;
+            compact_rows<double>(c, c->mean, n, 3, nk, keep, pos);
+            compact_rows<double>(c, c->log_scale, n, 3, nk, keep, pos);
+            compact_rows<double>(c, c->rotation, n, 4, nk, keep, pos);
+            compact_rows<double>(c, c->opacity_logit, n, 1, nk, keep, pos);
+            compact_rows<double>(c, c->color, n, 3, nk, keep, pos);
+            if (c->has_features && c->d > 0) compact_rows<float>(c, c->feature, n, c->d, nk, keep, pos);
+            if (c->opt_ready && c->opt_n == n) {
+                const int dims[5] = {3, 3, 4, 1, 3};
+                for (int g = 0; g < 5; ++g) {
+                    compact_rows<double>(c, c->am[g], n, dims[g], nk, keep, pos);
+                    compact_rows<double>(c, c->av[g], n, dims[g], nk, keep, pos);
+                }
+                if (c->opt_d > 0) {
+                    compact_rows<float>(c, c->fm, n, c->opt_d, nk, keep, pos);
+                    compact_rows<float>(c, c->fv, n, c->opt_d, nk, keep, pos);
+                }
+                c->opt_n = nk;
+            }
+            sync(c);
+            for (DevBuf* b : {&brem, &bkeep, &bpos}) b->release();
+            c->n = nk;
+            c->generation += 1;                                                 // mapper.cpp:153
+            scene_changed(c);
+        }
+        // the statistics window restarts at every prune (mapper.cpp:156-159)
+        CK(cudaMemsetAsync(c->stat_count.p, 0, std::max<int64_t>(c->n, 1) * sizeof(int32_t), st));
+        CK(cudaMemsetAsync(c->stat_maxc.p, 0, std::max<int64_t>(c->n, 1) * sizeof(double), st));
+        c->stat_n = c->n;
+        if (removed_out && nr) std::memcpy(removed_out, removed.data(), nr * sizeof(int32_t));
+        if (n_removed) *n_removed = nr;
         main_done(c);
     });
 }

@@ -154,6 +154,12 @@ class MapperConfig:
     eps: float = 1e-8
     min_log_scale: float = -10.0
     max_log_scale: float = 1.0
+    # host-side schedule of optimize_step / insert_gaussians (mapper.hpp:14-35)
+    prune_period: int = 500
+    prune_keep_ratio: float = 0.5
+    topk_count_threshold: int = 0
+    pruning: bool = True
+    tau_insert: float = 0.05
 
 
 @dataclass

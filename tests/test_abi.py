@@ -44,7 +44,7 @@ def test_struct_layouts_match_header(tmp_path):
                "tk_geom_grads": N.tk_geom_grads, "tk_device_view": N.tk_device_view,
                "tk_synth_arrays": N.tk_synth_arrays, "tk_synth_spec": N.tk_synth_spec,
                "tk_mapper_config": N.tk_mapper_config, "tk_frame_view": N.tk_frame_view,
-               "tk_scene_out": N.tk_scene_out}
+               "tk_scene_out": N.tk_scene_out, "tk_source_view": N.tk_source_view}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tk_render.h"', '#include "tk_synth.h"',
              "int main(void) {"]
     for name, cls in structs.items():
