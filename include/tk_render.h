@@ -28,6 +28,8 @@
  * tk_insert_gaussians              insert_gaussians (map/mapper.hpp:41-43, mapper.cpp:19-60)
  * tk_prune_map                     prune_map + OptimizerState::compact (mapper.hpp:53-54,
  *                                  mapper.cpp:80-160, optimizer.cpp:9-47)
+ * tk_checkpoint_save / _load       save_checkpoint / load_checkpoint, SPLF v1 (map/checkpoint.hpp:9-14)
+ * tk_segment_by_query              segment_by_query (eval/metrics.hpp, metrics.cpp:66-94)
  *
  * Memory spaces: every buffer argument is tagged TK_HOST or TK_DEVICE.  Host buffers are
  * copied in/out inside the call (pinned memory from tk_host_alloc is fastest); device buffers
@@ -258,6 +260,23 @@ tk_status tk_insert_gaussians(tk_ctx* ctx, const tk_source_view* src, double tau
  * n, may be NULL) receives the removed indices in ascending order. */
 tk_status tk_prune_map(tk_ctx* ctx, double keep_ratio, uint64_t seed, int32_t topk_count_threshold,
                        int32_t* removed_out, int64_t* n_removed);
+
+/* SPLF v1 checkpoint (checkpoint.cpp:39-98): little-endian "SPLF", u32 version, u32 D, u64 N, then
+ * per Gaussian f32 mean[3], log_scale[3], quat w,x,y,z, opacity_logit, color[3], feature[D].
+ * Packed / unpacked on the device; load replaces the resident map (generation 0, optimiser state
+ * and statistics invalidated).  Errors carry the reference's messages. */
+tk_status tk_checkpoint_save(tk_ctx* ctx, const char* path);
+tk_status tk_checkpoint_load(tk_ctx* ctx, const char* path);
+
+/* segment_by_query (metrics.cpp:66-94): per pixel the argmax over classes of embedding . F
+ * (first maximum wins; squared norm < 1e-12 -> 255).  feature: n_pixels x d fp32 (NULL: the last
+ * tk_render_feature result, d and n_pixels then come from the context); embeddings: host,
+ * classes x d fp64 row-major (classes x d_total for the context's sharded F).  fp64 dots in
+ * channel order (bit-identical to the reference on the same F).  Under tk_comm with nranks > 1
+ * each rank scores its channel slice and the partial dots are all-reduced (sum) with NCCL. */
+tk_status tk_segment_by_query(tk_ctx* ctx, const float* feature, int64_t n_pixels, int32_t d,
+                              int32_t feature_mem, const double* embeddings, int32_t classes,
+                              uint8_t* labels, int32_t labels_mem);
 
 /* Drop the cached PreparedScene / forward state: the next call re-projects, re-sorts and
  * re-bins (the reference recomputes prepare_scene in every call, render.cpp:295). */

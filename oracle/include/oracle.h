@@ -174,6 +174,10 @@ int orc_insert_gaussians(orc_map* m, orc_opt* o, int64_t n_src, const double* po
 /* prune_map (mapper.cpp:80-160) + OptimizerState::compact; returns the number removed. */
 int64_t orc_prune_map(orc_map* m, orc_opt* o, double keep_ratio, uint64_t seed, int32_t threshold,
                       int32_t* removed_out);
+int orc_checkpoint_save(const orc_map* m, const char* path);      /* checkpoint.cpp:39-63 */
+orc_map* orc_checkpoint_load(const char* path);                    /* checkpoint.cpp:65-98 */
+void orc_segment_by_query(int32_t w, int32_t h, int32_t d, const double* feature, int32_t classes,
+                          const double* emb, uint8_t* out);           /* metrics.cpp:66-94 */
 int64_t orc_map_size(const orc_map* m);
 double* orc_opt_moments(orc_opt* o, int32_t group, int32_t which, int64_t* count);
 uint64_t orc_map_generation(const orc_map* m);

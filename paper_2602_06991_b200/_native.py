@@ -153,6 +153,10 @@ RENDER_SYMBOLS = [
     ("tk_insert_gaussians", C.c_int, [C.c_void_p, C.POINTER(tk_source_view), C.c_double, C.POINTER(tk_pose),
                                       i32_p]),
     ("tk_prune_map", C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_void_p, i64_p]),
+    ("tk_checkpoint_save", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("tk_checkpoint_load", C.c_int, [C.c_void_p, C.c_char_p]),
+    ("tk_segment_by_query", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
+                                      C.c_int32, C.c_void_p, C.c_int32]),
 ]
 
 PHASES = ["prepare", "geom_fwd", "gather", "fbwd_index", "fbwd", "geom_bwd", "chain", "full_blend", "allgather",

@@ -221,14 +221,15 @@ class Renderer:
         N.check(self.lib.tk_loss_values(self.ctx, vals))
         return LossValues(vals[0], vals[1], vals[2])
 
-    def scene_download(self, n: int, d: int) -> dict:
-        """The resident map's parameters and selection statistics."""
+    def scene_download(self, n: int, d: int, stats: bool = True) -> dict:
+        """The resident map's parameters and (stats=True) selection statistics."""
         o = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
-                 opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d), np.float32),
-                 topk_count=np.zeros(n, np.int32), max_contribution=np.zeros(n))
-        out = N.tk_scene_out(N.TK_HOST, *[_p(o[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit",
-                                                              "color", "feature", "topk_count",
-                                                              "max_contribution")])
+                 opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d), np.float32))
+        if stats:
+            o.update(topk_count=np.zeros(n, np.int32), max_contribution=np.zeros(n))
+        out = N.tk_scene_out(N.TK_HOST, *[_p(o.get(x)) for x in ("mean", "log_scale", "rotation", "opacity_logit",
+                                                                  "color", "feature", "topk_count",
+                                                                  "max_contribution")])
         N.check(self.lib.tk_scene_download(self.ctx, C.byref(out)))
         return o
 
@@ -260,6 +261,36 @@ class Renderer:
         k = C.c_int64()
         N.check(self.lib.tk_prune_map(self.ctx, keep_ratio, seed & ((1 << 64) - 1), threshold, _p(out), C.byref(k)))
         return out[:k.value].copy()
+
+
+    # ---------------------------------------------------------------- checkpoint / query
+    def checkpoint_save(self, path: str) -> None:
+        """save_checkpoint (checkpoint.cpp:39-63) of the resident map (SPLF v1)."""
+        N.check(self.lib.tk_checkpoint_save(self.ctx, path.encode()))
+
+    def checkpoint_load(self, path: str) -> tuple[int, int]:
+        """load_checkpoint (checkpoint.cpp:65-98) straight into the device SoA; returns (n, d)."""
+        N.check(self.lib.tk_checkpoint_load(self.ctx, path.encode()))
+        n, d, _ = self.scene_info()
+        return n, d
+
+    def segment_by_query(self, feature: np.ndarray | None, embeddings: np.ndarray,
+                         shape: tuple[int, int] | None = None) -> np.ndarray:
+        """segment_by_query (metrics.cpp:66-94): H x W uint8 labels (255 = invalid).  feature None:
+        the last render_feature output of this context (shape = (H, W) then)."""
+        emb = _c(embeddings, np.float64)
+        if feature is None:
+            h, w = shape
+            f, n, d, mem = None, h * w, 0, N.TK_DEVICE
+        else:
+            f = _c(feature, np.float32)
+            h, w, d = f.shape
+            n, mem = h * w, N.TK_HOST
+        if feature is not None and emb.shape[1] != d:
+            raise RuntimeError("segment_by_query: embedding dimension mismatch")
+        out = np.zeros((h, w), np.uint8)
+        N.check(self.lib.tk_segment_by_query(self.ctx, _p(f), n, d, mem, _p(emb), emb.shape[0], _p(out), N.TK_HOST))
+        return out
 
 
 class MT19937_64:

@@ -3,6 +3,8 @@
 // follow Pose::apply's Eigen rotation formula operation by operation, like the oracle.
 #include "mapedit.cuh"
 
+#include <algorithm>
+
 namespace tk {
 
 namespace {
@@ -80,6 +82,135 @@ __global__ void k_compact(const T* __restrict__ src, T* __restrict__ dst, const 
     }
 }
 
+// SPLF record (checkpoint.cpp:41-55): f32 mean[3], log_scale[3], quat w,x,y,z, opacity_logit,
+// color[3], feature[D]; element-parallel over the n x (14 + D) record array.
+__global__ void k_splf_pack(SplfView v, float* __restrict__ rec) {
+    const int W = 14 + v.d;
+    const int64_t total = v.n * W;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / W;
+        const int c = static_cast<int>(e - r * W);
+        float x;
+        if (c < 3) x = static_cast<float>(v.mean[r * 3 + c]);
+        else if (c < 6) x = static_cast<float>(v.log_scale[r * 3 + c - 3]);
+        else if (c < 10) x = static_cast<float>(v.rotation[r * 4 + c - 6]);
+        else if (c == 10) x = static_cast<float>(v.opacity_logit[r]);
+        else if (c < 14) x = static_cast<float>(v.color[r * 3 + c - 11]);
+        else x = v.feature[r * v.d + c - 14];
+        rec[e] = x;
+    }
+}
+
+__global__ void k_splf_unpack(const float* __restrict__ rec, SplfView v) {
+    const int W = 14 + v.d;
+    const int64_t total = v.n * W;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / W;
+        const int c = static_cast<int>(e - r * W);
+        const float x = rec[e];
+        if (c < 3) v.mean[r * 3 + c] = x;
+        else if (c < 6) v.log_scale[r * 3 + c - 3] = x;
+        else if (c < 10) v.rotation[r * 4 + c - 6] = x;
+        else if (c == 10) v.opacity_logit[r] = x;
+        else if (c < 14) v.color[r * 3 + c - 11] = x;
+        else v.feature[r * v.d + c - 14] = x;
+    }
+}
+
+// segment_by_query (metrics.cpp:66-94): one warp per pixel, lane = class; the pixel's feature
+// row is broadcast channel by channel from registers, the embeddings are staged transposed in
+// shared memory (fp64; one chunk of channels per pass, the whole D when it fits), dots and the
+// squared norm accumulate in channel order without contraction (the reference's summation), and
+// the first maximum wins.  Multi-chunk passes carry the running sums through p.acc / p.nacc.
+__global__ void __launch_bounds__(256) k_segment_query(QueryParams p, int chunk) {
+    extern __shared__ double et[];  // [chunk][classes]
+    const int lane = threadIdx.x & 31;
+    const int warps = blockDim.x >> 5;
+    const int C = p.classes, D = p.d;
+    for (int c0 = 0; c0 < D; c0 += chunk) {
+        const int cn = min(chunk, D - c0);
+        const bool first = c0 == 0, last = c0 + cn >= D;
+        __syncthreads();
+        for (int e = threadIdx.x; e < cn * C; e += blockDim.x) {
+            const int ci = e / C, k = e - ci * C;
+            et[ci * C + k] = p.emb[static_cast<int64_t>(k) * p.d_total + p.c0 + c0 + ci];
+        }
+        __syncthreads();
+        for (int64_t px = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); px < p.n_pixels;
+             px += static_cast<int64_t>(gridDim.x) * warps) {
+            for (int cb = 0; cb < C; cb += 32) {
+                const int cls = cb + lane;
+                double dot = 0.0, norm2 = 0.0;
+                if (!first) {
+                    dot = cls < C ? p.acc[px * C + cls] : 0.0;
+                    norm2 = p.nacc[px];
+                }
+                for (int cc = 0; cc < cn; cc += 32) {
+                    const double fv = (cc + lane < cn) ? static_cast<double>(p.feat[px * D + c0 + cc + lane]) : 0.0;
+                    const int m = min(32, cn - cc);
+                    for (int j = 0; j < m; ++j) {
+                        const double f = __shfl_sync(0xffffffffu, fv, j);
+                        norm2 += f * f;
+                        if (cls < C) dot += et[(cc + j) * C + cls] * f;
+                    }
+                }
+                if (!last) {
+                    if (cls < C) p.acc[px * C + cls] = dot;
+                    if (lane == 0 && cb + 32 >= C) p.nacc[px] = norm2;
+                    continue;
+                }
+                if (p.partial) {
+                    if (cls < C) p.partial[px * C + cls] = dot;
+                    if (lane == 0 && cb == 0) p.norm2[px] = norm2;
+                    continue;
+                }
+                double best = cls < C ? dot : -1e300;  // argmax: first maximum wins (strict >)
+                int arg = cls < C ? cls : 0x7fffffff;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+                    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+                    if (ob > best || (ob == best && oa < arg)) {
+                        best = ob;
+                        arg = oa;
+                    }
+                }
+                if (lane == 0) {
+                    if (cb == 0) {
+                        p.best[px] = best;
+                        p.labels[px] = norm2 < 1e-12 ? 255 : static_cast<uint8_t>(arg);
+                    } else if (norm2 >= 1e-12 && best > p.best[px]) {
+                        p.best[px] = best;
+                        p.labels[px] = static_cast<uint8_t>(arg);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Argmax over the all-reduced partial scores of the D-sharded path.
+__global__ void k_query_argmax(const double* __restrict__ scores, const double* __restrict__ norm2, int64_t n,
+                               int C, uint8_t* __restrict__ labels) {
+    for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < n;
+         px += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (norm2[px] < 1e-12) {
+            labels[px] = 255;
+            continue;
+        }
+        int best = 0;
+        double bd = -1e300;
+        for (int k = 0; k < C; ++k)
+            if (scores[px * C + k] > bd) {
+                bd = scores[px * C + k];
+                best = k;
+            }
+        labels[px] = static_cast<uint8_t>(best);
+    }
+}
+
 inline unsigned grid_for(int64_t items) {
     const int64_t b = (items + 255) / 256;
     return static_cast<unsigned>(b < 1 ? 1 : (b < 148 * 32 ? b : 148 * 32));
@@ -113,6 +244,46 @@ void launch_compact_f64(const double* src, double* dst, const int32_t* keep, con
     if (n <= 0 || width <= 0) return;
     k_compact<double><<<grid_for(n * width), 256, 0, st>>>(src, dst, keep, pos, n, width);
     dbg_launch("k_compact_f64", st);
+}
+
+void launch_splf_pack(const SplfView& v, float* rec, cudaStream_t st) {
+    if (v.n <= 0) return;
+    k_splf_pack<<<grid_for(v.n * (14 + v.d)), 256, 0, st>>>(v, rec);
+    dbg_launch("k_splf_pack", st);
+}
+
+void launch_splf_unpack(const float* rec, const SplfView& v, cudaStream_t st) {
+    if (v.n <= 0) return;
+    k_splf_unpack<<<grid_for(v.n * (14 + v.d)), 256, 0, st>>>(rec, v);
+    dbg_launch("k_splf_unpack", st);
+}
+
+int segment_query_chunk(int d, int classes) {
+    const int fit = static_cast<int>((160 * 1024) / (sizeof(double) * (classes > 0 ? classes : 1)));
+    int chunk = fit >= d ? d : (fit / 32) * 32;
+    return chunk < 32 ? 32 : chunk;
+}
+
+void launch_segment_query(const QueryParams& p, cudaStream_t st) {
+    if (p.n_pixels <= 0 || p.d <= 0) return;
+    const int chunk = segment_query_chunk(p.d, p.classes);
+    const size_t smem = static_cast<size_t>(chunk) * p.classes * sizeof(double);
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+        cudaFuncSetAttribute(k_segment_query, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        configured = smem;
+    }
+    const int64_t per_sm = std::max<int64_t>(1, (227 * 1024) / static_cast<int64_t>(smem + 1024));
+    const int64_t blocks = std::min<int64_t>((p.n_pixels + 7) / 8, 148 * std::min<int64_t>(per_sm, 8));
+    k_segment_query<<<static_cast<unsigned>(blocks), 256, smem, st>>>(p, chunk);
+    dbg_launch("k_segment_query", st);
+}
+
+void launch_query_argmax(const double* scores, const double* norm2, int64_t n, int classes, uint8_t* labels,
+                         cudaStream_t st) {
+    if (n <= 0) return;
+    k_query_argmax<<<grid_for(n), 256, 0, st>>>(scores, norm2, n, classes, labels);
+    dbg_launch("k_query_argmax", st);
 }
 
 void launch_compact_f32(const float* src, float* dst, const int32_t* keep, const int32_t* pos, int64_t n, int width,

@@ -42,6 +42,41 @@ void launch_compact_f64(const double* src, double* dst, const int32_t* keep, con
 void launch_compact_f32(const float* src, float* dst, const int32_t* keep, const int32_t* pos, int64_t n, int width,
                         cudaStream_t st);
 
+// SoA view of the resident map for the SPLF checkpoint pack / unpack (checkpoint.cpp:39-98).
+struct SplfView {
+    int64_t n;
+    int d;
+    double* mean;
+    double* log_scale;
+    double* rotation;
+    double* opacity_logit;
+    double* color;
+    float* feature;
+};
+void launch_splf_pack(const SplfView& v, float* rec, cudaStream_t st);      // rec: n x (14 + d) f32
+void launch_splf_unpack(const float* rec, const SplfView& v, cudaStream_t st);
+
+// segment_by_query (eval/metrics.cpp:66-94) over a rendered H x W x D feature image.
+struct QueryParams {
+    int64_t n_pixels;
+    int d;              // channels held here (a shard [c0, c0 + d) of d_total under tk_comm)
+    int c0, d_total;
+    int classes;
+    const float* feat;  // n_pixels x d
+    const double* emb;  // classes x d_total (row-major, device)
+    uint8_t* labels;    // n_pixels (255 = kInvalidLabel)
+    double* best;       // n_pixels scratch
+    double* partial;    // non-null: write per-class partial dots (n_pixels x classes) instead
+    double* norm2;      //   and the partial squared norms (n_pixels)
+    double* acc;        // n_pixels x classes running dots (only when D spans several chunks)
+    double* nacc;       // n_pixels running squared norms (idem)
+};
+// channels per shared-memory pass (the whole D when classes x D x 8 B fits in 160 KB)
+int segment_query_chunk(int d, int classes);
+void launch_segment_query(const QueryParams& p, cudaStream_t st);
+void launch_query_argmax(const double* scores, const double* norm2, int64_t n, int classes, uint8_t* labels,
+                         cudaStream_t st);
+
 // Quaternion * vector as Eigen::Quaternion::_transformVector: uv = 2 (q.vec x v); v + w uv + q.vec x uv
 __host__ __device__ inline void quat_rotate_eigen(const double q[4], const double v[3], double out[3]) {
     const double qx = q[1], qy = q[2], qz = q[3];

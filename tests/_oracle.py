@@ -89,6 +89,11 @@ def lib():
         L.orc_map_set_stats.argtypes = [vp, vp, vp]
         L.orc_opt_moments.restype = C.POINTER(C.c_double)
         L.orc_opt_moments.argtypes = [vp, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]
+        L.orc_checkpoint_save.restype = C.c_int
+        L.orc_checkpoint_save.argtypes = [vp, C.c_char_p]
+        L.orc_checkpoint_load.restype = vp
+        L.orc_checkpoint_load.argtypes = [C.c_char_p]
+        L.orc_segment_by_query.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, C.c_int32, vp, vp]
         L.orc_update_contribution_stats.argtypes = [vp, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                                     vp, vp, vp]
         _lib = L
@@ -362,3 +367,34 @@ class OracleMapper:
         lib().orc_map_export(self.map.h, *[_p(o[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit",
                                                               "color", "feature", "topk_count", "max_contribution")])
         return o
+
+
+def checkpoint_save(m, path):
+    om = OracleMap(m)
+    if lib().orc_checkpoint_save(om.h, path.encode()):
+        raise RuntimeError(lib().orc_last_error().decode())
+
+
+def checkpoint_load(path):
+    """load_checkpoint -> dict of SoA arrays (fp64) + feature_dim."""
+    h = lib().orc_checkpoint_load(path.encode())
+    if not h:
+        raise RuntimeError(lib().orc_last_error().decode())
+    n = int(lib().orc_map_size(h))
+    d = int(lib().orc_map_feature_dim(h))
+    o = dict(mean=np.zeros((n, 3)), log_scale=np.zeros((n, 3)), rotation=np.zeros((n, 4)),
+             opacity_logit=np.zeros(n), color=np.zeros((n, 3)), feature=np.zeros((n, d)))
+    lib().orc_map_export(h, *[_p(o[x]) for x in ("mean", "log_scale", "rotation", "opacity_logit", "color",
+                                                 "feature")], None, None)
+    lib().orc_map_free(h)
+    o["feature_dim"] = d
+    return o
+
+
+def segment_by_query(feature, emb):
+    f = np.ascontiguousarray(feature, np.float64)
+    e = np.ascontiguousarray(emb, np.float64)
+    h, w, d = f.shape
+    out = np.zeros((h, w), np.uint8)
+    lib().orc_segment_by_query(w, h, d, _p(f), e.shape[0], _p(e), _p(out))
+    return out

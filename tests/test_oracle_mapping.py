@@ -285,3 +285,44 @@ def test_optimizer_state_in_lockstep_through_insert_and_prune():  # test_mapper.
     for i in range(om.size()):
         tag = int(round(mom[i * 3] - 100.0))
         assert np.linalg.norm(e["mean"][i] - pos[tag]) < 1e-12
+
+
+# ---- SPLF checkpoint (test_mapper.cpp:443-468) and segment_by_query (test_eval.cpp:65-113)
+def test_checkpoint_round_trips_bit_exactly(tmp_path):
+    m = synth.random_scene(25, 8, 5)
+    p1, p2 = str(tmp_path / "a.bin"), str(tmp_path / "b.bin")
+    O.checkpoint_save(m, p1)
+    loaded = O.checkpoint_load(p1)
+    assert loaded["mean"].shape[0] == 25 and loaded["feature_dim"] == 8
+    m2 = SceneMap(mean=loaded["mean"], log_scale=loaded["log_scale"], rotation=loaded["rotation"],
+                  opacity_logit=loaded["opacity_logit"], color=loaded["color"], feature=loaded["feature"],
+                  feature_dim=8)
+    O.checkpoint_save(m2, p2)
+    b1, b2 = open(p1, "rb").read(), open(p2, "rb").read()
+    assert b1 == b2 and len(b1) == 20 + 25 * (14 + 8) * 4
+    with pytest.raises(RuntimeError, match="cannot open"):
+        O.checkpoint_load(str(tmp_path / "missing.bin"))
+    p3 = str(tmp_path / "short.bin")
+    open(p3, "wb").write(b1[:40])
+    with pytest.raises(RuntimeError, match="truncated file .*short.bin"):
+        O.checkpoint_load(p3)
+
+
+def test_segmentation_by_query_kats():  # test_eval.cpp:65-90
+    emb = np.eye(4, 8)
+    feat = np.zeros((10, 10, 8))
+    feat[:, :5, 0] = 1.0
+    feat[:, 5:, 1] = 1.0
+    pred = O.segment_by_query(feat, emb)
+    assert (pred[:, :5] == 0).all() and (pred[:, 5:] == 1).all()
+    feat[0, 0] = 0.0
+    assert O.segment_by_query(feat, emb)[0, 0] == 255
+
+
+def test_random_unit_features_split_evenly():  # test_eval.cpp:93-113 (smaller)
+    rng = np.random.default_rng(123)
+    v = rng.uniform(-1, 1, (100, 1000, 16))
+    v /= np.linalg.norm(v, axis=-1, keepdims=True)
+    pred = O.segment_by_query(v, np.eye(4, 16))
+    frac = np.bincount(pred.ravel(), minlength=4)[:4] / pred.size
+    assert np.all(np.abs(frac - 0.25) < 0.01)
