@@ -392,6 +392,10 @@ def main_gpu(args, cfg):
         e2e = run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpose, ccam, cset, n, Ds, P,
                       K, max(2, min(args.steps, args.e2e_steps)), stream, dist)
 
+    extras = None
+    if not dshard and not args.no_mapping:
+        extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev)
+
     mapping = None
     if not dshard and not args.no_mapping:
         mapping = run_mapping(lib, slib, N, torch, ctx, W, H, D, n, cpose, ccam, cset, args.steps, args.warmup,
@@ -424,7 +428,7 @@ def main_gpu(args, cfg):
             "hbm_gbs": feature_path["achieved_gbs"],
             "roofline": roof, "feature_path": feature_path, "phases": phases,
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
-            "mapping": mapping, "setup_s": setup_s,
+            "mapping": mapping, "extras": extras, "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
     lib.tk_destroy(ctx)
@@ -603,6 +607,44 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
                                      "path": "keyframe uploaded once (device-resident keyframe store); "
                                              "tk_optimize_step + loss values read back every iteration"}
     return out
+
+
+def run_extras(lib, N, torch, ctx, W, H, D, n, steps, stream, dev):
+    """The other §8(f) rows on the config-3 map: segment_by_query over the resident F (32 classes,
+    fp64 dots in the reference's order) and the SPLF checkpoint save / load through the device."""
+    P = W * H
+    C_CLS = 32
+    emb = np.random.default_rng(5).normal(size=(C_CLS, D))
+    labels = torch.empty(P, dtype=torch.uint8, device=dev)
+    args_q = (ctx, None, P, 0, N.TK_DEVICE, emb.ctypes.data, C_CLS, C.c_void_p(labels.data_ptr()), N.TK_DEVICE)
+    N.check(lib.tk_segment_by_query(*args_q))  # warm-up
+    N.check(lib.tk_synchronize(ctx))
+    qs = max(2, min(steps, 5))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(qs):
+        N.check(lib.tk_segment_by_query(*args_q))
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    q_ms = ev0.elapsed_time(ev1) / qs
+    inv = float((labels == 255).float().mean().item())
+    query = {"ms_per_frame": q_ms, "pixels_per_s": P / (q_ms / 1000.0), "classes": C_CLS,
+             "fp64_dot_flops": 2.0 * P * C_CLS * D, "fp64_tflops": 2.0 * P * C_CLS * D / (q_ms / 1000.0) / 1e12,
+             "invalid_fraction": inv,
+             "path": "tk_segment_by_query on the resident render_feature output (F read once, fp64 dots)"}
+    path = os.path.join("/tmp", f"tk_bench_{os.getpid()}.splf")
+    t0 = time.time()
+    N.check(lib.tk_checkpoint_save(ctx, path.encode()))
+    t1 = time.time()
+    N.check(lib.tk_checkpoint_load(ctx, path.encode()))
+    t2 = time.time()
+    size = os.path.getsize(path)
+    os.remove(path)
+    ckpt = {"bytes": size, "save_s": t1 - t0, "load_s": t2 - t1, "save_gbs": size / (t1 - t0) / 1e9,
+            "load_gbs": size / (t2 - t1) / 1e9,
+            "path": "SPLF v1 file <-> pinned host <-> device pack/unpack (host file I/O included)"}
+    return {"segment_by_query": query, "checkpoint": ckpt}
 
 
 def main():

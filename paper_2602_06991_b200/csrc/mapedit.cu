@@ -119,12 +119,49 @@ __global__ void k_splf_unpack(const float* __restrict__ rec, SplfView v) {
     }
 }
 
-// segment_by_query (metrics.cpp:66-94): one warp per pixel, lane = class; the pixel's feature
-// row is broadcast channel by channel from registers, the embeddings are staged transposed in
-// shared memory (fp64; one chunk of channels per pass, the whole D when it fits), dots and the
-// squared norm accumulate in channel order without contraction (the reference's summation), and
-// the first maximum wins.  Multi-chunk passes carry the running sums through p.acc / p.nacc.
-__global__ void __launch_bounds__(256) k_segment_query(QueryParams p, int chunk) {
+// segment_by_query (metrics.cpp:66-94): lane = class, kQP pixels per warp at a time (independent
+// dot chains); each pixel's feature row is broadcast channel by channel from registers, the
+// embeddings are staged transposed in shared memory (fp64; one chunk of channels per pass, the
+// whole D when it fits) and one shared-memory read serves the warp's kQP pixels.  Dots and squared
+// norms accumulate in channel order without contraction (the reference's summation); the first
+// maximum wins.  Multi-chunk passes carry the running sums through p.acc / p.nacc.
+constexpr int kQP = 4;
+__device__ __forceinline__ void query_finish(const QueryParams& p, int64_t px, int cb, int cls, int lane,
+                                             double dot, double norm2, bool last) {
+    const int C = p.classes;
+    if (!last) {
+        if (cls < C) p.acc[px * C + cls] = dot;
+        if (lane == 0 && cb + 32 >= C) p.nacc[px] = norm2;
+        return;
+    }
+    if (p.partial) {
+        if (cls < C) p.partial[px * C + cls] = dot;
+        if (lane == 0 && cb == 0) p.norm2[px] = norm2;
+        return;
+    }
+    double best = cls < C ? dot : -1e300;  // argmax: first maximum wins (strict >)
+    int arg = cls < C ? cls : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ob > best || (ob == best && oa < arg)) {
+            best = ob;
+            arg = oa;
+        }
+    }
+    if (lane == 0) {
+        if (cb == 0) {
+            p.best[px] = best;
+            p.labels[px] = norm2 < 1e-12 ? 255 : static_cast<uint8_t>(arg);
+        } else if (norm2 >= 1e-12 && best > p.best[px]) {
+            p.best[px] = best;
+            p.labels[px] = static_cast<uint8_t>(arg);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512) k_segment_query(QueryParams p, int chunk) {
     extern __shared__ double et[];  // [chunk][classes]
     const int lane = threadIdx.x & 31;
     const int warps = blockDim.x >> 5;
@@ -138,54 +175,54 @@ __global__ void __launch_bounds__(256) k_segment_query(QueryParams p, int chunk)
             et[ci * C + k] = p.emb[static_cast<int64_t>(k) * p.d_total + p.c0 + c0 + ci];
         }
         __syncthreads();
-        for (int64_t px = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5); px < p.n_pixels;
-             px += static_cast<int64_t>(gridDim.x) * warps) {
+        for (int64_t px0 = (static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5)) * kQP; px0 < p.n_pixels;
+             px0 += static_cast<int64_t>(gridDim.x) * warps * kQP) {
             for (int cb = 0; cb < C; cb += 32) {
                 const int cls = cb + lane;
-                double dot = 0.0, norm2 = 0.0;
-                if (!first) {
-                    dot = cls < C ? p.acc[px * C + cls] : 0.0;
-                    norm2 = p.nacc[px];
-                }
-                for (int cc = 0; cc < cn; cc += 32) {
-                    const double fv = (cc + lane < cn) ? static_cast<double>(p.feat[px * D + c0 + cc + lane]) : 0.0;
-                    const int m = min(32, cn - cc);
-                    for (int j = 0; j < m; ++j) {
-                        const double f = __shfl_sync(0xffffffffu, fv, j);
-                        norm2 += f * f;
-                        if (cls < C) dot += et[(cc + j) * C + cls] * f;
-                    }
-                }
-                if (!last) {
-                    if (cls < C) p.acc[px * C + cls] = dot;
-                    if (lane == 0 && cb + 32 >= C) p.nacc[px] = norm2;
-                    continue;
-                }
-                if (p.partial) {
-                    if (cls < C) p.partial[px * C + cls] = dot;
-                    if (lane == 0 && cb == 0) p.norm2[px] = norm2;
-                    continue;
-                }
-                double best = cls < C ? dot : -1e300;  // argmax: first maximum wins (strict >)
-                int arg = cls < C ? cls : 0x7fffffff;
+                const int clsr = cls < C ? cls : C - 1;  // clamped read index (result discarded)
+                double dot[kQP], nrm[kQP];
+                int64_t px[kQP];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
-                    if (ob > best || (ob == best && oa < arg)) {
-                        best = ob;
-                        arg = oa;
+                for (int u = 0; u < kQP; ++u) {
+                    px[u] = min(px0 + u, p.n_pixels - 1);
+                    dot[u] = (!first && cls < C) ? p.acc[px[u] * C + cls] : 0.0;
+                    nrm[u] = first ? 0.0 : p.nacc[px[u]];
+                }
+                int cc = 0;
+                for (; cc + 32 <= cn; cc += 32) {
+                    double fv[kQP];
+#pragma unroll
+                    for (int u = 0; u < kQP; ++u) fv[u] = static_cast<double>(p.feat[px[u] * D + c0 + cc + lane]);
+#pragma unroll 8
+                    for (int j = 0; j < 32; ++j) {
+                        const double e = et[(cc + j) * C + clsr];
+#pragma unroll
+                        for (int u = 0; u < kQP; ++u) {
+                            const double f = __shfl_sync(0xffffffffu, fv[u], j);
+                            nrm[u] += f * f;
+                            dot[u] += e * f;
+                        }
                     }
                 }
-                if (lane == 0) {
-                    if (cb == 0) {
-                        p.best[px] = best;
-                        p.labels[px] = norm2 < 1e-12 ? 255 : static_cast<uint8_t>(arg);
-                    } else if (norm2 >= 1e-12 && best > p.best[px]) {
-                        p.best[px] = best;
-                        p.labels[px] = static_cast<uint8_t>(arg);
+                if (cc < cn) {  // channel tail (D % 32)
+                    const int m = cn - cc;
+                    double fv[kQP];
+#pragma unroll
+                    for (int u = 0; u < kQP; ++u)
+                        fv[u] = lane < m ? static_cast<double>(p.feat[px[u] * D + c0 + cc + lane]) : 0.0;
+                    for (int j = 0; j < m; ++j) {
+                        const double e = et[(cc + j) * C + clsr];
+#pragma unroll
+                        for (int u = 0; u < kQP; ++u) {
+                            const double f = __shfl_sync(0xffffffffu, fv[u], j);
+                            nrm[u] += f * f;
+                            dot[u] += e * f;
+                        }
                     }
                 }
+#pragma unroll
+                for (int u = 0; u < kQP; ++u)
+                    if (px0 + u < p.n_pixels) query_finish(p, px0 + u, cb, cls, lane, dot[u], nrm[u], last);
             }
         }
     }
@@ -274,8 +311,8 @@ void launch_segment_query(const QueryParams& p, cudaStream_t st) {
         configured = smem;
     }
     const int64_t per_sm = std::max<int64_t>(1, (227 * 1024) / static_cast<int64_t>(smem + 1024));
-    const int64_t blocks = std::min<int64_t>((p.n_pixels + 7) / 8, 148 * std::min<int64_t>(per_sm, 8));
-    k_segment_query<<<static_cast<unsigned>(blocks), 256, smem, st>>>(p, chunk);
+    const int64_t blocks = std::min<int64_t>((p.n_pixels + 16 * kQP - 1) / (16 * kQP), 148 * std::min<int64_t>(per_sm, 4));
+    k_segment_query<<<static_cast<unsigned>(blocks), 512, smem, st>>>(p, chunk);
     dbg_launch("k_segment_query", st);
 }
 

@@ -236,6 +236,8 @@ struct tk_ctx {
     DevBuf am[5], av[5], fm, fv, stat_count, stat_maxc;
     DevBuf ssim_rows, ssim_win, l_gc, l_gd, l_partial, l_values, l_fscale, l_signs;
     double* hvals = nullptr;  // pinned {map, geo, feat} of the last optimize_step
+    // segment_by_query scratch (kept across calls: no allocation on the query path)
+    DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
     // multi-GPU
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;
@@ -911,7 +913,8 @@ tk_status tk_destroy(tk_ctx* c) {
         c->av[g].release();
     }
     DevBuf* mapping[] = {&c->fm, &c->fv, &c->stat_count, &c->stat_maxc, &c->ssim_rows, &c->ssim_win, &c->l_gc,
-                         &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs};
+                         &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs, &c->q_feat,
+                         &c->q_emb, &c->q_labels, &c->q_best, &c->q_acc, &c->q_nacc, &c->q_part};
     for (DevBuf* b : mapping) b->release();
     if (c->hvals) cudaFreeHost(c->hvals);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -2011,7 +2014,8 @@ tk_status tk_segment_by_query(tk_ctx* c, const float* feature, int64_t n_pixels,
         if (d <= 0) fail(TK_ERR_BAD_ARG, "segment_by_query: embedding dimension mismatch");
         const int64_t P = feature ? n_pixels : c->fout_pixels;
         const float* F = feature;
-        DevBuf bf, be, bl, bb, bacc, bn, bpart;
+        DevBuf &bf = c->q_feat, &be = c->q_emb, &bl = c->q_labels, &bb = c->q_best, &bacc = c->q_acc, &bn = c->q_nacc,
+               &bpart = c->q_part;
         if (!F) {
             if (!c->f_out.p || c->fout_pixels <= 0) fail(TK_ERR_STATE, "segment_by_query: no rendered feature image");
             F = ptr<float>(c->f_out);
@@ -2050,9 +2054,10 @@ tk_status tk_segment_by_query(tk_ctx* c, const float* feature, int64_t n_pixels,
             c->launches += 1;
         }
         CK_LAUNCH(c);
-        if (labels_mem == TK_HOST) copy_out(labels, dl, P, TK_HOST, c);
-        sync(c);
-        for (DevBuf* b : {&bf, &be, &bl, &bb, &bacc, &bn, &bpart}) b->release();
+        if (labels_mem == TK_HOST) {
+            copy_out(labels, dl, P, TK_HOST, c);
+            sync(c);
+        }
         side_done(c, true);
     });
 }
