@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise an ncu launch list + an ncu --set full report into profiles/.
 
-  python scripts/profile_summary.py TAG launches.csv report.ncu-rep [bench.json]
+  python scripts/profile_summary.py TAG launches.csv report.ncu-rep [bench.json] [--title T] [--cmd C]
 
 Writes profiles/TAG_summary.md, profiles/TAG_launches.csv and profiles/TAG_ncu_traffic.json
 (DRAM bytes read+write per launch for each fully captured kernel; bench.py reads the latest
@@ -71,20 +71,28 @@ def full_report(path: str):
 
 
 def main():
-    tag, launches, rep = sys.argv[1:4]
-    bench = json.load(open(sys.argv[4])) if len(sys.argv) > 4 else None
+    argv = sys.argv[1:]
+    opts = {}
+    for key in ("--title", "--cmd"):
+        if key in argv:
+            i = argv.index(key)
+            opts[key] = argv[i + 1]
+            del argv[i:i + 2]
+    tag, launches, rep = argv[0:3]
+    bench = json.load(open(argv[3])) if len(argv) > 3 else None
     os.makedirs(PROFILES, exist_ok=True)
     shutil.copy(launches, os.path.join(PROFILES, f"{tag}_launches.csv"))
     agg, tot, n = launch_table(launches)
-    lines = [f"# {tag} — ncu summaries (config 3, one bench step)", "",
+    title = opts.get("--title", "config 3, one bench step")
+    cmd = opts.get("--cmd", "python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e")
+    lines = [f"# {tag} — ncu summaries ({title})", "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` on "
-             "`python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e` (cold, serialised launches: "
-             "compare shares, not absolutes).", "",
+             f"`{cmd}` (cold, serialised launches: compare shares, not absolutes).", "",
              "| kernel | launches | us | share |", "|---|---|---|---|"]
     for name, (t, c) in sorted(agg.items(), key=lambda x: -x[1][0]):
         lines.append(f"| {name} | {c} | {t / 1e3:.1f} | {100 * t / tot:.1f}% |")
     lines += ["", f"Kernel time in the step: {tot / 1e3:.1f} us over {n} launches.", ""]
-    recs = full_report(rep)
+    recs = [r for one in rep.split(",") for r in full_report(one)]
     traffic = {}
     lines += ["## ncu --set full (per launch)", "",
               "| kernel | time ms | DRAM read GB | DRAM write GB | DRAM % | SM % | fp64 pipe % | regs | warps active % | threads/inst |",
