@@ -48,13 +48,16 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
         for (int u = 0; u < 2; ++u) {
             bool valid;
             px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &valid);
-            c[u] = valid ? p.count[px[u]] : 0;
-            double wd = 0.0;
-            id[u] = 0;
-            if (lane < c[u]) {
-                id[u] = p.index[px[u] * p.k + lane];
-                wd = p.weight[px[u] * p.k + lane];
+            // the record slots load alongside the count (one memory round trip, not two)
+            int idl = 0;
+            double wdl = 0.0;
+            if (valid && lane < p.k) {
+                idl = p.index[px[u] * p.k + lane];
+                wdl = p.weight[px[u] * p.k + lane];
             }
+            c[u] = valid ? p.count[px[u]] : 0;
+            const double wd = lane < c[u] ? wdl : 0.0;
+            id[u] = lane < c[u] ? idl : 0;
             double sum = 0.0;
             for (int j = 0; j < c[u]; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
             wn[u] = lane < c[u] ? static_cast<float>(wd / sum) : 0.0f;

@@ -290,15 +290,18 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &in[u]);
+            // the record slots load alongside count / mask (one memory round trip, not two)
+            int idl = 0;
+            double wdl = 0.0;
+            if (in[u] && lane < p.k) {
+                idl = p.index[px[u] * p.k + lane];
+                wdl = p.weight[px[u] * p.k + lane];
+            }
             const int cnt = in[u] ? p.count[px[u]] : 0;
             const bool live = cnt > 0 && p.gt_valid[px[u]];
             c[u] = live ? cnt : 0;
-            double wd = 0.0;
-            id[u] = 0;
-            if (lane < c[u]) {
-                id[u] = p.index[px[u] * p.k + lane];
-                wd = p.weight[px[u] * p.k + lane];
-            }
+            const double wd = lane < c[u] ? wdl : 0.0;
+            id[u] = lane < c[u] ? idl : 0;
             double sum = 0.0;
             for (int j = 0; j < c[u]; ++j) sum += __shfl_sync(0xffffffffu, wd, j);
             wn[u] = lane < c[u] ? static_cast<float>(wd / sum) : 0.0f;
