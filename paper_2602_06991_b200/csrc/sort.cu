@@ -136,27 +136,40 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const int32_t* _
     }
     int64_t tot;
     const int64_t local = block_excl_scan<SCAN_THREADS>(s, &tot);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 predecessors at a time
+        const int lane = threadIdx.x;
         volatile unsigned long long* vs = status;
         int64_t excl = 0;
         if (bid == 0) {
-            vs[0] = kFlagPrefix | static_cast<unsigned long long>(tot);
+            if (lane == 0) vs[0] = kFlagPrefix | static_cast<unsigned long long>(tot);
         } else {
-            vs[bid] = kFlagAgg | static_cast<unsigned long long>(tot);
-            __threadfence();
-            for (int p = bid - 1;;) {
-                const unsigned long long w = vs[p];
-                const unsigned long long flag = w & ~kValMask;
-                if (flag == 0) continue;
-                excl += static_cast<int64_t>(w & kValMask);
-                if (flag == kFlagPrefix) break;
-                --p;
+            if (lane == 0) {
+                vs[bid] = kFlagAgg | static_cast<unsigned long long>(tot);
+                __threadfence();
             }
-            __threadfence();
-            vs[bid] = kFlagPrefix | static_cast<unsigned long long>(excl + tot);
+            __syncwarp();
+            for (int p = bid - 1;; p -= 32) {
+                const int q = p - lane;
+                unsigned long long w = q >= 0 ? vs[q] : (2ull << 62);  // before block 0: prefix 0
+                while (__any_sync(0xffffffffu, (w & ~kValMask) == 0))
+                    if ((w & ~kValMask) == 0) w = vs[q];
+                const unsigned pm = __ballot_sync(0xffffffffu, (w & ~kValMask) == kFlagPrefix);
+                const int first = pm ? __ffs(pm) - 1 : 32;  // closest predecessor holding a prefix
+                int64_t val = lane <= first ? static_cast<int64_t>(w & kValMask) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (pm) break;
+            }
+            if (lane == 0) {
+                __threadfence();
+                vs[bid] = kFlagPrefix | static_cast<unsigned long long>(excl + tot);
+            }
         }
-        excl_s = excl;
-        if (bid == nb - 1) *total = excl + tot;
+        if (lane == 0) {
+            excl_s = excl;
+            if (bid == nb - 1) *total = excl + tot;
+        }
     }
     __syncthreads();
     int64_t run = excl_s + local;
