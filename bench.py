@@ -467,21 +467,23 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
         keep.append(t)
         outs[name] = v
     view = N.tk_scene_view(n, Ds, *(a.ctypes.data for a in g_pin), f_pin.ctypes.data, 0)
-    gout = N.tk_geom_out(N.TK_HOST, *(outs[x].ctypes.data for x in ("color", "depth", "alpha", "index", "weight",
-                                                                    "count", "contrib")), 0, 0)
-    gg = N.tk_geom_grads(N.TK_HOST, *(outs[x].ctypes.data for x in ("gmean", "gls", "grot", "gop", "gcol")))
+    gout = N.tk_geom_out(N.TK_HOST_ASYNC, *(outs[x].ctypes.data for x in ("color", "depth", "alpha", "index",
+                                                                          "weight", "count", "contrib")), 0, 0)
+    gg = N.tk_geom_grads(N.TK_HOST_ASYNC, *(outs[x].ctypes.data for x in ("gmean", "gls", "grot", "gop", "gcol")))
     h2d = sum(a.nbytes for a in g_pin) + f_pin.nbytes + gF_pin.nbytes + gC_pin.nbytes + gD_pin.nbytes
     d2h = sum(v.nbytes for v in outs.values()) + 6 * 8
 
+    A = N.TK_HOST_ASYNC  # pinned buffers on the context's copy streams: H2D and D2H overlap
+
     def step():
         N.check(lib.tk_invalidate(ctx))
-        N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
+        N.check(lib.tk_scene_upload(ctx, C.byref(view), A))
         N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.byref(gout)))
-        N.check(lib.tk_render_feature(ctx, None, C.c_void_p(outs["F"].ctypes.data), N.TK_HOST))
-        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF_pin.ctypes.data), N.TK_HOST,
-                                        C.c_void_p(outs["df"].ctypes.data), N.TK_HOST))
+        N.check(lib.tk_render_feature(ctx, None, C.c_void_p(outs["F"].ctypes.data), A))
+        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF_pin.ctypes.data), A,
+                                        C.c_void_p(outs["df"].ctypes.data), A))
         N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
-                                          C.c_void_p(gC_pin.ctypes.data), C.c_void_p(gD_pin.ctypes.data), N.TK_HOST,
+                                          C.c_void_p(gC_pin.ctypes.data), C.c_void_p(gD_pin.ctypes.data), A,
                                           C.byref(gg)))
 
     step()
@@ -504,8 +506,10 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
     world = dist.get_world_size() if dist else 1
     return {"value": steps / (ms / 1000.0), "unit": "frames/s", "h2d_bytes_per_step": int(h2d * world),
             "d2h_bytes_per_step": int(d2h * world), "steps": steps, "ms_per_step": ms / steps,
-            "path": "C ABI with pinned host buffers: scene upload, render_geometric, render_feature, "
-                    "backward_feature, backward_geometric (host in/out)"}
+            "path": "C ABI with pinned host buffers (TK_HOST_ASYNC: host->device and device->host on the context's "
+                    "two copy streams, overlapping each other and the next step's upload): scene upload, "
+                    "render_geometric, render_feature, backward_feature, backward_geometric (host in/out); "
+                    "all copies complete inside the timed region (tk_synchronize before the end event)"}
 
 
 def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, warmup, e2e_steps, stream, dist):
@@ -537,7 +541,7 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
         N.check(lib.tk_optimize_step(ctx, C.byref(cfg), C.byref(ccam), C.byref(cset), 0, it[0], values, None))
         it[0] += 1
 
-    for _ in range(warmup):
+    for _ in range(max(warmup, cfg.feature_update_period)):  # warm-up covers a feature step too
         step()
     N.check(lib.tk_synchronize(ctx))
     steps = max(cfg.feature_update_period, (steps // cfg.feature_update_period) * cfg.feature_update_period)

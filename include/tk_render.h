@@ -56,7 +56,10 @@ typedef enum {
     TK_ERR_STATE = 6 /* e.g. no scene uploaded, no records rendered */
 } tk_status;
 
-enum { TK_HOST = 0, TK_DEVICE = 1 };
+/* TK_HOST_ASYNC: pinned host memory copied on the context's own copy streams (host->device and
+ * device->host run concurrently on the two copy engines); the call returns without waiting, the
+ * host buffer must stay untouched until tk_synchronize(). */
+enum { TK_HOST = 0, TK_DEVICE = 1, TK_HOST_ASYNC = 2 };
 
 typedef struct tk_ctx tk_ctx;
 
@@ -148,7 +151,8 @@ tk_status tk_create(int32_t device, tk_ctx** out);
 tk_status tk_destroy(tk_ctx* ctx);
 tk_status tk_synchronize(tk_ctx* ctx);
 /* The context runs the feature calls and the geometry backward on two side streams so they
- * overlap; tk_join orders the main stream (tk_get_stream) after all of them, device-side. */
+ * overlap, and TK_HOST_ASYNC copies on two copy streams; tk_join orders the main stream
+ * (tk_get_stream) after all of them, device-side. */
 tk_status tk_join(tk_ctx* ctx);
 void* tk_get_stream(tk_ctx* ctx); /* cudaStream_t of the main stream */
 

@@ -13,7 +13,7 @@ LIB_DIR = os.path.join(_HERE, "lib")
 RENDER_LIB = os.path.join(LIB_DIR, "libtkrender.so")
 SYNTH_LIB = os.path.join(LIB_DIR, "libtk_synth.so")
 
-TK_HOST, TK_DEVICE = 0, 1
+TK_HOST, TK_DEVICE, TK_HOST_ASYNC = 0, 1, 2
 TK_OK, TK_ERR_STALE_INDEX, TK_ERR_BAD_ARG, TK_ERR_CUDA, TK_ERR_NCCL, TK_ERR_OOM, TK_ERR_STATE = range(7)
 
 dbl_p = C.POINTER(C.c_double)

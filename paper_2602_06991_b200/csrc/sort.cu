@@ -395,7 +395,20 @@ __global__ void k_segment_offsets(const uint32_t* __restrict__ keys, int64_t n, 
     offsets[g] = static_cast<int32_t>(lo);
 }
 
+// Small device -> host-mapped copies (scalars, loss values): stores from a kernel travel over the
+// bus without a copy engine, so they never queue behind large asynchronous DMA transfers.
+__global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
 }  // namespace
+
+void copy_words_to_mapped(void* dst_mapped, const void* src, int words, cudaStream_t st) {
+    if (words <= 0) return;
+    k_copy_words<<<1, 32, 0, st>>>(static_cast<const unsigned long long*>(src),
+                                   static_cast<unsigned long long*>(dst_mapped), words);
+    dbg_launch("k_copy_words", st);
+}
 
 size_t scan_scratch_bytes(int64_t n) {
     const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;

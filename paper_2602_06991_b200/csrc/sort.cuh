@@ -7,6 +7,9 @@ namespace tk {
 
 size_t align_bytes(size_t b);  // round up to 256 B
 
+// words x 8 bytes from device memory into host-mapped (cudaHostAllocMapped) memory, by a kernel
+void copy_words_to_mapped(void* dst_mapped, const void* src, int words, cudaStream_t st);
+
 // Scratch bytes needed by scan_exclusive for n elements.
 size_t scan_scratch_bytes(int64_t n);
 // out[i] = sum(in[0..i)), out may alias nothing; *total (device, int64) = sum(in).

@@ -184,6 +184,14 @@ struct tk_ctx {
     cudaStream_t s_feat = nullptr, s_geo = nullptr;  // side streams: feature path, geometry backward
     cudaStream_t cur = nullptr;                       // stream the current call enqueues on
     cudaEvent_t ev_main = nullptr, ev_feat = nullptr, ev_geo = nullptr;
+    // TK_HOST_ASYNC copies: host->device on s_in, device->host on s_out (both copy engines busy at
+    // once); ev_cmp orders them after the compute issued so far, ev_in / ev_out order compute after them
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_cmp = nullptr, ev_in = nullptr, ev_out[5] = {};
+    bool out_pending[5] = {};
+    double* h_twist = nullptr;    // host-mapped pose twist of an asynchronous backward_geometric
+    double* h_twist_dev = nullptr;
+    double* twist_dst = nullptr;  //   copied into the caller's struct at tk_synchronize
     bool feat_pending = false, geo_pending = false;
     int64_t launches = 0;
     Profiler prof;
@@ -201,7 +209,8 @@ struct tk_ctx {
     DevBuf te[13];
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
     DevBuf scratch, scratch_feat, dscal;
-    int64_t* hscal = nullptr;  // pinned mirror of dscal
+    int64_t* hscal = nullptr;      // host-mapped mirror of dscal (written by k_copy_words)
+    int64_t* hscal_dev = nullptr;  //   its device address
     // prepared scene
     bool prepared = false;
     PrepKey prep_key{};
@@ -235,7 +244,9 @@ struct tk_ctx {
     int64_t step_geo = 0, step_feat = 0;
     DevBuf am[5], av[5], fm, fv, stat_count, stat_maxc;
     DevBuf ssim_rows, ssim_win, l_gc, l_gd, l_partial, l_values, l_fscale, l_signs;
-    double* hvals = nullptr;  // pinned {map, geo, feat} of the last optimize_step
+    double* hvals = nullptr;  // host-mapped {map, geo, feat} of the last optimize_step
+    double* hvals_dev = nullptr;
+    bool has_values = false;
     // segment_by_query scratch (kept across calls: no allocation on the query path)
     DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
     // multi-GPU
@@ -287,13 +298,34 @@ tk_status guarded(F&& f) {
 // Host <-> device copies made inside an API call (timed as TK_PHASE_COPY when profiling).
 void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
     if (bytes == 0) return;
+    if (mem == TK_HOST_ASYNC) {  // after the compute issued so far (it may still read dst), before what follows
+        CK(cudaEventRecord(c->ev_cmp, c->cur));
+        CK(cudaStreamWaitEvent(c->s_in, c->ev_cmp, 0));
+        if (c->out_pending[0]) CK(cudaStreamWaitEvent(c->s_in, c->ev_out[0], 0));  // untagged reads (misc)
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s_in));
+        CK(cudaEventRecord(c->ev_in, c->s_in));
+        CK(cudaStreamWaitEvent(c->cur, c->ev_in, 0));
+        return;
+    }
     PhaseScope phase(c, TK_PHASE_COPY);
     CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        c->cur));
 }
 
-void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
+// Asynchronous device->host copies are tagged by the buffers they read, so only the compute that
+// overwrites those buffers waits for them (kOutMisc: waited at the start of every call).
+enum OutTag { kOutMisc = 0, kOutRec = 1, kOutF = 2, kOutDF = 3, kOutGG = 4 };
+
+void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, int tag = kOutMisc) {
     if (bytes == 0 || dst == nullptr) return;
+    if (mem == TK_HOST_ASYNC) {  // after the compute that produced src; its overwriters wait for it
+        CK(cudaEventRecord(c->ev_cmp, c->cur));
+        CK(cudaStreamWaitEvent(c->s_out, c->ev_cmp, 0));
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->s_out));
+        CK(cudaEventRecord(c->ev_out[tag], c->s_out));
+        c->out_pending[tag] = true;
+        return;
+    }
     PhaseScope phase(c, TK_PHASE_COPY);
     CK(cudaMemcpyAsync(dst, src, bytes, mem == TK_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                        c->cur));
@@ -306,8 +338,20 @@ void sync(tk_ctx* c) { CK(cudaStreamSynchronize(c->cur)); }
 // backward on s_geo, each ordered after the main stream's latest work (ev_main), so the
 // HBM-bound feature kernels and the fp64-bound geometry backward overlap.  Main-stream work
 // first waits for outstanding side-stream work that still reads those buffers.
+// Compute issued from here on may overwrite the buffers an asynchronous device->host copy of
+// this tag still reads: order it after that copy.
+void wait_out(tk_ctx* c, int tag) {
+    if (c->out_pending[tag]) {
+        CK(cudaStreamWaitEvent(c->cur, c->ev_out[tag], 0));
+        if (c->cur != c->stream) CK(cudaStreamWaitEvent(c->stream, c->ev_out[tag], 0));
+        c->out_pending[tag] = false;
+    }
+}
+void wait_async_out(tk_ctx* c) { wait_out(c, kOutMisc); }
+
 void on_main(tk_ctx* c) {
     c->cur = c->stream;
+    wait_async_out(c);
     if (c->feat_pending) {
         CK(cudaStreamWaitEvent(c->stream, c->ev_feat, 0));
         c->feat_pending = false;
@@ -321,6 +365,7 @@ void main_done(tk_ctx* c) { CK(cudaEventRecord(c->ev_main, c->stream)); }
 void on_side(tk_ctx* c, bool feat) {
     c->cur = feat ? c->s_feat : c->s_geo;
     CK(cudaStreamWaitEvent(c->cur, c->ev_main, 0));
+    wait_async_out(c);
 }
 void side_done(tk_ctx* c, bool feat) {
     CK(cudaEventRecord(feat ? c->ev_feat : c->ev_geo, c->cur));
@@ -458,7 +503,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     tk::launch_compact(pp.valid, pos, pp.z, n, pp.key_min, dkeys, dvals, st);
     c->launches += n > 0;
     CK_LAUNCH(c);
-    CK(cudaMemcpyAsync(c->hscal, dscal, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    tk::copy_words_to_mapped(c->hscal_dev, dscal, 3, st);
     sync(c);
     const int64_t n_vis = n > 0 ? c->hscal[0] : 0;
     const uint64_t kmin = static_cast<uint64_t>(c->hscal[1]), kmax = static_cast<uint64_t>(c->hscal[2]);
@@ -484,7 +529,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
         tk::launch_sorted_ntiles(c->order, n_vis, pp.ntiles, nts, st);
         c->launches += n_vis > 0;
         tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st, &c->launches);
-        CK(cudaMemcpyAsync(c->hscal + 3, dscal + 3, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        tk::copy_words_to_mapped(c->hscal_dev + 3, dscal + 3, 5, st);
         sync(c);
     };
     const int lo = hb > 24 ? hb - 24 : 0;
@@ -563,6 +608,7 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
     gp.aux.wl = ptr<int32_t>(c->wl);
     gp.aux.wl_count = ensure<int32_t>(c->wl_count, tk::geom_blocks(f));
     if (records) {
+        wait_out(c, kOutRec);
         gp.color = ensure<double>(c->o_color, P * 3);
         gp.depth = ensure<double>(c->o_depth, P);
         gp.alpha = ensure<double>(c->o_alpha, P);
@@ -647,7 +693,7 @@ Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
     CK(cudaMemsetAsync(dscal + 5, 0xff, sizeof(int64_t), st));
     tk::launch_first_stale(r.index, slots, n, reinterpret_cast<unsigned long long*>(dscal + 5), st);
     c->launches += slots > 0;
-    CK(cudaMemcpyAsync(c->hscal + 5, dscal + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    tk::copy_words_to_mapped(c->hscal_dev + 5, dscal + 5, 1, st);
     sync(c);
     const uint64_t first = static_cast<uint64_t>(c->hscal[5]);
     if (first != ~0ull) {
@@ -878,8 +924,18 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_feat, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_geo, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking);
+        for (cudaEvent_t* ev : {&c->ev_cmp, &c->ev_in, &c->ev_out[0], &c->ev_out[1], &c->ev_out[2], &c->ev_out[3],
+                                &c->ev_out[4]})
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_twist), 8 * sizeof(double), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_twist_dev), c->h_twist, 0);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hvals), 4 * sizeof(double), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hvals_dev), c->hvals, 0);
         c->cur = c->stream;
-        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscal), 16 * sizeof(int64_t), cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscal), 16 * sizeof(int64_t), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hscal_dev), c->hscal, 0);
         if (e != cudaSuccess) {
             delete c;
             fail(TK_ERR_CUDA, std::string("tk_create: ") + cudaGetErrorString(e));
@@ -894,6 +950,8 @@ tk_status tk_destroy(tk_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->s_feat) cudaStreamSynchronize(c->s_feat);
     if (c->s_geo) cudaStreamSynchronize(c->s_geo);
+    if (c->s_in) cudaStreamSynchronize(c->s_in);
+    if (c->s_out) cudaStreamSynchronize(c->s_out);
     DevBuf* all[] = {&c->mean, &c->log_scale, &c->rotation, &c->opacity_logit, &c->color, &c->feature, &c->pmx,
                      &c->pmy, &c->pixx, &c->pixy, &c->piyy, &c->pz, &c->pop, &c->rect, &c->valid, &c->ntiles,
                      &c->pos, &c->dkeys, &c->dvals, &c->dkeys_alt, &c->dvals_alt, &c->ntiles_sorted, &c->pair_off,
@@ -922,8 +980,12 @@ tk_status tk_destroy(tk_ctx* c) {
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->s_feat && c->s_feat != c->stream) cudaStreamDestroy(c->s_feat);
     if (c->s_geo && c->s_geo != c->stream) cudaStreamDestroy(c->s_geo);
-    for (cudaEvent_t e : {c->ev_main, c->ev_feat, c->ev_geo})
+    for (cudaEvent_t e : {c->ev_main, c->ev_feat, c->ev_geo, c->ev_cmp, c->ev_in, c->ev_out[0], c->ev_out[1],
+                          c->ev_out[2], c->ev_out[3], c->ev_out[4]})
         if (e) cudaEventDestroy(e);
+    if (c->h_twist) cudaFreeHost(c->h_twist);
+    if (c->s_in) cudaStreamDestroy(c->s_in);
+    if (c->s_out) cudaStreamDestroy(c->s_out);
     delete c;
     return TK_OK;
 }
@@ -934,6 +996,13 @@ tk_status tk_synchronize(tk_ctx* c) {
         CK(cudaStreamSynchronize(c->s_feat));
         CK(cudaStreamSynchronize(c->s_geo));
         CK(cudaStreamSynchronize(c->stream));
+        CK(cudaStreamSynchronize(c->s_in));
+        CK(cudaStreamSynchronize(c->s_out));
+        for (bool& b : c->out_pending) b = false;
+        if (c->twist_dst) {
+            std::memcpy(c->twist_dst, c->h_twist, 6 * sizeof(double));
+            c->twist_dst = nullptr;
+        }
     });
 }
 
@@ -941,6 +1010,11 @@ tk_status tk_join(tk_ctx* c) {
     return guarded([&] {
         CK(cudaSetDevice(c->device));
         on_main(c);
+        // the copy streams too: the main stream then follows every asynchronous host copy
+        CK(cudaEventRecord(c->ev_in, c->s_in));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_in, 0));
+        CK(cudaEventRecord(c->ev_out[kOutMisc], c->s_out));
+        CK(cudaStreamWaitEvent(c->stream, c->ev_out[kOutMisc], 0));
         main_done(c);
     });
 }
@@ -1069,13 +1143,13 @@ tk_status tk_render_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera* c
             const int64_t P = static_cast<int64_t>(cam->width) * cam->height;
             const int64_t k = c->rec_k;
             cudaStream_t st = c->cur;
-            copy_out(out->color, c->o_color.p, P * 3 * sizeof(double), out->mem, c);
-            copy_out(out->depth, c->o_depth.p, P * sizeof(double), out->mem, c);
-            copy_out(out->alpha, c->o_alpha.p, P * sizeof(double), out->mem, c);
-            copy_out(out->topk_index, c->o_index.p, P * k * sizeof(int32_t), out->mem, c);
-            copy_out(out->topk_weight, c->o_weight.p, P * k * sizeof(double), out->mem, c);
-            copy_out(out->topk_count, c->o_count.p, P, out->mem, c);
-            copy_out(out->contributions, c->o_contrib.p, c->n * sizeof(double), out->mem, c);
+            copy_out(out->color, c->o_color.p, P * 3 * sizeof(double), out->mem, c, kOutRec);
+            copy_out(out->depth, c->o_depth.p, P * sizeof(double), out->mem, c, kOutRec);
+            copy_out(out->alpha, c->o_alpha.p, P * sizeof(double), out->mem, c, kOutRec);
+            copy_out(out->topk_index, c->o_index.p, P * k * sizeof(int32_t), out->mem, c, kOutRec);
+            copy_out(out->topk_weight, c->o_weight.p, P * k * sizeof(double), out->mem, c, kOutRec);
+            copy_out(out->topk_count, c->o_count.p, P, out->mem, c, kOutRec);
+            copy_out(out->contributions, c->o_contrib.p, c->n * sizeof(double), out->mem, c, kOutRec);
             out->generation = c->generation;
             out->map_size = c->n;
             if (out->mem == TK_HOST) sync(c);
@@ -1092,6 +1166,7 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
         const Records r = resolve_records(c, topk, "render_feature");
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
         const int64_t P = static_cast<int64_t>(r.w) * r.h;
+        wait_out(c, kOutF);
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_out, P * std::max(c->d, 1));
         tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, dst, r.w, r.h};
         {
@@ -1101,9 +1176,9 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
         c->launches += P > 0;
         CK_LAUNCH(c);
         c->fout_pixels = P;
-        if (out && out_mem == TK_HOST) {
-            copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
-            sync(c);
+        if (out && out_mem != TK_DEVICE) {
+            copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), out_mem, c, kOutF);
+            if (out_mem == TK_HOST) sync(c);
         }
         side_done(c, true);
     });
@@ -1125,12 +1200,13 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
         if (!grad) {
             if (grad_mem != TK_DEVICE) fail(TK_ERR_BAD_ARG, "null grad_feature");
             g = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
-        } else if (grad_mem == TK_HOST) {
+        } else if (grad_mem != TK_DEVICE) {
             float* dg = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
-            copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
+            copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), grad_mem, c);
             g = dg;
         }
         const SlotIndex si = build_slot_index(c, r);
+        wait_out(c, kOutDF);
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_grad_out, n * std::max(c->d, 1));
         tk::FeatBwdParams fp{n, r.k, c->d, si.seg, si.slots, si.wnorm, g, dst};
         {
@@ -1139,9 +1215,9 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
         }
         c->launches += n > 0;
         CK_LAUNCH(c);
-        if (out && out_mem == TK_HOST) {
-            copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), TK_HOST, c);
-            sync(c);
+        if (out && out_mem != TK_DEVICE) {
+            copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), out_mem, c, kOutDF);
+            if (out_mem == TK_HOST) sync(c);
         }
         side_done(c, true);
     });
@@ -1171,7 +1247,7 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
         ensure_scratch(c, P + 1);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
         tk::scan_exclusive(gp.list_count, off, P + 1, dscal + 6, c->scratch.p, st, &c->launches);
-        CK(cudaMemcpyAsync(c->hscal + 6, dscal + 6, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        tk::copy_words_to_mapped(c->hscal_dev + 6, dscal + 6, 1, st);
         sync(c);
         const int64_t total = c->hscal[6];
         if (total > INT32_MAX) fail(TK_ERR_BAD_ARG, "contributor lists exceed 2^31 entries");
@@ -1217,18 +1293,19 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         const int64_t n = c->n;
         const double* gc = grad_color;
         const double* gd = grad_depth;
-        if (grad_mem == TK_HOST) {
+        if (grad_mem != TK_DEVICE) {
             double* dgc = ensure<double>(c->g_color_in, P * 3);
-            copy_in(dgc, grad_color, P * 3 * sizeof(double), TK_HOST, c);
+            copy_in(dgc, grad_color, P * 3 * sizeof(double), grad_mem, c);
             gc = dgc;
             if (grad_depth) {
                 double* dgd = ensure<double>(c->g_depth_in, P);
-                copy_in(dgd, grad_depth, P * sizeof(double), TK_HOST, c);
+                copy_in(dgd, grad_depth, P * sizeof(double), grad_mem, c);
                 gd = dgd;
             }
         }
         double* mid = geom_sweep(c, f, gc, gd);
         const bool dev_out = out && out->mem == TK_DEVICE;
+        wait_out(c, kOutGG);
         tk::ChainParams cp = chain_params(c, pose, cam, s, mid);
         cp.g_mean = dev_out && out->mean ? out->mean : ensure<double>(c->gg_mean, n * 3);
         cp.g_log_scale = dev_out && out->log_scale ? out->log_scale : ensure<double>(c->gg_ls, n * 3);
@@ -1246,15 +1323,21 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         c->launches += 3;
         CK_LAUNCH(c);
         if (out) {
-            if (out->mem == TK_HOST) {
-                copy_out(out->mean, cp.g_mean, n * 3 * sizeof(double), TK_HOST, c);
-                copy_out(out->log_scale, cp.g_log_scale, n * 3 * sizeof(double), TK_HOST, c);
-                copy_out(out->rotation, cp.g_rotation, n * 4 * sizeof(double), TK_HOST, c);
-                copy_out(out->opacity_logit, cp.g_opacity_logit, n * sizeof(double), TK_HOST, c);
-                copy_out(out->color, cp.g_color, n * 3 * sizeof(double), TK_HOST, c);
+            if (out->mem != TK_DEVICE) {
+                copy_out(out->mean, cp.g_mean, n * 3 * sizeof(double), out->mem, c, kOutGG);
+                copy_out(out->log_scale, cp.g_log_scale, n * 3 * sizeof(double), out->mem, c, kOutGG);
+                copy_out(out->rotation, cp.g_rotation, n * 4 * sizeof(double), out->mem, c, kOutGG);
+                copy_out(out->opacity_logit, cp.g_opacity_logit, n * sizeof(double), out->mem, c, kOutGG);
+                copy_out(out->color, cp.g_color, n * 3 * sizeof(double), out->mem, c, kOutGG);
             }
-            copy_out(out->pose_twist, tout, 6 * sizeof(double), TK_HOST, c);
-            sync(c);
+            if (out->mem == TK_HOST_ASYNC) {  // the twist lands in the struct at tk_synchronize
+                // 48 bytes stored by a kernel: not queued behind the large copies of s_out
+                tk::copy_words_to_mapped(c->h_twist_dev, tout, 6, c->cur);
+                c->twist_dst = out->pose_twist;
+            } else {
+                copy_out(out->pose_twist, tout, 6 * sizeof(double), TK_HOST, c);
+                sync(c);
+            }
         }
         side_done(c, false);
     });
@@ -1403,7 +1486,7 @@ tk_status tk_keyframe_set(tk_ctx* c, int32_t slot, const tk_pose* pose, const tk
         tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, dep, c->cur);
         c->launches += 1;
         CK_LAUNCH(c);
-        CK(cudaMemcpyAsync(c->hscal + 9, dscal + 9, sizeof(int64_t), cudaMemcpyDeviceToHost, c->cur));
+        tk::copy_words_to_mapped(c->hscal_dev + 9, dscal + 9, 1, c->cur);
         sync(c);
         k.depth_n = c->hscal[9];
         main_done(c);
@@ -1557,8 +1640,8 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             c->launches += 1;
             CK_LAUNCH(c);
         }
-        if (!c->hvals) CK(cudaHostAlloc(reinterpret_cast<void**>(&c->hvals), 4 * sizeof(double), cudaHostAllocDefault));
-        CK(cudaMemcpyAsync(c->hvals, values, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        tk::copy_words_to_mapped(c->hvals_dev, values, 3, st);
+        c->has_values = true;
         // backward_geometric (mapper.cpp:179-180) on this forward
         double* mid = geom_sweep(c, f, gc, gd);
         {
@@ -1655,7 +1738,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
 
 tk_status tk_loss_values(tk_ctx* c, double values[3]) {
     return guarded([&] {
-        if (!c->hvals) fail(TK_ERR_STATE, "no optimize_step has run");
+        if (!c->has_values) fail(TK_ERR_STATE, "no optimize_step has run");
         CK(cudaSetDevice(c->device));
         CK(cudaStreamSynchronize(c->stream));
         std::memcpy(values, c->hvals, 3 * sizeof(double));
@@ -1733,7 +1816,7 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
         ensure_scratch(c, ns + 1);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
         tk::scan_exclusive(flag32, slot, ns, dscal + 10, c->scratch.p, st, &c->launches);
-        CK(cudaMemcpyAsync(c->hscal + 10, dscal + 10, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        tk::copy_words_to_mapped(c->hscal_dev + 10, dscal + 10, 1, st);
         sync(c);
         const int64_t total = c->hscal[10];
         c->launches += 1;
