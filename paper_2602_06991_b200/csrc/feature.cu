@@ -2,6 +2,8 @@
 // check.  fp32 features, HBM-bound: one warp per output row, 128-bit loads of the K selected
 // D-channel rows (read-only path) and 128-bit streaming stores of the output row.
 #include "feature.cuh"
+
+#include <algorithm>
 #include "sort.cuh"
 
 namespace tk {
@@ -268,26 +270,43 @@ __global__ void k_slot_fill(SlotKeyParams p, const int32_t* __restrict__ seg, in
     if (j < p.count[px] && id >= 0) recs[seg[id] + atomicAdd(&cursor[id], 1)] = static_cast<uint32_t>(s);
 }
 
-// One warp per Gaussian: rank of each record among its segment (slots are unique).
-__global__ void __launch_bounds__(kThreads) k_seg_sort(const int32_t* __restrict__ seg, int64_t n,
-                                                       const uint32_t* __restrict__ recs,
-                                                       uint32_t* __restrict__ sorted) {
+// Segments of <= kSmallSeg records (the common case: a few records per Gaussian) are ranked by
+// one thread each (count of smaller slot ids, from L1); longer ones are queued for a warp each.
+constexpr int kSmallSeg = 16;
+__global__ void k_seg_sort_small(const int32_t* __restrict__ seg, int64_t n, const uint32_t* __restrict__ recs,
+                                 uint32_t* __restrict__ sorted, int32_t* __restrict__ big, int32_t* __restrict__ n_big) {
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int r0 = seg[g], L = seg[g + 1] - r0;
+        if (L > kSmallSeg) {
+            big[atomicAdd(n_big, 1)] = static_cast<int32_t>(g);
+            continue;
+        }
+        for (int i = 0; i < L; ++i) {
+            const uint32_t v = recs[r0 + i];
+            int rank = 0;
+            for (int q = 0; q < L; ++q) rank += recs[r0 + q] < v ? 1 : 0;
+            sorted[r0 + rank] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_seg_sort_big(const int32_t* __restrict__ seg,
+                                                           const int32_t* __restrict__ big,
+                                                           const int32_t* __restrict__ n_big,
+                                                           const uint32_t* __restrict__ recs,
+                                                           uint32_t* __restrict__ sorted) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < n; g += nw) {
+    const int nb = *n_big;
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; w < nb; w += nw) {
+        const int64_t g = big[w];
         const int r0 = seg[g], L = seg[g + 1] - r0;
-        if (L <= 32) {
-            const uint32_t v = lane < L ? recs[r0 + lane] : 0xffffffffu;
+        for (int i = lane; i < L; i += 32) {
+            const uint32_t v = recs[r0 + i];
             int rank = 0;
-            for (int q = 0; q < L; ++q) rank += __shfl_sync(0xffffffffu, v, q) < v ? 1 : 0;
-            if (lane < L) sorted[r0 + rank] = v;
-        } else {
-            for (int i = lane; i < L; i += 32) {
-                const uint32_t v = recs[r0 + i];
-                int rank = 0;
-                for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
-                sorted[r0 + rank] = v;
-            }
+            for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
+            sorted[r0 + rank] = v;
         }
     }
 }
@@ -428,8 +447,17 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt
     scan_exclusive(cnt_seg, cnt_seg, n_gaussians + 1, total, scan_scratch, st, launches);
     if (p.n_slots > 0) k_slot_fill<<<g, 256, 0, st>>>(p, cnt_seg, cursor, recs);
     dbg_launch("k_slot_fill", st);
-    if (n_gaussians > 0) k_seg_sort<<<warp_grid(n_gaussians), kThreads, 0, st>>>(cnt_seg, n_gaussians, recs, sorted);
-    dbg_launch("k_seg_sort", st);
+    if (n_gaussians > 0) {
+        // the queue of long segments reuses the cursor array (its counts are no longer needed)
+        int32_t* n_big = cursor + n_gaussians;
+        cudaMemsetAsync(n_big, 0, sizeof(int32_t), st);
+        const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((n_gaussians + 255) / 256, 148 * 16));
+        k_seg_sort_small<<<g1, 256, 0, st>>>(cnt_seg, n_gaussians, recs, sorted, cursor, n_big);
+        dbg_launch("k_seg_sort_small", st);
+        k_seg_sort_big<<<148 * 4, kThreads, 0, st>>>(cnt_seg, cursor, n_big, recs, sorted);
+        dbg_launch("k_seg_sort_big", st);
+        *launches += 1;
+    }
     *launches += 3;
 }
 
