@@ -52,7 +52,7 @@ struct ChainParams {
     double* g_rotation;
     double* g_opacity_logit;
     double* g_color;
-    double* twist;  // n x 6, or null (mapping: no pose gradient)
+    double* twist;  // ceil(n / 128) x 6 block partials, or null (mapping: no pose gradient)
 };
 
 // In-place Adam over the five geometry groups (optimizer.hpp:25-53 layout: one m / v array per
@@ -81,7 +81,7 @@ void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);
 // Adam + clamps + renormalisation + peak statistic over every Gaussian (thread per Gaussian)
 void launch_geo_adam(const GeoAdamParams& a, int64_t n, cudaStream_t st);
-// deterministic two-level sum of twist[n][6] -> out[6] (device)
+// deterministic sum of k_chain's per-block twist partials -> out[6] (device)
 void launch_twist_reduce(const double* twist, int64_t n, double* partial, double* out, cudaStream_t st);
 
 }  // namespace tk

@@ -1312,7 +1312,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         cp.g_rotation = dev_out && out->rotation ? out->rotation : ensure<double>(c->gg_rot, n * 4);
         cp.g_opacity_logit = dev_out && out->opacity_logit ? out->opacity_logit : ensure<double>(c->gg_op, n);
         cp.g_color = dev_out && out->color ? out->color : ensure<double>(c->gg_col, n * 3);
-        cp.twist = ensure<double>(c->twist, n * 6);
+        cp.twist = ensure<double>(c->twist, (n + 127) / 128 * 6);
         double* tpart = ensure<double>(c->twist_part, 148 * 6);
         double* tout = ensure<double>(c->twist_out, 6);
         {
@@ -1320,7 +1320,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
             tk::launch_chain(cp, st);
             tk::launch_twist_reduce(cp.twist, n, tpart, tout, st);
         }
-        c->launches += 3;
+        c->launches += 2;
         CK_LAUNCH(c);
         if (out) {
             if (out->mem != TK_DEVICE) {
