@@ -123,7 +123,8 @@ typedef struct { /* GeomGrads, raster/backward.hpp:15-22; NULL pointers are skip
     double* rotation;      /* n x 4 (w,x,y,z) */
     double* opacity_logit; /* n */
     double* color;         /* n x 3 */
-    double pose_twist[6];  /* out: [nu, omega] */
+    double pose_twist[6];  /* out: [nu, omega]; with TK_HOST_ASYNC written at tk_synchronize
+                            * (the struct must stay alive until then) */
 } tk_geom_grads;
 
 typedef struct { /* resident device buffers of the last calls (read-only views) */

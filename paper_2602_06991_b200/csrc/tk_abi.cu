@@ -189,9 +189,13 @@ struct tk_ctx {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     cudaEvent_t ev_cmp = nullptr, ev_in = nullptr, ev_out[5] = {};
     bool out_pending[5] = {};
-    double* h_twist = nullptr;    // host-mapped pose twist of an asynchronous backward_geometric
+    // pose twists of asynchronous backward_geometric calls: a ring of host-mapped slots, copied
+    // into the callers' structs at tk_synchronize
+    static constexpr int kTwistSlots = 64;
+    double* h_twist = nullptr;
     double* h_twist_dev = nullptr;
-    double* twist_dst = nullptr;  //   copied into the caller's struct at tk_synchronize
+    std::vector<std::pair<double*, int>> twist_pending;
+    int twist_next = 0;
     bool feat_pending = false, geo_pending = false;
     int64_t launches = 0;
     Profiler prof;
@@ -929,7 +933,9 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         for (cudaEvent_t* ev : {&c->ev_cmp, &c->ev_in, &c->ev_out[0], &c->ev_out[1], &c->ev_out[2], &c->ev_out[3],
                                 &c->ev_out[4]})
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
-        if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_twist), 8 * sizeof(double), cudaHostAllocMapped);
+        if (e == cudaSuccess)
+            e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_twist), tk_ctx::kTwistSlots * 8 * sizeof(double),
+                              cudaHostAllocMapped);
         if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->h_twist_dev), c->h_twist, 0);
         if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hvals), 4 * sizeof(double), cudaHostAllocMapped);
         if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hvals_dev), c->hvals, 0);
@@ -999,10 +1005,8 @@ tk_status tk_synchronize(tk_ctx* c) {
         CK(cudaStreamSynchronize(c->s_in));
         CK(cudaStreamSynchronize(c->s_out));
         for (bool& b : c->out_pending) b = false;
-        if (c->twist_dst) {
-            std::memcpy(c->twist_dst, c->h_twist, 6 * sizeof(double));
-            c->twist_dst = nullptr;
-        }
+        for (const auto& t : c->twist_pending) std::memcpy(t.first, c->h_twist + 8 * t.second, 6 * sizeof(double));
+        c->twist_pending.clear();
     });
 }
 
@@ -1331,9 +1335,17 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
                 copy_out(out->color, cp.g_color, n * 3 * sizeof(double), out->mem, c, kOutGG);
             }
             if (out->mem == TK_HOST_ASYNC) {  // the twist lands in the struct at tk_synchronize
+                if (static_cast<int>(c->twist_pending.size()) == tk_ctx::kTwistSlots) {  // ring full: drain it
+                    sync(c);
+                    for (const auto& t : c->twist_pending)
+                        std::memcpy(t.first, c->h_twist + 8 * t.second, 6 * sizeof(double));
+                    c->twist_pending.clear();
+                }
+                const int slot = c->twist_next;
+                c->twist_next = (c->twist_next + 1) % tk_ctx::kTwistSlots;
                 // 48 bytes stored by a kernel: not queued behind the large copies of s_out
-                tk::copy_words_to_mapped(c->h_twist_dev, tout, 6, c->cur);
-                c->twist_dst = out->pose_twist;
+                tk::copy_words_to_mapped(c->h_twist_dev + 8 * slot, tout, 6, c->cur);
+                c->twist_pending.emplace_back(out->pose_twist, slot);
             } else {
                 copy_out(out->pose_twist, tout, 6 * sizeof(double), TK_HOST, c);
                 sync(c);
