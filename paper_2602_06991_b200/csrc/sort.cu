@@ -226,9 +226,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
     hist[static_cast<int64_t>(threadIdx.x) * nb + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// Stable scatter: rank every key of the block's tile (match_any within warps, prefix across
-// warps and rounds), place it digit-sorted in shared memory, then write each digit's run to
-// its global offset with consecutive threads on consecutive addresses.
+// Stable scatter.  Each warp owns a contiguous 256-key slice of the block's 2048-key tile and
+// ranks its keys round by round (match_any) against a warp-private digit counter row, so the
+// ranking needs no block barrier; one block scan over (digit, warp) counts then gives every
+// key's position in the digit-sorted tile, which is staged in shared memory and written out with
+// consecutive threads on consecutive addresses of each digit's global run.
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
@@ -236,8 +238,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
                                                            int nb) {
     __shared__ int32_t gbase[RS_RADIX];
     __shared__ int32_t lstart[RS_RADIX];
-    __shared__ int32_t run[RS_RADIX];
-    __shared__ int32_t wc[RS_WARPS][RS_RADIX];
+    __shared__ int32_t wc[RS_WARPS][RS_RADIX];  // per-warp digit counts, then per-(warp, digit) offsets
     __shared__ K skey[RS_TILE];
     __shared__ uint32_t sval[RS_TILE];
     __shared__ int32_t wsum[RS_WARPS];
@@ -246,30 +247,37 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * RS_TILE;
     const int tile_n = static_cast<int>(n - tile0 < RS_TILE ? n - tile0 : RS_TILE);
     gbase[tid] = offs[static_cast<int64_t>(tid) * nb + blockIdx.x];
-    run[tid] = 0;
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
-    // local digit counts of the tile -> lstart (exclusive prefix over digits)
+    __syncthreads();
+    constexpr int kSlice = RS_TILE / RS_WARPS;  // 256 keys per warp
     K key[RS_ROUNDS];
     uint32_t val[RS_ROUNDS];
     unsigned dig[RS_ROUNDS];
-    __syncthreads();
+    int pos[RS_ROUNDS];
 #pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
-        const int li = r * RS_THREADS + tid;
+        const int li = warp * kSlice + r * 32 + lane;
         dig[r] = RS_RADIX;
         if (li < tile_n) {
             key[r] = kin[tile0 + li];
             val[r] = vin[tile0 + li];
             dig[r] = static_cast<unsigned>(key[r] >> shift) & 0xffu;
         }
-        const unsigned peers = __match_any_sync(0xffffffffu, dig[r]);
-        if (dig[r] < RS_RADIX && lane == __ffs(peers) - 1) atomicAdd(&run[dig[r]], __popc(peers));
+        const unsigned d = dig[r];
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const int rank = __popc(peers & lt);
+        pos[r] = (d < RS_RADIX ? wc[warp][d] : 0) + rank;  // rank among this warp's keys of digit d
+        __syncwarp();
+        if (d < RS_RADIX && rank == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
-    {  // block exclusive scan of run[] (256 digits, one per thread) into lstart
-        const int v = run[tid];
-        int incl = v;
+    {  // thread = digit: counts over warps, exclusive over digits (lstart), then per-warp offsets
+        int32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) tot += wc[w][tid];
+        int incl = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int u = __shfl_up_sync(0xffffffffu, incl, o);
@@ -279,38 +287,27 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
         __syncthreads();
         int woff = 0;
         for (int w = 0; w < warp; ++w) woff += wsum[w];
-        lstart[tid] = woff + incl - v;
-        run[tid] = 0;
+        const int32_t start = woff + incl - tot;
+        lstart[tid] = start;
+        int32_t acc = start;
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) {
+            const int32_t c = wc[w][tid];
+            wc[w][tid] = acc;
+            acc += c;
+        }
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < RS_ROUNDS; ++r) {
         const unsigned d = dig[r];
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const int rank = __popc(peers & lt);
-        if (d < RS_RADIX && rank == 0) wc[warp][d] = __popc(peers);
-        __syncthreads();
-        {  // thread d: prefix over warps, continuing this digit's running count
-            int32_t acc = run[tid];
-#pragma unroll
-            for (int w = 0; w < RS_WARPS; ++w) {
-                const int32_t c = wc[w][tid];
-                wc[w][tid] = acc;
-                acc += c;
-            }
-            run[tid] = acc;
-        }
-        __syncthreads();
         if (d < RS_RADIX) {
-            const int lpos = lstart[d] + wc[warp][d] + rank;
+            const int lpos = wc[warp][d] + pos[r];
             skey[lpos] = key[r];
             sval[lpos] = val[r];
         }
-        __syncthreads();
-#pragma unroll
-        for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
-        __syncthreads();
     }
+    __syncthreads();
     for (int j = tid; j < tile_n; j += RS_THREADS) {
         const K kj = skey[j];
         const unsigned d = static_cast<unsigned>(kj >> shift) & 0xffu;
