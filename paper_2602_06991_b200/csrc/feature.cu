@@ -270,16 +270,29 @@ __global__ void k_slot_fill(SlotKeyParams p, const int32_t* __restrict__ seg, in
     if (j < p.count[px] && id >= 0) recs[seg[id] + atomicAdd(&cursor[id], 1)] = static_cast<uint32_t>(s);
 }
 
-// Segments of <= kSmallSeg records (the common case: a few records per Gaussian) are ranked by
-// one thread each (count of smaller slot ids, from L1); longer ones are queued for a warp each.
+// Deterministic order inside each Gaussian's record segment (ascending slot id), by length tier:
+// <= kSmallSeg records: one thread ranks them (count of smaller ids, from L1);
+// <= kWarpSeg: one warp (rank counts up to 128 records, a shared-memory bitonic sort beyond);
+// longer: one block bitonic-sorts kSortTile-record tiles and merges them by rank.
+// The medium and long segments are queued by the thread pass (medium from the front of `queue`,
+// long from the back; counters in counts[0], counts[1]).
 constexpr int kSmallSeg = 16;
+constexpr int kWarpSeg = 1024;
+constexpr int kSortTile = 8192;
+constexpr int kSortThreads = 512;
+
 __global__ void k_seg_sort_small(const int32_t* __restrict__ seg, int64_t n, const uint32_t* __restrict__ recs,
-                                 uint32_t* __restrict__ sorted, int32_t* __restrict__ big, int32_t* __restrict__ n_big) {
+                                 uint32_t* __restrict__ sorted, int32_t* __restrict__ queue,
+                                 int32_t* __restrict__ counts) {
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int r0 = seg[g], L = seg[g + 1] - r0;
+        if (L > kWarpSeg) {
+            queue[n - 1 - atomicAdd(counts + 1, 1)] = static_cast<int32_t>(g);
+            continue;
+        }
         if (L > kSmallSeg) {
-            big[atomicAdd(n_big, 1)] = static_cast<int32_t>(g);
+            queue[atomicAdd(counts, 1)] = static_cast<int32_t>(g);
             continue;
         }
         for (int i = 0; i < L; ++i) {
@@ -291,23 +304,108 @@ __global__ void k_seg_sort_small(const int32_t* __restrict__ seg, int64_t n, con
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_seg_sort_big(const int32_t* __restrict__ seg,
-                                                           const int32_t* __restrict__ big,
-                                                           const int32_t* __restrict__ n_big,
-                                                           const uint32_t* __restrict__ recs,
-                                                           uint32_t* __restrict__ sorted) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int nb = *n_big;
-    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; w < nb; w += nw) {
-        const int64_t g = big[w];
-        const int r0 = seg[g], L = seg[g + 1] - r0;
-        for (int i = lane; i < L; i += 32) {
-            const uint32_t v = recs[r0 + i];
-            int rank = 0;
-            for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
-            sorted[r0 + rank] = v;
+struct WarpSync {
+    __device__ void operator()() const { __syncwarp(); }
+};
+struct BlockSync {
+    __device__ void operator()() const { __syncthreads(); }
+};
+
+// In-place ascending bitonic sort of a[0..m), m a power of two, by `nthreads` cooperating threads
+// with index `t`; `sync` is the matching barrier (__syncwarp / __syncthreads).
+template <class Sync>
+__device__ __forceinline__ void bitonic_sort(uint32_t* a, int m, int t, int nthreads, Sync sync) {
+    for (int size = 2; size <= m; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            sync();
+            for (int i = t; i < (m >> 1); i += nthreads) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint32_t x = a[lo], y = a[hi];
+                if ((x > y) == up) {
+                    a[lo] = y;
+                    a[hi] = x;
+                }
+            }
         }
+    sync();
+}
+
+__global__ void __launch_bounds__(kThreads) k_seg_sort_warp(const int32_t* __restrict__ seg,
+                                                            const int32_t* __restrict__ queue,
+                                                            const int32_t* __restrict__ counts,
+                                                            const uint32_t* __restrict__ recs,
+                                                            uint32_t* __restrict__ sorted) {
+    __shared__ uint32_t buf[kWarps][kWarpSeg];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int nm = counts[0];
+    uint32_t* a = buf[warp];
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; w < nm; w += nw) {
+        const int64_t g = queue[w];
+        const int r0 = seg[g], L = seg[g + 1] - r0;
+        if (L <= 128) {  // short enough for a direct rank count (L^2 / 32 compares per lane)
+            for (int i = lane; i < L; i += 32) {
+                const uint32_t v = recs[r0 + i];
+                int rank = 0;
+                for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
+                sorted[r0 + rank] = v;
+            }
+            continue;
+        }
+        int m = 32;
+        while (m < L) m <<= 1;
+        for (int i = lane; i < m; i += 32) a[i] = i < L ? recs[r0 + i] : 0xffffffffu;
+        bitonic_sort(a, m, lane, 32, WarpSync{});
+        for (int i = lane; i < L; i += 32) sorted[r0 + i] = a[i];
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_seg_sort_block(const int32_t* __restrict__ seg, int64_t n,
+                                                                 const int32_t* __restrict__ queue,
+                                                                 const int32_t* __restrict__ counts,
+                                                                 uint32_t* __restrict__ recs,
+                                                                 uint32_t* __restrict__ sorted) {
+    __shared__ uint32_t tile[kSortTile];
+    const int nh = counts[1];
+    for (int w = blockIdx.x; w < nh; w += gridDim.x) {
+        const int64_t g = queue[n - 1 - w];
+        const int r0 = seg[g], L = seg[g + 1] - r0;
+        const int ntiles = (L + kSortTile - 1) / kSortTile;
+        for (int t = 0; t < ntiles; ++t) {  // sort each tile; results to sorted[]
+            const int t0 = t * kSortTile, tn = min(kSortTile, L - t0);
+            int m = 1;
+            while (m < tn) m <<= 1;
+            __syncthreads();
+            for (int i = threadIdx.x; i < m; i += blockDim.x) tile[i] = i < tn ? recs[r0 + t0 + i] : 0xffffffffu;
+            bitonic_sort(tile, m, threadIdx.x, blockDim.x, BlockSync{});
+            for (int i = threadIdx.x; i < tn; i += blockDim.x) sorted[r0 + t0 + i] = tile[i];
+        }
+        __syncthreads();
+        if (ntiles == 1) continue;
+        // merge: final rank = rank in own tile + lower bound in every other tile (ids are unique)
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+            const uint32_t v = sorted[r0 + i];
+            const int own = i / kSortTile;
+            int rank = i - own * kSortTile;
+            for (int t = 0; t < ntiles; ++t) {
+                if (t == own) continue;
+                int lo = 0, hi = min(kSortTile, L - t * kSortTile);
+                const uint32_t* tp = sorted + r0 + t * kSortTile;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (tp[mid] < v) lo = mid + 1;
+                    else hi = mid;
+                }
+                rank += lo;
+            }
+            recs[r0 + rank] = v;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < L; i += blockDim.x) sorted[r0 + i] = recs[r0 + i];
+        __syncthreads();
     }
 }
 
@@ -448,17 +546,19 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt
     if (p.n_slots > 0) k_slot_fill<<<g, 256, 0, st>>>(p, cnt_seg, cursor, recs);
     dbg_launch("k_slot_fill", st);
     if (n_gaussians > 0) {
-        // the queue of long segments reuses the cursor array (its counts are no longer needed)
-        int32_t* n_big = cursor + n_gaussians;
-        cudaMemsetAsync(n_big, 0, sizeof(int32_t), st);
+        // the queues of medium / long segments reuse the cursor array (its counts are no longer
+        // needed); cursor holds n_gaussians + 2 entries, the last two are the queue counters
+        int32_t* counts = cursor + n_gaussians;
+        cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
         const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((n_gaussians + 255) / 256, 148 * 16));
-        k_seg_sort_small<<<g1, 256, 0, st>>>(cnt_seg, n_gaussians, recs, sorted, cursor, n_big);
+        k_seg_sort_small<<<g1, 256, 0, st>>>(cnt_seg, n_gaussians, recs, sorted, cursor, counts);
         dbg_launch("k_seg_sort_small", st);
-        k_seg_sort_big<<<148 * 4, kThreads, 0, st>>>(cnt_seg, cursor, n_big, recs, sorted);
-        dbg_launch("k_seg_sort_big", st);
-        *launches += 1;
+        k_seg_sort_warp<<<148 * 4, kThreads, 0, st>>>(cnt_seg, cursor, counts, recs, sorted);
+        dbg_launch("k_seg_sort_warp", st);
+        k_seg_sort_block<<<148, kSortThreads, 0, st>>>(cnt_seg, n_gaussians, cursor, counts, recs, sorted);
+        dbg_launch("k_seg_sort_block", st);
+        *launches += 2;
     }
-    *launches += 3;
 }
 
 void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st) {

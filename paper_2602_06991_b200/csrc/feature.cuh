@@ -54,6 +54,7 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
 void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st);
 // Inverted index of the records by counting: cnt_seg (n+1) becomes the segment offsets, recs /
 // sorted hold the valid slot ids grouped by Gaussian (sorted: ascending within each segment).
+// cursor: n + 2 int32 of scratch.
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
                        uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches);
 void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st);

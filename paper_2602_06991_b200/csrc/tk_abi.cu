@@ -720,7 +720,7 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     const int64_t n = c->n;
     uint32_t* recs = ensure<uint32_t>(c->s_keys, slots);
     uint32_t* svals = ensure<uint32_t>(c->s_vals, slots);
-    int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 1);
+    int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 2);
     float* wn = ensure<float>(c->s_wnorm, slots);
     int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
     ensure_scratch(c, std::max<int64_t>(slots, n + 1), true);

@@ -294,3 +294,24 @@ def test_backward_feature_bit_deterministic(R):
     a = R.backward_feature(m, g.topk, gf)
     b = R.backward_feature(m, g.topk, gf)
     assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("w,h", [(64, 48), (160, 120)])
+def test_backward_feature_huge_segments(R, w, h):
+    """A Gaussian filling the view owns one Top-K record per pixel: segments beyond the block sort
+    tile (8192 records at 160x120) take the tiled bitonic + merge-by-rank path."""
+    m = synth.random_scene(300, 16, 4)
+    m.mean[1:, 2] += 3.0          # everything else behind the big one
+    m.mean[0] = (0.0, 0.0, 0.95)  # in front; z > 3 exp(max log_scale) keeps it past the cull
+    m.log_scale[0] = (-1.25, -1.25, -1.25)
+    m.opacity_logit[0] = -2.0
+    cam = synth.test_camera(w, h)
+    g = R.render_geometric(m, Pose(), cam, RenderSettings(top_k=4))
+    counts = np.bincount(g.topk.index[g.topk.index >= 0], minlength=m.size())
+    assert counts.max() > (8192 if w * h > 8192 else 100)
+    gf = synth.uniform_image((h, w, 16), 5).astype(np.float32)
+    a = R.backward_feature(m, g.topk, gf)
+    b = R.backward_feature(m, g.topk, gf)
+    assert a.tobytes() == b.tobytes()
+    o = O.backward_feature(m, w, h, 4, g.topk.index, g.topk.weight, g.topk.count, gf.astype(np.float64))
+    feat_close(a, o, 2e-5)
