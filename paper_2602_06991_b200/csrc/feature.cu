@@ -409,66 +409,135 @@ __global__ void __launch_bounds__(kSortThreads) k_seg_sort_block(const int32_t* 
     }
 }
 
+// Sum of w_j * dF[px_j] over records [r0, r1) of a segment for the channel pass at `base`
+// (acc4: 4 float4 per lane when VEC, acc1: 4 floats otherwise), records in slot order.
+template <bool VEC>
+__device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, int r1, int base, int lane,
+                                              float4 (&acc4)[4], float (&acc1)[4]) {
+    const int D = p.d;
+    const int dd = VEC ? D >> 2 : D;
+    for (int r = r0; r < r1; r += 32) {
+        const int nr = min(32, r1 - r);
+        int64_t spx = 0;
+        float sw = 0.f;
+        if (lane < nr) {
+            const uint32_t s = p.slots[r + lane];
+            spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+            sw = p.wnorm[s];
+        }
+#pragma unroll 2
+        for (int j = 0; j < nr; ++j) {
+            const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
+            float wj = __shfl_sync(0xffffffffu, sw, j);
+            if (!isfinite(wj)) {
+                // Zero-weight records: the reference skips pixels whose gradient row is all zero
+                // (backward.cpp:296-302), so 0/0 only propagates for live rows.
+                bool any = false;
+                for (int q = lane; q < D; q += 32) any |= p.grad[pxj * D + q] != 0.0f;
+                if (!__any_sync(0xffffffffu, any)) continue;
+            }
+            if (VEC) {
+                const float4* row = reinterpret_cast<const float4*>(p.grad + pxj * D);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    if (q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
+                }
+            } else {
+                const float* row = p.grad + pxj * D;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    if (q < dd) acc1[m] = fmaf(wj, __ldg(row + q), acc1[m]);
+                }
+            }
+        }
+    }
+}
+
+template <bool VEC>
+__device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lane, const float4 (&acc4)[4],
+                                           const float (&acc1)[4]) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int q = base + m * 32 + lane;
+        if (q < dd) {
+            if (VEC) __stcs(reinterpret_cast<float4*>(dst) + q, acc4[m]);
+            else __stcs(dst + q, acc1[m]);
+        }
+    }
+}
+
 // backward_feature (backward.cpp:288-319) as a deterministic segmented reduction: one warp per
-// Gaussian sums its records in (pixel, slot) order and writes the dense row once.
+// Gaussian sums its records in (pixel, slot) order and writes the dense row once (segments
+// longer than kLongSeg are left to the chunk / combine kernels).
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int D = p.d;
-    const int dd = VEC ? D >> 2 : D;
+    const int dd = VEC ? p.d >> 2 : p.d;
     for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n_gaussians; g += nw) {
         const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        if (r1 - r0 > kLongSeg) continue;
         for (int base = 0; base < dd; base += 128) {
             float4 acc4[4];
             float acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int r = r0; r < r1; r += 32) {
-                const int nr = min(32, r1 - r);
-                int64_t spx = 0;
-                float sw = 0.f;
-                if (lane < nr) {
-                    const uint32_t s = p.slots[r + lane];
-                    spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
-                    sw = p.wnorm[s];
-                }
-#pragma unroll 2
-                for (int j = 0; j < nr; ++j) {
-                    const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
-                    float wj = __shfl_sync(0xffffffffu, sw, j);
-                    if (!isfinite(wj)) {
-                        // Zero-weight records: the reference skips pixels whose gradient row is
-                        // all zero (backward.cpp:296-302), so 0/0 only propagates for live rows.
-                        bool any = false;
-                        for (int q = lane; q < D; q += 32) any |= p.grad[pxj * D + q] != 0.0f;
-                        if (!__any_sync(0xffffffffu, any)) continue;
-                    }
-                    if (VEC) {
-                        const float4* row = reinterpret_cast<const float4*>(p.grad + pxj * D);
+            accum_records<VEC>(p, r0, r1, base, lane, acc4, acc1);
+            store_pass<VEC>(p.out + g * p.d, dd, base, lane, acc4, acc1);
+        }
+    }
+}
+
+// One thread per queued long segment: reserve its chunk range and list its chunks.
+__global__ void k_long_plan(const int32_t* __restrict__ seg, int64_t n, LongPlan plan) {
+    const int nq = *plan.qcount;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x) {
+        const int g = plan.queue[n - 1 - i];
+        const int L = seg[g + 1] - seg[g];
+        if (L <= kLongSeg) continue;
+        const int nch = (L + kLongSeg - 1) / kLongSeg;
+        const int base = atomicAdd(&plan.counters[0], nch);
+        const int li = atomicAdd(&plan.counters[1], 1);
+        plan.longs[li] = make_int4(g, base, nch, 0);
+        for (int c = 0; c < nch; ++c) plan.items[base + c] = make_int4(g, c, base + c, 0);
+    }
+}
+
+// One warp per chunk of a long segment: partial sums into the plan's scratch rows.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_feat_bwd_chunks(FeatBwdParams p, LongPlan plan) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int dd = VEC ? p.d >> 2 : p.d;
+    const int ni = plan.counters[0];
+    for (int64_t it = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; it < ni; it += nw) {
+        const int4 item = plan.items[it];
+        const int s0 = p.seg[item.x];
+        const int r0 = s0 + item.y * kLongSeg, r1 = min(p.seg[item.x + 1], r0 + kLongSeg);
+        for (int base = 0; base < dd; base += 128) {
+            float4 acc4[4];
+            float acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const int q = base + m * 32 + lane;
-                            if (q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
-                        }
-                    } else {
-                        const float* row = p.grad + pxj * D;
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) {
-                            const int q = base + m * 32 + lane;
-                            if (q < dd) acc1[m] = fmaf(wj, __ldg(row + q), acc1[m]);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int q = base + m * 32 + lane;
-                if (q < dd) {
-                    if (VEC) __stcs(reinterpret_cast<float4*>(p.out + g * D) + q, acc4[m]);
-                    else __stcs(p.out + g * D + q, acc1[m]);
-                }
-            }
+            for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            accum_records<VEC>(p, r0, r1, base, lane, acc4, acc1);
+            store_pass<VEC>(plan.partial + static_cast<int64_t>(item.z) * p.d, dd, base, lane, acc4, acc1);
+        }
+    }
+}
+
+// One warp per long Gaussian: chunk partials added in chunk order, the dense row written once.
+__global__ void __launch_bounds__(kThreads) k_feat_bwd_combine(FeatBwdParams p, LongPlan plan) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int nl = plan.counters[1];
+    for (int64_t li = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; li < nl; li += nw) {
+        const int4 lg = plan.longs[li];
+        for (int q = lane; q < p.d; q += 32) {
+            float acc = 0.0f;
+            for (int c = 0; c < lg.z; ++c) acc += plan.partial[static_cast<int64_t>(lg.y + c) * p.d + q];
+            p.out[static_cast<int64_t>(lg.x) * p.d + q] = acc;
         }
     }
 }
@@ -561,11 +630,24 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt
     }
 }
 
-void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st) {
+void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st) {
+    cudaMemsetAsync(plan.counters, 0, 2 * sizeof(int32_t), st);
+    if (n <= 0) return;
+    k_long_plan<<<16, 256, 0, st>>>(seg, n, plan);
+    dbg_launch("k_long_plan", st);
+}
+
+void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st) {
     if (p.n_gaussians <= 0 || p.d <= 0) return;
-    if (vec_ok(p.grad, p.out, p.d)) k_feat_bwd<true><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
+    const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0;
+    if (vec) k_feat_bwd<true><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
     else k_feat_bwd<false><<<warp_grid(p.n_gaussians), kThreads, 0, st>>>(p);
     dbg_launch("k_feat_bwd", st);
+    if (vec) k_feat_bwd_chunks<true><<<148 * 8, kThreads, 0, st>>>(p, plan);
+    else k_feat_bwd_chunks<false><<<148 * 8, kThreads, 0, st>>>(p, plan);
+    dbg_launch("k_feat_bwd_chunks", st);
+    k_feat_bwd_combine<<<148 * 4, kThreads, 0, st>>>(p, plan);
+    dbg_launch("k_feat_bwd_combine", st);
 }
 
 void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st) {

@@ -49,6 +49,25 @@ struct FeatBwdParams {
     float* out;            // N x D
 };
 
+// Gaussians with more than kLongSeg records (a Gaussian filling the view owns one record per
+// pixel) are not summed by one warp: their records are cut into kLongSeg chunks summed by
+// separate warps into `partial`, then combined in chunk order (deterministic).  The plan is
+// built on the device from the long-segment queue of launch_slot_index.
+constexpr int kLongSeg = 1024;
+struct LongPlan {
+    int4* items;        // {g, chunk, slot in partial, -}
+    int4* longs;        // {g, first partial slot, chunks, -}
+    int32_t* counters;  // [0] items, [1] long Gaussians
+    float* partial;     // cap_items x D
+    int64_t cap_items;
+    const int32_t* queue;   // launch_slot_index's cursor scratch: long queue at its back
+    const int32_t* qcount;  // number of queued long segments (device)
+};
+// capacity of the chunk list for m valid records among n Gaussians
+inline int64_t long_plan_capacity(int64_t m, int64_t n) {
+    return m / kLongSeg + (m / kLongSeg < n ? m / kLongSeg : n) + 1;
+}
+
 void launch_feature_gather(const GatherParams& p, cudaStream_t st);
 void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
 void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st);
@@ -57,7 +76,11 @@ void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st);
 // cursor: n + 2 int32 of scratch.
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
                        uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches);
-void launch_feature_bwd(const FeatBwdParams& p, cudaStream_t st);
+// the long-segment queue left in cursor by launch_slot_index: entries cursor[n - 1 - i] for
+// i < cursor[n + 1]
+void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st);
+// backward_feature's reduction; long segments through plan (chunks + ordered combine)
+void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st);
 // *max_index = max over all slots (device int, preset to INT_MIN)
 void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st);
 // *first = smallest slot whose index >= n (device u64, preset to ~0)

@@ -9,6 +9,7 @@
 //     D-channel row, writes 2 sign bits per channel instead of the fp32 dL/dF image;
 //   feature Adam: per Gaussian reads the sign words of its records, then f, m, v (fp32) once.
 #include "mapping.cuh"
+#include "feature.cuh"
 #include "sort.cuh"
 
 namespace tk {
@@ -475,17 +476,66 @@ __device__ __forceinline__ float warp_sum(float s) {
     return s;
 }
 
+// Sum over records [r0, r1) of w_j * sign(F - F_gt)[px_j] for the channel pass at `base`
+// (4 float4 per lane), records in slot order.
+__device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int r1, int base, int lane, float scale,
+                                            float4 (&acc)[4]) {
+    const int d4 = p.d >> 2, wpp = (p.d + 15) >> 4;
+    const uint32_t* __restrict__ signs = p.signs;
+    for (int r = r0; r < r1; r += 32) {
+        const int nr = min(32, r1 - r);
+        int64_t spx = 0;
+        float sw = 0.f;
+        if (lane < nr) {
+            const uint32_t s = p.slots[r + lane];
+            spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+            sw = p.wnorm[s];
+        }
+        for (int j = 0; j < nr; ++j) {
+            const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
+            const float wj = __shfl_sync(0xffffffffu, sw, j);
+            const uint32_t* srow = signs + pxj * wpp;
+            if (!isfinite(wj)) {  // backward.cpp:296-302: all-zero gradient rows are skipped
+                bool any = false;
+                for (int q = lane; q < wpp; q += 32) any |= srow[q] != 0u;
+                if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q < d4) {
+                    const uint32_t b = __ldg(srow + (q >> 2)) >> (8 * (q & 3));
+                    acc[m].x += signed_w(b, 0, wj);
+                    acc[m].y += signed_w(b, 2, wj);
+                    acc[m].z += signed_w(b, 4, wj);
+                    acc[m].w += signed_w(b, 6, wj);
+                }
+            }
+        }
+    }
+}
+
 // backward_feature (backward.cpp:288-319) over the sign image, fused with the feature Adam
 // step and the renormalisation of mapper.cpp:239-252.  One warp per Gaussian (all N: Adam
-// moves every row through its moments); records summed in (pixel, slot) order.
-__global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p) {
+// moves every row through its moments); records summed in (pixel, slot) order.  LONG = false:
+// every Gaussian with <= kLongSeg records; LONG = true: the long Gaussians of the plan, whose
+// chunk partials (k_feature_adam_chunks) are added in chunk order.
+template <bool LONG>
+__global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
+    const int D = p.d, d4 = D >> 2;
     const float scale = *p.scale;
-    const uint32_t* __restrict__ signs = p.signs;
-    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
+    const int64_t count = LONG ? plan.counters[1] : p.n;
+    for (int64_t wi = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; wi < count; wi += nw) {
+        int64_t g = wi;
+        int4 lg = make_int4(0, 0, 0, 0);
+        if (LONG) {
+            lg = plan.longs[wi];
+            g = lg.x;
+        }
         const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        if (!LONG && r1 - r0 > kLongSeg) continue;
         float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
         float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
         float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
@@ -505,33 +555,20 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int r = r0; r < r1; r += 32) {
-                const int nr = min(32, r1 - r);
-                int64_t spx = 0;
-                float sw = 0.f;
-                if (lane < nr) {
-                    const uint32_t s = p.slots[r + lane];
-                    spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
-                    sw = p.wnorm[s];
-                }
-                for (int j = 0; j < nr; ++j) {
-                    const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
-                    const float wj = __shfl_sync(0xffffffffu, sw, j);
-                    const uint32_t* srow = signs + pxj * wpp;
-                    if (!isfinite(wj)) {  // backward.cpp:296-302: all-zero gradient rows are skipped
-                        bool any = false;
-                        for (int q = lane; q < wpp; q += 32) any |= srow[q] != 0u;
-                        if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
-                    }
+            if (!LONG) {
+                accum_signs(p, r0, r1, base, lane, scale, acc);
+            } else {
+                for (int c = 0; c < lg.z; ++c) {
+                    const float4* part = reinterpret_cast<const float4*>(plan.partial + static_cast<int64_t>(lg.y + c) * D);
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
                         if (q < d4) {
-                            const uint32_t b = __ldg(srow + (q >> 2)) >> (8 * (q & 3));
-                            acc[m].x += signed_w(b, 0, wj);
-                            acc[m].y += signed_w(b, 2, wj);
-                            acc[m].z += signed_w(b, 4, wj);
-                            acc[m].w += signed_w(b, 6, wj);
+                            const float4 t = part[q];
+                            acc[m].x += t.x;
+                            acc[m].y += t.y;
+                            acc[m].z += t.z;
+                            acc[m].w += t.w;
                         }
                     }
                 }
@@ -578,6 +615,31 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p)
                 f.z *= inv;
                 f.w *= inv;
                 frow[q] = f;
+            }
+        }
+    }
+}
+
+// One warp per chunk of a long segment: its sign sums into the plan's partial rows.
+__global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams p, LongPlan plan) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2;
+    const float scale = *p.scale;
+    const int ni = plan.counters[0];
+    for (int64_t it = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; it < ni; it += nw) {
+        const int4 item = plan.items[it];
+        const int r0 = p.seg[item.x] + item.y * kLongSeg, r1 = min(p.seg[item.x + 1], r0 + kLongSeg);
+        for (int base = 0; base < d4; base += 128) {
+            float4 acc[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+            accum_signs(p, r0, r1, base, lane, scale, acc);
+            float4* dst = reinterpret_cast<float4*>(plan.partial + static_cast<int64_t>(item.z) * D);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = base + m * 32 + lane;
+                if (q < d4) dst[q] = acc[m];
             }
         }
     }
@@ -685,8 +747,13 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
     if (p.n <= 0 || p.d <= 0) return;
     const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
-    if (vec) k_feature_adam_vec<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
-    else k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+    if (vec) {
+        k_feature_adam_vec<false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        k_feature_adam_chunks<<<148 * 8, kThreads, 0, st>>>(p, p.plan);
+        k_feature_adam_vec<true><<<148 * 4, kThreads, 0, st>>>(p, p.plan);
+    } else {
+        k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+    }
     dbg_launch("k_feature_adam", st);
 }
 

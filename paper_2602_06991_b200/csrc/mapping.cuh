@@ -3,6 +3,7 @@
 // Top-K gather + masked feature L1, the fused feature backward + Adam + renormalise, selection
 // statistics and the deterministic loss reduction.
 #pragma once
+#include "feature.cuh"
 #include "tk_common.cuh"
 
 namespace tk {
@@ -64,6 +65,7 @@ struct FeatAdamParams {
     float* m;
     float* v;
     float lr, beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bc1, inv_bc2;
+    LongPlan plan;           // segments longer than kLongSeg: chunk partials + ordered combine
 };
 
 void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int64_t* depth_n_out,

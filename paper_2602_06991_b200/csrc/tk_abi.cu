@@ -253,6 +253,7 @@ struct tk_ctx {
     bool has_values = false;
     // segment_by_query scratch (kept across calls: no allocation on the query path)
     DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
+    DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
     // multi-GPU
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;
@@ -712,6 +713,7 @@ struct SlotIndex {
     const int32_t* seg;
     const uint32_t* slots;
     const float* wnorm;
+    tk::LongPlan plan;  // chunks of the segments longer than tk::kLongSeg
 };
 
 // Inverted (Gaussian -> record slots) index of a TopKGrid, ascending slot order per Gaussian.
@@ -728,7 +730,17 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
     int64_t* dscal = ensure<int64_t>(c->dscal, 16);
     tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, c->cur, &c->launches);
-    return SlotIndex{seg, svals, wn};
+    tk::LongPlan plan{};
+    plan.cap_items = tk::long_plan_capacity(slots, n);
+    plan.items = ensure<int4>(c->lp_items, plan.cap_items);
+    plan.longs = ensure<int4>(c->lp_longs, plan.cap_items);
+    plan.counters = ensure<int32_t>(c->lp_counters, 2);
+    plan.partial = ensure<float>(c->lp_partial, plan.cap_items * std::max(c->d, 1));
+    plan.queue = cursor;
+    plan.qcount = cursor + n + 1;
+    tk::launch_long_plan(seg, n, plan, c->cur);
+    c->launches += 1;
+    return SlotIndex{seg, svals, wn, plan};
 }
 
 // The backward sweep of backward_geometric (backward.cpp:106-188) into the per-Gaussian
@@ -978,7 +990,8 @@ tk_status tk_destroy(tk_ctx* c) {
     }
     DevBuf* mapping[] = {&c->fm, &c->fv, &c->stat_count, &c->stat_maxc, &c->ssim_rows, &c->ssim_win, &c->l_gc,
                          &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs, &c->q_feat,
-                         &c->q_emb, &c->q_labels, &c->q_best, &c->q_acc, &c->q_nacc, &c->q_part};
+                         &c->q_emb, &c->q_labels, &c->q_best, &c->q_acc, &c->q_nacc, &c->q_part,
+                         &c->lp_items, &c->lp_longs, &c->lp_counters, &c->lp_partial};
     for (DevBuf* b : mapping) b->release();
     if (c->hvals) cudaFreeHost(c->hvals);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -1215,9 +1228,9 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
         tk::FeatBwdParams fp{n, r.k, c->d, si.seg, si.slots, si.wnorm, g, dst};
         {
             PhaseScope phase(c, TK_PHASE_FBWD);
-            tk::launch_feature_bwd(fp, st);
+            tk::launch_feature_bwd(fp, si.plan, st);
         }
-        c->launches += n > 0;
+        c->launches += n > 0 ? 3 : 0;
         CK_LAUNCH(c);
         if (out && out_mem != TK_DEVICE) {
             copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), out_mem, c, kOutDF);
@@ -1730,8 +1743,9 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fa.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
                 fa.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat))));
                 fa.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat))));
+                fa.plan = si.plan;
                 tk::launch_feature_adam(fa, st);
-                c->launches += n > 0;
+                c->launches += n > 0 ? 3 : 0;
                 CK_LAUNCH(c);
             }
         }
