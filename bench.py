@@ -397,9 +397,9 @@ def main_gpu(args, cfg):
         extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev)
 
     mapping = None
-    if not dshard and not args.no_mapping:
-        mapping = run_mapping(lib, slib, N, torch, ctx, W, H, D, n, cpose, ccam, cset, args.steps, args.warmup,
-                              0 if args.no_e2e else args.e2e_steps, stream, dist)
+    if not args.no_mapping:  # dshard: the D-sharded mapping iteration (NCCL all-reduces inside the step)
+        mapping = run_mapping(lib, slib, N, torch, ctx, W, H, Ds, n, cpose, ccam, cset, args.steps, args.warmup,
+                              0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -512,7 +512,8 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
                     "all copies complete inside the timed region (tk_synchronize before the end event)"}
 
 
-def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, warmup, e2e_steps, stream, dist):
+def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, warmup, e2e_steps, stream, dist,
+                sharded=False):
     """Mapping iterations/s: tk_optimize_step (mapper.cpp:162-255 without pruning) on one keyframe of
     the config-3 map: render_geometric, compute_losses (colour/depth L1 + D-SSIM + masked feature L1),
     backward_geometric, Adam over every group, features on every 5th iteration, statistics."""
@@ -574,14 +575,18 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
         return x
 
     ms = ms_max(ms)
-    world = dist.get_world_size() if dist else 1
+    # keyframe-parallel replicas: every rank's iterations count; D-sharded: one iteration spans all ranks
+    ranks = dist.get_world_size() if dist else 1
+    world = ranks if not sharded else 1
     out = {"metric": "mapping iterations/s (optimize_step fwd+losses+bwd+Adam, features every 5th iteration)",
            "value": world * steps / (ms / 1000.0), "unit": "iterations/s", "ms_per_iteration": ms / steps,
            "iterations": steps, "feature_update_period": cfg.feature_update_period, "gpu_launches": int(launches),
            "last_losses": {"map": vals[0], "geo": vals[1], "feat": vals[2]},
            "phases": {nm: {"ms_per_iteration": ph_ms[i] / steps, "launch_groups": int(ph_cnt[i])}
                       for i, nm in enumerate(N.PHASES) if ph_cnt[i]},
-           "target": ">= 15 mapping iterations/s end to end (BASELINE.json north_star)"}
+           "target": ">= 15 mapping iterations/s end to end (BASELINE.json north_star)",
+           "parallelism": ("D-sharded: D/G channels per rank, mask / loss / geometry-gradient / row-norm "
+                           "all-reduces over NCCL" if sharded else "one map per rank (replicas)")}
     if e2e_steps <= 0:
         return out
     e2e_steps = max(2, e2e_steps)
@@ -602,12 +607,12 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
     N.check(lib.tk_synchronize(ctx))
     ms_b = ms_max(ev0.elapsed_time(ev1))
     out["e2e"] = {"value": world * e2e_steps / (ms_a / 1000.0), "unit": "iterations/s",
-                  "h2d_bytes_per_step": int(world * (col.nbytes + dep.nbytes + feat.nbytes)),
-                  "d2h_bytes_per_step": int(world * 24), "steps": e2e_steps,
+                  "h2d_bytes_per_step": int(ranks * (col.nbytes + dep.nbytes + feat.nbytes)),
+                  "d2h_bytes_per_step": int(ranks * 24), "steps": e2e_steps,
                   "path": "C ABI: tk_keyframe_set from pinned host (colour, depth, D-channel feature) + "
                           "tk_optimize_step with the loss values read back, every iteration"}
     out["e2e_resident_keyframes"] = {"value": world * e2e_steps / (ms_b / 1000.0), "unit": "iterations/s",
-                                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(world * 24),
+                                     "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(ranks * 24),
                                      "path": "keyframe uploaded once (device-resident keyframe store); "
                                              "tk_optimize_step + loss values read back every iteration"}
     return out

@@ -231,7 +231,11 @@ tk_status tk_keyframe_set(tk_ctx* ctx, int32_t slot, const tk_pose* pose, const 
 /* Zero the Adam state of every group for the resident scene (n, d) and, when reset_stats,
  * the selection statistics (topk_count, max_contribution). */
 tk_status tk_optimizer_reset(tk_ctx* ctx, int32_t reset_stats);
-/* One optimisation step on keyframe `slot` (the caller samples it; mapper.cpp:167-168):
+/* Under tk_comm (D-sharded: every rank holds d = d_total / nranks feature channels and the same
+ * geometry) the step is the D-sharded mapping iteration: keyframe feature masks, the loss
+ * partials, the geometry gradients and the feature row norms are all-reduced with NCCL, so the
+ * geometry replicas stay bit-identical and each rank updates its channel slice.
+ * One optimisation step on keyframe `slot` (the caller samples it; mapper.cpp:167-168):
  * render, losses, backward, Adam per group (features on iteration % feature_update_period
  * == 0), renormalisation, statistics.  values_out (host, may be NULL = stay on the device,
  * no synchronisation) receives {map, geo, feat} (LossValues, losses.hpp:23-27). */

@@ -53,6 +53,7 @@ struct ChainParams {
     double* g_opacity_logit;
     double* g_color;
     double* twist;  // ceil(n / 128) x 6 block partials, or null (mapping: no pose gradient)
+    double mid_scale = 1.0;  // applied to mid (1 / ranks after a D-sharded all-reduce)
 };
 
 // In-place Adam over the five geometry groups (optimizer.hpp:25-53 layout: one m / v array per

@@ -423,6 +423,12 @@ __global__ void __launch_bounds__(kThreads) k_loss_finalize(FinalizeParams p) {
         __syncthreads();
     }
     if (threadIdx.x != 0) return;
+    if (p.replicas != 1.0) {  // colour / depth / SSIM / feat_n are identical on every shard
+        tot[kL1Color] /= p.replicas;
+        tot[kL1Depth] /= p.replicas;
+        tot[kSsimSum] /= p.replicas;
+        tot[kFeatCount] /= p.replicas;
+    }
     const double l1_color = tot[kL1Color] * p.inv_color_n;
     double secondary = 0.0;
     if (p.use_ssim) secondary = 0.5 * (1.0 - tot[kSsimSum] * p.inv_count);
@@ -590,6 +596,16 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
             }
         }
         const float ssum = warp_sum(ss);
+        if (p.row_ss) {  // D-sharded: the norm needs every shard's channels (k_feature_renorm)
+            if (lane == 0) p.row_ss[g] = ssum;
+            if (d4 <= 128)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = m * 32 + lane;
+                    if (q < d4) __stcs(frow + q, fk[m]);
+                }
+            continue;
+        }
         const bool renorm = ssum > 1e-24f;  // norm > 1e-12 (mapper.cpp:249)
         const float inv = renorm ? rsqrtf(ssum) : 1.0f;
         if (d4 <= 128) {
@@ -678,9 +694,23 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams
                 ss += f * f;
             }
         }
-        const float norm = sqrtf(warp_sum(ss));
+        const float ssum = warp_sum(ss);
+        if (p.row_ss) {  // D-sharded: k_feature_renorm scales once the norms are all-reduced
+            if (lane == 0) p.row_ss[g] = ssum;
+            continue;
+        }
+        const float norm = sqrtf(ssum);
         if (norm > 1e-12f)
             for (int q = lane; q < D; q += 32) frow[q] /= norm;
+    }
+}
+
+__global__ void k_feature_renorm(float* __restrict__ feat, const float* __restrict__ ss, int64_t n, int d) {
+    const int64_t total = n * d;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const float s2 = ss[e / d];
+        if (s2 > 1e-24f) feat[e] *= rsqrtf(s2);
     }
 }
 
@@ -741,6 +771,12 @@ void launch_topk_stats(const int32_t* index, const uint8_t* count, int64_t pixel
     if (pixels <= 0 || k <= 0) return;
     k_topk_stats<<<capped_grid(pixels, 256, 148 * 8), 256, 0, st>>>(index, count, pixels, k, topk_count);
     dbg_launch("k_topk_stats", st);
+}
+
+void launch_feature_renorm(float* feat, const float* ss, int64_t n, int d, cudaStream_t st) {
+    if (n <= 0 || d <= 0) return;
+    k_feature_renorm<<<capped_grid(n * d, 256, 148 * 32), 256, 0, st>>>(feat, ss, n, d);
+    dbg_launch("k_feature_renorm", st);
 }
 
 void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {

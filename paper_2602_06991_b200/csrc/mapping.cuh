@@ -46,6 +46,7 @@ struct FeatLossParams {
 struct FinalizeParams {
     const double* partial;
     int nparts;
+    double replicas = 1.0;   // partial rows summed over this many D-shards (replicated slots / replicas)
     double lambda_geo, lambda_feat, lambda1, lambda2;
     int use_ssim, secondary_l1, use_depth, feature_step, d;
     double inv_color_n, inv_depth_n, inv_count;
@@ -66,7 +67,11 @@ struct FeatAdamParams {
     float* v;
     float lr, beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bc1, inv_bc2;
     LongPlan plan;           // segments longer than kLongSeg: chunk partials + ordered combine
+    float* row_ss = nullptr; // D-sharded: per-Gaussian partial squared norms out, rows left unscaled
 };
+
+// D-sharded renormalisation: f /= sqrt(ss[g]) when sqrt(ss[g]) > 1e-12 (ss all-reduced over shards)
+void launch_feature_renorm(float* feat, const float* ss, int64_t n, int d, cudaStream_t st);
 
 void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int64_t* depth_n_out,
                      const float* gt_depth, cudaStream_t st);

@@ -254,6 +254,7 @@ struct tk_ctx {
     // segment_by_query scratch (kept across calls: no allocation on the query path)
     DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
     DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
+    DevBuf row_ss;                                        // D-sharded partial row norms
     // multi-GPU
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;
@@ -991,7 +992,7 @@ tk_status tk_destroy(tk_ctx* c) {
     DevBuf* mapping[] = {&c->fm, &c->fv, &c->stat_count, &c->stat_maxc, &c->ssim_rows, &c->ssim_win, &c->l_gc,
                          &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs, &c->q_feat,
                          &c->q_emb, &c->q_labels, &c->q_best, &c->q_acc, &c->q_nacc, &c->q_part,
-                         &c->lp_items, &c->lp_longs, &c->lp_counters, &c->lp_partial};
+                         &c->lp_items, &c->lp_longs, &c->lp_counters, &c->lp_partial, &c->row_ss};
     for (DevBuf* b : mapping) b->release();
     if (c->hvals) cudaFreeHost(c->hvals);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
@@ -1511,6 +1512,8 @@ tk_status tk_keyframe_set(tk_ctx* c, int32_t slot, const tk_pose* pose, const tk
         tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, dep, c->cur);
         c->launches += 1;
         CK_LAUNCH(c);
+        if (c->comm)  // D-sharded: a pixel's keyframe row is valid if any shard's channels are non-zero
+            NK(g_nccl.AllReduce(valid, valid, static_cast<size_t>(P), ncclUint8, ncclMax, c->comm, c->cur));
         tk::copy_words_to_mapped(c->hscal_dev + 9, dscal + 9, 1, c->cur);
         sync(c);
         k.depth_n = c->hscal[9];
@@ -1561,6 +1564,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
         if (kf.w != cam->width || kf.h != cam->height)
             fail(TK_ERR_BAD_ARG, "compute_losses: render/frame shape mismatch");
         const bool feature_step = (iteration % cfg->feature_update_period) == 0;  // mapper.cpp:171
+        const bool sharded = c->comm != nullptr;  // D-sharded mapping (features: this rank's slice)
         const bool use_ssim = cfg->lambda1 != 0.0 && cfg->color_secondary == 0;
         if (use_ssim && (cam->width < tk::kSsimWin || cam->height < tk::kSsimWin))
             fail(TK_ERR_BAD_ARG, "ssim: image smaller than the 11x11 window");
@@ -1644,9 +1648,13 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 tk::launch_feature_loss(fl, st);
                 c->launches += 1;
             }
+            if (sharded)  // feature partials differ per shard; colour / depth rows are replicas
+                NK(g_nccl.AllReduce(partial, partial, tk::kLossBlocks * tk::kLossSlots, ncclFloat64, ncclSum, c->comm,
+                                    st));
             tk::FinalizeParams fp{};
             fp.partial = partial;
             fp.nparts = tk::kLossBlocks;
+            fp.replicas = sharded ? static_cast<double>(c->nranks) : 1.0;
             fp.lambda_geo = cfg->lambda_geo;
             fp.lambda_feat = cfg->lambda_feat;
             fp.lambda1 = cfg->lambda1;
@@ -1655,7 +1663,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             fp.secondary_l1 = (cfg->lambda1 != 0.0 && cfg->color_secondary != 0) ? 1 : 0;
             fp.use_depth = lp.use_depth;
             fp.feature_step = feature_step ? 1 : 0;
-            fp.d = d;
+            fp.d = sharded ? c->d_total : d;  // losses.cpp:106: mean over every channel
             fp.inv_color_n = lp.inv_color_n;
             fp.inv_depth_n = lp.inv_depth_n;
             fp.inv_count = lp.inv_count;
@@ -1669,6 +1677,8 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
         c->has_values = true;
         // backward_geometric (mapper.cpp:179-180) on this forward
         double* mid = geom_sweep(c, f, gc, gd);
+        if (sharded)  // replicas stay bit-identical: one all-reduced geometry gradient on every shard
+            NK(g_nccl.AllReduce(mid, mid, static_cast<size_t>(n) * 10, ncclFloat64, ncclSum, c->comm, st));
         {
             PhaseScope phase(c, TK_PHASE_ADAM);
             // geometry groups (mapper.cpp:183-236): five adam_step calls, one step counter each
@@ -1698,6 +1708,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ga.contrib = ptr<unsigned long long>(c->o_contrib);
             ga.max_contrib = ptr<double>(c->stat_maxc);
             tk::ChainParams cp = chain_params(c, &kf.pose, cam, s, mid);
+            cp.mid_scale = sharded ? 1.0 / c->nranks : 1.0;
             cp.g_mean = ensure<double>(c->gg_mean, n * 3);
             cp.g_log_scale = ensure<double>(c->gg_ls, n * 3);
             cp.g_rotation = ensure<double>(c->gg_rot, n * 4);
@@ -1744,8 +1755,15 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fa.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat))));
                 fa.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat))));
                 fa.plan = si.plan;
+                if (sharded) fa.row_ss = ensure<float>(c->row_ss, n);
                 tk::launch_feature_adam(fa, st);
                 c->launches += n > 0 ? 3 : 0;
+                if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
+                    NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
+                                        st));
+                    tk::launch_feature_renorm(ptr<float>(c->feature), fa.row_ss, n, d, st);
+                    c->launches += 1;
+                }
                 CK_LAUNCH(c);
             }
         }

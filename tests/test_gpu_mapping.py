@@ -153,6 +153,26 @@ def test_long_segments_chunked(R):
     assert a.tobytes() == R.backward_feature(m, g.topk, gf).tobytes()
 
 
+def test_d_sharded_path_single_rank_matches_oracle():
+    """tk_comm with one rank drives the D-sharded mapping iteration (mask / loss / geometry-gradient
+    / row-norm all-reduces, split renormalisation); with one shard it must equal the oracle."""
+    import ctypes as C
+    m, cam, s, pose, frame = make_problem(seed=13)
+    cfg = MapperConfig(feature_update_period=1)
+    r = api.Renderer(0)
+    try:
+        uid = (C.c_uint8 * 128)()
+        N.check(r.lib.tk_comm_unique_id(uid))
+        N.check(r.lib.tk_comm_init(r.ctx, uid, 1, 0, m.feature_dim))
+        om, steps = run_both(r, m, cam, s, pose, frame, cfg, [1, 2, 3])
+        for it, ov, gv, fs in steps:
+            assert gv.geo == pytest.approx(ov["geo"], rel=1e-10)
+            assert gv.feat == pytest.approx(ov["feat"], rel=1e-5)
+        compare_state(r, om, m)
+    finally:
+        r.close()
+
+
 def test_deferred_loss_values(R):
     m, cam, s, pose, frame = make_problem(seed=8)
     cfg = MapperConfig()

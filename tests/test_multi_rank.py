@@ -57,6 +57,64 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
+def _feature_step_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        feat, index, weight, count, K = _records(P=60, N=40, K=3, seed=3)
+        rng = np.random.default_rng(7)
+        P, D = count.shape[0], feat.shape[1]
+        F = rng.standard_normal((P, D))
+        gt = rng.standard_normal((P, D))
+        gt[::7] = 0.0                      # invalid keyframe rows
+        gt[3, : D // 2] = 0.0              # valid only through the other shard's channels
+        m0 = rng.standard_normal((feat.shape[0], D)) * 1e-3
+        v0 = np.abs(rng.standard_normal((feat.shape[0], D))) * 1e-6
+        args = dict(k=K, lam=1.0, lr=1e-2, beta1=0.9, beta2=0.999, eps=1e-8, step=3, d_total=D)
+
+        def amax(x):
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return t.numpy()
+
+        def asum(x):
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            dist.all_reduce(t)
+            return t.numpy()
+
+        c0, c1 = tkdist.shard_range(D, world, rank)
+        fs, ms, vs, l1 = tkdist.feature_step_shard(F[:, c0:c1], gt[:, c0:c1], count, index, weight,
+                                                   feat=feat[:, c0:c1], m=m0[:, c0:c1], v=v0[:, c0:c1],
+                                                   allreduce_max=amax, allreduce_sum=asum, **args)
+        parts = [torch.zeros_like(torch.from_numpy(np.ascontiguousarray(fs))) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(fs)))
+        full_f = np.concatenate([p.numpy() for p in parts], axis=1)
+        ref_f, _, _, ref_l1 = tkdist.feature_step_shard(F, gt, count, index, weight, feat=feat, m=m0, v=v0,
+                                                        allreduce_max=lambda x: x, allreduce_sum=lambda x: x, **args)
+        q.put((rank, float(np.abs(full_f - ref_f).max()), abs(l1 - ref_l1)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_feature_step_equals_unsharded():
+    """The D-sharded mapping step's exchanges (mask max, |F-F_gt| sum, row-norm sum) reproduce the
+    unsharded feature L1 + backward + Adam + renormalisation (world 2, gloo)."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_feature_step_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, dmax, dl1 in res:
+        assert dmax < 1e-12 and dl1 < 1e-12, (rank, dmax, dl1)
+
+
 def test_shard_range():
     assert tkdist.shard_range(512, 8, 3) == (192, 256)
     assert tkdist.shard_range(768, 2, 1) == (384, 768)
