@@ -221,26 +221,6 @@ __global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
     }
 }
 
-// Record keys for the inverted (Gaussian -> slots) index, plus the renormalised weights.
-__global__ void k_slot_keys(SlotKeyParams p) {
-    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= p.n_slots) return;
-    const int64_t px = s / p.k;
-    const int j = static_cast<int>(s - px * p.k);
-    const int c = p.count[px];
-    const int32_t id = p.index[s];
-    const bool valid = j < c && id >= 0;
-    p.keys[s] = valid ? static_cast<uint32_t>(id) : static_cast<uint32_t>(p.n_gaussians);
-    p.vals[s] = static_cast<uint32_t>(s);
-    float wn = 0.0f;
-    if (valid) {
-        double sum = 0.0;                                    // backward.cpp:303-304, slot order
-        for (int jj = 0; jj < c; ++jj) sum += p.weight[px * p.k + jj];
-        wn = static_cast<float>(p.weight[s] / sum);
-    }
-    p.wnorm[s] = wn;
-}
-
 // Inverted index (Gaussian -> record slots) by counting: count, scan, fill, then sort every
 // segment by slot so the reduction order never depends on the atomic fill order.
 __global__ void k_slot_count(SlotKeyParams p, int32_t* __restrict__ cnt) {
@@ -542,16 +522,6 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd_combine(FeatBwdParams p, 
     }
 }
 
-__global__ void k_max_index(const int32_t* __restrict__ index, int64_t n, int32_t* __restrict__ out) {
-    int32_t m = INT32_MIN;
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        m = max(m, index[i]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
-}
-
 // First slot (in slot order) whose index is >= n: the reference throws on it (render.cpp:305-311).
 __global__ void k_first_stale(const int32_t* __restrict__ index, int64_t n_slots, int64_t n,
                               unsigned long long* __restrict__ first) {
@@ -599,11 +569,6 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
     dbg_launch("k_list_gather", st);
 }
 
-void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st) {
-    if (p.n_slots > 0) k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p);
-    dbg_launch("k_slot_keys", st);
-}
-
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
                        uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches) {
     const unsigned g = static_cast<unsigned>((p.n_slots + 255) / 256);
@@ -648,11 +613,6 @@ void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream
     dbg_launch("k_feat_bwd_chunks", st);
     k_feat_bwd_combine<<<148 * 4, kThreads, 0, st>>>(p, plan);
     dbg_launch("k_feat_bwd_combine", st);
-}
-
-void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st) {
-    if (n_slots > 0) k_max_index<<<296, 256, 0, st>>>(index, n_slots, max_index);
-    dbg_launch("k_max_index", st);
 }
 
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,

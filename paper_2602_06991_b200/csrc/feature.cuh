@@ -33,8 +33,8 @@ struct SlotKeyParams {
     const int32_t* index;
     const double* weight;
     const uint8_t* count;
-    uint32_t* keys;        // Gaussian id, or n_gaussians for unused slots
-    uint32_t* vals;        // slot id
+    uint32_t* keys;        // unused (kept for layout stability)
+    uint32_t* vals;        // unused
     float* wnorm;          // renormalised slot weight (render.cpp:324-329)
 };
 
@@ -70,7 +70,6 @@ inline int64_t long_plan_capacity(int64_t m, int64_t n) {
 
 void launch_feature_gather(const GatherParams& p, cudaStream_t st);
 void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
-void launch_slot_keys(const SlotKeyParams& p, cudaStream_t st);
 // Inverted index of the records by counting: cnt_seg (n+1) becomes the segment offsets, recs /
 // sorted hold the valid slot ids grouped by Gaussian (sorted: ascending within each segment).
 // cursor: n + 2 int32 of scratch.
@@ -81,8 +80,6 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt
 void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st);
 // backward_feature's reduction; long segments through plan (chunks + ordered combine)
 void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st);
-// *max_index = max over all slots (device int, preset to INT_MIN)
-void launch_max_index(const int32_t* index, int64_t n_slots, int32_t* max_index, cudaStream_t st);
 // *first = smallest slot whose index >= n (device u64, preset to ~0)
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,
                         cudaStream_t st);

@@ -64,53 +64,6 @@ __device__ int64_t block_excl_scan(int64_t v, int64_t* block_total) {
     return warp_off + incl - v;
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const int32_t* __restrict__ in, int64_t n,
-                                                              int64_t* __restrict__ bsum) {
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * SCAN_TILE;
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        const int64_t idx = base + static_cast<int64_t>(i) * SCAN_THREADS + threadIdx.x;
-        if (idx < n) s += in[idx];
-    }
-    int64_t tot;
-    block_excl_scan<SCAN_THREADS>(s, &tot);
-    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_blocks(int64_t* __restrict__ bsum, int64_t nb,
-                                                       int64_t* __restrict__ total) {
-    int64_t carry = 0;
-    for (int64_t base = 0; base < nb; base += 1024) {
-        const int64_t idx = base + threadIdx.x;
-        const int64_t v = idx < nb ? bsum[idx] : 0;
-        int64_t tot;
-        const int64_t ex = block_excl_scan<1024>(v, &tot);
-        if (idx < nb) bsum[idx] = carry + ex;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_apply(const int32_t* __restrict__ in, int32_t* __restrict__ out,
-                                                             int64_t n, const int64_t* __restrict__ bsum) {
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * SCAN_TILE + static_cast<int64_t>(threadIdx.x) * SCAN_ITEMS;
-    int32_t v[SCAN_ITEMS];
-    int64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        v[i] = base + i < n ? in[base + i] : 0;
-        s += v[i];
-    }
-    int64_t tot;
-    int64_t run = bsum[blockIdx.x] + block_excl_scan<SCAN_THREADS>(s, &tot);
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        if (base + i < n) out[base + i] = static_cast<int32_t>(run);
-        run += v[i];
-    }
-}
-
 // Single-pass scan with decoupled look-back: each block publishes its aggregate, then its
 // inclusive prefix once the predecessor's prefix is known (status word: 2-bit flag | 62-bit sum).
 // Block order comes from a ticket so a block only ever waits on blocks already running.
@@ -420,25 +373,15 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
         *launches += 1;
         return;
     }
+    // single pass: a block reads its whole tile before writing it, so in-place is safe
     const int64_t nb = std::max<int64_t>(1, (n + SCAN_TILE - 1) / SCAN_TILE);
-    {  // single pass: a block reads its whole tile before writing it, so in-place is safe
-        unsigned long long* status = static_cast<unsigned long long*>(scratch);
-        int* ticket = reinterpret_cast<int*>(status + nb);
-        cudaMemsetAsync(status, 0, (nb + 1) * sizeof(unsigned long long), st);
-        k_scan_lookback<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, status, ticket, total,
-                                                                          static_cast<int>(nb));
-        dbg_launch("k_scan_lookback", st);
-        *launches += 1;
-        return;
-    }
-    int64_t* bsum = static_cast<int64_t*>(scratch);
-    k_scan_reduce<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, n, bsum);
-    dbg_launch("k_scan_reduce", st);
-    k_scan_blocks<<<1, 1024, 0, st>>>(bsum, nb, total);
-    dbg_launch("k_scan_blocks", st);
-    k_scan_apply<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, bsum);
-    dbg_launch("k_scan_apply", st);
-    *launches += 3;
+    unsigned long long* status = static_cast<unsigned long long*>(scratch);
+    int* ticket = reinterpret_cast<int*>(status + nb);
+    cudaMemsetAsync(status, 0, (nb + 1) * sizeof(unsigned long long), st);
+    k_scan_lookback<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, status, ticket, total,
+                                                                      static_cast<int>(nb));
+    dbg_launch("k_scan_lookback", st);
+    *launches += 1;
 }
 
 size_t radix_scratch_bytes(int64_t n) {

@@ -210,7 +210,7 @@ struct tk_ctx {
     DevBuf pmx, pmy, pixx, pixy, piyy, pz, pop, rect, valid, ntiles, pos;
     DevBuf dkeys, dvals, dkeys_alt, dvals_alt, ntiles_sorted, pair_off;
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
-    DevBuf te[13];
+    DevBuf te;  // chunk-major tile entries (tk::EntryChunk)
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
     DevBuf scratch, scratch_feat, dscal;
     int64_t* hscal = nullptr;      // host-mapped mirror of dscal (written by k_copy_words)
@@ -438,7 +438,7 @@ FwdKey make_fwd_key(const PrepKey& pk, const tk_settings* s) {
 
 tk::TileEntries tile_entries(tk_ctx* c) {
     tk::TileEntries t;
-    t.chunks = ptr<tk::EntryChunk>(c->te[0]);
+    t.chunks = ptr<tk::EntryChunk>(c->te);
     return t;
 }
 
@@ -571,7 +571,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     c->launches += 1;
     tk::scan_exclusive(pcnt, pstart, n_tiles + 1, dscal + 4, c->scratch.p, st, &c->launches);
     const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
-    ensure<tk::EntryChunk>(c->te[0], padded_cap / tk::kChunk + 1);
+    ensure<tk::EntryChunk>(c->te, padded_cap / tk::kChunk + 1);
     ensure<int32_t>(c->wl, padded_cap * tk::geom_blocks_per_tile(s->tile_size));
     tk::MaterializeParams mp{};
     mp.n_pairs = n_pairs;
@@ -983,7 +983,7 @@ tk_status tk_destroy(tk_ctx* c) {
                      &c->gg_op, &c->gg_col, &c->l_count, &c->l_off, &c->l_src, &c->l_w, &c->gather_buf,
                      &c->wl, &c->wl_count};
     for (DevBuf* b : all) b->release();
-    for (DevBuf& b : c->te) b.release();
+    c->te.release();
     for (Keyframe& k : c->kfs) k.release();
     for (int g = 0; g < 5; ++g) {
         c->am[g].release();
