@@ -399,7 +399,8 @@ def main_gpu(args, cfg):
     mapping = None
     if not args.no_mapping:  # dshard: the D-sharded mapping iteration (NCCL all-reduces inside the step)
         mapping = run_mapping(lib, slib, N, torch, ctx, W, H, Ds, n, cpose, ccam, cset, args.steps, args.warmup,
-                              0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard)
+                              0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard, scene=scene,
+                              cam=cam, gt_pose=pose, d_total=D, c0=c0)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -513,10 +514,11 @@ def run_e2e(lib, N, torch, ctx, scene, geo, feat, gF_host, gC_host, gD_host, cpo
 
 
 def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, warmup, e2e_steps, stream, dist,
-                sharded=False):
+                sharded=False, scene=None, cam=None, gt_pose=None, d_total=None, c0=0):
     """Mapping iterations/s: tk_optimize_step (mapper.cpp:162-255 without pruning) on one keyframe of
     the config-3 map: render_geometric, compute_losses (colour/depth L1 + D-SSIM + masked feature L1),
-    backward_geometric, Adam over every group, features on every 5th iteration, statistics."""
+    backward_geometric, Adam over every group, features on every 5th iteration, statistics.  The
+    keyframe is render_ground_truth of the bench scene; the optimised map is a perturbed copy."""
     P = W * H
 
     def pinned(count, dtype):
@@ -528,9 +530,29 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
     td, dep = pinned(P, torch.float32)
     tf, feat = pinned(P * D, torch.float32)
     keep += [tc, td, tf]
-    slib.tk_synth_hash_fill_f32(col.size, 21, 0.0, 1.0, col.ctypes.data)
-    slib.tk_synth_hash_fill_f32(dep.size, 22, 0.5, 4.0, dep.ctypes.data)
-    slib.tk_synth_hash_fill_f32(feat.size, 23, -1.0, 1.0, feat.ctypes.data)
+    # keyframe: render_ground_truth of the bench scene (scene.cpp:232-276; K = 1 labels -> class
+    # embeddings); the map being optimised is that scene with its means and
+    # colours perturbed (seeded), so every loss term has gradient
+    from paper_2602_06991_b200 import api, synth
+    from paper_2602_06991_b200.api import to_pose
+    emb = synth.unit_features(4, d_total, 99)[:, c0:c0 + D]
+    rr = api.Renderer(0)
+    try:
+        gt_frame, _ = synth.render_ground_truth(rr, scene, scene.class_ids, emb, [gt_pose], cam)[0]
+    finally:
+        rr.close()
+    col[:] = gt_frame.color.ravel()
+    dep[:] = gt_frame.depth.ravel()
+    feat[:] = gt_frame.feature.ravel()
+    del gt_frame
+    rng = np.random.default_rng(17)
+    spacing = float(np.median(np.exp(scene.log_scale[:, 0]))) * 2.0
+    pert = [np.ascontiguousarray(scene.mean + rng.normal(0.0, 0.3 * spacing, scene.mean.shape)),
+            np.ascontiguousarray(scene.log_scale, np.float64), np.ascontiguousarray(scene.rotation, np.float64),
+            np.ascontiguousarray(scene.opacity_logit, np.float64),
+            np.ascontiguousarray(np.clip(scene.color + rng.normal(0.0, 0.05, scene.color.shape), 0.0, 1.0))]
+    view = N.tk_scene_view(n, D, *(a.ctypes.data for a in pert), None, scene.generation)  # features kept
+    N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
     frame = N.tk_frame_view(W, H, D, col.ctypes.data, dep.ctypes.data, feat.ctypes.data, N.TK_HOST)
     cfg = N.tk_mapper_config()
     lib.tk_default_mapper_config(C.byref(cfg))

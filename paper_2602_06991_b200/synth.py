@@ -90,10 +90,35 @@ def bench_scene(n_gaussians: int, width: int, height: int, d: int, seed: int = 7
     truncated to N, camera fx=fy=0.9W, far 20, pose = orbit(8)[0]; features are seeded unit rows."""
     spec = default_spec(seed=seed, spacing=math.sqrt(70.0 / max(1, n_gaussians)), feature_dim=max(d, 4),
                         classes=4)
-    scene, _ = build_synthetic_scene(spec, truncate=n_gaussians)
+    scene, cls = build_synthetic_scene(spec, truncate=n_gaussians)
+    scene.class_ids = cls  # for render_ground_truth (scene.cpp:232-276)
     scene.feature = None
     scene.feature_dim = d
     cam = CameraIntrinsics(fx=0.9 * width, fy=0.9 * width, cx=0.5 * (width - 1), cy=0.5 * (height - 1),
                            width=width, height=height, near_plane=0.05, far_plane=20.0)
     pose = generate_trajectory("orbit", 8, spec)[0]
     return scene, cam, pose, spec
+
+
+def render_ground_truth(renderer, scene, class_ids: np.ndarray, embeddings: np.ndarray, poses, cam) -> list:
+    """render_ground_truth (proj/src/synth/scene.cpp:232-276): a K = 1 render of the scene per pose
+    (on the GPU, through `renderer`); colour clamped to [0, 1]; depth, label and the label's class
+    embedding only where alpha > 0.5 and a Top-1 record exists (label 255 elsewhere).  Returns
+    [(Frame, label image)]."""
+    from .types import Frame, RenderSettings
+    s = RenderSettings(top_k=1, transmittance_floor=1e-4, background=(0.0, 0.0, 0.0))
+    emb = np.ascontiguousarray(embeddings, np.float32)
+    out = []
+    for pose in poses:
+        r = renderer.render_geometric(scene, pose, cam, s)
+        h, w = cam.height, cam.width
+        covered = (r.alpha > 0.5) & (r.topk.count.reshape(h, w) > 0)
+        top = r.topk.index.reshape(h, w)
+        label = np.full((h, w), 255, np.uint8)
+        label[covered] = class_ids[top[covered]]
+        feat = np.zeros((h, w, emb.shape[1]), np.float32)
+        feat[covered] = emb[label[covered]]
+        frame = Frame(color=np.clip(r.color, 0.0, 1.0).astype(np.float32),
+                      depth=np.where(covered, r.depth, 0.0).astype(np.float32), feature=feat)
+        out.append((frame, label))
+    return out
