@@ -330,6 +330,7 @@ def main_gpu(args, cfg):
     M = int(valid.size)
 
     # ---- timed region (device-resident inputs)
+    N.check(lib.tk_pair_count(ctx, None, 1))
     launches0 = lib.tk_kernel_launches(ctx)
     N.check(lib.tk_profile_read(ctx, None, None, 1))
     N.check(lib.tk_profile_enable(ctx, 1))
@@ -353,6 +354,10 @@ def main_gpu(args, cfg):
     ph_ms = (C.c_double * len(N.PHASES))()
     ph_cnt = (C.c_int64 * len(N.PHASES))()
     N.check(lib.tk_profile_read(ctx, ph_ms, ph_cnt, 1))
+    pairs_total = C.c_int64()
+    N.check(lib.tk_pair_count(ctx, C.byref(pairs_total), 1))
+    fp64_rate = C.c_double()
+    N.check(lib.tk_fp64_rate(ctx, C.byref(fp64_rate)))
     if dist:
         t = torch.tensor([ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -381,6 +386,23 @@ def main_gpu(args, cfg):
     if tr:
         roof["traffic"] = tr["bytes"]
         roof["traffic_source"] = f"profiles/{tr['source']} ({tr['kernel']}, dram read+write per launch)"
+    # ---- fp64 roofline of the geometric sweeps (compute-bound): pixel-entry pairs blended per frame
+    # x the DP operations this implementation spends per pair on the reference's formulas
+    # (forward render.cpp:196-216: offsets 2, power 8, exp 15, alpha/weight 2, blend 5, T 2 = 34;
+    #  backward backward.cpp:130-160: the same 25 to recover alpha, 41 for the adjoint = 66)
+    pairs = pairs_total.value / max(1, args.steps)
+    t_fwd = ph_ms[1] / max(1, ph_cnt[1])
+    t_bwd = ph_ms[5] / max(1, ph_cnt[5])
+    dp_peak = fp64_rate.value
+    roof64 = None
+    if pairs > 0 and t_bwd > 0 and dp_peak > 0:
+        roof64 = {"kernel": "k_geom_bwd (backward_geometric sweep)", "bound": "fp64",
+                  "achieved": pairs * 66 / (t_bwd / 1000.0), "peak": dp_peak, "unit": "DP op/s",
+                  "frac": pairs * 66 / (t_bwd / 1000.0) / dp_peak, "pairs_per_frame": pairs, "dp_ops_per_pair": 66,
+                  "peak_kind": "measured (tk_fp64_rate: DFMA throughput probe, live)",
+                  "forward": {"kernel": "k_geom_fwd", "achieved": pairs * 34 / (t_fwd / 1000.0),
+                              "frac": pairs * 34 / (t_fwd / 1000.0) / dp_peak, "dp_ops_per_pair": 34,
+                              "pairs_per_s": pairs / (t_fwd / 1000.0)}}
     feat_bytes = bytes_gather + bytes_fbwd
     feat_ms = ph_ms[2] / max(1, ph_cnt[2]) + (ph_ms[3] / max(1, ph_cnt[3])) + ph_ms[4] / max(1, ph_cnt[4])
     feature_path = {"algorithmic_bytes": feat_bytes, "ms": feat_ms,
@@ -427,7 +449,7 @@ def main_gpu(args, cfg):
                                                                                         P * D * 4 / 1e9),
                        "records": {"distinct_gaussians": U, "valid_slots": M}},
             "hbm_gbs": feature_path["achieved_gbs"],
-            "roofline": roof, "feature_path": feature_path, "phases": phases,
+            "roofline": roof, "roofline_fp64": roof64, "feature_path": feature_path, "phases": phases,
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
             "mapping": mapping, "extras": extras, "setup_s": setup_s,
         }

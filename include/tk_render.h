@@ -291,6 +291,14 @@ tk_status tk_segment_by_query(tk_ctx* ctx, const float* feature, int64_t n_pixel
  * re-bins (the reference recomputes prepare_scene in every call, render.cpp:295). */
 tk_status tk_invalidate(tk_ctx* ctx);
 
+/* Pixel-entry pairs the geometric forward blended (power >= cutoff, pixel not saturated) since
+ * the last reset -- the work unit of the fp64-bound sweeps (synchronises). */
+tk_status tk_pair_count(tk_ctx* ctx, int64_t* pairs, int32_t reset);
+
+/* Measured fp64 FMA instructions per second of the context's device (a ~30 ms probe): the
+ * denominator of the fp64 roofline of the geometric sweeps. */
+tk_status tk_fp64_rate(tk_ctx* ctx, double* fma_per_s);
+
 /* Profiling: number of kernels this context launched since creation. */
 int64_t tk_kernel_launches(tk_ctx* ctx);
 

@@ -140,6 +140,8 @@ RENDER_SYMBOLS = [
     ("tk_allreduce_sum_f64", C.c_int, [C.c_void_p, dbl_p, C.c_int32]),
     ("tk_kernel_launches", C.c_int64, [C.c_void_p]),
     ("tk_invalidate", C.c_int, [C.c_void_p]),
+    ("tk_pair_count", C.c_int, [C.c_void_p, i64_p, C.c_int32]),
+    ("tk_fp64_rate", C.c_int, [C.c_void_p, dbl_p]),
     ("tk_profile_enable", C.c_int, [C.c_void_p, C.c_int32]),
     ("tk_profile_read", C.c_int, [C.c_void_p, dbl_p, i64_p, C.c_int32]),
     ("tk_default_mapper_config", None, [C.POINTER(tk_mapper_config)]),

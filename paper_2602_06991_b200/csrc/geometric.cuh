@@ -25,6 +25,7 @@ struct GeomFwdParams {
     const int32_t* list_offsets;
     int32_t* list_src;
     double* list_w;
+    unsigned long long* pair_count;  // += pixel-entry pairs blended (power >= cutoff, pixel live), or null
 };
 
 struct GeomBwdParams {

@@ -353,6 +353,45 @@ __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigne
 
 }  // namespace
 
+// fp64 FMA throughput probe (8 independent chains per thread): the denominator of the fp64
+// roofline the bench reports for the geometric sweeps.
+__global__ void k_dfma_probe(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = fma(x[j], a, b);
+    double s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s += x[j];
+    if (s == 12345.678) out[0] = s;
+}
+
+double measure_fp64_fma_rate(cudaStream_t st) {
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return 0.0;
+    const int blocks = 148 * 8, threads = 256, iters = 1 << 13;
+    k_dfma_probe<<<blocks, threads, 0, st>>>(out, 16, 0.999, 1e-3);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, st);
+        k_dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 0.999, 1e-3);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return static_cast<double>(blocks) * threads * iters * 8 / (best / 1e3);
+}
+
 void copy_words_to_mapped(void* dst_mapped, const void* src, int words, cudaStream_t st) {
     if (words <= 0) return;
     k_copy_words<<<1, 32, 0, st>>>(static_cast<const unsigned long long*>(src),

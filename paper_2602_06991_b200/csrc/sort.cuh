@@ -7,6 +7,9 @@ namespace tk {
 
 size_t align_bytes(size_t b);  // round up to 256 B
 
+// measured fp64 FMA instructions per second of the device (throughput probe, ~30 ms)
+double measure_fp64_fma_rate(cudaStream_t st);
+
 // words x 8 bytes from device memory into host-mapped (cudaHostAllocMapped) memory, by a kernel
 void copy_words_to_mapped(void* dst_mapped, const void* src, int words, cudaStream_t st);
 

@@ -613,6 +613,7 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
     gp.aux.n_iter = ensure<int32_t>(c->aux_n, P);
     gp.aux.wl = ptr<int32_t>(c->wl);
     gp.aux.wl_count = ensure<int32_t>(c->wl_count, tk::geom_blocks(f));
+    gp.pair_count = reinterpret_cast<unsigned long long*>(ensure<int64_t>(c->dscal, 16) + 13);  // tk_pair_count
     if (records) {
         wait_out(c, kOutRec);
         gp.color = ensure<double>(c->o_color, P * 3);
@@ -954,6 +955,11 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hvals_dev), c->hvals, 0);
         c->cur = c->stream;
         if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(&c->hscal), 16 * sizeof(int64_t), cudaHostAllocMapped);
+        if (e == cudaSuccess) e = cudaMalloc(&c->dscal.p, 16 * sizeof(int64_t));
+        if (e == cudaSuccess) {
+            c->dscal.bytes = 16 * sizeof(int64_t);
+            e = cudaMemset(c->dscal.p, 0, 16 * sizeof(int64_t));
+        }
         if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hscal_dev), c->hscal, 0);
         if (e != cudaSuccess) {
             delete c;
@@ -1366,6 +1372,27 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
             }
         }
         side_done(c, false);
+    });
+}
+
+tk_status tk_fp64_rate(tk_ctx* c, double* fma_per_s) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+        *fma_per_s = tk::measure_fp64_fma_rate(c->stream);
+        CK_LAUNCH(c);
+    });
+}
+
+tk_status tk_pair_count(tk_ctx* c, int64_t* pairs, int32_t reset) {
+    return guarded([&] {
+        CK(cudaSetDevice(c->device));
+        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+        CK(cudaStreamSynchronize(c->stream));
+        tk::copy_words_to_mapped(c->hscal_dev + 13, dscal + 13, 1, c->stream);
+        CK(cudaStreamSynchronize(c->stream));
+        if (pairs) *pairs = c->hscal[13];
+        if (reset) CK(cudaMemsetAsync(dscal + 13, 0, sizeof(int64_t), c->stream));
     });
 }
 
