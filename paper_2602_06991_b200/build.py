@@ -33,6 +33,8 @@ CUDA_UNITS = [
     ("mapping.cu", ["--fmad=false"]),
     ("mapedit.cu", ["--fmad=false"]),
     ("tk_abi.cu", []),
+    ("tk_abi_map.cu", []),
+    ("tk_abi_io.cu", []),
 ]
 
 

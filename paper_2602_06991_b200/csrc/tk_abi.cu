@@ -1,305 +1,9 @@
 // tk_abi.cu — the C ABI (include/tk_render.h): context, device-resident scene mirror, and the
-// host orchestration of the sm_100a kernels for each reference entry point.
-#include <dlfcn.h>
-#include <nccl.h>
+// host orchestration of the sm_100a kernels for each reference frame entry point.  The mapping
+// iteration lives in tk_abi_map.cu, checkpoints and queries in tk_abi_io.cu.
+#include "tk_abi_internal.cuh"
 
-#include <algorithm>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <random>
-#include <string>
-#include <vector>
-
-#include "feature.cuh"
-#include "geometric.cuh"
-#include "mapedit.cuh"
-#include "mapping.cuh"
-#include "prepare.cuh"
-#include "sort.cuh"
-#include "tk_common.cuh"
-#include "tk_render.h"
-
-namespace {
-
-thread_local std::string g_err;
-
-struct TkError {
-    tk_status st;
-    std::string msg;
-};
-
-[[noreturn]] void fail(tk_status st, const std::string& msg) { throw TkError{st, msg}; }
-
-#define CK(call)                                                                               \
-    do {                                                                                       \
-        cudaError_t e_ = (call);                                                               \
-        if (e_ != cudaSuccess)                                                                 \
-            fail(e_ == cudaErrorMemoryAllocation ? TK_ERR_OOM : TK_ERR_CUDA,                   \
-                 std::string(#call) + ": " + cudaGetErrorString(e_));                          \
-    } while (0)
-
-#define CK_LAUNCH(ctx)                                                                         \
-    do {                                                                                       \
-        cudaError_t e_ = cudaGetLastError();                                                   \
-        if (e_ != cudaSuccess) fail(TK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
-    } while (0)
-
-struct DevBuf {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-    }
-};
-
-template <class T>
-T* ensure(DevBuf& b, size_t count) {
-    const size_t need = std::max<size_t>(count, 1) * sizeof(T);
-    if (b.bytes < need) {
-        b.release();
-        const size_t alloc = tk::align_bytes(need + need / 8);
-        CK(cudaMalloc(&b.p, alloc));
-        b.bytes = alloc;
-    }
-    return static_cast<T*>(b.p);
-}
-
-template <class T>
-T* ptr(const DevBuf& b) {
-    return static_cast<T*>(b.p);
-}
-
-struct PrepKey {
-    double pose[7];
-    double fx, fy, cx, cy, near_plane, far_plane, dilation;
-    int width, height, tile_size;
-    uint64_t scene_version;
-    bool operator==(const PrepKey& o) const { return std::memcmp(this, &o, sizeof(PrepKey)) == 0; }
-};
-
-struct FwdKey {
-    PrepKey prep;
-    double tfloor, alpha_clamp, bg[3];
-    bool operator==(const FwdKey& o) const { return std::memcmp(this, &o, sizeof(FwdKey)) == 0; }
-};
-
-// NCCL entry points, resolved at tk_comm_init time so the library loads without NCCL.
-struct NcclApi {
-    void* handle = nullptr;
-    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                              cudaStream_t) = nullptr;
-    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-    const char* (*GetErrorString)(ncclResult_t) = nullptr;
-    bool load() {
-        if (handle) return true;
-        handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!handle) handle = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-        if (!handle) return false;
-        GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(handle, "ncclGetUniqueId"));
-        CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(handle, "ncclCommInitRank"));
-        AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(handle, "ncclAllGather"));
-        AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(handle, "ncclAllReduce"));
-        CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(handle, "ncclCommDestroy"));
-        GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(handle, "ncclGetErrorString"));
-        return GetUniqueId && CommInitRank && AllGather && AllReduce && CommDestroy && GetErrorString;
-    }
-};
-NcclApi g_nccl;
-
-#define NK(call)                                                                               \
-    do {                                                                                       \
-        ncclResult_t r_ = (call);                                                              \
-        if (r_ != ncclSuccess) fail(TK_ERR_NCCL, std::string(#call) + ": " + g_nccl.GetErrorString(r_)); \
-    } while (0)
-
-// CUDA-event phase timer on the context stream (tk_profile_*).
-struct Profiler {
-    bool on = false;
-    std::vector<cudaEvent_t> pool;
-    struct Rec {
-        int phase;
-        cudaEvent_t a, b;
-    };
-    std::vector<Rec> pending;
-    double ms[TK_NUM_PHASES] = {};
-    int64_t cnt[TK_NUM_PHASES] = {};
-    cudaEvent_t get() {
-        if (!pool.empty()) {
-            cudaEvent_t e = pool.back();
-            pool.pop_back();
-            return e;
-        }
-        cudaEvent_t e;
-        CK(cudaEventCreate(&e));
-        return e;
-    }
-    void drain() {
-        for (const Rec& r : pending) {
-            float t = 0.f;
-            CK(cudaEventSynchronize(r.b));
-            CK(cudaEventElapsedTime(&t, r.a, r.b));
-            ms[r.phase] += t;
-            cnt[r.phase] += 1;
-            pool.push_back(r.a);
-            pool.push_back(r.b);
-        }
-        pending.clear();
-    }
-    ~Profiler() {
-        for (const Rec& r : pending) {
-            cudaEventDestroy(r.a);
-            cudaEventDestroy(r.b);
-        }
-        for (cudaEvent_t e : pool) cudaEventDestroy(e);
-    }
-};
-
-// One keyframe of SceneMap::keyframes, device-resident (ground-truth images + pose).
-struct Keyframe {
-    tk_pose pose{};
-    int w = 0, h = 0, d = 0;
-    bool has_feature = false;
-    int64_t depth_n = 0;  // pixels with valid ground-truth depth (losses.cpp:68-71)
-    DevBuf color, depth, feature, valid;
-    void release() {
-        color.release();
-        depth.release();
-        feature.release();
-        valid.release();
-    }
-};
-
-}  // namespace
-
-struct tk_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;                    // main stream (tk_get_stream)
-    cudaStream_t s_feat = nullptr, s_geo = nullptr;  // side streams: feature path, geometry backward
-    cudaStream_t cur = nullptr;                       // stream the current call enqueues on
-    cudaEvent_t ev_main = nullptr, ev_feat = nullptr, ev_geo = nullptr;
-    // TK_HOST_ASYNC copies: host->device on s_in, device->host on s_out (both copy engines busy at
-    // once); ev_cmp orders them after the compute issued so far, ev_in / ev_out order compute after them
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev_cmp = nullptr, ev_in = nullptr, ev_out[5] = {};
-    bool out_pending[5] = {};
-    // pose twists of asynchronous backward_geometric calls: a ring of host-mapped slots, copied
-    // into the callers' structs at tk_synchronize
-    static constexpr int kTwistSlots = 64;
-    double* h_twist = nullptr;
-    double* h_twist_dev = nullptr;
-    std::vector<std::pair<double*, int>> twist_pending;
-    int twist_next = 0;
-    bool feat_pending = false, geo_pending = false;
-    int64_t launches = 0;
-    Profiler prof;
-    // scene mirror
-    int64_t n = 0;
-    int32_t d = 0;
-    uint64_t generation = 0;
-    uint64_t scene_version = 0;
-    bool has_scene = false, has_features = false;
-    DevBuf mean, log_scale, rotation, opacity_logit, color, feature;
-    // projection, per Gaussian
-    DevBuf pmx, pmy, pixx, pixy, piyy, pz, pop, rect, valid, ntiles, pos;
-    DevBuf dkeys, dvals, dkeys_alt, dvals_alt, ntiles_sorted, pair_off;
-    DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
-    DevBuf te;  // chunk-major tile entries (tk::EntryChunk)
-    DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
-    DevBuf scratch, scratch_feat, dscal;
-    int64_t* hscal = nullptr;      // host-mapped mirror of dscal (written by k_copy_words)
-    int64_t* hscal_dev = nullptr;  //   its device address
-    // prepared scene
-    bool prepared = false;
-    PrepKey prep_key{};
-    int64_t n_vis = 0, n_pairs = 0;
-    int tiles_x = 0, tiles_y = 0;
-    const uint32_t* order = nullptr;
-    const uint32_t* tile_keys_sorted = nullptr;
-    const uint32_t* tile_vals_sorted = nullptr;
-    // forward outputs / records
-    DevBuf o_color, o_depth, o_alpha, o_index, o_weight, o_count, o_contrib, aux_t, aux_n;
-    bool has_records = false;
-    int rec_w = 0, rec_h = 0, rec_k = 0;
-    uint64_t rec_generation = 0;
-    int64_t rec_map_size = 0;
-    bool aux_valid = false;
-    FwdKey aux_key{};
-    // external records staging
-    DevBuf x_index, x_weight, x_count;
-    // feature
-    DevBuf f_out, f_grad_in, f_grad_out, s_keys, s_vals, s_keys_alt, s_vals_alt, s_wnorm, s_seg;
-    int64_t fout_pixels = 0;
-    // geometric backward
-    DevBuf g_color_in, g_depth_in, mid, twist, twist_part, twist_out, gg_mean, gg_ls, gg_rot, gg_op, gg_col;
-    // full blend
-    DevBuf l_count, l_off, l_src, l_w;
-    // mapping iteration: keyframes, optimiser state (per group m / v), statistics, loss scratch
-    std::vector<Keyframe> kfs;
-    bool opt_ready = false;
-    int64_t opt_n = 0, stat_n = -1;
-    int32_t opt_d = 0;
-    int64_t step_geo = 0, step_feat = 0;
-    DevBuf am[5], av[5], fm, fv, stat_count, stat_maxc;
-    DevBuf ssim_rows, ssim_win, l_gc, l_gd, l_partial, l_values, l_fscale, l_signs;
-    double* hvals = nullptr;  // host-mapped {map, geo, feat} of the last optimize_step
-    double* hvals_dev = nullptr;
-    bool has_values = false;
-    // segment_by_query scratch (kept across calls: no allocation on the query path)
-    DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
-    DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
-    DevBuf row_ss;                                        // D-sharded partial row norms
-    // multi-GPU
-    ncclComm_t comm = nullptr;
-    int nranks = 1, rank = 0, d_total = 0;
-    DevBuf gather_buf;
-};
-
-namespace {
-
-struct PhaseScope {
-    tk_ctx* c;
-    int phase;
-    cudaEvent_t a = nullptr;
-    PhaseScope(tk_ctx* ctx, int ph) : c(ctx), phase(ph) {
-        if (c->prof.on) {
-            a = c->prof.get();
-            CK(cudaEventRecord(a, c->cur));
-        }
-    }
-    ~PhaseScope() {
-        if (a) {
-            cudaEvent_t b = c->prof.get();
-            cudaEventRecord(b, c->cur);
-            c->prof.pending.push_back({phase, a, b});
-        }
-    }
-};
-
-tk_status guard_status(const TkError& e) {
-    g_err = e.msg;
-    return e.st;
-}
-
-template <class F>
-tk_status guarded(F&& f) {
-    try {
-        f();
-        g_err.clear();
-        return TK_OK;
-    } catch (const TkError& e) {
-        return guard_status(e);
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return TK_ERR_STATE;
-    }
-}
+namespace tkabi {
 
 // Host <-> device copies made inside an API call (timed as TK_PHASE_COPY when profiling).
 void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
@@ -318,11 +22,8 @@ void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
                        c->cur));
 }
 
-// Asynchronous device->host copies are tagged by the buffers they read, so only the compute that
-// overwrites those buffers waits for them (kOutMisc: waited at the start of every call).
-enum OutTag { kOutMisc = 0, kOutRec = 1, kOutF = 2, kOutDF = 3, kOutGG = 4 };
 
-void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, int tag = kOutMisc) {
+void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, int tag) {
     if (bytes == 0 || dst == nullptr) return;
     if (mem == TK_HOST_ASYNC) {  // after the compute that produced src; its overwriters wait for it
         CK(cudaEventRecord(c->ev_cmp, c->cur));
@@ -442,7 +143,7 @@ tk::TileEntries tile_entries(tk_ctx* c) {
     return t;
 }
 
-void ensure_scratch(tk_ctx* c, int64_t n, bool feat = false) {
+void ensure_scratch(tk_ctx* c, int64_t n, bool feat) {
     const size_t need = std::max(tk::radix_scratch_bytes(n), tk::scan_scratch_bytes(n + 1));
     ensure<char>(feat ? c->scratch_feat : c->scratch, need);
 }
@@ -647,12 +348,6 @@ std::string stale_message(const char* fn, int32_t idx, int64_t n) {
            std::to_string(n) + " (stale snapshot)";
 }
 
-struct Records {
-    int w = 0, h = 0, k = 0;
-    const int32_t* index = nullptr;
-    const double* weight = nullptr;
-    const uint8_t* count = nullptr;
-};
 
 // Resolve a TopKGrid argument to device pointers, with the reference's stale-index check
 // (render.cpp:305-311, backward.cpp:278-283) done before any work.
@@ -711,12 +406,6 @@ Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
     return r;
 }
 
-struct SlotIndex {
-    const int32_t* seg;
-    const uint32_t* slots;
-    const float* wnorm;
-    tk::LongPlan plan;  // chunks of the segments longer than tk::kLongSeg
-};
 
 // Inverted (Gaussian -> record slots) index of a TopKGrid, ascending slot order per Gaussian.
 SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
@@ -788,98 +477,6 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     cp.dilation = s->cov2d_dilation;
     return cp;
 }
-
-// Grow a device array to new_count elements keeping the first old_count (structural edits).
-template <class T>
-T* grow_keep(tk_ctx* c, DevBuf& b, int64_t old_count, int64_t new_count, bool zero_tail) {
-    const size_t need = static_cast<size_t>(std::max<int64_t>(new_count, 1)) * sizeof(T);
-    if (b.bytes < need) {
-        DevBuf nb;
-        const size_t alloc = tk::align_bytes(need + need / 8);
-        CK(cudaMalloc(&nb.p, alloc));
-        nb.bytes = alloc;
-        if (old_count > 0 && b.p)
-            CK(cudaMemcpyAsync(nb.p, b.p, old_count * sizeof(T), cudaMemcpyDeviceToDevice, c->cur));
-        CK(cudaStreamSynchronize(c->cur));
-        b.release();
-        b = nb;
-    }
-    if (zero_tail && new_count > old_count)
-        CK(cudaMemsetAsync(ptr<T>(b) + old_count, 0, (new_count - old_count) * sizeof(T), c->cur));
-    return ptr<T>(b);
-}
-
-// Keep the rows flagged in keep (n rows of `width` elements) in order, into a fresh buffer.
-template <class T>
-void compact_rows(tk_ctx* c, DevBuf& b, int64_t n, int width, int64_t n_keep, const int32_t* keep,
-                  const int32_t* pos) {
-    if (!b.p || width <= 0) return;
-    DevBuf nb;
-    ensure<T>(nb, std::max<int64_t>(n_keep, 1) * width);
-    if (sizeof(T) == 8)
-        tk::launch_compact_f64(reinterpret_cast<const double*>(b.p), static_cast<double*>(nb.p), keep, pos, n, width,
-                               c->cur);
-    else
-        tk::launch_compact_f32(reinterpret_cast<const float*>(b.p), static_cast<float*>(nb.p), keep, pos, n, width,
-                               c->cur);
-    c->launches += n > 0;
-    CK_LAUNCH(c);
-    CK(cudaStreamSynchronize(c->cur));
-    b.release();
-    b = nb;
-}
-
-// prune_map's candidate draw (mapper.cpp:80-139), host side: candidates have topk_count <=
-// threshold; ceil(keep_ratio * candidates) survive, drawn without replacement proportionally to
-// max_contribution with std::mt19937_64(seed), uniformly once the mass is exhausted.
-std::vector<int32_t> prune_select(const std::vector<int32_t>& counts, const std::vector<double>& maxc,
-                                  double keep_ratio, uint64_t seed, int32_t threshold) {
-    std::vector<int32_t> cand;
-    for (size_t i = 0; i < counts.size(); ++i)
-        if (counts[i] <= threshold) cand.push_back(static_cast<int32_t>(i));
-    std::vector<int32_t> removed;
-    if (cand.empty()) return removed;
-    std::vector<double> score(cand.size());
-    double total = 0.0;
-    for (size_t i = 0; i < cand.size(); ++i) {
-        score[i] = maxc[cand[i]];
-        total += score[i];
-    }
-    if (!(total > 0.0)) return removed;  // survival weights undefined: keep every candidate
-    const size_t keep = static_cast<size_t>(std::ceil(keep_ratio * static_cast<double>(cand.size())));
-    if (keep >= cand.size()) return removed;
-    std::mt19937_64 rng(seed);
-    std::vector<uint8_t> kept(cand.size(), 0);
-    std::vector<size_t> pool(cand.size());
-    for (size_t i = 0; i < pool.size(); ++i) pool[i] = i;
-    double mass = total;
-    for (size_t draw = 0; draw < keep; ++draw) {
-        size_t pick = 0;
-        if (mass > 0.0) {
-            const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53 * mass;  // canonical_unit * mass
-            double acc = 0.0;
-            pick = pool.size() - 1;
-            for (size_t q = 0; q < pool.size(); ++q) {
-                acc += score[pool[q]];
-                if (u < acc) {
-                    pick = q;
-                    break;
-                }
-            }
-        } else {
-            pick = static_cast<size_t>(rng() % pool.size());
-        }
-        const size_t chosen = pool[pick];
-        kept[chosen] = 1;
-        mass -= score[chosen];
-        if (mass < 0.0) mass = 0.0;
-        pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(pick));
-    }
-    for (size_t i = 0; i < cand.size(); ++i)
-        if (!kept[i]) removed.push_back(cand[i]);
-    return removed;
-}
-
 void scene_changed(tk_ctx* c) {
     c->scene_version += 1;
     c->prepared = false;
@@ -891,7 +488,7 @@ void require_features(tk_ctx* c) {
     if (!c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
 }
 
-}  // namespace
+}  // namespace tkabi
 
 // =========================================================================================
 extern "C" {
@@ -1483,736 +1080,6 @@ tk_status tk_allreduce_sum_f64(tk_ctx* c, double* values, int32_t count) {
         sync(c);
         tmp.release();
         main_done(c);
-    });
-}
-
-// ------------------------------------------------------------------ mapping iteration
-void tk_default_mapper_config(tk_mapper_config* cfg) {
-    cfg->lambda_geo = 1.0;  // losses.hpp:9-21
-    cfg->lambda_feat = 1.0;
-    cfg->lambda1 = 0.2;
-    cfg->lambda2 = 1.0;
-    cfg->color_secondary = 0;
-    cfg->feature_update_period = 5;  // mapper.hpp:16
-    cfg->l1_deadband = 0.0;
-    cfg->lr_mean = 2e-3;  // optimizer.hpp:15-22
-    cfg->lr_log_scale = 5e-3;
-    cfg->lr_rotation = 1e-3;
-    cfg->lr_opacity = 5e-2;
-    cfg->lr_color = 2e-2;
-    cfg->lr_feature = 1e-2;
-    cfg->beta1 = 0.9;  // optimizer.hpp:9-13
-    cfg->beta2 = 0.999;
-    cfg->eps = 1e-8;
-    cfg->min_log_scale = -10.0;  // mapper.hpp:31-32
-    cfg->max_log_scale = 1.0;
-}
-
-tk_status tk_keyframe_set(tk_ctx* c, int32_t slot, const tk_pose* pose, const tk_frame_view* fr) {
-    return guarded([&] {
-        if (!c || !pose || !fr) fail(TK_ERR_BAD_ARG, "null argument");
-        if (slot < 0 || slot > (1 << 20)) fail(TK_ERR_BAD_ARG, "keyframe slot out of range");
-        if (fr->width <= 0 || fr->height <= 0 || fr->d < 0) fail(TK_ERR_BAD_ARG, "bad frame shape");
-        if (!fr->color || !fr->depth) fail(TK_ERR_BAD_ARG, "frame needs color and depth");
-        if (fr->d > 0 && !fr->feature) fail(TK_ERR_BAD_ARG, "frame feature is NULL but d > 0");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        if (static_cast<size_t>(slot) >= c->kfs.size()) c->kfs.resize(slot + 1);
-        Keyframe& k = c->kfs[slot];
-        k.pose = *pose;
-        k.w = fr->width;
-        k.h = fr->height;
-        k.d = fr->d;
-        k.has_feature = fr->d > 0;
-        const int64_t P = static_cast<int64_t>(k.w) * k.h;
-        float* col = ensure<float>(k.color, P * 3);
-        float* dep = ensure<float>(k.depth, P);
-        copy_in(col, fr->color, P * 3 * sizeof(float), fr->mem, c);
-        copy_in(dep, fr->depth, P * sizeof(float), fr->mem, c);
-        float* feat = nullptr;
-        if (k.has_feature) {
-            feat = ensure<float>(k.feature, P * k.d);
-            copy_in(feat, fr->feature, static_cast<size_t>(P) * k.d * sizeof(float), fr->mem, c);
-        }
-        uint8_t* valid = ensure<uint8_t>(k.valid, P);
-        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-        tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, dep, c->cur);
-        c->launches += 1;
-        CK_LAUNCH(c);
-        if (c->comm)  // D-sharded: a pixel's keyframe row is valid if any shard's channels are non-zero
-            NK(g_nccl.AllReduce(valid, valid, static_cast<size_t>(P), ncclUint8, ncclMax, c->comm, c->cur));
-        tk::copy_words_to_mapped(c->hscal_dev + 9, dscal + 9, 1, c->cur);
-        sync(c);
-        k.depth_n = c->hscal[9];
-        main_done(c);
-    });
-}
-
-tk_status tk_optimizer_reset(tk_ctx* c, int32_t reset_stats) {
-    return guarded([&] {
-        if (!c) fail(TK_ERR_BAD_ARG, "null context");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        const int64_t n = c->n;
-        const int dims[5] = {3, 3, 4, 1, 3};
-        for (int g = 0; g < 5; ++g) {
-            CK(cudaMemsetAsync(ensure<double>(c->am[g], n * dims[g]), 0, std::max<int64_t>(n, 1) * dims[g] * 8, c->cur));
-            CK(cudaMemsetAsync(ensure<double>(c->av[g], n * dims[g]), 0, std::max<int64_t>(n, 1) * dims[g] * 8, c->cur));
-        }
-        const int64_t nd = n * std::max(c->d, 1);
-        CK(cudaMemsetAsync(ensure<float>(c->fm, nd), 0, std::max<int64_t>(nd, 1) * 4, c->cur));
-        CK(cudaMemsetAsync(ensure<float>(c->fv, nd), 0, std::max<int64_t>(nd, 1) * 4, c->cur));
-        if (reset_stats || c->stat_n != n) {
-            CK(cudaMemsetAsync(ensure<int32_t>(c->stat_count, n), 0, std::max<int64_t>(n, 1) * 4, c->cur));
-            CK(cudaMemsetAsync(ensure<double>(c->stat_maxc, n), 0, std::max<int64_t>(n, 1) * 8, c->cur));
-            c->stat_n = n;
-        }
-        c->step_geo = c->step_feat = 0;
-        c->opt_ready = true;
-        c->opt_n = n;
-        c->opt_d = c->d;
-        main_done(c);
-    });
-}
-
-tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_camera* cam, const tk_settings* s,
-                           int32_t slot, int64_t iteration, double* values_out, int32_t* feature_step_out) {
-    return guarded([&] {
-        check_frame(cam, s);
-        if (!cfg) fail(TK_ERR_BAD_ARG, "null mapper config");
-        if (slot < 0 || static_cast<size_t>(slot) >= c->kfs.size() || c->kfs[slot].w == 0)
-            fail(TK_ERR_BAD_ARG, "optimize_step: no keyframe in that slot");
-        if (cfg->feature_update_period <= 0) fail(TK_ERR_BAD_ARG, "feature_update_period must be positive");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        if (!c->opt_ready || c->opt_n != c->n || c->opt_d != c->d || c->stat_n != c->n)
-            fail(TK_ERR_STATE, "optimizer state does not match the scene (tk_optimizer_reset)");
-        const Keyframe& kf = c->kfs[slot];
-        if (kf.w != cam->width || kf.h != cam->height)
-            fail(TK_ERR_BAD_ARG, "compute_losses: render/frame shape mismatch");
-        const bool feature_step = (iteration % cfg->feature_update_period) == 0;  // mapper.cpp:171
-        const bool sharded = c->comm != nullptr;  // D-sharded mapping (features: this rank's slice)
-        const bool use_ssim = cfg->lambda1 != 0.0 && cfg->color_secondary == 0;
-        if (use_ssim && (cam->width < tk::kSsimWin || cam->height < tk::kSsimWin))
-            fail(TK_ERR_BAD_ARG, "ssim: image smaller than the 11x11 window");
-        if (feature_step) {
-            if (c->d <= 0 || !c->has_features)
-                fail(TK_ERR_BAD_ARG, "compute_losses: feature loss requested but render has no feature image");
-            if (kf.d != c->d) fail(TK_ERR_BAD_ARG, "compute_losses: feature shape mismatch");
-        }
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        cudaStream_t st = c->cur;
-        // render_geometric on the keyframe pose (mapper.cpp:173)
-        prepare(c, &kf.pose, cam, s);
-        forward(c, cam, s, true);
-        const tk::Frame f = make_frame(c, cam, s);
-        const int64_t P = static_cast<int64_t>(f.width) * f.height;
-        const int64_t n = c->n;
-        const int d = c->d;
-        double* gc = ensure<double>(c->l_gc, P * 3);
-        double* gd = ensure<double>(c->l_gd, P);
-        double* partial = ensure<double>(c->l_partial, tk::kLossBlocks * tk::kLossSlots);
-        double* values = ensure<double>(c->l_values, 4);
-        float* fscale = ensure<float>(c->l_fscale, 1);
-        const int wpp = (d + 15) / 16;
-        uint32_t* signs = feature_step ? ensure<uint32_t>(c->l_signs, P * std::max(wpp, 1)) : nullptr;
-        {
-            PhaseScope phase(c, TK_PHASE_LOSS);
-            CK(cudaMemsetAsync(partial, 0, tk::kLossBlocks * tk::kLossSlots * sizeof(double), st));
-            tk::launch_topk_stats(ptr<int32_t>(c->o_index), ptr<uint8_t>(c->o_count), P, f.k,
-                                  ptr<int32_t>(c->stat_count), st);
-            c->launches += 1;
-            // compute_losses (mapper.cpp:176, losses.cpp:22-133)
-            tk::ColorLossParams lp{};
-            lp.w = f.width;
-            lp.h = f.height;
-            lp.color = ptr<double>(c->o_color);
-            lp.depth = ptr<double>(c->o_depth);
-            lp.gt_color = ptr<float>(kf.color);
-            lp.gt_depth = ptr<float>(kf.depth);
-            lp.lambda_geo = cfg->lambda_geo;
-            lp.lambda1 = cfg->lambda1;
-            lp.lambda2 = cfg->lambda2;
-            lp.deadband = cfg->l1_deadband;
-            lp.use_ssim = use_ssim ? 1 : 0;
-            lp.use_depth = (kf.depth_n > 0 && cfg->lambda2 != 0.0) ? 1 : 0;
-            lp.inv_color_n = 1.0 / (static_cast<double>(f.width) * f.height * 3.0);
-            lp.inv_depth_n = kf.depth_n > 0 ? 1.0 / static_cast<double>(kf.depth_n) : 0.0;
-            {
-                const int ow = f.width - tk::kSsimWin + 1, oh = f.height - tk::kSsimWin + 1;
-                const size_t count = use_ssim ? static_cast<size_t>(ow) * oh * 3 : 1;  // ssim.cpp:119-123
-                lp.inv_count = 1.0 / static_cast<double>(count);
-                double sum = 0.0;  // gaussian_kernel(), ssim.cpp:18-28
-                for (int i = 0; i < tk::kSsimWin; ++i) {
-                    const double dd = i - tk::kSsimWin / 2;
-                    lp.kern[i] = std::exp(-0.5 * dd * dd / (1.5 * 1.5));
-                    sum += lp.kern[i];
-                }
-                for (double& v : lp.kern) v /= sum;
-                if (use_ssim) {
-                    lp.win = ensure<double>(c->ssim_win, 15LL * oh * ow);
-                }
-            }
-            lp.grad_color = gc;
-            lp.grad_depth = gd;
-            lp.partial = partial;
-            tk::launch_color_loss(lp, st, &c->launches);
-            if (feature_step) {
-                tk::FeatLossParams fl{};
-                fl.width = f.width;
-                fl.height = f.height;
-                fl.k = f.k;
-                fl.d = d;
-                fl.index = ptr<int32_t>(c->o_index);
-                fl.weight = ptr<double>(c->o_weight);
-                fl.count = ptr<uint8_t>(c->o_count);
-                fl.feat = ptr<float>(c->feature);
-                fl.gt = ptr<float>(kf.feature);
-                fl.gt_valid = ptr<uint8_t>(kf.valid);
-                fl.signs = signs;
-                fl.partial = partial;
-                tk::launch_feature_loss(fl, st);
-                c->launches += 1;
-            }
-            if (sharded)  // feature partials differ per shard; colour / depth rows are replicas
-                NK(g_nccl.AllReduce(partial, partial, tk::kLossBlocks * tk::kLossSlots, ncclFloat64, ncclSum, c->comm,
-                                    st));
-            tk::FinalizeParams fp{};
-            fp.partial = partial;
-            fp.nparts = tk::kLossBlocks;
-            fp.replicas = sharded ? static_cast<double>(c->nranks) : 1.0;
-            fp.lambda_geo = cfg->lambda_geo;
-            fp.lambda_feat = cfg->lambda_feat;
-            fp.lambda1 = cfg->lambda1;
-            fp.lambda2 = cfg->lambda2;
-            fp.use_ssim = lp.use_ssim;
-            fp.secondary_l1 = (cfg->lambda1 != 0.0 && cfg->color_secondary != 0) ? 1 : 0;
-            fp.use_depth = lp.use_depth;
-            fp.feature_step = feature_step ? 1 : 0;
-            fp.d = sharded ? c->d_total : d;  // losses.cpp:106: mean over every channel
-            fp.inv_color_n = lp.inv_color_n;
-            fp.inv_depth_n = lp.inv_depth_n;
-            fp.inv_count = lp.inv_count;
-            fp.values = values;
-            fp.feat_scale = fscale;
-            tk::launch_loss_finalize(fp, st);
-            c->launches += 1;
-            CK_LAUNCH(c);
-        }
-        tk::copy_words_to_mapped(c->hvals_dev, values, 3, st);
-        c->has_values = true;
-        // backward_geometric (mapper.cpp:179-180) on this forward
-        double* mid = geom_sweep(c, f, gc, gd);
-        if (sharded)  // replicas stay bit-identical: one all-reduced geometry gradient on every shard
-            NK(g_nccl.AllReduce(mid, mid, static_cast<size_t>(n) * 10, ncclFloat64, ncclSum, c->comm, st));
-        {
-            PhaseScope phase(c, TK_PHASE_ADAM);
-            // geometry groups (mapper.cpp:183-236): five adam_step calls, one step counter each
-            c->step_geo += 1;
-            tk::GeoAdamParams ga{};
-            ga.mean = ptr<double>(c->mean);
-            ga.log_scale = ptr<double>(c->log_scale);
-            ga.rotation = ptr<double>(c->rotation);
-            ga.opacity_logit = ptr<double>(c->opacity_logit);
-            ga.color = ptr<double>(c->color);
-            for (int g = 0; g < 5; ++g) {
-                ga.m[g] = ptr<double>(c->am[g]);
-                ga.v[g] = ptr<double>(c->av[g]);
-            }
-            ga.lr[0] = cfg->lr_mean;
-            ga.lr[1] = cfg->lr_log_scale;
-            ga.lr[2] = cfg->lr_rotation;
-            ga.lr[3] = cfg->lr_opacity;
-            ga.lr[4] = cfg->lr_color;
-            ga.beta1 = cfg->beta1;
-            ga.beta2 = cfg->beta2;
-            ga.eps = cfg->eps;
-            ga.bc1 = 1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_geo));  // optimizer.cpp:52-53
-            ga.bc2 = 1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_geo));
-            ga.min_log_scale = cfg->min_log_scale;
-            ga.max_log_scale = cfg->max_log_scale;
-            ga.contrib = ptr<unsigned long long>(c->o_contrib);
-            ga.max_contrib = ptr<double>(c->stat_maxc);
-            tk::ChainParams cp = chain_params(c, &kf.pose, cam, s, mid);
-            cp.mid_scale = sharded ? 1.0 / c->nranks : 1.0;
-            cp.g_mean = ensure<double>(c->gg_mean, n * 3);
-            cp.g_log_scale = ensure<double>(c->gg_ls, n * 3);
-            cp.g_rotation = ensure<double>(c->gg_rot, n * 4);
-            cp.g_opacity_logit = ensure<double>(c->gg_op, n);
-            cp.g_color = ensure<double>(c->gg_col, n * 3);
-            cp.twist = nullptr;
-            tk::launch_chain(cp, st);
-            ga.g[0] = cp.g_mean;
-            ga.g[1] = cp.g_log_scale;
-            ga.g[2] = cp.g_rotation;
-            ga.g[3] = cp.g_opacity_logit;
-            ga.g[4] = cp.g_color;
-            tk::launch_geo_adam(ga, n, st);
-            c->launches += n > 0 ? 2 : 0;
-            CK_LAUNCH(c);
-            if (feature_step && d > 0) {  // mapper.cpp:239-252
-                c->step_feat += 1;
-                Records r;
-                r.w = f.width;
-                r.h = f.height;
-                r.k = f.k;
-                r.index = ptr<int32_t>(c->o_index);
-                r.weight = ptr<double>(c->o_weight);
-                r.count = ptr<uint8_t>(c->o_count);
-                const SlotIndex si = build_slot_index(c, r);
-                tk::FeatAdamParams fa{};
-                fa.n = n;
-                fa.k = f.k;
-                fa.d = d;
-                fa.seg = si.seg;
-                fa.slots = si.slots;
-                fa.wnorm = si.wnorm;
-                fa.signs = signs;
-                fa.scale = fscale;
-                fa.feat = ptr<float>(c->feature);
-                fa.m = ptr<float>(c->fm);
-                fa.v = ptr<float>(c->fv);
-                fa.lr = static_cast<float>(cfg->lr_feature);
-                fa.beta1 = static_cast<float>(cfg->beta1);
-                fa.beta2 = static_cast<float>(cfg->beta2);
-                fa.eps = static_cast<float>(cfg->eps);
-                fa.one_m_beta1 = static_cast<float>(1.0 - cfg->beta1);
-                fa.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
-                fa.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat))));
-                fa.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat))));
-                fa.plan = si.plan;
-                if (sharded) fa.row_ss = ensure<float>(c->row_ss, n);
-                tk::launch_feature_adam(fa, st);
-                c->launches += n > 0 ? 3 : 0;
-                if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
-                    NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
-                                        st));
-                    tk::launch_feature_renorm(ptr<float>(c->feature), fa.row_ss, n, d, st);
-                    c->launches += 1;
-                }
-                CK_LAUNCH(c);
-            }
-        }
-        // the scene changed: the next render re-projects (records keep the pre-step snapshot)
-        c->scene_version += 1;
-        c->prepared = false;
-        c->aux_valid = false;
-        if (feature_step_out) *feature_step_out = feature_step ? 1 : 0;
-        if (values_out) {
-            sync(c);
-            std::memcpy(values_out, c->hvals, 3 * sizeof(double));
-        }
-        main_done(c);
-    });
-}
-
-tk_status tk_loss_values(tk_ctx* c, double values[3]) {
-    return guarded([&] {
-        if (!c->has_values) fail(TK_ERR_STATE, "no optimize_step has run");
-        CK(cudaSetDevice(c->device));
-        CK(cudaStreamSynchronize(c->stream));
-        std::memcpy(values, c->hvals, 3 * sizeof(double));
-    });
-}
-
-tk_status tk_scene_download(tk_ctx* c, const tk_scene_out* o) {
-    return guarded([&] {
-        if (!c || !o) fail(TK_ERR_BAD_ARG, "null argument");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        if ((o->topk_count || o->max_contribution) && c->stat_n != c->n)
-            fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        const int64_t n = c->n;
-        copy_out(o->mean, c->mean.p, n * 3 * sizeof(double), o->mem, c);
-        copy_out(o->log_scale, c->log_scale.p, n * 3 * sizeof(double), o->mem, c);
-        copy_out(o->rotation, c->rotation.p, n * 4 * sizeof(double), o->mem, c);
-        copy_out(o->opacity_logit, c->opacity_logit.p, n * sizeof(double), o->mem, c);
-        copy_out(o->color, c->color.p, n * 3 * sizeof(double), o->mem, c);
-        if (o->feature && c->has_features)
-            copy_out(o->feature, c->feature.p, static_cast<size_t>(n) * c->d * sizeof(float), o->mem, c);
-        copy_out(o->topk_count, c->stat_count.p, n * sizeof(int32_t), o->mem, c);
-        copy_out(o->max_contribution, c->stat_maxc.p, n * sizeof(double), o->mem, c);
-        if (o->mem == TK_HOST) sync(c);
-        main_done(c);
-    });
-}
-
-// ------------------------------------------------------------------ structural edits
-tk_status tk_scene_info(tk_ctx* c, int64_t* n, int32_t* d, uint64_t* generation) {
-    return guarded([&] {
-        if (!c) fail(TK_ERR_BAD_ARG, "null context");
-        if (n) *n = c->n;
-        if (d) *d = c->d;
-        if (generation) *generation = c->generation;
-    });
-}
-
-tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, const tk_pose* w2c,
-                              int32_t* inserted) {
-    return guarded([&] {
-        if (!c || !src || !w2c) fail(TK_ERR_BAD_ARG, "null argument");
-        if (src->n < 0 || src->d < 0) fail(TK_ERR_BAD_ARG, "negative source size");
-        if (src->n > 0 && (!src->position || !src->color || !src->spacing || !src->distance))
-            fail(TK_ERR_BAD_ARG, "insert_gaussians: position, color, spacing and distance are required");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        cudaStream_t st = c->cur;
-        const int64_t ns = src->n;
-        if (inserted) *inserted = 0;
-        if (ns == 0) {
-            main_done(c);
-            return;
-        }
-        DevBuf bpos, bcol, bsp, bdist, bfeat, bflag, bflag32, bslot;
-        auto dev_in = [&](DevBuf& b, const void* p, size_t bytes) -> const void* {
-            if (src->mem == TK_DEVICE) return p;
-            ensure<char>(b, bytes);
-            copy_in(b.p, p, bytes, TK_HOST, c);
-            return b.p;
-        };
-        const double* pos = static_cast<const double*>(dev_in(bpos, src->position, ns * 3 * sizeof(double)));
-        const double* col = static_cast<const double*>(dev_in(bcol, src->color, ns * 3 * sizeof(double)));
-        const double* sp = static_cast<const double*>(dev_in(bsp, src->spacing, ns * sizeof(double)));
-        const double* dist = static_cast<const double*>(dev_in(bdist, src->distance, ns * sizeof(double)));
-        const float* feat = (src->feature && src->d > 0)
-                                ? static_cast<const float*>(dev_in(bfeat, src->feature, ns * src->d * sizeof(float)))
-                                : nullptr;
-        uint8_t* flag = ensure<uint8_t>(bflag, ns);
-        int32_t* flag32 = ensure<int32_t>(bflag32, ns);
-        int32_t* slot = ensure<int32_t>(bslot, ns);
-        tk::launch_insert_flags(dist, ns, tau, flag, flag32, st);
-        ensure_scratch(c, ns + 1);
-        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-        tk::scan_exclusive(flag32, slot, ns, dscal + 10, c->scratch.p, st, &c->launches);
-        tk::copy_words_to_mapped(c->hscal_dev + 10, dscal + 10, 1, st);
-        sync(c);
-        const int64_t total = c->hscal[10];
-        c->launches += 1;
-        if (total > 0) {
-            if (c->d == 0 && feat && (c->n == 0 || !c->has_features)) c->d = src->d;  // mapper.cpp:40-41
-            const int64_t n0 = c->n, n1 = n0 + total;
-            const int d = c->d;
-            tk::InsertParams ip{};
-            ip.n_src = ns;
-            ip.base = n0;
-            ip.position = pos;
-            ip.color = col;
-            ip.feature = feat;
-            ip.d_src = src->d;
-            ip.spacing = sp;
-            ip.slot = slot;
-            ip.flag = flag;
-            // se3_inverse (pose.cpp:14-19) and its normalised rotation (mapper.cpp:25-26)
-            const double qi[4] = {w2c->qw, -w2c->qx, -w2c->qy, -w2c->qz};
-            const double t[3] = {w2c->tx, w2c->ty, w2c->tz};
-            double ti[3];
-            tk::quat_rotate_eigen(qi, t, ti);
-            const double qn = std::sqrt(((qi[0] * qi[0] + qi[1] * qi[1]) + qi[2] * qi[2]) + qi[3] * qi[3]);
-            for (int a = 0; a < 4; ++a) {
-                ip.qi[a] = qi[a];
-                ip.rot[a] = qi[a] / qn;
-            }
-            for (int a = 0; a < 3; ++a) ip.ti[a] = -ti[a];
-            ip.opacity_logit = std::log(0.5 / (1.0 - 0.5));                     // logit(0.5)
-            ip.d = d;
-            ip.mean = grow_keep<double>(c, c->mean, n0 * 3, n1 * 3, false);
-            ip.log_scale = grow_keep<double>(c, c->log_scale, n0 * 3, n1 * 3, false);
-            ip.rotation = grow_keep<double>(c, c->rotation, n0 * 4, n1 * 4, false);
-            ip.opacity = grow_keep<double>(c, c->opacity_logit, n0, n1, false);
-            ip.color_out = grow_keep<double>(c, c->color, n0 * 3, n1 * 3, false);
-            if (d > 0) {
-                ip.feat = grow_keep<float>(c, c->feature, c->has_features ? n0 * d : 0, n1 * d, false);
-                c->has_features = true;
-            }
-            tk::launch_insert_fill(ip, st);
-            c->launches += 1;
-            CK_LAUNCH(c);
-            if (c->opt_ready && c->opt_n == n0) {  // OptimizerState::extend (optimizer.cpp:29-36)
-                const int dims[5] = {3, 3, 4, 1, 3};
-                for (int g = 0; g < 5; ++g) {
-                    grow_keep<double>(c, c->am[g], n0 * dims[g], n1 * dims[g], true);
-                    grow_keep<double>(c, c->av[g], n0 * dims[g], n1 * dims[g], true);
-                }
-                grow_keep<float>(c, c->fm, n0 * c->opt_d, n1 * d, true);
-                grow_keep<float>(c, c->fv, n0 * c->opt_d, n1 * d, true);
-                if (c->opt_d != d) {  // the feature group is sized now (mapper.cpp:54)
-                    CK(cudaMemsetAsync(c->fm.p, 0, n1 * d * sizeof(float), st));
-                    CK(cudaMemsetAsync(c->fv.p, 0, n1 * d * sizeof(float), st));
-                }
-                c->opt_n = n1;
-                c->opt_d = d;
-            }
-            if (c->stat_n == n0) {
-                grow_keep<int32_t>(c, c->stat_count, n0, n1, true);
-                grow_keep<double>(c, c->stat_maxc, n0, n1, true);
-                c->stat_n = n1;
-            }
-            c->n = n1;
-            c->generation += 1;                                                 // mapper.cpp:56
-            scene_changed(c);
-            if (inserted) *inserted = static_cast<int32_t>(total);
-        }
-        sync(c);
-        for (DevBuf* b : {&bpos, &bcol, &bsp, &bdist, &bfeat, &bflag, &bflag32, &bslot}) b->release();
-        main_done(c);
-    });
-}
-
-tk_status tk_prune_map(tk_ctx* c, double keep_ratio, uint64_t seed, int32_t threshold, int32_t* removed_out,
-                       int64_t* n_removed) {
-    return guarded([&] {
-        if (!c) fail(TK_ERR_BAD_ARG, "null context");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        if (c->stat_n != c->n) fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        cudaStream_t st = c->cur;
-        const int64_t n = c->n;
-        std::vector<int32_t> counts(n);
-        std::vector<double> maxc(n);
-        copy_out(counts.data(), c->stat_count.p, n * sizeof(int32_t), TK_HOST, c);
-        copy_out(maxc.data(), c->stat_maxc.p, n * sizeof(double), TK_HOST, c);
-        sync(c);
-        const std::vector<int32_t> removed = prune_select(counts, maxc, keep_ratio, seed, threshold);
-        const int64_t nr = static_cast<int64_t>(removed.size());
-        if (nr > 0) {  // mapper.cpp:141-154 + OptimizerState::compact
-            DevBuf brem, bkeep, bpos;
-            int32_t* drem = ensure<int32_t>(brem, nr);
-            copy_in(drem, removed.data(), nr * sizeof(int32_t), TK_HOST, c);
-            int32_t* keep = ensure<int32_t>(bkeep, n);
-            int32_t* pos = ensure<int32_t>(bpos, n);
-            tk::launch_keep_flags(drem, nr, n, keep, st);
-            ensure_scratch(c, n + 1);
-            int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-            tk::scan_exclusive(keep, pos, n, dscal + 11, c->scratch.p, st, &c->launches);
-            c->launches += 2;
-            const int64_t nk = n - nr;
-            compact_rows<double>(c, c->mean, n, 3, nk, keep, pos);
-            compact_rows<double>(c, c->log_scale, n, 3, nk, keep, pos);
-            compact_rows<double>(c, c->rotation, n, 4, nk, keep, pos);
-            compact_rows<double>(c, c->opacity_logit, n, 1, nk, keep, pos);
-            compact_rows<double>(c, c->color, n, 3, nk, keep, pos);
-            if (c->has_features && c->d > 0) compact_rows<float>(c, c->feature, n, c->d, nk, keep, pos);
-            if (c->opt_ready && c->opt_n == n) {
-                const int dims[5] = {3, 3, 4, 1, 3};
-                for (int g = 0; g < 5; ++g) {
-                    compact_rows<double>(c, c->am[g], n, dims[g], nk, keep, pos);
-                    compact_rows<double>(c, c->av[g], n, dims[g], nk, keep, pos);
-                }
-                if (c->opt_d > 0) {
-                    compact_rows<float>(c, c->fm, n, c->opt_d, nk, keep, pos);
-                    compact_rows<float>(c, c->fv, n, c->opt_d, nk, keep, pos);
-                }
-                c->opt_n = nk;
-            }
-            sync(c);
-            for (DevBuf* b : {&brem, &bkeep, &bpos}) b->release();
-            c->n = nk;
-            c->generation += 1;                                                 // mapper.cpp:153
-            scene_changed(c);
-        }
-        // the statistics window restarts at every prune (mapper.cpp:156-159)
-        CK(cudaMemsetAsync(c->stat_count.p, 0, std::max<int64_t>(c->n, 1) * sizeof(int32_t), st));
-        CK(cudaMemsetAsync(c->stat_maxc.p, 0, std::max<int64_t>(c->n, 1) * sizeof(double), st));
-        c->stat_n = c->n;
-        if (removed_out && nr) std::memcpy(removed_out, removed.data(), nr * sizeof(int32_t));
-        if (n_removed) *n_removed = nr;
-        main_done(c);
-    });
-}
-
-// ------------------------------------------------------------------ checkpoint / query
-namespace {
-constexpr char kSplfMagic[4] = {'S', 'P', 'L', 'F'};
-constexpr uint32_t kSplfVersion = 1;
-
-tk::SplfView splf_view(tk_ctx* c) {
-    tk::SplfView v{};
-    v.n = c->n;
-    v.d = c->d;
-    v.mean = ptr<double>(c->mean);
-    v.log_scale = ptr<double>(c->log_scale);
-    v.rotation = ptr<double>(c->rotation);
-    v.opacity_logit = ptr<double>(c->opacity_logit);
-    v.color = ptr<double>(c->color);
-    v.feature = ptr<float>(c->feature);
-    return v;
-}
-}  // namespace
-
-tk_status tk_checkpoint_save(tk_ctx* c, const char* path) {
-    return guarded([&] {
-        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
-        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
-        if (c->d > 0 && !c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        const int64_t n = c->n;
-        const int64_t W = 14 + c->d;
-        DevBuf rec;
-        float* drec = ensure<float>(rec, n * W);
-        tk::launch_splf_pack(splf_view(c), drec, c->cur);
-        c->launches += n > 0;
-        CK_LAUNCH(c);
-        const size_t body = static_cast<size_t>(n) * W * sizeof(float);
-        char* host = nullptr;
-        CK(cudaHostAlloc(reinterpret_cast<void**>(&host), 20 + body, cudaHostAllocDefault));
-        std::memcpy(host, kSplfMagic, 4);                                        // checkpoint.cpp:42-45
-        const uint32_t ver = kSplfVersion, dim = static_cast<uint32_t>(c->d);
-        const uint64_t cnt = static_cast<uint64_t>(n);
-        std::memcpy(host + 4, &ver, 4);
-        std::memcpy(host + 8, &dim, 4);
-        std::memcpy(host + 12, &cnt, 8);
-        copy_out(host + 20, drec, body, TK_HOST, c);
-        sync(c);
-        rec.release();
-        FILE* f = std::fopen(path, "wb");
-        if (!f) {
-            cudaFreeHost(host);
-            fail(TK_ERR_BAD_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
-        }
-        const size_t wrote = std::fwrite(host, 1, 20 + body, f);
-        const int closed = std::fclose(f);
-        cudaFreeHost(host);
-        if (wrote != 20 + body || closed != 0) fail(TK_ERR_BAD_ARG, std::string("checkpoint: write failed for ") + path);
-        main_done(c);
-    });
-}
-
-tk_status tk_checkpoint_load(tk_ctx* c, const char* path) {
-    return guarded([&] {
-        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
-        FILE* f = std::fopen(path, "rb");
-        if (!f) fail(TK_ERR_BAD_ARG, std::string("checkpoint: cannot open ") + path);
-        char hdr[20];
-        const size_t got = std::fread(hdr, 1, 20, f);
-        if (got < 4 || std::memcmp(hdr, kSplfMagic, 4) != 0) {
-            std::fclose(f);
-            fail(TK_ERR_BAD_ARG, std::string("checkpoint: bad magic in ") + path);
-        }
-        uint32_t ver = 0, dim = 0;
-        uint64_t cnt = 0;
-        if (got >= 8) std::memcpy(&ver, hdr + 4, 4);
-        if (got >= 8 && ver != kSplfVersion) {
-            std::fclose(f);
-            fail(TK_ERR_BAD_ARG, "checkpoint: unsupported version " + std::to_string(ver) + " in " + path);
-        }
-        if (got < 20) {
-            std::fclose(f);
-            fail(TK_ERR_BAD_ARG, std::string("checkpoint: truncated file ") + path);
-        }
-        std::memcpy(&dim, hdr + 8, 4);
-        std::memcpy(&cnt, hdr + 12, 8);
-        if (cnt > static_cast<uint64_t>(INT32_MAX - 1)) {
-            std::fclose(f);
-            fail(TK_ERR_BAD_ARG, std::string("checkpoint: count too large in ") + path);
-        }
-        const int64_t n = static_cast<int64_t>(cnt);
-        const int64_t W = 14 + static_cast<int64_t>(dim);
-        const size_t body = static_cast<size_t>(n) * W * sizeof(float);
-        char* host = nullptr;
-        if (cudaHostAlloc(reinterpret_cast<void**>(&host), std::max<size_t>(body, 1), cudaHostAllocDefault) != cudaSuccess) {
-            std::fclose(f);
-            fail(TK_ERR_OOM, "checkpoint: pinned staging allocation failed");
-        }
-        const size_t rb = std::fread(host, 1, body, f);
-        std::fclose(f);
-        if (rb != body) {
-            cudaFreeHost(host);
-            fail(TK_ERR_BAD_ARG, std::string("checkpoint: truncated file ") + path);
-        }
-        CK(cudaSetDevice(c->device));
-        on_main(c);
-        DevBuf rec;
-        float* drec = ensure<float>(rec, n * W);
-        copy_in(drec, host, body, TK_HOST, c);
-        ensure<double>(c->mean, n * 3);
-        ensure<double>(c->log_scale, n * 3);
-        ensure<double>(c->rotation, n * 4);
-        ensure<double>(c->opacity_logit, n);
-        ensure<double>(c->color, n * 3);
-        ensure<float>(c->feature, n * std::max<int64_t>(dim, 1));
-        c->n = n;
-        c->d = static_cast<int32_t>(dim);
-        tk::launch_splf_unpack(drec, splf_view(c), c->cur);
-        c->launches += n > 0;
-        CK_LAUNCH(c);
-        sync(c);
-        rec.release();
-        cudaFreeHost(host);
-        c->generation = 0;  // a loaded SceneMap starts at generation 0 (scene_map.hpp)
-        c->has_scene = true;
-        c->has_features = true;
-        c->opt_ready = false;
-        c->stat_n = -1;
-        scene_changed(c);
-        main_done(c);
-    });
-}
-
-tk_status tk_segment_by_query(tk_ctx* c, const float* feature, int64_t n_pixels, int32_t d_feature,
-                              int32_t feature_mem, const double* embeddings, int32_t classes, uint8_t* labels,
-                              int32_t labels_mem) {
-    return guarded([&] {
-        if (!c || !embeddings || !labels) fail(TK_ERR_BAD_ARG, "null argument");
-        if (classes <= 0 || classes > 255) fail(TK_ERR_BAD_ARG, "segment_by_query: classes must be in [1, 255]");
-        CK(cudaSetDevice(c->device));
-        on_side(c, true);
-        cudaStream_t st = c->cur;
-        // the context's own F under D-sharding is a channel slice: score it and all-reduce
-        const bool sharded = !feature && c->comm && c->nranks > 1;
-        const int d = feature ? d_feature : c->d, d_total = sharded ? c->d_total : d;
-        if (d <= 0) fail(TK_ERR_BAD_ARG, "segment_by_query: embedding dimension mismatch");
-        const int64_t P = feature ? n_pixels : c->fout_pixels;
-        const float* F = feature;
-        DevBuf &bf = c->q_feat, &be = c->q_emb, &bl = c->q_labels, &bb = c->q_best, &bacc = c->q_acc, &bn = c->q_nacc,
-               &bpart = c->q_part;
-        if (!F) {
-            if (!c->f_out.p || c->fout_pixels <= 0) fail(TK_ERR_STATE, "segment_by_query: no rendered feature image");
-            F = ptr<float>(c->f_out);
-        } else if (feature_mem == TK_HOST) {
-            float* df = ensure<float>(bf, P * d);
-            copy_in(df, feature, static_cast<size_t>(P) * d * sizeof(float), TK_HOST, c);
-            F = df;
-        }
-        double* de = ensure<double>(be, static_cast<int64_t>(classes) * d_total);
-        copy_in(de, embeddings, static_cast<size_t>(classes) * d_total * sizeof(double), TK_HOST, c);
-        uint8_t* dl = (labels_mem == TK_DEVICE) ? labels : ensure<uint8_t>(bl, P);
-        tk::QueryParams q{};
-        q.n_pixels = P;
-        q.d = d;
-        q.c0 = sharded ? c->rank * d : 0;
-        q.d_total = d_total;
-        q.classes = classes;
-        q.feat = F;
-        q.emb = de;
-        q.labels = dl;
-        q.best = ensure<double>(bb, P);
-        if (tk::segment_query_chunk(d, classes) < d) {
-            q.acc = ensure<double>(bacc, P * classes);
-            q.nacc = ensure<double>(bn, P);
-        }
-        if (sharded) {  // per-rank partial dots over its channel slice, all-reduced (sum) with NCCL
-            double* part = ensure<double>(bpart, P * (classes + 1));
-            q.partial = part;
-            q.norm2 = part + P * classes;
-            tk::launch_segment_query(q, st);
-            NK(g_nccl.AllReduce(part, part, static_cast<size_t>(P) * (classes + 1), ncclFloat64, ncclSum, c->comm, st));
-            tk::launch_query_argmax(part, part + P * classes, P, classes, dl, st);
-            c->launches += 2;
-        } else {
-            tk::launch_segment_query(q, st);
-            c->launches += 1;
-        }
-        CK_LAUNCH(c);
-        if (labels_mem == TK_HOST) {
-            copy_out(labels, dl, P, TK_HOST, c);
-            sync(c);
-        }
-        side_done(c, true);
     });
 }
 

@@ -1,0 +1,199 @@
+// tk_abi_io.cu — the C ABI of the map formats and queries: SPLF checkpoints and
+// segment_by_query.
+#include "tk_abi_internal.cuh"
+
+// ------------------------------------------------------------------ checkpoint / query
+namespace {
+constexpr char kSplfMagic[4] = {'S', 'P', 'L', 'F'};
+constexpr uint32_t kSplfVersion = 1;
+
+tk::SplfView splf_view(tk_ctx* c) {
+    tk::SplfView v{};
+    v.n = c->n;
+    v.d = c->d;
+    v.mean = ptr<double>(c->mean);
+    v.log_scale = ptr<double>(c->log_scale);
+    v.rotation = ptr<double>(c->rotation);
+    v.opacity_logit = ptr<double>(c->opacity_logit);
+    v.color = ptr<double>(c->color);
+    v.feature = ptr<float>(c->feature);
+    return v;
+}
+}  // namespace
+
+extern "C" {
+
+tk_status tk_checkpoint_save(tk_ctx* c, const char* path) {
+    return guarded([&] {
+        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
+        if (c->d > 0 && !c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        const int64_t n = c->n;
+        const int64_t W = 14 + c->d;
+        DevBuf rec;
+        float* drec = ensure<float>(rec, n * W);
+        tk::launch_splf_pack(splf_view(c), drec, c->cur);
+        c->launches += n > 0;
+        CK_LAUNCH(c);
+        const size_t body = static_cast<size_t>(n) * W * sizeof(float);
+        char* host = nullptr;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&host), 20 + body, cudaHostAllocDefault));
+        std::memcpy(host, kSplfMagic, 4);                                        // checkpoint.cpp:42-45
+        const uint32_t ver = kSplfVersion, dim = static_cast<uint32_t>(c->d);
+        const uint64_t cnt = static_cast<uint64_t>(n);
+        std::memcpy(host + 4, &ver, 4);
+        std::memcpy(host + 8, &dim, 4);
+        std::memcpy(host + 12, &cnt, 8);
+        copy_out(host + 20, drec, body, TK_HOST, c);
+        sync(c);
+        rec.release();
+        FILE* f = std::fopen(path, "wb");
+        if (!f) {
+            cudaFreeHost(host);
+            fail(TK_ERR_BAD_ARG, std::string("checkpoint: cannot open ") + path + " for writing");
+        }
+        const size_t wrote = std::fwrite(host, 1, 20 + body, f);
+        const int closed = std::fclose(f);
+        cudaFreeHost(host);
+        if (wrote != 20 + body || closed != 0) fail(TK_ERR_BAD_ARG, std::string("checkpoint: write failed for ") + path);
+        main_done(c);
+    });
+}
+
+tk_status tk_checkpoint_load(tk_ctx* c, const char* path) {
+    return guarded([&] {
+        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
+        FILE* f = std::fopen(path, "rb");
+        if (!f) fail(TK_ERR_BAD_ARG, std::string("checkpoint: cannot open ") + path);
+        char hdr[20];
+        const size_t got = std::fread(hdr, 1, 20, f);
+        if (got < 4 || std::memcmp(hdr, kSplfMagic, 4) != 0) {
+            std::fclose(f);
+            fail(TK_ERR_BAD_ARG, std::string("checkpoint: bad magic in ") + path);
+        }
+        uint32_t ver = 0, dim = 0;
+        uint64_t cnt = 0;
+        if (got >= 8) std::memcpy(&ver, hdr + 4, 4);
+        if (got >= 8 && ver != kSplfVersion) {
+            std::fclose(f);
+            fail(TK_ERR_BAD_ARG, "checkpoint: unsupported version " + std::to_string(ver) + " in " + path);
+        }
+        if (got < 20) {
+            std::fclose(f);
+            fail(TK_ERR_BAD_ARG, std::string("checkpoint: truncated file ") + path);
+        }
+        std::memcpy(&dim, hdr + 8, 4);
+        std::memcpy(&cnt, hdr + 12, 8);
+        if (cnt > static_cast<uint64_t>(INT32_MAX - 1)) {
+            std::fclose(f);
+            fail(TK_ERR_BAD_ARG, std::string("checkpoint: count too large in ") + path);
+        }
+        const int64_t n = static_cast<int64_t>(cnt);
+        const int64_t W = 14 + static_cast<int64_t>(dim);
+        const size_t body = static_cast<size_t>(n) * W * sizeof(float);
+        char* host = nullptr;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&host), std::max<size_t>(body, 1), cudaHostAllocDefault) != cudaSuccess) {
+            std::fclose(f);
+            fail(TK_ERR_OOM, "checkpoint: pinned staging allocation failed");
+        }
+        const size_t rb = std::fread(host, 1, body, f);
+        std::fclose(f);
+        if (rb != body) {
+            cudaFreeHost(host);
+            fail(TK_ERR_BAD_ARG, std::string("checkpoint: truncated file ") + path);
+        }
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        DevBuf rec;
+        float* drec = ensure<float>(rec, n * W);
+        copy_in(drec, host, body, TK_HOST, c);
+        ensure<double>(c->mean, n * 3);
+        ensure<double>(c->log_scale, n * 3);
+        ensure<double>(c->rotation, n * 4);
+        ensure<double>(c->opacity_logit, n);
+        ensure<double>(c->color, n * 3);
+        ensure<float>(c->feature, n * std::max<int64_t>(dim, 1));
+        c->n = n;
+        c->d = static_cast<int32_t>(dim);
+        tk::launch_splf_unpack(drec, splf_view(c), c->cur);
+        c->launches += n > 0;
+        CK_LAUNCH(c);
+        sync(c);
+        rec.release();
+        cudaFreeHost(host);
+        c->generation = 0;  // a loaded SceneMap starts at generation 0 (scene_map.hpp)
+        c->has_scene = true;
+        c->has_features = true;
+        c->opt_ready = false;
+        c->stat_n = -1;
+        scene_changed(c);
+        main_done(c);
+    });
+}
+
+tk_status tk_segment_by_query(tk_ctx* c, const float* feature, int64_t n_pixels, int32_t d_feature,
+                              int32_t feature_mem, const double* embeddings, int32_t classes, uint8_t* labels,
+                              int32_t labels_mem) {
+    return guarded([&] {
+        if (!c || !embeddings || !labels) fail(TK_ERR_BAD_ARG, "null argument");
+        if (classes <= 0 || classes > 255) fail(TK_ERR_BAD_ARG, "segment_by_query: classes must be in [1, 255]");
+        CK(cudaSetDevice(c->device));
+        on_side(c, true);
+        cudaStream_t st = c->cur;
+        // the context's own F under D-sharding is a channel slice: score it and all-reduce
+        const bool sharded = !feature && c->comm && c->nranks > 1;
+        const int d = feature ? d_feature : c->d, d_total = sharded ? c->d_total : d;
+        if (d <= 0) fail(TK_ERR_BAD_ARG, "segment_by_query: embedding dimension mismatch");
+        const int64_t P = feature ? n_pixels : c->fout_pixels;
+        const float* F = feature;
+        DevBuf &bf = c->q_feat, &be = c->q_emb, &bl = c->q_labels, &bb = c->q_best, &bacc = c->q_acc, &bn = c->q_nacc,
+               &bpart = c->q_part;
+        if (!F) {
+            if (!c->f_out.p || c->fout_pixels <= 0) fail(TK_ERR_STATE, "segment_by_query: no rendered feature image");
+            F = ptr<float>(c->f_out);
+        } else if (feature_mem == TK_HOST) {
+            float* df = ensure<float>(bf, P * d);
+            copy_in(df, feature, static_cast<size_t>(P) * d * sizeof(float), TK_HOST, c);
+            F = df;
+        }
+        double* de = ensure<double>(be, static_cast<int64_t>(classes) * d_total);
+        copy_in(de, embeddings, static_cast<size_t>(classes) * d_total * sizeof(double), TK_HOST, c);
+        uint8_t* dl = (labels_mem == TK_DEVICE) ? labels : ensure<uint8_t>(bl, P);
+        tk::QueryParams q{};
+        q.n_pixels = P;
+        q.d = d;
+        q.c0 = sharded ? c->rank * d : 0;
+        q.d_total = d_total;
+        q.classes = classes;
+        q.feat = F;
+        q.emb = de;
+        q.labels = dl;
+        q.best = ensure<double>(bb, P);
+        if (tk::segment_query_chunk(d, classes) < d) {
+            q.acc = ensure<double>(bacc, P * classes);
+            q.nacc = ensure<double>(bn, P);
+        }
+        if (sharded) {  // per-rank partial dots over its channel slice, all-reduced (sum) with NCCL
+            double* part = ensure<double>(bpart, P * (classes + 1));
+            q.partial = part;
+            q.norm2 = part + P * classes;
+            tk::launch_segment_query(q, st);
+            NK(g_nccl.AllReduce(part, part, static_cast<size_t>(P) * (classes + 1), ncclFloat64, ncclSum, c->comm, st));
+            tk::launch_query_argmax(part, part + P * classes, P, classes, dl, st);
+            c->launches += 2;
+        } else {
+            tk::launch_segment_query(q, st);
+            c->launches += 1;
+        }
+        CK_LAUNCH(c);
+        if (labels_mem == TK_HOST) {
+            copy_out(labels, dl, P, TK_HOST, c);
+            sync(c);
+        }
+        side_done(c, true);
+    });
+}
+
+}  // extern "C"
