@@ -10,7 +10,8 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
-RENDER_LIB = os.path.join(LIB_DIR, "libtkrender.so")
+# TK_RENDER_LIB: load an alternative build of the same library (A/B kernel experiments)
+RENDER_LIB = os.environ.get("TK_RENDER_LIB") or os.path.join(LIB_DIR, "libtkrender.so")
 SYNTH_LIB = os.path.join(LIB_DIR, "libtk_synth.so")
 
 TK_HOST, TK_DEVICE, TK_HOST_ASYNC = 0, 1, 2

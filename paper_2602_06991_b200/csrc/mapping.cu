@@ -288,9 +288,26 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
         int c[2], id[2];
         float wn[2];
         bool in[2];
+        float4 gt[2][4];
+        // keyframe rows first: they do not depend on the records, so their loads overlap the
+        // record loads and the Top-K row gather (a pixel without records wastes its first pass)
+        auto load_gt = [&](int base, bool first) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float4* grow = reinterpret_cast<const float4*>(p.gt + px[u] * D);
+                const bool want = first ? in[u] : c[u] > 0;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    gt[u][m] = (want && q < d4) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        };
+#pragma unroll
+        for (int u = 0; u < 2; ++u) px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &in[u]);
+        load_gt(0, true);
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            px[u] = tiled_pixel(v0 + u, p.width, p.height, tiles_x, &in[u]);
             // the record slots load alongside count / mask (one memory round trip, not two)
             int idl = 0;
             double wdl = 0.0;
@@ -310,17 +327,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
         }
         const int cmax = max(c[0], c[1]);
         for (int base = 0; base < d4; base += 128) {
-            // keyframe rows first: their loads overlap the Top-K row gather below
-            float4 gt[2][4];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const float4* grow = reinterpret_cast<const float4*>(p.gt + px[u] * D);
-#pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    const int q = base + m * 32 + lane;
-                    gt[u][m] = (c[u] > 0 && q < d4) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
+            if (base > 0) load_gt(base, false);
             float4 acc[2][4];
 #pragma unroll
             for (int u = 0; u < 2; ++u)
@@ -482,6 +489,9 @@ __device__ __forceinline__ float warp_sum(float s) {
     return s;
 }
 
+#ifndef SIGN_GROUP
+#define SIGN_GROUP 2
+#endif
 // Sum over records [r0, r1) of w_j * sign(F - F_gt)[px_j] for the channel pass at `base`
 // (4 float4 per lane), records in slot order.
 __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int r1, int base, int lane, float scale,
@@ -497,24 +507,37 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
             spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
             sw = p.wnorm[s];
         }
-        for (int j = 0; j < nr; ++j) {
-            const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
-            const float wj = __shfl_sync(0xffffffffu, sw, j);
-            const uint32_t* srow = signs + pxj * wpp;
-            if (!isfinite(wj)) {  // backward.cpp:296-302: all-zero gradient rows are skipped
-                bool any = false;
-                for (int q = lane; q < wpp; q += 32) any |= srow[q] != 0u;
-                if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
+        // kGroup records' sign words are loaded before any is summed (the loads overlap); the
+        // sums still run record by record, so the result is that of the sequential sweep
+        constexpr int kGroup = SIGN_GROUP;
+        for (int j = 0; j < nr; j += kGroup) {
+            const uint32_t* srow[kGroup];
+            float wj[kGroup];
+            uint32_t bw[kGroup][4];
+#pragma unroll
+            for (int t = 0; t < kGroup; ++t) {
+                srow[t] = signs + __shfl_sync(0xffffffffu, spx, j + t) * wpp;
+                wj[t] = __shfl_sync(0xffffffffu, sw, j + t);
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int q = base + m * 32 + lane;
+                    bw[t][m] = (j + t < nr && q < d4) ? __ldg(srow[t] + (q >> 2)) >> (8 * (q & 3)) : 0u;
+                }
             }
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int q = base + m * 32 + lane;
-                if (q < d4) {
-                    const uint32_t b = __ldg(srow + (q >> 2)) >> (8 * (q & 3));
-                    acc[m].x += signed_w(b, 0, wj);
-                    acc[m].y += signed_w(b, 2, wj);
-                    acc[m].z += signed_w(b, 4, wj);
-                    acc[m].w += signed_w(b, 6, wj);
+            for (int t = 0; t < kGroup; ++t) {
+                if (j + t >= nr) break;
+                if (!isfinite(wj[t])) {  // backward.cpp:296-302: all-zero gradient rows are skipped
+                    bool any = false;
+                    for (int q = lane; q < wpp; q += 32) any |= srow[t][q] != 0u;
+                    if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
+                }
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    acc[m].x += signed_w(bw[t][m], 0, wj[t]);
+                    acc[m].y += signed_w(bw[t][m], 2, wj[t]);
+                    acc[m].z += signed_w(bw[t][m], 4, wj[t]);
+                    acc[m].w += signed_w(bw[t][m], 6, wj[t]);
                 }
             }
         }
@@ -540,15 +563,14 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
             lg = plan.longs[wi];
             g = lg.x;
         }
-        const int r0 = p.seg[g], r1 = p.seg[g + 1];
-        if (!LONG && r1 - r0 > kLongSeg) continue;
         float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
         float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
         float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
         float ss = 0.0f;
         float4 fk[4], mk[4], vk[4];
-        for (int base = 0; base < d4; base += 128) {
-            // the row's parameter / moment loads go out first and overlap the record sweep
+        // the row's parameter / moment loads go out first: they overlap the segment bounds and
+        // the record sweep (a skipped long row only wastes its first pass of loads)
+        auto load_pass = [&](int base) {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int q = base + m * 32 + lane;
@@ -558,6 +580,12 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                     vk[m] = __ldcs(vrow + q);
                 }
             }
+        };
+        load_pass(0);
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        if (!LONG && r1 - r0 > kLongSeg) continue;
+        for (int base = 0; base < d4; base += 128) {
+            if (base > 0) load_pass(base);
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
