@@ -1,0 +1,131 @@
+#!/usr/bin/env python
+"""Device timeline of mapping iterations (or frames) from CUPTI through torch.profiler.
+
+  python scripts/timeline.py [--mode map|frame] [--iters 6] [--out gpurun_out/timeline.txt]
+
+Prints, for the last iteration, every kernel / memcpy / memset on the device in start order with
+its duration and the idle gap before it, then totals (busy, idle, largest gaps).  The numbers
+are wall-clock on the device (no replay), so gaps from host synchronisation are visible.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import CONFIGS  # noqa: E402
+from paper_2602_06991_b200 import _native as N, synth  # noqa: E402
+from paper_2602_06991_b200.api import to_camera, to_pose, to_settings  # noqa: E402
+from paper_2602_06991_b200.types import Pose, RenderSettings  # noqa: E402
+
+
+def setup(cfg):
+    lib, slib = N.render_lib(), N.synth_lib()
+    n, W, H, D, K = cfg["n"], cfg["w"], cfg["h"], cfg["d"], cfg["k"]
+    scene, cam, pose, _ = synth.bench_scene(n, W, H, D)
+    feat = synth.unit_features(scene.size(), D, 7)
+    h = C.c_void_p()
+    N.check(lib.tk_create(0, C.byref(h)))
+    geo = [np.ascontiguousarray(a, np.float64) for a in (scene.mean, scene.log_scale, scene.rotation,
+                                                          scene.opacity_logit, scene.color)]
+    view = N.tk_scene_view(scene.size(), D, *(a.ctypes.data for a in geo), feat.ctypes.data, scene.generation)
+    N.check(lib.tk_scene_upload(h, C.byref(view), N.TK_HOST))
+    return lib, slib, h, scene, cam, pose, (W, H, D, K), (geo, feat)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mode", default="map", choices=["map", "frame"])
+    ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--out", default="gpurun_out/timeline.txt")
+    args = ap.parse_args()
+    lib, slib, ctx, scene, cam, pose, (W, H, D, K), keep = setup(CONFIGS[args.config])
+    P = W * H
+    ccam, cset = to_camera(cam), to_settings(RenderSettings(top_k=K))
+    if args.mode == "map":
+        col = np.empty(P * 3, np.float32)
+        dep = np.empty(P, np.float32)
+        gtf = np.empty(P * D, np.float32)
+        slib.tk_synth_hash_fill_f32(col.size, 21, 0.0, 1.0, col.ctypes.data)
+        slib.tk_synth_hash_fill_f32(dep.size, 22, 0.5, 4.0, dep.ctypes.data)
+        slib.tk_synth_hash_fill_f32(gtf.size, 23, -1.0, 1.0, gtf.ctypes.data)
+        frame = N.tk_frame_view(W, H, D, col.ctypes.data, dep.ctypes.data, gtf.ctypes.data, N.TK_HOST)
+        mc = N.tk_mapper_config()
+        lib.tk_default_mapper_config(C.byref(mc))
+        N.check(lib.tk_optimizer_reset(ctx, 1))
+        N.check(lib.tk_keyframe_set(ctx, 0, C.byref(to_pose(pose)), C.byref(frame)))
+
+        def step(it):
+            vals = (C.c_double * 3)()
+            N.check(lib.tk_optimize_step(ctx, C.byref(mc), C.byref(ccam), C.byref(cset), 0, it, vals, None))
+    else:
+        cp = to_pose(pose)
+        gF = torch.rand(P * D, device="cuda", dtype=torch.float32)
+        gC = torch.rand(P * 3, device="cuda", dtype=torch.float64)
+        gD = torch.rand(P, device="cuda", dtype=torch.float64)
+        fo = torch.empty(P * D, device="cuda", dtype=torch.float32)
+        dfo = torch.empty(scene.size() * D, device="cuda", dtype=torch.float32)
+
+        def step(it):
+            N.check(lib.tk_invalidate(ctx))
+            gout = N.tk_geom_out(N.TK_DEVICE, None, None, None, None, None, None, None, 0, 0)
+            N.check(lib.tk_render_geometric(ctx, C.byref(cp), C.byref(ccam), C.byref(cset), C.byref(gout)))
+            N.check(lib.tk_render_feature(ctx, None, C.c_void_p(fo.data_ptr()), N.TK_DEVICE))
+            N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), N.TK_DEVICE,
+                                            C.c_void_p(dfo.data_ptr()), N.TK_DEVICE))
+            gg = N.tk_geom_grads(N.TK_DEVICE, None, None, None, None, None)
+            N.check(lib.tk_backward_geometric(ctx, C.byref(cp), C.byref(ccam), C.byref(cset),
+                                              C.c_void_p(gC.data_ptr()), C.c_void_p(gD.data_ptr()), N.TK_DEVICE,
+                                              C.byref(gg)))
+            N.check(lib.tk_synchronize(ctx))
+
+    for it in range(1, args.iters):
+        step(it)
+    torch.cuda.synchronize()
+    marks = []
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        for it in range(args.iters, args.iters + 5):
+            marks.append(len(marks))
+            step(it)
+        torch.cuda.synchronize()
+    tmp = "/tmp/tk_trace.json"
+    prof.export_chrome_trace(tmp)
+    ev = [e for e in json.load(open(tmp))["traceEvents"]
+          if e.get("ph") == "X" and e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+    ev.sort(key=lambda e: e["ts"])
+    # split into iterations at the project kernel (start of every prepare)
+    starts = [i for i, e in enumerate(ev) if "k_project" in e["name"]]
+    lo, hi = (starts[-2], starts[-1]) if len(starts) >= 2 else (0, len(ev))
+    if args.mode == "map" and len(starts) >= 5:
+        lo, hi = starts[-1], len(ev)  # last iteration: a feature step when iters+4 is a multiple of 5
+    seg = ev[lo:hi]
+    lines = []
+    t0 = seg[0]["ts"]
+    prev_end = t0
+    busy = 0.0
+    gaps = []
+    for e in seg:
+        gap = e["ts"] - prev_end
+        gaps.append((gap, e["name"][:60]))
+        lines.append(f"{e['ts'] - t0:9.1f} {e['dur']:8.1f} gap {gap:7.1f}  s{e['args'].get('stream')} {e['name'][:90]}")
+        busy += e["dur"]
+        prev_end = max(prev_end, e["ts"] + e["dur"])
+    span = prev_end - t0
+    gaps.sort(reverse=True)
+    lines.append(f"span {span:.1f} us, busy (sum of durations) {busy:.1f} us, {len(seg)} device ops")
+    lines.append("largest gaps: " + "; ".join(f"{g:.1f} before {n}" for g, n in gaps[:8]))
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    open(args.out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines[-2:]))
+    lib.tk_destroy(ctx)
+
+
+if __name__ == "__main__":
+    main()
