@@ -42,10 +42,22 @@ def feat_close(a, b, tol=FEAT_TOL):
     np.testing.assert_array_less(np.abs(np.asarray(a, np.float64) - b), tol * np.maximum(1.0, np.abs(b)) + 1e-30)
 
 
+def aniso_scene():
+    """Needle- and sheet-like Gaussians at random orientations: their cutoff ellipses fill little
+    of their bounding boxes, so the exact ellipse-vs-block cull decides many block corners."""
+    m = synth.random_scene(400, 8, 23)
+    ls = m.log_scale.copy()
+    ls[:, 0] += 1.5
+    ls[:, 1] -= 2.5
+    m.log_scale = ls
+    return m
+
+
 SCENES = [
     ("random300_seed1", lambda: synth.random_scene(300, 8, 1), lambda: synth.test_camera(64, 48), Pose()),
     ("random250_seed17", lambda: synth.random_scene(250, 8, 17), lambda: synth.test_camera(64, 64),
      Pose(axis_angle(0.2, (0, 1, 0)), (0.05, -0.02, 0.1))),
+    ("aniso400_seed23", aniso_scene, lambda: synth.test_camera(96, 80), Pose(axis_angle(0.3, (1, 0, 0)), (0, 0, 0))),
     ("random2000_seed5", lambda: synth.random_scene(2000, 16, 5), lambda: synth.test_camera(160, 120), Pose()),
 ]
 
