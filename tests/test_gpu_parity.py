@@ -132,7 +132,7 @@ def test_single_and_two_gaussian_kats(R):  # test_raster.cpp:60-100 (log_scale -
     assert o.depth[16, 16] == pytest.approx(1.24, rel=1e-9)
 
 
-@pytest.mark.parametrize("d", [3, 4, 16, 512])
+@pytest.mark.parametrize("d", [3, 4, 16, 512, 1000, 1030])
 @pytest.mark.parametrize("k", [1, 3, 16])
 def test_render_feature_matches_oracle(R, d, k):
     m, c = synth.random_scene(600, d, 21), synth.test_camera(64, 48)
@@ -183,7 +183,7 @@ def test_stale_device_records_after_map_shrinks(R):
     assert b"stale snapshot" in R.lib.tk_last_error()
 
 
-@pytest.mark.parametrize("d", [4, 64, 512])
+@pytest.mark.parametrize("d", [4, 64, 512, 1000, 1030])
 @pytest.mark.parametrize("k", [1, 3, 8])
 def test_backward_feature_matches_oracle(R, d, k):
     m, c = synth.random_scene(500, d, 33), synth.test_camera(48, 40)
