@@ -710,7 +710,8 @@ def main():
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20,
+                    help="e2e steps (capped at --steps): enough to amortise the copy pipeline fill and drain")
     ap.add_argument("--no-mapping", action="store_true", help="skip the mapping-iteration measurement")
     ap.add_argument("--mode", default="keyframe", choices=["keyframe", "dshard"],
                     help="multi-GPU decomposition (N > 1)")

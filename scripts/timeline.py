@@ -39,9 +39,55 @@ def setup(cfg):
     return lib, slib, h, scene, cam, pose, (W, H, D, K), (geo, feat)
 
 
+def e2e_step(lib, ctx, scene, keep, pose, ccam, cset, P, D, K):
+    """bench.py's e2e step: pinned host scene and upstream grads in, host outputs back (TK_HOST_ASYNC)."""
+    geo, feat = keep
+    n = scene.size()
+    hold = []
+
+    def pinned(n_el, dt):
+        t = torch.empty(n_el, dtype=dt, pin_memory=True)
+        hold.append(t)
+        return t
+
+    g_pin = [pinned(a.size, torch.float64) for a in geo]
+    for t, a in zip(g_pin, geo):
+        t.numpy()[...] = a.ravel()
+    f_pin = pinned(feat.size, torch.float32)
+    f_pin.numpy()[...] = feat.ravel()
+    gF, gC, gD = pinned(P * D, torch.float32), pinned(P * 3, torch.float64), pinned(P, torch.float64)
+    for t in (gF, gC, gD):
+        t.uniform_()
+    o = {nm: pinned(sz, dt) for nm, sz, dt in [
+        ("color", P * 3, torch.float64), ("depth", P, torch.float64), ("alpha", P, torch.float64),
+        ("index", P * K, torch.int32), ("weight", P * K, torch.float64), ("count", P, torch.uint8),
+        ("contrib", n, torch.float64), ("F", P * D, torch.float32), ("df", n * D, torch.float32),
+        ("gmean", n * 3, torch.float64), ("gls", n * 3, torch.float64), ("grot", n * 4, torch.float64),
+        ("gop", n, torch.float64), ("gcol", n * 3, torch.float64)]}
+    view = N.tk_scene_view(n, D, *(t.data_ptr() for t in g_pin), f_pin.data_ptr(), 0)
+    A = N.TK_HOST_ASYNC
+    gout = N.tk_geom_out(A, *(o[x].data_ptr() for x in ("color", "depth", "alpha", "index", "weight", "count",
+                                                         "contrib")), 0, 0)
+    gg = N.tk_geom_grads(A, *(o[x].data_ptr() for x in ("gmean", "gls", "grot", "gop", "gcol")))
+    cp = to_pose(pose)
+
+    def step(it):
+        _ = hold
+        N.check(lib.tk_invalidate(ctx))
+        N.check(lib.tk_scene_upload(ctx, C.byref(view), A))
+        N.check(lib.tk_render_geometric(ctx, C.byref(cp), C.byref(ccam), C.byref(cset), C.byref(gout)))
+        N.check(lib.tk_render_feature(ctx, None, C.c_void_p(o["F"].data_ptr()), A))
+        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), A, C.c_void_p(o["df"].data_ptr()), A))
+        N.check(lib.tk_backward_geometric(ctx, C.byref(cp), C.byref(ccam), C.byref(cset), C.c_void_p(gC.data_ptr()),
+                                          C.c_void_p(gD.data_ptr()), A, C.byref(gg)))
+        if it % 5 == 4:
+            N.check(lib.tk_synchronize(ctx))
+    return step
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="map", choices=["map", "frame"])
+    ap.add_argument("--mode", default="map", choices=["map", "frame", "e2e"])
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--config", default="c3")
     ap.add_argument("--out", default="gpurun_out/timeline.txt")
@@ -65,6 +111,8 @@ def main():
         def step(it):
             vals = (C.c_double * 3)()
             N.check(lib.tk_optimize_step(ctx, C.byref(mc), C.byref(ccam), C.byref(cset), 0, it, vals, None))
+    elif args.mode == "e2e":
+        step = e2e_step(lib, ctx, scene, keep, pose, ccam, cset, P, D, K)
     else:
         cp = to_pose(pose)
         gF = torch.rand(P * D, device="cuda", dtype=torch.float32)
@@ -105,6 +153,8 @@ def main():
     lo, hi = (starts[-2], starts[-1]) if len(starts) >= 2 else (0, len(ev))
     if args.mode == "map" and len(starts) >= 5:
         lo, hi = starts[-1], len(ev)  # last iteration: a feature step when iters+4 is a multiple of 5
+    if args.mode == "e2e":
+        lo, hi = 0, len(ev)
     seg = ev[lo:hi]
     lines = []
     t0 = seg[0]["ts"]
@@ -118,12 +168,17 @@ def main():
         busy += e["dur"]
         prev_end = max(prev_end, e["ts"] + e["dur"])
     span = prev_end - t0
+    streams = {}
+    for e in seg:
+        streams.setdefault((e["args"].get("stream"), e["cat"]), []).append(e["dur"])
+    for (sid, cat), d in sorted(streams.items(), key=lambda x: str(x[0])):
+        lines.append(f"stream {sid} {cat}: {len(d)} ops, busy {sum(d):.1f} us of {span:.1f}")
     gaps.sort(reverse=True)
     lines.append(f"span {span:.1f} us, busy (sum of durations) {busy:.1f} us, {len(seg)} device ops")
     lines.append("largest gaps: " + "; ".join(f"{g:.1f} before {n}" for g, n in gaps[:8]))
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     open(args.out, "w").write("\n".join(lines) + "\n")
-    print("\n".join(lines[-2:]))
+    print("\n".join(ln for ln in lines if ln.startswith(("span", "stream", "largest"))))
     lib.tk_destroy(ctx)
 
 
