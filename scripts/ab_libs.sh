@@ -25,6 +25,8 @@ for r in rows[1:]:
     by.setdefault(r[h.index("Kernel Name")].split("(")[0][-40:], []).append(float(r[h.index("Metric Value")]))
 j = json.loads(open(f"gpurun_out/ab_{v}.json").read().strip().splitlines()[-1])
 ker = ", ".join(f"{k} {statistics.median(t) / 1e3:.1f}us x{len(t)}" for k, t in sorted(by.items()))
-print(f"{v}: value {j['value']:.2f} e2e {j['e2e']['value']:.3f} | {ker}")
+e2e = (j.get("e2e") or {}).get("value", float("nan"))
+map_v = (j.get("mapping") or {}).get("value", float("nan"))
+print(f"{v}: value {j['value']:.2f} e2e {e2e:.3f} mapping {map_v:.2f} | {ker}")
 PY
 done
