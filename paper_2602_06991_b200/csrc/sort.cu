@@ -152,6 +152,15 @@ __global__ void __launch_bounds__(1024) k_scan_single(const int32_t* __restrict_
     if (threadIdx.x == 0) *total = tot;
 }
 
+// TK_RADIX_LEGACY=1: per-pass histogram + scan + scatter instead of onesweep (A/B, tests).
+bool legacy_radix() {
+    static const bool on = [] {
+        const char* e = std::getenv("TK_RADIX_LEGACY");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ROUNDS = 8;
@@ -184,25 +193,45 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ ke
 // ranking needs no block barrier; one block scan over (digit, warp) counts then gives every
 // key's position in the digit-sorted tile, which is staged in shared memory and written out with
 // consecutive threads on consecutive addresses of each digit's global run.
-template <typename K>
+//
+// ONESWEEP = true: the pass needs no per-block histogram.  Blocks take tiles in ticket order,
+// publish their per-digit counts in a status word per (tile, digit) and look back over the
+// predecessors' words (decoupled look-back, one thread per digit) for the digit's offset; the
+// digit's global start comes from the all-pass histogram of k_rs_ghist.
+constexpr uint32_t kOsAgg = 1u << 30, kOsPrefix = 2u << 30, kOsMask = kOsAgg - 1;
+
+struct OnesweepArgs {
+    const int32_t* gcount;  // [256] digit totals of this pass
+    uint32_t* status;       // [nb][256] (flag | value), zeroed
+    int* ticket;            // zeroed
+};
+
+template <typename K, bool ONESWEEP>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            int64_t n, int shift, const int32_t* __restrict__ offs,
-                                                           int nb) {
+                                                           int nb, OnesweepArgs os) {
     __shared__ int32_t gbase[RS_RADIX];
     __shared__ int32_t lstart[RS_RADIX];
     __shared__ int32_t wc[RS_WARPS][RS_RADIX];  // per-warp digit counts, then per-(warp, digit) offsets
     __shared__ K skey[RS_TILE];
     __shared__ uint32_t sval[RS_TILE];
     __shared__ int32_t wsum[RS_WARPS];
+    __shared__ int32_t gsum[RS_WARPS];
+    __shared__ int bid_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t tile0 = static_cast<int64_t>(blockIdx.x) * RS_TILE;
-    const int tile_n = static_cast<int>(n - tile0 < RS_TILE ? n - tile0 : RS_TILE);
-    gbase[tid] = offs[static_cast<int64_t>(tid) * nb + blockIdx.x];
+    if (ONESWEEP) {
+        if (tid == 0) bid_s = atomicAdd(os.ticket, 1);
+    } else {
+        gbase[tid] = offs[static_cast<int64_t>(tid) * nb + blockIdx.x];
+    }
 #pragma unroll
     for (int w = 0; w < RS_WARPS; ++w) wc[w][tid] = 0;
     __syncthreads();
+    const int bid = ONESWEEP ? bid_s : static_cast<int>(blockIdx.x);
+    const int64_t tile0 = static_cast<int64_t>(bid) * RS_TILE;
+    const int tile_n = static_cast<int>(n - tile0 < RS_TILE ? n - tile0 : RS_TILE);
     constexpr int kSlice = RS_TILE / RS_WARPS;  // 256 keys per warp
     K key[RS_ROUNDS];
     uint32_t val[RS_ROUNDS];
@@ -249,6 +278,47 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
             wc[w][tid] = acc;
             acc += c;
         }
+        if (ONESWEEP) {
+            // publish this tile's count of digit tid, then look back for the earlier tiles' total
+            volatile uint32_t* st = os.status;
+            const int64_t me = static_cast<int64_t>(bid) * RS_RADIX + tid;
+            uint32_t excl = 0;
+            if (bid == 0) {
+                st[me] = kOsPrefix | static_cast<uint32_t>(tot);
+            } else {
+                st[me] = kOsAgg | static_cast<uint32_t>(tot);
+                // eight predecessors' words per round go out together; consumed in order up to
+                // the nearest one holding a prefix (block 0 always does)
+                constexpr int kLB = 8;
+                bool done = false;
+                for (int64_t q = me - RS_RADIX; !done; q -= kLB * RS_RADIX) {
+                    uint32_t w[kLB];
+#pragma unroll
+                    for (int j = 0; j < kLB; ++j) w[j] = q - j * RS_RADIX >= 0 ? st[q - j * RS_RADIX] : uint32_t{kOsPrefix};
+#pragma unroll
+                    for (int j = 0; j < kLB; ++j) {
+                        if (done) break;
+                        while ((w[j] & ~kOsMask) == 0) w[j] = st[q - j * RS_RADIX];
+                        excl += w[j] & kOsMask;
+                        done = (w[j] & kOsPrefix) != 0;
+                    }
+                }
+                st[me] = kOsPrefix | (excl + static_cast<uint32_t>(tot));
+            }
+            // the digit's global start: exclusive scan of the pass histogram over digits
+            const int32_t gc = os.gcount[tid];
+            int ginc = gc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, ginc, o);
+                if (lane >= o) ginc += u;
+            }
+            if (lane == 31) gsum[warp] = ginc;
+            __syncthreads();
+            int goff = 0;
+            for (int w = 0; w < warp; ++w) goff += gsum[w];
+            gbase[tid] = goff + ginc - gc + static_cast<int32_t>(excl);
+        }
     }
     __syncthreads();
 #pragma unroll
@@ -270,6 +340,29 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
     }
 }
 
+// Digit totals of every pass at once (the histograms are order independent): counts[p][d].
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_ghist(const K* __restrict__ keys, int64_t n, int begin_bit,
+                                                         int npass, int32_t* __restrict__ counts) {
+    __shared__ int32_t cnt[8][RS_RADIX];
+    for (int p = 0; p < 8; ++p) cnt[p][threadIdx.x] = 0;
+    __syncthreads();
+    const unsigned lane = threadIdx.x & 31;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * RS_THREADS + threadIdx.x; i - threadIdx.x < n;
+         i += static_cast<int64_t>(gridDim.x) * RS_THREADS) {
+        const bool in = i < n;
+        const K k = in ? keys[i] : K(0);
+        for (int p = 0; p < npass; ++p) {
+            const unsigned d = in ? static_cast<unsigned>(k >> (begin_bit + 8 * p)) & 0xffu : RS_RADIX;
+            const unsigned peers = __match_any_sync(0xffffffffu, d);
+            if (d < RS_RADIX && lane == static_cast<unsigned>(__ffs(peers) - 1)) atomicAdd(&cnt[p][d], __popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; ++p)
+        if (cnt[p][threadIdx.x]) atomicAdd(&counts[p * RS_RADIX + threadIdx.x], cnt[p][threadIdx.x]);
+}
+
 template <typename K>
 void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int begin_bit,
                      int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt, int64_t* launches) {
@@ -288,11 +381,40 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
     K* kout = keys_alt;
     uint32_t* vout = vals_alt;
     bool in_alt = false;
+    const int npass = (end_bit - begin_bit + 7) / 8;
+    if (n < (1LL << 30) && npass <= 8 && !legacy_radix()) {
+        // onesweep: one all-pass histogram, then one look-back scatter per pass
+        char* op = static_cast<char*>(scratch);
+        int32_t* gcount = reinterpret_cast<int32_t*>(op);
+        int* tickets = reinterpret_cast<int*>(op + 8 * RS_RADIX * sizeof(int32_t));
+        uint32_t* status = reinterpret_cast<uint32_t*>(op + align_bytes(8 * RS_RADIX * sizeof(int32_t) + 8 * sizeof(int)));
+        const size_t status_words = static_cast<size_t>(nb) * RS_RADIX;
+        cudaMemsetAsync(scratch, 0,
+                        align_bytes(8 * RS_RADIX * sizeof(int32_t) + 8 * sizeof(int)) +
+                            npass * status_words * sizeof(uint32_t),
+                        st);
+        const int hblocks = static_cast<int>(std::min<int64_t>(nb, 148 * 4));
+        k_rs_ghist<K><<<hblocks, RS_THREADS, 0, st>>>(kin, n, begin_bit, npass, gcount);
+        dbg_launch("k_rs_ghist", st);
+        *launches += 1;
+        for (int p = 0; p < npass; ++p) {
+            const OnesweepArgs os{gcount + p * RS_RADIX, status + p * status_words, tickets + p};
+            k_rs_scatter<K, true><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, begin_bit + 8 * p, nullptr, nb,
+                                                             os);
+            dbg_launch("k_rs_onesweep", st);
+            *launches += 1;
+            std::swap(kin, kout);
+            std::swap(vin, vout);
+            in_alt = !in_alt;
+        }
+        *result_in_alt = in_alt;
+        return;
+    }
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         k_rs_hist<K><<<nb, RS_THREADS, 0, st>>>(kin, n, shift, hist, nb);
         dbg_launch("k_rs_hist", st);
         scan_exclusive(hist, hist, hn, total, scan_scratch, st, launches);
-        k_rs_scatter<K><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb);
+        k_rs_scatter<K, false><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb, OnesweepArgs{});
         dbg_launch("k_rs_scatter", st);
         *launches += 2;
         std::swap(kin, kout);
@@ -426,7 +548,9 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
 size_t radix_scratch_bytes(int64_t n) {
     const int64_t nb = (n + RS_TILE - 1) / RS_TILE + 1;
     const int64_t hn = static_cast<int64_t>(RS_RADIX) * nb;
-    return align_bytes(hn * sizeof(int32_t)) + 256 + scan_scratch_bytes(hn);
+    const size_t legacy = align_bytes(hn * sizeof(int32_t)) + 256 + scan_scratch_bytes(hn);
+    const size_t onesweep = align_bytes(8 * RS_RADIX * sizeof(int32_t) + 8 * sizeof(int)) + 8 * hn * sizeof(uint32_t);
+    return std::max(legacy, onesweep);
 }
 
 void radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,

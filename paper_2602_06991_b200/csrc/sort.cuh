@@ -22,7 +22,9 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
 
 // Stable LSD radix sort of (key, value) pairs over key bits [begin_bit, end_bit), 8 bits per
 // pass.  Results end in keys_out/vals_out (buffers are ping-ponged internally; the *_alt
-// buffers are scratch of the same size).
+// buffers are scratch of the same size).  Onesweep: one all-pass digit histogram, then one
+// scatter per pass whose blocks find their digit offsets by decoupled look-back (n < 2^30;
+// TK_RADIX_LEGACY=1 or larger n: per-pass histogram + scan + scatter).
 size_t radix_scratch_bytes(int64_t n);
 void radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt,
                           int64_t n, int begin_bit, int end_bit, void* scratch, cudaStream_t st,
