@@ -631,6 +631,21 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
            "target": ">= 15 mapping iterations/s end to end (BASELINE.json north_star)",
            "parallelism": ("D-sharded: D/G channels per rank, mask / loss / geometry-gradient / row-norm "
                            "all-reduces over NCCL" if sharded else "one map per rank (replicas)")}
+    # the feature step on every iteration too (feature_update_period 5 and 1)
+    period = cfg.feature_update_period
+    cfg.feature_update_period = 1
+    step()
+    steps1 = max(2, min(steps, 10))
+    ev0.record(stream)
+    for _ in range(steps1):
+        step()
+    ev1.record(stream)
+    N.check(lib.tk_synchronize(ctx))
+    ms1 = ms_max(ev0.elapsed_time(ev1))
+    cfg.feature_update_period = period
+    out["feature_every_iteration"] = {"value": world * steps1 / (ms1 / 1000.0), "unit": "iterations/s",
+                                      "ms_per_iteration": ms1 / steps1, "iterations": steps1,
+                                      "feature_update_period": 1}
     if e2e_steps <= 0:
         return out
     e2e_steps = max(2, e2e_steps)

@@ -185,14 +185,16 @@ __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 __syncthreads();
+                // windows outside the valid range are staged as zeros: their term is
+                // tw * (0 + 0 * (a - 0) + 0 * (b - 0)) = +0, which leaves every sum bit-identical
+                // (a sum starting at +0 is never -0), so the gather below needs no bounds tests
                 for (int e = threadIdx.x; e < kCWY * kCWX; e += kThreads) {
                     const int ey = e / kCWX, ex = e - ey * kCWX;
                     const int wy = y0 - kHalo + ey, wx = x0 - kHalo + ex;
-                    if (wy >= 0 && wy < oh && wx >= 0 && wx < ow) {
-                        const double* src = p.win + c * plane_w + static_cast<int64_t>(wy) * ow + wx;
+                    const bool ok = wy >= 0 && wy < oh && wx >= 0 && wx < ow;
+                    const double* src = p.win + c * plane_w + static_cast<int64_t>(ok ? wy : 0) * ow + (ok ? wx : 0);
 #pragma unroll
-                        for (int m = 0; m < 5; ++m) sw[(m * kCWY + ey) * kCWX + ex] = src[m * 3 * plane_w];
-                    }
+                    for (int m = 0; m < 5; ++m) sw[(m * kCWY + ey) * kCWX + ex] = ok ? src[m * 3 * plane_w] : 0.0;
                 }
                 __syncthreads();
                 if (x >= p.w) continue;
@@ -204,13 +206,11 @@ __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
                     av[j] = p.color[q];
                     bv[j] = static_cast<double>(p.gt_color[q]);
                 }
-                const int wy_lo = max(0, ys - kHalo), wy_hi = min(oh - 1, ys + kCR - 1);
-                for (int wy = wy_lo; wy <= wy_hi; ++wy) {
+                for (int wy = ys - kHalo; wy <= ys + kCR - 1; ++wy) {
                     const int ey = wy - (y0 - kHalo);
+#pragma unroll
                     for (int kx = kHalo; kx >= 0; --kx) {  // wx = x - kx ascending
-                        const int wx = x - kx;
-                        if (wx < 0 || wx >= ow) continue;
-                        const int ex = wx - (x0 - kHalo);
+                        const int ex = lx + kHalo - kx;
                         const double* wp = sw + ey * kCWX + ex;
                         const double mu_a = wp[0], mu_b = wp[kCWY * kCWX], d_mu = wp[2 * kCWY * kCWX];
                         const double dv2 = wp[3 * kCWY * kCWX], d_cov = wp[4 * kCWY * kCWX];
