@@ -4,7 +4,10 @@
 #include "feature.cuh"
 
 #include <algorithm>
+#include <cstdlib>
+
 #include "sort.cuh"
+#include "tk_common.cuh"
 
 namespace tk {
 
@@ -98,6 +101,156 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
                 }
             }
         }
+    }
+}
+
+// render_feature (render.cpp:319-334) with a tile's distinct feature rows staged in shared
+// memory.  One CTA per 16 x 16 pixel tile (persistent over tiles): thread t loads pixel t's
+// records and normalised weights; the tile's distinct Gaussian ids are deduplicated in a shared
+// hash table and up to `rows` of them are bulk-copied (TMA, one cp.async.bulk per row) into
+// shared memory; then warp w writes pixels 32w..32w+31 (lane = channel quad), reading each
+// record's row from shared memory (ids beyond the staged set read global memory).  Neighbouring
+// pixels share many of their K rows, so part of the P*K row reads through L2 become one read per
+// distinct (tile, Gaussian); the sums keep the slot order, so F is bit-identical to
+// k_gather_tiled's.
+constexpr int kGSide = 16, kGPix = kGSide * kGSide;
+
+template <int KMAX>
+__global__ void __launch_bounds__(kGPix) k_gather_staged(GatherParams p, int rows) {
+    constexpr int kHash = 2 * kGPix * KMAX;  // power of two, load factor <= 1/2
+    extern __shared__ __align__(128) unsigned char gsm[];
+    const int D = p.d, d4 = D >> 2;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm);                                // bulk-copy barrier
+    int* ucount = reinterpret_cast<int*>(gsm + 8);                                   // distinct ids
+    float* srow = reinterpret_cast<float*>(gsm + 128);                               // [rows][D]
+    int* hkey = reinterpret_cast<int*>(gsm + 128 + static_cast<size_t>(rows) * D * 4);  // [kHash]
+    int* hslot = hkey + kHash;                                                       // [kHash]
+    int* row_id = hslot + kHash;                                                     // [rows]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tiles_x = (p.width + kGSide - 1) / kGSide, tiles_y = (p.height + kGSide - 1) / kGSide;
+    if (tid == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    unsigned phase = 0;
+    for (int tile = blockIdx.x; tile < tiles_x * tiles_y; tile += gridDim.x) {
+        for (int h = tid; h < kHash; h += kGPix) {
+            hkey[h] = -1;
+            hslot[h] = 0;  // reference count until the ids are numbered
+        }
+        if (tid == 0) ucount[0] = 0;
+        __syncthreads();
+        // this thread's pixel: records, normalised weights (slot order), hash insertion
+        const int tx0 = (tile % tiles_x) * kGSide, ty0 = (tile / tiles_x) * kGSide;
+        const int x = tx0 + (tid % kGSide), y = ty0 + tid / kGSide;
+        const bool in = x < p.width && y < p.height;
+        const int64_t px = static_cast<int64_t>(y) * p.width + x;
+        const int c = in ? p.count[px] : -1;
+        int gid[KMAX], hpos[KMAX];
+        float wn[KMAX];
+        double wd[KMAX];
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            gid[j] = 0;
+            wd[j] = 0.0;
+            if (j < c) {
+                gid[j] = p.index[px * p.k + j];
+                wd[j] = p.weight[px * p.k + j];
+                sum += wd[j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            wn[j] = j < c ? static_cast<float>(wd[j] / sum) : 0.0f;
+            hpos[j] = 0;
+            if (j < c) {
+                unsigned h = (static_cast<unsigned>(gid[j]) * 2654435761u) & (kHash - 1);
+                while (true) {
+                    const int old = atomicCAS(&hkey[h], -1, gid[j]);
+                    if (old == -1 || old == gid[j]) break;
+                    h = (h + 1) & (kHash - 1);
+                }
+                atomicAdd(&hslot[h], 1);
+                hpos[j] = static_cast<int>(h);
+            }
+        }
+        __syncthreads();
+        // number the ids read by two or more records (a row read once gains nothing from staging)
+        for (int h = tid; h < kHash; h += kGPix) {
+            const int g = hkey[h];
+            if (g >= 0) {
+                const int sl = hslot[h] >= 2 ? atomicAdd(ucount, 1) : rows;
+                hslot[h] = sl < rows ? sl : rows;
+                if (sl < rows) row_id[sl] = g;
+            }
+        }
+        __syncthreads();
+        const int staged = min(ucount[0], rows);
+        if (staged > 0) {
+            if (tid == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(staged) * D * 4);
+            for (int r = tid; r < staged; r += kGPix)
+                bulk_g2s(srow + static_cast<size_t>(r) * D, p.feat + static_cast<int64_t>(row_id[r]) * D, D * 4, bar);
+        }
+        int slot[KMAX];  // staged row, or -1 - gid (read from global)
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+            const int sl = j < c ? hslot[hpos[j]] : 0;
+            slot[j] = sl < rows ? sl : -1 - gid[j];
+        }
+        if (staged > 0) {
+            mbar_wait(bar, phase);
+            phase ^= 1u;
+        }
+        // warp w: the tile's pixels 32w .. 32w + 31, two at a time
+        for (int i = 0; i < 32; i += 2) {
+            int ci[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) ci[u] = __shfl_sync(0xffffffffu, c, i + u);
+            for (int base = 0; base < d4; base += 128) {
+                float4 acc[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) acc[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int sj = __shfl_sync(0xffffffffu, slot[j], i + u);
+                        const float wj = __shfl_sync(0xffffffffu, wn[j], i + u);
+                        if (j < ci[u] && sj >= 0) {  // staged row (shared memory)
+                            const float4* row = reinterpret_cast<const float4*>(srow + static_cast<size_t>(sj) * D);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int q = base + m * 32 + lane;
+                                if (q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
+                            }
+                        } else if (j < ci[u]) {  // beyond the staged set: global (L2)
+                            const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(-1 - sj) * D);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int q = base + m * 32 + lane;
+                                if (q < d4) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (ci[u] < 0) continue;
+                    const int t = warp * 32 + i + u;
+                    const int64_t pxo = static_cast<int64_t>(ty0 + t / kGSide) * p.width + tx0 + (t % kGSide);
+                    float4* orow = reinterpret_cast<float4*>(p.out + pxo * D);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        if (q < d4) __stcs(orow + q, acc[u][m]);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // the staged rows and the hash are reused by the next tile
     }
 }
 
@@ -553,9 +706,54 @@ inline bool vec_ok(const void* a, const void* b, int d) {
 
 }  // namespace
 
+// Shared memory of k_gather_staged: staged rows + hash (keys, slots) + row ids + counters/barrier
+// (TK_GATHER_SMEM_KB overrides, experiments).
+size_t staged_smem() {
+    static const size_t b = [] {
+        const char* e = std::getenv("TK_GATHER_SMEM_KB");
+        const int kb = e ? std::atoi(e) : 0;
+        return static_cast<size_t>(kb >= 24 && kb <= 224 ? kb : 112) * 1024;
+    }();
+    return b;
+}
+
+template <int KMAX>
+bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
+    constexpr size_t kHash = 2 * kGPix * KMAX;
+    const size_t fixed = kHash * 8 + 128;
+    const size_t budget = staged_smem();
+    const int rows = static_cast<int>(std::min<size_t>(kGPix * KMAX, (budget - fixed) / (static_cast<size_t>(p.d) * 4 + 4)));
+    if (rows < 8) return false;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_gather_staged<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(budget));
+        configured = true;
+    }
+    const size_t smem = 128 + static_cast<size_t>(rows) * p.d * 4 + kHash * 8 + static_cast<size_t>(rows) * 4;
+    const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
+    const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
+    k_gather_staged<KMAX><<<std::min(tiles, 148 * per_sm), kGPix, smem, st>>>(p, rows);
+    return true;
+}
+
+bool gather_staged_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TK_GATHER_STAGED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
-    if (vec_ok(p.feat, p.out, p.d) && p.width > 0 && static_cast<int64_t>(p.width) * p.height == p.n_pixels)
+    const bool img = p.width > 0 && static_cast<int64_t>(p.width) * p.height == p.n_pixels;
+    if (vec_ok(p.feat, p.out, p.d) && img && gather_staged_enabled() && p.k <= 8 &&
+        (p.k <= 4 ? launch_gather_staged<4>(p, st) : launch_gather_staged<8>(p, st))) {
+        dbg_launch("k_gather_staged", st);
+        return;
+    }
+    if (vec_ok(p.feat, p.out, p.d) && img)
         k_gather_tiled<<<warp_grid((p.n_pixels + 1) / 2), kThreads, 0, st>>>(p);
     else if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
     else k_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);

@@ -16,6 +16,8 @@ for envs in "$@"; do
   python - "$i" "$envs" <<'PY'
 import json, sys
 j = json.loads(open(f"gpurun_out/abe_{sys.argv[1]}.json").read().strip().splitlines()[-1])
-print(f"[{sys.argv[2]}] value {j['value']:.2f} {j['unit']} ms/step {j['ms_per_step']:.3f} e2e {j['e2e']['value']:.3f}")
+e2e = (j.get('e2e') or {}).get('value', float('nan'))
+mp = (j.get('mapping') or {}).get('value', float('nan'))
+print(f"[{sys.argv[2]}] value {j['value']:.2f} {j['unit']} ms/step {j['ms_per_step']:.3f} e2e {e2e:.3f} mapping {mp:.2f}")
 PY
 done
