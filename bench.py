@@ -286,6 +286,11 @@ def main_gpu(args, cfg):
             N.check(lib.tk_comm_unique_id(uid))
         uid = (C.c_uint8 * 128)(*tkdist.broadcast_bytes(dist, bytes(uid) if rank == 0 else None, 128))
         N.check(lib.tk_comm_init(ctx, uid, world, rank, D))
+        gather_mode = args.gather
+        if gather_mode == "p2p" and lib.tk_comm_p2p_setup(ctx, P) != N.TK_OK:  # needs CUDA IPC + P2P
+            gather_mode = "nccl (p2p setup failed: " + lib.tk_last_error().decode() + ")"
+    else:
+        gather_mode = None
 
     dev = torch.device("cuda", local)
     gF_host = np.empty(P * Ds, np.float32)
@@ -303,9 +308,12 @@ def main_gpu(args, cfg):
     def step():
         N.check(lib.tk_invalidate(ctx))
         N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
-        N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))
-        if dshard:
-            N.check(lib.tk_allgather_feature(ctx, C.c_void_p(Ffull.data_ptr()), N.TK_DEVICE))
+        if gather_mode == "p2p":  # fused: slices stored straight into every rank's full map
+            N.check(lib.tk_render_feature_gathered(ctx, None, None, N.TK_DEVICE))
+        else:
+            N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))
+            if dshard:
+                N.check(lib.tk_allgather_feature(ctx, C.c_void_p(Ffull.data_ptr()), N.TK_DEVICE))
         N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), N.TK_DEVICE, None, N.TK_DEVICE))
         N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
                                           C.c_void_p(gC.data_ptr()), C.c_void_p(gD.data_ptr()), N.TK_DEVICE,
@@ -443,7 +451,10 @@ def main_gpu(args, cfg):
             "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
             "config": {"workload": cfg["label"], "gaussians": n, "width": W, "height": H, "feature_dim": D,
-                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": (f"feature-dim shard d{world} + NCCL all-gather" if dshard else
+                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": (f"feature-dim shard d{world} + " + ("render_feature fused with the all-gather over "
+                                                                                "NVLink peer stores" if gather_mode == "p2p"
+                                                                                else f"NCCL all-gather [{gather_mode}]")
+                                       if dshard else
                                        f"keyframe-parallel x{world}: rank r renders orbit keyframe r, all D"),
                        "l2": "inputs larger than L2 (features %.2f GB, F %.2f GB)" % (n * D * 4 / 1e9,
                                                                                         P * D * 4 / 1e9),
@@ -730,6 +741,8 @@ def main():
     ap.add_argument("--no-mapping", action="store_true", help="skip the mapping-iteration measurement")
     ap.add_argument("--mode", default="keyframe", choices=["keyframe", "dshard"],
                     help="multi-GPU decomposition (N > 1)")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="dshard: fused render + all-gather over peer memory, or render + NCCL all-gather")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])

@@ -193,6 +193,24 @@ tk_status tk_comm_init(tk_ctx* ctx, const uint8_t id[128], int32_t nranks, int32
  * H*W*d_total HWC map (channel-interleaved), on every rank. */
 tk_status tk_allgather_feature(tk_ctx* ctx, float* out, int32_t out_mem);
 tk_status tk_allreduce_sum_f64(tk_ctx* ctx, double* values, int32_t count); /* host values */
+/* Fused render_feature + all-gather over peer memory (NVLink P2P stores, no NCCL data path):
+ * each rank gathers its d_shard channels and stores every output row slice straight into every
+ * rank's full [H*W][d_total] buffer at channel offset rank * d_shard, then (under tk_comm) a
+ * stream-ordered NCCL all-reduce of one word acts as the rank barrier, after which the calling
+ * rank's buffer holds the full HWC map -- the tk_allgather_feature result without the gather
+ * buffer or the interleave pass.  Peer buffers come from tk_comm_p2p_setup (collective: each rank
+ * allocates n_pixels * d_total floats and the CUDA IPC handles are exchanged over NCCL; call again,
+ * on every rank, for a larger frame) or, for ranks driven from one process, from
+ * tk_comm_set_peers (every rank's device buffer in rank order; the caller orders the ranks'
+ * streams: there is no barrier).  d_shard % 4 == 0, nranks <= 8.  out: NULL or a copy of the
+ * calling rank's full map (TK_HOST / TK_DEVICE / TK_HOST_ASYNC); tk_comm_gathered_buffer returns
+ * the buffer itself. */
+tk_status tk_comm_p2p_setup(tk_ctx* ctx, int64_t n_pixels);
+tk_status tk_comm_set_peers(tk_ctx* ctx, int32_t rank, int32_t nranks, int32_t d_total,
+                            float* const* buffers, int64_t n_pixels);
+tk_status tk_render_feature_gathered(tk_ctx* ctx, const tk_topk_view* topk, float* out,
+                                     int32_t out_mem);
+tk_status tk_comm_gathered_buffer(tk_ctx* ctx, float** buffer);
 
 /* ---- one mapping iteration on the device (map/mapper.cpp:162-255) ---- */
 typedef struct { /* MapperConfig knobs of one iteration; same layout as the oracle's orc_mapper_config */

@@ -150,6 +150,22 @@ class Renderer:
         N.check(self.lib.tk_render_feature(self.ctx, C.byref(view), _p(out), N.TK_HOST))
         return out
 
+    def comm_set_peers(self, rank: int, nranks: int, d_total: int, buffers: list[int], n_pixels: int) -> None:
+        """Register every rank's full-width output buffer (device pointers, rank order) for the
+        fused render + all-gather of ranks driven from one process (tk_comm_set_peers)."""
+        arr = (C.c_void_p * len(buffers))(*buffers)
+        N.check(self.lib.tk_comm_set_peers(self.ctx, rank, nranks, d_total, arr, n_pixels))
+
+    def render_feature_gathered(self, m: SceneMap, topk: TopKGrid | None = None) -> None:
+        """render_feature of this rank's channel slice stored into every rank's full-width buffer
+        (tk_render_feature_gathered; topk None = this context's own records)."""
+        self._sync_scene(m)
+        if topk is None:
+            N.check(self.lib.tk_render_feature_gathered(self.ctx, None, None, N.TK_HOST))
+            return
+        view, keep = self._topk_view(topk)
+        N.check(self.lib.tk_render_feature_gathered(self.ctx, C.byref(view), None, N.TK_HOST))
+
     def render_feature_full_blend(self, m: SceneMap, pose: Pose, cam: CameraIntrinsics,
                                   s: RenderSettings) -> np.ndarray:
         """render_feature_full_blend (render.cpp:339-343)."""

@@ -26,6 +26,17 @@ __device__ __forceinline__ float4 fma4(float a, float4 x, float4 acc) {
 
 __device__ __forceinline__ float4 ldg4(const float4* p) { return __ldg(p); }
 
+// Store float4 q of pixel px's output row: to p.out, or (fused all-gather) into every rank's
+// full-width buffer at this rank's channel offset -- local HBM or a peer's over NVLink.
+__device__ __forceinline__ void store_out4(const GatherParams& p, int64_t px, int q, float4 v) {
+    if (p.n_peers == 0) {
+        __stcs(reinterpret_cast<float4*>(p.out + px * p.d) + q, v);
+        return;
+    }
+    for (int r = 0; r < p.n_peers; ++r)
+        __stcs(reinterpret_cast<float4*>(p.peers[r] + px * p.peer_stride + p.peer_off) + q, v);
+}
+
 // Pixel of virtual index v when the image is walked in 16x16 tiles (neighbouring pixels share
 // most of their Top-K Gaussians, so tile order keeps those feature rows L2-resident).
 __device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height, int tiles_x, bool* valid) {
@@ -93,15 +104,15 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
                 if (c[u] < 0) continue;
-                float4* orow = reinterpret_cast<float4*>(p.out + px[u] * D);
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int q = base + m * 32 + lane;
-                    if (q < d4) __stcs(orow + q, acc[u][m]);
+                    if (q < d4) store_out4(p, px[u], q, acc[u][m]);
                 }
             }
         }
     }
+    if (p.n_peers > 0) __threadfence_system();  // peer stores complete before the rank barrier
 }
 
 // render_feature (render.cpp:319-334) with a tile's distinct feature rows staged in shared
@@ -241,17 +252,17 @@ __global__ void __launch_bounds__(kGPix) k_gather_staged(GatherParams p, int row
                     if (ci[u] < 0) continue;
                     const int t = warp * 32 + i + u;
                     const int64_t pxo = static_cast<int64_t>(ty0 + t / kGSide) * p.width + tx0 + (t % kGSide);
-                    float4* orow = reinterpret_cast<float4*>(p.out + pxo * D);
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
-                        if (q < d4) __stcs(orow + q, acc[u][m]);
+                        if (q < d4) store_out4(p, pxo, q, acc[u][m]);
                     }
                 }
             }
         }
         __syncthreads();  // the staged rows and the hash are reused by the next tile
     }
+    if (p.n_peers > 0) __threadfence_system();  // peer stores complete before the rank barrier
 }
 
 // render_feature (render.cpp:319-334): F[p] = sum_j (w_j / sum_w) f[idx_j], sum in slot order.

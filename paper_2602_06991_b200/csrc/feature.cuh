@@ -4,6 +4,8 @@
 
 namespace tk {
 
+constexpr int kMaxPeers = 8;
+
 struct GatherParams {
     int64_t n_pixels;
     int k;                 // record slots per pixel
@@ -14,6 +16,12 @@ struct GatherParams {
     int d;
     float* out;            // P x D
     int width, height;     // image shape (0: plain pixel order)
+    // Fused gather + all-gather over peer memory: n_peers > 0 stores every output row slice into
+    // peers[r] + px * peer_stride + peer_off for every rank r (its own HBM and, over NVLink, the
+    // other ranks'); out is then unused.  D % 4 == 0 and peer_off % 4 == 0.
+    int n_peers = 0;
+    int peer_stride = 0, peer_off = 0;
+    float* peers[kMaxPeers] = {};
 };
 
 struct ListGatherParams {

@@ -477,6 +477,17 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     cp.dilation = s->cov2d_dilation;
     return cp;
 }
+// Drop the fused all-gather's peer buffers (IPC mappings closed, own buffer freed).
+void release_peers(tk_ctx* c) {
+    if (c->peer_ipc)
+        for (int r = 0; r < c->peer_n; ++r)
+            if (r != c->peer_rank && c->peer_ptrs[r]) cudaIpcCloseMemHandle(c->peer_ptrs[r]);
+    c->peer_own.release();
+    for (float*& q : c->peer_ptrs) q = nullptr;
+    c->peer_n = 0;
+    c->peer_ipc = false;
+}
+
 void scene_changed(tk_ctx* c) {
     c->scene_version += 1;
     c->prepared = false;
@@ -598,6 +609,7 @@ tk_status tk_destroy(tk_ctx* c) {
                          &c->lp_items, &c->lp_longs, &c->lp_counters, &c->lp_partial, &c->row_ss};
     for (DevBuf* b : mapping) b->release();
     if (c->hvals) cudaFreeHost(c->hvals);
+    release_peers(c);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
     if (c->hscal) cudaFreeHost(c->hscal);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1064,6 +1076,114 @@ tk_status tk_allgather_feature(tk_ctx* c, float* out, int32_t out_mem) {
         sync(c);
         tmp.release();
         side_done(c, true);
+    });
+}
+
+tk_status tk_comm_set_peers(tk_ctx* c, int32_t rank, int32_t nranks, int32_t d_total, float* const* buffers,
+                            int64_t n_pixels) {
+    return guarded([&] {
+        if (!c || !buffers) fail(TK_ERR_BAD_ARG, "null argument");
+        if (nranks < 1 || nranks > tk::kMaxPeers || rank < 0 || rank >= nranks)
+            fail(TK_ERR_BAD_ARG, "bad rank / nranks (1 <= nranks <= 8)");
+        if (d_total <= 0 || d_total % nranks || (d_total / nranks) % 4 || n_pixels < 0)
+            fail(TK_ERR_BAD_ARG, "d_total must split into nranks slices of a multiple of 4 channels");
+        for (int r = 0; r < nranks; ++r)
+            if (!buffers[r]) fail(TK_ERR_BAD_ARG, "null peer buffer");
+        CK(cudaSetDevice(c->device));
+        release_peers(c);
+        for (int r = 0; r < nranks; ++r) c->peer_ptrs[r] = buffers[r];
+        c->peer_n = nranks;
+        c->peer_rank = rank;
+        c->peer_dtotal = d_total;
+        c->peer_pixels = n_pixels;
+    });
+}
+
+tk_status tk_comm_p2p_setup(tk_ctx* c, int64_t n_pixels) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (!c->comm) fail(TK_ERR_STATE, "tk_comm_init not called");
+        if (c->nranks > tk::kMaxPeers) fail(TK_ERR_BAD_ARG, "fused all-gather supports up to 8 ranks");
+        if (c->d_total % c->nranks || (c->d_total / c->nranks) % 4)
+            fail(TK_ERR_BAD_ARG, "d_total must split into nranks slices of a multiple of 4 channels");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        sync(c);
+        release_peers(c);
+        float* own = ensure<float>(c->peer_own, static_cast<size_t>(std::max<int64_t>(n_pixels, 1)) * c->d_total);
+        // every rank's IPC handle to every rank (NCCL all-gather of the 64-byte handles)
+        cudaIpcMemHandle_t mine;
+        CK(cudaIpcGetMemHandle(&mine, own));
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        DevBuf hb;
+        uint8_t* dh = ensure<uint8_t>(hb, 64 * (c->nranks + 1));
+        CK(cudaMemcpyAsync(dh + 64 * c->nranks, &mine, 64, cudaMemcpyHostToDevice, c->cur));
+        NK(g_nccl.AllGather(dh + 64 * c->nranks, dh, 64, ncclUint8, c->comm, c->cur));
+        std::vector<cudaIpcMemHandle_t> all(c->nranks);
+        CK(cudaMemcpyAsync(all.data(), dh, 64 * c->nranks, cudaMemcpyDeviceToHost, c->cur));
+        sync(c);
+        hb.release();
+        c->peer_ipc = true;
+        c->peer_n = c->nranks;
+        c->peer_rank = c->rank;
+        c->peer_dtotal = c->d_total;
+        c->peer_pixels = n_pixels;
+        for (int r = 0; r < c->nranks; ++r) {
+            if (r == c->rank) {
+                c->peer_ptrs[r] = own;
+                continue;
+            }
+            void* q = nullptr;
+            CK(cudaIpcOpenMemHandle(&q, all[r], cudaIpcMemLazyEnablePeerAccess));
+            c->peer_ptrs[r] = static_cast<float*>(q);
+        }
+        main_done(c);
+    });
+}
+
+tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float* out, int32_t out_mem) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (c->peer_n == 0) fail(TK_ERR_STATE, "no peer buffers (tk_comm_p2p_setup or tk_comm_set_peers)");
+        CK(cudaSetDevice(c->device));
+        on_side(c, true);
+        require_features(c);
+        if (c->d * c->peer_n != c->peer_dtotal) fail(TK_ERR_BAD_ARG, "d_total must equal nranks * d_shard");
+        const Records r = resolve_records(c, topk, "render_feature");
+        if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
+        const int64_t P = static_cast<int64_t>(r.w) * r.h;
+        if (P > c->peer_pixels) fail(TK_ERR_BAD_ARG, "frame larger than the registered peer buffers");
+        if (reinterpret_cast<uintptr_t>(ptr<float>(c->feature)) % 16) fail(TK_ERR_BAD_ARG, "feature rows misaligned");
+        wait_out(c, kOutF);
+        tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, nullptr, r.w, r.h};
+        gp.n_peers = c->peer_n;
+        gp.peer_stride = c->peer_dtotal;
+        gp.peer_off = c->peer_rank * c->d;
+        for (int q = 0; q < c->peer_n; ++q) gp.peers[q] = c->peer_ptrs[q];
+        {
+            PhaseScope phase(c, TK_PHASE_GATHER);
+            tk::launch_feature_gather(gp, c->cur);
+        }
+        c->launches += P > 0;
+        CK_LAUNCH(c);
+        if (c->comm && c->peer_ipc) {  // stream-ordered rank barrier: every peer's slice has landed
+            int32_t* w = ensure<int32_t>(c->peer_word, 1);
+            NK(g_nccl.AllReduce(w, w, 1, ncclInt32, ncclSum, c->comm, c->cur));
+        }
+        if (out) {
+            const size_t bytes = static_cast<size_t>(P) * c->peer_dtotal * sizeof(float);
+            copy_out(out, c->peer_ptrs[c->peer_rank], bytes, out_mem == TK_DEVICE ? TK_DEVICE : out_mem, c, kOutF);
+            if (out_mem == TK_HOST) sync(c);
+        }
+        side_done(c, true);
+    });
+}
+
+tk_status tk_comm_gathered_buffer(tk_ctx* c, float** buffer) {
+    return guarded([&] {
+        if (!c || !buffer) fail(TK_ERR_BAD_ARG, "null argument");
+        if (c->peer_n == 0) fail(TK_ERR_STATE, "no peer buffers");
+        *buffer = c->peer_ptrs[c->peer_rank];
     });
 }
 

@@ -264,6 +264,12 @@ struct tk_ctx {
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;
     DevBuf gather_buf;
+    // fused render_feature + all-gather over peer memory: every rank's full-width output buffer
+    float* peer_ptrs[tk::kMaxPeers] = {};
+    int peer_n = 0, peer_rank = 0, peer_dtotal = 0;
+    int64_t peer_pixels = 0;
+    bool peer_ipc = false;  // peer_ptrs[r != peer_rank] opened from CUDA IPC handles (tk_comm_p2p_setup)
+    DevBuf peer_own, peer_word;
 };
 
 namespace tkabi {
@@ -350,6 +356,7 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
 tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s,
                              const double* mid);
 void scene_changed(tk_ctx* c);
+void release_peers(tk_ctx* c);
 void require_features(tk_ctx* c);
 
 }  // namespace tkabi
