@@ -735,12 +735,9 @@ bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
     const size_t budget = staged_smem();
     const int rows = static_cast<int>(std::min<size_t>(kGPix * KMAX, (budget - fixed) / (static_cast<size_t>(p.d) * 4 + 4)));
     if (rows < 8) return false;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_gather_staged<KMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(budget));
-        configured = true;
-    }
+    static FuncAttrCache attr;
+    set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget));
     const size_t smem = 128 + static_cast<size_t>(rows) * p.d * 4 + kHash * 8 + static_cast<size_t>(rows) * 4;
     const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
     const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));

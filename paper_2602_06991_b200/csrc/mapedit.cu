@@ -305,11 +305,10 @@ void launch_segment_query(const QueryParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
     const int chunk = segment_query_chunk(p.d, p.classes);
     const size_t smem = static_cast<size_t>(chunk) * p.classes * sizeof(double);
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-        cudaFuncSetAttribute(k_segment_query, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = smem;
-    }
+    static FuncAttrCache attr;
+    if (smem > 48 * 1024)
+        set_func_attr(attr, reinterpret_cast<const void*>(k_segment_query), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                      static_cast<int>(smem), true);
     const int64_t per_sm = std::max<int64_t>(1, (227 * 1024) / static_cast<int64_t>(smem + 1024));
     const int64_t blocks = std::min<int64_t>((p.n_pixels + 16 * kQP - 1) / (16 * kQP), 148 * std::min<int64_t>(per_sm, 4));
     k_segment_query<<<static_cast<unsigned>(blocks), 512, smem, st>>>(p, chunk);

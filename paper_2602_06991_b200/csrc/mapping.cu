@@ -768,11 +768,9 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launc
         dbg_launch("k_ssim_stats", st);
         *launches += 1;
     }
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_color_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kColorSmem));
-        configured = true;
-    }
+    static FuncAttrCache attr;
+    set_func_attr(attr, reinterpret_cast<const void*>(k_color_loss), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                  static_cast<int>(kColorSmem));
     const int64_t tiles = static_cast<int64_t>((p.w + kCX - 1) / kCX) * ((p.h + kCY - 1) / kCY);
     k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, kColorSmem, st>>>(p);
     dbg_launch("k_color_loss", st);
