@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include "sort.cuh"
+#include "tile_stage.cuh"
 #include "tk_common.cuh"
 
 namespace tk {
@@ -115,103 +116,36 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
     if (p.n_peers > 0) __threadfence_system();  // peer stores complete before the rank barrier
 }
 
-// render_feature (render.cpp:319-334) with a tile's distinct feature rows staged in shared
-// memory.  One CTA per 16 x 16 pixel tile (persistent over tiles): thread t loads pixel t's
-// records and normalised weights; the tile's distinct Gaussian ids are deduplicated in a shared
-// hash table and up to `rows` of them are bulk-copied (TMA, one cp.async.bulk per row) into
-// shared memory; then warp w writes pixels 32w..32w+31 (lane = channel quad), reading each
-// record's row from shared memory (ids beyond the staged set read global memory).  Neighbouring
-// pixels share many of their K rows, so part of the P*K row reads through L2 become one read per
-// distinct (tile, Gaussian); the sums keep the slot order, so F is bit-identical to
-// k_gather_tiled's.
-constexpr int kGSide = 16, kGPix = kGSide * kGSide;
+// render_feature (render.cpp:319-334) over tile-staged rows (tile_stage.cuh): one CTA per
+// 16 x 16 pixel tile (persistent over tiles), then warp w writes pixels 32w..32w+31 (lane =
+// channel quad), each record's row read from shared memory or, unstaged, from global memory.
+// F is bit-identical to k_gather_tiled's (same weights, same slot-order FMAs per channel).
+constexpr int kGSide = kStageSide, kGPix = kStagePix;
 
 template <int KMAX>
-__global__ void __launch_bounds__(kGPix) k_gather_staged(GatherParams p, int rows) {
-    constexpr int kHash = 2 * kGPix * KMAX;  // power of two, load factor <= 1/2
+__global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int rows) {
     extern __shared__ __align__(128) unsigned char gsm[];
     const int D = p.d, d4 = D >> 2;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(gsm);                                // bulk-copy barrier
-    int* ucount = reinterpret_cast<int*>(gsm + 8);                                   // distinct ids
-    float* srow = reinterpret_cast<float*>(gsm + 128);                               // [rows][D]
-    int* hkey = reinterpret_cast<int*>(gsm + 128 + static_cast<size_t>(rows) * D * 4);  // [kHash]
-    int* hslot = hkey + kHash;                                                       // [kHash]
-    int* row_id = hslot + kHash;                                                     // [rows]
+    const StageSmem sm = stage_layout<KMAX>(gsm, rows, D);
+    const float* srow = sm.srow;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tiles_x = (p.width + kGSide - 1) / kGSide, tiles_y = (p.height + kGSide - 1) / kGSide;
-    if (tid == 0) {
-        mbar_init(bar, 1);
-        fence_mbar_init();
-    }
+    stage_init(sm);
     unsigned phase = 0;
     for (int tile = blockIdx.x; tile < tiles_x * tiles_y; tile += gridDim.x) {
-        for (int h = tid; h < kHash; h += kGPix) {
-            hkey[h] = -1;
-            hslot[h] = 0;  // reference count until the ids are numbered
-        }
-        if (tid == 0) ucount[0] = 0;
-        __syncthreads();
-        // this thread's pixel: records, normalised weights (slot order), hash insertion
         const int tx0 = (tile % tiles_x) * kGSide, ty0 = (tile / tiles_x) * kGSide;
         const int x = tx0 + (tid % kGSide), y = ty0 + tid / kGSide;
         const bool in = x < p.width && y < p.height;
         const int64_t px = static_cast<int64_t>(y) * p.width + x;
-        const int c = in ? p.count[px] : -1;
-        int gid[KMAX], hpos[KMAX];
+        const StagedPixel<KMAX> sp =
+            stage_tile<KMAX>(sm, rows, D, p.feat, p.index, p.weight, p.k, px, in ? p.count[px] : -1, phase);
+        const int c = sp.c;
+        int slot[KMAX];
         float wn[KMAX];
-        double wd[KMAX];
-        double sum = 0.0;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
-            gid[j] = 0;
-            wd[j] = 0.0;
-            if (j < c) {
-                gid[j] = p.index[px * p.k + j];
-                wd[j] = p.weight[px * p.k + j];
-                sum += wd[j];
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            wn[j] = j < c ? static_cast<float>(wd[j] / sum) : 0.0f;
-            hpos[j] = 0;
-            if (j < c) {
-                unsigned h = (static_cast<unsigned>(gid[j]) * 2654435761u) & (kHash - 1);
-                while (true) {
-                    const int old = atomicCAS(&hkey[h], -1, gid[j]);
-                    if (old == -1 || old == gid[j]) break;
-                    h = (h + 1) & (kHash - 1);
-                }
-                atomicAdd(&hslot[h], 1);
-                hpos[j] = static_cast<int>(h);
-            }
-        }
-        __syncthreads();
-        // number the ids read by two or more records (a row read once gains nothing from staging)
-        for (int h = tid; h < kHash; h += kGPix) {
-            const int g = hkey[h];
-            if (g >= 0) {
-                const int sl = hslot[h] >= 2 ? atomicAdd(ucount, 1) : rows;
-                hslot[h] = sl < rows ? sl : rows;
-                if (sl < rows) row_id[sl] = g;
-            }
-        }
-        __syncthreads();
-        const int staged = min(ucount[0], rows);
-        if (staged > 0) {
-            if (tid == 0) mbar_arrive_expect_tx(bar, static_cast<unsigned>(staged) * D * 4);
-            for (int r = tid; r < staged; r += kGPix)
-                bulk_g2s(srow + static_cast<size_t>(r) * D, p.feat + static_cast<int64_t>(row_id[r]) * D, D * 4, bar);
-        }
-        int slot[KMAX];  // staged row, or -1 - gid (read from global)
-#pragma unroll
-        for (int j = 0; j < KMAX; ++j) {
-            const int sl = j < c ? hslot[hpos[j]] : 0;
-            slot[j] = sl < rows ? sl : -1 - gid[j];
-        }
-        if (staged > 0) {
-            mbar_wait(bar, phase);
-            phase ^= 1u;
+            slot[j] = sp.slot[j];
+            wn[j] = sp.wn[j];
         }
         // warp w: the tile's pixels 32w .. 32w + 31, two at a time
         for (int i = 0; i < 32; i += 2) {
@@ -730,15 +664,13 @@ size_t staged_smem() {
 
 template <int KMAX>
 bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
-    constexpr size_t kHash = 2 * kGPix * KMAX;
-    const size_t fixed = kHash * 8 + 128;
     const size_t budget = staged_smem();
-    const int rows = static_cast<int>(std::min<size_t>(kGPix * KMAX, (budget - fixed) / (static_cast<size_t>(p.d) * 4 + 4)));
+    const int rows = stage_rows<KMAX>(budget, p.d);
     if (rows < 8) return false;
     static FuncAttrCache attr;
     set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX>),
                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget));
-    const size_t smem = 128 + static_cast<size_t>(rows) * p.d * 4 + kHash * 8 + static_cast<size_t>(rows) * 4;
+    const size_t smem = stage_smem_bytes<KMAX>(rows, p.d);
     const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
     const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
     k_gather_staged<KMAX><<<std::min(tiles, 148 * per_sm), kGPix, smem, st>>>(p, rows);

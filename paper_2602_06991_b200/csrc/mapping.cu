@@ -9,6 +9,11 @@
 //     D-channel row, writes 2 sign bits per channel instead of the fp32 dL/dF image;
 //   feature Adam: per Gaussian reads the sign words of its records, then f, m, v (fp32) once.
 #include "mapping.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "tile_stage.cuh"
 #include "feature.cuh"
 #include "sort.cuh"
 
@@ -25,9 +30,9 @@ constexpr int kHalo = kSsimWin - 1;
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
 // Deterministic block sum of NV doubles (fixed shuffle tree, then warps in order).
-template <int NV>
+template <int NV, int NW = kWarps>
 __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restrict__ dst) {
-    __shared__ double sh[NV][kWarps];
+    __shared__ double sh[NV][NW];
 #pragma unroll
     for (int a = 0; a < NV; ++a)
 #pragma unroll
@@ -39,7 +44,7 @@ __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restr
     __syncthreads();
     if (threadIdx.x < NV) {
         double s = 0.0;
-        for (int w = 0; w < kWarps; ++w) s += sh[threadIdx.x][w];
+        for (int w = 0; w < NW; ++w) s += sh[threadIdx.x][w];
         dst[threadIdx.x] = s;
     }
 }
@@ -270,6 +275,108 @@ __device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height,
     const int x = static_cast<int>(t % tiles_x) * 16 + (l & 15), y = static_cast<int>(t / tiles_x) * 16 + (l >> 4);
     *valid = x < width && y < height;
     return static_cast<int64_t>(y) * width + x;
+}
+
+// k_feature_loss_vec over tile-staged rows (tile_stage.cuh): one CTA per 16 x 16 tile; a pixel
+// uses its records only when live (count > 0 and a non-zero keyframe row, losses.cpp:98-104);
+// warp w then computes pixels 32w..32w+31 two at a time, keyframe rows loaded first, the
+// rendered rows from shared memory (or global for unstaged ids), and stores sign(F - GT) as
+// 2-bit codes plus the |F - GT| and live-pixel partial sums.  The rendered row, the signs and
+// the live count are those of k_feature_loss_vec; the |F - GT| sum differs only in fp64
+// summation order.
+template <int KMAX>
+__global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossParams p, int rows) {
+    extern __shared__ __align__(128) unsigned char gsm[];
+    const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
+    const StageSmem sm = stage_layout<KMAX>(gsm, rows, D);
+    const float* srow = sm.srow;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tiles_x = (p.width + kStageSide - 1) / kStageSide, tiles_y = (p.height + kStageSide - 1) / kStageSide;
+    stage_init(sm);
+    unsigned phase = 0;
+    double v[2] = {0.0, 0.0};
+    for (int tile = blockIdx.x; tile < tiles_x * tiles_y; tile += gridDim.x) {
+        const int tx0 = (tile % tiles_x) * kStageSide, ty0 = (tile / tiles_x) * kStageSide;
+        const int x = tx0 + (tid % kStageSide), y = ty0 + tid / kStageSide;
+        const bool in = x < p.width && y < p.height;
+        const int64_t px = static_cast<int64_t>(y) * p.width + x;
+        const int cnt = in ? p.count[px] : 0;
+        const bool live = cnt > 0 && p.gt_valid[px];
+        if (live) v[1] += 1.0;
+        const StagedPixel<KMAX> sp =
+            stage_tile<KMAX>(sm, rows, D, p.feat, p.index, p.weight, p.k, px, in ? (live ? cnt : 0) : -1, phase);
+        for (int i = 0; i < 32; i += 2) {
+            int ci[2];
+            int64_t pxo[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                ci[u] = __shfl_sync(0xffffffffu, sp.c, i + u);
+                const int t = warp * 32 + i + u;
+                pxo[u] = static_cast<int64_t>(ty0 + t / kStageSide) * p.width + tx0 + (t % kStageSide);
+            }
+            for (int base = 0; base < d4; base += 128) {
+                float4 gt[2][4], acc[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const float4* grow = reinterpret_cast<const float4*>(p.gt + pxo[u] * D);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        gt[u][m] = (ci[u] > 0 && q < d4) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        acc[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < KMAX; ++j) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int sj = __shfl_sync(0xffffffffu, sp.slot[j], i + u);
+                        const float wj = __shfl_sync(0xffffffffu, sp.wn[j], i + u);
+                        if (j < ci[u] && sj >= 0) {
+                            const float4* row = reinterpret_cast<const float4*>(srow + static_cast<size_t>(sj) * D);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int q = base + m * 32 + lane;
+                                if (q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
+                            }
+                        } else if (j < ci[u]) {
+                            const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(-1 - sj) * D);
+#pragma unroll
+                            for (int m = 0; m < 4; ++m) {
+                                const int q = base + m * 32 + lane;
+                                if (q < d4) acc[u][m] = fma4(wj, __ldg(row + q), acc[u][m]);
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (ci[u] < 0) continue;
+                    uint32_t* srw = p.signs + pxo[u] * wpp;
+                    float sabs = 0.0f;
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int q = base + m * 32 + lane;
+                        uint32_t byte = 0;
+                        if (ci[u] > 0 && q < d4) {
+                            const float4 t = gt[u][m];
+                            const float dx = acc[u][m].x - t.x, dy = acc[u][m].y - t.y;
+                            const float dz = acc[u][m].z - t.z, dw = acc[u][m].w - t.w;
+                            sabs += (fabsf(dx) + fabsf(dy)) + (fabsf(dz) + fabsf(dw));
+                            byte = sign_bits(dx) | (sign_bits(dy) << 2) | (sign_bits(dz) << 4) | (sign_bits(dw) << 6);
+                        }
+                        uint32_t word = byte << (8 * (lane & 3));
+                        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+                        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+                        if ((lane & 3) == 0 && q < d4) srw[q >> 2] = word;
+                    }
+                    v[0] += static_cast<double>(sabs);
+                }
+            }
+        }
+        __syncthreads();  // the staged rows and the hash are reused by the next tile
+    }
+    block_sum_store<2, kStagePix / 32>(v, p.partial + blockIdx.x * kLossSlots + kFeatAbs);
 }
 
 // render_feature (render.cpp:319-334) fused with the masked feature L1 (losses.cpp:92-118):
@@ -777,11 +884,38 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launc
     *launches += 1;
 }
 
+template <int KMAX>
+bool launch_feature_loss_staged(const FeatLossParams& p, cudaStream_t st) {
+    constexpr size_t kBudget = 112 * 1024;
+    const int rows = stage_rows<KMAX>(kBudget, p.d);
+    if (rows < 8) return false;
+    static FuncAttrCache attr;
+    set_func_attr(attr, reinterpret_cast<const void*>(k_feature_loss_staged<KMAX>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBudget));
+    const int tiles = ((p.width + kStageSide - 1) / kStageSide) * ((p.height + kStageSide - 1) / kStageSide);
+    const int grid = std::min(std::min(tiles, 148 * 2), kLossBlocks);
+    k_feature_loss_staged<KMAX><<<grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st>>>(p, rows);
+    return true;
+}
+
+bool loss_staged_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TK_LOSS_STAGED");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_feature_loss(const FeatLossParams& p, cudaStream_t st) {
     const int64_t P = static_cast<int64_t>(p.width) * p.height;
     if (P <= 0 || p.d <= 0) return;
     const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(p.gt) % 16) == 0;
+    if (vec && loss_staged_enabled() && p.k <= 8 &&
+        (p.k <= 4 ? launch_feature_loss_staged<4>(p, st) : launch_feature_loss_staged<8>(p, st))) {
+        dbg_launch("k_feature_loss_staged", st);
+        return;
+    }
     if (vec) k_feature_loss_vec<<<capped_grid((P + 1) / 2, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
     else k_feature_loss_scalar<<<capped_grid(P, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
     dbg_launch("k_feature_loss", st);
