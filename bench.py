@@ -424,7 +424,7 @@ def main_gpu(args, cfg):
 
     extras = None
     if not dshard and not args.no_mapping:
-        extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev)
+        extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev, cpose, ccam, cset)
 
     mapping = None
     if not args.no_mapping:  # dshard: the D-sharded mapping iteration (NCCL all-reduces inside the step)
@@ -688,10 +688,30 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
     return out
 
 
-def run_extras(lib, N, torch, ctx, W, H, D, n, steps, stream, dev):
-    """The other §8(f) rows on the config-3 map: segment_by_query over the resident F (32 classes,
-    fp64 dots in the reference's order) and the SPLF checkpoint save / load through the device."""
+def run_extras(lib, N, torch, ctx, W, H, D, n, steps, stream, dev, cpose=None, ccam=None, cset=None):
+    """The other rows on the config-3 map: the vanilla full-blend feature render (render.cpp:339-343,
+    the paper's baseline renderer), segment_by_query over the resident F (32 classes, fp64 dots in
+    the reference's order) and the SPLF checkpoint save / load through the device."""
     P = W * H
+    full_blend = None
+    if cpose is not None:
+        Fb = torch.empty(P * D, dtype=torch.float32, device=dev)
+        fb_args = (ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.c_void_p(Fb.data_ptr()), N.TK_DEVICE)
+        N.check(lib.tk_render_feature_full_blend(*fb_args))  # warm-up
+        N.check(lib.tk_synchronize(ctx))
+        fs = max(2, min(steps, 5))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(fs):
+            N.check(lib.tk_render_feature_full_blend(*fb_args))
+        e1.record(stream)
+        N.check(lib.tk_synchronize(ctx))
+        fb_ms = e0.elapsed_time(e1) / fs
+        full_blend = {"ms_per_frame": fb_ms, "frames_per_s": 1000.0 / fb_ms,
+                      "path": "tk_render_feature_full_blend: contributor count pass, scan, contributor-list pass "
+                              "(every w > 0 entry), list gather of all contributors' D-channel rows"}
+        del Fb
     C_CLS = 32
     emb = np.random.default_rng(5).normal(size=(C_CLS, D))
     labels = torch.empty(P, dtype=torch.uint8, device=dev)
@@ -723,7 +743,7 @@ def run_extras(lib, N, torch, ctx, W, H, D, n, steps, stream, dev):
     ckpt = {"bytes": size, "save_s": t1 - t0, "load_s": t2 - t1, "save_gbs": size / (t1 - t0) / 1e9,
             "load_gbs": size / (t2 - t1) / 1e9,
             "path": "SPLF v1 file <-> pinned host <-> device pack/unpack (host file I/O included)"}
-    return {"segment_by_query": query, "checkpoint": ckpt}
+    return {"full_blend_feature": full_blend, "segment_by_query": query, "checkpoint": ckpt}
 
 
 def main():
