@@ -348,14 +348,18 @@ def main_gpu(args, cfg):
     N.check(lib.tk_synchronize(ctx))
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    ev_step = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]  # per-step spread
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
-    N.check(lib.tk_join(ctx))  # the main stream now follows the side streams' work
+        N.check(lib.tk_join(ctx))  # the main stream now follows the side streams' work
+        ev_step[i].record(stream)
     ev1.record(stream)
     N.check(lib.tk_synchronize(ctx))
     barrier()
     clk = clocks.stop()
+    step_ms = [ev0.elapsed_time(ev_step[0])] + [ev_step[i - 1].elapsed_time(ev_step[i]) for i in range(1, args.steps)]
+    step_stats = {"median": float(np.median(step_ms)), "best": float(min(step_ms)), "worst": float(max(step_ms))}
     N.check(lib.tk_profile_enable(ctx, 0))
     ms = ev0.elapsed_time(ev1)
     launches = lib.tk_kernel_launches(ctx) - launches0
@@ -447,7 +451,7 @@ def main_gpu(args, cfg):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms_step, "step_ms": step_stats, "higher_is_better": True,
             "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
             "config": {"workload": cfg["label"], "gaussians": n, "width": W, "height": H, "feature_dim": D,

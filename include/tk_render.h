@@ -58,7 +58,10 @@ typedef enum {
 
 /* TK_HOST_ASYNC: pinned host memory copied on the context's own copy streams (host->device and
  * device->host run concurrently on the two copy engines); the call returns without waiting, the
- * host buffer must stay untouched until tk_synchronize(). */
+ * host buffer must stay untouched until tk_synchronize().  Asynchronous scene uploads are
+ * double-buffered (the next scene streams in while the current frame still computes on the
+ * previous one; device views from tk_device_view_get refer to the scene current at the call), and
+ * asynchronous upstream-gradient uploads wait only for the previous call that read their buffer. */
 enum { TK_HOST = 0, TK_DEVICE = 1, TK_HOST_ASYNC = 2 };
 
 typedef struct tk_ctx tk_ctx;

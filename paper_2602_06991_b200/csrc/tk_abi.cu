@@ -6,11 +6,18 @@
 namespace tkabi {
 
 // Host <-> device copies made inside an API call (timed as TK_PHASE_COPY when profiling).
-void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c) {
+// TK_HOST_ASYNC: the copy runs on s_in after the compute that may still read dst -- all compute
+// issued so far, or, when the caller knows dst's last reader, only `reader` (`has_reader` false:
+// dst has not been read yet) -- and the compute that follows waits for it.
+void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, const ReaderEvent* reader) {
     if (bytes == 0) return;
-    if (mem == TK_HOST_ASYNC) {  // after the compute issued so far (it may still read dst), before what follows
-        CK(cudaEventRecord(c->ev_cmp, c->cur));
-        CK(cudaStreamWaitEvent(c->s_in, c->ev_cmp, 0));
+    if (mem == TK_HOST_ASYNC) {
+        if (!reader) {
+            CK(cudaEventRecord(c->ev_cmp, c->cur));
+            CK(cudaStreamWaitEvent(c->s_in, c->ev_cmp, 0));
+        } else if (reader->pending) {
+            CK(cudaStreamWaitEvent(c->s_in, reader->ev, 0));
+        }
         if (c->out_pending[0]) CK(cudaStreamWaitEvent(c->s_in, c->ev_out[0], 0));  // untagged reads (misc)
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s_in));
         CK(cudaEventRecord(c->ev_in, c->s_in));
@@ -553,7 +560,7 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking);
         for (cudaEvent_t* ev : {&c->ev_cmp, &c->ev_in, &c->ev_out[0], &c->ev_out[1], &c->ev_out[2], &c->ev_out[3],
-                                &c->ev_out[4]})
+                                &c->ev_out[4], &c->ev_scene_free, &c->fgrad_reader.ev, &c->ggrad_reader.ev})
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
         if (e == cudaSuccess)
             e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_twist), tk_ctx::kTwistSlots * 8 * sizeof(double),
@@ -616,7 +623,8 @@ tk_status tk_destroy(tk_ctx* c) {
     if (c->s_feat && c->s_feat != c->stream) cudaStreamDestroy(c->s_feat);
     if (c->s_geo && c->s_geo != c->stream) cudaStreamDestroy(c->s_geo);
     for (cudaEvent_t e : {c->ev_main, c->ev_feat, c->ev_geo, c->ev_cmp, c->ev_in, c->ev_out[0], c->ev_out[1],
-                          c->ev_out[2], c->ev_out[3], c->ev_out[4]})
+                          c->ev_out[2], c->ev_out[3], c->ev_out[4], c->ev_scene_free, c->fgrad_reader.ev,
+                          c->ggrad_reader.ev})
         if (e) cudaEventDestroy(e);
     if (c->h_twist) cudaFreeHost(c->h_twist);
     if (c->s_in) cudaStreamDestroy(c->s_in);
@@ -675,6 +683,46 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
         const int64_t n = s->n;
         if (!s->feature && c->has_features && (n != c->n || s->d != c->d))
             fail(TK_ERR_BAD_ARG, "feature == NULL requires unchanged n and d");
+        if (mem == TK_HOST_ASYNC) {
+            // Double buffer: the copies fill the back set, waiting only for the compute that read
+            // it (issued before the previous upload) -- not for the frame still running on the
+            // front set -- then the sets swap; compute issued from here on waits for the copies.
+            if (c->scene_free_pending) CK(cudaStreamWaitEvent(c->s_in, c->ev_scene_free, 0));
+            if (c->out_pending[0]) CK(cudaStreamWaitEvent(c->s_in, c->ev_out[0], 0));
+            auto up = [&](void* dst, const void* src, size_t bytes) {
+                if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->s_in));
+            };
+            up(ensure<double>(c->mean_b, n * 3), s->mean, n * 3 * sizeof(double));
+            up(ensure<double>(c->log_scale_b, n * 3), s->log_scale, n * 3 * sizeof(double));
+            up(ensure<double>(c->rotation_b, n * 4), s->rotation, n * 4 * sizeof(double));
+            up(ensure<double>(c->opacity_logit_b, n), s->opacity_logit, n * sizeof(double));
+            up(ensure<double>(c->color_b, n * 3), s->color, n * 3 * sizeof(double));
+            if (s->feature)
+                up(ensure<float>(c->feature_b, n * std::max(s->d, 1)), s->feature,
+                   static_cast<size_t>(n) * s->d * sizeof(float));
+            CK(cudaEventRecord(c->ev_in, c->s_in));
+            CK(cudaEventRecord(c->ev_scene_free, st));  // the outgoing front set: read by compute so far
+            c->scene_free_pending = true;
+            CK(cudaStreamWaitEvent(st, c->ev_in, 0));
+            std::swap(c->mean, c->mean_b);
+            std::swap(c->log_scale, c->log_scale_b);
+            std::swap(c->rotation, c->rotation_b);
+            std::swap(c->opacity_logit, c->opacity_logit_b);
+            std::swap(c->color, c->color_b);
+            if (s->feature) {
+                std::swap(c->feature, c->feature_b);
+                c->has_features = true;
+            }
+            c->n = n;
+            c->d = s->d;
+            c->generation = s->generation;
+            c->scene_version += 1;
+            c->has_scene = true;
+            c->prepared = false;
+            c->aux_valid = false;
+            main_done(c);
+            return;
+        }
         copy_in(ensure<double>(c->mean, n * 3), s->mean, n * 3 * sizeof(double), mem, c);
         copy_in(ensure<double>(c->log_scale, n * 3), s->log_scale, n * 3 * sizeof(double), mem, c);
         copy_in(ensure<double>(c->rotation, n * 4), s->rotation, n * 4 * sizeof(double), mem, c);
@@ -835,7 +883,7 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
             g = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
         } else if (grad_mem != TK_DEVICE) {
             float* dg = ensure<float>(c->f_grad_in, P * std::max(c->d, 1));
-            copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), grad_mem, c);
+            copy_in(dg, grad, static_cast<size_t>(P) * c->d * sizeof(float), grad_mem, c, &c->fgrad_reader);
             g = dg;
         }
         const SlotIndex si = build_slot_index(c, r);
@@ -848,6 +896,7 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
         }
         c->launches += n > 0 ? 3 : 0;
         CK_LAUNCH(c);
+        c->fgrad_reader.record(st);  // the next asynchronous grad_feature upload waits only for this
         if (out && out_mem != TK_DEVICE) {
             copy_out(out, dst, static_cast<size_t>(n) * c->d * sizeof(float), out_mem, c, kOutDF);
             if (out_mem == TK_HOST) sync(c);
@@ -928,15 +977,16 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         const double* gd = grad_depth;
         if (grad_mem != TK_DEVICE) {
             double* dgc = ensure<double>(c->g_color_in, P * 3);
-            copy_in(dgc, grad_color, P * 3 * sizeof(double), grad_mem, c);
+            copy_in(dgc, grad_color, P * 3 * sizeof(double), grad_mem, c, &c->ggrad_reader);
             gc = dgc;
             if (grad_depth) {
                 double* dgd = ensure<double>(c->g_depth_in, P);
-                copy_in(dgd, grad_depth, P * sizeof(double), grad_mem, c);
+                copy_in(dgd, grad_depth, P * sizeof(double), grad_mem, c, &c->ggrad_reader);
                 gd = dgd;
             }
         }
         double* mid = geom_sweep(c, f, gc, gd);
+        c->ggrad_reader.record(c->cur);  // the next asynchronous grad upload waits only for the sweep
         const bool dev_out = out && out->mem == TK_DEVICE;
         wait_out(c, kOutGG);
         tk::ChainParams cp = chain_params(c, pose, cam, s, mid);

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <random>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "feature.cuh"
@@ -49,9 +50,28 @@ struct TkError {
         if (e_ != cudaSuccess) fail(TK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
     } while (0)
 
+// Owning device allocation (move-only; freed on destruction or release()).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void release() {
         if (p) cudaFree(p);
         p = nullptr;
@@ -165,6 +185,17 @@ struct Profiler {
 };
 
 // One keyframe of SceneMap::keyframes, device-resident (ground-truth images + pose).
+// The last kernel that reads a device input buffer: an asynchronous upload into the buffer waits
+// for it alone rather than for all compute issued so far.
+struct ReaderEvent {
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+    void record(cudaStream_t st) {
+        CK(cudaEventRecord(ev, st));
+        pending = true;
+    }
+};
+
 struct Keyframe {
     tk_pose pose{};
     int w = 0, h = 0, d = 0;
@@ -211,6 +242,13 @@ struct tk_ctx {
     uint64_t scene_version = 0;
     bool has_scene = false, has_features = false;
     DevBuf mean, log_scale, rotation, opacity_logit, color, feature;
+    // TK_HOST_ASYNC uploads are double-buffered: the next scene lands in the back set (which only
+    // waits for the compute that read it, ev_scene_free) while the front set is still in use
+    DevBuf mean_b, log_scale_b, rotation_b, opacity_logit_b, color_b, feature_b;
+    cudaEvent_t ev_scene_free = nullptr;
+    bool scene_free_pending = false;
+    // last readers of the asynchronous upstream-gradient inputs (feature backward; geometry sweep)
+    ReaderEvent fgrad_reader, ggrad_reader;
     // projection, per Gaussian
     DevBuf pmx, pmy, pixx, pixy, piyy, pz, pop, rect, valid, ntiles, pos;
     DevBuf dkeys, dvals, dkeys_alt, dvals_alt, ntiles_sorted, pair_off;
@@ -331,7 +369,7 @@ struct SlotIndex {
 };
 
 // helpers defined in tk_abi.cu
-void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c);
+void copy_in(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, const ReaderEvent* reader = nullptr);
 void copy_out(void* dst, const void* src, size_t bytes, int mem, tk_ctx* c, int tag = kOutMisc);
 void sync(tk_ctx* c);
 void wait_out(tk_ctx* c, int tag);

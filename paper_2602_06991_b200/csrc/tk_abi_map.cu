@@ -16,8 +16,7 @@ T* grow_keep(tk_ctx* c, DevBuf& b, int64_t old_count, int64_t new_count, bool ze
         if (old_count > 0 && b.p)
             CK(cudaMemcpyAsync(nb.p, b.p, old_count * sizeof(T), cudaMemcpyDeviceToDevice, c->cur));
         CK(cudaStreamSynchronize(c->cur));
-        b.release();
-        b = nb;
+        b = std::move(nb);
     }
     if (zero_tail && new_count > old_count)
         CK(cudaMemsetAsync(ptr<T>(b) + old_count, 0, (new_count - old_count) * sizeof(T), c->cur));
@@ -40,8 +39,7 @@ void compact_rows(tk_ctx* c, DevBuf& b, int64_t n, int width, int64_t n_keep, co
     c->launches += n > 0;
     CK_LAUNCH(c);
     CK(cudaStreamSynchronize(c->cur));
-    b.release();
-    b = nb;
+    b = std::move(nb);
 }
 
 // prune_map's candidate draw (mapper.cpp:80-139), host side: candidates have topk_count <=

@@ -86,3 +86,59 @@ def test_async_host_buffers_match_synchronous():
         for p in keep:
             R.lib.tk_host_free(p)
         R.close()
+
+
+def test_async_double_buffered_upload_keeps_features_and_frames():
+    """TK_HOST_ASYNC scene uploads are double-buffered: a geometry-only async upload (feature NULL)
+    keeps the current features, and back-to-back frames on alternating buffers all match the
+    synchronous path (no frame sees another frame's scene)."""
+    cam = synth.test_camera(80, 56)
+    s = RenderSettings(top_k=3)
+    a = synth.random_scene(1200, 16, 11)
+    b = synth.random_scene(1200, 16, 12)
+    hybrid = b.copy()
+    hybrid.feature = a.feature.copy()  # b's geometry with a's features
+
+    def frame_sync(m):
+        R = api.Renderer(0)
+        try:
+            g = R.render_geometric(m, Pose(), cam, s)
+            return g.topk.index.copy(), R.render_feature(m, g.topk)
+        finally:
+            R.close()
+
+    plan = [(a, True, a), (b, False, hybrid), (b, True, b), (a, True, a), (a, False, a)]
+    want = [frame_sync(w) for _, _, w in plan]
+    R = api.Renderer(0)
+    keep = []
+    try:
+        lib = R.lib
+        cp, cc, cs = to_pose(Pose()), to_camera(cam), to_settings(s)
+        P = cam.width * cam.height
+        outs = []
+        for m, with_feat, _ in plan:
+            arrays = (m.mean, m.log_scale, m.rotation, m.opacity_logit, m.color)
+            geo = [pinned(lib, x.shape, np.float64, keep) for x in arrays]
+            for dst, x in zip(geo, arrays):
+                dst[...] = x
+            feat = None
+            if with_feat:
+                feat = pinned(lib, (m.size(), 16), np.float32, keep)
+                feat[...] = m.feature
+            view = N.tk_scene_view(m.size(), 16, *(x.ctypes.data for x in geo),
+                                   feat.ctypes.data if feat is not None else None, 0)
+            N.check(lib.tk_scene_upload(R.ctx, C.byref(view), N.TK_HOST_ASYNC))
+            idx = pinned(lib, (P * 3,), np.int32, keep)
+            F = pinned(lib, (P * 16,), np.float32, keep)
+            gout = N.tk_geom_out(N.TK_HOST_ASYNC, None, None, None, idx.ctypes.data, None, None, None, 0, 0)
+            N.check(lib.tk_render_geometric(R.ctx, C.byref(cp), C.byref(cc), C.byref(cs), C.byref(gout)))
+            N.check(lib.tk_render_feature(R.ctx, None, C.c_void_p(F.ctypes.data), N.TK_HOST_ASYNC))
+            outs.append((idx, F))
+        N.check(lib.tk_synchronize(R.ctx))
+        for i, ((idx, F), (widx, wF)) in enumerate(zip(outs, want)):
+            assert (idx == widx.ravel()).all(), i
+            assert np.array_equal(F.reshape(wF.shape), wF), i
+    finally:
+        for p in keep:
+            R.lib.tk_host_free(p)
+        R.close()
