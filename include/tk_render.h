@@ -263,6 +263,12 @@ tk_status tk_optimizer_reset(tk_ctx* ctx, int32_t reset_stats);
 tk_status tk_optimize_step(tk_ctx* ctx, const tk_mapper_config* cfg, const tk_camera* cam,
                            const tk_settings* s, int32_t slot, int64_t iteration, double* values_out,
                            int32_t* feature_step_out);
+/* The feature Adam of tk_optimize_step is lazy (TK_LAZY_ADAM=0 for eager): a feature step updates
+ * only the rows the frame's records reach; every other row's zero-gradient steps are replayed,
+ * bit-identically to the eager step, right before anything reads feature rows (the feature
+ * renders, tk_scene_download, structural edits, checkpoints, tk_device_view_get) or the next step
+ * that reaches them.  tk_optimizer_flush brings every row up to date now (asynchronous). */
+tk_status tk_optimizer_flush(tk_ctx* ctx);
 /* Loss values of the last tk_optimize_step (synchronises). */
 tk_status tk_loss_values(tk_ctx* ctx, double values[3]);
 tk_status tk_scene_download(tk_ctx* ctx, const tk_scene_out* out);

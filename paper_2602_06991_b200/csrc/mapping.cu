@@ -582,12 +582,31 @@ __device__ __forceinline__ float signed_w(uint32_t bits, int sh, float w) {
 
 // adam_step (optimizer.cpp:57-61) in fp32 with the bias corrections as host reciprocals and a
 // reciprocal-sqrt / fast-divide epilogue (the fp32 feature path's stated tolerance).
-__device__ __forceinline__ float adam1(float g, float& m, float& v, float f, const FeatAdamParams& p) {
+__device__ __forceinline__ float adam1(float g, float& m, float& v, float f, const AdamStepParams& p) {
     m = fmaf(p.beta1, m, p.one_m_beta1 * g);
     v = fmaf(p.beta2, v, p.one_m_beta2 * g * g);
     const float mhat = m * p.inv_bc1, vhat = v * p.inv_bc2;
     const float den = vhat * rsqrtf(fmaxf(vhat, 1e-30f)) + p.eps;
     return f - __fdividef(p.lr * mhat, den);
+}
+
+// One Adam step of a channel quad (gradient a * scale) and its squared-norm contribution: the one
+// code path of the eager step and of k_feature_catchup's replay, so both round alike.
+__device__ __forceinline__ float adam_quad(float4& f, float4& mm, float4& vv, float4 a, float scale,
+                                           const AdamStepParams& s) {
+    f.x = adam1(a.x * scale, mm.x, vv.x, f.x, s);
+    f.y = adam1(a.y * scale, mm.y, vv.y, f.y, s);
+    f.z = adam1(a.z * scale, mm.z, vv.z, f.z, s);
+    f.w = adam1(a.w * scale, mm.w, vv.w, f.w, s);
+    return f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
+}
+
+__device__ __forceinline__ float4 scale4(float4 f, float inv) {
+    f.x *= inv;
+    f.y *= inv;
+    f.z *= inv;
+    f.w *= inv;
+    return f;
 }
 
 __device__ __forceinline__ float warp_sum(float s) {
@@ -656,7 +675,7 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
 // moves every row through its moments); records summed in (pixel, slot) order.  LONG = false:
 // every Gaussian with <= kLongSeg records; LONG = true: the long Gaussians of the plan, whose
 // chunk partials (k_feature_adam_chunks) are added in chunk order.
-template <bool LONG>
+template <bool LONG, bool LAZY>
 __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -688,9 +707,19 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                 }
             }
         };
-        load_pass(0);
-        const int r0 = p.seg[g], r1 = p.seg[g + 1];
-        if (!LONG && r1 - r0 > kLongSeg) continue;
+        int r0, r1;
+        if (LAZY) {  // rows without records wait for k_feature_catchup: no loads for them
+            r0 = p.seg[g];
+            r1 = p.seg[g + 1];
+            if (!LONG && (r1 == r0 || r1 - r0 > kLongSeg)) continue;
+            load_pass(0);
+        } else {
+            load_pass(0);
+            r0 = p.seg[g];
+            r1 = p.seg[g + 1];
+            if (!LONG && r1 - r0 > kLongSeg) continue;
+        }
+        if (p.last && lane == 0) p.last[g] = p.cur;
         for (int base = 0; base < d4; base += 128) {
             if (base > 0) load_pass(base);
             float4 acc[4];
@@ -719,13 +748,9 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                 const int q = base + m * 32 + lane;
                 if (q >= d4) continue;
                 float4 f = fk[m], mm = mk[m], vv = vk[m];
-                f.x = adam1(acc[m].x * scale, mm.x, vv.x, f.x, p);
-                f.y = adam1(acc[m].y * scale, mm.y, vv.y, f.y, p);
-                f.z = adam1(acc[m].z * scale, mm.z, vv.z, f.z, p);
-                f.w = adam1(acc[m].w * scale, mm.w, vv.w, f.w, p);
+                ss += adam_quad(f, mm, vv, acc[m], scale, p.st);
                 __stcs(mrow + q, mm);
                 __stcs(vrow + q, vv);
-                ss += f.x * f.x + f.y * f.y + f.z * f.z + f.w * f.w;
                 fk[m] = f;
                 if (d4 > 128) frow[q] = f;
             }
@@ -747,16 +772,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int q = m * 32 + lane;
-                if (q < d4) {
-                    float4 f = fk[m];
-                    if (renorm) {
-                        f.x *= inv;
-                        f.y *= inv;
-                        f.z *= inv;
-                        f.w *= inv;
-                    }
-                    __stcs(frow + q, f);
-                }
+                if (q < d4) __stcs(frow + q, renorm ? scale4(fk[m], inv) : fk[m]);
             }
         } else if (renorm) {
             for (int q = lane; q < d4; q += 32) {
@@ -769,6 +785,67 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
             }
         }
     }
+}
+
+// Replay of the zero-gradient feature steps a lazy step skipped (rows without records): steps
+// last[g] + 1 .. target of every stale row (ONLY_ACTIVE: of the rows with records in p.seg, before
+// a step reads them), each with its own constants tab[t], the row held in registers throughout.
+// Step by step it runs the eager kernel's arithmetic for a row with no records (gradient +0,
+// adam_quad, warp_sum, renormalisation), so the result is bit-identical to having run every step
+// eagerly.  D % 4 == 0 and D <= 512 (one register pass per row).
+template <bool ONLY_ACTIVE>
+__global__ void __launch_bounds__(kThreads) k_feature_catchup(FeatAdamParams p, int target) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2;
+    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
+        if (ONLY_ACTIVE && p.seg[g] == p.seg[g + 1]) continue;
+        const int from = p.last[g];
+        if (from >= target) continue;
+        float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
+        float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
+        float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
+        float4 fk[4], mk[4], vk[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int q = m * 32 + lane;
+            if (q < d4) {
+                fk[m] = __ldcs(frow + q);
+                mk[m] = __ldcs(mrow + q);
+                vk[m] = __ldcs(vrow + q);
+            }
+        }
+        const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = from + 1; t <= target; ++t) {
+            const AdamStepParams st = p.tab[t];
+            float ss = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                if (m * 32 + lane < d4) ss += adam_quad(fk[m], mk[m], vk[m], zero, 0.0f, st);
+            const float ssum = warp_sum(ss);
+            const bool renorm = ssum > 1e-24f;
+            const float inv = renorm ? rsqrtf(ssum) : 1.0f;
+            if (renorm)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) fk[m] = scale4(fk[m], inv);
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int q = m * 32 + lane;
+            if (q < d4) {
+                __stcs(frow + q, fk[m]);
+                __stcs(mrow + q, mk[m]);
+                __stcs(vrow + q, vk[m]);
+            }
+        }
+        if (lane == 0) p.last[g] = target;
+    }
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t value) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        a[i] = value;
 }
 
 // One warp per chunk of a long segment: its sign sums into the plan's partial rows.
@@ -803,6 +880,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams
     const float scale = *p.scale;
     for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
         const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        if (p.last && lane == 0) p.last[g] = p.cur;
         float* frow = p.feat + g * D;
         float ss = 0.0f;
         for (int base = 0; base < D; base += 32) {
@@ -822,7 +900,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams
             }
             if (q < D) {
                 float mm = p.m[g * D + q], vv = p.v[g * D + q];
-                const float f = adam1(acc * scale, mm, vv, frow[q], p);
+                const float f = adam1(acc * scale, mm, vv, frow[q], p.st);
                 p.m[g * D + q] = mm;
                 p.v[g * D + q] = vv;
                 frow[q] = f;
@@ -944,13 +1022,34 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
     const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
     if (vec) {
-        k_feature_adam_vec<false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        if (p.lazy) k_feature_adam_vec<false, true><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        else k_feature_adam_vec<false, false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
         k_feature_adam_chunks<<<148 * 8, kThreads, 0, st>>>(p, p.plan);
-        k_feature_adam_vec<true><<<148 * 4, kThreads, 0, st>>>(p, p.plan);
+        k_feature_adam_vec<true, false><<<148 * 4, kThreads, 0, st>>>(p, p.plan);
     } else {
         k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
     }
     dbg_launch("k_feature_adam", st);
+}
+
+bool feature_adam_lazy_ok(const FeatAdamParams& p) {
+    return p.d > 0 && (p.d % 4) == 0 && p.d <= 512 && !p.row_ss && p.last && p.tab &&
+           (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 &&
+           (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
+}
+
+void launch_feature_catchup(const FeatAdamParams& p, int target, bool only_active, cudaStream_t st) {
+    if (p.n <= 0 || p.d <= 0 || target <= 0) return;
+    const unsigned grid = capped_grid(p.n, kWarps, 148 * 32);
+    if (only_active) k_feature_catchup<true><<<grid, kThreads, 0, st>>>(p, target);
+    else k_feature_catchup<false><<<grid, kThreads, 0, st>>>(p, target);
+    dbg_launch("k_feature_catchup", st);
+}
+
+void launch_fill_i32(int32_t* a, int64_t n, int32_t value, cudaStream_t st) {
+    if (n <= 0) return;
+    k_fill_i32<<<capped_grid(n, 256, 148 * 8), 256, 0, st>>>(a, n, value);
+    dbg_launch("k_fill_i32", st);
 }
 
 }  // namespace tk

@@ -54,6 +54,11 @@ struct FinalizeParams {
     float* feat_scale;       // lambda_feat / (feat_n * d), or 0
 };
 
+// Constants of one feature Adam step (optimizer.cpp:49-63 in fp32; bias corrections as host reciprocals).
+struct AdamStepParams {
+    float lr, beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bc1, inv_bc2;
+};
+
 struct FeatAdamParams {
     int64_t n;
     int k, d;
@@ -65,10 +70,25 @@ struct FeatAdamParams {
     float* feat;             // N x D, updated in place
     float* m;
     float* v;
-    float lr, beta1, beta2, one_m_beta1, one_m_beta2, eps, inv_bc1, inv_bc2;
+    AdamStepParams st;       // this step's constants
     LongPlan plan;           // segments longer than kLongSeg: chunk partials + ordered combine
     float* row_ss = nullptr; // D-sharded: per-Gaussian partial squared norms out, rows left unscaled
+    // Feature steps applied per row (last[g] = cur for every row a step processes).  lazy != 0:
+    // rows without records are skipped; their zero-gradient steps are replayed from tab[] (step
+    // t's constants, 1-based) by k_feature_catchup before anything reads them.
+    int32_t* last = nullptr;
+    int cur = 0;
+    int lazy = 0;
+    const AdamStepParams* tab = nullptr;
 };
+
+// Whether the feature Adam of this shape can run lazily (vector path, one register pass per row).
+bool feature_adam_lazy_ok(const FeatAdamParams& p);
+// Replay the skipped zero-gradient steps up to `target` of rows with last[g] < target -- every row
+// (only_active = false) or the rows with records in p.seg (true).
+void launch_feature_catchup(const FeatAdamParams& p, int target, bool only_active, cudaStream_t st);
+// last[0..n) = value
+void launch_fill_i32(int32_t* a, int64_t n, int32_t value, cudaStream_t st);
 
 // D-sharded renormalisation: f /= sqrt(ss[g]) when sqrt(ss[g]) > 1e-12 (ss all-reduced over shards)
 void launch_feature_renorm(float* feat, const float* ss, int64_t n, int d, cudaStream_t st);

@@ -484,6 +484,23 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     cp.dilation = s->cov2d_dilation;
     return cp;
 }
+void flush_features(tk_ctx* c) {
+    if (!c->feat_stale) return;
+    c->feat_stale = false;
+    if (!c->opt_ready || c->opt_n != c->n || c->opt_d != c->d || !c->f_last.p) return;
+    tk::FeatAdamParams fa{};
+    fa.n = c->n;
+    fa.d = c->d;
+    fa.feat = ptr<float>(c->feature);
+    fa.m = ptr<float>(c->fm);
+    fa.v = ptr<float>(c->fv);
+    fa.last = ptr<int32_t>(c->f_last);
+    fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
+    tk::launch_feature_catchup(fa, static_cast<int>(c->step_feat), false, c->cur);
+    c->launches += 1;
+    CK_LAUNCH(c);
+}
+
 // Drop the fused all-gather's peer buffers (IPC mappings closed, own buffer freed).
 void release_peers(tk_ctx* c) {
     if (c->peer_ipc)
@@ -679,6 +696,7 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
         if (s->n > INT32_MAX - 1) fail(TK_ERR_BAD_ARG, "scene larger than 2^31-1 Gaussians");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         cudaStream_t st = c->cur;
         const int64_t n = s->n;
         if (!s->feature && c->has_features && (n != c->n || s->d != c->d))
@@ -747,6 +765,12 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
 tk_status tk_device_view_get(tk_ctx* c, tk_device_view* v) {
     return guarded([&] {
         std::memset(v, 0, sizeof(*v));
+        if (c->feat_stale) {  // the view exposes the feature rows: bring them up to date
+            CK(cudaSetDevice(c->device));
+            on_main(c);
+            flush_features(c);
+            main_done(c);
+        }
         v->color = ptr<double>(c->o_color);
         v->depth = ptr<double>(c->o_depth);
         v->alpha = ptr<double>(c->o_alpha);
@@ -843,6 +867,7 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
     return guarded([&] {
         CK(cudaSetDevice(c->device));
         on_side(c, true);
+        flush_features(c);  // lazily optimised feature rows must be current
         require_features(c);
         const Records r = resolve_records(c, topk, "render_feature");
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
@@ -911,6 +936,7 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
         check_frame(cam, s);
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         require_features(c);
         prepare(c, pose, cam, s);
         cudaStream_t st = c->cur;
@@ -1197,6 +1223,7 @@ tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float*
         if (c->peer_n == 0) fail(TK_ERR_STATE, "no peer buffers (tk_comm_p2p_setup or tk_comm_set_peers)");
         CK(cudaSetDevice(c->device));
         on_side(c, true);
+        flush_features(c);  // lazily optimised feature rows must be current
         require_features(c);
         if (c->d * c->peer_n != c->peer_dtotal) fail(TK_ERR_BAD_ARG, "d_total must equal nranks * d_shard");
         const Records r = resolve_records(c, topk, "render_feature");

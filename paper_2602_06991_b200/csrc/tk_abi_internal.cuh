@@ -297,6 +297,11 @@ struct tk_ctx {
     // segment_by_query scratch (kept across calls: no allocation on the query path)
     DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
     DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
+    // lazy feature Adam: steps applied per row, every step's constants (host + device, 1-based);
+    // feat_stale: some rows lag the step count (replayed by flush_features before features are read)
+    DevBuf f_last, f_tab;
+    std::vector<tk::AdamStepParams> f_tab_host;
+    bool feat_stale = false;
     DevBuf row_ss;                                        // D-sharded partial row norms
     // multi-GPU
     ncclComm_t comm = nullptr;
@@ -395,6 +400,9 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
                              const double* mid);
 void scene_changed(tk_ctx* c);
 void release_peers(tk_ctx* c);
+// Bring every row of the lazily optimised features up to the current feature step (no-op unless
+// a lazy step left rows behind).  Called before anything reads or replaces features or moments.
+void flush_features(tk_ctx* c);
 void require_features(tk_ctx* c);
 
 }  // namespace tkabi

@@ -30,6 +30,7 @@ tk_status tk_checkpoint_save(tk_ctx* c, const char* path) {
         if (c->d > 0 && !c->has_features) fail(TK_ERR_STATE, "scene has no features uploaded");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         const int64_t n = c->n;
         const int64_t W = 14 + c->d;
         DevBuf rec;
@@ -106,6 +107,7 @@ tk_status tk_checkpoint_load(tk_ctx* c, const char* path) {
         }
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         DevBuf rec;
         float* drec = ensure<float>(rec, n * W);
         copy_in(drec, host, body, TK_HOST, c);

@@ -165,6 +165,7 @@ tk_status tk_optimizer_reset(tk_ctx* c, int32_t reset_stats) {
         if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // pending lazy steps land before the moments are dropped
         const int64_t n = c->n;
         const int dims[5] = {3, 3, 4, 1, 3};
         for (int g = 0; g < 5; ++g) {
@@ -180,6 +181,9 @@ tk_status tk_optimizer_reset(tk_ctx* c, int32_t reset_stats) {
             c->stat_n = n;
         }
         c->step_geo = c->step_feat = 0;
+        tk::launch_fill_i32(ensure<int32_t>(c->f_last, n), n, 0, c->cur);
+        c->f_tab_host.assign(1, tk::AdamStepParams{});  // index 0 unused: steps are 1-based
+        c->feat_stale = false;
         c->opt_ready = true;
         c->opt_n = n;
         c->opt_d = c->d;
@@ -211,6 +215,14 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fail(TK_ERR_BAD_ARG, "compute_losses: feature loss requested but render has no feature image");
             if (kf.d != c->d) fail(TK_ERR_BAD_ARG, "compute_losses: feature shape mismatch");
         }
+        // Lazy feature Adam (TK_LAZY_ADAM=0: eager): a feature step updates only the rows this
+        // frame's records reach; the other rows' zero-gradient steps are replayed bit-identically
+        // (k_feature_catchup) right before anything reads them.
+        static const bool lazy_env = [] {
+            const char* e = std::getenv("TK_LAZY_ADAM");
+            return !(e && e[0] == '0');
+        }();
+        const bool lazy_feat = feature_step && lazy_env && !sharded && c->d % 4 == 0 && c->d <= 512;
         CK(cudaSetDevice(c->device));
         on_main(c);
         cudaStream_t st = c->cur;
@@ -228,6 +240,55 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
         float* fscale = ensure<float>(c->l_fscale, 1);
         const int wpp = (d + 15) / 16;
         uint32_t* signs = feature_step ? ensure<uint32_t>(c->l_signs, P * std::max(wpp, 1)) : nullptr;
+        // this feature step's Adam constants (step k, 1-based), kept per step for lazy replays
+        const int64_t kstep = c->step_feat + 1;
+        tk::AdamStepParams ast{};
+        if (feature_step && d > 0) {
+            ast.lr = static_cast<float>(cfg->lr_feature);
+            ast.beta1 = static_cast<float>(cfg->beta1);
+            ast.beta2 = static_cast<float>(cfg->beta2);
+            ast.eps = static_cast<float>(cfg->eps);
+            ast.one_m_beta1 = static_cast<float>(1.0 - cfg->beta1);
+            ast.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
+            ast.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(kstep))));
+            ast.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(kstep))));
+            if (c->f_tab_host.size() != static_cast<size_t>(kstep)) fail(TK_ERR_STATE, "feature step table out of sync");
+            c->f_tab_host.push_back(ast);
+            const int64_t cap = static_cast<int64_t>(c->f_tab.bytes / sizeof(tk::AdamStepParams));
+            tk::AdamStepParams* tab = cap > kstep ? ptr<tk::AdamStepParams>(c->f_tab)
+                                                  : grow_keep<tk::AdamStepParams>(c, c->f_tab, kstep, 2 * kstep + 64, false);
+            CK(cudaMemcpyAsync(tab + kstep, &c->f_tab_host[kstep], sizeof(tk::AdamStepParams), cudaMemcpyHostToDevice,
+                               st));
+        }
+        // lazy: the rows this frame's records reach catch up to step k-1 before the loss reads them
+        SlotIndex early_si{};
+        bool have_si = false;
+        if (lazy_feat) {
+            Records r;
+            r.w = f.width;
+            r.h = f.height;
+            r.k = f.k;
+            r.index = ptr<int32_t>(c->o_index);
+            r.weight = ptr<double>(c->o_weight);
+            r.count = ptr<uint8_t>(c->o_count);
+            early_si = build_slot_index(c, r);
+            have_si = true;
+            tk::FeatAdamParams fa{};
+            fa.n = n;
+            fa.d = d;
+            fa.seg = early_si.seg;
+            fa.feat = ptr<float>(c->feature);
+            fa.m = ptr<float>(c->fm);
+            fa.v = ptr<float>(c->fv);
+            fa.last = ptr<int32_t>(c->f_last);
+            fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
+            if (c->feat_stale) {
+                tk::launch_feature_catchup(fa, static_cast<int>(kstep - 1), true, st);
+                c->launches += 1;
+            }
+        } else if (feature_step && d > 0) {
+            flush_features(c);  // an eager step needs every row at step k-1 (step_feat is still k-1)
+        }
         {
             PhaseScope phase(c, TK_PHASE_LOSS);
             CK(cudaMemsetAsync(partial, 0, tk::kLossBlocks * tk::kLossSlots * sizeof(double), st));
@@ -363,7 +424,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             c->launches += n > 0 ? 2 : 0;
             CK_LAUNCH(c);
             if (feature_step && d > 0) {  // mapper.cpp:239-252
-                c->step_feat += 1;
+                c->step_feat = kstep;
                 Records r;
                 r.w = f.width;
                 r.h = f.height;
@@ -371,7 +432,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 r.index = ptr<int32_t>(c->o_index);
                 r.weight = ptr<double>(c->o_weight);
                 r.count = ptr<uint8_t>(c->o_count);
-                const SlotIndex si = build_slot_index(c, r);
+                const SlotIndex si = have_si ? early_si : build_slot_index(c, r);
                 tk::FeatAdamParams fa{};
                 fa.n = n;
                 fa.k = f.k;
@@ -384,17 +445,16 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fa.feat = ptr<float>(c->feature);
                 fa.m = ptr<float>(c->fm);
                 fa.v = ptr<float>(c->fv);
-                fa.lr = static_cast<float>(cfg->lr_feature);
-                fa.beta1 = static_cast<float>(cfg->beta1);
-                fa.beta2 = static_cast<float>(cfg->beta2);
-                fa.eps = static_cast<float>(cfg->eps);
-                fa.one_m_beta1 = static_cast<float>(1.0 - cfg->beta1);
-                fa.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
-                fa.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(c->step_feat))));
-                fa.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(c->step_feat))));
+                fa.st = ast;
                 fa.plan = si.plan;
                 if (sharded) fa.row_ss = ensure<float>(c->row_ss, n);
+                fa.last = ptr<int32_t>(c->f_last);
+                fa.cur = static_cast<int>(kstep);
+                fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
+                fa.lazy = lazy_feat ? 1 : 0;
+                if (lazy_feat && !tk::feature_adam_lazy_ok(fa)) fail(TK_ERR_STATE, "lazy feature Adam: bad layout");
                 tk::launch_feature_adam(fa, st);
+                if (fa.lazy) c->feat_stale = true;
                 c->launches += n > 0 ? 3 : 0;
                 if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
                     NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
@@ -418,6 +478,16 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
     });
 }
 
+tk_status tk_optimizer_flush(tk_ctx* c) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        flush_features(c);
+        main_done(c);
+    });
+}
+
 tk_status tk_loss_values(tk_ctx* c, double values[3]) {
     return guarded([&] {
         if (!c->has_values) fail(TK_ERR_STATE, "no optimize_step has run");
@@ -435,6 +505,7 @@ tk_status tk_scene_download(tk_ctx* c, const tk_scene_out* o) {
             fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         const int64_t n = c->n;
         copy_out(o->mean, c->mean.p, n * 3 * sizeof(double), o->mem, c);
         copy_out(o->log_scale, c->log_scale.p, n * 3 * sizeof(double), o->mem, c);
@@ -470,6 +541,7 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
         if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         cudaStream_t st = c->cur;
         const int64_t ns = src->n;
         if (inserted) *inserted = 0;
@@ -555,6 +627,8 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
                 }
                 c->opt_n = n1;
                 c->opt_d = d;
+                // every row is current (flushed on entry); the new rows start at this step
+                tk::launch_fill_i32(ensure<int32_t>(c->f_last, n1), n1, static_cast<int32_t>(c->step_feat), st);
             }
             if (c->stat_n == n0) {
                 grow_keep<int32_t>(c, c->stat_count, n0, n1, true);
@@ -580,6 +654,7 @@ tk_status tk_prune_map(tk_ctx* c, double keep_ratio, uint64_t seed, int32_t thre
         if (c->stat_n != c->n) fail(TK_ERR_STATE, "no selection statistics for this scene (tk_optimizer_reset)");
         CK(cudaSetDevice(c->device));
         on_main(c);
+        flush_features(c);  // lazily optimised feature rows must be current
         cudaStream_t st = c->cur;
         const int64_t n = c->n;
         std::vector<int32_t> counts(n);
@@ -618,6 +693,8 @@ tk_status tk_prune_map(tk_ctx* c, double keep_ratio, uint64_t seed, int32_t thre
                     compact_rows<float>(c, c->fv, n, c->opt_d, nk, keep, pos);
                 }
                 c->opt_n = nk;
+                // every row is current (flushed on entry)
+                tk::launch_fill_i32(ensure<int32_t>(c->f_last, nk), nk, static_cast<int32_t>(c->step_feat), st);
             }
             sync(c);
             for (DevBuf* b : {&brem, &bkeep, &bpos}) b->release();
