@@ -679,23 +679,16 @@ template <bool LONG, bool LAZY>
 __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     const int D = p.d, d4 = D >> 2;
     const float scale = *p.scale;
-    const int64_t count = LONG ? plan.counters[1] : p.n;
-    for (int64_t wi = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; wi < count; wi += nw) {
-        int64_t g = wi;
-        int4 lg = make_int4(0, 0, 0, 0);
-        if (LONG) {
-            lg = plan.longs[wi];
-            g = lg.x;
-        }
+    // One row: Adam over its channel quads (gradient = sign sums of its records, or the long
+    // plan's chunk partials), then the renormalisation (mapper.cpp:249).
+    auto process_row = [&](int64_t g, int r0, int r1, int4 lg, bool loaded, float4 (&fk)[4], float4 (&mk)[4],
+                           float4 (&vk)[4]) {
         float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
         float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
         float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
-        float ss = 0.0f;
-        float4 fk[4], mk[4], vk[4];
-        // the row's parameter / moment loads go out first: they overlap the segment bounds and
-        // the record sweep (a skipped long row only wastes its first pass of loads)
         auto load_pass = [&](int base) {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -707,19 +700,9 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                 }
             }
         };
-        int r0, r1;
-        if (LAZY) {  // rows without records wait for k_feature_catchup: no loads for them
-            r0 = p.seg[g];
-            r1 = p.seg[g + 1];
-            if (!LONG && (r1 == r0 || r1 - r0 > kLongSeg)) continue;
-            load_pass(0);
-        } else {
-            load_pass(0);
-            r0 = p.seg[g];
-            r1 = p.seg[g + 1];
-            if (!LONG && r1 - r0 > kLongSeg) continue;
-        }
+        if (!loaded) load_pass(0);
         if (p.last && lane == 0) p.last[g] = p.cur;
+        float ss = 0.0f;
         for (int base = 0; base < d4; base += 128) {
             if (base > 0) load_pass(base);
             float4 acc[4];
@@ -764,7 +747,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                     const int q = m * 32 + lane;
                     if (q < d4) __stcs(frow + q, fk[m]);
                 }
-            continue;
+            return;
         }
         const bool renorm = ssum > 1e-24f;  // norm > 1e-12 (mapper.cpp:249)
         const float inv = renorm ? rsqrtf(ssum) : 1.0f;
@@ -784,6 +767,42 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
                 frow[q] = f;
             }
         }
+    };
+    float4 fk[4], mk[4], vk[4];
+    if (LONG) {
+        for (int64_t wi = warp_id; wi < plan.counters[1]; wi += nw) {
+            const int4 lg = plan.longs[wi];
+            process_row(lg.x, p.seg[lg.x], p.seg[lg.x + 1], lg, false, fk, mk, vk);
+        }
+    } else if (LAZY) {
+        // only the rows with records (the active list); the others wait for k_feature_catchup
+        const int na = *p.n_active;
+        for (int64_t wi = warp_id; wi < na; wi += nw) {
+            const int64_t g = p.active[wi];
+            const int r0 = p.seg[g], r1 = p.seg[g + 1];
+            if (r1 - r0 > kLongSeg) continue;
+            process_row(g, r0, r1, make_int4(0, 0, 0, 0), false, fk, mk, vk);
+        }
+    } else {
+        for (int64_t g = warp_id; g < p.n; g += nw) {
+            float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
+            float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
+            float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
+            // the row's parameter / moment loads go out first: they overlap the segment bounds and
+            // the record sweep (a skipped long row only wastes its first pass of loads)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = m * 32 + lane;
+                if (q < d4) {
+                    fk[m] = __ldcs(frow + q);
+                    mk[m] = __ldcs(mrow + q);
+                    vk[m] = __ldcs(vrow + q);
+                }
+            }
+            const int r0 = p.seg[g], r1 = p.seg[g + 1];
+            if (r1 - r0 > kLongSeg) continue;
+            process_row(g, r0, r1, make_int4(0, 0, 0, 0), true, fk, mk, vk);
+        }
     }
 }
 
@@ -798,10 +817,20 @@ __global__ void __launch_bounds__(kThreads) k_feature_catchup(FeatAdamParams p, 
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
-    for (int64_t g = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; g < p.n; g += nw) {
-        if (ONLY_ACTIVE && p.seg[g] == p.seg[g + 1]) continue;
-        const int from = p.last[g];
-        if (from >= target) continue;
+    const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+    const int64_t count = ONLY_ACTIVE ? *p.n_active : (p.n + 31) / 32;
+    for (int64_t wi = warp_id; wi < count; wi += nw) {
+      // ONLY_ACTIVE: one active row per warp visit; else 32 consecutive rows tested together
+      const int64_t g0 = ONLY_ACTIVE ? 0 : wi * 32;
+      const int64_t gl = ONLY_ACTIVE ? (lane == 0 ? p.active[wi] : -1) : g0 + lane;
+      int from_l = target;
+      if (gl >= 0 && gl < p.n) from_l = p.last[gl];
+      unsigned stale = __ballot_sync(0xffffffffu, from_l < target);
+      while (stale) {
+        const int l = __ffs(stale) - 1;
+        stale &= stale - 1;
+        const int64_t g = ONLY_ACTIVE ? __shfl_sync(0xffffffffu, gl, l) : g0 + l;
+        const int from = __shfl_sync(0xffffffffu, from_l, l);
         float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
         float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
         float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
@@ -839,6 +868,21 @@ __global__ void __launch_bounds__(kThreads) k_feature_catchup(FeatAdamParams p, 
             }
         }
         if (lane == 0) p.last[g] = target;
+      }
+    }
+}
+
+__global__ void k_active_rows(const int32_t* __restrict__ seg, int64_t n, int32_t* __restrict__ active,
+                              int32_t* __restrict__ n_active) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < n;
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const bool a = g < n && seg[g + 1] > seg[g];
+        const unsigned m = __ballot_sync(0xffffffffu, a);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(n_active, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (a) active[base + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(g);
     }
 }
 
@@ -1033,7 +1077,7 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
 }
 
 bool feature_adam_lazy_ok(const FeatAdamParams& p) {
-    return p.d > 0 && (p.d % 4) == 0 && p.d <= 512 && !p.row_ss && p.last && p.tab &&
+    return p.d > 0 && (p.d % 4) == 0 && p.d <= 512 && !p.row_ss && p.last && p.tab && p.active && p.n_active &&
            (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 &&
            (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
 }
@@ -1044,6 +1088,13 @@ void launch_feature_catchup(const FeatAdamParams& p, int target, bool only_activ
     if (only_active) k_feature_catchup<true><<<grid, kThreads, 0, st>>>(p, target);
     else k_feature_catchup<false><<<grid, kThreads, 0, st>>>(p, target);
     dbg_launch("k_feature_catchup", st);
+}
+
+void launch_active_rows(const int32_t* seg, int64_t n, int32_t* active, int32_t* n_active, cudaStream_t st) {
+    cudaMemsetAsync(n_active, 0, sizeof(int32_t), st);
+    if (n <= 0) return;
+    k_active_rows<<<capped_grid(n, 256, 148 * 8), 256, 0, st>>>(seg, n, active, n_active);
+    dbg_launch("k_active_rows", st);
 }
 
 void launch_fill_i32(int32_t* a, int64_t n, int32_t value, cudaStream_t st) {

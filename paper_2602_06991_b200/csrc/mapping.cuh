@@ -80,12 +80,17 @@ struct FeatAdamParams {
     int cur = 0;
     int lazy = 0;
     const AdamStepParams* tab = nullptr;
+    const int32_t* active = nullptr;    // lazy: the rows with records (any order), *n_active of them
+    const int32_t* n_active = nullptr;
 };
+
+// active[0 .. *n_active) = the rows g with seg[g + 1] > seg[g] (unordered)
+void launch_active_rows(const int32_t* seg, int64_t n, int32_t* active, int32_t* n_active, cudaStream_t st);
 
 // Whether the feature Adam of this shape can run lazily (vector path, one register pass per row).
 bool feature_adam_lazy_ok(const FeatAdamParams& p);
 // Replay the skipped zero-gradient steps up to `target` of rows with last[g] < target -- every row
-// (only_active = false) or the rows with records in p.seg (true).
+// (only_active = false) or the rows of p.active (true).
 void launch_feature_catchup(const FeatAdamParams& p, int target, bool only_active, cudaStream_t st);
 // last[0..n) = value
 void launch_fill_i32(int32_t* a, int64_t n, int32_t value, cudaStream_t st);

@@ -273,7 +273,12 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             r.count = ptr<uint8_t>(c->o_count);
             early_si = build_slot_index(c, r);
             have_si = true;
+            tk::launch_active_rows(early_si.seg, n, ensure<int32_t>(c->f_active, n), ensure<int32_t>(c->f_active_n, 1),
+                                   st);
+            c->launches += n > 0;
             tk::FeatAdamParams fa{};
+            fa.active = ptr<int32_t>(c->f_active);
+            fa.n_active = ptr<int32_t>(c->f_active_n);
             fa.n = n;
             fa.d = d;
             fa.seg = early_si.seg;
@@ -452,6 +457,10 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fa.cur = static_cast<int>(kstep);
                 fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
                 fa.lazy = lazy_feat ? 1 : 0;
+                if (lazy_feat) {
+                    fa.active = ptr<int32_t>(c->f_active);
+                    fa.n_active = ptr<int32_t>(c->f_active_n);
+                }
                 if (lazy_feat && !tk::feature_adam_lazy_ok(fa)) fail(TK_ERR_STATE, "lazy feature Adam: bad layout");
                 tk::launch_feature_adam(fa, st);
                 if (fa.lazy) c->feat_stale = true;
