@@ -297,6 +297,14 @@ tk_status tk_insert_gaussians(tk_ctx* ctx, const tk_source_view* src, double tau
 tk_status tk_prune_map(tk_ctx* ctx, double keep_ratio, uint64_t seed, int32_t topk_count_threshold,
                        int32_t* removed_out, int64_t* n_removed);
 
+/* FEAT feature frames (synth/dataset.cpp:48-76: "FEAT", uint32 h, w, d, then h*w*d fp32 HWC):
+ * load replaces keyframe `slot`'s feature image (same h x w as the keyframe; its row-validity mask
+ * is recomputed) straight from the file; save writes it.  Errors carry the reference's messages
+ * ("dataset: cannot open <path>", "dataset: bad magic in <path>", "dataset: truncated header in
+ * <path>", "dataset: truncated data in <path>", "dataset: write failed for <path>"). */
+tk_status tk_keyframe_load_features(tk_ctx* ctx, int32_t slot, const char* path);
+tk_status tk_keyframe_save_features(tk_ctx* ctx, int32_t slot, const char* path);
+
 /* SPLF v1 checkpoint (checkpoint.cpp:39-98): little-endian "SPLF", u32 version, u32 D, u64 N, then
  * per Gaussian f32 mean[3], log_scale[3], quat w,x,y,z, opacity_logit, color[3], feature[D].
  * Packed / unpacked on the device; load replaces the resident map (generation 0, optimiser state

@@ -140,6 +140,8 @@ RENDER_SYMBOLS = [
     ("tk_allgather_feature", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
     ("tk_comm_p2p_setup", C.c_int, [C.c_void_p, C.c_int64]),
     ("tk_optimizer_flush", C.c_int, [C.c_void_p]),
+    ("tk_keyframe_load_features", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
+    ("tk_keyframe_save_features", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p]),
     ("tk_comm_set_peers", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]),
     ("tk_render_feature_gathered", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     ("tk_comm_gathered_buffer", C.c_int, [C.c_void_p, C.c_void_p]),

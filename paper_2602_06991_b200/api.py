@@ -217,6 +217,14 @@ class Renderer:
         view = N.tk_frame_view(w, h, d, _p(col), _p(dep), _p(feat), N.TK_HOST)
         N.check(self.lib.tk_keyframe_set(self.ctx, slot, C.byref(to_pose(pose)), C.byref(view)))
 
+    def keyframe_load_features(self, slot: int, path: str) -> None:
+        """Replace keyframe `slot`'s feature image from a FEAT file (dataset.cpp:63-76)."""
+        N.check(self.lib.tk_keyframe_load_features(self.ctx, slot, str(path).encode()))
+
+    def keyframe_save_features(self, slot: int, path: str) -> None:
+        """Write keyframe `slot`'s feature image as a FEAT file (dataset.cpp:48-61)."""
+        N.check(self.lib.tk_keyframe_save_features(self.ctx, slot, str(path).encode()))
+
     def optimizer_reset(self, reset_stats: bool = True) -> None:
         """A zeroed OptimizerState (optimizer.hpp:25-53) for the resident map."""
         N.check(self.lib.tk_optimizer_reset(self.ctx, int(reset_stats)))

@@ -23,6 +23,91 @@ tk::SplfView splf_view(tk_ctx* c) {
 
 extern "C" {
 
+// ------------------------------------------------------------------ FEAT feature frames
+// read_feature_bin / write_feature_bin (synth/dataset.cpp:48-76): "FEAT", uint32 h, w, d, then
+// h * w * d fp32 in HWC order -- the keyframe's feature image, streamed through pinned memory.
+namespace {
+constexpr char kFeatMagic[4] = {'F', 'E', 'A', 'T'};
+}
+
+tk_status tk_keyframe_load_features(tk_ctx* c, int32_t slot, const char* path) {
+    return guarded([&] {
+        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
+        if (slot < 0 || static_cast<size_t>(slot) >= c->kfs.size() || c->kfs[slot].w == 0)
+            fail(TK_ERR_BAD_ARG, "keyframe_load_features: no keyframe in that slot");
+        std::FILE* fp = std::fopen(path, "rb");
+        if (!fp) fail(TK_ERR_BAD_ARG, std::string("dataset: cannot open ") + path);
+        struct Closer {
+            std::FILE* f;
+            ~Closer() { std::fclose(f); }
+        } closer{fp};
+        char magic[4];
+        uint32_t hdr[3];
+        if (std::fread(magic, 1, 4, fp) != 4 || std::memcmp(magic, kFeatMagic, 4) != 0)
+            fail(TK_ERR_BAD_ARG, std::string("dataset: bad magic in ") + path);
+        if (std::fread(hdr, 4, 3, fp) != 3) fail(TK_ERR_BAD_ARG, std::string("dataset: truncated header in ") + path);
+        Keyframe& k = c->kfs[slot];
+        const uint32_t h = hdr[0], w = hdr[1], d = hdr[2];
+        if (static_cast<int>(h) != k.h || static_cast<int>(w) != k.w)
+            fail(TK_ERR_BAD_ARG, "keyframe_load_features: feature image shape differs from the keyframe");
+        const int64_t P = static_cast<int64_t>(w) * h;
+        const size_t bytes = static_cast<size_t>(P) * d * sizeof(float);
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        float* host = nullptr;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&host), std::max<size_t>(bytes, 4), cudaHostAllocDefault));
+        struct HostFree {
+            float* p;
+            ~HostFree() { cudaFreeHost(p); }
+        } hf{host};
+        if (std::fread(host, 1, bytes, fp) != bytes) fail(TK_ERR_BAD_ARG, std::string("dataset: truncated data in ") + path);
+        k.d = static_cast<int>(d);
+        k.has_feature = d > 0;
+        float* feat = d > 0 ? ensure<float>(k.feature, static_cast<size_t>(P) * d) : nullptr;
+        if (d > 0) copy_in(feat, host, bytes, TK_HOST, c);
+        uint8_t* valid = ensure<uint8_t>(k.valid, P);
+        int64_t* dscal = ensure<int64_t>(c->dscal, 16);
+        tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, ptr<float>(k.depth), c->cur);
+        c->launches += 1;
+        CK_LAUNCH(c);
+        if (c->comm) NK(g_nccl.AllReduce(valid, valid, static_cast<size_t>(P), ncclUint8, ncclMax, c->comm, c->cur));
+        tk::copy_words_to_mapped(c->hscal_dev + 9, dscal + 9, 1, c->cur);
+        sync(c);
+        k.depth_n = c->hscal[9];
+        main_done(c);
+    });
+}
+
+tk_status tk_keyframe_save_features(tk_ctx* c, int32_t slot, const char* path) {
+    return guarded([&] {
+        if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
+        if (slot < 0 || static_cast<size_t>(slot) >= c->kfs.size() || c->kfs[slot].w == 0)
+            fail(TK_ERR_BAD_ARG, "keyframe_save_features: no keyframe in that slot");
+        const Keyframe& k = c->kfs[slot];
+        const int64_t P = static_cast<int64_t>(k.w) * k.h;
+        const size_t bytes = static_cast<size_t>(P) * (k.has_feature ? k.d : 0) * sizeof(float);
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        float* host = nullptr;
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&host), std::max<size_t>(bytes, 4), cudaHostAllocDefault));
+        struct HostFree {
+            float* p;
+            ~HostFree() { cudaFreeHost(p); }
+        } hf{host};
+        if (bytes) copy_out(host, ptr<float>(k.feature), bytes, TK_HOST, c);
+        sync(c);
+        std::FILE* fp = std::fopen(path, "wb");
+        if (!fp) fail(TK_ERR_BAD_ARG, std::string("dataset: cannot open ") + path + " for writing");
+        const uint32_t hdr[3] = {static_cast<uint32_t>(k.h), static_cast<uint32_t>(k.w),
+                                 static_cast<uint32_t>(k.has_feature ? k.d : 0)};
+        const bool ok = std::fwrite(kFeatMagic, 1, 4, fp) == 4 && std::fwrite(hdr, 4, 3, fp) == 3 &&
+                        std::fwrite(host, 1, bytes, fp) == bytes;
+        const bool closed = std::fclose(fp) == 0;
+        if (!ok || !closed) fail(TK_ERR_BAD_ARG, std::string("dataset: write failed for ") + path);
+        main_done(c);
+    });
+}
+
 tk_status tk_checkpoint_save(tk_ctx* c, const char* path) {
     return guarded([&] {
         if (!c || !path) fail(TK_ERR_BAD_ARG, "null argument");
