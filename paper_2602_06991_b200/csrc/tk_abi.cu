@@ -609,29 +609,7 @@ tk_status tk_destroy(tk_ctx* c) {
     if (c->s_geo) cudaStreamSynchronize(c->s_geo);
     if (c->s_in) cudaStreamSynchronize(c->s_in);
     if (c->s_out) cudaStreamSynchronize(c->s_out);
-    DevBuf* all[] = {&c->mean, &c->log_scale, &c->rotation, &c->opacity_logit, &c->color, &c->feature, &c->pmx,
-                     &c->pmy, &c->pixx, &c->pixy, &c->piyy, &c->pz, &c->pop, &c->rect, &c->valid, &c->ntiles,
-                     &c->pos, &c->dkeys, &c->dvals, &c->dkeys_alt, &c->dvals_alt, &c->ntiles_sorted, &c->pair_off,
-                     &c->tkeys, &c->tvals, &c->tkeys_alt, &c->tvals_alt, &c->tile_offsets, &c->padded_cnt,
-                     &c->padded_start, &c->scratch, &c->scratch_feat, &c->dscal, &c->o_color, &c->o_depth, &c->o_alpha, &c->o_index,
-                     &c->o_weight, &c->o_count, &c->o_contrib, &c->aux_t, &c->aux_n, &c->x_index, &c->x_weight,
-                     &c->x_count, &c->f_out, &c->f_grad_in, &c->f_grad_out, &c->s_keys, &c->s_vals,
-                     &c->s_keys_alt, &c->s_vals_alt, &c->s_wnorm, &c->s_seg, &c->g_color_in, &c->g_depth_in,
-                     &c->mid, &c->twist, &c->twist_part, &c->twist_out, &c->gg_mean, &c->gg_ls, &c->gg_rot,
-                     &c->gg_op, &c->gg_col, &c->l_count, &c->l_off, &c->l_src, &c->l_w, &c->gather_buf,
-                     &c->wl, &c->wl_count};
-    for (DevBuf* b : all) b->release();
-    c->te.release();
-    for (Keyframe& k : c->kfs) k.release();
-    for (int g = 0; g < 5; ++g) {
-        c->am[g].release();
-        c->av[g].release();
-    }
-    DevBuf* mapping[] = {&c->fm, &c->fv, &c->stat_count, &c->stat_maxc, &c->ssim_rows, &c->ssim_win, &c->l_gc,
-                         &c->l_gd, &c->l_partial, &c->l_values, &c->l_fscale, &c->l_signs, &c->q_feat,
-                         &c->q_emb, &c->q_labels, &c->q_best, &c->q_acc, &c->q_nacc, &c->q_part,
-                         &c->lp_items, &c->lp_longs, &c->lp_counters, &c->lp_partial, &c->row_ss};
-    for (DevBuf* b : mapping) b->release();
+    // device buffers (DevBuf members, keyframes) are freed by their destructors in `delete c`
     if (c->hvals) cudaFreeHost(c->hvals);
     release_peers(c);
     if (c->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(c->comm);
