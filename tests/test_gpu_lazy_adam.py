@@ -61,6 +61,13 @@ for it in range(1, 16):
         out["F7"] = F
     if it == 10:
         out["removed"] = r.prune_map(0.6, 1234, 2)
+    if it == 12:  # new Gaussians enter with fresh moments at the current feature step
+        rs = np.random.default_rng(9)
+        npts = 200
+        pos = np.c_[rs.uniform(-1, 1, npts), rs.uniform(-0.7, 0.7, npts), rs.uniform(2, 5, npts)]
+        out["inserted"] = np.array([r.insert_gaussians(pos, rs.uniform(0, 1, (npts, 3)),
+                                                       rs.normal(0, 1, (npts, D)).astype(np.float32),
+                                                       np.full(npts, 0.05), np.full(npts, 1.0), 0.05, Pose())])
 n, d, _ = r.scene_info()
 for k, v in r.scene_download(n, d).items():
     out[k] = v
