@@ -334,7 +334,8 @@ tk_status tk_pair_count(tk_ctx* ctx, int64_t* pairs, int32_t reset);
  * denominator of the fp64 roofline of the geometric sweeps. */
 tk_status tk_fp64_rate(tk_ctx* ctx, double* fma_per_s);
 
-/* Profiling: number of kernels this context launched since creation. */
+/* Profiling: number of kernels the library has launched from the calling host thread (every
+ * launch site counts itself; take differences around a region to count that region's kernels). */
 int64_t tk_kernel_launches(tk_ctx* ctx);
 
 /* Per-phase device time (CUDA events on the context stream).  Phases: */

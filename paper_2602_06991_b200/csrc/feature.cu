@@ -708,13 +708,13 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
 }
 
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
-                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches) {
+                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st) {
     const unsigned g = static_cast<unsigned>((p.n_slots + 255) / 256);
     cudaMemsetAsync(cnt_seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
     cudaMemsetAsync(cursor, 0, (n_gaussians + 1) * sizeof(int32_t), st);
     if (p.n_slots > 0) k_slot_count<<<g, 256, 0, st>>>(p, cnt_seg);
     dbg_launch("k_slot_count", st);
-    scan_exclusive(cnt_seg, cnt_seg, n_gaussians + 1, total, scan_scratch, st, launches);
+    scan_exclusive(cnt_seg, cnt_seg, n_gaussians + 1, total, scan_scratch, st);
     if (p.n_slots > 0) k_slot_fill<<<g, 256, 0, st>>>(p, cnt_seg, cursor, recs);
     dbg_launch("k_slot_fill", st);
     if (n_gaussians > 0) {
@@ -729,7 +729,6 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt
         dbg_launch("k_seg_sort_warp", st);
         k_seg_sort_block<<<148, kSortThreads, 0, st>>>(cnt_seg, n_gaussians, cursor, counts, recs, sorted);
         dbg_launch("k_seg_sort_block", st);
-        *launches += 2;
     }
 }
 

@@ -82,7 +82,7 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
 // sorted hold the valid slot ids grouped by Gaussian (sorted: ascending within each segment).
 // cursor: n + 2 int32 of scratch.
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
-                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st, int64_t* launches);
+                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st);
 // the long-segment queue left in cursor by launch_slot_index: entries cursor[n - 1 - i] for
 // i < cursor[n + 1]
 void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st);

@@ -987,7 +987,7 @@ void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int
     dbg_launch("k_gt_valid", st);
 }
 
-void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launches) {
+void launch_color_loss(const ColorLossParams& p, cudaStream_t st) {
     const int64_t P = static_cast<int64_t>(p.w) * p.h;
     if (P <= 0) return;
     if (p.use_ssim) {
@@ -995,7 +995,6 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launc
         const int64_t tiles = 3LL * ((ow + kSW - 1) / kSW) * ((oh + kSH - 1) / kSH);
         k_ssim_stats<<<capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st>>>(p);
         dbg_launch("k_ssim_stats", st);
-        *launches += 1;
     }
     static FuncAttrCache attr;
     set_func_attr(attr, reinterpret_cast<const void*>(k_color_loss), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1003,7 +1002,6 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launc
     const int64_t tiles = static_cast<int64_t>((p.w + kCX - 1) / kCX) * ((p.h + kCY - 1) / kCY);
     k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, kColorSmem, st>>>(p);
     dbg_launch("k_color_loss", st);
-    *launches += 1;
 }
 
 template <int KMAX>
@@ -1068,12 +1066,15 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
     if (vec) {
         if (p.lazy) k_feature_adam_vec<false, true><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
         else k_feature_adam_vec<false, false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        dbg_launch("k_feature_adam_vec", st);
         k_feature_adam_chunks<<<148 * 8, kThreads, 0, st>>>(p, p.plan);
+        dbg_launch("k_feature_adam_chunks", st);
         k_feature_adam_vec<true, false><<<148 * 4, kThreads, 0, st>>>(p, p.plan);
+        dbg_launch("k_feature_adam_vec<long>", st);
     } else {
         k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+        dbg_launch("k_feature_adam_scalar", st);
     }
-    dbg_launch("k_feature_adam", st);
 }
 
 bool feature_adam_lazy_ok(const FeatAdamParams& p) {

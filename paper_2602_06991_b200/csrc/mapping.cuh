@@ -100,7 +100,7 @@ void launch_feature_renorm(float* feat, const float* ss, int64_t n, int d, cudaS
 
 void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int64_t* depth_n_out,
                      const float* gt_depth, cudaStream_t st);
-void launch_color_loss(const ColorLossParams& p, cudaStream_t st, int64_t* launches);
+void launch_color_loss(const ColorLossParams& p, cudaStream_t st);
 void launch_feature_loss(const FeatLossParams& p, cudaStream_t st);
 void launch_loss_finalize(const FinalizeParams& p, cudaStream_t st);
 void launch_topk_stats(const int32_t* index, const uint8_t* count, int64_t pixels, int k, int32_t* topk_count,

@@ -250,9 +250,11 @@ void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntil
 
 void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, const int32_t* ntiles_sorted,
                        const int32_t* pair_off, int tiles_x, uint32_t* tkeys, uint32_t* tvals, cudaStream_t st) {
-    if (nv > 0)
+    if (nv > 0) {
         k_emit_pairs<<<blocks_for(nv, 128), 128, 0, st>>>(order, nv, rect, ntiles_sorted, pair_off, tiles_x, tkeys,
                                                           tvals);
+        dbg_launch("k_emit_pairs", st);
+    }
 }
 
 void launch_padded_counts(const int32_t* tile_offsets, int n_tiles, int32_t* padded, cudaStream_t st) {
@@ -268,9 +270,11 @@ void launch_materialize(const MaterializeParams& p, cudaStream_t st) {
 void launch_export_entries(const uint32_t* order, int64_t nv, const double* mx, const double* my, const double* ixx,
                            const double* ixy, const double* iyy, const double* z, const double* opacity,
                            double* out7, int32_t* src, cudaStream_t st) {
-    if (nv > 0)
+    if (nv > 0) {
         k_export_entries<<<blocks_for(nv, 256), 256, 0, st>>>(order, nv, mx, my, ixx, ixy, iyy, z, opacity, out7,
                                                               src);
+        dbg_launch("k_export_entries", st);
+    }
 }
 
 }  // namespace tk

@@ -17,7 +17,14 @@ namespace tk {
 
 size_t align_bytes(size_t b) { return (b + 255) / 256 * 256; }
 
+namespace {
+thread_local int64_t t_launches = 0;  // kernels launched by this host thread (dbg_launch after each)
+}
+
+int64_t launch_count() { return t_launches; }
+
 void dbg_launch(const char* name, cudaStream_t st) {
+    ++t_launches;
     static const int on = [] {
         const char* e = std::getenv("TK_SYNC_CHECK");
         return e && e[0] == '1' ? 1 : 0;
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_ghist(const K* __restrict__ k
 
 template <typename K>
 void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n, int begin_bit,
-                     int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt, int64_t* launches) {
+                     int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt) {
     *result_in_alt = false;
     if (n <= 0 || end_bit <= begin_bit) return;
     const int nb = static_cast<int>((n + RS_TILE - 1) / RS_TILE);
@@ -396,13 +403,11 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
         const int hblocks = static_cast<int>(std::min<int64_t>(nb, 148 * 4));
         k_rs_ghist<K><<<hblocks, RS_THREADS, 0, st>>>(kin, n, begin_bit, npass, gcount);
         dbg_launch("k_rs_ghist", st);
-        *launches += 1;
         for (int p = 0; p < npass; ++p) {
             const OnesweepArgs os{gcount + p * RS_RADIX, status + p * status_words, tickets + p};
             k_rs_scatter<K, true><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, begin_bit + 8 * p, nullptr, nb,
                                                              os);
             dbg_launch("k_rs_onesweep", st);
-            *launches += 1;
             std::swap(kin, kout);
             std::swap(vin, vout);
             in_alt = !in_alt;
@@ -413,10 +418,9 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
         k_rs_hist<K><<<nb, RS_THREADS, 0, st>>>(kin, n, shift, hist, nb);
         dbg_launch("k_rs_hist", st);
-        scan_exclusive(hist, hist, hn, total, scan_scratch, st, launches);
+        scan_exclusive(hist, hist, hn, total, scan_scratch, st);
         k_rs_scatter<K, false><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb, OnesweepArgs{});
         dbg_launch("k_rs_scatter", st);
-        *launches += 2;
         std::swap(kin, kout);
         std::swap(vin, vout);
         in_alt = !in_alt;
@@ -526,12 +530,10 @@ size_t scan_scratch_bytes(int64_t n) {
     return align_bytes(static_cast<size_t>(nb + 2) * sizeof(int64_t));
 }
 
-void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch, cudaStream_t st,
-                    int64_t* launches) {
+void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch, cudaStream_t st) {
     if (n <= kSmallScan) {
         k_scan_single<<<1, 1024, 0, st>>>(in, out, n, total);
         dbg_launch("k_scan_single", st);
-        *launches += 1;
         return;
     }
     // single pass: a block reads its whole tile before writing it, so in-place is safe
@@ -542,7 +544,6 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
     k_scan_lookback<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, status, ticket, total,
                                                                       static_cast<int>(nb));
     dbg_launch("k_scan_lookback", st);
-    *launches += 1;
 }
 
 size_t radix_scratch_bytes(int64_t n) {
@@ -554,33 +555,25 @@ size_t radix_scratch_bytes(int64_t n) {
 }
 
 void radix_sort_pairs_u64(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                          int begin_bit, int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt,
-                          int64_t* launches) {
-    radix_sort_impl<uint64_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, st, result_in_alt,
-                              launches);
+                          int begin_bit, int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt) {
+    radix_sort_impl<uint64_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, st, result_in_alt);
 }
 
 void radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, int64_t n,
-                          int begin_bit, int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt,
-                          int64_t* launches) {
-    radix_sort_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, st, result_in_alt,
-                              launches);
+                          int begin_bit, int end_bit, void* scratch, cudaStream_t st, bool* result_in_alt) {
+    radix_sort_impl<uint32_t>(keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, scratch, st, result_in_alt);
 }
 
-void fixup_runs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int lo_bit, int32_t* overflow, cudaStream_t st,
-                    int64_t* launches) {
+void fixup_runs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int lo_bit, int32_t* overflow, cudaStream_t st) {
     if (n <= 1 || lo_bit <= 0) return;
     k_fixup_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, vals, n, lo_bit, overflow);
     dbg_launch("k_fixup_runs", st);
-    *launches += 1;
 }
 
-void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments, cudaStream_t st,
-                         int64_t* launches) {
+void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments, cudaStream_t st) {
     const int64_t total = n_segments + 1;
     k_segment_offsets<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(keys, n, offsets, n_segments);
     dbg_launch("k_segment_offsets", st);
-    *launches += 1;
 }
 
 }  // namespace tk

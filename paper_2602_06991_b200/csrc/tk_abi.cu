@@ -205,17 +205,15 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     CK(cudaMemsetAsync(dscal + 1, 0xff, sizeof(int64_t), st));
     CK(cudaMemsetAsync(dscal + 2, 0, sizeof(int64_t), st));
     tk::launch_project(pp, st);
-    c->launches += n > 0;
     CK_LAUNCH(c);
 
     int32_t* pos = ensure<int32_t>(c->pos, n);
-    tk::scan_exclusive(pp.valid, pos, n, dscal + 0, c->scratch.p, st, &c->launches);
+    tk::scan_exclusive(pp.valid, pos, n, dscal + 0, c->scratch.p, st);
     uint64_t* dkeys = ensure<uint64_t>(c->dkeys, n);
     uint32_t* dvals = ensure<uint32_t>(c->dvals, n);
     uint64_t* dkeys_alt = ensure<uint64_t>(c->dkeys_alt, n);
     uint32_t* dvals_alt = ensure<uint32_t>(c->dvals_alt, n);
     tk::launch_compact(pp.valid, pos, pp.z, n, pp.key_min, dkeys, dvals, st);
-    c->launches += n > 0;
     CK_LAUNCH(c);
     tk::copy_words_to_mapped(c->hscal_dev, dscal, 3, st);
     sync(c);
@@ -233,16 +231,14 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
         bool alt = false;
         CK(cudaMemsetAsync(dscal + 7, 0, sizeof(int64_t), st));
         if (n_vis > 1) {
-            tk::radix_sort_pairs_u64(dkeys, dvals, dkeys_alt, dvals_alt, n_vis, lo_bit, hb, c->scratch.p, st, &alt,
-                                     &c->launches);
+            tk::radix_sort_pairs_u64(dkeys, dvals, dkeys_alt, dvals_alt, n_vis, lo_bit, hb, c->scratch.p, st, &alt);
             tk::fixup_runs_u64(alt ? dkeys_alt : dkeys, alt ? dvals_alt : dvals, n_vis, lo_bit,
-                               reinterpret_cast<int32_t*>(dscal + 7), st, &c->launches);
+                               reinterpret_cast<int32_t*>(dscal + 7), st);
             CK_LAUNCH(c);
         }
         c->order = alt ? dvals_alt : dvals;
         tk::launch_sorted_ntiles(c->order, n_vis, pp.ntiles, nts, st);
-        c->launches += n_vis > 0;
-        tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st, &c->launches);
+        tk::scan_exclusive(nts, poff, n_vis, dscal + 3, c->scratch.p, st);
         tk::copy_words_to_mapped(c->hscal_dev + 3, dscal + 3, 5, st);
         sync(c);
     };
@@ -261,23 +257,20 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     uint32_t* tkeys_alt = ensure<uint32_t>(c->tkeys_alt, n_pairs);
     uint32_t* tvals_alt = ensure<uint32_t>(c->tvals_alt, n_pairs);
     tk::launch_emit_pairs(c->order, n_vis, pp.rect, nts, poff, f.tiles_x, tkeys, tvals, st);
-    c->launches += n_vis > 0;
     ensure_scratch(c, std::max<int64_t>(n_pairs, n_tiles + 1));
     bool talt = false;
     const int tbits = bits_for(static_cast<uint64_t>(n_tiles - 1));
     if (n_pairs > 1 && tbits > 0) {
-        tk::radix_sort_pairs_u32(tkeys, tvals, tkeys_alt, tvals_alt, n_pairs, 0, tbits, c->scratch.p, st, &talt,
-                                 &c->launches);
+        tk::radix_sort_pairs_u32(tkeys, tvals, tkeys_alt, tvals_alt, n_pairs, 0, tbits, c->scratch.p, st, &talt);
     }
     c->tile_keys_sorted = talt ? tkeys_alt : tkeys;
     c->tile_vals_sorted = talt ? tvals_alt : tvals;
     int32_t* toff = ensure<int32_t>(c->tile_offsets, n_tiles + 1);
-    tk::segment_offsets_u32(c->tile_keys_sorted, n_pairs, toff, n_tiles, st, &c->launches);
+    tk::segment_offsets_u32(c->tile_keys_sorted, n_pairs, toff, n_tiles, st);
     int32_t* pcnt = ensure<int32_t>(c->padded_cnt, n_tiles + 1);
     int32_t* pstart = ensure<int32_t>(c->padded_start, n_tiles + 1);
     tk::launch_padded_counts(toff, n_tiles, pcnt, st);
-    c->launches += 1;
-    tk::scan_exclusive(pcnt, pstart, n_tiles + 1, dscal + 4, c->scratch.p, st, &c->launches);
+    tk::scan_exclusive(pcnt, pstart, n_tiles + 1, dscal + 4, c->scratch.p, st);
     const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
     ensure<tk::EntryChunk>(c->te, padded_cap / tk::kChunk + 1);
     ensure<int32_t>(c->wl, padded_cap * tk::geom_blocks_per_tile(s->tile_size));
@@ -298,7 +291,6 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     mp.color = ptr<double>(c->color);
     mp.out = tile_entries(c);
     tk::launch_materialize(mp, st);
-    c->launches += n_pairs > 0;
     CK_LAUNCH(c);
     c->prepared = true;
     c->prep_key = key;
@@ -338,7 +330,6 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
         PhaseScope phase(c, TK_PHASE_GEOM_FWD);
         tk::launch_geom_fwd(tk::kGeomForward, gp, nblk, st);
     }
-    c->launches += 1;
     CK_LAUNCH(c);
     if (records) {
         c->has_records = true;
@@ -401,7 +392,6 @@ Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
     int64_t* dscal = ensure<int64_t>(c->dscal, 16);
     CK(cudaMemsetAsync(dscal + 5, 0xff, sizeof(int64_t), st));
     tk::launch_first_stale(r.index, slots, n, reinterpret_cast<unsigned long long*>(dscal + 5), st);
-    c->launches += slots > 0;
     tk::copy_words_to_mapped(c->hscal_dev + 5, dscal + 5, 1, st);
     sync(c);
     const uint64_t first = static_cast<uint64_t>(c->hscal[5]);
@@ -427,7 +417,7 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
     tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
     int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-    tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, c->cur, &c->launches);
+    tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, c->cur);
     tk::LongPlan plan{};
     plan.cap_items = tk::long_plan_capacity(slots, n);
     plan.items = ensure<int4>(c->lp_items, plan.cap_items);
@@ -437,7 +427,6 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     plan.queue = cursor;
     plan.qcount = cursor + n + 1;
     tk::launch_long_plan(seg, n, plan, c->cur);
-    c->launches += 1;
     return SlotIndex{seg, svals, wn, plan};
 }
 
@@ -463,7 +452,6 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
         PhaseScope phase(c, TK_PHASE_GEOM_BWD);
         tk::launch_geom_bwd(bp, tk::geom_blocks(f), c->cur);
     }
-    c->launches += 1;
     CK_LAUNCH(c);
     return mid;
 }
@@ -497,7 +485,6 @@ void flush_features(tk_ctx* c) {
     fa.last = ptr<int32_t>(c->f_last);
     fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
     tk::launch_feature_catchup(fa, static_cast<int>(c->step_feat), false, c->cur);
-    c->launches += 1;
     CK_LAUNCH(c);
 }
 
@@ -656,7 +643,7 @@ tk_status tk_join(tk_ctx* c) {
 }
 
 void* tk_get_stream(tk_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
-int64_t tk_kernel_launches(tk_ctx* c) { return c ? c->launches : 0; }
+int64_t tk_kernel_launches(tk_ctx* c) { return c ? tk::launch_count() : 0; }
 
 tk_status tk_host_alloc(size_t bytes, void** out) {
     return guarded([&] { CK(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocDefault)); });
@@ -857,7 +844,6 @@ tk_status tk_render_feature(tk_ctx* c, const tk_topk_view* topk, float* out, int
             PhaseScope phase(c, TK_PHASE_GATHER);
             tk::launch_feature_gather(gp, c->cur);
         }
-        c->launches += P > 0;
         CK_LAUNCH(c);
         c->fout_pixels = P;
         if (out && out_mem != TK_DEVICE) {
@@ -897,7 +883,6 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
             PhaseScope phase(c, TK_PHASE_FBWD);
             tk::launch_feature_bwd(fp, si.plan, st);
         }
-        c->launches += n > 0 ? 3 : 0;
         CK_LAUNCH(c);
         c->fgrad_reader.record(st);  // the next asynchronous grad_feature upload waits only for this
         if (out && out_mem != TK_DEVICE) {
@@ -932,7 +917,7 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
         tk::launch_geom_fwd(tk::kGeomCount, gp, nblk, st);
         ensure_scratch(c, P + 1);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-        tk::scan_exclusive(gp.list_count, off, P + 1, dscal + 6, c->scratch.p, st, &c->launches);
+        tk::scan_exclusive(gp.list_count, off, P + 1, dscal + 6, c->scratch.p, st);
         tk::copy_words_to_mapped(c->hscal_dev + 6, dscal + 6, 1, st);
         sync(c);
         const int64_t total = c->hscal[6];
@@ -944,7 +929,6 @@ tk_status tk_render_feature_full_blend(tk_ctx* c, const tk_pose* pose, const tk_
         float* dst = (out && out_mem == TK_DEVICE) ? out : ensure<float>(c->f_out, P * std::max(c->d, 1));
         tk::ListGatherParams lp{P, off, gp.list_src, gp.list_w, ptr<float>(c->feature), c->d, dst};
         tk::launch_list_gather(lp, st);
-        c->launches += 3;
         CK_LAUNCH(c);
         if (out && out_mem == TK_HOST) {
             copy_out(out, dst, static_cast<size_t>(P) * c->d * sizeof(float), TK_HOST, c);
@@ -1007,7 +991,6 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
             tk::launch_chain(cp, st);
             tk::launch_twist_reduce(cp.twist, n, tpart, tout, st);
         }
-        c->launches += 2;
         CK_LAUNCH(c);
         if (out) {
             if (out->mem != TK_DEVICE) {
@@ -1124,7 +1107,6 @@ tk_status tk_allgather_feature(tk_ctx* c, float* out, int32_t out_mem) {
         DevBuf tmp;
         if (!dst) dst = ensure<float>(tmp, slice * c->nranks);
         tk::launch_interleave(gath, P, c->d, c->nranks, dst, st);
-        c->launches += 1;
         CK_LAUNCH(c);
         if (out && out_mem == TK_HOST) copy_out(out, dst, slice * c->nranks * sizeof(float), TK_HOST, c);
         sync(c);
@@ -1219,7 +1201,6 @@ tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float*
             PhaseScope phase(c, TK_PHASE_GATHER);
             tk::launch_feature_gather(gp, c->cur);
         }
-        c->launches += P > 0;
         CK_LAUNCH(c);
         if (c->comm && c->peer_ipc) {  // stream-ordered rank barrier: every peer's slice has landed
             int32_t* w = ensure<int32_t>(c->peer_word, 1);

@@ -233,7 +233,6 @@ struct tk_ctx {
     std::vector<std::pair<double*, int>> twist_pending;
     int twist_next = 0;
     bool feat_pending = false, geo_pending = false;
-    int64_t launches = 0;
     Profiler prof;
     // scene mirror
     int64_t n = 0;

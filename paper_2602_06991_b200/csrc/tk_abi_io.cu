@@ -68,7 +68,6 @@ tk_status tk_keyframe_load_features(tk_ctx* c, int32_t slot, const char* path) {
         uint8_t* valid = ensure<uint8_t>(k.valid, P);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
         tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, ptr<float>(k.depth), c->cur);
-        c->launches += 1;
         CK_LAUNCH(c);
         if (c->comm) NK(g_nccl.AllReduce(valid, valid, static_cast<size_t>(P), ncclUint8, ncclMax, c->comm, c->cur));
         tk::copy_words_to_mapped(c->hscal_dev + 9, dscal + 9, 1, c->cur);
@@ -121,7 +120,6 @@ tk_status tk_checkpoint_save(tk_ctx* c, const char* path) {
         DevBuf rec;
         float* drec = ensure<float>(rec, n * W);
         tk::launch_splf_pack(splf_view(c), drec, c->cur);
-        c->launches += n > 0;
         CK_LAUNCH(c);
         const size_t body = static_cast<size_t>(n) * W * sizeof(float);
         char* host = nullptr;
@@ -205,7 +203,6 @@ tk_status tk_checkpoint_load(tk_ctx* c, const char* path) {
         c->n = n;
         c->d = static_cast<int32_t>(dim);
         tk::launch_splf_unpack(drec, splf_view(c), c->cur);
-        c->launches += n > 0;
         CK_LAUNCH(c);
         sync(c);
         rec.release();
@@ -269,10 +266,8 @@ tk_status tk_segment_by_query(tk_ctx* c, const float* feature, int64_t n_pixels,
             tk::launch_segment_query(q, st);
             NK(g_nccl.AllReduce(part, part, static_cast<size_t>(P) * (classes + 1), ncclFloat64, ncclSum, c->comm, st));
             tk::launch_query_argmax(part, part + P * classes, P, classes, dl, st);
-            c->launches += 2;
         } else {
             tk::launch_segment_query(q, st);
-            c->launches += 1;
         }
         CK_LAUNCH(c);
         if (labels_mem == TK_HOST) {

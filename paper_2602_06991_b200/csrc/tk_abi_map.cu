@@ -36,7 +36,6 @@ void compact_rows(tk_ctx* c, DevBuf& b, int64_t n, int width, int64_t n_keep, co
     else
         tk::launch_compact_f32(reinterpret_cast<const float*>(b.p), static_cast<float*>(nb.p), keep, pos, n, width,
                                c->cur);
-    c->launches += n > 0;
     CK_LAUNCH(c);
     CK(cudaStreamSynchronize(c->cur));
     b = std::move(nb);
@@ -148,7 +147,6 @@ tk_status tk_keyframe_set(tk_ctx* c, int32_t slot, const tk_pose* pose, const tk
         uint8_t* valid = ensure<uint8_t>(k.valid, P);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
         tk::launch_gt_valid(feat, P, k.d, valid, dscal + 9, dep, c->cur);
-        c->launches += 1;
         CK_LAUNCH(c);
         if (c->comm)  // D-sharded: a pixel's keyframe row is valid if any shard's channels are non-zero
             NK(g_nccl.AllReduce(valid, valid, static_cast<size_t>(P), ncclUint8, ncclMax, c->comm, c->cur));
@@ -275,7 +273,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             have_si = true;
             tk::launch_active_rows(early_si.seg, n, ensure<int32_t>(c->f_active, n), ensure<int32_t>(c->f_active_n, 1),
                                    st);
-            c->launches += n > 0;
             tk::FeatAdamParams fa{};
             fa.active = ptr<int32_t>(c->f_active);
             fa.n_active = ptr<int32_t>(c->f_active_n);
@@ -289,7 +286,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
             if (c->feat_stale) {
                 tk::launch_feature_catchup(fa, static_cast<int>(kstep - 1), true, st);
-                c->launches += 1;
             }
         } else if (feature_step && d > 0) {
             flush_features(c);  // an eager step needs every row at step k-1 (step_feat is still k-1)
@@ -299,7 +295,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             CK(cudaMemsetAsync(partial, 0, tk::kLossBlocks * tk::kLossSlots * sizeof(double), st));
             tk::launch_topk_stats(ptr<int32_t>(c->o_index), ptr<uint8_t>(c->o_count), P, f.k,
                                   ptr<int32_t>(c->stat_count), st);
-            c->launches += 1;
             // compute_losses (mapper.cpp:176, losses.cpp:22-133)
             tk::ColorLossParams lp{};
             lp.w = f.width;
@@ -334,7 +329,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             lp.grad_color = gc;
             lp.grad_depth = gd;
             lp.partial = partial;
-            tk::launch_color_loss(lp, st, &c->launches);
+            tk::launch_color_loss(lp, st);
             if (feature_step) {
                 tk::FeatLossParams fl{};
                 fl.width = f.width;
@@ -350,7 +345,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 fl.signs = signs;
                 fl.partial = partial;
                 tk::launch_feature_loss(fl, st);
-                c->launches += 1;
             }
             if (sharded)  // feature partials differ per shard; colour / depth rows are replicas
                 NK(g_nccl.AllReduce(partial, partial, tk::kLossBlocks * tk::kLossSlots, ncclFloat64, ncclSum, c->comm,
@@ -374,7 +368,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             fp.values = values;
             fp.feat_scale = fscale;
             tk::launch_loss_finalize(fp, st);
-            c->launches += 1;
             CK_LAUNCH(c);
         }
         tk::copy_words_to_mapped(c->hvals_dev, values, 3, st);
@@ -426,7 +419,6 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ga.g[3] = cp.g_opacity_logit;
             ga.g[4] = cp.g_color;
             tk::launch_geo_adam(ga, n, st);
-            c->launches += n > 0 ? 2 : 0;
             CK_LAUNCH(c);
             if (feature_step && d > 0) {  // mapper.cpp:239-252
                 c->step_feat = kstep;
@@ -464,12 +456,10 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
                 if (lazy_feat && !tk::feature_adam_lazy_ok(fa)) fail(TK_ERR_STATE, "lazy feature Adam: bad layout");
                 tk::launch_feature_adam(fa, st);
                 if (fa.lazy) c->feat_stale = true;
-                c->launches += n > 0 ? 3 : 0;
                 if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
                     NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
                                         st));
                     tk::launch_feature_renorm(ptr<float>(c->feature), fa.row_ss, n, d, st);
-                    c->launches += 1;
                 }
                 CK_LAUNCH(c);
             }
@@ -578,11 +568,10 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
         tk::launch_insert_flags(dist, ns, tau, flag, flag32, st);
         ensure_scratch(c, ns + 1);
         int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-        tk::scan_exclusive(flag32, slot, ns, dscal + 10, c->scratch.p, st, &c->launches);
+        tk::scan_exclusive(flag32, slot, ns, dscal + 10, c->scratch.p, st);
         tk::copy_words_to_mapped(c->hscal_dev + 10, dscal + 10, 1, st);
         sync(c);
         const int64_t total = c->hscal[10];
-        c->launches += 1;
         if (total > 0) {
             if (c->d == 0 && feat && (c->n == 0 || !c->has_features)) c->d = src->d;  // mapper.cpp:40-41
             const int64_t n0 = c->n, n1 = n0 + total;
@@ -620,7 +609,6 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
                 c->has_features = true;
             }
             tk::launch_insert_fill(ip, st);
-            c->launches += 1;
             CK_LAUNCH(c);
             if (c->opt_ready && c->opt_n == n0) {  // OptimizerState::extend (optimizer.cpp:29-36)
                 const int dims[5] = {3, 3, 4, 1, 3};
@@ -682,8 +670,7 @@ tk_status tk_prune_map(tk_ctx* c, double keep_ratio, uint64_t seed, int32_t thre
             tk::launch_keep_flags(drem, nr, n, keep, st);
             ensure_scratch(c, n + 1);
             int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-            tk::scan_exclusive(keep, pos, n, dscal + 11, c->scratch.p, st, &c->launches);
-            c->launches += 2;
+            tk::scan_exclusive(keep, pos, n, dscal + 11, c->scratch.p, st);
             const int64_t nk = n - nr;
             compact_rows<double>(c, c->mean, n, 3, nk, keep, pos);
             compact_rows<double>(c, c->log_scale, n, 3, nk, keep, pos);
