@@ -287,8 +287,13 @@ def main_gpu(args, cfg):
         uid = (C.c_uint8 * 128)(*tkdist.broadcast_bytes(dist, bytes(uid) if rank == 0 else None, 128))
         N.check(lib.tk_comm_init(ctx, uid, world, rank, D))
         gather_mode = args.gather
-        if gather_mode == "p2p" and lib.tk_comm_p2p_setup(ctx, P) != N.TK_OK:  # needs CUDA IPC + P2P
-            gather_mode = "nccl (p2p setup failed: " + lib.tk_last_error().decode() + ")"
+        if gather_mode == "p2p":  # needs CUDA IPC + P2P; every rank must take the same path
+            ok = lib.tk_comm_p2p_setup(ctx, P) == N.TK_OK
+            why = "" if ok else lib.tk_last_error().decode()
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                gather_mode = "nccl (p2p setup failed on a rank" + (f": {why}" if why else "") + ")"
     else:
         gather_mode = None
 
