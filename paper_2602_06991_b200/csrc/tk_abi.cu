@@ -1146,10 +1146,20 @@ tk_status tk_comm_p2p_setup(tk_ctx* c, int64_t n_pixels) {
         on_main(c);
         sync(c);
         release_peers(c);
-        float* own = ensure<float>(c->peer_own, static_cast<size_t>(std::max<int64_t>(n_pixels, 1)) * c->d_total);
-        // every rank's IPC handle to every rank (NCCL all-gather of the 64-byte handles)
+        // every rank's IPC handle to every rank (NCCL all-gather of the 64-byte handles).  A rank
+        // that cannot export its buffer still joins the all-gather (with a zero handle), so every
+        // rank sees the failure and returns the same error instead of hanging in the collective.
         cudaIpcMemHandle_t mine;
-        CK(cudaIpcGetMemHandle(&mine, own));
+        std::memset(&mine, 0, sizeof(mine));
+        float* own = nullptr;
+        std::string export_error;
+        try {
+            own = ensure<float>(c->peer_own, static_cast<size_t>(std::max<int64_t>(n_pixels, 1)) * c->d_total);
+            CK(cudaIpcGetMemHandle(&mine, own));
+        } catch (const TkError& e) {
+            export_error = e.msg;
+            std::memset(&mine, 0, sizeof(mine));
+        }
         static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
         DevBuf hb;
         uint8_t* dh = ensure<uint8_t>(hb, 64 * (c->nranks + 1));
@@ -1159,6 +1169,13 @@ tk_status tk_comm_p2p_setup(tk_ctx* c, int64_t n_pixels) {
         CK(cudaMemcpyAsync(all.data(), dh, 64 * c->nranks, cudaMemcpyDeviceToHost, c->cur));
         sync(c);
         hb.release();
+        static const cudaIpcMemHandle_t zero{};
+        for (int r = 0; r < c->nranks; ++r)
+            if (std::memcmp(&all[r], &zero, sizeof(zero)) == 0) {
+                c->peer_own.release();
+                fail(TK_ERR_CUDA, "tk_comm_p2p_setup: rank " + std::to_string(r) + " could not export its buffer" +
+                                      (export_error.empty() ? std::string() : " (" + export_error + ")"));
+            }
         c->peer_ipc = true;
         c->peer_n = c->nranks;
         c->peer_rank = c->rank;
