@@ -161,22 +161,30 @@ __global__ void __launch_bounds__(kThreads) k_ssim_stats(ColorLossParams p) {
 // (losses.cpp:128-130).  Each thread owns a 1 x 4 pixel column of a 16 x 64 tile, so one
 // shared-memory window read serves up to four pixels; (inv_count * wgt) comes from a 11 x 11
 // table computed like the reference's product.
-constexpr int kCX = 16, kCY = 64, kCR = 4;
+#ifndef TK_CL_KCR
+#define TK_CL_KCR 4
+#endif
+constexpr int kCX = 16, kCR = TK_CL_KCR, kCY = (kThreads / kCX) * kCR;
 constexpr int kCWX = kCX + kHalo, kCWY = kCY + kHalo;
-constexpr size_t kColorSmem = (5 * kCWY * kCWX + kSsimWin * kSsimWin) * sizeof(double);
+// weight table rows ky = -(kCR-1) .. kHalo+kCR-1: rows outside 0..kHalo hold zeros, so taps of a
+// window that does not cover the pixel add +-0 (no branch; sums unchanged bit for bit)
+constexpr int kTwRows = kSsimWin + 2 * (kCR - 1);
+constexpr size_t kColorSmem = (5 * kCWY * kCWX + kTwRows * kSsimWin) * sizeof(double);
 
 __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
     extern __shared__ double smem[];
     double* sw = smem;                        // [5][kCWY][kCWX]
-    double* tw = smem + 5 * kCWY * kCWX;      // [11][11] inv_count * (kern[ky] * kern[kx])
+    double* tw = smem + 5 * kCWY * kCWX;      // [kTwRows][11] inv_count * (kern[ky] * kern[kx]), zero rows around
     const int ow = p.w - kHalo, oh = p.h - kHalo;
     const int64_t plane_w = static_cast<int64_t>(oh > 0 ? oh : 0) * (ow > 0 ? ow : 0);
     const int tx = (p.w + kCX - 1) / kCX, ty = (p.h + kCY - 1) / kCY;
     const int lx = threadIdx.x % kCX, lr = threadIdx.x / kCX;
     const double scale = -0.5 * p.lambda1;
     const double fold_d = p.lambda_geo * p.lambda2;
-    for (int e = threadIdx.x; e < kSsimWin * kSsimWin; e += kThreads)
-        tw[e] = p.inv_count * (p.kern[e / kSsimWin] * p.kern[e % kSsimWin]);
+    for (int e = threadIdx.x; e < kTwRows * kSsimWin; e += kThreads) {
+        const int ky = e / kSsimWin - (kCR - 1), kx = e % kSsimWin;
+        tw[e] = ky >= 0 && ky <= kHalo ? p.inv_count * (p.kern[ky] * p.kern[kx]) : 0.0;
+    }
     double v[2] = {0.0, 0.0};
     for (int tile = blockIdx.x; tile < tx * ty; tile += gridDim.x) {
         const int x0 = (tile % tx) * kCX, y0 = (tile / tx) * kCY;
@@ -222,8 +230,7 @@ __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
 #pragma unroll
                         for (int j = 0; j < kCR; ++j) {
                             const int ky = ys + j - wy;
-                            if (ky < 0 || ky > kHalo) continue;
-                            g[c][j] += tw[ky * kSsimWin + kx] * (d_mu + dv2 * (av[j] - mu_a) + d_cov * (bv[j] - mu_b));
+                            g[c][j] += tw[(ky + kCR - 1) * kSsimWin + kx] * (d_mu + dv2 * (av[j] - mu_a) + d_cov * (bv[j] - mu_b));
                         }
                     }
                 }
