@@ -250,7 +250,9 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ast.one_m_beta2 = static_cast<float>(1.0 - cfg->beta2);
             ast.inv_bc1 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta1, static_cast<double>(kstep))));
             ast.inv_bc2 = static_cast<float>(1.0 / (1.0 - std::pow(cfg->beta2, static_cast<double>(kstep))));
-            if (c->f_tab_host.size() != static_cast<size_t>(kstep)) fail(TK_ERR_STATE, "feature step table out of sync");
+            // a step that failed after recording its constants left an extra entry: drop it
+            if (c->f_tab_host.size() < static_cast<size_t>(kstep)) fail(TK_ERR_STATE, "feature step table out of sync");
+            c->f_tab_host.resize(static_cast<size_t>(kstep));
             c->f_tab_host.push_back(ast);
             const int64_t cap = static_cast<int64_t>(c->f_tab.bytes / sizeof(tk::AdamStepParams));
             tk::AdamStepParams* tab = cap > kstep ? ptr<tk::AdamStepParams>(c->f_tab)
