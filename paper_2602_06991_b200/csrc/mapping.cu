@@ -627,8 +627,22 @@ __device__ __forceinline__ float warp_sum(float s) {
 #endif
 // Sum over records [r0, r1) of w_j * sign(F - F_gt)[px_j] for the channel pass at `base`
 // (4 float4 per lane), records in slot order.
+// Sign-code table: byte b of a sign word (four 2-bit codes, 01 = +1, 10 = -1, bit 1 dominating
+// like signed_w) -> the four channel factors.  acc + fma(w, +-1 or 0) rounds exactly like the
+// acc + (+-w or +0) of signed_w for a finite w, so the sums are unchanged bit for bit.
+__device__ __forceinline__ void init_sign_table(float4* tab) {
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = (b >> (2 * i + 1)) & 1 ? -1.0f : ((b >> (2 * i)) & 1 ? 1.0f : 0.0f);
+        tab[b] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    __syncthreads();
+}
+
+template <int GROUP = SIGN_GROUP>
 __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int r1, int base, int lane, float scale,
-                                            float4 (&acc)[4]) {
+                                            float4 (&acc)[4], const float4* __restrict__ stab) {
     const int d4 = p.d >> 2, wpp = (p.d + 15) >> 4;
     const uint32_t* __restrict__ signs = p.signs;
     for (int r = r0; r < r1; r += 32) {
@@ -642,7 +656,7 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
         }
         // kGroup records' sign words are loaded before any is summed (the loads overlap); the
         // sums still run record by record, so the result is that of the sequential sweep
-        constexpr int kGroup = SIGN_GROUP;
+        constexpr int kGroup = GROUP;
         for (int j = 0; j < nr; j += kGroup) {
             const uint32_t* srow[kGroup];
             float wj[kGroup];
@@ -665,12 +679,23 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
                     for (int q = lane; q < wpp; q += 32) any |= srow[t][q] != 0u;
                     if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
                 }
+                if (isfinite(wj[t])) {
 #pragma unroll
-                for (int m = 0; m < 4; ++m) {
-                    acc[m].x += signed_w(bw[t][m], 0, wj[t]);
-                    acc[m].y += signed_w(bw[t][m], 2, wj[t]);
-                    acc[m].z += signed_w(bw[t][m], 4, wj[t]);
-                    acc[m].w += signed_w(bw[t][m], 6, wj[t]);
+                    for (int m = 0; m < 4; ++m) {
+                        const float4 f = stab[bw[t][m] & 0xffu];
+                        acc[m].x = fmaf(wj[t], f.x, acc[m].x);
+                        acc[m].y = fmaf(wj[t], f.y, acc[m].y);
+                        acc[m].z = fmaf(wj[t], f.z, acc[m].z);
+                        acc[m].w = fmaf(wj[t], f.w, acc[m].w);
+                    }
+                } else {  // 0/0 weights of live rows: signed_w keeps the zero codes at +0
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        acc[m].x += signed_w(bw[t][m], 0, wj[t]);
+                        acc[m].y += signed_w(bw[t][m], 2, wj[t]);
+                        acc[m].z += signed_w(bw[t][m], 4, wj[t]);
+                        acc[m].w += signed_w(bw[t][m], 6, wj[t]);
+                    }
                 }
             }
         }
@@ -684,6 +709,8 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
 // chunk partials (k_feature_adam_chunks) are added in chunk order.
 template <bool LONG, bool LAZY>
 __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
+    __shared__ float4 stab[256];
+    init_sign_table(stab);
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -716,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (!LONG) {
-                accum_signs(p, r0, r1, base, lane, scale, acc);
+                accum_signs(p, r0, r1, base, lane, scale, acc, stab);
             } else {
                 for (int c = 0; c < lg.z; ++c) {
                     const float4* part = reinterpret_cast<const float4*>(plan.partial + static_cast<int64_t>(lg.y + c) * D);
@@ -782,13 +809,46 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
             process_row(lg.x, p.seg[lg.x], p.seg[lg.x + 1], lg, false, fk, mk, vk);
         }
     } else if (LAZY) {
-        // only the rows with records (the active list); the others wait for k_feature_catchup
+        // only the rows with records (the active list): their sign sums were gathered by
+        // k_active_grad into p.grad, so the Adam pass is a plain stream (no record sweep here)
         const int na = *p.n_active;
         for (int64_t wi = warp_id; wi < na; wi += nw) {
             const int64_t g = p.active[wi];
             const int r0 = p.seg[g], r1 = p.seg[g + 1];
             if (r1 - r0 > kLongSeg) continue;
-            process_row(g, r0, r1, make_int4(0, 0, 0, 0), false, fk, mk, vk);
+            float4* __restrict__ frow = reinterpret_cast<float4*>(p.feat + g * D);
+            float4* __restrict__ mrow = reinterpret_cast<float4*>(p.m + g * D);
+            float4* __restrict__ vrow = reinterpret_cast<float4*>(p.v + g * D);
+            const float4* __restrict__ grow = reinterpret_cast<const float4*>(p.grad + wi * D);
+            float4 acc[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = m * 32 + lane;
+                if (q < d4) {
+                    fk[m] = __ldcs(frow + q);
+                    mk[m] = __ldcs(mrow + q);
+                    vk[m] = __ldcs(vrow + q);
+                    acc[m] = __ldcs(grow + q);
+                }
+            }
+            if (lane == 0) p.last[g] = p.cur;
+            float ss = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = m * 32 + lane;
+                if (q >= d4) continue;
+                ss += adam_quad(fk[m], mk[m], vk[m], acc[m], scale, p.st);
+                __stcs(mrow + q, mk[m]);
+                __stcs(vrow + q, vk[m]);
+            }
+            const float ssum = warp_sum(ss);
+            const bool renorm = ssum > 1e-24f;  // norm > 1e-12 (mapper.cpp:249)
+            const float inv = renorm ? rsqrtf(ssum) : 1.0f;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int q = m * 32 + lane;
+                if (q < d4) __stcs(frow + q, renorm ? scale4(fk[m], inv) : fk[m]);
+            }
         }
     } else {
         for (int64_t g = warp_id; g < p.n; g += nw) {
@@ -809,6 +869,34 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
             const int r0 = p.seg[g], r1 = p.seg[g + 1];
             if (r1 - r0 > kLongSeg) continue;
             process_row(g, r0, r1, make_int4(0, 0, 0, 0), true, fk, mk, vk);
+        }
+    }
+}
+
+// Lazy step, phase 1: the sign sums of every active row with at most kLongSeg records, in slot
+// order (accum_signs, the eager kernel's sweep), into p.grad[active position].  Only the sums are
+// held per lane, so twice the warps of the Adam kernel are resident to hide the sweep's latency.
+__global__ void __launch_bounds__(kThreads) k_active_grad(FeatAdamParams p) {
+    __shared__ float4 stab[256];
+    init_sign_table(stab);
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d, d4 = D >> 2;
+    const float scale = *p.scale;
+    const int na = *p.n_active;
+    for (int64_t wi = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; wi < na; wi += nw) {
+        const int64_t g = p.active[wi];
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        if (r1 - r0 > kLongSeg) continue;
+        float4 acc[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+        accum_signs(p, r0, r1, 0, lane, scale, acc, stab);
+        float4* __restrict__ grow = reinterpret_cast<float4*>(p.grad + wi * D);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const int q = m * 32 + lane;
+            if (q < d4) grow[q] = acc[m];
         }
     }
 }
@@ -901,6 +989,8 @@ __global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t value) {
 
 // One warp per chunk of a long segment: its sign sums into the plan's partial rows.
 __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams p, LongPlan plan) {
+    __shared__ float4 stab[256];
+    init_sign_table(stab);
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -913,7 +1003,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum_signs(p, r0, r1, base, lane, scale, acc);
+            accum_signs(p, r0, r1, base, lane, scale, acc, stab);
             float4* dst = reinterpret_cast<float4*>(plan.partial + static_cast<int64_t>(item.z) * D);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -1071,8 +1161,13 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
     const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
     if (vec) {
-        if (p.lazy) k_feature_adam_vec<false, true><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
-        else k_feature_adam_vec<false, false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        if (p.lazy) {
+            k_active_grad<<<148 * 32, kThreads, 0, st>>>(p);
+            dbg_launch("k_active_grad", st);
+            k_feature_adam_vec<false, true><<<148 * 16, kThreads, 0, st>>>(p, p.plan);
+        } else {
+            k_feature_adam_vec<false, false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+        }
         dbg_launch("k_feature_adam_vec", st);
         k_feature_adam_chunks<<<148 * 8, kThreads, 0, st>>>(p, p.plan);
         dbg_launch("k_feature_adam_chunks", st);
@@ -1086,6 +1181,7 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
 
 bool feature_adam_lazy_ok(const FeatAdamParams& p) {
     return p.d > 0 && (p.d % 4) == 0 && p.d <= 512 && !p.row_ss && p.last && p.tab && p.active && p.n_active &&
+           p.grad && p.cap_active > 0 &&
            (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 &&
            (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
 }

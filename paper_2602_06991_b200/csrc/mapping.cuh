@@ -82,6 +82,8 @@ struct FeatAdamParams {
     const AdamStepParams* tab = nullptr;
     const int32_t* active = nullptr;    // lazy: the rows with records (any order), *n_active of them
     const int32_t* n_active = nullptr;
+    float* grad = nullptr;              // lazy: [cap_active][D] sign sums of the active rows (scratch)
+    int64_t cap_active = 0;
 };
 
 // active[0 .. *n_active) = the rows g with seg[g + 1] > seg[g] (unordered)

@@ -298,7 +298,7 @@ struct tk_ctx {
     DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
     // lazy feature Adam: steps applied per row, every step's constants (host + device, 1-based);
     // feat_stale: some rows lag the step count (replayed by flush_features before features are read)
-    DevBuf f_last, f_tab, f_active, f_active_n;
+    DevBuf f_last, f_tab, f_active, f_active_n, f_active_grad;
     std::vector<tk::AdamStepParams> f_tab_host;
     bool feat_stale = false;
     DevBuf row_ss;                                        // D-sharded partial row norms

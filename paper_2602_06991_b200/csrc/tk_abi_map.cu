@@ -374,6 +374,58 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
         }
         tk::copy_words_to_mapped(c->hvals_dev, values, 3, st);
         c->has_values = true;
+        // the feature half first (mapper.cpp:239-252; independent of the geometry half): its
+        // sign image was just written by the loss and is still in L2 for the record sweep
+        {
+            PhaseScope phase(c, TK_PHASE_ADAM);
+            if (feature_step && d > 0) {  // mapper.cpp:239-252
+                c->step_feat = kstep;
+                Records r;
+                r.w = f.width;
+                r.h = f.height;
+                r.k = f.k;
+                r.index = ptr<int32_t>(c->o_index);
+                r.weight = ptr<double>(c->o_weight);
+                r.count = ptr<uint8_t>(c->o_count);
+                const SlotIndex si = have_si ? early_si : build_slot_index(c, r);
+                tk::FeatAdamParams fa{};
+                fa.n = n;
+                fa.k = f.k;
+                fa.d = d;
+                fa.seg = si.seg;
+                fa.slots = si.slots;
+                fa.wnorm = si.wnorm;
+                fa.signs = signs;
+                fa.scale = fscale;
+                fa.feat = ptr<float>(c->feature);
+                fa.m = ptr<float>(c->fm);
+                fa.v = ptr<float>(c->fv);
+                fa.st = ast;
+                fa.plan = si.plan;
+                if (sharded) fa.row_ss = ensure<float>(c->row_ss, n);
+                fa.last = ptr<int32_t>(c->f_last);
+                fa.cur = static_cast<int>(kstep);
+                fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
+                fa.lazy = lazy_feat ? 1 : 0;
+                if (lazy_feat) {
+                    fa.active = ptr<int32_t>(c->f_active);
+                    fa.n_active = ptr<int32_t>(c->f_active_n);
+                    // active rows <= rows with records <= min(n, record slots)
+                    const int64_t cap = std::min<int64_t>(n, static_cast<int64_t>(P) * f.k);
+                    fa.grad = ensure<float>(c->f_active_grad, std::max<int64_t>(cap, 1) * d);
+                    fa.cap_active = cap;
+                }
+                if (lazy_feat && !tk::feature_adam_lazy_ok(fa)) fail(TK_ERR_STATE, "lazy feature Adam: bad layout");
+                tk::launch_feature_adam(fa, st);
+                if (fa.lazy) c->feat_stale = true;
+                if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
+                    NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
+                                        st));
+                    tk::launch_feature_renorm(ptr<float>(c->feature), fa.row_ss, n, d, st);
+                }
+                CK_LAUNCH(c);
+            }
+        }
         // backward_geometric (mapper.cpp:179-180) on this forward
         double* mid = geom_sweep(c, f, gc, gd);
         if (sharded)  // replicas stay bit-identical: one all-reduced geometry gradient on every shard
@@ -422,49 +474,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ga.g[4] = cp.g_color;
             tk::launch_geo_adam(ga, n, st);
             CK_LAUNCH(c);
-            if (feature_step && d > 0) {  // mapper.cpp:239-252
-                c->step_feat = kstep;
-                Records r;
-                r.w = f.width;
-                r.h = f.height;
-                r.k = f.k;
-                r.index = ptr<int32_t>(c->o_index);
-                r.weight = ptr<double>(c->o_weight);
-                r.count = ptr<uint8_t>(c->o_count);
-                const SlotIndex si = have_si ? early_si : build_slot_index(c, r);
-                tk::FeatAdamParams fa{};
-                fa.n = n;
-                fa.k = f.k;
-                fa.d = d;
-                fa.seg = si.seg;
-                fa.slots = si.slots;
-                fa.wnorm = si.wnorm;
-                fa.signs = signs;
-                fa.scale = fscale;
-                fa.feat = ptr<float>(c->feature);
-                fa.m = ptr<float>(c->fm);
-                fa.v = ptr<float>(c->fv);
-                fa.st = ast;
-                fa.plan = si.plan;
-                if (sharded) fa.row_ss = ensure<float>(c->row_ss, n);
-                fa.last = ptr<int32_t>(c->f_last);
-                fa.cur = static_cast<int>(kstep);
-                fa.tab = ptr<tk::AdamStepParams>(c->f_tab);
-                fa.lazy = lazy_feat ? 1 : 0;
-                if (lazy_feat) {
-                    fa.active = ptr<int32_t>(c->f_active);
-                    fa.n_active = ptr<int32_t>(c->f_active_n);
-                }
-                if (lazy_feat && !tk::feature_adam_lazy_ok(fa)) fail(TK_ERR_STATE, "lazy feature Adam: bad layout");
-                tk::launch_feature_adam(fa, st);
-                if (fa.lazy) c->feat_stale = true;
-                if (sharded) {  // mapper.cpp:249: the norm of the whole row, over every shard
-                    NK(g_nccl.AllReduce(fa.row_ss, fa.row_ss, static_cast<size_t>(n), ncclFloat32, ncclSum, c->comm,
-                                        st));
-                    tk::launch_feature_renorm(ptr<float>(c->feature), fa.row_ss, n, d, st);
-                }
-                CK_LAUNCH(c);
-            }
+
         }
         // the scene changed: the next render re-projects (records keep the pre-step snapshot)
         c->scene_version += 1;
