@@ -627,22 +627,9 @@ __device__ __forceinline__ float warp_sum(float s) {
 #endif
 // Sum over records [r0, r1) of w_j * sign(F - F_gt)[px_j] for the channel pass at `base`
 // (4 float4 per lane), records in slot order.
-// Sign-code table: byte b of a sign word (four 2-bit codes, 01 = +1, 10 = -1, bit 1 dominating
-// like signed_w) -> the four channel factors.  acc + fma(w, +-1 or 0) rounds exactly like the
-// acc + (+-w or +0) of signed_w for a finite w, so the sums are unchanged bit for bit.
-__device__ __forceinline__ void init_sign_table(float4* tab) {
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
-        float v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = (b >> (2 * i + 1)) & 1 ? -1.0f : ((b >> (2 * i)) & 1 ? 1.0f : 0.0f);
-        tab[b] = make_float4(v[0], v[1], v[2], v[3]);
-    }
-    __syncthreads();
-}
-
 template <int GROUP = SIGN_GROUP>
 __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int r1, int base, int lane, float scale,
-                                            float4 (&acc)[4], const float4* __restrict__ stab) {
+                                            float4 (&acc)[4]) {
     const int d4 = p.d >> 2, wpp = (p.d + 15) >> 4;
     const uint32_t* __restrict__ signs = p.signs;
     for (int r = r0; r < r1; r += 32) {
@@ -679,23 +666,12 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
                     for (int q = lane; q < wpp; q += 32) any |= srow[t][q] != 0u;
                     if (!__any_sync(0xffffffffu, any) || scale == 0.0f) continue;
                 }
-                if (isfinite(wj[t])) {
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        const float4 f = stab[bw[t][m] & 0xffu];
-                        acc[m].x = fmaf(wj[t], f.x, acc[m].x);
-                        acc[m].y = fmaf(wj[t], f.y, acc[m].y);
-                        acc[m].z = fmaf(wj[t], f.z, acc[m].z);
-                        acc[m].w = fmaf(wj[t], f.w, acc[m].w);
-                    }
-                } else {  // 0/0 weights of live rows: signed_w keeps the zero codes at +0
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) {
-                        acc[m].x += signed_w(bw[t][m], 0, wj[t]);
-                        acc[m].y += signed_w(bw[t][m], 2, wj[t]);
-                        acc[m].z += signed_w(bw[t][m], 4, wj[t]);
-                        acc[m].w += signed_w(bw[t][m], 6, wj[t]);
-                    }
+                for (int m = 0; m < 4; ++m) {
+                    acc[m].x += signed_w(bw[t][m], 0, wj[t]);
+                    acc[m].y += signed_w(bw[t][m], 2, wj[t]);
+                    acc[m].z += signed_w(bw[t][m], 4, wj[t]);
+                    acc[m].w += signed_w(bw[t][m], 6, wj[t]);
                 }
             }
         }
@@ -709,8 +685,6 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
 // chunk partials (k_feature_adam_chunks) are added in chunk order.
 template <bool LONG, bool LAZY>
 __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
-    __shared__ float4 stab[256];
-    init_sign_table(stab);
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -743,7 +717,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (!LONG) {
-                accum_signs(p, r0, r1, base, lane, scale, acc, stab);
+                accum_signs(p, r0, r1, base, lane, scale, acc);
             } else {
                 for (int c = 0; c < lg.z; ++c) {
                     const float4* part = reinterpret_cast<const float4*>(plan.partial + static_cast<int64_t>(lg.y + c) * D);
@@ -877,8 +851,6 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
 // order (accum_signs, the eager kernel's sweep), into p.grad[active position].  Only the sums are
 // held per lane, so twice the warps of the Adam kernel are resident to hide the sweep's latency.
 __global__ void __launch_bounds__(kThreads) k_active_grad(FeatAdamParams p) {
-    __shared__ float4 stab[256];
-    init_sign_table(stab);
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -891,7 +863,7 @@ __global__ void __launch_bounds__(kThreads) k_active_grad(FeatAdamParams p) {
         float4 acc[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-        accum_signs(p, r0, r1, 0, lane, scale, acc, stab);
+        accum_signs(p, r0, r1, 0, lane, scale, acc);
         float4* __restrict__ grow = reinterpret_cast<float4*>(p.grad + wi * D);
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -989,8 +961,6 @@ __global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t value) {
 
 // One warp per chunk of a long segment: its sign sums into the plan's partial rows.
 __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams p, LongPlan plan) {
-    __shared__ float4 stab[256];
-    init_sign_table(stab);
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -1003,7 +973,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum_signs(p, r0, r1, base, lane, scale, acc, stab);
+            accum_signs(p, r0, r1, base, lane, scale, acc);
             float4* dst = reinterpret_cast<float4*>(plan.partial + static_cast<int64_t>(item.z) * D);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
