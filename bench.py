@@ -12,11 +12,13 @@ Nothing is cached across steps (tk_invalidate each step); inputs are larger than
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c1|c5] [--impl ours|reference]
 
-Under torchrun (N > 1) the default is keyframe-parallel weak scaling (config 4's 8-keyframe
-batch): rank r renders orbit keyframe r with all D channels, no data-path collective.  With
---mode dshard the feature dimension is sharded D/N per GPU: every rank
-recomputes the integer Top-K records, gathers/scatters its channel slice, and the rendered map
-is all-gathered with NCCL (tk_allgather_feature).  Rank 0 prints one JSON line.
+Under torchrun (N > 1) the default is config 4's partitioning (BASELINE.json north_star, SURVEY.md
+§8e): the feature dimension is sharded D/N per GPU, every rank recomputes the integer Top-K records,
+gathers/scatters its channel slice, and the rendered map is all-gathered over NVLink (render_feature
+fused with peer stores, or NCCL with --gather nccl) -- strong scaling of one frame.  A secondary
+"keyframe_parallel" block times config 4's 8-keyframe batch as independent replicas (rank r renders
+orbit keyframe r with all D channels; weak scaling, aggregate frames/s).  --mode keyframe makes that
+the headline instead.  Rank 0 prints one JSON line.
 
 The line also carries "mapping": one mapping iteration (tk_optimize_step: render, losses with
 D-SSIM and the masked feature L1, backward, Adam over every group, features on every 5th
@@ -48,6 +50,24 @@ CONFIGS = {
 }
 
 
+def bench_config(cfg, world, mode, gather):
+    """The workload's `config` object, identical for both arms (the reference arm runs the same
+    scene, pose, seeds and settings on the host)."""
+    D = cfg["d"]
+    dshard = world > 1 and mode == "dshard"
+    P = cfg["w"] * cfg["h"]
+    if dshard:
+        par = (f"feature-dim shard d{world}: D/{world} channels per GPU, Top-K recomputed per GPU, F all-gathered "
+               + ("by render_feature fused with NVLink peer stores" if gather == "p2p" else "with NCCL"))
+    elif world > 1:
+        par = f"keyframe-parallel x{world}: rank r renders orbit keyframe r, all D"
+    else:
+        par = "single GPU"
+    return {"workload": cfg["label"], "gaussians": cfg["n"], "width": cfg["w"], "height": cfg["h"], "feature_dim": D,
+            "top_k": cfg["k"], "feature_dim_per_gpu": D // world if dshard else D, "parallelism": par,
+            "l2": "inputs larger than L2 (features %.2f GB, F %.2f GB)" % (cfg["n"] * D * 4 / 1e9, P * D * 4 / 1e9)}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -61,7 +81,8 @@ def ncu_traffic(kernel_prefix: str):
     """DRAM bytes (read + write) per launch of a kernel from the latest committed ncu --set full
     capture (profiles/*_ncu_traffic.json, written by scripts/profile_summary.py), else None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")), key=os.path.getmtime)
+    # newest capture by name (r01b < r01i < r02a ...): checkout mtimes carry no order
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
     for f in reversed(files):
         try:
             t = json.load(open(f))
@@ -152,7 +173,7 @@ import json, sys, time, os
 sys.path.insert(0, {root!r}); sys.path.insert(0, os.path.join({root!r}, "tests"))
 import numpy as np, ctypes as C
 import _oracle as O
-from paper_2602_06991_b200 import synth
+import scenegen as synth
 from paper_2602_06991_b200.types import RenderSettings
 cfg = {cfg!r}
 scene, cam, pose, _ = synth.bench_scene(cfg["n"], cfg["w"], cfg["h"], cfg["d"])
@@ -160,8 +181,7 @@ scene.feature = synth.unit_features(scene.size(), cfg["d"], 7, dtype=np.float64)
 s = RenderSettings(top_k=cfg["k"])
 P = cfg["w"] * cfg["h"]
 gf = np.empty(P * cfg["d"], np.float32)
-from paper_2602_06991_b200 import _native as N
-N.synth_lib().tk_synth_hash_fill_f32(gf.size, 11, -1.0, 1.0, gf.ctypes.data)
+synth.N.synth_lib().tk_synth_hash_fill_f32(gf.size, 11, -1.0, 1.0, gf.ctypes.data)
 gf = gf.astype(np.float64)
 gc = synth.uniform_image((cfg["h"], cfg["w"], 3), 12)
 gd = synth.uniform_image((cfg["h"], cfg["w"]), 13)
@@ -171,6 +191,9 @@ threads = L.orc_max_threads()
 times = np.zeros(6)
 budget, frames, total = {budget!r}, 0, 0.0
 best = None
+for _ in range({warmup}):
+    L.orc_time_frame(om.h, C.byref(O.pose_c(pose)), C.byref(O.cam_c(cam)), C.byref(O.settings_c(s)),
+                     gf.ctypes.data, gc.ctypes.data, gd.ctypes.data, 1, {fthreads}, times.ctypes.data)
 while True:
     L.orc_time_frame(om.h, C.byref(O.pose_c(pose)), C.byref(O.cam_c(cam)), C.byref(O.settings_c(s)),
                      gf.ctypes.data, gc.ctypes.data, gd.ctypes.data, 1, {fthreads}, times.ctypes.data)
@@ -179,19 +202,20 @@ while True:
     best = times.copy() if best is None else np.minimum(best, times)
     if frames >= {max_frames} or total >= budget:
         break
-print("CPU_RESULT " + json.dumps(dict(frames=frames, seconds=total, threads=int(threads),
+print("CPU_RESULT " + json.dumps(dict(frames=frames, seconds=total, threads=int(threads), warmup={warmup},
                                      phases=dict(zip(["prepare_scene", "geometric_pass", "render_feature",
                                                       "backward_feature", "backward_geometric", "frame"],
                                                      [float(x) for x in best])))))
 """
 
 
-def run_cpu_oracle(cfg, budget_s, max_frames, timeout_s):
+def run_cpu_oracle(cfg, budget_s, max_frames, timeout_s, warmup=0):
     cores, model, mem_gb = host_info()
     # backward_feature keeps one N x D fp64 partial per thread (backward.cpp:290-291): cap threads to RAM
     per_thread_gb = cfg["n"] * cfg["d"] * 8 / 1e9
     fthreads = max(1, min(cores, int((mem_gb * 0.5 - 3 * per_thread_gb) / max(per_thread_gb, 1e-9))))
-    code = CPU_SNIPPET.format(root=ROOT, cfg=cfg, budget=budget_s, max_frames=max_frames, fthreads=fthreads)
+    code = CPU_SNIPPET.format(root=ROOT, cfg=cfg, budget=budget_s, max_frames=max_frames, fthreads=fthreads,
+                              warmup=warmup)
     env = dict(os.environ, OMP_NUM_THREADS=str(cores))
     try:
         res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=timeout_s,
@@ -205,22 +229,28 @@ def run_cpu_oracle(cfg, budget_s, max_frames, timeout_s):
 
 
 def reference_arm(args, cfg):
+    """The reference's CPU path (the oracle port: the reference cannot be built here) on
+    this host's cores, same workload and config as the GPU arm.  One warm-up frame, then full frames
+    until the step count or a 120 s budget is reached; `steps` / `warmup` report what actually ran."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    warm = 1 if args.warmup > 0 else 0
     r, err, cores, model, fthreads = run_cpu_oracle(cfg, budget_s=120.0, max_frames=max(1, args.steps),
-                                                     timeout_s=900)
+                                                     timeout_s=900, warmup=warm)
     line = {"impl": "reference", "metric": METRIC, "unit": "frames/s", "higher_is_better": True,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg["label"], "top_k": cfg["k"]}}
+            "n_gpus": args.gpus, "steps": 0, "warmup": 0, "steps_requested": args.steps,
+            "warmup_requested": args.warmup, "dtype": "f64", "data": "synthetic",
+            "config": bench_config(cfg, world, args.mode, args.gather)}
     if r is None:
         line.update({"value": None, "error": err})
     else:
         v = r["frames"] / r["seconds"]
-        sample = (f"{r['frames']} full frame(s) of the workload through the oracle port (oracle/src/oracle.cpp, "
-                  f"restating render.cpp/backward.cpp), OpenMP {cores} threads ({fthreads} for backward_feature, "
-                  f"RAM-capped N x D fp64 per-thread partials); host {model}")
-        line.update({"value": v, "ms_per_step": 1000.0 / v,
+        sample = (f"{r['frames']} timed full frame(s) after {r['warmup']} warm-up frame(s) of the workload through "
+                  f"the oracle port (oracle/src/oracle.cpp, restating render.cpp/backward.cpp), OpenMP {cores} threads "
+                  f"({fthreads} for backward_feature, RAM-capped N x D fp64 per-thread partials); host {model}")
+        line.update({"value": v, "ms_per_step": 1000.0 / v, "steps": r["frames"], "warmup": r["warmup"],
                      "cpu_baseline": {"value": v, "unit": "frames/s", "cores": cores, "kind": "port",
                                       "sample": sample, "phases_s": r["phases"]},
                      "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
@@ -232,7 +262,7 @@ def main_gpu(args, cfg):
     import torch
 
     from paper_2602_06991_b200 import _native as N
-    from paper_2602_06991_b200 import synth
+    import scenegen as synth
     from paper_2602_06991_b200.api import to_camera, to_pose, to_settings
     from paper_2602_06991_b200.types import RenderSettings
 
@@ -246,7 +276,7 @@ def main_gpu(args, cfg):
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     lib = N.render_lib()
-    slib = N.synth_lib()
+    slib = synth.N.synth_lib()
 
     n, W, H, D, K = cfg["n"], cfg["w"], cfg["h"], cfg["d"], args.k or cfg["k"]
     P = W * H
@@ -380,7 +410,8 @@ def main_gpu(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = args.steps / (ms / 1000.0)
+    # dshard: the ranks render one frame together; keyframe-parallel: every rank's frames count
+    value = (1 if dshard else world) * args.steps / (ms / 1000.0)
 
     phases = {name: {"ms_per_step": ph_ms[i] / args.steps, "launch_groups": int(ph_cnt[i])}
               for i, name in enumerate(N.PHASES) if ph_cnt[i]}
@@ -425,6 +456,21 @@ def main_gpu(args, cfg):
     feature_path = {"algorithmic_bytes": feat_bytes, "ms": feat_ms,
                     "achieved_gbs": feat_bytes / (feat_ms / 1000.0) / 1e9 if feat_ms > 0 else 0.0}
 
+    # ---- whole-frame HBM roofline: §8(d) algorithmic bytes of the feature frame (F write, dF read,
+    # dense df write, distinct rows read, records read by the forward and the backward) over the
+    # measured step time -- what the ">= 60 % of HBM roofline" target in BASELINE.json is quoted on
+    frame_bytes = P * Ds * 4 + P * Ds * 4 + n * Ds * 4 + U * Ds * 4 + 2 * P * (K * 12 + 1)
+    frame_roof = {"algorithmic_bytes_per_frame": frame_bytes, "ms_per_frame": ms_step,
+                  "achieved_gbs": frame_bytes / (ms_step / 1000.0) / 1e9, "peak": peak,
+                  "frac": frame_bytes / (ms_step / 1000.0) / 1e9 / peak,
+                  "formula": "P*D*4 (F) + P*D*4 (dF) + N*D*4 (df) + U*D*4 (rows) + 2*P*(K*12+1) (records)"}
+    multi = None
+    if world > 1:
+        multi = {"ranks": world, "per_gpu_feature_dim": Ds,
+                 "per_gpu_hbm_frac": frame_roof["frac"],
+                 "nvlink_bytes_received_per_gpu": (P * D * 4 * (world - 1) // world) if dshard else 0,
+                 "nvlink_gbs_per_gpu": ((P * D * 4 * (world - 1) / world) / (ms_step / 1000.0) / 1e9) if dshard else 0.0}
+
     # ---- e2e through the C ABI with pinned host buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -432,7 +478,7 @@ def main_gpu(args, cfg):
                       K, max(2, min(args.steps, args.e2e_steps)), stream, dist)
 
     extras = None
-    if not dshard and not args.no_mapping:
+    if not dshard and not args.no_mapping and not args.no_extras:
         extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev, cpose, ccam, cset)
 
     mapping = None
@@ -440,6 +486,14 @@ def main_gpu(args, cfg):
         mapping = run_mapping(lib, slib, N, torch, ctx, W, H, Ds, n, cpose, ccam, cset, args.steps, args.warmup,
                               0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard, scene=scene,
                               cam=cam, gt_pose=pose, d_total=D, c0=c0)
+
+    k_sweep = ref_grid = None
+    if world == 1 and not args.no_extras:
+        k_sweep = run_k_sweep(lib, N, torch, dev, args.steps, peak)
+        ref_grid = run_reference_grid(lib, N, torch, dev)
+    kf_block = None
+    if world > 1 and dshard and not args.no_extras:
+        kf_block = run_keyframe_parallel(lib, N, torch, dev, cfg, K, rank, world, args.steps, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -459,15 +513,10 @@ def main_gpu(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_step, "step_ms": step_stats, "higher_is_better": True,
             "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
-            "config": {"workload": cfg["label"], "gaussians": n, "width": W, "height": H, "feature_dim": D,
-                       "top_k": K, "feature_dim_per_gpu": Ds, "parallelism": (f"feature-dim shard d{world} + " + ("render_feature fused with the all-gather over "
-                                                                                "NVLink peer stores" if gather_mode == "p2p"
-                                                                                else f"NCCL all-gather [{gather_mode}]")
-                                       if dshard else
-                                       f"keyframe-parallel x{world}: rank r renders orbit keyframe r, all D"),
-                       "l2": "inputs larger than L2 (features %.2f GB, F %.2f GB)" % (n * D * 4 / 1e9,
-                                                                                        P * D * 4 / 1e9),
-                       "records": {"distinct_gaussians": U, "valid_slots": M}},
+            "config": bench_config(dict(cfg, n=n, k=K), world, args.mode, args.gather),
+            "gather_path": gather_mode, "records": {"distinct_gaussians": U, "valid_slots": M},
+            "frame_roofline": frame_roof, "multi_gpu": multi, "keyframe_parallel": kf_block,
+            "k_sweep": k_sweep, "fslam_bench_grid": ref_grid,
             "hbm_gbs": feature_path["achieved_gbs"],
             "roofline": roof, "roofline_fp64": roof64, "feature_path": feature_path, "phases": phases,
             "gpu_launches": int(launches), "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
@@ -575,7 +624,8 @@ def run_mapping(lib, slib, N, torch, ctx, W, H, D, n, kpose, ccam, cset, steps, 
     # keyframe: render_ground_truth of the bench scene (scene.cpp:232-276; K = 1 labels -> class
     # embeddings); the map being optimised is that scene with its means and
     # colours perturbed (seeded), so every loss term has gradient
-    from paper_2602_06991_b200 import api, synth
+    from paper_2602_06991_b200 import api
+    import scenegen as synth
     from paper_2602_06991_b200.api import to_pose
     emb = synth.unit_features(4, d_total, 99)[:, c0:c0 + D]
     rr = api.Renderer(0)
@@ -759,6 +809,196 @@ def run_extras(lib, N, torch, ctx, W, H, D, n, steps, stream, dev, cpose=None, c
     return {"full_blend_feature": full_blend, "segment_by_query": query, "checkpoint": ckpt}
 
 
+def _frame_runner(lib, N, torch, dev, scene_args, D, feat_seed=7):
+    """A context holding one bench-recipe scene (features seeded unit rows) plus device upstream
+    gradients of the frame's shape; returns (ctx, step(cset, invalidate), objects to keep alive)."""
+    import scenegen as synth
+    from paper_2602_06991_b200.api import to_camera, to_pose
+    n_g, W, H = scene_args
+    scene, cam, pose, _ = synth.bench_scene(n_g, W, H, D)
+    feat = synth.unit_features(scene.size(), D, feat_seed)
+    n, P = scene.size(), W * H
+    h = C.c_void_p()
+    N.check(lib.tk_create(dev.index or 0, C.byref(h)))
+    ctx = h
+    geo = [np.ascontiguousarray(a, np.float64) for a in (scene.mean, scene.log_scale, scene.rotation,
+                                                          scene.opacity_logit, scene.color)]
+    view = N.tk_scene_view(n, D, *(a.ctypes.data for a in geo), feat.ctypes.data, scene.generation)
+    N.check(lib.tk_scene_upload(ctx, C.byref(view), N.TK_HOST))
+    gF = torch.empty(P * D, dtype=torch.float32, device=dev).uniform_(-1.0, 1.0)
+    gC = torch.empty(P * 3, dtype=torch.float64, device=dev).uniform_(-1.0, 1.0)
+    gD = torch.empty(P, dtype=torch.float64, device=dev).uniform_(-1.0, 1.0)
+    cpose, ccam = to_pose(pose), to_camera(cam)
+    grads = N.tk_geom_grads()
+    grads.mem = N.TK_DEVICE
+
+    def frame(cset):
+        N.check(lib.tk_invalidate(ctx))
+        N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
+        N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))
+        N.check(lib.tk_backward_feature(ctx, None, C.c_void_p(gF.data_ptr()), N.TK_DEVICE, None, N.TK_DEVICE))
+        N.check(lib.tk_backward_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset),
+                                          C.c_void_p(gC.data_ptr()), C.c_void_p(gD.data_ptr()), N.TK_DEVICE,
+                                          C.byref(grads)))
+
+    keep = (geo, feat, gF, gC, gD, grads)
+    return ctx, frame, cpose, ccam, n, P, keep
+
+
+def _events_ms(torch, stream, fn, reps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def _records_stats(lib, N, ctx, cpose, ccam, cset, P, k):
+    idx = np.empty(P * max(k, 1), np.int32)
+    out = N.tk_geom_out(N.TK_HOST, None, None, None, idx.ctypes.data, None, None, None, 0, 0)
+    N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.byref(out)))
+    v = idx[idx >= 0]
+    return int(np.unique(v).size), int(v.size)
+
+
+def run_k_sweep(lib, N, torch, dev, steps, peak):
+    """BASELINE config 2: the config-1 scene (100k Gaussians, 640x480, D=512), forward + backward
+    frame at K = 1/4/8/16 (and 3), frames/s and the feature path's algorithmic GB/s (§8(d) bytes of
+    gather + backward_feature over their CUDA-event time), plus the full-blend feature pass against
+    the Top-K feature pass (SPEC.md:462 ordering)."""
+    from paper_2602_06991_b200.api import to_settings
+    from paper_2602_06991_b200.types import RenderSettings
+    D = 512
+    ctx, frame, cpose, ccam, n, P, keep = _frame_runner(lib, N, torch, dev, (100_000, 640, 480), D)
+    stream = torch.cuda.ExternalStream(lib.tk_get_stream(ctx), device=dev)
+    out = {"workload": "config 2: 100k Gaussians, 640x480, D=512 (bench recipe, orbit pose 0)", "k": {}}
+    try:
+        reps = max(5, min(steps, 20))
+        for k in (1, 3, 4, 8, 16):
+            cset = to_settings(RenderSettings(top_k=k))
+            for _ in range(3):
+                frame(cset)
+            N.check(lib.tk_synchronize(ctx))
+            N.check(lib.tk_profile_read(ctx, None, None, 1))
+            N.check(lib.tk_profile_enable(ctx, 1))
+            ms = _events_ms(torch, stream, lambda: frame(cset), reps)
+            N.check(lib.tk_profile_enable(ctx, 0))
+            ph_ms = (C.c_double * len(N.PHASES))()
+            ph_cnt = (C.c_int64 * len(N.PHASES))()
+            N.check(lib.tk_profile_read(ctx, ph_ms, ph_cnt, 1))
+            U, M = _records_stats(lib, N, ctx, cpose, ccam, cset, P, k)
+            fb = (P * D * 4 + U * D * 4 + P * k * 12 + P) + (P * D * 4 + n * D * 4 + M * 8 + (n + 1) * 4)
+            fms = sum(ph_ms[i] / max(1, ph_cnt[i]) for i in (2, 3, 4))
+            out["k"][str(k)] = {"frames_per_s": 1000.0 / ms, "ms_per_frame": ms,
+                                "feature_path": {"ms": fms, "algorithmic_bytes": fb,
+                                                 "achieved_gbs": fb / (fms / 1000.0) / 1e9,
+                                                 "frac": fb / (fms / 1000.0) / 1e9 / peak},
+                                "records": {"distinct_gaussians": U, "valid_slots": M}}
+        # feature pass alone (records resident, as cmd_bench times render_feature) vs the full blend
+        Fb = torch.empty(P * D, dtype=torch.float32, device=dev)
+        passes = {}
+        for k in (1, 3, 10):
+            cset = to_settings(RenderSettings(top_k=k))
+            N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
+            passes[f"K={k}"] = _events_ms(torch, stream, lambda: N.check(lib.tk_render_feature(
+                ctx, None, None, N.TK_DEVICE)), reps)
+        cset = to_settings(RenderSettings(top_k=3))
+        fb_args = (ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.c_void_p(Fb.data_ptr()), N.TK_DEVICE)
+        N.check(lib.tk_render_feature_full_blend(*fb_args))
+        passes["full_blend"] = _events_ms(torch, stream, lambda: N.check(lib.tk_render_feature_full_blend(*fb_args)),
+                                          max(3, reps // 4))
+        out["feature_pass_ms"] = passes
+        out["full_blend_over_topk3"] = passes["full_blend"] / passes["K=3"]
+        out["ordering_k1_k3_k10_full"] = bool(passes["K=1"] <= passes["K=3"] <= passes["K=10"] <= passes["full_blend"])
+        del Fb
+    finally:
+        lib.tk_destroy(ctx)
+        del keep
+    return out
+
+
+def run_keyframe_parallel(lib, N, torch, dev, cfg, K, rank, world, steps, dist):
+    """Config 4's 8-keyframe batch as independent replicas: rank r renders orbit keyframe r (of 8)
+    with all D channels, forward + backward, no data-path collective.  Aggregate frames/s over
+    ranks (weak scaling), time = max over ranks."""
+    import scenegen as synth
+    from paper_2602_06991_b200.api import to_settings
+    from paper_2602_06991_b200.types import RenderSettings
+    ctx, frame, cpose, ccam, n, P, keep = _frame_runner(lib, N, torch, dev, (cfg["n"], cfg["w"], cfg["h"]), cfg["d"])
+    try:
+        _, _, _, spec = synth.bench_scene(cfg["n"], cfg["w"], cfg["h"], cfg["d"])
+        pose = synth.generate_trajectory("orbit", 8, spec)[rank % 8]
+        from paper_2602_06991_b200.api import to_pose
+        cp = to_pose(pose)
+        cpose.qw, cpose.qx, cpose.qy, cpose.qz, cpose.tx, cpose.ty, cpose.tz = (cp.qw, cp.qx, cp.qy, cp.qz, cp.tx,
+                                                                                 cp.ty, cp.tz)
+        stream = torch.cuda.ExternalStream(lib.tk_get_stream(ctx), device=dev)
+        cset = to_settings(RenderSettings(top_k=K))
+        for _ in range(3):
+            frame(cset)
+        N.check(lib.tk_synchronize(ctx))
+        dist.barrier()
+        ms = _events_ms(torch, stream, lambda: frame(cset), max(3, steps))
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    finally:
+        lib.tk_destroy(ctx)
+        del keep
+    return {"value": world / (ms / 1000.0), "unit": "frames/s", "per_gpu_frames_per_s": 1000.0 / ms,
+            "ms_per_step": ms, "scaling": "weak",
+            "path": "rank r renders orbit keyframe r of config 4's batch, all D channels, fwd + bwd"}
+
+
+def run_reference_grid(lib, N, torch, dev):
+    """The reference's own bench table (fslam_main.cpp:167-223, `fslam bench` defaults: 10k Gaussians,
+    256x256, seed 7, orbit pose 0): render_feature for D in {16, 64} x K in {1, 3, 5, 10} on resident
+    records, the full-blend feature pass on the prepared scene, and the tiled render_geometric (K=3,
+    re-prepared each call).  SPEC.md:462 (acceptance 4) on the D=64 rows: K=1 <= K=3 <= K=10 <= full
+    blend and full blend >= 2x K=3."""
+    from paper_2602_06991_b200.api import to_settings
+    from paper_2602_06991_b200.types import RenderSettings
+    out = {"workload": "fslam bench defaults: 10k Gaussians, 256x256, D in {16, 64}", "rows": []}
+    acc = None
+    for D in (16, 64):
+        ctx, frame, cpose, ccam, n, P, keep = _frame_runner(lib, N, torch, dev, (10_000, 256, 256), D)
+        stream = torch.cuda.ExternalStream(lib.tk_get_stream(ctx), device=dev)
+        try:
+            t = {}
+            for k in (1, 3, 5, 10):
+                cset = to_settings(RenderSettings(top_k=k))
+                N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
+                fn = lambda: N.check(lib.tk_render_feature(ctx, None, None, N.TK_DEVICE))  # noqa: E731
+                _events_ms(torch, stream, fn, 5)
+                t[k] = _events_ms(torch, stream, fn, 50)
+                out["rows"].append({"D": D, "K": k, "feature_ms": t[k], "fps": 1000.0 / t[k]})
+            Fb = torch.empty(P * D, dtype=torch.float32, device=dev)
+            cset = to_settings(RenderSettings(top_k=3))
+            fb = lambda: N.check(lib.tk_render_feature_full_blend(  # noqa: E731
+                ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), C.c_void_p(Fb.data_ptr()), N.TK_DEVICE))
+            fb()
+            tf = _events_ms(torch, stream, fb, 20)
+            out["rows"].append({"D": D, "K": "full", "feature_ms": tf, "fps": 1000.0 / tf})
+
+            def tiled():
+                N.check(lib.tk_invalidate(ctx))
+                N.check(lib.tk_render_geometric(ctx, C.byref(cpose), C.byref(ccam), C.byref(cset), None))
+            tiled()
+            tg = _events_ms(torch, stream, tiled, 20)
+            out["rows"].append({"D": D, "K": "geometric tiled (K=3)", "ms": tg, "gaussians": n})
+            if D == 64:
+                acc = {"k1_le_k3_le_k10_le_full": bool(t[1] <= t[3] <= t[10] <= tf), "full_over_k3": tf / t[3],
+                       "full_ge_2x_k3": bool(tf >= 2.0 * t[3])}
+            del Fb
+        finally:
+            lib.tk_destroy(ctx)
+            del keep
+    out["spec_acceptance_4"] = acc
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -772,8 +1012,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20,
                     help="e2e steps (capped at --steps): enough to amortise the copy pipeline fill and drain")
     ap.add_argument("--no-mapping", action="store_true", help="skip the mapping-iteration measurement")
-    ap.add_argument("--mode", default="keyframe", choices=["keyframe", "dshard"],
-                    help="multi-GPU decomposition (N > 1)")
+    ap.add_argument("--mode", default="dshard", choices=["dshard", "keyframe"],
+                    help="multi-GPU decomposition (N > 1): config 4's D/N feature sharding (default) or "
+                         "keyframe-parallel replicas")
+    ap.add_argument("--no-extras", action="store_true", help="skip the K sweep, the fslam bench grid and extras")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="dshard: fused render + all-gather over peer memory, or render + NCCL all-gather")
     args = ap.parse_args()

@@ -296,6 +296,11 @@ tk_status tk_insert_gaussians(tk_ctx* ctx, const tk_source_view* src, double tau
  * n, may be NULL) receives the removed indices in ascending order. */
 tk_status tk_prune_map(tk_ctx* ctx, double keep_ratio, uint64_t seed, int32_t topk_count_threshold,
                        int32_t* removed_out, int64_t* n_removed);
+/* The candidate draw of prune_map alone (mapper.cpp:80-139), on host statistics; no context, no
+ * GPU.  Same removed indices as the reference's sequential scan, bit for bit, in O(C log C)
+ * (Fenwick pool with an exact rounding-bounded fallback).  removed_out: capacity n. */
+tk_status tk_prune_draw(const int32_t* topk_count, const double* max_contribution, int64_t n, double keep_ratio,
+                        uint64_t seed, int32_t topk_count_threshold, int32_t* removed_out, int64_t* n_removed);
 
 /* FEAT feature frames (synth/dataset.cpp:48-76: "FEAT", uint32 h, w, d, then h*w*d fp32 HWC):
  * load replaces keyframe `slot`'s feature image (same h x w as the keyframe; its row-validity mask

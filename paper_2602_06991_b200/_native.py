@@ -1,4 +1,4 @@
-"""ctypes binding of the C ABI in include/tk_render.h and include/tk_synth.h.
+"""ctypes binding of the C ABI in include/tk_render.h.
 
 The product path is the CUDA library lib/libtkrender.so; there is no CPU fallback.  Loading
 fails loudly if the library is missing (run ``python -m paper_2602_06991_b200.build``).
@@ -12,7 +12,6 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "lib")
 # TK_RENDER_LIB: load an alternative build of the same library (A/B kernel experiments)
 RENDER_LIB = os.environ.get("TK_RENDER_LIB") or os.path.join(LIB_DIR, "libtkrender.so")
-SYNTH_LIB = os.path.join(LIB_DIR, "libtk_synth.so")
 
 TK_HOST, TK_DEVICE, TK_HOST_ASYNC = 0, 1, 2
 TK_OK, TK_ERR_STALE_INDEX, TK_ERR_BAD_ARG, TK_ERR_CUDA, TK_ERR_NCCL, TK_ERR_OOM, TK_ERR_STATE = range(7)
@@ -96,18 +95,6 @@ class tk_source_view(C.Structure):
                 ("feature", C.c_void_p), ("spacing", C.c_void_p), ("distance", C.c_void_p), ("mem", C.c_int32)]
 
 
-class tk_synth_arrays(C.Structure):
-    _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("mean", C.c_void_p), ("log_scale", C.c_void_p),
-                ("rotation", C.c_void_p), ("opacity_logit", C.c_void_p), ("color", C.c_void_p),
-                ("feature", C.c_void_p)]
-
-
-class tk_synth_spec(C.Structure):
-    _fields_ = [("room_min", C.c_double * 3), ("room_max", C.c_double * 3), ("classes", C.c_int32),
-                ("feature_dim", C.c_int32), ("spacing", C.c_double), ("jitter", C.c_double),
-                ("opacity", C.c_double), ("boxes", C.c_int32), ("seed", C.c_uint64)]
-
-
 # (name, restype, argtypes) of every symbol include/tk_render.h declares.
 RENDER_SYMBOLS = [
     ("tk_default_settings", None, [C.POINTER(tk_settings)]),
@@ -163,6 +150,8 @@ RENDER_SYMBOLS = [
     ("tk_insert_gaussians", C.c_int, [C.c_void_p, C.POINTER(tk_source_view), C.c_double, C.POINTER(tk_pose),
                                       i32_p]),
     ("tk_prune_map", C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_void_p, i64_p]),
+    ("tk_prune_draw", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_uint64, C.c_int32, C.c_void_p,
+                                i64_p]),
     ("tk_checkpoint_save", C.c_int, [C.c_void_p, C.c_char_p]),
     ("tk_checkpoint_load", C.c_int, [C.c_void_p, C.c_char_p]),
     ("tk_segment_by_query", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
@@ -172,19 +161,8 @@ RENDER_SYMBOLS = [
 PHASES = ["prepare", "geom_fwd", "gather", "fbwd_index", "fbwd", "geom_bwd", "chain", "full_blend", "allgather",
           "copy", "loss", "adam"]
 
-SYNTH_SYMBOLS = [
-    ("tk_synth_default_spec", None, [C.POINTER(tk_synth_spec)]),
-    ("tk_synth_random_scene", None, [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
-                                     C.POINTER(tk_synth_arrays)]),
-    ("tk_synth_build_scene", C.c_int64, [C.POINTER(tk_synth_spec), C.POINTER(tk_synth_arrays), C.c_void_p]),
-    ("tk_synth_trajectory", C.c_int, [C.c_int32, C.c_int32, C.POINTER(tk_synth_spec), C.c_void_p]),
-    ("tk_synth_unit_features", None, [C.c_int64, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p]),
-    ("tk_synth_uniform_fill", None, [C.c_int64, C.c_uint64, C.c_double, C.c_double, C.c_void_p]),
-    ("tk_synth_hash_fill_f32", None, [C.c_int64, C.c_uint64, C.c_float, C.c_float, C.c_void_p]),
-]
 
 _render = None
-_synth = None
 
 
 def _bind(lib, symbols):
@@ -203,15 +181,6 @@ def render_lib():
             raise ImportError(f"{RENDER_LIB} missing: build it with `python -m paper_2602_06991_b200.build`")
         _render = _bind(C.CDLL(RENDER_LIB, mode=C.RTLD_GLOBAL), RENDER_SYMBOLS)
     return _render
-
-
-def synth_lib():
-    global _synth
-    if _synth is None:
-        if not os.path.exists(SYNTH_LIB):
-            raise ImportError(f"{SYNTH_LIB} missing: build it with `python -m paper_2602_06991_b200.build`")
-        _synth = _bind(C.CDLL(SYNTH_LIB), SYNTH_SYMBOLS)
-    return _synth
 
 
 class TkError(RuntimeError):

@@ -1,7 +1,6 @@
 """Build the native libraries in-tree (nvcc / g++ only; no torch extension machinery).
 
   lib/libtkrender.so   sm_100a CUDA kernels + the C ABI of include/tk_render.h
-  lib/libtk_synth.so   host C++ synthetic-input generators (include/tk_synth.h)
 
 The geometry TUs (prepare.cu, geometric.cu) and the loss / optimiser TU (mapping.cu) are compiled with --fmad=false so their fp64
 arithmetic rounds like the reference's x86-64 build (no FMA contraction); the feature TU is
@@ -79,12 +78,6 @@ def build(force: bool = False, verbose: bool = False) -> dict[str, str]:
         if force or _stale(so, objs):
             _run([nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", so, "-ldl"], log)
         out["tkrender"] = so
-        synth_src = os.path.join(CSRC, "host", "synth.cpp")
-        synth_so = os.path.join(LIB, "libtk_synth.so")
-        if force or _stale(synth_so, [synth_src, os.path.join(INCLUDE, "tk_synth.h")]):
-            _run(["g++", "-O3", "-std=c++17", "-fopenmp", "-fPIC", "-shared", "-I" + INCLUDE, synth_src,
-                  "-o", synth_so], log)
-        out["synth"] = synth_so
     if verbose:
         print(open(os.path.join(BUILD, "build.log")).read())
     return out

@@ -36,7 +36,33 @@ struct GeomBwdParams {
     PixelAux aux;              // from the forward
     const double* grad_color;  // P x 3
     const double* grad_depth;  // P or null
-    double* mid;               // n x 10: mx,my,ixx,ixy,iyy,z,opacity,cr,cg,cb
+    // Deterministic flush (default): each warp writes its per-entry MidGrad partial to its own
+    // slot (padded entry position x sub-block) and flags it; k_mid_reduce sums the slots of each
+    // Gaussian in a fixed order.  part == null: fp64 atomicAdd into mid (TK_GEOM_BWD_ATOMIC=1).
+    double* mid;               // n x 10: mx,my,ixx,ixy,iyy,z,opacity,cr,cg,cb (atomic mode)
+    double* part;              // padded entries x nsub x 10 partials, or null
+    uint8_t* part_flag;        // padded entries x nsub: 1 = partial written this sweep (zeroed first)
+    int nsub;                  // warp blocks per tile
+};
+
+// Fixed-order per-Gaussian sum of the backward's slot partials (backward.cpp:166-178 merges its
+// per-thread partials in thread order; here: the Gaussian's tile pairs in emission order -- tile
+// rows, then columns, as render.cpp:146-153 emits them -- and the warp blocks of each tile in
+// block order).  Bit-deterministic run to run.
+struct MidReduceParams {
+    int64_t nv;                   // depth-sorted visible Gaussians
+    int64_t n_pairs;              // tile pairs (emission order)
+    double* pair_sum;             // n_pairs x 10 scratch (level 1)
+    const uint32_t* order;        // depth rank -> Gaussian id
+    const int32_t* ntiles_sorted; // tile pairs per depth rank
+    const int32_t* pair_off;      // first pair (emission index) per depth rank
+    const int32_t* pair_pos;      // emission index -> padded tile-entry position (k_materialize)
+    const double* part;
+    const uint8_t* part_flag;
+    int nsub;
+    double* mid;                  // n x 10 (zeroed beforehand; written for binned ranks)
+    int32_t* big_list;            // nv: medium ranks from the front, huge ranks from the back
+    int32_t* big_count;           // [medium, huge], zeroed beforehand
 };
 
 struct ChainParams {
@@ -80,6 +106,7 @@ int geom_blocks(const Frame& f);
 int geom_blocks_per_tile(int tile_size);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);
 void launch_geom_bwd(const GeomBwdParams& p, int n_blocks, cudaStream_t st);
+void launch_mid_reduce(const MidReduceParams& p, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);
 // Adam + clamps + renormalisation + peak statistic over every Gaussian (thread per Gaussian)
 void launch_geo_adam(const GeoAdamParams& a, int64_t n, cudaStream_t st);

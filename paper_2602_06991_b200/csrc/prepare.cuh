@@ -31,6 +31,12 @@ struct MaterializeParams {
     const uint32_t* order;       // depth rank -> Gaussian id
     const double *mx, *my, *ixx, *ixy, *iyy, *z, *opacity, *color;
     TileEntries out;
+    // inverse of the pair emission (k_emit_pairs): pair_pos[pair_off[s] + local] = padded position
+    // of depth rank s's local-th tile (row-major in its rectangle); null = not needed
+    const int4* rect;
+    const int32_t* pair_off;
+    int tiles_x;
+    int32_t* pair_pos;
 };
 
 void launch_project(const ProjectParams& p, cudaStream_t st);

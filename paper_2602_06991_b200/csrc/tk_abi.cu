@@ -274,6 +274,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     const int64_t padded_cap = n_pairs + static_cast<int64_t>(tk::kEntryAlign) * n_tiles + 128;
     ensure<tk::EntryChunk>(c->te, padded_cap / tk::kChunk + 1);
     ensure<int32_t>(c->wl, padded_cap * tk::geom_blocks_per_tile(s->tile_size));
+    c->padded_cap = padded_cap;
     tk::MaterializeParams mp{};
     mp.n_pairs = n_pairs;
     mp.tile_keys = c->tile_keys_sorted;
@@ -290,6 +291,10 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     mp.opacity = pp.opacity;
     mp.color = ptr<double>(c->color);
     mp.out = tile_entries(c);
+    mp.rect = pp.rect;
+    mp.pair_off = poff;
+    mp.tiles_x = f.tiles_x;
+    mp.pair_pos = ensure<int32_t>(c->pair_pos, n_pairs);
     tk::launch_materialize(mp, st);
     CK_LAUNCH(c);
     c->prepared = true;
@@ -448,9 +453,35 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
     bp.grad_color = gc;
     bp.grad_depth = gd;
     bp.mid = mid;
+    bp.nsub = tk::geom_blocks_per_tile(f.tile_size);
+    if (!c->geom_atomic) {
+        const int64_t slots = c->padded_cap * bp.nsub;
+        bp.part = ensure<double>(c->g_part, slots * 10);
+        // flags + the big-rank counter behind them, zeroed in one memset
+        const int64_t fbytes = tk::align_up(std::max<int64_t>(slots, 1), 16);
+        bp.part_flag = ensure<uint8_t>(c->g_flag, fbytes + 16);
+        CK(cudaMemsetAsync(bp.part_flag, 0, fbytes + 16, c->cur));
+    }
     {
         PhaseScope phase(c, TK_PHASE_GEOM_BWD);
         tk::launch_geom_bwd(bp, tk::geom_blocks(f), c->cur);
+        if (!c->geom_atomic) {
+            tk::MidReduceParams mr{};
+            mr.nv = c->n_vis;
+            mr.n_pairs = c->n_pairs;
+            mr.pair_sum = ensure<double>(c->g_pairsum, std::max<int64_t>(c->n_pairs, 1) * 10);
+            mr.order = c->order;
+            mr.ntiles_sorted = ptr<int32_t>(c->ntiles_sorted);
+            mr.pair_off = ptr<int32_t>(c->pair_off);
+            mr.pair_pos = ptr<int32_t>(c->pair_pos);
+            mr.part = bp.part;
+            mr.part_flag = bp.part_flag;
+            mr.nsub = bp.nsub;
+            mr.mid = mid;
+            mr.big_list = ensure<int32_t>(c->g_big, std::max<int64_t>(c->n_vis, 1));
+            mr.big_count = reinterpret_cast<int32_t*>(bp.part_flag + tk::align_up(std::max<int64_t>(c->padded_cap * bp.nsub, 1), 16));
+            tk::launch_mid_reduce(mr, c->cur);
+        }
     }
     CK_LAUNCH(c);
     return mid;
@@ -545,6 +576,8 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         // Side streams only with TK_OVERLAP=1: on B200 the fp64 geometry backward and the feature
         // kernels each fill the SMs' register files, so overlapping them measured no gain; the
         // default aliases every stream to the main one (per-kernel times stay unambiguous).
+        const char* gat = std::getenv("TK_GEOM_BWD_ATOMIC");
+        c->geom_atomic = gat && gat[0] == '1';
         const char* overlap = std::getenv("TK_OVERLAP");
         if (!(overlap && overlap[0] == '1')) {
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_feat, cudaStreamNonBlocking);

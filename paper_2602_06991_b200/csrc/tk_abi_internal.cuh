@@ -254,6 +254,8 @@ struct tk_ctx {
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
     DevBuf te;  // chunk-major tile entries (tk::EntryChunk)
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
+    DevBuf pair_pos;      // pair emission index -> padded tile-entry position (fixed-order merge)
+    int64_t padded_cap = 0;
     DevBuf scratch, scratch_feat, dscal;
     int64_t* hscal = nullptr;      // host-mapped mirror of dscal (written by k_copy_words)
     int64_t* hscal_dev = nullptr;  //   its device address
@@ -279,6 +281,8 @@ struct tk_ctx {
     DevBuf f_out, f_grad_in, f_grad_out, s_keys, s_vals, s_keys_alt, s_vals_alt, s_wnorm, s_seg;
     int64_t fout_pixels = 0;
     // geometric backward
+    bool geom_atomic = false;  // TK_GEOM_BWD_ATOMIC=1: fp64 atomicAdd flush (non-deterministic)
+    DevBuf g_part, g_flag, g_big, g_pairsum;  // per-(entry, warp block) MidGrad partials, written flags, big ranks
     DevBuf g_color_in, g_depth_in, mid, twist, twist_part, twist_out, gg_mean, gg_ls, gg_rot, gg_op, gg_col;
     // full blend
     DevBuf l_count, l_off, l_src, l_w;

@@ -44,6 +44,75 @@ void compact_rows(tk_ctx* c, DevBuf& b, int64_t n, int width, int64_t n_keep, co
 // prune_map's candidate draw (mapper.cpp:80-139), host side: candidates have topk_count <=
 // threshold; ceil(keep_ratio * candidates) survive, drawn without replacement proportionally to
 // max_contribution with std::mt19937_64(seed), uniformly once the mass is exhausted.
+//
+// The reference finds each weighted pick with a sequential scan of the remaining pool (fp64
+// running sum, first position with u < acc) and erases it from a vector: O(C) per draw, O(C^2)
+// per prune -- minutes to hours at config-3 candidate counts.  The same picks, bit for bit, in
+// O(log C) per draw: Fenwick trees over the candidate order hold the pool membership and the
+// pool scores.  A Fenwick descent locates the position p where the pool's prefix sum passes u;
+// the pick is certain when u clears both of p's prefix bounds by B, a bound on |sequential fp64
+// running sum - Fenwick prefix sum| (both are sums of <= C non-negative terms of total <= total:
+// each within ~C eps total of the exact sum).  Only when u falls within B of a boundary, or past
+// the pool's end (the reference's "no break: last pool element" case), does the draw replay the
+// reference's scan exactly over the current pool.  Uniform draws pick the (rng() % size)-th pool
+// element by a count descent.  Negative or non-finite scores take the reference loop verbatim.
+struct Fenwick {
+    std::vector<double> s;
+    std::vector<int32_t> c;
+    size_t n = 0, top = 1;
+    explicit Fenwick(const std::vector<double>& v) : s(v.size() + 1, 0.0), c(v.size() + 1, 0), n(v.size()) {
+        for (size_t i = 1; i <= n; ++i) {
+            s[i] += v[i - 1];
+            c[i] += 1;
+            const size_t j = i + (i & (~i + 1));
+            if (j <= n) {
+                s[j] += s[i];
+                c[j] += c[i];
+            }
+        }
+        while (top * 2 <= n) top *= 2;
+    }
+    void rebuild_counts(const std::vector<uint8_t>& gone) {  // membership = !gone
+        std::fill(c.begin(), c.end(), 0);
+        for (size_t i = 1; i <= n; ++i) {
+            c[i] += gone[i - 1] ? 0 : 1;
+            const size_t j = i + (i & (~i + 1));
+            if (j <= n) c[j] += c[i];
+        }
+    }
+    void remove(size_t i, double v) {
+        for (size_t k = i + 1; k <= n; k += k & (~k + 1)) {
+            s[k] -= v;
+            c[k] -= 1;
+        }
+    }
+    double prefix(size_t i) const {  // sum over positions < i
+        double r = 0.0;
+        for (size_t k = i; k > 0; k -= k & (~k + 1)) r += s[k];
+        return r;
+    }
+    size_t first_above(double u) const {  // first position whose inclusive prefix sum exceeds u (n: none)
+        size_t pos = 0;
+        double rem = u;
+        for (size_t st = top; st > 0; st >>= 1)
+            if (pos + st <= n && s[pos + st] <= rem) {
+                pos += st;
+                rem -= s[pos];
+            }
+        return pos;
+    }
+    size_t kth(size_t k) const {  // position of the k-th (0-based) pool member
+        size_t pos = 0;
+        int64_t rem = static_cast<int64_t>(k);
+        for (size_t st = top; st > 0; st >>= 1)
+            if (pos + st <= n && c[pos + st] <= rem) {
+                pos += st;
+                rem -= c[pos];
+            }
+        return pos;
+    }
+};
+
 std::vector<int32_t> prune_select(const std::vector<int32_t>& counts, const std::vector<double>& maxc,
                                   double keep_ratio, uint64_t seed, int32_t threshold) {
     std::vector<int32_t> cand;
@@ -53,41 +122,103 @@ std::vector<int32_t> prune_select(const std::vector<int32_t>& counts, const std:
     if (cand.empty()) return removed;
     std::vector<double> score(cand.size());
     double total = 0.0;
+    bool plain = true;  // every score finite and >= 0: the fast draw applies
     for (size_t i = 0; i < cand.size(); ++i) {
         score[i] = maxc[cand[i]];
         total += score[i];
+        plain = plain && std::isfinite(score[i]) && score[i] >= 0.0;
     }
     if (!(total > 0.0)) return removed;  // survival weights undefined: keep every candidate
     const size_t keep = static_cast<size_t>(std::ceil(keep_ratio * static_cast<double>(cand.size())));
     if (keep >= cand.size()) return removed;
+    const size_t C = cand.size();
     std::mt19937_64 rng(seed);
-    std::vector<uint8_t> kept(cand.size(), 0);
-    std::vector<size_t> pool(cand.size());
-    for (size_t i = 0; i < pool.size(); ++i) pool[i] = i;
+    std::vector<uint8_t> kept(C, 0);
     double mass = total;
-    for (size_t draw = 0; draw < keep; ++draw) {
-        size_t pick = 0;
-        if (mass > 0.0) {
-            const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53 * mass;  // canonical_unit * mass
-            double acc = 0.0;
-            pick = pool.size() - 1;
-            for (size_t q = 0; q < pool.size(); ++q) {
-                acc += score[pool[q]];
-                if (u < acc) {
-                    pick = q;
-                    break;
+    if (!plain || !std::isfinite(total)) {  // the reference loop verbatim
+        std::vector<size_t> pool(C);
+        for (size_t i = 0; i < C; ++i) pool[i] = i;
+        for (size_t draw = 0; draw < keep; ++draw) {
+            size_t pick = 0;
+            if (mass > 0.0) {
+                const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53 * mass;  // canonical_unit * mass
+                double acc = 0.0;
+                pick = pool.size() - 1;
+                for (size_t q = 0; q < pool.size(); ++q) {
+                    acc += score[pool[q]];
+                    if (u < acc) {
+                        pick = q;
+                        break;
+                    }
                 }
+            } else {
+                pick = static_cast<size_t>(rng() % pool.size());
             }
-        } else {
-            pick = static_cast<size_t>(rng() % pool.size());
+            const size_t chosen = pool[pick];
+            kept[chosen] = 1;
+            mass -= score[chosen];
+            if (mass < 0.0) mass = 0.0;
+            pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(pick));
         }
-        const size_t chosen = pool[pick];
-        kept[chosen] = 1;
-        mass -= score[chosen];
-        if (mass < 0.0) mass = 0.0;
-        pool.erase(pool.begin() + static_cast<std::ptrdiff_t>(pick));
+    } else {
+        // Error bound of both running sums against the exact pool sum: <= (2C + C + 128) eps S, S =
+        // the pool sum when the tree was (re)built (subtractions leave errors of that size behind);
+        // the tree is rebuilt from the remaining scores whenever the pool sum falls below S / 16, so
+        // the bound stays within 16x of the current mass.
+        // TK_PRUNE_BOUND_SCALE (tests only) widens the bound to force the exact fallback path
+        const char* bs = std::getenv("TK_PRUNE_BOUND_SCALE");
+        const double scale = bs ? std::max(1.0, std::atof(bs)) : 1.0;
+        std::vector<double> live(score);
+        std::vector<size_t> positive;  // the exact fallback scans only these: adding 0.0 is exact
+        for (size_t i = 0; i < C; ++i)
+            if (score[i] > 0.0) positive.push_back(i);
+        Fenwick fw(live);
+        double built_sum = fw.prefix(C);
+        double bound = scale * 1.02 * (3.0 * static_cast<double>(C) + 128.0) * 0x1.0p-53 * built_sum;
+        size_t pool_n = C;
+        for (size_t draw = 0; draw < keep; ++draw) {
+            size_t chosen = C;
+            if (mass > 0.0) {
+                const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53 * mass;
+                const size_t p = fw.first_above(u);
+                if (p < C && !kept[p] && score[p] > 0.0) {
+                    const double lo = fw.prefix(p), hi = lo + score[p];
+                    if (lo + bound <= u && u < hi - bound) chosen = p;
+                }
+                if (chosen == C) {  // within rounding reach of a boundary: the reference's scan
+                    double acc = 0.0;
+                    for (size_t q : positive) {
+                        if (kept[q]) continue;
+                        acc += score[q];
+                        if (u < acc) {
+                            chosen = q;
+                            break;
+                        }
+                    }
+                    if (chosen == C) chosen = fw.kth(pool_n - 1);  // no break: the pool's last element
+                }
+            } else {
+                chosen = fw.kth(static_cast<size_t>(rng() % pool_n));
+            }
+            kept[chosen] = 1;
+            fw.remove(chosen, score[chosen]);
+            live[chosen] = 0.0;
+            --pool_n;
+            mass -= score[chosen];
+            if (mass < 0.0) mass = 0.0;
+            if (score[chosen] > 0.0 && fw.prefix(C) < built_sum * (1.0 / 16.0) && pool_n > 0) {
+                fw = Fenwick(live);
+                fw.rebuild_counts(kept);
+                built_sum = fw.prefix(C);
+                bound = scale * 1.02 * (3.0 * static_cast<double>(C) + 128.0) * 0x1.0p-53 * built_sum;
+                std::vector<size_t> still;
+                for (size_t q : positive)
+                    if (!kept[q]) still.push_back(q);
+                positive.swap(still);
+            }
+        }
     }
-    for (size_t i = 0; i < cand.size(); ++i)
+    for (size_t i = 0; i < C; ++i)
         if (!kept[i]) removed.push_back(cand[i]);
     return removed;
 }
@@ -428,7 +559,11 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
         }
         // backward_geometric (mapper.cpp:179-180) on this forward
         double* mid = geom_sweep(c, f, gc, gd);
-        if (sharded)  // replicas stay bit-identical: one all-reduced geometry gradient on every shard
+        // The fixed-order merge makes every replica's geometry gradient bit-identical, so the
+        // D-sharded step needs no collective here; the atomic flush (TK_GEOM_BWD_ATOMIC=1) is
+        // order-dependent and all-reduces it so the replicas cannot drift.
+        const bool geo_allreduce = sharded && c->geom_atomic;
+        if (geo_allreduce)
             NK(g_nccl.AllReduce(mid, mid, static_cast<size_t>(n) * 10, ncclFloat64, ncclSum, c->comm, st));
         {
             PhaseScope phase(c, TK_PHASE_ADAM);
@@ -459,7 +594,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
             ga.contrib = ptr<unsigned long long>(c->o_contrib);
             ga.max_contrib = ptr<double>(c->stat_maxc);
             tk::ChainParams cp = chain_params(c, &kf.pose, cam, s, mid);
-            cp.mid_scale = sharded ? 1.0 / c->nranks : 1.0;
+            cp.mid_scale = geo_allreduce ? 1.0 / c->nranks : 1.0;
             cp.g_mean = ensure<double>(c->gg_mean, n * 3);
             cp.g_log_scale = ensure<double>(c->gg_ls, n * 3);
             cp.g_rotation = ensure<double>(c->gg_rot, n * 4);
@@ -652,6 +787,18 @@ tk_status tk_insert_gaussians(tk_ctx* c, const tk_source_view* src, double tau, 
         sync(c);
         for (DevBuf* b : {&bpos, &bcol, &bsp, &bdist, &bfeat, &bflag, &bflag32, &bslot}) b->release();
         main_done(c);
+    });
+}
+
+tk_status tk_prune_draw(const int32_t* topk_count, const double* max_contribution, int64_t n, double keep_ratio,
+                        uint64_t seed, int32_t threshold, int32_t* removed_out, int64_t* n_removed) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && (!topk_count || !max_contribution))) fail(TK_ERR_BAD_ARG, "bad statistics arrays");
+        std::vector<int32_t> counts(topk_count, topk_count + n);
+        std::vector<double> maxc(max_contribution, max_contribution + n);
+        const std::vector<int32_t> removed = prune_select(counts, maxc, keep_ratio, seed, threshold);
+        if (removed_out && !removed.empty()) std::memcpy(removed_out, removed.data(), removed.size() * sizeof(int32_t));
+        if (n_removed) *n_removed = static_cast<int64_t>(removed.size());
     });
 }
 

@@ -1,4 +1,6 @@
-"""Synthetic inputs (restated reference generators, see include/tk_synth.h)."""
+"""Synthetic inputs: the reference's generators (testutil.hpp, scene.cpp) restated in host C++
+(scenegen/csrc/synth.cpp, scenegen/include/tk_synth.h) so the GPU path and the oracle see identical
+inputs.  Input synthesis for the tests and the bench; the product library never loads it."""
 from __future__ import annotations
 
 import ctypes as C
@@ -6,8 +8,9 @@ import math
 
 import numpy as np
 
-from . import _native as N
-from .types import CameraIntrinsics, Pose, SceneMap
+from paper_2602_06991_b200.types import CameraIntrinsics, Pose, SceneMap
+
+from . import _lib as N
 
 
 def _arrays(n: int, d: int, with_features: bool):
@@ -105,7 +108,7 @@ def render_ground_truth(renderer, scene, class_ids: np.ndarray, embeddings: np.n
     (on the GPU, through `renderer`); colour clamped to [0, 1]; depth, label and the label's class
     embedding only where alpha > 0.5 and a Top-1 record exists (label 255 elsewhere).  Returns
     [(Frame, label image)]."""
-    from .types import Frame, RenderSettings
+    from paper_2602_06991_b200.types import Frame, RenderSettings
     s = RenderSettings(top_k=1, transmittance_floor=1e-4, background=(0.0, 0.0, 0.0))
     emb = np.ascontiguousarray(embeddings, np.float32)
     out = []

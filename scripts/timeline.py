@@ -20,13 +20,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from bench import CONFIGS  # noqa: E402
-from paper_2602_06991_b200 import _native as N, synth  # noqa: E402
+from paper_2602_06991_b200 import _native as N  # noqa: E402
+import scenegen as synth
 from paper_2602_06991_b200.api import to_camera, to_pose, to_settings  # noqa: E402
 from paper_2602_06991_b200.types import Pose, RenderSettings  # noqa: E402
 
 
 def setup(cfg):
-    lib, slib = N.render_lib(), N.synth_lib()
+    lib, slib = N.render_lib(), synth.N.synth_lib()
     n, W, H, D, K = cfg["n"], cfg["w"], cfg["h"], cfg["d"], cfg["k"]
     scene, cam, pose, _ = synth.bench_scene(n, W, H, D)
     feat = synth.unit_features(scene.size(), D, 7)

@@ -210,6 +210,44 @@ def backward_feature(m, w, h, k, index, weight, count, grad):
     return out
 
 
+def _mem_available_gb() -> float:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable"):
+                return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 16.0
+
+
+def backward_feature_slices(m, w, h, k, index, weight, count, grad, width=64):
+    """backward_feature (backward.cpp:273-321) one channel slice at a time: the op never mixes
+    channels (each channel of dF scatters into the same channel of df), so the oracle run on a map
+    holding channels [c0, c1) and on grad[..., c0:c1] is exactly that slice of the full result.
+    Keeps the oracle's per-thread N x width fp64 partials (backward.cpp:290-291) within host RAM
+    at configs 3 and 5.  Yields (c0, c1, df_slice[n, c1 - c0])."""
+    from paper_2602_06991_b200.types import SceneMap
+    n, d = m.size(), m.feature_dim
+    L = lib()
+    cores = L.orc_max_threads()
+    per_thread_gb = n * width * 8 / 2**30
+    threads = max(1, min(cores, int((_mem_available_gb() * 0.5 - 2 * per_thread_gb) / max(per_thread_gb, 1e-9))))
+    L.orc_set_threads(threads)
+    try:
+        idx = np.ascontiguousarray(index, np.int32)
+        wt = np.ascontiguousarray(weight, np.float64)
+        cnt = np.ascontiguousarray(count, np.uint8)
+        g3 = grad.reshape(h, w, d)
+        for c0 in range(0, d, width):
+            c1 = min(d, c0 + width)
+            ms = SceneMap(m.mean, m.log_scale, m.rotation, m.opacity_logit, m.color,
+                          np.ascontiguousarray(m.feature[:, c0:c1]), m.generation, c1 - c0)
+            yield c0, c1, backward_feature(ms, w, h, k, idx, wt, cnt,
+                                           np.ascontiguousarray(g3[..., c0:c1], np.float64)).reshape(n, c1 - c0)
+    finally:
+        L.orc_set_threads(cores)
+
+
 def backward_geometric(m, pose, cam, s, grad_color, grad_depth):
     om = OracleMap(m)
     n = m.size()

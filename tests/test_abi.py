@@ -7,12 +7,14 @@ import re
 import pytest
 
 from paper_2602_06991_b200 import _native as N
+from scenegen import _lib as S
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER_DIRS = {"tk_render.h": os.path.join(ROOT, "include"), "tk_synth.h": os.path.join(ROOT, "scenegen", "include")}
 
 
 def declared(header):
-    txt = open(os.path.join(ROOT, "include", header)).read()
+    txt = open(os.path.join(HEADER_DIRS[header], header)).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
     return sorted(set(re.findall(r"\b(tk_[a-z0-9_]+)\s*\(", txt)))
 
@@ -21,9 +23,10 @@ def declared(header):
 def built():
     from paper_2602_06991_b200 import build
     build.build()
+    S.build()
 
 
-@pytest.mark.parametrize("header,path", [("tk_render.h", N.RENDER_LIB), ("tk_synth.h", N.SYNTH_LIB)])
+@pytest.mark.parametrize("header,path", [("tk_render.h", N.RENDER_LIB), ("tk_synth.h", S.SYNTH_LIB)])
 def test_library_exports_every_declared_symbol(header, path):
     lib = C.CDLL(path)
     names = declared(header)
@@ -34,7 +37,7 @@ def test_library_exports_every_declared_symbol(header, path):
 
 def test_ctypes_bindings_cover_header():
     assert sorted(n for n, _, _ in N.RENDER_SYMBOLS) == declared("tk_render.h")
-    assert sorted(n for n, _, _ in N.SYNTH_SYMBOLS) == declared("tk_synth.h")
+    assert sorted(n for n, _, _ in S.SYNTH_SYMBOLS) == declared("tk_synth.h")
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -42,7 +45,7 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"tk_camera": N.tk_camera, "tk_pose": N.tk_pose, "tk_settings": N.tk_settings,
                "tk_scene_view": N.tk_scene_view, "tk_topk_view": N.tk_topk_view, "tk_geom_out": N.tk_geom_out,
                "tk_geom_grads": N.tk_geom_grads, "tk_device_view": N.tk_device_view,
-               "tk_synth_arrays": N.tk_synth_arrays, "tk_synth_spec": N.tk_synth_spec,
+               "tk_synth_arrays": S.tk_synth_arrays, "tk_synth_spec": S.tk_synth_spec,
                "tk_mapper_config": N.tk_mapper_config, "tk_frame_view": N.tk_frame_view,
                "tk_scene_out": N.tk_scene_out, "tk_source_view": N.tk_source_view}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "tk_render.h"', '#include "tk_synth.h"',
@@ -56,7 +59,7 @@ def test_struct_layouts_match_header(tmp_path):
     src.write_text("\n".join(lines))
     exe = tmp_path / "layout"
     import subprocess
-    subprocess.run(["gcc", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    subprocess.run(["gcc", "-I" + os.path.join(ROOT, "include"), "-I" + HEADER_DIRS["tk_synth.h"], str(src), "-o", str(exe)], check=True)
     got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
     for name, cls in structs.items():
         assert int(got[name]) == C.sizeof(cls), name
@@ -104,7 +107,7 @@ def test_create_without_gpu_fails_cleanly():
 
 
 def test_synth_generators_are_deterministic():
-    from paper_2602_06991_b200 import synth
+    import scenegen as synth
     a = synth.random_scene(50, 8, 3)
     b = synth.random_scene(50, 8, 3)
     assert (a.mean == b.mean).all() and (a.feature == b.feature).all()

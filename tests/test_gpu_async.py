@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 from paper_2602_06991_b200 import _native as N
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.api import to_camera, to_pose, to_settings
 from paper_2602_06991_b200.types import Pose, RenderSettings
 

@@ -20,8 +20,13 @@ def run_bench(*args):
     return json.loads(lines[0])
 
 
-def test_bench_line_contract():
-    j = run_bench("--config", "c1", "--steps", "3", "--warmup", "3", "--e2e-steps", "3")
+@pytest.fixture(scope="module")
+def gpu_line():
+    return run_bench("--config", "c1", "--steps", "3", "--warmup", "3", "--e2e-steps", "3")
+
+
+def test_bench_line_contract(gpu_line):
+    j = gpu_line
     for key, typ in [("metric", str), ("value", float), ("unit", str), ("n_gpus", int), ("steps", int),
                      ("warmup", int), ("ms_per_step", float), ("higher_is_better", bool), ("scaling", str),
                      ("dtype", str), ("data", str), ("config", dict), ("gpu_launches", int)]:
@@ -38,9 +43,20 @@ def test_bench_line_contract():
     clk = j["clocks"]
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(clk)
     assert j["step_ms"]["best"] <= j["step_ms"]["median"] <= j["step_ms"]["worst"]
+    fr = j["frame_roofline"]
+    assert 0 < fr["frac"] <= 1.0 and abs(fr["achieved_gbs"] - fr["algorithmic_bytes_per_frame"] /
+                                         (j["ms_per_step"] / 1000.0) / 1e9) < 1e-6 * fr["achieved_gbs"]
+    ks = j["k_sweep"]
+    assert set(ks["k"]) >= {"1", "4", "8", "16"} and all(v["frames_per_s"] > 0 for v in ks["k"].values())
+    assert {"K=1", "K=3", "K=10", "full_blend"} <= set(ks["feature_pass_ms"])
+    grid = j["fslam_bench_grid"]
+    assert len(grid["rows"]) == 2 * 6 and grid["spec_acceptance_4"] is not None
 
 
-def test_reference_arm_line():
-    j = run_bench("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1")
+def test_reference_arm_line(gpu_line):
+    j = run_bench("--impl", "reference", "--config", "c1", "--steps", "2", "--warmup", "3")
     assert j["impl"] == "reference" and j["value"] > 0 and j["unit"] == "frames/s"
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["cpu_baseline"]["kind"] in ("port", "reference")
+    # honest about what ran: one warm-up frame, then the frames actually timed; same config object
+    assert j["warmup"] == 1 and 1 <= j["steps"] <= 2 and j["steps_requested"] == 2
+    assert j["config"] == gpu_line["config"] and j["metric"] == gpu_line["metric"]

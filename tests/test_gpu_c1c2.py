@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import RenderSettings
 
 pytestmark = pytest.mark.gpu
@@ -47,3 +48,24 @@ def test_c1_c2_forward_backward_match_oracle(scene, k):
         a, b = getattr(gg, f), go[f]
         scale = max(1e-12, np.abs(b).max())
         np.testing.assert_array_less(np.abs(a - b), 1e-4 * np.maximum(np.abs(b), 1e-2 * scale) + 1e-12)
+
+
+def test_c1_full_blend_matches_oracle(scene):
+    """render_feature_full_blend (render.cpp:242-289, 339-343: every contributor, no
+    renormalisation) at full config-1 size against the oracle."""
+    r, m, cam, pose = scene
+    s = RenderSettings()
+    f = r.render_feature_full_blend(m, pose, cam, s)
+    o = O.render_feature_full_blend(m, pose, cam, s)
+    assert (np.abs(f.astype(np.float64) - o) <= 2e-5 * np.maximum(1.0, np.abs(o))).all()
+
+
+def test_c1_backward_geometric_bit_deterministic(scene):
+    r, m, cam, pose = scene
+    s = RenderSettings(top_k=3)
+    gc = synth.uniform_image((H, W, 3), 12)
+    gd = synth.uniform_image((H, W), 13)
+    a = r.backward_geometric(m, pose, cam, s, gc, gd)
+    b = r.backward_geometric(m, pose, cam, s, gc, gd)
+    for f in ("mean", "log_scale", "rotation", "opacity_logit", "color", "pose_twist"):
+        assert getattr(a, f).tobytes() == getattr(b, f).tobytes(), f

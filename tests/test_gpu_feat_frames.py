@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 
 from paper_2602_06991_b200 import _native as N
-from paper_2602_06991_b200 import api, dataset, synth
+from paper_2602_06991_b200 import api, dataset
+import scenegen as synth
 from paper_2602_06991_b200.types import Frame, MapperConfig, Pose, RenderSettings
 
 pytestmark = pytest.mark.gpu

@@ -8,7 +8,8 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import RenderSettings
 
 pytestmark = pytest.mark.gpu
@@ -143,3 +144,63 @@ def test_fullsize_mapping_iterations_match_oracle(full):
     assert dev.max() <= 2 * cfg.lr_feature + 2e-5
     assert (g["topk_count"] == o["topk_count"]).all()
     np.testing.assert_allclose(g["max_contribution"], o["max_contribution"], rtol=1e-9, atol=0)
+
+
+def test_fullsize_backward_feature_matches_oracle_elementwise(full):
+    """backward_feature at config 3 element by element against the oracle, run one 64-channel
+    slice at a time (the op never mixes channels, so each slice is exact) to keep the oracle's
+    per-thread N x D fp64 partials within host RAM."""
+    r, m, cam, pose = full
+    g = r.render_geometric(m, pose, cam, RenderSettings(top_k=K))
+    G = synth.uniform_image((H, W, D), 11).astype(np.float32)
+    df = r.backward_feature(m, g.topk, G).reshape(m.size(), D)
+    for c0, c1, o in O.backward_feature_slices(m, W, H, K, g.topk.index, g.topk.weight, g.topk.count, G):
+        a = df[:, c0:c1].astype(np.float64)
+        bad = np.abs(a - o) > 2e-5 * np.maximum(1.0, np.abs(o))
+        assert not bad.any(), (c0, c1, int(bad.sum()))
+        # rows no record references are exactly zero on both sides (dense N x D, backward.cpp:315)
+        assert np.array_equal((a == 0).all(axis=1), (o == 0).all(axis=1)), (c0, c1)
+
+
+GEOM_FIELDS = ("mean", "log_scale", "rotation", "opacity_logit", "color", "pose_twist")
+
+
+def test_fullsize_backward_geometric_bit_deterministic(full):
+    """backward_geometric twice on fresh forwards (the drop-in re-uploads and re-prepares on every
+    call): every gradient byte-identical (the reference merges its per-thread partials in a fixed
+    order, backward.cpp:166-178; the GPU sums each Gaussian's slot partials in a fixed order)."""
+    r, m, cam, pose = full
+    s = RenderSettings(top_k=K)
+    gc = synth.uniform_image((H, W, 3), 12)
+    gd = synth.uniform_image((H, W), 13)
+    a = r.backward_geometric(m, pose, cam, s, gc, gd)
+    for _ in range(2):
+        b = r.backward_geometric(m, pose, cam, s, gc, gd)
+        for f in GEOM_FIELDS:
+            assert getattr(a, f).tobytes() == getattr(b, f).tobytes(), f
+
+
+def test_fullsize_mapping_run_bit_deterministic(full):
+    """Ten tk_optimize_step iterations (features every 5th step) from the same start, twice: the
+    optimised map, its Adam-driven geometry and the selection statistics are byte-identical."""
+    from paper_2602_06991_b200.types import MapperConfig
+    r, m, cam, pose = full
+    emb = synth.unit_features(4, D, 99)
+    gt, _ = synth.render_ground_truth(r, m, m.class_ids, emb, [pose], cam)[0]
+    rng = np.random.default_rng(23)
+    spacing = float(np.median(np.exp(m.log_scale[:, 0]))) * 2.0
+    mp = m.copy()
+    mp.mean = m.mean + rng.normal(0.0, 0.3 * spacing, m.mean.shape)
+    cfg = MapperConfig()
+    s = RenderSettings(top_k=K)
+    runs = []
+    for _ in range(2):
+        r.upload(mp)
+        r.optimizer_reset(True)
+        r.keyframe_set(0, pose, gt)
+        losses = [r.optimize_step(cfg, cam, s, 0, it)[0] for it in range(10)]
+        runs.append((r.scene_download(mp.size(), D), [(v.map, v.geo, v.feat) for v in losses]))
+    (a, la), (b, lb) = runs
+    assert la == lb
+    for key in a:
+        assert a[key].tobytes() == b[key].tobytes(), key

@@ -10,7 +10,8 @@ import pytest
 import torch
 
 from paper_2602_06991_b200 import _native as N
-from paper_2602_06991_b200 import api, dist, synth
+from paper_2602_06991_b200 import api, dist
+import scenegen as synth
 from paper_2602_06991_b200.types import Pose, RenderSettings
 
 pytestmark = pytest.mark.gpu

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import Pose, RenderSettings
 
 pytestmark = pytest.mark.gpu

@@ -20,7 +20,8 @@ import numpy as np
 sys.path.insert(0, sys.argv[1])
 sys.path.insert(0, sys.argv[1] + "/tests")
 from _se3 import axis_angle
-from paper_2602_06991_b200 import _native as N, api, synth
+from paper_2602_06991_b200 import _native as N, api
+import scenegen as synth
 from paper_2602_06991_b200.api import to_camera, to_pose, to_settings
 from paper_2602_06991_b200.types import Frame, MapperConfig, Pose, RenderSettings
 

@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 import torch
 
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import Frame, MapperConfig, Pose, RenderSettings
 
 pytestmark = pytest.mark.gpu

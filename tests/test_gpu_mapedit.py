@@ -11,7 +11,8 @@ import pytest
 
 import _oracle as O
 from _se3 import axis_angle
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import Frame, MapperConfig, Pose, RenderSettings, SceneMap
 
 pytestmark = pytest.mark.gpu

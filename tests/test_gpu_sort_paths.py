@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import RenderSettings
 
 pytestmark = pytest.mark.gpu
@@ -19,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
-from paper_2602_06991_b200 import api, synth
+from paper_2602_06991_b200 import api
+import scenegen as synth
 from paper_2602_06991_b200.types import RenderSettings
 m, cam, pose, _ = synth.bench_scene(int(sys.argv[3]), 320, 240, 4)
 p = api.Renderer(0).prepare_scene(m, pose, cam, RenderSettings())

@@ -14,6 +14,8 @@ import torch.multiprocessing as mp
 
 from paper_2602_06991_b200 import dist as tkdist
 
+import _dist_ref as dref
+
 
 def _free_port():
     s = socket.socket()
@@ -45,11 +47,11 @@ def _worker(rank, world, port, q):
     try:
         feat, index, weight, count, K = _records()
         mine = tkdist.shard_features(feat, world, rank)
-        part = tkdist.gather_reference(mine, index, weight, count, K)
+        part = dref.gather_reference(mine, index, weight, count, K)
         parts = [torch.zeros_like(torch.from_numpy(part)) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(part))
         full = tkdist.interleave([p.numpy() for p in parts])
-        ref = tkdist.gather_reference(feat, index, weight, count, K)
+        ref = dref.gather_reference(feat, index, weight, count, K)
         uid = tkdist.broadcast_bytes(dist, bytes(range(128)) if rank == 0 else None, 128)
         tmax = tkdist.max_over_ranks(dist, 1.0 + rank)
         q.put((rank, bool(np.array_equal(full, ref)), uid == bytes(range(128)), tmax))
@@ -86,13 +88,13 @@ def _feature_step_worker(rank, world, port, q):
             return t.numpy()
 
         c0, c1 = tkdist.shard_range(D, world, rank)
-        fs, ms, vs, l1 = tkdist.feature_step_shard(F[:, c0:c1], gt[:, c0:c1], count, index, weight,
+        fs, ms, vs, l1 = dref.feature_step_shard(F[:, c0:c1], gt[:, c0:c1], count, index, weight,
                                                    feat=feat[:, c0:c1], m=m0[:, c0:c1], v=v0[:, c0:c1],
                                                    allreduce_max=amax, allreduce_sum=asum, **args)
         parts = [torch.zeros_like(torch.from_numpy(np.ascontiguousarray(fs))) for _ in range(world)]
         dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(fs)))
         full_f = np.concatenate([p.numpy() for p in parts], axis=1)
-        ref_f, _, _, ref_l1 = tkdist.feature_step_shard(F, gt, count, index, weight, feat=feat, m=m0, v=v0,
+        ref_f, _, _, ref_l1 = dref.feature_step_shard(F, gt, count, index, weight, feat=feat, m=m0, v=v0,
                                                         allreduce_max=lambda x: x, allreduce_sum=lambda x: x, **args)
         q.put((rank, float(np.abs(full_f - ref_f).max()), abs(l1 - ref_l1)))
     finally:

@@ -12,7 +12,7 @@ import pytest
 
 import _oracle as O
 from _se3 import axis_angle, rel_error, se3_apply_twist
-from paper_2602_06991_b200 import synth
+import scenegen as synth
 from paper_2602_06991_b200.types import CameraIntrinsics, Pose, RenderSettings, SceneMap
 
 
@@ -160,7 +160,7 @@ def test_stale_topk_index_is_a_hard_error():  # test_raster.cpp:243-253
 def test_k_covering_every_contributor_matches_full_blend():  # test_raster.cpp:255-283
     m = synth.random_scene(40, 5, 31)
     rng = np.random.Generator(np.random.MT19937(0))
-    from paper_2602_06991_b200.synth import uniform_image
+    from scenegen import uniform_image
     m.log_scale[:] = np.repeat(uniform_image((40,), 77, -4.5, -3.5)[:, None], 3, axis=1)
     cam = synth.test_camera(40, 40)
     s = RenderSettings(top_k=32, transmittance_floor=0.0)

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import _oracle as O
-from paper_2602_06991_b200 import synth
+import scenegen as synth
 from paper_2602_06991_b200.types import MapperConfig, Pose, RenderSettings, SceneMap
 
 
