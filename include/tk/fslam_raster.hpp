@@ -18,9 +18,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tk_render.h"
@@ -68,6 +70,11 @@ struct SceneMap {  // scene_map.hpp:16-27
     std::vector<Gaussian3D> gaussians;
     std::uint64_t generation = 0;
     int feature_dim = 0;
+    // Not in the reference: edit counters for the device mirror's UploadPolicy::kVersioned.  A
+    // caller that edits parameters in place (optimize_step's Adam, mapper.cpp:183-252) bumps
+    // geometry_version / feature_version; structural edits bump generation as in the reference.
+    std::uint64_t geometry_version = 0;
+    std::uint64_t feature_version = 0;
     std::size_t size() const { return gaussians.size(); }
     bool empty() const { return gaussians.empty(); }
 };
@@ -106,6 +113,11 @@ struct TopKGrid {  // render.hpp:27-44
     std::vector<std::int32_t> index;
     std::vector<double> weight;
     std::vector<std::uint8_t> count;
+    // Not in the reference: set by Renderer::render_geometric to name the records the context
+    // still holds on the device, so render_feature / backward_feature on this grid skip the
+    // host -> device copy of index / weight / count.  Records are treated as the immutable value
+    // outputs they are in the reference; a grid built or edited by hand must keep device_token 0.
+    std::uint64_t device_token = 0;
     TopKGrid() = default;
     TopKGrid(int w, int h, int kk)
         : width(w), height(h), k(kk), index(static_cast<std::size_t>(w) * h * kk, -1),
@@ -171,50 +183,114 @@ inline tk_settings to_c(const RenderSettings& s) {
 }
 }  // namespace detail
 
-// One device context.  Every entry point uploads the map it is given (the reference takes the
-// map by const reference on every call, so in-place edits between calls are always seen).
+// Upload policy of the device mirror.
+//   kAlways    (default): the reference's pure semantics -- every entry point copies the parts of the
+//              map it reads (geometry for prepare / render_geometric / backward_geometric, features
+//              for render_feature, both for the full blend; backward_feature reads only the map's
+//              size and feature_dim), so in-place edits between calls are always seen.
+//   kVersioned: a part is copied only when (generation, size, feature_dim, its version counter)
+//              differs from the copy on the device (the mirror keyed by
+//              SceneMap::generation plus explicit dirty counters).  The caller bumps
+//              SceneMap::geometry_version / feature_version after in-place edits.
+enum class UploadPolicy { kAlways, kVersioned };
+
+// One device context with a resident copy of the last map it was given.  Host staging is pinned
+// (tk_host_alloc) and packed by several threads for large maps.
 class Renderer {
 public:
-    explicit Renderer(int device = 0) { detail::check(tk_create(device, &ctx_)); }
-    ~Renderer() { tk_destroy(ctx_); }
+    explicit Renderer(int device = 0, UploadPolicy policy = UploadPolicy::kAlways) : policy_(policy) {
+        detail::check(tk_create(device, &ctx_));
+    }
+    ~Renderer() {
+        tk_destroy(ctx_);
+        for (auto& b : pinned_) tk_host_free(b.p);
+    }
     Renderer(const Renderer&) = delete;
     Renderer& operator=(const Renderer&) = delete;
     tk_ctx* context() const { return ctx_; }
+    void set_policy(UploadPolicy p) { policy_ = p; }
+    // bytes copied host -> device for the map so far (geometry, features) -- the boundary's cost
+    std::uint64_t geometry_bytes_uploaded() const { return geo_bytes_; }
+    std::uint64_t feature_bytes_uploaded() const { return feat_bytes_; }
+    void invalidate() { geo_key_.valid = feat_key_.valid = false; }
 
+    // Whole map (geometry + features), as before: kept for callers that want one explicit upload.
     void upload(const SceneMap& m) {
+        sync_geometry(m, true);
+        sync_features(m, true);
+    }
+
+    // The geometry half: SoA fp64 mean / log_scale / rotation / opacity_logit / color.
+    void sync_geometry(const SceneMap& m, bool force = false) {
         const std::size_t n = m.size();
         const int d = m.feature_dim;
-        mean_.resize(n * 3);
-        ls_.resize(n * 3);
-        rot_.resize(n * 4);
-        op_.resize(n);
-        col_.resize(n * 3);
-        feat_.assign(n * static_cast<std::size_t>(d), 0.0f);
-        for (std::size_t i = 0; i < n; ++i) {
-            const Gaussian3D& g = m.gaussians[i];
-            const double mv[3] = {g.mean.x, g.mean.y, g.mean.z}, lv[3] = {g.log_scale.x, g.log_scale.y, g.log_scale.z};
-            const double cv[3] = {g.color.x, g.color.y, g.color.z};
-            for (int a = 0; a < 3; ++a) {
-                mean_[i * 3 + a] = mv[a];
-                ls_[i * 3 + a] = lv[a];
-                col_[i * 3 + a] = cv[a];
+        const Key key{m.generation, n, d, m.geometry_version, true};
+        if (!force && policy_ == UploadPolicy::kVersioned && key == geo_key_) return;
+        double* mean = stage<double>(0, n * 3);
+        double* ls = stage<double>(1, n * 3);
+        double* rot = stage<double>(2, n * 4);
+        double* op = stage<double>(3, n);
+        double* col = stage<double>(4, n * 3);
+        parallel_rows(n, n * 14, [&](std::size_t i0, std::size_t i1) {
+            for (std::size_t i = i0; i < i1; ++i) {
+                const Gaussian3D& g = m.gaussians[i];
+                mean[i * 3 + 0] = g.mean.x;
+                mean[i * 3 + 1] = g.mean.y;
+                mean[i * 3 + 2] = g.mean.z;
+                ls[i * 3 + 0] = g.log_scale.x;
+                ls[i * 3 + 1] = g.log_scale.y;
+                ls[i * 3 + 2] = g.log_scale.z;
+                rot[i * 4 + 0] = g.rotation.w;
+                rot[i * 4 + 1] = g.rotation.x;
+                rot[i * 4 + 2] = g.rotation.y;
+                rot[i * 4 + 3] = g.rotation.z;
+                op[i] = g.opacity_logit;
+                col[i * 3 + 0] = g.color.x;
+                col[i * 3 + 1] = g.color.y;
+                col[i * 3 + 2] = g.color.z;
             }
-            rot_[i * 4 + 0] = g.rotation.w;
-            rot_[i * 4 + 1] = g.rotation.x;
-            rot_[i * 4 + 2] = g.rotation.y;
-            rot_[i * 4 + 3] = g.rotation.z;
-            op_[i] = g.opacity_logit;
-            for (int c = 0; c < d && c < static_cast<int>(g.feature.size()); ++c)
-                feat_[i * d + c] = static_cast<float>(g.feature[c]);
+        });
+        // a new size or feature_dim invalidates the resident features: ship them in the same call
+        const bool reshape = !dev_shape_valid_ || dev_n_ != n || dev_d_ != d;
+        const float* feat = nullptr;
+        if (reshape) {
+            feat = pack_features(m);
+            feat_key_ = Key{m.generation, n, d, m.feature_version, true};
+            feat_bytes_ += n * static_cast<std::uint64_t>(d) * sizeof(float);
         }
-        tk_scene_view v{static_cast<int64_t>(n), d, mean_.data(), ls_.data(), rot_.data(), op_.data(), col_.data(),
-                        feat_.data(), m.generation};
+        tk_scene_view v{static_cast<int64_t>(n), d, mean, ls, rot, op, col, feat, m.generation};
         detail::check(tk_scene_upload(ctx_, &v, TK_HOST));
+        geo_bytes_ += n * 14 * sizeof(double);
+        geo_key_ = key;
+        dev_shape_valid_ = true;
+        dev_n_ = n;
+        dev_d_ = d;
+    }
+
+    // The feature half: fp32 rows N x D (the reference's unit-norm fp64 features, rounded once).
+    void sync_features(const SceneMap& m, bool force = false) {
+        const std::size_t n = m.size();
+        const int d = m.feature_dim;
+        if (!dev_shape_valid_ || dev_n_ != n || dev_d_ != d) {
+            sync_geometry(m, true);  // ships the features with the new shape
+            return;
+        }
+        const Key key{m.generation, n, d, m.feature_version, true};
+        if (!force && policy_ == UploadPolicy::kVersioned && key == feat_key_) return;
+        const float* feat = pack_features(m);
+        detail::check(tk_scene_upload_features(ctx_, static_cast<int64_t>(n), d, feat, TK_HOST));
+        feat_bytes_ += n * static_cast<std::uint64_t>(d) * sizeof(float);
+        feat_key_ = key;
+    }
+
+    // Only the map's size and feature_dim on the device (backward_feature).
+    void sync_shape(const SceneMap& m) {
+        if (!dev_shape_valid_ || dev_n_ != m.size() || dev_d_ != m.feature_dim) sync_geometry(m, true);
     }
 
     raster_detail::PreparedScene prepare_scene(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
                                                const RenderSettings& s) {
-        upload(m);
+        sync_geometry(m);
         const tk_pose p = detail::to_c(pose);
         const tk_camera c = detail::to_c(cam);
         const tk_settings st = detail::to_c(s);
@@ -242,7 +318,7 @@ public:
 
     RenderOutput render_geometric(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
                                   const RenderSettings& s) {  // render.cpp:293-299
-        upload(m);
+        sync_geometry(m);
         const int w = cam.width, h = cam.height, k = std::min(std::max(s.top_k, 0), kMaxTopK);
         RenderOutput out;
         out.color = ImageD(w, h, 3);
@@ -259,46 +335,54 @@ public:
         detail::check(tk_render_geometric(ctx_, &p, &c, &st, &g));
         out.generation = g.generation;
         out.map_size = static_cast<std::size_t>(g.map_size);
+        out.topk.device_token = records_token_ = ++token_seq_;  // the context now holds these records
         return out;
     }
 
     ImageD render_feature(const SceneMap& m, const TopKGrid& t) {  // render.cpp:301-337
-        upload(m);
+        sync_features(m);
         std::vector<float> f(static_cast<std::size_t>(t.width) * t.height * m.feature_dim);
         tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
-        detail::check(tk_render_feature(ctx_, &v, f.data(), TK_HOST));
+        detail::check(tk_render_feature(ctx_, resident(t) ? nullptr : &v, f.data(), TK_HOST));
         ImageD out(t.width, t.height, m.feature_dim);
-        for (std::size_t i = 0; i < f.size(); ++i) out.data[i] = f[i];
+        widen(f, out.data);
         return out;
     }
 
     ImageD render_feature_full_blend(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
                                      const RenderSettings& s) {  // render.cpp:339-343
-        upload(m);
+        sync_geometry(m);
+        sync_features(m);
         std::vector<float> f(static_cast<std::size_t>(cam.width) * cam.height * m.feature_dim);
         const tk_pose p = detail::to_c(pose);
         const tk_camera c = detail::to_c(cam);
         const tk_settings st = detail::to_c(s);
         detail::check(tk_render_feature_full_blend(ctx_, &p, &c, &st, f.data(), TK_HOST));
         ImageD out(cam.width, cam.height, m.feature_dim);
-        for (std::size_t i = 0; i < f.size(); ++i) out.data[i] = f[i];
+        widen(f, out.data);
         return out;
     }
 
     std::vector<double> backward_feature(const SceneMap& m, const TopKGrid& t,
                                          const ImageD& grad_feature) {  // backward.cpp:273-321
-        upload(m);
-        std::vector<float> g(grad_feature.data.begin(), grad_feature.data.end());
+        sync_shape(m);
+        float* g = stage<float>(6, grad_feature.data.size());
+        const double* gs = grad_feature.data.data();
+        parallel_rows(grad_feature.data.size(), grad_feature.data.size(), [&](std::size_t i0, std::size_t i1) {
+            for (std::size_t i = i0; i < i1; ++i) g[i] = static_cast<float>(gs[i]);
+        });
         std::vector<float> o(m.size() * static_cast<std::size_t>(m.feature_dim));
         tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
-        detail::check(tk_backward_feature(ctx_, &v, g.data(), TK_HOST, o.data(), TK_HOST));
-        return std::vector<double>(o.begin(), o.end());
+        detail::check(tk_backward_feature(ctx_, resident(t) ? nullptr : &v, g, TK_HOST, o.data(), TK_HOST));
+        std::vector<double> out(o.size());
+        widen(o, out);
+        return out;
     }
 
     GeomGrads backward_geometric(const SceneMap& m, const Pose& pose, const CameraIntrinsics& cam,
                                  const RenderSettings& s, const ImageD& grad_color,
                                  const ImageD& grad_depth) {  // backward.cpp:72-271
-        upload(m);
+        sync_geometry(m);
         const std::size_t n = m.size();
         std::vector<double> gm(n * 3), gl(n * 3), gr(n * 4), go(n), gc(n * 3);
         tk_geom_grads out{TK_HOST, gm.data(), gl.data(), gr.data(), go.data(), gc.data(), {0, 0, 0, 0, 0, 0}};
@@ -324,9 +408,87 @@ public:
     }
 
 private:
+    struct Key {
+        std::uint64_t generation = 0;
+        std::size_t n = 0;
+        int d = 0;
+        std::uint64_t version = 0;
+        bool valid = false;
+        bool operator==(const Key& o) const {
+            return valid && o.valid && generation == o.generation && n == o.n && d == o.d && version == o.version;
+        }
+    };
+    struct Pinned {
+        void* p = nullptr;
+        std::size_t bytes = 0;
+    };
+
+    template <class T>
+    T* stage(int slot, std::size_t count) {  // pinned staging buffer `slot`, grown on demand
+        if (pinned_.size() <= static_cast<std::size_t>(slot)) pinned_.resize(slot + 1);
+        Pinned& b = pinned_[slot];
+        const std::size_t need = std::max<std::size_t>(count, 1) * sizeof(T);
+        if (b.bytes < need) {
+            if (b.p) tk_host_free(b.p);
+            b.p = nullptr;
+            b.bytes = 0;
+            detail::check(tk_host_alloc(need, &b.p));
+            b.bytes = need;
+        }
+        return static_cast<T*>(b.p);
+    }
+
+    const float* pack_features(const SceneMap& m) {
+        const std::size_t n = m.size();
+        const int d = m.feature_dim;
+        float* f = stage<float>(5, n * static_cast<std::size_t>(d));
+        parallel_rows(n, n * static_cast<std::size_t>(d), [&](std::size_t i0, std::size_t i1) {
+            for (std::size_t i = i0; i < i1; ++i) {
+                const std::vector<double>& src = m.gaussians[i].feature;
+                const int c1 = std::min<int>(d, static_cast<int>(src.size()));
+                float* row = f + i * static_cast<std::size_t>(d);
+                for (int c = 0; c < c1; ++c) row[c] = static_cast<float>(src[c]);
+                for (int c = c1; c < d; ++c) row[c] = 0.0f;
+            }
+        });
+        return f;
+    }
+
+    // rows [0, n) split over the host's threads when the copy is large (>= 4M elements)
+    template <class F>
+    static void parallel_rows(std::size_t n, std::size_t elems, F&& fn) {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned t = elems < (std::size_t(1) << 22) ? 1u : std::min<unsigned>(hw, 32u);
+        if (t <= 1 || n < t) {
+            fn(std::size_t(0), n);
+            return;
+        }
+        std::vector<std::thread> pool;
+        const std::size_t step = (n + t - 1) / t;
+        for (unsigned k = 0; k < t; ++k) {
+            const std::size_t i0 = std::min(n, k * step), i1 = std::min(n, i0 + step);
+            if (i0 < i1) pool.emplace_back([&fn, i0, i1] { fn(i0, i1); });
+        }
+        for (auto& th : pool) th.join();
+    }
+
+    static void widen(const std::vector<float>& f, std::vector<double>& d) {  // fp32 results -> fp64 API
+        parallel_rows(f.size(), f.size(), [&](std::size_t i0, std::size_t i1) {
+            for (std::size_t i = i0; i < i1; ++i) d[i] = f[i];
+        });
+    }
+
+    bool resident(const TopKGrid& t) const { return t.device_token != 0 && t.device_token == records_token_; }
+
     tk_ctx* ctx_ = nullptr;
-    std::vector<double> mean_, ls_, rot_, op_, col_;
-    std::vector<float> feat_;
+    UploadPolicy policy_ = UploadPolicy::kAlways;
+    std::vector<Pinned> pinned_;
+    Key geo_key_, feat_key_;
+    bool dev_shape_valid_ = false;
+    std::size_t dev_n_ = 0;
+    int dev_d_ = 0;
+    std::uint64_t geo_bytes_ = 0, feat_bytes_ = 0;
+    std::uint64_t records_token_ = 0, token_seq_ = 0;
 };
 
 // Free functions with the reference signatures, on a per-thread default context (device 0).

@@ -164,6 +164,10 @@ tk_status tk_host_alloc(size_t bytes, void** out); /* pinned host memory */
 tk_status tk_host_free(void* p);
 
 tk_status tk_scene_upload(tk_ctx* ctx, const tk_scene_view* scene, int32_t mem);
+/* Replace the resident features only (n, d must match the resident geometry); the geometry, the
+ * prepared scene and the forward records stay valid.  For drop-in callers whose map changed only
+ * in its features (mapper.cpp:239-252, the feature Adam step). */
+tk_status tk_scene_upload_features(tk_ctx* ctx, int64_t n, int32_t d, const float* feature, int32_t mem);
 tk_status tk_device_view_get(tk_ctx* ctx, tk_device_view* out);
 
 tk_status tk_prepare_scene(tk_ctx* ctx, const tk_pose* pose, const tk_camera* cam,

@@ -108,6 +108,7 @@ RENDER_SYMBOLS = [
     ("tk_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     ("tk_host_free", C.c_int, [C.c_void_p]),
     ("tk_scene_upload", C.c_int, [C.c_void_p, C.POINTER(tk_scene_view), C.c_int32]),
+    ("tk_scene_upload_features", C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32]),
     ("tk_device_view_get", C.c_int, [C.c_void_p, C.POINTER(tk_device_view)]),
     ("tk_prepare_scene", C.c_int, [C.c_void_p, C.POINTER(tk_pose), C.POINTER(tk_camera), C.POINTER(tk_settings),
                                    i64_p, i64_p, i32_p, i32_p]),

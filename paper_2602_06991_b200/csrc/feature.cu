@@ -356,6 +356,9 @@ __global__ void k_slot_fill(SlotKeyParams p, const int32_t* __restrict__ seg, in
 // long from the back; counters in counts[0], counts[1]).
 constexpr int kSmallSeg = 16;
 constexpr int kWarpSeg = 1024;
+// k_long_plan visits exactly the segments k_seg_sort_small queued (L > kWarpSeg), and the feature
+// kernels skip exactly the segments with L > kLongSeg: the two thresholds must be one.
+static_assert(kWarpSeg == kLongSeg, "long-segment plan and feature kernels must agree on the threshold");
 constexpr int kSortTile = 8192;
 constexpr int kSortThreads = 512;
 
@@ -645,9 +648,11 @@ inline unsigned warp_grid(int64_t rows) {
     return static_cast<unsigned>(blocks < cap ? (blocks > 0 ? blocks : 1) : cap);
 }
 
-// One warp per row with no grid-stride cap: blocks retire in row order, so the warps in flight
-// cover one contiguous window of rows (k_feat_bwd: the <= K Gaussians that read a pixel's dF row
-// are then closer in time; 0.745 -> 0.729 ms against the capped persistent grid).
+// One warp per row with no grid-stride cap.  Observed on this driver and B200 (not guaranteed by
+// CUDA): blocks are dispatched roughly in index order, so the warps in flight cover a narrow
+// window of rows (k_feat_bwd: the <= K Gaussians that read a pixel's dF row are then closer in
+// time; 0.745 -> 0.729 ms against the capped persistent grid, warp_grid, kept as the fallback if
+// a later measurement regresses).  Correctness never depends on the order.
 inline unsigned warp_grid_all(int64_t rows) {
     return static_cast<unsigned>(std::max<int64_t>(1, (rows + kWarps - 1) / kWarps));
 }

@@ -760,6 +760,22 @@ tk_status tk_scene_upload(tk_ctx* c, const tk_scene_view* s, int32_t mem) {
     });
 }
 
+tk_status tk_scene_upload_features(tk_ctx* c, int64_t n, int32_t d, const float* feature, int32_t mem) {
+    return guarded([&] {
+        if (!c || (!feature && n * d > 0)) fail(TK_ERR_BAD_ARG, "null argument");
+        if (!c->has_scene || n != c->n || d != c->d)
+            fail(TK_ERR_BAD_ARG, "tk_scene_upload_features: n and d must match the resident geometry");
+        CK(cudaSetDevice(c->device));
+        on_main(c);
+        flush_features(c);  // pending lazy rows would otherwise overwrite the new values
+        if (mem == TK_HOST_ASYNC) mem = TK_HOST;
+        copy_in(ensure<float>(c->feature, n * std::max(d, 1)), feature, static_cast<size_t>(n) * d * sizeof(float), mem,
+                c);
+        c->has_features = true;  // geometry, the PreparedScene and the forward state stay valid
+        main_done(c);
+    });
+}
+
 tk_status tk_device_view_get(tk_ctx* c, tk_device_view* v) {
     return guarded([&] {
         std::memset(v, 0, sizeof(*v));
@@ -892,7 +908,8 @@ tk_status tk_backward_feature(tk_ctx* c, const tk_topk_view* topk, const float* 
     return guarded([&] {
         CK(cudaSetDevice(c->device));
         on_side(c, true);
-        require_features(c);
+        // backward.cpp:273-321 reads the map's size and feature_dim only, never feature values
+        if (!c->has_scene) fail(TK_ERR_STATE, "no scene uploaded (tk_scene_upload)");
         const Records r = resolve_records(c, topk, "backward_feature");
         if (r.k > tk::kMaxTopK) fail(TK_ERR_BAD_ARG, "TopKGrid k exceeds 32");
         cudaStream_t st = c->cur;
@@ -1210,6 +1227,8 @@ tk_status tk_comm_p2p_setup(tk_ctx* c, int64_t n_pixels) {
                                       (export_error.empty() ? std::string() : " (" + export_error + ")"));
             }
         c->peer_ipc = true;
+        // the barrier word (tk_render_feature_gathered), initialised once; a max-reduce keeps it 0
+        CK(cudaMemsetAsync(ensure<int32_t>(c->peer_word, 1), 0, sizeof(int32_t), c->cur));
         c->peer_n = c->nranks;
         c->peer_rank = c->rank;
         c->peer_dtotal = c->d_total;
@@ -1243,6 +1262,15 @@ tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float*
         if (reinterpret_cast<uintptr_t>(ptr<float>(c->feature)) % 16) fail(TK_ERR_BAD_ARG, "feature rows misaligned");
         wait_out(c, kOutF);
         tk::GatherParams gp{P, r.k, r.index, r.weight, r.count, ptr<float>(c->feature), c->d, nullptr, r.w, r.h};
+        if (c->comm && c->peer_ipc) {
+            // Stream-ordered rank barrier BEFORE the peer stores: every rank's stream has passed
+            // everything it enqueued before this call -- its reads of the previous frame's
+            // gathered buffer included -- so this frame's stores cannot overwrite a map a peer is
+            // still reading (write-after-read across ranks).  Readers on other streams must be
+            // ordered before the next call by the caller (tk_comm_gathered_buffer contract).
+            NK(g_nccl.AllReduce(ptr<int32_t>(c->peer_word), ptr<int32_t>(c->peer_word), 1, ncclInt32, ncclMax,
+                                c->comm, c->cur));
+        }
         gp.n_peers = c->peer_n;
         gp.peer_stride = c->peer_dtotal;
         gp.peer_off = c->peer_rank * c->d;
@@ -1253,8 +1281,8 @@ tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float*
         }
         CK_LAUNCH(c);
         if (c->comm && c->peer_ipc) {  // stream-ordered rank barrier: every peer's slice has landed
-            int32_t* w = ensure<int32_t>(c->peer_word, 1);
-            NK(g_nccl.AllReduce(w, w, 1, ncclInt32, ncclSum, c->comm, c->cur));
+            NK(g_nccl.AllReduce(ptr<int32_t>(c->peer_word), ptr<int32_t>(c->peer_word), 1, ncclInt32, ncclMax,
+                                c->comm, c->cur));
         }
         if (out) {
             const size_t bytes = static_cast<size_t>(P) * c->peer_dtotal * sizeof(float);

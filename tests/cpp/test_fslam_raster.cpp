@@ -229,6 +229,45 @@ int main() {
         CHECK(mx == 0.0);
         CHECK(g.pose_twist[0] == 0.0 && g.pose_twist[5] == 0.0);
     }
+    {  // device mirror: resident records, per-part uploads, the versioned policy
+        SceneMap m = random_scene(400, 8, 3);
+        const CameraIntrinsics cam = test_camera(64, 48);
+        RenderSettings s;
+        const RenderOutput a = r.render_geometric(m, Pose::identity(), cam, s);
+        CHECK(a.topk.device_token != 0);
+        TopKGrid host = a.topk;
+        host.device_token = 0;  // forces the host -> device copy of the records
+        const ImageD f_res = r.render_feature(m, a.topk), f_host = r.render_feature(m, host);
+        CHECK(f_res.data == f_host.data);
+        ImageD gf(64, 48, 8);
+        for (size_t i = 0; i < gf.data.size(); ++i) gf.data[i] = std::cos(0.11 * static_cast<double>(i));
+        CHECK(r.backward_feature(m, a.topk, gf) == r.backward_feature(m, host, gf));
+        // kAlways sees an in-place edit; kVersioned sees it once the caller bumps the counter
+        Renderer rv(0, UploadPolicy::kVersioned);
+        const RenderOutput v0 = rv.render_geometric(m, Pose::identity(), cam, s);
+        const ImageD fv0 = rv.render_feature(m, v0.topk);
+        const uint64_t geo0 = rv.geometry_bytes_uploaded(), feat0 = rv.feature_bytes_uploaded();
+        rv.backward_geometric(m, Pose::identity(), cam, s, ImageD(64, 48, 3, 0.5), ImageD(64, 48, 1, 0.25));
+        rv.render_feature(m, v0.topk);
+        CHECK(rv.geometry_bytes_uploaded() == geo0 && rv.feature_bytes_uploaded() == feat0);  // nothing re-sent
+        for (auto& g : m.gaussians) g.feature[0] = -g.feature[0];
+        CHECK(r.render_feature(m, a.topk).data != f_res.data);    // kAlways: the edit is seen
+        CHECK(rv.render_feature(m, v0.topk).data == fv0.data);    // kVersioned, no bump: resident copy
+        m.feature_version += 1;
+        CHECK(rv.render_feature(m, v0.topk).data == r.render_feature(m, a.topk).data);
+        CHECK(rv.feature_bytes_uploaded() > feat0 && rv.geometry_bytes_uploaded() == geo0);
+        m.gaussians[7].mean.x += 0.05;
+        m.geometry_version += 1;
+        const RenderOutput v1 = rv.render_geometric(m, Pose::identity(), cam, s);
+        const RenderOutput a1 = r.render_geometric(m, Pose::identity(), cam, s);
+        CHECK(v1.topk.index == a1.topk.index && v1.color.data == a1.color.data);
+        CHECK(rv.geometry_bytes_uploaded() > geo0);
+        m.gaussians.pop_back();  // structural edit: size change ships both halves
+        m.generation += 1;
+        const RenderOutput v2 = rv.render_geometric(m, Pose::identity(), cam, s);
+        const RenderOutput a2 = r.render_geometric(m, Pose::identity(), cam, s);
+        CHECK(v2.topk.index == a2.topk.index && rv.render_feature(m, v2.topk).data == r.render_feature(m, a2.topk).data);
+    }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
