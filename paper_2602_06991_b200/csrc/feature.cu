@@ -319,9 +319,13 @@ __global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
     }
 }
 
-// Inverted index (Gaussian -> record slots) by counting: count, scan, fill, then sort every
-// segment by slot so the reduction order never depends on the atomic fill order.
-__global__ void k_slot_count(SlotKeyParams p, int32_t* __restrict__ cnt) {
+// Inverted index (Gaussian -> record slots) by a stable radix sort: key = Gaussian id of the slot
+// (n for an empty slot: it sorts past every segment), value = slot id.  Slots enter in ascending
+// order and the LSD sort is stable, so every Gaussian's records come out in slot (pixel, j) order
+// -- the fixed reduction order of backward_feature -- with no atomics and no per-segment sort, at a
+// cost independent of how many records one Gaussian owns (a near-camera Gaussian in the Top-K of
+// every pixel: one segment of P records).  The renormalised slot weight is computed on the way.
+__global__ void k_slot_keys(SlotKeyParams p, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= p.n_slots) return;
     const int64_t px = s / p.k;
@@ -329,167 +333,30 @@ __global__ void k_slot_count(SlotKeyParams p, int32_t* __restrict__ cnt) {
     const int c = p.count[px];
     const int32_t id = p.index[s];
     float wn = 0.0f;
+    uint32_t key = static_cast<uint32_t>(p.n_gaussians);
     if (j < c && id >= 0) {
-        atomicAdd(&cnt[id], 1);
+        key = static_cast<uint32_t>(id);
         double sum = 0.0;                                    // backward.cpp:303-304, slot order
         for (int jj = 0; jj < c; ++jj) sum += p.weight[px * p.k + jj];
         wn = static_cast<float>(p.weight[s] / sum);
     }
     p.wnorm[s] = wn;
+    keys[s] = key;
+    vals[s] = static_cast<uint32_t>(s);
 }
 
-__global__ void k_slot_fill(SlotKeyParams p, const int32_t* __restrict__ seg, int32_t* __restrict__ cursor,
-                            uint32_t* __restrict__ recs) {
-    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= p.n_slots) return;
-    const int64_t px = s / p.k;
-    const int j = static_cast<int>(s - px * p.k);
-    const int32_t id = p.index[s];
-    if (j < p.count[px] && id >= 0) recs[seg[id] + atomicAdd(&cursor[id], 1)] = static_cast<uint32_t>(s);
-}
-
-// Deterministic order inside each Gaussian's record segment (ascending slot id), by length tier:
-// <= kSmallSeg records: one thread ranks them (count of smaller ids, from L1);
-// <= kWarpSeg: one warp (rank counts up to 128 records, a shared-memory bitonic sort beyond);
-// longer: one block bitonic-sorts kSortTile-record tiles and merges them by rank.
-// The medium and long segments are queued by the thread pass (medium from the front of `queue`,
-// long from the back; counters in counts[0], counts[1]).
-constexpr int kSmallSeg = 16;
-constexpr int kWarpSeg = 1024;
-// k_long_plan visits exactly the segments k_seg_sort_small queued (L > kWarpSeg), and the feature
-// kernels skip exactly the segments with L > kLongSeg: the two thresholds must be one.
-static_assert(kWarpSeg == kLongSeg, "long-segment plan and feature kernels must agree on the threshold");
-constexpr int kSortTile = 8192;
-constexpr int kSortThreads = 512;
-
-__global__ void k_seg_sort_small(const int32_t* __restrict__ seg, int64_t n, const uint32_t* __restrict__ recs,
-                                 uint32_t* __restrict__ sorted, int32_t* __restrict__ queue,
-                                 int32_t* __restrict__ counts) {
+// Segments longer than kLongSeg go to the chunked path: queued at the back of `queue`
+// (queue[n - 1 - i], i < counts[1]); the queue order is irrelevant (each segment is summed by its
+// own chunks and combined in chunk order).
+__global__ void k_long_queue(const int32_t* __restrict__ seg, int64_t n, int32_t* __restrict__ queue,
+                             int32_t* __restrict__ counts) {
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
-         g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int r0 = seg[g], L = seg[g + 1] - r0;
-        if (L > kWarpSeg) {
-            queue[n - 1 - atomicAdd(counts + 1, 1)] = static_cast<int32_t>(g);
-            continue;
-        }
-        if (L > kSmallSeg) {
-            queue[atomicAdd(counts, 1)] = static_cast<int32_t>(g);
-            continue;
-        }
-        for (int i = 0; i < L; ++i) {
-            const uint32_t v = recs[r0 + i];
-            int rank = 0;
-            for (int q = 0; q < L; ++q) rank += recs[r0 + q] < v ? 1 : 0;
-            sorted[r0 + rank] = v;
-        }
-    }
+         g += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (seg[g + 1] - seg[g] > kLongSeg) queue[n - 1 - atomicAdd(counts + 1, 1)] = static_cast<int32_t>(g);
 }
 
-struct WarpSync {
-    __device__ void operator()() const { __syncwarp(); }
-};
-struct BlockSync {
-    __device__ void operator()() const { __syncthreads(); }
-};
-
-// In-place ascending bitonic sort of a[0..m), m a power of two, by `nthreads` cooperating threads
-// with index `t`; `sync` is the matching barrier (__syncwarp / __syncthreads).
-template <class Sync>
-__device__ __forceinline__ void bitonic_sort(uint32_t* a, int m, int t, int nthreads, Sync sync) {
-    for (int size = 2; size <= m; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            sync();
-            for (int i = t; i < (m >> 1); i += nthreads) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = (lo & size) == 0;
-                const uint32_t x = a[lo], y = a[hi];
-                if ((x > y) == up) {
-                    a[lo] = y;
-                    a[hi] = x;
-                }
-            }
-        }
-    sync();
-}
-
-__global__ void __launch_bounds__(kThreads) k_seg_sort_warp(const int32_t* __restrict__ seg,
-                                                            const int32_t* __restrict__ queue,
-                                                            const int32_t* __restrict__ counts,
-                                                            const uint32_t* __restrict__ recs,
-                                                            uint32_t* __restrict__ sorted) {
-    __shared__ uint32_t buf[kWarps][kWarpSeg];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int nm = counts[0];
-    uint32_t* a = buf[warp];
-    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; w < nm; w += nw) {
-        const int64_t g = queue[w];
-        const int r0 = seg[g], L = seg[g + 1] - r0;
-        if (L <= 128) {  // short enough for a direct rank count (L^2 / 32 compares per lane)
-            for (int i = lane; i < L; i += 32) {
-                const uint32_t v = recs[r0 + i];
-                int rank = 0;
-                for (int q = 0; q < L; ++q) rank += __ldg(recs + r0 + q) < v ? 1 : 0;
-                sorted[r0 + rank] = v;
-            }
-            continue;
-        }
-        int m = 32;
-        while (m < L) m <<= 1;
-        for (int i = lane; i < m; i += 32) a[i] = i < L ? recs[r0 + i] : 0xffffffffu;
-        bitonic_sort(a, m, lane, 32, WarpSync{});
-        for (int i = lane; i < L; i += 32) sorted[r0 + i] = a[i];
-        __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(kSortThreads) k_seg_sort_block(const int32_t* __restrict__ seg, int64_t n,
-                                                                 const int32_t* __restrict__ queue,
-                                                                 const int32_t* __restrict__ counts,
-                                                                 uint32_t* __restrict__ recs,
-                                                                 uint32_t* __restrict__ sorted) {
-    __shared__ uint32_t tile[kSortTile];
-    const int nh = counts[1];
-    for (int w = blockIdx.x; w < nh; w += gridDim.x) {
-        const int64_t g = queue[n - 1 - w];
-        const int r0 = seg[g], L = seg[g + 1] - r0;
-        const int ntiles = (L + kSortTile - 1) / kSortTile;
-        for (int t = 0; t < ntiles; ++t) {  // sort each tile; results to sorted[]
-            const int t0 = t * kSortTile, tn = min(kSortTile, L - t0);
-            int m = 1;
-            while (m < tn) m <<= 1;
-            __syncthreads();
-            for (int i = threadIdx.x; i < m; i += blockDim.x) tile[i] = i < tn ? recs[r0 + t0 + i] : 0xffffffffu;
-            bitonic_sort(tile, m, threadIdx.x, blockDim.x, BlockSync{});
-            for (int i = threadIdx.x; i < tn; i += blockDim.x) sorted[r0 + t0 + i] = tile[i];
-        }
-        __syncthreads();
-        if (ntiles == 1) continue;
-        // merge: final rank = rank in own tile + lower bound in every other tile (ids are unique)
-        for (int i = threadIdx.x; i < L; i += blockDim.x) {
-            const uint32_t v = sorted[r0 + i];
-            const int own = i / kSortTile;
-            int rank = i - own * kSortTile;
-            for (int t = 0; t < ntiles; ++t) {
-                if (t == own) continue;
-                int lo = 0, hi = min(kSortTile, L - t * kSortTile);
-                const uint32_t* tp = sorted + r0 + t * kSortTile;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (tp[mid] < v) lo = mid + 1;
-                    else hi = mid;
-                }
-                rank += lo;
-            }
-            recs[r0 + rank] = v;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < L; i += blockDim.x) sorted[r0 + i] = recs[r0 + i];
-        __syncthreads();
-    }
-}
-
+// Inverted index (Gaussian -> record slots) by counting: count, scan, fill, then sort every
+// segment by slot so the reduction order never depends on the atomic fill order.
 // Sum of w_j * dF[px_j] over records [r0, r1) of a segment for the channel pass at `base`
 // (acc4: 4 float4 per lane when VEC, acc1: 4 floats otherwise), records in slot order.
 template <bool VEC>
@@ -571,18 +438,126 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     }
 }
 
-// One thread per queued long segment: reserve its chunk range and list its chunks.
+// backward_feature with the dF rows streamed through shared memory by the TMA unit: a persistent
+// grid of kFbWarps-warp CTAs, one warp per Gaussian (grid-stride in Gaussian order, so the warps
+// in flight cover one window of Gaussians, as in k_feat_bwd).  Lane 0 keeps kFbRing records' dF
+// rows in flight (one cp.async.bulk of D*4 bytes each, completion on a per-slot mbarrier); every
+// lane adds w * row for its NV4 float4 channel groups in record (slot) order -- the same
+// arithmetic and order as k_feat_bwd, so the result is bit-identical -- and writes the dense row
+// with streaming stores.  Rows without records are written as zeros.  Bytes in flight come from
+// the bulk copies, not from warps: a few warps per SM saturate HBM, which leaves registers and
+// issue slots for the fp64 geometry backward running beside it on another stream.
+constexpr int kFbWarps = 4;
+constexpr int kFbRing = 8;
+
+template <int NV4>
+__global__ void __launch_bounds__(kFbWarps * 32) k_feat_bwd_tma(FeatBwdParams p) {
+    extern __shared__ __align__(128) unsigned char fb_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int D = p.d, d4 = D >> 2;
+    const unsigned row_bytes = static_cast<unsigned>(D) * 4u;
+    float4* ring = reinterpret_cast<float4*>(fb_smem) + static_cast<size_t>(warp) * kFbRing * d4;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(fb_smem + static_cast<size_t>(kFbWarps) * kFbRing * row_bytes) +
+                    warp * kFbRing;
+    if (lane == 0) {
+        for (int r = 0; r < kFbRing; ++r) mbar_init(&bar[r], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    unsigned phase_bits = 0;  // parity of each ring slot's next completion
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kFbWarps;
+    for (int64_t g = static_cast<int64_t>(blockIdx.x) * kFbWarps + warp; g < p.n_gaussians; g += nw) {
+        const int r0 = p.seg[g], r1 = p.seg[g + 1];
+        const int L = r1 - r0;
+        if (L > kLongSeg) continue;  // chunked path
+        float4 acc[NV4];
+#pragma unroll
+        for (int m = 0; m < NV4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (L > 0) {
+            // record i's pixel and weight live in lane (i % 32) of the current 32-record batch
+            auto rec = [&](int i, int64_t& px, float& w) {
+                const uint32_t sl = p.slots[r0 + i];
+                px = static_cast<int64_t>(sl / static_cast<uint32_t>(p.k));
+                w = p.wnorm[sl];
+            };
+            int64_t bpx = 0;
+            float bw = 0.f;
+            if (lane < L) rec(lane, bpx, bw);
+            // prologue: the first min(L, kFbRing) rows
+            for (int i = 0; i < L && i < kFbRing; ++i) {
+                const int64_t px = __shfl_sync(0xffffffffu, bpx, i);
+                if (lane == 0) {
+                    mbar_arrive_expect_tx(&bar[i], row_bytes);
+                    bulk_g2s(ring + static_cast<size_t>(i) * d4, p.grad + px * D, row_bytes, &bar[i]);
+                }
+            }
+            int64_t npx = 0;  // the next batch's records (for issuing loads past the batch end)
+            float nwt = 0.f;
+            if (lane < L - 32) rec(32 + lane, npx, nwt);
+            for (int i = 0; i < L; ++i) {
+                if (i > 0 && (i & 31) == 0) {  // next batch
+                    bpx = npx;
+                    bw = nwt;
+                    if (lane + i + 32 < L) rec(i + 32 + lane, npx, nwt);
+                }
+                const int slot = i % kFbRing;
+                const float wj = __shfl_sync(0xffffffffu, bw, i & 31);
+                mbar_wait(&bar[slot], (phase_bits >> slot) & 1u);
+                phase_bits ^= 1u << slot;
+                const float4* row = ring + static_cast<size_t>(slot) * d4;
+                bool live = true;
+                if (!isfinite(wj)) {  // backward.cpp:296-302: a zero dF row is skipped
+                    bool any = false;
+                    for (int q = lane; q < d4; q += 32) {
+                        const float4 v = row[q];
+                        any |= v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
+                    }
+                    live = __any_sync(0xffffffffu, any);
+                }
+                if (live) {
+#pragma unroll
+                    for (int m = 0; m < NV4; ++m) {
+                        const int q = m * 32 + lane;
+                        if (q < d4) acc[m] = fma4(wj, row[q], acc[m]);
+                    }
+                }
+                __syncwarp();  // every lane is done with this slot
+                const int nxt = i + kFbRing;
+                if (nxt < L) {
+                    // pixel of record nxt: batch (nxt >> 5) is the current or the next one
+                    const bool cur_batch = (nxt >> 5) == (i >> 5);
+                    const int64_t pc = __shfl_sync(0xffffffffu, bpx, nxt & 31);
+                    const int64_t pn = __shfl_sync(0xffffffffu, npx, nxt & 31);
+                    if (lane == 0) {
+                        const int64_t px = cur_batch ? pc : pn;
+                        mbar_arrive_expect_tx(&bar[slot], row_bytes);
+                        bulk_g2s(ring + static_cast<size_t>(slot) * d4, p.grad + px * D, row_bytes, &bar[slot]);
+                    }
+                }
+            }
+        }
+        float4* dst = reinterpret_cast<float4*>(p.out + g * D);
+#pragma unroll
+        for (int m = 0; m < NV4; ++m) {
+            const int q = m * 32 + lane;
+            if (q < d4) __stcs(dst + q, acc[m]);
+        }
+    }
+}
+
+// One thread per queued long segment: reserve its partial rows and list its items.
 __global__ void k_long_plan(const int32_t* __restrict__ seg, int64_t n, LongPlan plan) {
     const int nq = *plan.qcount;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x) {
         const int g = plan.queue[n - 1 - i];
-        const int L = seg[g + 1] - seg[g];
-        if (L <= kLongSeg) continue;
-        const int nch = (L + kLongSeg - 1) / kLongSeg;
+        const int r0 = seg[g], r1 = seg[g + 1];
+        if (r1 - r0 <= kLongSeg) continue;
+        const int nch = (r1 - r0 + kLongSeg - 1) / kLongSeg;
         const int base = atomicAdd(&plan.counters[0], nch);
         const int li = atomicAdd(&plan.counters[1], 1);
         plan.longs[li] = make_int4(g, base, nch, 0);
-        for (int c = 0; c < nch; ++c) plan.items[base + c] = make_int4(g, c, base + c, 0);
+        for (int c = 0; c < nch; ++c)
+            plan.items[base + c] = make_int4(g, r0 + c * kLongSeg, min(r1, r0 + (c + 1) * kLongSeg), base + c);
     }
 }
 
@@ -595,15 +570,14 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd_chunks(FeatBwdParams p, L
     const int ni = plan.counters[0];
     for (int64_t it = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; it < ni; it += nw) {
         const int4 item = plan.items[it];
-        const int s0 = p.seg[item.x];
-        const int r0 = s0 + item.y * kLongSeg, r1 = min(p.seg[item.x + 1], r0 + kLongSeg);
+        const int r0 = item.y, r1 = item.z;
         for (int base = 0; base < dd; base += 128) {
             float4 acc4[4];
             float acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
             accum_records<VEC>(p, r0, r1, base, lane, acc4, acc1);
-            store_pass<VEC>(plan.partial + static_cast<int64_t>(item.z) * p.d, dd, base, lane, acc4, acc1);
+            store_pass<VEC>(plan.partial + static_cast<int64_t>(item.w) * p.d, dd, base, lane, acc4, acc1);
         }
     }
 }
@@ -616,8 +590,18 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd_combine(FeatBwdParams p, 
     for (int64_t li = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; li < nl; li += nw) {
         const int4 lg = plan.longs[li];
         for (int q = lane; q < p.d; q += 32) {
+            // partial rows added in order; their loads issued 8 ahead of the dependent adds
+            const float* col = plan.partial + static_cast<int64_t>(lg.y) * p.d + q;
             float acc = 0.0f;
-            for (int c = 0; c < lg.z; ++c) acc += plan.partial[static_cast<int64_t>(lg.y + c) * p.d + q];
+            int c = 0;
+            for (; c + 8 <= lg.z; c += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = col[static_cast<int64_t>(c + u) * p.d];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc += v[u];
+            }
+            for (; c < lg.z; ++c) acc += col[static_cast<int64_t>(c) * p.d];
             p.out[static_cast<int64_t>(lg.x) * p.d + q] = acc;
         }
     }
@@ -719,28 +703,29 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
     dbg_launch("k_list_gather", st);
 }
 
-void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* cnt_seg, int32_t* cursor, uint32_t* recs,
-                       uint32_t* sorted, int64_t* total, void* scan_scratch, cudaStream_t st) {
-    const unsigned g = static_cast<unsigned>((p.n_slots + 255) / 256);
-    cudaMemsetAsync(cnt_seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
-    cudaMemsetAsync(cursor, 0, (n_gaussians + 1) * sizeof(int32_t), st);
-    if (p.n_slots > 0) k_slot_count<<<g, 256, 0, st>>>(p, cnt_seg);
-    dbg_launch("k_slot_count", st);
-    scan_exclusive(cnt_seg, cnt_seg, n_gaussians + 1, total, scan_scratch, st);
-    if (p.n_slots > 0) k_slot_fill<<<g, 256, 0, st>>>(p, cnt_seg, cursor, recs);
-    dbg_launch("k_slot_fill", st);
+void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg, int32_t* queue, uint32_t* keys,
+                       uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t** sorted_vals,
+                       void* radix_scratch, cudaStream_t st) {
+    int32_t* counts = queue + n_gaussians;  // [0] unused, [1] long segments
+    cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
+    *sorted_vals = vals;
+    if (p.n_slots <= 0) {
+        cudaMemsetAsync(seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
+        return;
+    }
+    k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p, keys, vals);
+    dbg_launch("k_slot_keys", st);
+    int bits = 0;
+    while (bits < 32 && (static_cast<uint64_t>(n_gaussians) >> bits) != 0) ++bits;  // keys in [0, n]
+    bool alt = false;
+    if (p.n_slots > 1 && bits > 0)
+        radix_sort_pairs_u32(keys, vals, keys_alt, vals_alt, p.n_slots, 0, bits, radix_scratch, st, &alt);
+    *sorted_vals = alt ? vals_alt : vals;
+    segment_offsets_u32(alt ? keys_alt : keys, p.n_slots, seg, n_gaussians, st);
     if (n_gaussians > 0) {
-        // the queues of medium / long segments reuse the cursor array (its counts are no longer
-        // needed); cursor holds n_gaussians + 2 entries, the last two are the queue counters
-        int32_t* counts = cursor + n_gaussians;
-        cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
         const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((n_gaussians + 255) / 256, 148 * 16));
-        k_seg_sort_small<<<g1, 256, 0, st>>>(cnt_seg, n_gaussians, recs, sorted, cursor, counts);
-        dbg_launch("k_seg_sort_small", st);
-        k_seg_sort_warp<<<148 * 4, kThreads, 0, st>>>(cnt_seg, cursor, counts, recs, sorted);
-        dbg_launch("k_seg_sort_warp", st);
-        k_seg_sort_block<<<148, kSortThreads, 0, st>>>(cnt_seg, n_gaussians, cursor, counts, recs, sorted);
-        dbg_launch("k_seg_sort_block", st);
+        k_long_queue<<<g1, 256, 0, st>>>(seg, n_gaussians, queue, counts);
+        dbg_launch("k_long_queue", st);
     }
 }
 
@@ -751,12 +736,46 @@ void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaS
     dbg_launch("k_long_plan", st);
 }
 
+template <int NV4>
+bool launch_feat_bwd_tma(const FeatBwdParams& p, cudaStream_t st) {
+    static FuncAttrCache attr;
+    static const int ctas = [] {
+        const char* e = std::getenv("TK_FBWD_CTAS");  // resident CTAs per SM (default 2)
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    const size_t smem = static_cast<size_t>(kFbWarps) * kFbRing * p.d * 4 + kFbWarps * kFbRing * 8;
+    if (smem > 200 * 1024) return false;
+    set_func_attr(attr, reinterpret_cast<const void*>(k_feat_bwd_tma<NV4>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem), true);
+    k_feat_bwd_tma<NV4><<<148 * ctas, kFbWarps * 32, smem, st>>>(p);
+    return true;
+}
+
+bool feat_bwd_tma_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TK_FBWD_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st) {
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0;
-    if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
-    else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
-    dbg_launch("k_feat_bwd", st);
+    const int nv4 = (p.d / 4 + 31) / 32;
+    bool done = false;
+    if (vec && feat_bwd_tma_enabled() && (reinterpret_cast<uintptr_t>(p.grad) % 16) == 0) {
+        if (nv4 <= 4) done = launch_feat_bwd_tma<4>(p, st);
+        else if (nv4 <= 6) done = launch_feat_bwd_tma<6>(p, st);
+        else if (nv4 <= 8) done = launch_feat_bwd_tma<8>(p, st);
+    }
+    if (done) {
+        dbg_launch("k_feat_bwd_tma", st);
+    } else {
+        if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
+        else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
+        dbg_launch("k_feat_bwd", st);
+    }
     if (vec) k_feat_bwd_chunks<true><<<148 * 8, kThreads, 0, st>>>(p, plan);
     else k_feat_bwd_chunks<false><<<148 * 8, kThreads, 0, st>>>(p, plan);
     dbg_launch("k_feat_bwd_chunks", st);

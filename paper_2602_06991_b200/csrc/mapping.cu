@@ -968,13 +968,13 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams
     const int ni = plan.counters[0];
     for (int64_t it = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; it < ni; it += nw) {
         const int4 item = plan.items[it];
-        const int r0 = p.seg[item.x] + item.y * kLongSeg, r1 = min(p.seg[item.x + 1], r0 + kLongSeg);
+        const int r0 = item.y, r1 = item.z;
         for (int base = 0; base < d4; base += 128) {
             float4 acc[4];
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
             accum_signs(p, r0, r1, base, lane, scale, acc);
-            float4* dst = reinterpret_cast<float4*>(plan.partial + static_cast<int64_t>(item.z) * D);
+            float4* dst = reinterpret_cast<float4*>(plan.partial + static_cast<int64_t>(item.w) * D);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int q = base + m * 32 + lane;

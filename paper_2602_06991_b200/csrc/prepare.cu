@@ -155,11 +155,31 @@ __global__ void k_sorted_ntiles(const uint32_t* __restrict__ order, int64_t nv, 
 }
 
 // One thread per sorted entry: emit (tile, depth rank) pairs in rank order (render.cpp:146-153).
+// An entry spanning more than kEmitThread tiles (a near-camera Gaussian can cover the whole
+// image) is queued for k_emit_big, which writes its rectangle with a whole warp; the pair
+// positions depend only on pair_off and the tile's place in the rectangle, not on who writes.
+constexpr int kEmitThread = 64;
+
+__device__ __forceinline__ void emit_pair(const int4& r, int32_t o0, int local, uint32_t s, int tiles_x,
+                                          uint32_t* tkeys, uint32_t* tvals) {
+    const int w = r.y - r.x + 1;
+    const int ty = r.z + local / w, tx = r.x + local % w;
+    tkeys[o0 + local] = static_cast<uint32_t>(ty * tiles_x + tx);
+    tvals[o0 + local] = s;
+}
+
 __global__ void k_emit_pairs(const uint32_t* __restrict__ order, int64_t nv, const int4* __restrict__ rect,
                              const int32_t* __restrict__ ntiles_sorted, const int32_t* __restrict__ pair_off,
-                             int tiles_x, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals) {
+                             int tiles_x, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                             int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (s >= nv || ntiles_sorted[s] == 0) return;
+    if (s >= nv) return;
+    const int nt = ntiles_sorted[s];
+    if (nt == 0) return;
+    if (nt > kEmitThread) {
+        big[atomicAdd(nbig, 1)] = static_cast<int32_t>(s);
+        return;
+    }
     const int4 r = rect[order[s]];
     int32_t o = pair_off[s];
     for (int ty = r.z; ty <= r.w; ++ty)
@@ -168,6 +188,22 @@ __global__ void k_emit_pairs(const uint32_t* __restrict__ order, int64_t nv, con
             tvals[o] = static_cast<uint32_t>(s);
             ++o;
         }
+}
+
+__global__ void __launch_bounds__(256) k_emit_big(const uint32_t* __restrict__ order, const int4* __restrict__ rect,
+                                                  const int32_t* __restrict__ ntiles_sorted,
+                                                  const int32_t* __restrict__ pair_off, int tiles_x,
+                                                  uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                                                  const int32_t* __restrict__ big, const int32_t* __restrict__ nbig) {
+    const int lane = threadIdx.x & 31;
+    const int nb = *nbig;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nb; w += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t s = static_cast<uint32_t>(big[w]);
+        const int4 r = rect[order[s]];
+        const int nt = ntiles_sorted[s];
+        const int32_t o0 = pair_off[s];
+        for (int local = lane; local < nt; local += 32) emit_pair(r, o0, local, s, tiles_x, tkeys, tvals);
+    }
 }
 
 __global__ void k_padded_counts(const int32_t* __restrict__ tile_offsets, int n_tiles, int32_t* __restrict__ padded) {
@@ -254,11 +290,15 @@ void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntil
 }
 
 void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, const int32_t* ntiles_sorted,
-                       const int32_t* pair_off, int tiles_x, uint32_t* tkeys, uint32_t* tvals, cudaStream_t st) {
+                       const int32_t* pair_off, int tiles_x, uint32_t* tkeys, uint32_t* tvals, int32_t* big,
+                       int32_t* nbig, cudaStream_t st) {
     if (nv > 0) {
+        cudaMemsetAsync(nbig, 0, sizeof(int32_t), st);
         k_emit_pairs<<<blocks_for(nv, 128), 128, 0, st>>>(order, nv, rect, ntiles_sorted, pair_off, tiles_x, tkeys,
-                                                          tvals);
+                                                          tvals, big, nbig);
         dbg_launch("k_emit_pairs", st);
+        k_emit_big<<<148 * 2, 256, 0, st>>>(order, rect, ntiles_sorted, pair_off, tiles_x, tkeys, tvals, big, nbig);
+        dbg_launch("k_emit_big", st);
     }
 }
 

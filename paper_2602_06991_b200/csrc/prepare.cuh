@@ -44,8 +44,10 @@ void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, i
                     uint64_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntiles, int32_t* ntiles_sorted,
                           cudaStream_t st);
+// big: nv int32 scratch, nbig: one device int32 (ranks spanning many tiles, emitted by warps)
 void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, const int32_t* ntiles_sorted,
-                       const int32_t* pair_off, int tiles_x, uint32_t* tkeys, uint32_t* tvals, cudaStream_t st);
+                       const int32_t* pair_off, int tiles_x, uint32_t* tkeys, uint32_t* tvals, int32_t* big,
+                       int32_t* nbig, cudaStream_t st);
 void launch_padded_counts(const int32_t* tile_offsets, int n_tiles, int32_t* padded, cudaStream_t st);
 void launch_materialize(const MaterializeParams& p, cudaStream_t st);
 void launch_export_entries(const uint32_t* order, int64_t nv, const double* mx, const double* my, const double* ixx,

@@ -256,7 +256,9 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     uint32_t* tvals = ensure<uint32_t>(c->tvals, n_pairs);
     uint32_t* tkeys_alt = ensure<uint32_t>(c->tkeys_alt, n_pairs);
     uint32_t* tvals_alt = ensure<uint32_t>(c->tvals_alt, n_pairs);
-    tk::launch_emit_pairs(c->order, n_vis, pp.rect, nts, poff, f.tiles_x, tkeys, tvals, st);
+    tk::launch_emit_pairs(c->order, n_vis, pp.rect, nts, poff, f.tiles_x, tkeys, tvals,
+                          ensure<int32_t>(c->emit_big, std::max<int64_t>(n_vis, 1)),
+                          reinterpret_cast<int32_t*>(dscal + 14), st);  // emit queue count
     ensure_scratch(c, std::max<int64_t>(n_pairs, n_tiles + 1));
     bool talt = false;
     const int tbits = bits_for(static_cast<uint64_t>(n_tiles - 1));
@@ -413,26 +415,28 @@ Records resolve_records(tk_ctx* c, const tk_topk_view* v, const char* fn) {
 SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     const int64_t slots = static_cast<int64_t>(r.w) * r.h * r.k;
     const int64_t n = c->n;
-    uint32_t* recs = ensure<uint32_t>(c->s_keys, slots);
-    uint32_t* svals = ensure<uint32_t>(c->s_vals, slots);
-    int32_t* cursor = ensure<int32_t>(c->s_keys_alt, n + 2);
+    uint32_t* keys = ensure<uint32_t>(c->s_keys, slots);
+    uint32_t* vals = ensure<uint32_t>(c->s_vals, slots);
+    uint32_t* keys_alt = ensure<uint32_t>(c->s_keys_alt, slots);
+    uint32_t* vals_alt = ensure<uint32_t>(c->s_vals_alt, slots);
+    int32_t* queue = ensure<int32_t>(c->s_queue, n + 2);
     float* wn = ensure<float>(c->s_wnorm, slots);
     int32_t* seg = ensure<int32_t>(c->s_seg, n + 1);
     ensure_scratch(c, std::max<int64_t>(slots, n + 1), true);
     PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
     tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
-    int64_t* dscal = ensure<int64_t>(c->dscal, 16);
-    tk::launch_slot_index(sk, n, seg, cursor, recs, svals, dscal + 8, c->scratch_feat.p, c->cur);
+    const uint32_t* sorted = nullptr;
+    tk::launch_slot_index(sk, n, seg, queue, keys, vals, keys_alt, vals_alt, &sorted, c->scratch_feat.p, c->cur);
     tk::LongPlan plan{};
     plan.cap_items = tk::long_plan_capacity(slots, n);
     plan.items = ensure<int4>(c->lp_items, plan.cap_items);
     plan.longs = ensure<int4>(c->lp_longs, plan.cap_items);
     plan.counters = ensure<int32_t>(c->lp_counters, 2);
     plan.partial = ensure<float>(c->lp_partial, plan.cap_items * std::max(c->d, 1));
-    plan.queue = cursor;
-    plan.qcount = cursor + n + 1;
+    plan.queue = queue;
+    plan.qcount = queue + n + 1;
     tk::launch_long_plan(seg, n, plan, c->cur);
-    return SlotIndex{seg, svals, wn, plan};
+    return SlotIndex{seg, sorted, wn, plan};
 }
 
 // The backward sweep of backward_geometric (backward.cpp:106-188) into the per-Gaussian

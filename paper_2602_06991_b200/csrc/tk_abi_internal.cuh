@@ -255,6 +255,7 @@ struct tk_ctx {
     DevBuf te;  // chunk-major tile entries (tk::EntryChunk)
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
     DevBuf pair_pos;      // pair emission index -> padded tile-entry position (fixed-order merge)
+    DevBuf emit_big;      // depth ranks whose tile rectangles are emitted by whole warps
     int64_t padded_cap = 0;
     DevBuf scratch, scratch_feat, dscal;
     int64_t* hscal = nullptr;      // host-mapped mirror of dscal (written by k_copy_words)
@@ -278,7 +279,7 @@ struct tk_ctx {
     // external records staging
     DevBuf x_index, x_weight, x_count;
     // feature
-    DevBuf f_out, f_grad_in, f_grad_out, s_keys, s_vals, s_keys_alt, s_vals_alt, s_wnorm, s_seg;
+    DevBuf f_out, f_grad_in, f_grad_out, s_keys, s_vals, s_keys_alt, s_vals_alt, s_queue, s_wnorm, s_seg;
     int64_t fout_pixels = 0;
     // geometric backward
     bool geom_atomic = false;  // TK_GEOM_BWD_ATOMIC=1: fp64 atomicAdd flush (non-deterministic)
