@@ -438,113 +438,6 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     }
 }
 
-// backward_feature with the dF rows streamed through shared memory by the TMA unit: a persistent
-// grid of kFbWarps-warp CTAs, one warp per Gaussian (grid-stride in Gaussian order, so the warps
-// in flight cover one window of Gaussians, as in k_feat_bwd).  Lane 0 keeps kFbRing records' dF
-// rows in flight (one cp.async.bulk of D*4 bytes each, completion on a per-slot mbarrier); every
-// lane adds w * row for its NV4 float4 channel groups in record (slot) order -- the same
-// arithmetic and order as k_feat_bwd, so the result is bit-identical -- and writes the dense row
-// with streaming stores.  Rows without records are written as zeros.  Bytes in flight come from
-// the bulk copies, not from warps: a few warps per SM saturate HBM, which leaves registers and
-// issue slots for the fp64 geometry backward running beside it on another stream.
-constexpr int kFbWarps = 4;
-constexpr int kFbRing = 8;
-
-template <int NV4>
-__global__ void __launch_bounds__(kFbWarps * 32) k_feat_bwd_tma(FeatBwdParams p) {
-    extern __shared__ __align__(128) unsigned char fb_smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int D = p.d, d4 = D >> 2;
-    const unsigned row_bytes = static_cast<unsigned>(D) * 4u;
-    float4* ring = reinterpret_cast<float4*>(fb_smem) + static_cast<size_t>(warp) * kFbRing * d4;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(fb_smem + static_cast<size_t>(kFbWarps) * kFbRing * row_bytes) +
-                    warp * kFbRing;
-    if (lane == 0) {
-        for (int r = 0; r < kFbRing; ++r) mbar_init(&bar[r], 1);
-        fence_mbar_init();
-    }
-    __syncwarp();
-    unsigned phase_bits = 0;  // parity of each ring slot's next completion
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * kFbWarps;
-    for (int64_t g = static_cast<int64_t>(blockIdx.x) * kFbWarps + warp; g < p.n_gaussians; g += nw) {
-        const int r0 = p.seg[g], r1 = p.seg[g + 1];
-        const int L = r1 - r0;
-        if (L > kLongSeg) continue;  // chunked path
-        float4 acc[NV4];
-#pragma unroll
-        for (int m = 0; m < NV4; ++m) acc[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (L > 0) {
-            // record i's pixel and weight live in lane (i % 32) of the current 32-record batch
-            auto rec = [&](int i, int64_t& px, float& w) {
-                const uint32_t sl = p.slots[r0 + i];
-                px = static_cast<int64_t>(sl / static_cast<uint32_t>(p.k));
-                w = p.wnorm[sl];
-            };
-            int64_t bpx = 0;
-            float bw = 0.f;
-            if (lane < L) rec(lane, bpx, bw);
-            // prologue: the first min(L, kFbRing) rows
-            for (int i = 0; i < L && i < kFbRing; ++i) {
-                const int64_t px = __shfl_sync(0xffffffffu, bpx, i);
-                if (lane == 0) {
-                    mbar_arrive_expect_tx(&bar[i], row_bytes);
-                    bulk_g2s(ring + static_cast<size_t>(i) * d4, p.grad + px * D, row_bytes, &bar[i]);
-                }
-            }
-            int64_t npx = 0;  // the next batch's records (for issuing loads past the batch end)
-            float nwt = 0.f;
-            if (lane < L - 32) rec(32 + lane, npx, nwt);
-            for (int i = 0; i < L; ++i) {
-                if (i > 0 && (i & 31) == 0) {  // next batch
-                    bpx = npx;
-                    bw = nwt;
-                    if (lane + i + 32 < L) rec(i + 32 + lane, npx, nwt);
-                }
-                const int slot = i % kFbRing;
-                const float wj = __shfl_sync(0xffffffffu, bw, i & 31);
-                mbar_wait(&bar[slot], (phase_bits >> slot) & 1u);
-                phase_bits ^= 1u << slot;
-                const float4* row = ring + static_cast<size_t>(slot) * d4;
-                bool live = true;
-                if (!isfinite(wj)) {  // backward.cpp:296-302: a zero dF row is skipped
-                    bool any = false;
-                    for (int q = lane; q < d4; q += 32) {
-                        const float4 v = row[q];
-                        any |= v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
-                    }
-                    live = __any_sync(0xffffffffu, any);
-                }
-                if (live) {
-#pragma unroll
-                    for (int m = 0; m < NV4; ++m) {
-                        const int q = m * 32 + lane;
-                        if (q < d4) acc[m] = fma4(wj, row[q], acc[m]);
-                    }
-                }
-                __syncwarp();  // every lane is done with this slot
-                const int nxt = i + kFbRing;
-                if (nxt < L) {
-                    // pixel of record nxt: batch (nxt >> 5) is the current or the next one
-                    const bool cur_batch = (nxt >> 5) == (i >> 5);
-                    const int64_t pc = __shfl_sync(0xffffffffu, bpx, nxt & 31);
-                    const int64_t pn = __shfl_sync(0xffffffffu, npx, nxt & 31);
-                    if (lane == 0) {
-                        const int64_t px = cur_batch ? pc : pn;
-                        mbar_arrive_expect_tx(&bar[slot], row_bytes);
-                        bulk_g2s(ring + static_cast<size_t>(slot) * d4, p.grad + px * D, row_bytes, &bar[slot]);
-                    }
-                }
-            }
-        }
-        float4* dst = reinterpret_cast<float4*>(p.out + g * D);
-#pragma unroll
-        for (int m = 0; m < NV4; ++m) {
-            const int q = m * 32 + lane;
-            if (q < d4) __stcs(dst + q, acc[m]);
-        }
-    }
-}
-
 // One thread per queued long segment: reserve its partial rows and list its items.
 __global__ void k_long_plan(const int32_t* __restrict__ seg, int64_t n, LongPlan plan) {
     const int nq = *plan.qcount;
@@ -736,46 +629,12 @@ void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaS
     dbg_launch("k_long_plan", st);
 }
 
-template <int NV4>
-bool launch_feat_bwd_tma(const FeatBwdParams& p, cudaStream_t st) {
-    static FuncAttrCache attr;
-    static const int ctas = [] {
-        const char* e = std::getenv("TK_FBWD_CTAS");  // resident CTAs per SM (default 2)
-        return e ? std::max(1, std::atoi(e)) : 2;
-    }();
-    const size_t smem = static_cast<size_t>(kFbWarps) * kFbRing * p.d * 4 + kFbWarps * kFbRing * 8;
-    if (smem > 200 * 1024) return false;
-    set_func_attr(attr, reinterpret_cast<const void*>(k_feat_bwd_tma<NV4>),
-                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem), true);
-    k_feat_bwd_tma<NV4><<<148 * ctas, kFbWarps * 32, smem, st>>>(p);
-    return true;
-}
-
-bool feat_bwd_tma_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("TK_FBWD_TMA");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st) {
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0;
-    const int nv4 = (p.d / 4 + 31) / 32;
-    bool done = false;
-    if (vec && feat_bwd_tma_enabled() && (reinterpret_cast<uintptr_t>(p.grad) % 16) == 0) {
-        if (nv4 <= 4) done = launch_feat_bwd_tma<4>(p, st);
-        else if (nv4 <= 6) done = launch_feat_bwd_tma<6>(p, st);
-        else if (nv4 <= 8) done = launch_feat_bwd_tma<8>(p, st);
-    }
-    if (done) {
-        dbg_launch("k_feat_bwd_tma", st);
-    } else {
-        if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
-        else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
-        dbg_launch("k_feat_bwd", st);
-    }
+    if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
+    else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
+    dbg_launch("k_feat_bwd", st);
     if (vec) k_feat_bwd_chunks<true><<<148 * 8, kThreads, 0, st>>>(p, plan);
     else k_feat_bwd_chunks<false><<<148 * 8, kThreads, 0, st>>>(p, plan);
     dbg_launch("k_feat_bwd_chunks", st);
