@@ -59,7 +59,22 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def build(force: bool = False, verbose: bool = False) -> dict[str, str]:
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: list[str] | None = None) -> dict[str, str]:
+    """Compile libtkrender.so.  variant/defines: an A/B build with extra -D flags into
+    lib/<variant>/libtkrender.so (loaded through TK_RENDER_LIB; scripts/ab_libs.sh)."""
+    global LIB, BUILD
+    if variant:
+        lib0, build0 = LIB, BUILD
+        LIB, BUILD = os.path.join(lib0, variant), os.path.join(build0 + "_" + variant)
+        try:
+            return _build(force, verbose, ["-D" + d for d in (defines or [])])
+        finally:
+            LIB, BUILD = lib0, build0
+    return _build(force, verbose, [])
+
+
+def _build(force: bool, verbose: bool, extra_flags: list[str]) -> dict[str, str]:
     os.makedirs(LIB, exist_ok=True)
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
@@ -72,7 +87,7 @@ def build(force: bool = False, verbose: bool = False) -> dict[str, str]:
             s = os.path.join(CSRC, src)
             o = os.path.join(BUILD, src.replace(".cu", ".o"))
             if force or _stale(o, [s] + headers):
-                _run([nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", s, "-o", o], log)
+                _run([nvcc, *ARCH, *NVCC_FLAGS, *extra, *extra_flags, "-c", s, "-o", o], log)
             objs.append(o)
         so = os.path.join(LIB, "libtkrender.so")
         if force or _stale(so, objs):
@@ -84,4 +99,8 @@ def build(force: bool = False, verbose: bool = False) -> dict[str, str]:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2602_06991_b200.build [--force] [-v] [--variant NAME -DFOO ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else None
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, variant=var, defines=defs))

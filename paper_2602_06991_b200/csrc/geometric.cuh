@@ -37,11 +37,13 @@ struct GeomBwdParams {
     const double* grad_color;  // P x 3
     const double* grad_depth;  // P or null
     // Deterministic flush (default): each warp writes its per-entry MidGrad partial to its own
-    // slot (padded entry position x sub-block) and flags it; k_mid_reduce sums the slots of each
-    // Gaussian in a fixed order.  part == null: fp64 atomicAdd into mid (TK_GEOM_BWD_ATOMIC=1).
+    // slot (tile pair in emission order x warp block, so each Gaussian's slots are contiguous)
+    // and flags it; k_mid_* sum every Gaussian's slots in a fixed order.  part == null: fp64
+    // atomicAdd into mid (TK_GEOM_BWD_ATOMIC=1).
     double* mid;               // n x 10: mx,my,ixx,ixy,iyy,z,opacity,cr,cg,cb (atomic mode)
-    double* part;              // padded entries x nsub x 10 partials, or null
-    uint8_t* part_flag;        // padded entries x nsub: 1 = partial written this sweep (zeroed first)
+    double* part;              // pairs x nsub x 10 partials, or null
+    uint8_t* part_flag;        // pairs x nsub: 1 = partial written this sweep (zeroed first)
+    const int32_t* entry_pair; // padded entry position -> pair emission index (k_materialize)
     int nsub;                  // warp blocks per tile
 };
 
@@ -51,16 +53,13 @@ struct GeomBwdParams {
 // block order).  Bit-deterministic run to run.
 struct MidReduceParams {
     int64_t nv;                   // depth-sorted visible Gaussians
-    int64_t n_pairs;              // tile pairs (emission order)
-    double* pair_sum;             // n_pairs x 10 scratch (level 1)
     const uint32_t* order;        // depth rank -> Gaussian id
     const int32_t* ntiles_sorted; // tile pairs per depth rank
     const int32_t* pair_off;      // first pair (emission index) per depth rank
-    const int32_t* pair_pos;      // emission index -> padded tile-entry position (k_materialize)
-    const double* part;
-    const uint8_t* part_flag;
+    const double* part;           // pairs x nsub x 10
+    const uint8_t* part_flag;     // pairs x nsub
     int nsub;
-    double* mid;                  // n x 10 (zeroed beforehand; written for binned ranks)
+    double* mid;                  // n x 10 (zeroed beforehand; written for touched ranks)
     int32_t* big_list;            // nv: medium ranks from the front, huge ranks from the back
     int32_t* big_count;           // [medium, huge], zeroed beforehand
 };

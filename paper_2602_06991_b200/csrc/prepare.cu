@@ -233,10 +233,10 @@ __global__ void k_materialize(MaterializeParams p) {
     ch.f[8][l] = p.color[i * 3 + 1];
     ch.f[9][l] = p.color[i * 3 + 2];
     ch.src[l] = static_cast<int32_t>(i);
-    if (p.pair_pos) {
+    if (p.entry_pair) {
         const int4 r = p.rect[i];
         const int tx = static_cast<int>(t % static_cast<uint32_t>(p.tiles_x)), ty = static_cast<int>(t / static_cast<uint32_t>(p.tiles_x));
-        p.pair_pos[p.pair_off[s] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x)] = static_cast<int32_t>(dst);
+        p.entry_pair[dst] = p.pair_off[s] + (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
     }
     // Bounding box of {d : -0.5 d^T A d >= cutoff}, A = (ixx, ixy; ixy, iyy): |d_x| <= sqrt(R Sxx)
     // with R = -2 cutoff and S = A^-1.  Inflated (1e-6 relative + 1e-3 px) so that rounding can

@@ -31,12 +31,12 @@ struct MaterializeParams {
     const uint32_t* order;       // depth rank -> Gaussian id
     const double *mx, *my, *ixx, *ixy, *iyy, *z, *opacity, *color;
     TileEntries out;
-    // inverse of the pair emission (k_emit_pairs): pair_pos[pair_off[s] + local] = padded position
-    // of depth rank s's local-th tile (row-major in its rectangle); null = not needed
+    // emission index of every materialised entry (k_emit_pairs order: depth rank s's tiles at
+    // pair_off[s] + local, row-major in its rectangle): entry_pair[padded position]; null = not needed
     const int4* rect;
     const int32_t* pair_off;
     int tiles_x;
-    int32_t* pair_pos;
+    int32_t* entry_pair;
 };
 
 void launch_project(const ProjectParams& p, cudaStream_t st);

@@ -296,7 +296,7 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
     mp.rect = pp.rect;
     mp.pair_off = poff;
     mp.tiles_x = f.tiles_x;
-    mp.pair_pos = ensure<int32_t>(c->pair_pos, n_pairs);
+    mp.entry_pair = ensure<int32_t>(c->entry_pair, padded_cap);
     tk::launch_materialize(mp, st);
     CK_LAUNCH(c);
     c->prepared = true;
@@ -459,11 +459,12 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
     bp.mid = mid;
     bp.nsub = tk::geom_blocks_per_tile(f.tile_size);
     if (!c->geom_atomic) {
-        const int64_t slots = c->padded_cap * bp.nsub;
+        const int64_t slots = std::max<int64_t>(c->n_pairs, 1) * bp.nsub;
         bp.part = ensure<double>(c->g_part, slots * 10);
-        // flags + the big-rank counter behind them, zeroed in one memset
-        const int64_t fbytes = tk::align_up(std::max<int64_t>(slots, 1), 16);
+        // flags + the queue counters behind them, zeroed in one memset
+        const int64_t fbytes = tk::align_up(slots, 16);
         bp.part_flag = ensure<uint8_t>(c->g_flag, fbytes + 16);
+        bp.entry_pair = ptr<int32_t>(c->entry_pair);
         CK(cudaMemsetAsync(bp.part_flag, 0, fbytes + 16, c->cur));
     }
     {
@@ -472,18 +473,16 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
         if (!c->geom_atomic) {
             tk::MidReduceParams mr{};
             mr.nv = c->n_vis;
-            mr.n_pairs = c->n_pairs;
-            mr.pair_sum = ensure<double>(c->g_pairsum, std::max<int64_t>(c->n_pairs, 1) * 10);
             mr.order = c->order;
             mr.ntiles_sorted = ptr<int32_t>(c->ntiles_sorted);
             mr.pair_off = ptr<int32_t>(c->pair_off);
-            mr.pair_pos = ptr<int32_t>(c->pair_pos);
             mr.part = bp.part;
             mr.part_flag = bp.part_flag;
             mr.nsub = bp.nsub;
             mr.mid = mid;
             mr.big_list = ensure<int32_t>(c->g_big, std::max<int64_t>(c->n_vis, 1));
-            mr.big_count = reinterpret_cast<int32_t*>(bp.part_flag + tk::align_up(std::max<int64_t>(c->padded_cap * bp.nsub, 1), 16));
+            mr.big_count = reinterpret_cast<int32_t*>(
+                bp.part_flag + tk::align_up(std::max<int64_t>(c->n_pairs, 1) * bp.nsub, 16));
             tk::launch_mid_reduce(mr, c->cur);
         }
     }

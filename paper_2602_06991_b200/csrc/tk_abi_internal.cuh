@@ -254,7 +254,7 @@ struct tk_ctx {
     DevBuf tkeys, tvals, tkeys_alt, tvals_alt, tile_offsets, padded_cnt, padded_start;
     DevBuf te;  // chunk-major tile entries (tk::EntryChunk)
     DevBuf wl, wl_count;  // per-warp culled entry lists (forward -> backward)
-    DevBuf pair_pos;      // pair emission index -> padded tile-entry position (fixed-order merge)
+    DevBuf entry_pair;    // padded tile-entry position -> pair emission index (fixed-order merge)
     DevBuf emit_big;      // depth ranks whose tile rectangles are emitted by whole warps
     int64_t padded_cap = 0;
     DevBuf scratch, scratch_feat, dscal;
@@ -283,7 +283,7 @@ struct tk_ctx {
     int64_t fout_pixels = 0;
     // geometric backward
     bool geom_atomic = false;  // TK_GEOM_BWD_ATOMIC=1: fp64 atomicAdd flush (non-deterministic)
-    DevBuf g_part, g_flag, g_big, g_pairsum;  // per-(entry, warp block) MidGrad partials, written flags, big ranks
+    DevBuf g_part, g_flag, g_big;  // per-(entry, warp block) MidGrad partials, written flags, big ranks
     DevBuf g_color_in, g_depth_in, mid, twist, twist_part, twist_out, gg_mean, gg_ls, gg_rot, gg_op, gg_col;
     // full blend
     DevBuf l_count, l_off, l_src, l_w;
