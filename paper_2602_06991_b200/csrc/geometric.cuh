@@ -59,7 +59,7 @@ struct MidReduceParams {
     const double* part;           // pairs x nsub x 10
     const uint8_t* part_flag;     // pairs x nsub
     int nsub;
-    double* mid;                  // n x 10 (zeroed beforehand; written for touched ranks)
+    double* mid;                  // nv x 10 by depth rank, written for every rank with tile pairs
     int32_t* big_list;            // nv: medium ranks from the front, huge ranks from the back
     int32_t* big_count;           // [medium, huge], zeroed beforehand
 };
@@ -78,9 +78,16 @@ struct ChainParams {
     double* g_rotation;
     double* g_opacity_logit;
     double* g_color;
-    double* twist;  // ceil(n / 128) x 6 block partials, or null (mapping: no pose gradient)
+    double* twist;  // ceil(items / 128) x 6 block partials, or null (mapping: no pose gradient)
     double mid_scale = 1.0;  // applied to mid (1 / ranks after a D-sharded all-reduce)
+    // Rank mode (the deterministic merge): mid is indexed by depth rank, written for every rank
+    // with tile pairs; the chain runs over those ranks only and the outputs are zero-filled first.
+    const uint32_t* order = nullptr;       // depth rank -> Gaussian id (null: mid by Gaussian id)
+    const int32_t* ntiles_sorted = nullptr;
+    int64_t nv = 0;
 };
+// number of per-block twist partials the chain writes (k_twist_final's input)
+__host__ __device__ inline int64_t chain_items(const ChainParams& p) { return p.order ? p.nv : p.n; }
 
 // In-place Adam over the five geometry groups (optimizer.hpp:25-53 layout: one m / v array per
 // group, strided like the parameters).  Group order: mean, log_scale, rotation, opacity, color.
@@ -109,7 +116,7 @@ void launch_mid_reduce(const MidReduceParams& p, cudaStream_t st);
 void launch_chain(const ChainParams& p, cudaStream_t st);
 // Adam + clamps + renormalisation + peak statistic over every Gaussian (thread per Gaussian)
 void launch_geo_adam(const GeoAdamParams& a, int64_t n, cudaStream_t st);
-// deterministic sum of k_chain's per-block twist partials -> out[6] (device)
-void launch_twist_reduce(const double* twist, int64_t n, double* partial, double* out, cudaStream_t st);
+// deterministic sum of k_chain's per-block twist partials -> out[6] (device); items = chain_items()
+void launch_twist_reduce(const double* twist, int64_t items, double* partial, double* out, cudaStream_t st);
 
 }  // namespace tk

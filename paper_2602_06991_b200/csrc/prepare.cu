@@ -29,7 +29,7 @@ __device__ __forceinline__ void quat_to_matrix(double w, double x, double y, dou
 
 // Projection of Gaussian i; writes the ProjEntry fields, radius and tile rectangle.
 #ifndef TK_PROJECT_MINB
-#define TK_PROJECT_MINB 4  // 64 registers, 8 resident blocks: 70 -> 49 us (3: 54 us)
+#define TK_PROJECT_MINB 4  // 64 registers, 4 resident blocks: 70 -> 49 us (3 blocks: 54 us)
 #endif
 __global__ void __launch_bounds__(256, TK_PROJECT_MINB) k_project(ProjectParams p) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;

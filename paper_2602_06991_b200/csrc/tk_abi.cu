@@ -444,7 +444,7 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
 double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double* gd) {
     const int64_t n = c->n;
     double* mid = ensure<double>(c->mid, n * 10);
-    CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), c->cur));
+    if (c->geom_atomic) CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), c->cur));
     tk::GeomBwdParams bp{};
     bp.f = f;
     bp.te = tile_entries(c);
@@ -504,6 +504,11 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     cp.fx = cam->fx;
     cp.fy = cam->fy;
     cp.dilation = s->cov2d_dilation;
+    if (!c->geom_atomic) {  // geom_sweep's fixed-order merge leaves mid by depth rank
+        cp.order = c->order;
+        cp.ntiles_sorted = ptr<int32_t>(c->ntiles_sorted);
+        cp.nv = c->n_vis;
+    }
     return cp;
 }
 void flush_features(tk_ctx* c) {
@@ -1042,7 +1047,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
         {
             PhaseScope phase(c, TK_PHASE_CHAIN);
             tk::launch_chain(cp, st);
-            tk::launch_twist_reduce(cp.twist, n, tpart, tout, st);
+            tk::launch_twist_reduce(cp.twist, tk::chain_items(cp), tpart, tout, st);
         }
         CK_LAUNCH(c);
         if (out) {
