@@ -486,6 +486,8 @@ def main_gpu(args, cfg):
         mapping = run_mapping(lib, slib, N, torch, ctx, W, H, Ds, n, cpose, ccam, cset, args.steps, args.warmup,
                               0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard, scene=scene,
                               cam=cam, gt_pose=pose, d_total=D, c0=c0)
+        if not dshard and not args.no_extras and extras is not None:
+            extras["mapedit"] = run_mapedit(lib, N, ctx, Ds, cpose)
 
     k_sweep = ref_grid = dropin = None
     if world == 1 and not args.no_extras:
@@ -918,6 +920,47 @@ def run_k_sweep(lib, N, torch, dev, steps, peak):
         lib.tk_destroy(ctx)
         del keep
     return out
+
+
+def run_mapedit(lib, N, ctx, D, kpose, n_insert=100_000):
+    """Structural edits on the config-3 map after the mapping run (its selection statistics):
+    insert_gaussians with n_insert source points (mapper.cpp:19-60; all farther than tau, so all
+    inserted) and prune_map with the reference defaults keep_ratio 0.5, threshold 0
+    (mapper.hpp:17-19; mapper.cpp:80-160: the exact candidate draw on the host, the compaction of
+    the map, features and every optimiser group on the device).  Host wall time, synchronised."""
+    rng = np.random.default_rng(3)
+    pos = np.ascontiguousarray(np.stack([rng.uniform(-1, 1, n_insert), rng.uniform(-1, 1, n_insert),
+                                         rng.uniform(1.0, 5.0, n_insert)], 1))
+    col = np.ascontiguousarray(rng.uniform(0, 1, (n_insert, 3)))
+    feat = np.ascontiguousarray(rng.normal(size=(n_insert, D)).astype(np.float32))
+    sp = np.full(n_insert, 0.02)
+    dist = np.full(n_insert, np.inf)
+    view = N.tk_source_view(n_insert, D, pos.ctypes.data, col.ctypes.data, feat.ctypes.data, sp.ctypes.data,
+                            dist.ctypes.data, N.TK_HOST)
+    n0, d0, g0 = C.c_int64(), C.c_int32(), C.c_uint64()
+    N.check(lib.tk_scene_info(ctx, C.byref(n0), C.byref(d0), C.byref(g0)))
+    N.check(lib.tk_synchronize(ctx))
+    inserted = C.c_int32()
+    t0 = time.time()
+    N.check(lib.tk_insert_gaussians(ctx, C.byref(view), 0.01, C.byref(kpose), C.byref(inserted)))
+    N.check(lib.tk_synchronize(ctx))
+    t1 = time.time()
+    n1 = C.c_int64()
+    N.check(lib.tk_scene_info(ctx, C.byref(n1), C.byref(d0), C.byref(g0)))
+    removed = C.c_int64()
+    t2 = time.time()
+    N.check(lib.tk_prune_map(ctx, 0.5, 42, 0, None, C.byref(removed)))
+    N.check(lib.tk_synchronize(ctx))
+    t3 = time.time()
+    return {"insert": {"source_points": n_insert, "inserted": inserted.value, "map_before": n0.value,
+                       "ms": 1000.0 * (t1 - t0),
+                       "path": "tk_insert_gaussians: host source points -> device flags, scan, one warp per "
+                               "inserted Gaussian; every Adam group and the statistics grow in lockstep"},
+            "prune": {"map_before": n1.value, "removed": removed.value, "keep_ratio": 0.5, "threshold": 0,
+                      "ms": 1000.0 * (t3 - t2),
+                      "path": "tk_prune_map: statistics to the host, the reference's exact weighted draw "
+                              "without replacement in O(C log C) (Fenwick pool, rounding-bounded fallback to "
+                              "the sequential scan), device compaction of the map, features and optimiser state"}}
 
 
 def run_dropin(cfg, iters):

@@ -92,18 +92,26 @@ int main(int argc, char** argv) {
     for (int pol = 0; pol < 2; ++pol) {
         const UploadPolicy policy = pol == 0 ? UploadPolicy::kAlways : UploadPolicy::kVersioned;
         Renderer r(0, policy);
+        double call_s[4] = {0, 0, 0, 0};  // render_geometric, render_feature, backward_geometric, backward_feature
+        auto timed = [&](int k, auto&& fn) {
+            const auto a = std::chrono::steady_clock::now();
+            fn();
+            call_s[k] += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+        };
         auto iteration = [&](int it) {
             const bool feature_step = it % period == 0;
-            RenderOutput render = r.render_geometric(map, pose, cam, s);
-            if (feature_step) render.feature = r.render_feature(map, render.topk);
-            const GeomGrads g = r.backward_geometric(map, pose, cam, s, gc, gd);
+            RenderOutput render;
+            timed(0, [&] { render = r.render_geometric(map, pose, cam, s); });
+            if (feature_step) timed(1, [&] { render.feature = r.render_feature(map, render.topk); });
+            timed(2, [&] { const GeomGrads g = r.backward_geometric(map, pose, cam, s, gc, gd); });
             map.geometry_version += 1;  // Adam on the five geometry groups (mapper.cpp:183-236)
             if (feature_step) {
-                const std::vector<double> fg = r.backward_feature(map, render.topk, gf);
+                timed(3, [&] { const std::vector<double> fg = r.backward_feature(map, render.topk, gf); });
                 map.feature_version += 1;  // feature Adam + renormalise (mapper.cpp:239-252)
             }
         };
         iteration(0);  // warm-up: allocations, first upload of both halves
+        for (double& v : call_s) v = 0.0;
         const uint64_t geo0 = r.geometry_bytes_uploaded(), feat0 = r.feature_bytes_uploaded();
         const auto t0 = std::chrono::steady_clock::now();
         for (int it = 1; it <= iters; ++it) iteration(it);
@@ -119,9 +127,12 @@ int main(int argc, char** argv) {
                           fsteps * (P * D * 4.0 + P * D * 4.0 + n * D * 4.0);
         std::printf("%s{\"policy\": \"%s\", \"iterations_per_s\": %.4f, \"ms_per_iteration\": %.3f, \"iterations\": %d, "
                     "\"feature_update_period\": %d, \"geometry_upload_bytes_per_iteration\": %.0f, "
-                    "\"feature_upload_bytes_per_iteration\": %.0f, \"other_transfer_bytes_per_iteration\": %.0f}",
+                    "\"feature_upload_bytes_per_iteration\": %.0f, \"other_transfer_bytes_per_iteration\": %.0f, "
+                    "\"ms_per_call_type_per_iteration\": {\"render_geometric\": %.2f, \"render_feature\": %.2f, "
+                    "\"backward_geometric\": %.2f, \"backward_feature\": %.2f}}",
                     pol ? ", " : "", pol == 0 ? "always" : "versioned", iters / sec, 1000.0 * sec / iters, iters, period,
-                    geo, fe, io);
+                    geo, fe, io, 1000.0 * call_s[0] / iters, 1000.0 * call_s[1] / iters, 1000.0 * call_s[2] / iters,
+                    1000.0 * call_s[3] / iters);
     }
     std::printf("]\n");
     return 0;
