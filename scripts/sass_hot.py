@@ -12,7 +12,7 @@ def main(rep, regex, minc=0):
                           "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
-    data = rows[2:]
+    data = [r for r in rows[2:] if len(r) == len(h)]  # one kernel's rows (a report may hold several)
     si, ie = h.index("Source"), h.index("Instructions Executed")
     ws = h.index("Warp Stall Sampling (All Samples)")
     vals = [int(r[ie]) if r[ie].isdigit() else 0 for r in data]
