@@ -50,15 +50,18 @@ CONFIGS = {
 }
 
 
-def bench_config(cfg, world, mode, gather):
+def bench_config(cfg, world, mode, gather, geo_split=False):
     """The workload's `config` object, identical for both arms (the reference arm runs the same
     scene, pose, seeds and settings on the host)."""
     D = cfg["d"]
     dshard = world > 1 and mode == "dshard"
     P = cfg["w"] * cfg["h"]
     if dshard:
-        par = (f"feature-dim shard d{world}: D/{world} channels per GPU, Top-K recomputed per GPU, F all-gathered "
-               + ("by render_feature fused with NVLink peer stores" if gather == "p2p" else "with NCCL"))
+        par = (f"feature-dim shard d{world}: D/{world} channels per GPU, "
+               + ("geometric sweeps split by tile-row bands (records all-gathered, gradients sum-reduced)"
+                  if geo_split else "Top-K recomputed per GPU")
+               + ", F all-gathered " + ("by render_feature fused with NVLink peer stores" if gather == "p2p"
+                                         else "with NCCL"))
     elif world > 1:
         par = f"keyframe-parallel x{world}: rank r renders orbit keyframe r, all D"
     else:
@@ -242,7 +245,7 @@ def reference_arm(args, cfg):
     line = {"impl": "reference", "metric": METRIC, "unit": "frames/s", "higher_is_better": True,
             "n_gpus": args.gpus, "steps": 0, "warmup": 0, "steps_requested": args.steps,
             "warmup_requested": args.warmup, "dtype": "f64", "data": "synthetic",
-            "config": bench_config(cfg, world, args.mode, args.gather)}
+            "config": bench_config(cfg, world, args.mode, args.gather, args.geo_split)}
     if r is None:
         line.update({"value": None, "error": err})
     else:
@@ -324,6 +327,8 @@ def main_gpu(args, cfg):
             dist.all_reduce(flag, op=dist.ReduceOp.MIN)
             if int(flag.item()) == 0:
                 gather_mode = "nccl (p2p setup failed on a rank" + (f": {why}" if why else "") + ")"
+        if args.geo_split:
+            N.check(lib.tk_geometry_band(ctx, rank, world))
     else:
         gather_mode = None
 
@@ -482,6 +487,8 @@ def main_gpu(args, cfg):
         extras = run_extras(lib, N, torch, ctx, W, H, D, n, args.steps, stream, dev, cpose, ccam, cset)
 
     mapping = None
+    if args.geo_split and dshard:  # the mapping iteration sweeps the whole image on every rank
+        N.check(lib.tk_geometry_band(ctx, 0, 1))
     if not args.no_mapping:  # dshard: the D-sharded mapping iteration (NCCL all-reduces inside the step)
         mapping = run_mapping(lib, slib, N, torch, ctx, W, H, Ds, n, cpose, ccam, cset, args.steps, args.warmup,
                               0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard, scene=scene,
@@ -516,7 +523,7 @@ def main_gpu(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_step, "step_ms": step_stats, "higher_is_better": True,
             "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
-            "config": bench_config(dict(cfg, n=n, k=K), world, args.mode, args.gather),
+            "config": bench_config(dict(cfg, n=n, k=K), world, args.mode, args.gather, args.geo_split),
             "gather_path": gather_mode, "records": {"distinct_gaussians": U, "valid_slots": M},
             "frame_roofline": frame_roof, "multi_gpu": multi, "keyframe_parallel": kf_block,
             "k_sweep": k_sweep, "fslam_bench_grid": ref_grid, "e2e_dropin": dropin,
@@ -1092,6 +1099,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the K sweep, the fslam bench grid and extras")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="dshard: fused render + all-gather over peer memory, or render + NCCL all-gather")
+    ap.add_argument("--geo-split", action="store_true",
+                    help="dshard: split the geometric sweeps by tile-row bands across the ranks (records "
+                         "all-gathered, geometry gradients sum-reduced: tk_geometry_band)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = dict(CONFIGS[args.config])

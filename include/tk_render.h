@@ -219,6 +219,18 @@ tk_status tk_render_feature_gathered(tk_ctx* ctx, const tk_topk_view* topk, floa
                                      int32_t out_mem);
 tk_status tk_comm_gathered_buffer(tk_ctx* ctx, float** buffer);
 
+/* Geometry split across ranks (the Amdahl term of the D-sharded frame): the geometric forward and
+ * backward sweeps cover only band `band` of `nbands` bands of whole tile rows (rows_b =
+ * ceil(tiles_y / nbands)).  Under tk_comm with nranks == nbands and band == rank, tk_render_geometric
+ * all-gathers the per-pixel records, colour, depth and alpha of every band (NCCL, equal band-sized
+ * chunks) and max-reduces the peak contributions, and tk_backward_geometric sum-reduces the merged
+ * per-Gaussian projected gradients (N_vis x 10 fp64) before the chain rule, so every rank ends with
+ * the whole frame's outputs; the sum over bands is fixed for a fixed nbands (NCCL reduction order),
+ * not bit-identical to the unsplit sweep.  Without tk_comm the context sweeps its band only (band
+ * outputs valid, the rest stale): single-process simulation of the split.  nbands = 1 restores the
+ * whole-image sweeps.  Not supported by tk_optimize_step. */
+tk_status tk_geometry_band(tk_ctx* ctx, int32_t band, int32_t nbands);
+
 /* ---- one mapping iteration on the device (map/mapper.cpp:162-255) ---- */
 typedef struct { /* MapperConfig knobs of one iteration; same layout as the oracle's orc_mapper_config */
     double lambda_geo, lambda_feat, lambda1, lambda2; /* LossWeights, losses.hpp:9-21 */

@@ -133,6 +133,7 @@ RENDER_SYMBOLS = [
     ("tk_comm_set_peers", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64]),
     ("tk_render_feature_gathered", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
     ("tk_comm_gathered_buffer", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("tk_geometry_band", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("tk_allreduce_sum_f64", C.c_int, [C.c_void_p, dbl_p, C.c_int32]),
     ("tk_kernel_launches", C.c_int64, [C.c_void_p]),
     ("tk_invalidate", C.c_int, [C.c_void_p]),

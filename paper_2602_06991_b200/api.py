@@ -94,6 +94,10 @@ class Renderer:
         # it on every call so in-place edits are always seen.
         self.upload(m)
 
+    def geometry_band(self, band: int, nbands: int) -> None:
+        """Sweep only band `band` of `nbands` bands of tile rows (tk_geometry_band)."""
+        N.check(self.lib.tk_geometry_band(self.ctx, band, nbands))
+
     def launches(self) -> int:
         return int(self.lib.tk_kernel_launches(self.ctx))
 

@@ -107,7 +107,7 @@ struct GeoAdamParams {
     double* max_contrib;
 };
 
-// number of one-warp CTAs covering the frame (8x4 pixel blocks per tile)
+// number of one-warp CTAs covering the frame's swept tiles [tile_begin, tile_end)
 int geom_blocks(const Frame& f);
 int geom_blocks_per_tile(int tile_size);
 void launch_geom_fwd(int mode, const GeomFwdParams& p, int n_blocks, cudaStream_t st);

@@ -111,9 +111,28 @@ tk::Frame make_frame(tk_ctx* c, const tk_camera* cam, const tk_settings* s) {
     f.tfloor = s->transmittance_floor;
     f.alpha_clamp = s->alpha_clamp;
     for (int i = 0; i < 3; ++i) f.bg[i] = s->background[i];
+    f.tile_begin = 0;
+    f.tile_end = f.tiles_x * f.tiles_y;
     (void)c;
     return f;
 }
+
+// Geometry split (tk_geometry_band): the sweeps cover tile rows [band * rows_b, (band + 1) * rows_b),
+// rows_b = ceil(tiles_y / bands); the pixels of a band are one contiguous run of `band_pixels`
+// pixels (the last band padded), so the per-pixel records all-gather as equal NCCL chunks.
+int64_t band_pixels(const tk::Frame& f, int bands) {
+    const int rows_b = (f.tiles_y + bands - 1) / bands;
+    return static_cast<int64_t>(rows_b) * f.tile_size * f.width;
+}
+void apply_band(tk_ctx* c, tk::Frame& f) {
+    if (c->band_n <= 1) return;
+    const int rows_b = (f.tiles_y + c->band_n - 1) / c->band_n;
+    const int ty0 = std::min(f.tiles_y, c->band * rows_b), ty1 = std::min(f.tiles_y, ty0 + rows_b);
+    f.tile_begin = ty0 * f.tiles_x;
+    f.tile_end = ty1 * f.tiles_x;
+}
+// all ranks of tk_comm take part: records are all-gathered and MidGrad sum-reduced
+bool band_collective(const tk_ctx* c) { return c->band_n > 1 && c->comm && c->nranks == c->band_n; }
 
 PrepKey make_prep_key(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_settings* s) {
     PrepKey k;
@@ -307,8 +326,11 @@ void prepare(tk_ctx* c, const tk_pose* pose, const tk_camera* cam, const tk_sett
 // geometric_pass (render.cpp:158-240).  Record/colour outputs are optional (null = skip);
 // the per-pixel aux (final T, entries visited) is always written for the backward.
 void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records) {
-    const tk::Frame f = make_frame(c, cam, s);
-    const int64_t P = static_cast<int64_t>(f.width) * f.height;
+    tk::Frame f = make_frame(c, cam, s);
+    apply_band(c, f);
+    const bool gather = band_collective(c) && records;
+    // record buffers hold whole bands when they are all-gathered (the last band padded)
+    const int64_t P = gather ? band_pixels(f, c->band_n) * c->band_n : static_cast<int64_t>(f.width) * f.height;
     const int k = f.k;
     cudaStream_t st = c->cur;
     tk::GeomFwdParams gp{};
@@ -338,6 +360,19 @@ void forward(tk_ctx* c, const tk_camera* cam, const tk_settings* s, bool records
         tk::launch_geom_fwd(tk::kGeomForward, gp, nblk, st);
     }
     CK_LAUNCH(c);
+    if (gather) {  // every rank swept its band: assemble the whole frame's records on every rank
+        const int64_t bp = band_pixels(f, c->band_n);
+        const int64_t off = bp * c->rank;
+        const size_t kk = static_cast<size_t>(std::max(k, 1));
+        NK(g_nccl.AllGather(gp.topk_index + off * kk, gp.topk_index, bp * kk, ncclInt32, c->comm, st));
+        NK(g_nccl.AllGather(gp.topk_weight + off * kk, gp.topk_weight, bp * kk, ncclFloat64, c->comm, st));
+        NK(g_nccl.AllGather(gp.topk_count + off, gp.topk_count, bp, ncclUint8, c->comm, st));
+        NK(g_nccl.AllGather(gp.color + off * 3, gp.color, bp * 3, ncclFloat64, c->comm, st));
+        NK(g_nccl.AllGather(gp.depth + off, gp.depth, bp, ncclFloat64, c->comm, st));
+        NK(g_nccl.AllGather(gp.alpha + off, gp.alpha, bp, ncclFloat64, c->comm, st));
+        // peak weights: positive doubles order like their bit patterns (render.cpp:212's max)
+        NK(g_nccl.AllReduce(gp.contrib, gp.contrib, static_cast<size_t>(c->n), ncclUint64, ncclMax, c->comm, st));
+    }
     if (records) {
         c->has_records = true;
         c->rec_w = f.width;
@@ -441,7 +476,9 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
 
 // The backward sweep of backward_geometric (backward.cpp:106-188) into the per-Gaussian
 // projected-space gradients (n x 10), on the forward state of this context.
-double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double* gd) {
+double* geom_sweep(tk_ctx* c, const tk::Frame& f0, const double* gc, const double* gd) {
+    tk::Frame f = f0;
+    apply_band(c, f);
     const int64_t n = c->n;
     double* mid = ensure<double>(c->mid, n * 10);
     if (c->geom_atomic) CK(cudaMemsetAsync(mid, 0, std::max<int64_t>(n, 1) * 10 * sizeof(double), c->cur));
@@ -487,6 +524,10 @@ double* geom_sweep(tk_ctx* c, const tk::Frame& f, const double* gc, const double
         }
     }
     CK_LAUNCH(c);
+    if (band_collective(c)) {  // each rank merged its band's partials: sum them over the ranks
+        if (c->geom_atomic) fail(TK_ERR_STATE, "the geometry split needs the deterministic merge");
+        NK(g_nccl.AllReduce(mid, mid, static_cast<size_t>(c->n_vis) * 10, ncclFloat64, ncclSum, c->comm, c->cur));
+    }
     return mid;
 }
 
@@ -1298,6 +1339,20 @@ tk_status tk_render_feature_gathered(tk_ctx* c, const tk_topk_view* topk, float*
             if (out_mem == TK_HOST) sync(c);
         }
         side_done(c, true);
+    });
+}
+
+tk_status tk_geometry_band(tk_ctx* c, int32_t band, int32_t nbands) {
+    return guarded([&] {
+        if (!c) fail(TK_ERR_BAD_ARG, "null context");
+        if (nbands < 1 || band < 0 || band >= nbands) fail(TK_ERR_BAD_ARG, "band must be in [0, nbands)");
+        if (c->comm && nbands > 1 && (nbands != c->nranks || band != c->rank))
+            fail(TK_ERR_BAD_ARG, "under tk_comm the geometry split needs nbands == nranks and band == rank");
+        if (nbands > 1 && c->geom_atomic) fail(TK_ERR_STATE, "the geometry split needs the deterministic merge");
+        c->band = band;
+        c->band_n = nbands;
+        c->prepared = false;  // the forward state of another band is no use
+        c->aux_valid = false;
     });
 }
 

@@ -307,6 +307,8 @@ struct tk_ctx {
     std::vector<tk::AdamStepParams> f_tab_host;
     bool feat_stale = false;
     DevBuf row_ss;                                        // D-sharded partial row norms
+    // geometry split: this context sweeps band `band` of `band_n` (tk_geometry_band)
+    int band = 0, band_n = 1;
     // multi-GPU
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0, d_total = 0;

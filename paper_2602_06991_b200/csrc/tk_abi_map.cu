@@ -325,6 +325,7 @@ tk_status tk_optimize_step(tk_ctx* c, const tk_mapper_config* cfg, const tk_came
     return guarded([&] {
         check_frame(cam, s);
         if (!cfg) fail(TK_ERR_BAD_ARG, "null mapper config");
+        if (c->band_n > 1) fail(TK_ERR_STATE, "optimize_step: the geometry split (tk_geometry_band) is frame-API only");
         if (slot < 0 || static_cast<size_t>(slot) >= c->kfs.size() || c->kfs[slot].w == 0)
             fail(TK_ERR_BAD_ARG, "optimize_step: no keyframe in that slot");
         if (cfg->feature_update_period <= 0) fail(TK_ERR_BAD_ARG, "feature_update_period must be positive");

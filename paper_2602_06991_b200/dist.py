@@ -47,3 +47,14 @@ def max_over_ranks(dist, value: float) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def band_rows(height: int, tile_size: int, nbands: int, band: int) -> tuple[int, int]:
+    """Pixel rows [y0, y1) swept by `band` under the geometry split (tk_geometry_band): whole tile
+    rows, rows_b = ceil(tiles_y / nbands) per band, the last band possibly shorter or empty."""
+    tiles_y = (height + tile_size - 1) // tile_size
+    rows_b = (tiles_y + nbands - 1) // nbands
+    ty0 = min(tiles_y, band * rows_b)
+    ty1 = min(tiles_y, ty0 + rows_b)
+    return min(height, ty0 * tile_size), min(height, ty1 * tile_size)
+

@@ -140,3 +140,72 @@ def test_two_rank_feature_shard_allgather_matches_full_render():
         assert equal, f"rank {rank}: sharded gather != full gather"
         assert uid_ok
         assert tmax == 2.0
+
+
+def _band_worker(rank, world, port, q):
+    """The geometry split's data flow with the CPU oracle as the per-rank compute: rank r owns the
+    pixel rows of its band; records are all-gathered (equal band chunks, the last padded), the
+    peak contributions max-reduced, and the geometry gradients of the band-masked upstream
+    gradients sum-reduced -- the whole frame's outputs on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    import _oracle as O
+    import scenegen as synth
+    from paper_2602_06991_b200.types import Pose, RenderSettings
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = synth.random_scene(120, 4, 9)
+        cam = synth.test_camera(40, 36)
+        s = RenderSettings(top_k=3, tile_size=8, background=(0.1, 0.2, 0.3))
+        W, H, K = cam.width, cam.height, 3
+        full = O.render_geometric(m, Pose(), cam, s)
+        y0, y1 = tkdist.band_rows(H, s.tile_size, world, rank)
+        bp = tkdist.band_rows(H, s.tile_size, world, 0)[1] * W  # pixels per band chunk (padded)
+        # this rank's band of records, padded to the chunk
+        idx = np.full(bp * K, -1, np.int32)
+        idx[:(y1 - y0) * W * K] = full["index"][y0 * W * K:y1 * W * K]
+        parts = [torch.zeros(bp * K, dtype=torch.int32) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(idx))
+        gathered = np.concatenate([p.numpy() for p in parts])[:W * H * K]
+        contrib = torch.from_numpy(np.ascontiguousarray(full["contributions"]))
+        dist.all_reduce(contrib, op=dist.ReduceOp.MAX)
+        gc = synth.uniform_image((H, W, 3), 12)
+        gd = synth.uniform_image((H, W), 13)
+        mask = np.zeros((H, W))
+        mask[y0:y1] = 1.0
+        g = O.backward_geometric(m, Pose(), cam, s, gc * mask[..., None], gd * mask)
+        mine = torch.from_numpy(np.concatenate([g[f].ravel() for f in ("mean", "log_scale", "rotation",
+                                                                        "opacity_logit", "color", "pose_twist")]))
+        dist.all_reduce(mine)
+        ref = O.backward_geometric(m, Pose(), cam, s, gc, gd)
+        refv = np.concatenate([ref[f].ravel() for f in ("mean", "log_scale", "rotation", "opacity_logit", "color",
+                                                        "pose_twist")])
+        err = float(np.max(np.abs(mine.numpy() - refv) / (np.abs(refv) + 1e-9 * np.abs(refv).max() + 1e-300)))
+        q.put((rank, bool(np.array_equal(gathered, full["index"])),
+               bool(np.array_equal(contrib.numpy(), full["contributions"])), err))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_geometry_split_band_flow_matches_whole_frame():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_band_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, rec_ok, contrib_ok, err in res:
+        assert rec_ok and contrib_ok and err < 1e-9, (rank, rec_ok, contrib_ok, err)
+
+
+def test_band_rows_cover_the_image():
+    for H, ts, G in [(680, 16, 8), (480, 16, 3), (36, 8, 2), (10, 32, 4)]:
+        rows = [tkdist.band_rows(H, ts, G, b) for b in range(G)]
+        assert rows[0][0] == 0 and rows[-1][1] == H
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
