@@ -50,11 +50,11 @@ CONFIGS = {
 }
 
 
-def bench_config(cfg, world, mode, gather, geo_split=False):
+def bench_config(cfg, world, mode, gather, geo_split=False, force_multi=False):
     """The workload's `config` object, identical for both arms (the reference arm runs the same
     scene, pose, seeds and settings on the host)."""
     D = cfg["d"]
-    dshard = world > 1 and mode == "dshard"
+    dshard = (world > 1 or force_multi) and mode == "dshard"
     P = cfg["w"] * cfg["h"]
     if dshard:
         par = (f"feature-dim shard d{world}: D/{world} channels per GPU, "
@@ -273,10 +273,18 @@ def main_gpu(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
-    if world > 1:
+    if world > 1 or args.force_multi:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo")
+        if world == 1:  # --force-multi: the N > 1 code path as a one-rank group (tests, one GPU)
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.setdefault("MASTER_PORT", str(sk.getsockname()[1]))
+            sk.close()
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     lib = N.render_lib()
     slib = synth.N.synth_lib()
@@ -286,7 +294,7 @@ def main_gpu(args, cfg):
     # keyframe mode (default): rank r renders keyframe r of the config-4 orbit batch with all D
     # channels -- independent views, no data-path collective (weak scaling).  dshard mode: every
     # rank renders the same view for its D/G channel slice and NCCL all-gathers the map.
-    dshard = world > 1 and args.mode == "dshard"
+    dshard = (world > 1 or args.force_multi) and args.mode == "dshard"
     shards = world if dshard else 1
     if D % shards:
         raise SystemExit("D must divide by the number of GPUs")
@@ -470,7 +478,7 @@ def main_gpu(args, cfg):
                   "frac": frame_bytes / (ms_step / 1000.0) / 1e9 / peak,
                   "formula": "P*D*4 (F) + P*D*4 (dF) + N*D*4 (df) + U*D*4 (rows) + 2*P*(K*12+1) (records)"}
     multi = None
-    if world > 1:
+    if world > 1 or args.force_multi:
         multi = {"ranks": world, "per_gpu_feature_dim": Ds,
                  "per_gpu_hbm_frac": frame_roof["frac"],
                  "nvlink_bytes_received_per_gpu": (P * D * 4 * (world - 1) // world) if dshard else 0,
@@ -497,12 +505,12 @@ def main_gpu(args, cfg):
             extras["mapedit"] = run_mapedit(lib, N, ctx, Ds, cpose)
 
     k_sweep = ref_grid = dropin = None
-    if world == 1 and not args.no_extras:
+    if world == 1 and not args.force_multi and not args.no_extras:
         k_sweep = run_k_sweep(lib, N, torch, dev, args.steps, peak)
         ref_grid = run_reference_grid(lib, N, torch, dev)
         dropin = run_dropin(dict(cfg, n=n), max(5, min(args.steps, 10)))
     kf_block = None
-    if world > 1 and dshard and not args.no_extras:
+    if (world > 1 or args.force_multi) and dshard and not args.no_extras:
         kf_block = run_keyframe_parallel(lib, N, torch, dev, cfg, K, rank, world, args.steps, dist)
 
     cpu = None
@@ -523,7 +531,8 @@ def main_gpu(args, cfg):
             "warmup": args.warmup, "ms_per_step": ms_step, "step_ms": step_stats, "higher_is_better": True,
             "scaling": "strong" if dshard else "weak", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic",
-            "config": bench_config(dict(cfg, n=n, k=K), world, args.mode, args.gather, args.geo_split),
+            "config": bench_config(dict(cfg, n=n, k=K), world, args.mode, args.gather, args.geo_split,
+                                   args.force_multi),
             "gather_path": gather_mode, "records": {"distinct_gaussians": U, "valid_slots": M},
             "frame_roofline": frame_roof, "multi_gpu": multi, "keyframe_parallel": kf_block,
             "k_sweep": k_sweep, "fslam_bench_grid": ref_grid, "e2e_dropin": dropin,
@@ -1099,6 +1108,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the K sweep, the fslam bench grid and extras")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
                     help="dshard: fused render + all-gather over peer memory, or render + NCCL all-gather")
+    ap.add_argument("--force-multi", action="store_true",
+                    help="run the N > 1 code path (process group, NCCL, D-sharding) with one rank (tests)")
     ap.add_argument("--geo-split", action="store_true",
                     help="dshard: split the geometric sweeps by tile-row bands across the ranks (records "
                          "all-gathered, geometry gradients sum-reduced: tk_geometry_band)")

@@ -60,3 +60,16 @@ def test_reference_arm_line(gpu_line):
     # honest about what ran: one warm-up frame, then the frames actually timed; same config object
     assert j["warmup"] == 1 and 1 <= j["steps"] <= 2 and j["steps_requested"] == 2
     assert j["config"] == gpu_line["config"] and j["metric"] == gpu_line["metric"]
+
+
+@pytest.mark.parametrize("extra", [[], ["--geo-split"], ["--gather", "nccl"]])
+def test_multi_gpu_code_path_one_rank(extra):
+    """The N > 1 path (process group, tk_comm over NCCL, D-sharded frame with the fused or NCCL
+    all-gather, optional geometry split, the keyframe-parallel block) run as a one-rank group:
+    the only multi-GPU coverage a one-GPU box allows; the contract keys must be there."""
+    j = run_bench("--config", "c1", "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu", "--force-multi",
+                  *extra)
+    assert j["value"] > 0 and j["multi_gpu"]["ranks"] == 1 and j["keyframe_parallel"]["value"] > 0
+    assert "feature-dim shard" in j["config"]["parallelism"]
+    assert (j["gather_path"] or "").startswith("p2p" if "--gather" not in extra else "nccl")
+    assert j["mapping"]["value"] > 0
