@@ -328,3 +328,22 @@ def test_backward_feature_huge_segments(R, w, h):
     assert a.tobytes() == b.tobytes()
     o = O.backward_feature(m, w, h, 4, g.topk.index, g.topk.weight, g.topk.count, gf.astype(np.float64))
     feat_close(a, o, 2e-5)
+
+
+@pytest.mark.parametrize("tile", [8, 13, 32])
+def test_backward_geometric_tile_sizes_match_oracle(R, tile):
+    """The fixed-order merge at 1, 4 and 16 warp blocks per tile (tile sizes 8, 13, 32): slot
+    indexing (pair x warp block) and the merge tiers match the oracle, and the result is the same
+    byte for byte when repeated."""
+    m, c = synth.random_scene(900, 4, 71), synth.test_camera(100, 76)
+    s = RenderSettings(tile_size=tile, background=(0.2, 0.1, 0.0))
+    gc = synth.uniform_image((c.height, c.width, 3), 21)
+    gd = synth.uniform_image((c.height, c.width), 22)
+    g = R.backward_geometric(m, Pose(), c, s, gc, gd)
+    o = O.backward_geometric(m, Pose(), c, s, gc, gd)
+    for f in ("mean", "log_scale", "rotation", "opacity_logit", "color"):
+        geom_close(getattr(g, f), o[f])
+    geom_close(g.pose_twist, o["pose_twist"])
+    again = R.backward_geometric(m, Pose(), c, s, gc, gd)
+    for f in ("mean", "log_scale", "rotation", "opacity_logit", "color", "pose_twist"):
+        assert getattr(g, f).tobytes() == getattr(again, f).tobytes(), f
