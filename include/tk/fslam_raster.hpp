@@ -341,11 +341,12 @@ public:
 
     ImageD render_feature(const SceneMap& m, const TopKGrid& t) {  // render.cpp:301-337
         sync_features(m);
-        std::vector<float> f(static_cast<std::size_t>(t.width) * t.height * m.feature_dim);
+        const std::size_t nf = static_cast<std::size_t>(t.width) * t.height * m.feature_dim;
+        float* f = stage<float>(7, nf);  // pinned: the read-back runs at the full PCIe rate
         tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
-        detail::check(tk_render_feature(ctx_, resident(t) ? nullptr : &v, f.data(), TK_HOST));
+        detail::check(tk_render_feature(ctx_, resident(t) ? nullptr : &v, f, TK_HOST));
         ImageD out(t.width, t.height, m.feature_dim);
-        widen(f, out.data);
+        widen(f, nf, out.data);
         return out;
     }
 
@@ -353,13 +354,14 @@ public:
                                      const RenderSettings& s) {  // render.cpp:339-343
         sync_geometry(m);
         sync_features(m);
-        std::vector<float> f(static_cast<std::size_t>(cam.width) * cam.height * m.feature_dim);
+        const std::size_t nf = static_cast<std::size_t>(cam.width) * cam.height * m.feature_dim;
+        float* f = stage<float>(7, nf);
         const tk_pose p = detail::to_c(pose);
         const tk_camera c = detail::to_c(cam);
         const tk_settings st = detail::to_c(s);
-        detail::check(tk_render_feature_full_blend(ctx_, &p, &c, &st, f.data(), TK_HOST));
+        detail::check(tk_render_feature_full_blend(ctx_, &p, &c, &st, f, TK_HOST));
         ImageD out(cam.width, cam.height, m.feature_dim);
-        widen(f, out.data);
+        widen(f, nf, out.data);
         return out;
     }
 
@@ -371,11 +373,12 @@ public:
         parallel_rows(grad_feature.data.size(), grad_feature.data.size(), [&](std::size_t i0, std::size_t i1) {
             for (std::size_t i = i0; i < i1; ++i) g[i] = static_cast<float>(gs[i]);
         });
-        std::vector<float> o(m.size() * static_cast<std::size_t>(m.feature_dim));
+        const std::size_t no = m.size() * static_cast<std::size_t>(m.feature_dim);
+        float* o = stage<float>(8, no);
         tk_topk_view v{t.width, t.height, t.k, t.index.data(), t.weight.data(), t.count.data(), TK_HOST};
-        detail::check(tk_backward_feature(ctx_, resident(t) ? nullptr : &v, g, TK_HOST, o.data(), TK_HOST));
-        std::vector<double> out(o.size());
-        widen(o, out);
+        detail::check(tk_backward_feature(ctx_, resident(t) ? nullptr : &v, g, TK_HOST, o, TK_HOST));
+        std::vector<double> out(no);
+        widen(o, no, out);
         return out;
     }
 
@@ -384,8 +387,12 @@ public:
                                  const ImageD& grad_depth) {  // backward.cpp:72-271
         sync_geometry(m);
         const std::size_t n = m.size();
-        std::vector<double> gm(n * 3), gl(n * 3), gr(n * 4), go(n), gc(n * 3);
-        tk_geom_grads out{TK_HOST, gm.data(), gl.data(), gr.data(), go.data(), gc.data(), {0, 0, 0, 0, 0, 0}};
+        double* gm = stage<double>(9, n * 3);
+        double* gl = stage<double>(10, n * 3);
+        double* gr = stage<double>(11, n * 4);
+        double* go = stage<double>(12, n);
+        double* gc = stage<double>(13, n * 3);
+        tk_geom_grads out{TK_HOST, gm, gl, gr, go, gc, {0, 0, 0, 0, 0, 0}};
         const tk_pose p = detail::to_c(pose);
         const tk_camera c = detail::to_c(cam);
         const tk_settings st = detail::to_c(s);
@@ -395,14 +402,16 @@ public:
         g.mean.resize(n);
         g.log_scale.resize(n);
         g.rotation.resize(n);
-        g.opacity_logit = go;
+        g.opacity_logit.assign(go, go + n);
         g.color.resize(n);
-        for (std::size_t i = 0; i < n; ++i) {
-            g.mean[i] = {gm[i * 3], gm[i * 3 + 1], gm[i * 3 + 2]};
-            g.log_scale[i] = {gl[i * 3], gl[i * 3 + 1], gl[i * 3 + 2]};
-            g.rotation[i] = {gr[i * 4], gr[i * 4 + 1], gr[i * 4 + 2], gr[i * 4 + 3]};
-            g.color[i] = {gc[i * 3], gc[i * 3 + 1], gc[i * 3 + 2]};
-        }
+        parallel_rows(n, n * 14, [&](std::size_t i0, std::size_t i1) {
+            for (std::size_t i = i0; i < i1; ++i) {
+                g.mean[i] = {gm[i * 3], gm[i * 3 + 1], gm[i * 3 + 2]};
+                g.log_scale[i] = {gl[i * 3], gl[i * 3 + 1], gl[i * 3 + 2]};
+                g.rotation[i] = {gr[i * 4], gr[i * 4 + 1], gr[i * 4 + 2], gr[i * 4 + 3]};
+                g.color[i] = {gc[i * 3], gc[i * 3 + 1], gc[i * 3 + 2]};
+            }
+        });
         for (int a = 0; a < 6; ++a) g.pose_twist[a] = out.pose_twist[a];
         return g;
     }
@@ -472,8 +481,8 @@ private:
         for (auto& th : pool) th.join();
     }
 
-    static void widen(const std::vector<float>& f, std::vector<double>& d) {  // fp32 results -> fp64 API
-        parallel_rows(f.size(), f.size(), [&](std::size_t i0, std::size_t i1) {
+    static void widen(const float* f, std::size_t n, std::vector<double>& d) {  // fp32 results -> fp64 API
+        parallel_rows(n, n, [&](std::size_t i0, std::size_t i1) {
             for (std::size_t i = i0; i < i1; ++i) d[i] = f[i];
         });
     }
