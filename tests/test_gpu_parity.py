@@ -330,9 +330,9 @@ def test_backward_feature_huge_segments(R, w, h):
     feat_close(a, o, 2e-5)
 
 
-@pytest.mark.parametrize("tile", [8, 13, 32])
+@pytest.mark.parametrize("tile", [8, 13, 32, 64])
 def test_backward_geometric_tile_sizes_match_oracle(R, tile):
-    """The fixed-order merge at 1, 4 and 16 warp blocks per tile (tile sizes 8, 13, 32): slot
+    """The fixed-order merge at 1, 4, 16 and 64 warp blocks per tile (tile sizes 8, 13, 32, 64): slot
     indexing (pair x warp block) and the merge tiers match the oracle, and the result is the same
     byte for byte when repeated."""
     m, c = synth.random_scene(900, 4, 71), synth.test_camera(100, 76)
@@ -347,3 +347,25 @@ def test_backward_geometric_tile_sizes_match_oracle(R, tile):
     again = R.backward_geometric(m, Pose(), c, s, gc, gd)
     for f in ("mean", "log_scale", "rotation", "opacity_logit", "color", "pose_twist"):
         assert getattr(g, f).tobytes() == getattr(again, f).tobytes(), f
+
+
+def test_features_only_upload_keeps_geometry_state(R):
+    """tk_scene_upload_features replaces the features only (the prepared scene and the forward
+    records stay valid): the gather then reads the new rows; n / d mismatches are rejected."""
+    import ctypes as C
+    from paper_2602_06991_b200 import _native as N
+    m, c = synth.random_scene(300, 8, 5), synth.test_camera(48, 40)
+    s = RenderSettings()
+    g = R.render_geometric(m, Pose(), c, s)
+    m2 = m.copy()
+    m2.feature = (m.feature.astype(np.float32) * -0.5).astype(np.float32)
+    feat = np.ascontiguousarray(m2.feature, np.float32)
+    N.check(R.lib.tk_scene_upload_features(R.ctx, m.size(), 8, feat.ctypes.data, N.TK_HOST))
+    out = np.zeros((40, 48, 8), np.float32)
+    N.check(R.lib.tk_render_feature(R.ctx, None, out.ctypes.data, N.TK_HOST))  # resident records
+    ref = O.render_feature(m2, 48, 40, 3, g.topk.index, g.topk.weight, g.topk.count)
+    feat_close(out, ref)
+    with pytest.raises(N.TkError):
+        N.check(R.lib.tk_scene_upload_features(R.ctx, m.size() + 1, 8, feat.ctypes.data, N.TK_HOST))
+    with pytest.raises(N.TkError):
+        N.check(R.lib.tk_scene_upload_features(R.ctx, m.size(), 4, feat.ctypes.data, N.TK_HOST))
