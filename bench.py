@@ -502,7 +502,7 @@ def main_gpu(args, cfg):
                               0 if args.no_e2e else args.e2e_steps, stream, dist, sharded=dshard, scene=scene,
                               cam=cam, gt_pose=pose, d_total=D, c0=c0)
         if not dshard and not args.no_extras and extras is not None:
-            extras["mapedit"] = run_mapedit(lib, N, ctx, Ds, cpose)
+            extras["mapedit"] = run_mapedit(lib, N, ctx, Ds, cpose, ccam, cset)
 
     k_sweep = ref_grid = dropin = None
     if world == 1 and not args.force_multi and not args.no_extras:
@@ -938,7 +938,7 @@ def run_k_sweep(lib, N, torch, dev, steps, peak):
     return out
 
 
-def run_mapedit(lib, N, ctx, D, kpose, n_insert=100_000):
+def run_mapedit(lib, N, ctx, D, kpose, ccam=None, cset=None, n_insert=100_000):
     """Structural edits on the config-3 map after the mapping run (its selection statistics):
     insert_gaussians with n_insert source points (mapper.cpp:19-60; all farther than tau, so all
     inserted) and prune_map with the reference defaults keep_ratio 0.5, threshold 0
@@ -953,27 +953,44 @@ def run_mapedit(lib, N, ctx, D, kpose, n_insert=100_000):
     dist = np.full(n_insert, np.inf)
     view = N.tk_source_view(n_insert, D, pos.ctypes.data, col.ctypes.data, feat.ctypes.data, sp.ctypes.data,
                             dist.ctypes.data, N.TK_HOST)
-    n0, d0, g0 = C.c_int64(), C.c_int32(), C.c_uint64()
-    N.check(lib.tk_scene_info(ctx, C.byref(n0), C.byref(d0), C.byref(g0)))
-    N.check(lib.tk_synchronize(ctx))
-    inserted = C.c_int32()
-    t0 = time.time()
-    N.check(lib.tk_insert_gaussians(ctx, C.byref(view), 0.01, C.byref(kpose), C.byref(inserted)))
-    N.check(lib.tk_synchronize(ctx))
-    t1 = time.time()
-    n1 = C.c_int64()
-    N.check(lib.tk_scene_info(ctx, C.byref(n1), C.byref(d0), C.byref(g0)))
-    removed = C.c_int64()
-    t2 = time.time()
-    N.check(lib.tk_prune_map(ctx, 0.5, 42, 0, None, C.byref(removed)))
-    N.check(lib.tk_synchronize(ctx))
-    t3 = time.time()
-    return {"insert": {"source_points": n_insert, "inserted": inserted.value, "map_before": n0.value,
-                       "ms": 1000.0 * (t1 - t0),
+
+    def cycle():
+        n0, d0, g0 = C.c_int64(), C.c_int32(), C.c_uint64()
+        N.check(lib.tk_scene_info(ctx, C.byref(n0), C.byref(d0), C.byref(g0)))
+        N.check(lib.tk_synchronize(ctx))
+        inserted = C.c_int32()
+        t0 = time.time()
+        N.check(lib.tk_insert_gaussians(ctx, C.byref(view), 0.01, C.byref(kpose), C.byref(inserted)))
+        N.check(lib.tk_synchronize(ctx))
+        t1 = time.time()
+        n1 = C.c_int64()
+        N.check(lib.tk_scene_info(ctx, C.byref(n1), C.byref(d0), C.byref(g0)))
+        removed = C.c_int64()
+        t2 = time.time()
+        N.check(lib.tk_prune_map(ctx, 0.5, 42, 0, None, C.byref(removed)))
+        N.check(lib.tk_synchronize(ctx))
+        t3 = time.time()
+        return n0.value, inserted.value, 1000.0 * (t1 - t0), n1.value, removed.value, 1000.0 * (t3 - t2)
+
+    # First cycle: the map grows past its allocations (every Adam group, the statistics and the
+    # 2 GB feature array are reallocated, from the driver: box-dependent); second cycle, after five
+    # mapping iterations have rebuilt the selection statistics: steady state (the device pool of
+    # tk_abi.cu serves the regrown and compacted arrays), the number a SLAM loop sees.
+    c0 = cycle()
+    if ccam is not None:  # fresh selection statistics for the second prune (the first one reset them)
+        cfg = N.tk_mapper_config()
+        lib.tk_default_mapper_config(C.byref(cfg))
+        N.check(lib.tk_optimizer_reset(ctx, 1))
+        for i in range(1, 6):
+            N.check(lib.tk_optimize_step(ctx, C.byref(cfg), C.byref(ccam), C.byref(cset), 0, i, None, None))
+    c1 = cycle()
+    return {"insert": {"source_points": n_insert, "inserted": c1[1], "map_before": c1[0], "ms": c1[2],
+                       "cold": {"map_before": c0[0], "inserted": c0[1], "ms": c0[2]},
                        "path": "tk_insert_gaussians: host source points -> device flags, scan, one warp per "
-                               "inserted Gaussian; every Adam group and the statistics grow in lockstep"},
-            "prune": {"map_before": n1.value, "removed": removed.value, "keep_ratio": 0.5, "threshold": 0,
-                      "ms": 1000.0 * (t3 - t2),
+                               "inserted Gaussian; every Adam group and the statistics grow in lockstep "
+                               "(ms: second insert+prune cycle; cold: the first, which reallocates the map)"},
+            "prune": {"map_before": c1[3], "removed": c1[4], "keep_ratio": 0.5, "threshold": 0, "ms": c1[5],
+                      "cold": {"map_before": c0[3], "removed": c0[4], "ms": c0[5]},
                       "path": "tk_prune_map: statistics to the host, the reference's exact weighted draw "
                               "without replacement in O(C log C) (Fenwick pool, rounding-bounded fallback to "
                               "the sequential scan), device compaction of the map, features and optimiser state"}}

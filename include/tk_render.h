@@ -126,8 +126,9 @@ typedef struct { /* GeomGrads, raster/backward.hpp:15-22; NULL pointers are skip
     double* rotation;      /* n x 4 (w,x,y,z) */
     double* opacity_logit; /* n */
     double* color;         /* n x 3 */
-    double pose_twist[6];  /* out: [nu, omega]; with TK_HOST_ASYNC written at tk_synchronize
-                            * (the struct must stay alive until then) */
+    double pose_twist[6];  /* out: [nu, omega]; with TK_HOST_ASYNC or TK_DEVICE written at
+                            * tk_synchronize (the struct must stay alive until then), so a
+                            * device-resident frame never waits on the host */
 } tk_geom_grads;
 
 typedef struct { /* resident device buffers of the last calls (read-only views) */

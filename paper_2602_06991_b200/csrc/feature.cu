@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
 // every pixel: one segment of P records).  The renormalised slot weight is computed on the way.
 __global__ void k_slot_keys(SlotKeyParams p, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p.zero2 && s < 2) p.zero2[s] = 0;
     if (s >= p.n_slots) return;
     const int64_t px = s / p.k;
     const int j = static_cast<int>(s - px * p.k);
@@ -349,7 +350,9 @@ __global__ void k_slot_keys(SlotKeyParams p, uint32_t* __restrict__ keys, uint32
 // (queue[n - 1 - i], i < counts[1]); the queue order is irrelevant (each segment is summed by its
 // own chunks and combined in chunk order).
 __global__ void k_long_queue(const int32_t* __restrict__ seg, int64_t n, int32_t* __restrict__ queue,
-                             int32_t* __restrict__ counts) {
+                             int32_t* __restrict__ counts, int32_t* __restrict__ plan_counters) {
+    if (plan_counters && blockIdx.x == 0)  // the long plan's counters start at zero (no memset)
+        for (int i = threadIdx.x; i < kPlanCounters + 1; i += blockDim.x) plan_counters[i] = 0;
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x)
         if (seg[g + 1] - seg[g] > kLongSeg) queue[n - 1 - atomicAdd(counts + 1, 1)] = static_cast<int32_t>(g);
@@ -438,65 +441,246 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     }
 }
 
-// One thread per queued long segment: reserve its partial rows and list its items.
-__global__ void k_long_plan(const int32_t* __restrict__ seg, int64_t n, LongPlan plan) {
-    const int nq = *plan.qcount;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += gridDim.x * blockDim.x) {
-        const int g = plan.queue[n - 1 - i];
+// ---- long segments: band-major plan (feature.cuh)
+__device__ __forceinline__ int record_row(const LongPlan& pl, int r) {
+    return static_cast<int>((pl.slots[r] / static_cast<uint32_t>(pl.k)) / static_cast<uint32_t>(pl.width));
+}
+
+// Lane b's band of records [lo, hi) within [r0, r1): records ascend in slot (pixel) order, so
+// band b starts at the first record on pixel row >= b * band_rows.
+__device__ __forceinline__ void band_range(const LongPlan& pl, int r0, int r1, int lane, int& lo, int& hi) {
+    int a = r0, b = r1;
+    if (lane > 0) {
+        const int row0 = lane * pl.band_rows;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (record_row(pl, mid) < row0) a = mid + 1;
+            else b = mid;
+        }
+    }
+    lo = a;
+    hi = __shfl_down_sync(0xffffffffu, lo, 1);
+    if (lane == kBands - 1) hi = r1;
+}
+
+// One warp per queued long segment: its items per band, its partial rows (numbered in record
+// order), its level-1 groups.
+__global__ void __launch_bounds__(kThreads) k_long_count(const int32_t* __restrict__ seg, int64_t n, LongPlan pl) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int nq = *pl.qcount;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; i < nq; i += nw) {
+        const int g = pl.queue[n - 1 - i];
         const int r0 = seg[g], r1 = seg[g + 1];
         if (r1 - r0 <= kLongSeg) continue;
-        const int nch = (r1 - r0 + kLongSeg - 1) / kLongSeg;
-        const int base = atomicAdd(&plan.counters[0], nch);
-        const int li = atomicAdd(&plan.counters[1], 1);
-        plan.longs[li] = make_int4(g, base, nch, 0);
-        for (int c = 0; c < nch; ++c)
-            plan.items[base + c] = make_int4(g, r0 + c * kLongSeg, min(r1, r0 + (c + 1) * kLongSeg), base + c);
-    }
-}
-
-// One warp per chunk of a long segment: partial sums into the plan's scratch rows.
-template <bool VEC>
-__global__ void __launch_bounds__(kThreads) k_feat_bwd_chunks(FeatBwdParams p, LongPlan plan) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int dd = VEC ? p.d >> 2 : p.d;
-    const int ni = plan.counters[0];
-    for (int64_t it = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; it < ni; it += nw) {
-        const int4 item = plan.items[it];
-        const int r0 = item.y, r1 = item.z;
-        for (int base = 0; base < dd; base += 128) {
-            float4 acc4[4];
-            float acc1[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum_records<VEC>(p, r0, r1, base, lane, acc4, acc1);
-            store_pass<VEC>(plan.partial + static_cast<int64_t>(item.w) * p.d, dd, base, lane, acc4, acc1);
+        int lo, hi;
+        band_range(pl, r0, r1, lane, lo, hi);
+        const int nb = (hi - lo + kLongItem - 1) / kLongItem;
+        const int ng = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(nb)));
+        const int ngrp = (ng + kCombineGroup - 1) / kCombineGroup;
+        int base = 0, li = 0, l1 = 0;
+        if (lane == 0) {
+            base = atomicAdd(&pl.counters[0], ng);
+            li = atomicAdd(&pl.counters[1], 1);
+            l1 = atomicAdd(&pl.counters[2], ngrp);
+            pl.longs[li] = make_int4(g, base, ng, l1);
         }
+        li = __shfl_sync(0xffffffffu, li, 0);
+        l1 = __shfl_sync(0xffffffffu, l1, 0);
+        for (int q = lane; q < ngrp; q += 32) pl.l1_map[l1 + q] = make_int2(li, q);
+        if (nb > 0) atomicAdd(&pl.counters[kPlanBandCnt + lane], nb);
+    }
+    // the last block to finish turns the band counts into the bands' offsets in the item list
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&pl.counters[kPlanCounters], 1) == static_cast<int>(gridDim.x) - 1;
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+        __threadfence();
+        const int v = atomicAdd(&pl.counters[kPlanBandCnt + lane], 0);  // L2 value
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += u;
+        }
+        pl.counters[kPlanBandOff + lane] = x - v;
     }
 }
 
-// One warp per long Gaussian: chunk partials added in chunk order, the dense row written once.
-__global__ void __launch_bounds__(kThreads) k_feat_bwd_combine(FeatBwdParams p, LongPlan plan) {
+// One warp per long Gaussian: its items into the band-major list (the order within a band is
+// the atomics' order and irrelevant: every item owns its partial row).
+__global__ void __launch_bounds__(kThreads) k_long_fill(const int32_t* __restrict__ seg, LongPlan pl) {
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
-    const int nl = plan.counters[1];
+    const int nl = pl.counters[1];
     for (int64_t li = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; li < nl; li += nw) {
-        const int4 lg = plan.longs[li];
-        for (int q = lane; q < p.d; q += 32) {
-            // partial rows added in order; their loads issued 8 ahead of the dependent adds
-            const float* col = plan.partial + static_cast<int64_t>(lg.y) * p.d + q;
-            float acc = 0.0f;
-            int c = 0;
-            for (; c + 8 <= lg.z; c += 8) {
-                float v[8];
+        const int4 lg = pl.longs[li];
+        const int g = lg.x;
+        int lo, hi;
+        band_range(pl, seg[g], seg[g + 1], lane, lo, hi);
+        const int nb = (hi - lo + kLongItem - 1) / kLongItem;
+        int local = nb;  // exclusive scan over the bands: first partial row of this band
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = col[static_cast<int64_t>(c + u) * p.d];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc += v[u];
-            }
-            for (; c < lg.z; ++c) acc += col[static_cast<int64_t>(c) * p.d];
-            p.out[static_cast<int64_t>(lg.x) * p.d + q] = acc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, local, o);
+            if (lane >= o) local += u;
         }
+        local -= nb;
+        if (nb > 0) {
+            const int pos = pl.counters[kPlanBandOff + lane] + atomicAdd(&pl.counters[kPlanBandFill + lane], nb);
+            for (int c = 0; c < nb; ++c)
+                pl.items[pos + c] = make_int4(g, lo + c * kLongItem, min(hi, lo + (c + 1) * kLongItem), lg.y + local + c);
+        }
+    }
+}
+
+// Column helpers of the long-segment kernels: VEC = float4 columns, else float columns.
+template <bool VEC> struct Col;
+template <> struct Col<true> {
+    using T = float4;
+    static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+    static __device__ __forceinline__ T ld(const float* row, int q) { return __ldg(reinterpret_cast<const float4*>(row) + q); }
+    static __device__ __forceinline__ T ldcs(const float* row, int q) { return __ldcs(reinterpret_cast<const float4*>(row) + q); }
+    static __device__ __forceinline__ void st(float* row, int q, T v) { reinterpret_cast<float4*>(row)[q] = v; }
+    static __device__ __forceinline__ T fma(float w, T x, T a) { return fma4(w, x, a); }
+    static __device__ __forceinline__ T add(T a, T b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+};
+template <> struct Col<false> {
+    using T = float;
+    static __device__ __forceinline__ T zero() { return 0.f; }
+    static __device__ __forceinline__ T ld(const float* row, int q) { return __ldg(row + q); }
+    static __device__ __forceinline__ T ldcs(const float* row, int q) { return __ldcs(row + q); }
+    static __device__ __forceinline__ void st(float* row, int q, T v) { row[q] = v; }
+    static __device__ __forceinline__ T fma(float w, T x, T a) { return fmaf(w, x, a); }
+    static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+};
+
+// Persistent warps over the band-major (item, 32-column block) list: the item's records summed
+// in slot order into its partial row (per channel: acc = fma(w_j, dF_j, acc), j ascending, as in
+// accum_records), eight record rows in flight per lane.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads, 3) k_feat_bwd_items(FeatBwdParams p, LongPlan plan) {
+    using C = Col<VEC>;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    const int dd = VEC ? D >> 2 : D;
+    const int parts = (dd + 31) >> 5;
+    const int64_t ntask = static_cast<int64_t>(plan.counters[0]) * parts;
+    for (int64_t t = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; t < ntask; t += nw) {
+        const int it = static_cast<int>(t / parts);
+        const int q = static_cast<int>(t - static_cast<int64_t>(it) * parts) * 32 + lane;
+        const bool on = q < dd;
+        const int4 item = plan.items[it];
+        typename C::T acc = C::zero();
+        for (int r = item.y; r < item.z; r += 32) {
+            const int nr = min(32, item.z - r);
+            int64_t spx = 0;
+            float sw = 0.f;
+            if (lane < nr) {
+                const uint32_t s = p.slots[r + lane];
+                spx = static_cast<int64_t>(s / static_cast<uint32_t>(p.k));
+                sw = p.wnorm[s];
+            }
+            if (!__any_sync(0xffffffffu, lane < nr && !isfinite(sw))) {
+                int j = 0;
+                for (; j + 8 <= nr; j += 8) {
+                    typename C::T v[8];
+                    float w[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int64_t px = __shfl_sync(0xffffffffu, spx, j + u);
+                        w[u] = __shfl_sync(0xffffffffu, sw, j + u);
+                        v[u] = on ? C::ld(p.grad + px * D, q) : C::zero();
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = C::fma(w[u], v[u], acc);
+                }
+                for (; j < nr; ++j) {
+                    const int64_t px = __shfl_sync(0xffffffffu, spx, j);
+                    const float wj = __shfl_sync(0xffffffffu, sw, j);
+                    if (on) acc = C::fma(wj, C::ld(p.grad + px * D, q), acc);
+                }
+            } else {
+                for (int j = 0; j < nr; ++j) {
+                    const int64_t pxj = __shfl_sync(0xffffffffu, spx, j);
+                    const float wj = __shfl_sync(0xffffffffu, sw, j);
+                    if (!isfinite(wj)) {  // as accum_records: only live gradient rows propagate 0/0
+                        bool any = false;
+                        for (int c = lane; c < D; c += 32) any |= p.grad[pxj * D + c] != 0.0f;
+                        if (!__any_sync(0xffffffffu, any)) continue;
+                    }
+                    if (on) acc = C::fma(wj, C::ld(p.grad + pxj * D, q), acc);
+                }
+            }
+        }
+        if (on) C::st(plan.partial + static_cast<int64_t>(item.w) * D, q, acc);
+    }
+}
+
+// Level 1 of the combine: each group of kCombineGroup consecutive partial rows of a long
+// Gaussian added in row order (all loads of the group issued before the adds).
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_long_combine1(FeatBwdParams p, LongPlan plan) {
+    using C = Col<VEC>;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    const int dd = VEC ? D >> 2 : D;
+    const int parts = (dd + 31) >> 5;
+    const int64_t ntask = static_cast<int64_t>(plan.counters[2]) * parts;
+    for (int64_t t = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; t < ntask; t += nw) {
+        const int r = static_cast<int>(t / parts);
+        const int q = static_cast<int>(t - static_cast<int64_t>(r) * parts) * 32 + lane;
+        if (q >= dd) continue;
+        const int2 m = plan.l1_map[r];
+        const int4 lg = plan.longs[m.x];
+        const int c0 = m.y * kCombineGroup, c1 = min(lg.z, c0 + kCombineGroup);
+        const float* base = plan.partial + static_cast<int64_t>(lg.y) * D;
+        typename C::T acc = C::zero();
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {
+            typename C::T v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = C::ldcs(base + static_cast<int64_t>(c + u) * D, q);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = C::add(acc, v[u]);
+        }
+        for (; c < c1; ++c) acc = C::add(acc, C::ldcs(base + static_cast<int64_t>(c) * D, q));
+        C::st(plan.l1 + static_cast<int64_t>(r) * D, q, acc);
+    }
+}
+
+// Level 2: a long Gaussian's group sums added in group order, the dense row written once.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_long_combine2(FeatBwdParams p, LongPlan plan) {
+    using C = Col<VEC>;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int D = p.d;
+    const int dd = VEC ? D >> 2 : D;
+    const int parts = (dd + 31) >> 5;
+    const int64_t ntask = static_cast<int64_t>(plan.counters[1]) * parts;
+    for (int64_t t = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; t < ntask; t += nw) {
+        const int li = static_cast<int>(t / parts);
+        const int q = static_cast<int>(t - static_cast<int64_t>(li) * parts) * 32 + lane;
+        if (q >= dd) continue;
+        const int4 lg = plan.longs[li];
+        const int ngrp = (lg.z + kCombineGroup - 1) / kCombineGroup;
+        const float* base = plan.l1 + static_cast<int64_t>(lg.w) * D;
+        typename C::T acc = C::zero();
+        int c = 0;
+        for (; c + 8 <= ngrp; c += 8) {
+            typename C::T v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = C::ldcs(base + static_cast<int64_t>(c + u) * D, q);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = C::add(acc, v[u]);
+        }
+        for (; c < ngrp; ++c) acc = C::add(acc, C::ldcs(base + static_cast<int64_t>(c) * D, q));
+        C::st(p.out + static_cast<int64_t>(lg.x) * D, q, acc);
     }
 }
 
@@ -598,15 +782,18 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
 
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg, int32_t* queue, uint32_t* keys,
                        uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t** sorted_vals,
-                       void* radix_scratch, cudaStream_t st) {
+                       void* radix_scratch, int32_t* plan_counters, cudaStream_t st) {
     int32_t* counts = queue + n_gaussians;  // [0] unused, [1] long segments
-    cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
     *sorted_vals = vals;
-    if (p.n_slots <= 0) {
-        cudaMemsetAsync(seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
-        return;
+    if (p.n_slots <= 0 || n_gaussians <= 0) {
+        cudaMemsetAsync(counts, 0, 2 * sizeof(int32_t), st);
+        if (p.n_slots <= 0) cudaMemsetAsync(seg, 0, (n_gaussians + 1) * sizeof(int32_t), st);
+        if (plan_counters) cudaMemsetAsync(plan_counters, 0, (kPlanCounters + 1) * sizeof(int32_t), st);
+        if (p.n_slots <= 0) return;
     }
-    k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(p, keys, vals);
+    SlotKeyParams q = p;
+    q.zero2 = n_gaussians > 0 ? counts : nullptr;  // k_slot_keys zeroes the queue counters
+    k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(q, keys, vals);
     dbg_launch("k_slot_keys", st);
     int bits = 0;
     while (bits < 32 && (static_cast<uint64_t>(n_gaussians) >> bits) != 0) ++bits;  // keys in [0, n]
@@ -617,29 +804,37 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg
     segment_offsets_u32(alt ? keys_alt : keys, p.n_slots, seg, n_gaussians, st);
     if (n_gaussians > 0) {
         const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((n_gaussians + 255) / 256, 148 * 16));
-        k_long_queue<<<g1, 256, 0, st>>>(seg, n_gaussians, queue, counts);
+        k_long_queue<<<g1, 256, 0, st>>>(seg, n_gaussians, queue, counts, plan_counters);
         dbg_launch("k_long_queue", st);
     }
 }
 
 void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st) {
-    cudaMemsetAsync(plan.counters, 0, 2 * sizeof(int32_t), st);
+    // counters zeroed by k_long_queue (launch_slot_index)
     if (n <= 0) return;
-    k_long_plan<<<16, 256, 0, st>>>(seg, n, plan);
-    dbg_launch("k_long_plan", st);
+    k_long_count<<<148 * 2, kThreads, 0, st>>>(seg, n, plan);
+    dbg_launch("k_long_count", st);
+    k_long_fill<<<148 * 2, kThreads, 0, st>>>(seg, plan);
+    dbg_launch("k_long_fill", st);
 }
 
 void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st) {
     if (p.n_gaussians <= 0 || p.d <= 0) return;
-    const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0;
+    const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0 &&
+                     (reinterpret_cast<uintptr_t>(plan.l1) % 16) == 0;
     if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
     else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
     dbg_launch("k_feat_bwd", st);
-    if (vec) k_feat_bwd_chunks<true><<<148 * 8, kThreads, 0, st>>>(p, plan);
-    else k_feat_bwd_chunks<false><<<148 * 8, kThreads, 0, st>>>(p, plan);
-    dbg_launch("k_feat_bwd_chunks", st);
-    k_feat_bwd_combine<<<148 * 4, kThreads, 0, st>>>(p, plan);
-    dbg_launch("k_feat_bwd_combine", st);
+    // persistent grids: the band-major item list is walked in order by every resident warp
+    if (vec) k_feat_bwd_items<true><<<148 * 6, kThreads, 0, st>>>(p, plan);
+    else k_feat_bwd_items<false><<<148 * 6, kThreads, 0, st>>>(p, plan);
+    dbg_launch("k_feat_bwd_items", st);
+    if (vec) k_long_combine1<true><<<148 * 4, kThreads, 0, st>>>(p, plan);
+    else k_long_combine1<false><<<148 * 4, kThreads, 0, st>>>(p, plan);
+    dbg_launch("k_long_combine1", st);
+    if (vec) k_long_combine2<true><<<148 * 2, kThreads, 0, st>>>(p, plan);
+    else k_long_combine2<false><<<148 * 2, kThreads, 0, st>>>(p, plan);
+    dbg_launch("k_long_combine2", st);
 }
 
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,

@@ -44,6 +44,7 @@ struct SlotKeyParams {
     uint32_t* keys;        // unused (kept for layout stability)
     uint32_t* vals;        // unused
     float* wnorm;          // renormalised slot weight (render.cpp:324-329)
+    int32_t* zero2 = nullptr;  // two counters zeroed on the way (launch_slot_index)
 };
 
 struct FeatBwdParams {
@@ -58,25 +59,50 @@ struct FeatBwdParams {
 };
 
 // Gaussians with more than kLongSeg records (a near-camera Gaussian in the Top-K of most pixels
-// owns one record per pixel) are not summed by one warp: their slot-sorted records are cut into
-// items of kLongSeg records, each summed by its own warp into its own partial row, and the combine
-// adds a Gaussian's partial rows in item order (deterministic).  The plan is built on the device
-// from the long-segment queue of launch_slot_index.  (Ordering the items by pixel band, so that
-// the warps in flight share dF rows in L2, was measured: 8.3 -> 7.4 GB of DRAM reads at config 2,
-// K = 16, no faster -- every item is in flight at once -- and 26 us slower to plan at config 3.)
-constexpr int kLongSeg = 1024;
+// owns one record per pixel) are not summed by one warp.  Their slot-sorted records (pixel order)
+// are cut at kBands pixel-row band boundaries and into items of at most kLongItem records; each
+// item is summed into its own partial row, and a Gaussian's partial rows (numbered in record
+// order) are added in that order by a fixed two-level tree (groups of kCombineGroup rows, then
+// the group sums), so the result never depends on execution order: deterministic.
+// The items are listed band-major and a persistent grid of warps walks the list in order, one
+// warp per (item, 128-channel column block), so the items in flight cover a narrow band of image
+// rows and the dF rows that the long Gaussians of a pixel share are re-read from L2, not HBM.
+// (Round 2 before this: kLongSeg-record items, all in flight at once, one warp per item over all
+// D channels and a serial per-Gaussian combine -- 1.2 ms of a 1.7 ms feature backward at config 1,
+// K = 16, DRAM-bound on dF re-reads.)
+#ifndef TK_LONG_SEG
+#define TK_LONG_SEG 1024
+#endif
+constexpr int kLongSeg = TK_LONG_SEG;
+#ifndef TK_LONG_ITEM
+#define TK_LONG_ITEM 128
+#endif
+constexpr int kLongItem = TK_LONG_ITEM;
+constexpr int kBands = 32;  // one lane per band in the plan kernels
+constexpr int kCombineGroup = 32;
+// counters: [0] items (= partial rows), [1] long Gaussians, [2] level-1 rows, then per band:
+// item counts, fill cursors, exclusive offsets
+constexpr int kPlanBandCnt = 3, kPlanBandFill = kPlanBandCnt + kBands, kPlanBandOff = kPlanBandFill + kBands;
+constexpr int kPlanCounters = kPlanBandOff + kBands;  // + 1: k_long_count's done counter
 struct LongPlan {
-    int4* items;        // {g, first record, end record, partial row}
-    int4* longs;        // {g, first partial row, partial rows, -}
-    int32_t* counters;  // [0] items, [1] long Gaussians
+    int4* items;        // {g, first record, end record, partial row}, band-major
+    int4* longs;        // {g, first partial row, partial rows, first level-1 row}
+    int32_t* counters;  // kPlanCounters
+    int2* l1_map;       // level-1 row -> {long Gaussian, group}
     float* partial;     // cap_items x D
-    int64_t cap_items;
+    float* l1;          // cap_l1 x D
+    int64_t cap_items, cap_l1;
     const int32_t* queue;   // launch_slot_index's queue: long segments at its back
     const int32_t* qcount;  // number of queued long segments (device)
+    const uint32_t* slots;  // records sorted by (Gaussian, slot): record -> slot
+    int k, width, band_rows;
 };
-// capacity of the item list for m valid records among n Gaussians
-inline int64_t long_plan_capacity(int64_t m, int64_t n) {
-    return m / kLongSeg + (m / kLongSeg < n ? m / kLongSeg : n) + 1;
+// capacity of the item list for m valid records among n Gaussians (each long Gaussian adds at
+// most one partial item per band) and of the level-1 rows
+inline int64_t long_plan_longs(int64_t m, int64_t n) { return m / kLongSeg < n ? m / kLongSeg : n; }
+inline int64_t long_plan_capacity(int64_t m, int64_t n) { return m / kLongItem + long_plan_longs(m, n) * kBands + 1; }
+inline int64_t long_plan_l1_capacity(int64_t m, int64_t n) {
+    return long_plan_capacity(m, n) / kCombineGroup + long_plan_longs(m, n) + 1;
 }
 
 void launch_feature_gather(const GatherParams& p, cudaStream_t st);
@@ -87,10 +113,10 @@ void launch_list_gather(const ListGatherParams& p, cudaStream_t st);
 // at its back, counters at [n], [n+1]).  radix_scratch: radix_scratch_bytes(n_slots).
 void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg, int32_t* queue, uint32_t* keys,
                        uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt, const uint32_t** sorted_vals,
-                       void* radix_scratch, cudaStream_t st);
+                       void* radix_scratch, int32_t* plan_counters, cudaStream_t st);
 // the long-segment queue left by launch_slot_index: entries queue[n - 1 - i] for i < queue[n + 1]
 void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st);
-// backward_feature's reduction; long segments through plan (chunks + ordered combine)
+// backward_feature's reduction; long segments through plan (band-major items + two-level combine)
 void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream_t st);
 // *first = smallest slot whose index >= n (device u64, preset to ~0)
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,

@@ -3,7 +3,69 @@
 // iteration lives in tk_abi_map.cu, checkpoints and queries in tk_abi_io.cu.
 #include "tk_abi_internal.cuh"
 
+#include <map>
+#include <mutex>
+
 namespace tkabi {
+
+// ---------------------------------------------------------------- device memory pool
+namespace {
+std::mutex g_pool_mu;
+std::map<int, std::multimap<size_t, void*>> g_pool;  // device -> cached blocks by size
+int g_live_ctx = 0;
+}  // namespace
+
+void* pool_alloc(size_t bytes, size_t* got) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        auto& m = g_pool[dev];
+        auto it = m.lower_bound(bytes);
+        if (it != m.end() && it->first / 2 <= bytes) {
+            void* p = it->second;
+            *got = it->first;
+            m.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        pool_trim();
+        e = cudaMalloc(&p, bytes);
+    }
+    CK(e);
+    *got = bytes;
+    return p;
+}
+
+void pool_free(void* p, size_t bytes) {
+    if (!p) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+        cudaFree(p);  // a faulted context: hand the block back directly
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool[dev].emplace(bytes, p);
+}
+
+void pool_trim() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto& [dev, m] : g_pool) {
+        if (m.empty()) continue;
+        cudaSetDevice(dev);
+        cudaDeviceSynchronize();
+        for (auto& kv : m) cudaFree(kv.second);
+        m.clear();
+    }
+    cudaSetDevice(cur);
+}
+
 
 // Host <-> device copies made inside an API call (timed as TK_PHASE_COPY when profiling).
 // TK_HOST_ASYNC: the copy runs on s_in after the compute that may still read dst -- all compute
@@ -461,15 +523,24 @@ SlotIndex build_slot_index(tk_ctx* c, const Records& r) {
     PhaseScope phase(c, TK_PHASE_FBWD_INDEX);
     tk::SlotKeyParams sk{slots, r.k, n, r.index, r.weight, r.count, nullptr, nullptr, wn};
     const uint32_t* sorted = nullptr;
-    tk::launch_slot_index(sk, n, seg, queue, keys, vals, keys_alt, vals_alt, &sorted, c->scratch_feat.p, c->cur);
+    int32_t* plan_counters = ensure<int32_t>(c->lp_counters, tk::kPlanCounters + 1);
+    tk::launch_slot_index(sk, n, seg, queue, keys, vals, keys_alt, vals_alt, &sorted, c->scratch_feat.p, plan_counters,
+                          c->cur);
     tk::LongPlan plan{};
     plan.cap_items = tk::long_plan_capacity(slots, n);
+    plan.cap_l1 = tk::long_plan_l1_capacity(slots, n);
     plan.items = ensure<int4>(c->lp_items, plan.cap_items);
-    plan.longs = ensure<int4>(c->lp_longs, plan.cap_items);
-    plan.counters = ensure<int32_t>(c->lp_counters, 2);
+    plan.longs = ensure<int4>(c->lp_longs, tk::long_plan_longs(slots, n) + 1);
+    plan.counters = plan_counters;
+    plan.l1_map = ensure<int2>(c->lp_l1map, plan.cap_l1);
     plan.partial = ensure<float>(c->lp_partial, plan.cap_items * std::max(c->d, 1));
+    plan.l1 = ensure<float>(c->lp_l1, plan.cap_l1 * std::max(c->d, 1));
     plan.queue = queue;
     plan.qcount = queue + n + 1;
+    plan.slots = sorted;
+    plan.k = r.k;
+    plan.width = std::max(r.w, 1);
+    plan.band_rows = std::max(1, (r.h + tk::kBands - 1) / tk::kBands);
     tk::launch_long_plan(seg, n, plan, c->cur);
     return SlotIndex{seg, sorted, wn, plan};
 }
@@ -548,6 +619,7 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     if (!c->geom_atomic) {  // geom_sweep's fixed-order merge leaves mid by depth rank
         cp.order = c->order;
         cp.ntiles_sorted = ptr<int32_t>(c->ntiles_sorted);
+        cp.valid = ptr<int32_t>(c->valid);
         cp.nv = c->n_vis;
     }
     return cp;
@@ -616,6 +688,10 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         if (device < 0 || device >= count) fail(TK_ERR_BAD_ARG, "device index out of range");
         CK(cudaSetDevice(device));
         tk_ctx* c = new tk_ctx;
+        {
+            std::lock_guard<std::mutex> lk(g_pool_mu);
+            ++g_live_ctx;
+        }
         c->device = device;
         cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
         // The HBM-bound feature chain (short dependent launches) gets the highest priority so its
@@ -664,6 +740,10 @@ tk_status tk_create(int32_t device, tk_ctx** out) {
         if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->hscal_dev), c->hscal, 0);
         if (e != cudaSuccess) {
             delete c;
+            {
+                std::lock_guard<std::mutex> lk(g_pool_mu);
+                --g_live_ctx;
+            }
             fail(TK_ERR_CUDA, std::string("tk_create: ") + cudaGetErrorString(e));
         }
         *out = c;
@@ -694,6 +774,13 @@ tk_status tk_destroy(tk_ctx* c) {
     if (c->s_in) cudaStreamDestroy(c->s_in);
     if (c->s_out) cudaStreamDestroy(c->s_out);
     delete c;
+    bool last = false;
+    {
+        std::lock_guard<std::mutex> lk(tkabi::g_pool_mu);
+        last = --g_live_ctx <= 0;
+        if (last) g_live_ctx = 0;
+    }
+    if (last) pool_trim();
     return TK_OK;
 }
 
@@ -1099,7 +1186,7 @@ tk_status tk_backward_geometric(tk_ctx* c, const tk_pose* pose, const tk_camera*
                 copy_out(out->opacity_logit, cp.g_opacity_logit, n * sizeof(double), out->mem, c, kOutGG);
                 copy_out(out->color, cp.g_color, n * 3 * sizeof(double), out->mem, c, kOutGG);
             }
-            if (out->mem == TK_HOST_ASYNC) {  // the twist lands in the struct at tk_synchronize
+            if (out->mem == TK_HOST_ASYNC || out->mem == TK_DEVICE) {  // the twist lands at tk_synchronize
                 if (static_cast<int>(c->twist_pending.size()) == tk_ctx::kTwistSlots) {  // ring full: drain it
                     sync(c);
                     for (const auto& t : c->twist_pending)

@@ -50,7 +50,18 @@ struct TkError {
         if (e_ != cudaSuccess) fail(TK_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
     } while (0)
 
-// Owning device allocation (move-only; freed on destruction or release()).
+// Device memory pool (tk_abi.cu): freed blocks are cached per device and handed back to
+// later allocations of up to their size (a block serves requests of at least half its size), so
+// the map edits that regrow or compact GB-sized arrays (insert_gaussians, prune_map) and the
+// capacity growth of the frame buffers do not pay cudaMalloc / cudaFree on every call.  A free
+// synchronises the device first (as cudaFree does), so a cached block is never reused while a
+// kernel on another stream still reads it.  On cudaMalloc failure the cache is returned to the
+// driver and the allocation retried; the cache is emptied when the last context is destroyed.
+void* pool_alloc(size_t bytes, size_t* got);
+void pool_free(void* p, size_t bytes);
+void pool_trim();
+
+// Owning device allocation (move-only; returned to the pool on destruction or release()).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
@@ -73,7 +84,7 @@ struct DevBuf {
     }
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, bytes);
         p = nullptr;
         bytes = 0;
     }
@@ -84,9 +95,7 @@ T* ensure(DevBuf& b, size_t count) {
     const size_t need = std::max<size_t>(count, 1) * sizeof(T);
     if (b.bytes < need) {
         b.release();
-        const size_t alloc = tk::align_bytes(need + need / 8);
-        CK(cudaMalloc(&b.p, alloc));
-        b.bytes = alloc;
+        b.p = pool_alloc(tk::align_bytes(need + need / 8), &b.bytes);
     }
     return static_cast<T*>(b.p);
 }
@@ -300,7 +309,7 @@ struct tk_ctx {
     bool has_values = false;
     // segment_by_query scratch (kept across calls: no allocation on the query path)
     DevBuf q_feat, q_emb, q_labels, q_best, q_acc, q_nacc, q_part;
-    DevBuf lp_items, lp_longs, lp_counters, lp_partial;  // long-segment chunk plan
+    DevBuf lp_items, lp_longs, lp_counters, lp_partial, lp_l1, lp_l1map;  // long-segment plan
     // lazy feature Adam: steps applied per row, every step's constants (host + device, 1-based);
     // feat_stale: some rows lag the step count (replayed by flush_features before features are read)
     DevBuf f_last, f_tab, f_active, f_active_n, f_active_grad;

@@ -10,9 +10,7 @@ T* grow_keep(tk_ctx* c, DevBuf& b, int64_t old_count, int64_t new_count, bool ze
     const size_t need = static_cast<size_t>(std::max<int64_t>(new_count, 1)) * sizeof(T);
     if (b.bytes < need) {
         DevBuf nb;
-        const size_t alloc = tk::align_bytes(need + need / 8);
-        CK(cudaMalloc(&nb.p, alloc));
-        nb.bytes = alloc;
+        nb.p = pool_alloc(tk::align_bytes(need + need / 8), &nb.bytes);
         if (old_count > 0 && b.p)
             CK(cudaMemcpyAsync(nb.p, b.p, old_count * sizeof(T), cudaMemcpyDeviceToDevice, c->cur));
         CK(cudaStreamSynchronize(c->cur));
