@@ -52,6 +52,7 @@ __device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height,
 // per warp (all 2*K*D/128 row loads issued before the FMAs), pixels visited in tile order,
 // 128-bit read-only loads of the selected rows and 128-bit streaming stores of the output row.
 __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -124,6 +125,7 @@ constexpr int kGSide = kStageSide, kGPix = kStagePix;
 
 template <int KMAX>
 __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int rows) {
+    pdl_prologue();
     extern __shared__ __align__(128) unsigned char gsm[];
     const int D = p.d, d4 = D >> 2;
     const StageSmem sm = stage_layout<KMAX>(gsm, rows, D);
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 // render_feature (render.cpp:319-334): F[p] = sum_j (w_j / sum_w) f[idx_j], sum in slot order.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_gather(GatherParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d;
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(GatherParams p) {
 // feature_pass_full_blend (render.cpp:277-280): F[p] = sum_i w_i f_i over the contributor list.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d;
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(kThreads) k_list_gather(ListGatherParams p) {
 // cost independent of how many records one Gaussian owns (a near-camera Gaussian in the Top-K of
 // every pixel: one segment of P records).  The renormalised slot weight is computed on the way.
 __global__ void k_slot_keys(SlotKeyParams p, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_prologue();
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (p.zero2 && s < 2) p.zero2[s] = 0;
     if (s >= p.n_slots) return;
@@ -351,6 +356,7 @@ __global__ void k_slot_keys(SlotKeyParams p, uint32_t* __restrict__ keys, uint32
 // own chunks and combined in chunk order).
 __global__ void k_long_queue(const int32_t* __restrict__ seg, int64_t n, int32_t* __restrict__ queue,
                              int32_t* __restrict__ counts, int32_t* __restrict__ plan_counters) {
+    pdl_prologue();
     if (plan_counters && blockIdx.x == 0)  // the long plan's counters start at zero (no memset)
         for (int i = threadIdx.x; i < kPlanCounters + 1; i += blockDim.x) plan_counters[i] = 0;
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < n;
@@ -424,6 +430,7 @@ __device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lan
 // longer than kLongSeg are left to the chunk / combine kernels).
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int dd = VEC ? p.d >> 2 : p.d;
@@ -466,6 +473,7 @@ __device__ __forceinline__ void band_range(const LongPlan& pl, int r0, int r1, i
 // One warp per queued long segment: its items per band, its partial rows (numbered in record
 // order), its level-1 groups.
 __global__ void __launch_bounds__(kThreads) k_long_count(const int32_t* __restrict__ seg, int64_t n, LongPlan pl) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int nq = *pl.qcount;
@@ -512,6 +520,7 @@ __global__ void __launch_bounds__(kThreads) k_long_count(const int32_t* __restri
 // One warp per long Gaussian: its items into the band-major list (the order within a band is
 // the atomics' order and irrelevant: every item owns its partial row).
 __global__ void __launch_bounds__(kThreads) k_long_fill(const int32_t* __restrict__ seg, LongPlan pl) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int nl = pl.counters[1];
@@ -562,6 +571,7 @@ template <> struct Col<false> {
 // accum_records), eight record rows in flight per lane.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads, 3) k_feat_bwd_items(FeatBwdParams p, LongPlan plan) {
+    pdl_prologue();
     using C = Col<VEC>;
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -624,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_feat_bwd_items(FeatBwdParams p,
 // Gaussian added in row order (all loads of the group issued before the adds).
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_long_combine1(FeatBwdParams p, LongPlan plan) {
+    pdl_prologue();
     using C = Col<VEC>;
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -656,6 +667,7 @@ __global__ void __launch_bounds__(kThreads) k_long_combine1(FeatBwdParams p, Lon
 // Level 2: a long Gaussian's group sums added in group order, the dense row written once.
 template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_long_combine2(FeatBwdParams p, LongPlan plan) {
+    pdl_prologue();
     using C = Col<VEC>;
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
@@ -687,12 +699,14 @@ __global__ void __launch_bounds__(kThreads) k_long_combine2(FeatBwdParams p, Lon
 // First slot (in slot order) whose index is >= n: the reference throws on it (render.cpp:305-311).
 __global__ void k_first_stale(const int32_t* __restrict__ index, int64_t n_slots, int64_t n,
                               unsigned long long* __restrict__ first) {
+    pdl_prologue();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_slots;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         if (index[i] >= n) atomicMin(first, static_cast<unsigned long long>(i));
 }
 
 __global__ void k_interleave(const float* __restrict__ in, int64_t n_pixels, int ds, int g, float* __restrict__ out) {
+    pdl_prologue();
     const int64_t total = n_pixels * g * ds;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -746,7 +760,7 @@ bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
     const size_t smem = stage_smem_bytes<KMAX>(rows, p.d);
     const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
     const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
-    k_gather_staged<KMAX><<<std::min(tiles, 148 * per_sm), kGPix, smem, st>>>(p, rows);
+    launch_k<false>(k_gather_staged<KMAX>, std::min(tiles, 148 * per_sm), kGPix, smem, st, p, rows);
     return true;
 }
 
@@ -767,16 +781,16 @@ void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
         return;
     }
     if (vec_ok(p.feat, p.out, p.d) && img)
-        k_gather_tiled<<<warp_grid((p.n_pixels + 1) / 2), kThreads, 0, st>>>(p);
-    else if (vec_ok(p.feat, p.out, p.d)) k_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
-    else k_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+        launch_k<false>(k_gather_tiled, warp_grid((p.n_pixels + 1) / 2), kThreads, 0, st, p);
+    else if (vec_ok(p.feat, p.out, p.d)) launch_k<false>(k_gather<true>, warp_grid(p.n_pixels), kThreads, 0, st, p);
+    else launch_k<false>(k_gather<false>, warp_grid(p.n_pixels), kThreads, 0, st, p);
     dbg_launch("k_gather", st);
 }
 
 void launch_list_gather(const ListGatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
-    if (vec_ok(p.feat, p.out, p.d)) k_list_gather<true><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
-    else k_list_gather<false><<<warp_grid(p.n_pixels), kThreads, 0, st>>>(p);
+    if (vec_ok(p.feat, p.out, p.d)) launch_k<false>(k_list_gather<true>, warp_grid(p.n_pixels), kThreads, 0, st, p);
+    else launch_k<false>(k_list_gather<false>, warp_grid(p.n_pixels), kThreads, 0, st, p);
     dbg_launch("k_list_gather", st);
 }
 
@@ -793,7 +807,7 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg
     }
     SlotKeyParams q = p;
     q.zero2 = n_gaussians > 0 ? counts : nullptr;  // k_slot_keys zeroes the queue counters
-    k_slot_keys<<<static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st>>>(q, keys, vals);
+    launch_k(k_slot_keys, static_cast<unsigned>((p.n_slots + 255) / 256), 256, 0, st, q, keys, vals);
     dbg_launch("k_slot_keys", st);
     int bits = 0;
     while (bits < 32 && (static_cast<uint64_t>(n_gaussians) >> bits) != 0) ++bits;  // keys in [0, n]
@@ -804,7 +818,7 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg
     segment_offsets_u32(alt ? keys_alt : keys, p.n_slots, seg, n_gaussians, st);
     if (n_gaussians > 0) {
         const unsigned g1 = static_cast<unsigned>(std::min<int64_t>((n_gaussians + 255) / 256, 148 * 16));
-        k_long_queue<<<g1, 256, 0, st>>>(seg, n_gaussians, queue, counts, plan_counters);
+        launch_k(k_long_queue, g1, 256, 0, st, seg, n_gaussians, queue, counts, plan_counters);
         dbg_launch("k_long_queue", st);
     }
 }
@@ -812,9 +826,9 @@ void launch_slot_index(const SlotKeyParams& p, int64_t n_gaussians, int32_t* seg
 void launch_long_plan(const int32_t* seg, int64_t n, const LongPlan& plan, cudaStream_t st) {
     // counters zeroed by k_long_queue (launch_slot_index)
     if (n <= 0) return;
-    k_long_count<<<148 * 2, kThreads, 0, st>>>(seg, n, plan);
+    launch_k(k_long_count, 148 * 2, kThreads, 0, st, seg, n, plan);
     dbg_launch("k_long_count", st);
-    k_long_fill<<<148 * 2, kThreads, 0, st>>>(seg, plan);
+    launch_k(k_long_fill, 148 * 2, kThreads, 0, st, seg, plan);
     dbg_launch("k_long_fill", st);
 }
 
@@ -822,29 +836,29 @@ void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(plan.l1) % 16) == 0;
-    if (vec) k_feat_bwd<true><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
-    else k_feat_bwd<false><<<warp_grid_all(p.n_gaussians), kThreads, 0, st>>>(p);
+    if (vec) launch_k<false>(k_feat_bwd<true>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    else launch_k<false>(k_feat_bwd<false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
     dbg_launch("k_feat_bwd", st);
     // persistent grids: the band-major item list is walked in order by every resident warp
-    if (vec) k_feat_bwd_items<true><<<148 * 6, kThreads, 0, st>>>(p, plan);
-    else k_feat_bwd_items<false><<<148 * 6, kThreads, 0, st>>>(p, plan);
+    if (vec) launch_k<false>(k_feat_bwd_items<true>, 148 * 6, kThreads, 0, st, p, plan);
+    else launch_k<false>(k_feat_bwd_items<false>, 148 * 6, kThreads, 0, st, p, plan);
     dbg_launch("k_feat_bwd_items", st);
-    if (vec) k_long_combine1<true><<<148 * 4, kThreads, 0, st>>>(p, plan);
-    else k_long_combine1<false><<<148 * 4, kThreads, 0, st>>>(p, plan);
+    if (vec) launch_k<false>(k_long_combine1<true>, 148 * 4, kThreads, 0, st, p, plan);
+    else launch_k<false>(k_long_combine1<false>, 148 * 4, kThreads, 0, st, p, plan);
     dbg_launch("k_long_combine1", st);
-    if (vec) k_long_combine2<true><<<148 * 2, kThreads, 0, st>>>(p, plan);
-    else k_long_combine2<false><<<148 * 2, kThreads, 0, st>>>(p, plan);
+    if (vec) launch_k<false>(k_long_combine2<true>, 148 * 2, kThreads, 0, st, p, plan);
+    else launch_k<false>(k_long_combine2<false>, 148 * 2, kThreads, 0, st, p, plan);
     dbg_launch("k_long_combine2", st);
 }
 
 void launch_first_stale(const int32_t* index, int64_t n_slots, int64_t n, unsigned long long* first,
                         cudaStream_t st) {
-    if (n_slots > 0) k_first_stale<<<296, 256, 0, st>>>(index, n_slots, n, first);
+    if (n_slots > 0) launch_k<false>(k_first_stale, 296, 256, 0, st, index, n_slots, n, first);
     dbg_launch("k_first_stale", st);
 }
 
 void launch_interleave(const float* in, int64_t n_pixels, int ds, int g, float* out, cudaStream_t st) {
-    if (n_pixels > 0) k_interleave<<<148 * 8, 256, 0, st>>>(in, n_pixels, ds, g, out);
+    if (n_pixels > 0) launch_k<false>(k_interleave, 148 * 8, 256, 0, st, in, n_pixels, ds, g, out);
     dbg_launch("k_interleave", st);
 }
 

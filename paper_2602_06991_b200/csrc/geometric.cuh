@@ -81,12 +81,9 @@ struct ChainParams {
     double* twist;  // ceil(items / 128) x 6 block partials, or null (mapping: no pose gradient)
     double mid_scale = 1.0;  // applied to mid (1 / ranks after a D-sharded all-reduce)
     // Rank mode (the deterministic merge): mid is indexed by depth rank, written for every rank
-    // with tile pairs.  The chain runs one thread per depth rank (Gaussian order[t]; untouched
-    // ranks write zero rows) and, in the same launch, one thread per invisible Gaussian (!valid[i])
-    // writes its zero row, so the dense outputs need no separate zero fill.
+    // with tile pairs; the chain runs over those ranks only and the outputs are zero-filled first.
     const uint32_t* order = nullptr;       // depth rank -> Gaussian id (null: mid by Gaussian id)
     const int32_t* ntiles_sorted = nullptr;
-    const int32_t* valid = nullptr;
     int64_t nv = 0;
 };
 // number of per-block twist partials the chain writes (k_twist_final's input)

@@ -11,6 +11,7 @@ namespace {
 
 __global__ void k_insert_flags(const double* __restrict__ distance, int64_t n, double tau, uint8_t* __restrict__ flag,
                                int32_t* __restrict__ flag_i32) {
+    pdl_prologue();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const bool f = !(distance[i] < tau);  // mapper.cpp:30 skips distance < tau only
@@ -21,6 +22,7 @@ __global__ void k_insert_flags(const double* __restrict__ distance, int64_t n, d
 
 // One warp per source point: geometry on lane 0, the feature row (normalised in fp64) across lanes.
 __global__ void __launch_bounds__(256) k_insert_fill(InsertParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
     for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < p.n_src; i += nw) {
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(256) k_insert_fill(InsertParams p) {
 }
 
 __global__ void k_fill_one(int32_t* __restrict__ v, int64_t n) {
+    pdl_prologue();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         v[i] = 1;
@@ -64,6 +67,7 @@ __global__ void k_fill_one(int32_t* __restrict__ v, int64_t n) {
 
 __global__ void k_keep_flags(const int32_t* __restrict__ removed, int64_t n_removed, int64_t n,
                              int32_t* __restrict__ keep) {
+    pdl_prologue();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_removed;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int32_t r = removed[i];
@@ -74,6 +78,7 @@ __global__ void k_keep_flags(const int32_t* __restrict__ removed, int64_t n_remo
 template <class T>
 __global__ void k_compact(const T* __restrict__ src, T* __restrict__ dst, const int32_t* __restrict__ keep,
                           const int32_t* __restrict__ pos, int64_t n, int width) {
+    pdl_prologue();
     const int64_t total = n * width;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -85,6 +90,7 @@ __global__ void k_compact(const T* __restrict__ src, T* __restrict__ dst, const 
 // SPLF record (checkpoint.cpp:41-55): f32 mean[3], log_scale[3], quat w,x,y,z, opacity_logit,
 // color[3], feature[D]; element-parallel over the n x (14 + D) record array.
 __global__ void k_splf_pack(SplfView v, float* __restrict__ rec) {
+    pdl_prologue();
     const int W = 14 + v.d;
     const int64_t total = v.n * W;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
@@ -103,6 +109,7 @@ __global__ void k_splf_pack(SplfView v, float* __restrict__ rec) {
 }
 
 __global__ void k_splf_unpack(const float* __restrict__ rec, SplfView v) {
+    pdl_prologue();
     const int W = 14 + v.d;
     const int64_t total = v.n * W;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
@@ -162,6 +169,7 @@ __device__ __forceinline__ void query_finish(const QueryParams& p, int64_t px, i
 }
 
 __global__ void __launch_bounds__(512) k_segment_query(QueryParams p, int chunk) {
+    pdl_prologue();
     extern __shared__ double et[];  // [chunk][classes]
     const int lane = threadIdx.x & 31;
     const int warps = blockDim.x >> 5;
@@ -231,6 +239,7 @@ __global__ void __launch_bounds__(512) k_segment_query(QueryParams p, int chunk)
 // Argmax over the all-reduced partial scores of the D-sharded path.
 __global__ void k_query_argmax(const double* __restrict__ scores, const double* __restrict__ norm2, int64_t n,
                                int C, uint8_t* __restrict__ labels) {
+    pdl_prologue();
     for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < n;
          px += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         if (norm2[px] < 1e-12) {
@@ -258,40 +267,40 @@ inline unsigned grid_for(int64_t items) {
 void launch_insert_flags(const double* distance, int64_t n, double tau, uint8_t* flag, int32_t* flag_i32,
                          cudaStream_t st) {
     if (n <= 0) return;
-    k_insert_flags<<<grid_for(n), 256, 0, st>>>(distance, n, tau, flag, flag_i32);
+    launch_k<false>(k_insert_flags, grid_for(n), 256, 0, st, distance, n, tau, flag, flag_i32);
     dbg_launch("k_insert_flags", st);
 }
 
 void launch_insert_fill(const InsertParams& p, cudaStream_t st) {
     if (p.n_src <= 0) return;
-    k_insert_fill<<<grid_for(p.n_src * 32), 256, 0, st>>>(p);
+    launch_k<false>(k_insert_fill, grid_for(p.n_src * 32), 256, 0, st, p);
     dbg_launch("k_insert_fill", st);
 }
 
 void launch_keep_flags(const int32_t* removed, int64_t n_removed, int64_t n, int32_t* keep, cudaStream_t st) {
     if (n <= 0) return;
-    k_fill_one<<<grid_for(n), 256, 0, st>>>(keep, n);  // keep = 1, then 0 at the removed rows
+    launch_k<false>(k_fill_one, grid_for(n), 256, 0, st, keep, n);  // keep = 1, then 0 at the removed rows
     dbg_launch("k_fill_one", st);
-    if (n_removed > 0) k_keep_flags<<<grid_for(n_removed), 256, 0, st>>>(removed, n_removed, n, keep);
+    if (n_removed > 0) launch_k<false>(k_keep_flags, grid_for(n_removed), 256, 0, st, removed, n_removed, n, keep);
     dbg_launch("k_keep_flags", st);
 }
 
 void launch_compact_f64(const double* src, double* dst, const int32_t* keep, const int32_t* pos, int64_t n,
                         int width, cudaStream_t st) {
     if (n <= 0 || width <= 0) return;
-    k_compact<double><<<grid_for(n * width), 256, 0, st>>>(src, dst, keep, pos, n, width);
+    launch_k<false>(k_compact<double>, grid_for(n * width), 256, 0, st, src, dst, keep, pos, n, width);
     dbg_launch("k_compact_f64", st);
 }
 
 void launch_splf_pack(const SplfView& v, float* rec, cudaStream_t st) {
     if (v.n <= 0) return;
-    k_splf_pack<<<grid_for(v.n * (14 + v.d)), 256, 0, st>>>(v, rec);
+    launch_k<false>(k_splf_pack, grid_for(v.n * (14 + v.d)), 256, 0, st, v, rec);
     dbg_launch("k_splf_pack", st);
 }
 
 void launch_splf_unpack(const float* rec, const SplfView& v, cudaStream_t st) {
     if (v.n <= 0) return;
-    k_splf_unpack<<<grid_for(v.n * (14 + v.d)), 256, 0, st>>>(rec, v);
+    launch_k<false>(k_splf_unpack, grid_for(v.n * (14 + v.d)), 256, 0, st, rec, v);
     dbg_launch("k_splf_unpack", st);
 }
 
@@ -311,21 +320,21 @@ void launch_segment_query(const QueryParams& p, cudaStream_t st) {
                       static_cast<int>(smem), true);
     const int64_t per_sm = std::max<int64_t>(1, (227 * 1024) / static_cast<int64_t>(smem + 1024));
     const int64_t blocks = std::min<int64_t>((p.n_pixels + 16 * kQP - 1) / (16 * kQP), 148 * std::min<int64_t>(per_sm, 4));
-    k_segment_query<<<static_cast<unsigned>(blocks), 512, smem, st>>>(p, chunk);
+    launch_k<false>(k_segment_query, static_cast<unsigned>(blocks), 512, smem, st, p, chunk);
     dbg_launch("k_segment_query", st);
 }
 
 void launch_query_argmax(const double* scores, const double* norm2, int64_t n, int classes, uint8_t* labels,
                          cudaStream_t st) {
     if (n <= 0) return;
-    k_query_argmax<<<grid_for(n), 256, 0, st>>>(scores, norm2, n, classes, labels);
+    launch_k<false>(k_query_argmax, grid_for(n), 256, 0, st, scores, norm2, n, classes, labels);
     dbg_launch("k_query_argmax", st);
 }
 
 void launch_compact_f32(const float* src, float* dst, const int32_t* keep, const int32_t* pos, int64_t n, int width,
                         cudaStream_t st) {
     if (n <= 0 || width <= 0) return;
-    k_compact<float><<<grid_for(n * width), 256, 0, st>>>(src, dst, keep, pos, n, width);
+    launch_k<false>(k_compact<float>, grid_for(n * width), 256, 0, st, src, dst, keep, pos, n, width);
     dbg_launch("k_compact_f32", st);
 }
 

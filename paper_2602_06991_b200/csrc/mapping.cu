@@ -53,6 +53,7 @@ __device__ __forceinline__ void block_sum_store(double (&v)[NV], double* __restr
 __global__ void __launch_bounds__(kThreads) k_gt_valid(const float* __restrict__ gt, int64_t pixels, int d,
                                                        uint8_t* __restrict__ valid, const float* __restrict__ gt_depth,
                                                        unsigned long long* __restrict__ depth_n) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     unsigned long long cnt = 0;
@@ -78,6 +79,7 @@ constexpr int kSW = 32, kSH = 8;
 constexpr int kPW = kSW + kHalo, kPH = kSH + kHalo;
 
 __global__ void __launch_bounds__(kThreads) k_ssim_stats(ColorLossParams p) {
+    pdl_prologue();
     __shared__ double pa[kPH][kPW], pb[kPH][kPW];
     __shared__ double hs[5][kPH][kSW];
     const int ow = p.w - kHalo, oh = p.h - kHalo;
@@ -172,6 +174,7 @@ constexpr int kTwRows = kSsimWin + 2 * (kCR - 1);
 constexpr size_t kColorSmem = (5 * kCWY * kCWX + kTwRows * kSsimWin) * sizeof(double);
 
 __global__ void __launch_bounds__(kThreads) k_color_loss(ColorLossParams p) {
+    pdl_prologue();
     extern __shared__ double smem[];
     double* sw = smem;                        // [5][kCWY][kCWX]
     double* tw = smem + 5 * kCWY * kCWX;      // [kTwRows][11] inv_count * (kern[ky] * kern[kx]), zero rows around
@@ -293,6 +296,7 @@ __device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height,
 // summation order.
 template <int KMAX>
 __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossParams p, int rows) {
+    pdl_prologue();
     extern __shared__ __align__(128) unsigned char gsm[];
     const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
     const StageSmem sm = stage_layout<KMAX>(gsm, rows, D);
@@ -391,6 +395,7 @@ __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossPa
 // gradient is lambda_feat * sign / (feat_n * D), with the scalar applied in the Adam kernel).
 // D % 4 == 0: two pixels per warp in 16x16 tile order, 128-bit loads.
 __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2, wpp = (D + 15) >> 4;
@@ -492,6 +497,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_vec(FeatLossParams p)
 
 // Any D: one pixel per warp, scalar channels.
 __global__ void __launch_bounds__(kThreads) k_feature_loss_scalar(FeatLossParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, wpp = (D + 15) >> 4;
@@ -536,6 +542,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_loss_scalar(FeatLossParams
 
 // Loss values (losses.cpp:84-126) from the per-block partials, summed in a fixed order.
 __global__ void __launch_bounds__(kThreads) k_loss_finalize(FinalizeParams p) {
+    pdl_prologue();
     __shared__ double tot[kLossSlots];
     for (int s = 0; s < kLossSlots; ++s) {
         double v[1] = {0.0};
@@ -573,6 +580,7 @@ __global__ void __launch_bounds__(kThreads) k_loss_finalize(FinalizeParams p) {
 // update_contribution_stats (mapper.cpp:68-73): Top-K selection counts (integer atomics).
 __global__ void k_topk_stats(const int32_t* __restrict__ index, const uint8_t* __restrict__ count, int64_t pixels,
                              int k, int32_t* __restrict__ topk_count) {
+    pdl_prologue();
     for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < pixels;
          px += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int c = count[px];
@@ -685,6 +693,7 @@ __device__ __forceinline__ void accum_signs(const FeatAdamParams& p, int r0, int
 // chunk partials (k_feature_adam_chunks) are added in chunk order.
 template <bool LONG, bool LAZY>
 __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p, LongPlan plan) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
@@ -851,6 +860,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_vec(FeatAdamParams p,
 // order (accum_signs, the eager kernel's sweep), into p.grad[active position].  Only the sums are
 // held per lane, so twice the warps of the Adam kernel are resident to hide the sweep's latency.
 __global__ void __launch_bounds__(kThreads) k_active_grad(FeatAdamParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -881,6 +891,7 @@ __global__ void __launch_bounds__(kThreads) k_active_grad(FeatAdamParams p) {
 // eagerly.  D % 4 == 0 and D <= 512 (one register pass per row).
 template <bool ONLY_ACTIVE>
 __global__ void __launch_bounds__(kThreads) k_feature_catchup(FeatAdamParams p, int target) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -941,6 +952,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_catchup(FeatAdamParams p, 
 
 __global__ void k_active_rows(const int32_t* __restrict__ seg, int64_t n, int32_t* __restrict__ active,
                               int32_t* __restrict__ n_active) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g - lane < n;
          g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -954,6 +966,7 @@ __global__ void k_active_rows(const int32_t* __restrict__ seg, int64_t n, int32_
 }
 
 __global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t value) {
+    pdl_prologue();
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         a[i] = value;
@@ -961,6 +974,7 @@ __global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t value) {
 
 // One warp per chunk of a long segment: its sign sums into the plan's partial rows.
 __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams p, LongPlan plan) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, d4 = D >> 2;
@@ -985,6 +999,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_chunks(FeatAdamParams
 }
 
 __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams p) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int64_t nw = static_cast<int64_t>(gridDim.x) * kWarps;
     const int D = p.d, wpp = (D + 15) >> 4;
@@ -1030,6 +1045,7 @@ __global__ void __launch_bounds__(kThreads) k_feature_adam_scalar(FeatAdamParams
 }
 
 __global__ void k_feature_renorm(float* __restrict__ feat, const float* __restrict__ ss, int64_t n, int d) {
+    pdl_prologue();
     const int64_t total = n * d;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1049,7 +1065,7 @@ void launch_gt_valid(const float* gt, int64_t pixels, int d, uint8_t* valid, int
                      const float* gt_depth, cudaStream_t st) {
     cudaMemsetAsync(depth_n_out, 0, sizeof(int64_t), st);
     if (pixels <= 0) return;
-    k_gt_valid<<<capped_grid(pixels, kWarps, 148 * 16), kThreads, 0, st>>>(
+    launch_k<false>(k_gt_valid, capped_grid(pixels, kWarps, 148 * 16), kThreads, 0, st, 
         gt, pixels, d, valid, gt_depth, reinterpret_cast<unsigned long long*>(depth_n_out));
     dbg_launch("k_gt_valid", st);
 }
@@ -1060,14 +1076,14 @@ void launch_color_loss(const ColorLossParams& p, cudaStream_t st) {
     if (p.use_ssim) {
         const int ow = p.w - kHalo, oh = p.h - kHalo;
         const int64_t tiles = 3LL * ((ow + kSW - 1) / kSW) * ((oh + kSH - 1) / kSH);
-        k_ssim_stats<<<capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st>>>(p);
+        launch_k<false>(k_ssim_stats, capped_grid(tiles, 1, kLossBlocks), kThreads, 0, st, p);
         dbg_launch("k_ssim_stats", st);
     }
     static FuncAttrCache attr;
     set_func_attr(attr, reinterpret_cast<const void*>(k_color_loss), cudaFuncAttributeMaxDynamicSharedMemorySize,
                   static_cast<int>(kColorSmem));
     const int64_t tiles = static_cast<int64_t>((p.w + kCX - 1) / kCX) * ((p.h + kCY - 1) / kCY);
-    k_color_loss<<<capped_grid(tiles, 1, kLossBlocks), kThreads, kColorSmem, st>>>(p);
+    launch_k<false>(k_color_loss, capped_grid(tiles, 1, kLossBlocks), kThreads, kColorSmem, st, p);
     dbg_launch("k_color_loss", st);
 }
 
@@ -1081,7 +1097,7 @@ bool launch_feature_loss_staged(const FeatLossParams& p, cudaStream_t st) {
                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBudget));
     const int tiles = ((p.width + kStageSide - 1) / kStageSide) * ((p.height + kStageSide - 1) / kStageSide);
     const int grid = std::min(std::min(tiles, 148 * 2), kLossBlocks);
-    k_feature_loss_staged<KMAX><<<grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st>>>(p, rows);
+    launch_k<false>(k_feature_loss_staged<KMAX>, grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st, p, rows);
     return true;
 }
 
@@ -1103,26 +1119,26 @@ void launch_feature_loss(const FeatLossParams& p, cudaStream_t st) {
         dbg_launch("k_feature_loss_staged", st);
         return;
     }
-    if (vec) k_feature_loss_vec<<<capped_grid((P + 1) / 2, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
-    else k_feature_loss_scalar<<<capped_grid(P, kWarps, kLossBlocks), kThreads, 0, st>>>(p);
+    if (vec) launch_k<false>(k_feature_loss_vec, capped_grid((P + 1) / 2, kWarps, kLossBlocks), kThreads, 0, st, p);
+    else launch_k<false>(k_feature_loss_scalar, capped_grid(P, kWarps, kLossBlocks), kThreads, 0, st, p);
     dbg_launch("k_feature_loss", st);
 }
 
 void launch_loss_finalize(const FinalizeParams& p, cudaStream_t st) {
-    k_loss_finalize<<<1, kThreads, 0, st>>>(p);
+    launch_k<false>(k_loss_finalize, 1, kThreads, 0, st, p);
     dbg_launch("k_loss_finalize", st);
 }
 
 void launch_topk_stats(const int32_t* index, const uint8_t* count, int64_t pixels, int k, int32_t* topk_count,
                        cudaStream_t st) {
     if (pixels <= 0 || k <= 0) return;
-    k_topk_stats<<<capped_grid(pixels, 256, 148 * 8), 256, 0, st>>>(index, count, pixels, k, topk_count);
+    launch_k<false>(k_topk_stats, capped_grid(pixels, 256, 148 * 8), 256, 0, st, index, count, pixels, k, topk_count);
     dbg_launch("k_topk_stats", st);
 }
 
 void launch_feature_renorm(float* feat, const float* ss, int64_t n, int d, cudaStream_t st) {
     if (n <= 0 || d <= 0) return;
-    k_feature_renorm<<<capped_grid(n * d, 256, 148 * 32), 256, 0, st>>>(feat, ss, n, d);
+    launch_k<false>(k_feature_renorm, capped_grid(n * d, 256, 148 * 32), 256, 0, st, feat, ss, n, d);
     dbg_launch("k_feature_renorm", st);
 }
 
@@ -1132,19 +1148,19 @@ void launch_feature_adam(const FeatAdamParams& p, cudaStream_t st) {
                      (reinterpret_cast<uintptr_t>(p.m) % 16) == 0 && (reinterpret_cast<uintptr_t>(p.v) % 16) == 0;
     if (vec) {
         if (p.lazy) {
-            k_active_grad<<<148 * 32, kThreads, 0, st>>>(p);
+            launch_k<false>(k_active_grad, 148 * 32, kThreads, 0, st, p);
             dbg_launch("k_active_grad", st);
-            k_feature_adam_vec<false, true><<<148 * 16, kThreads, 0, st>>>(p, p.plan);
+            launch_k<false>(k_feature_adam_vec<false, true>, 148 * 16, kThreads, 0, st, p, p.plan);
         } else {
-            k_feature_adam_vec<false, false><<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p, p.plan);
+            launch_k<false>(k_feature_adam_vec<false, false>, capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st, p, p.plan);
         }
         dbg_launch("k_feature_adam_vec", st);
-        k_feature_adam_chunks<<<148 * 8, kThreads, 0, st>>>(p, p.plan);
+        launch_k<false>(k_feature_adam_chunks, 148 * 8, kThreads, 0, st, p, p.plan);
         dbg_launch("k_feature_adam_chunks", st);
-        k_feature_adam_vec<true, false><<<148 * 4, kThreads, 0, st>>>(p, p.plan);
+        launch_k<false>(k_feature_adam_vec<true, false>, 148 * 4, kThreads, 0, st, p, p.plan);
         dbg_launch("k_feature_adam_vec<long>", st);
     } else {
-        k_feature_adam_scalar<<<capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st>>>(p);
+        launch_k<false>(k_feature_adam_scalar, capped_grid(p.n, kWarps, 148 * 32), kThreads, 0, st, p);
         dbg_launch("k_feature_adam_scalar", st);
     }
 }
@@ -1159,21 +1175,21 @@ bool feature_adam_lazy_ok(const FeatAdamParams& p) {
 void launch_feature_catchup(const FeatAdamParams& p, int target, bool only_active, cudaStream_t st) {
     if (p.n <= 0 || p.d <= 0 || target <= 0) return;
     const unsigned grid = capped_grid(p.n, kWarps, 148 * 32);
-    if (only_active) k_feature_catchup<true><<<grid, kThreads, 0, st>>>(p, target);
-    else k_feature_catchup<false><<<grid, kThreads, 0, st>>>(p, target);
+    if (only_active) launch_k<false>(k_feature_catchup<true>, grid, kThreads, 0, st, p, target);
+    else launch_k<false>(k_feature_catchup<false>, grid, kThreads, 0, st, p, target);
     dbg_launch("k_feature_catchup", st);
 }
 
 void launch_active_rows(const int32_t* seg, int64_t n, int32_t* active, int32_t* n_active, cudaStream_t st) {
     cudaMemsetAsync(n_active, 0, sizeof(int32_t), st);
     if (n <= 0) return;
-    k_active_rows<<<capped_grid(n, 256, 148 * 8), 256, 0, st>>>(seg, n, active, n_active);
+    launch_k<false>(k_active_rows, capped_grid(n, 256, 148 * 8), 256, 0, st, seg, n, active, n_active);
     dbg_launch("k_active_rows", st);
 }
 
 void launch_fill_i32(int32_t* a, int64_t n, int32_t value, cudaStream_t st) {
     if (n <= 0) return;
-    k_fill_i32<<<capped_grid(n, 256, 148 * 8), 256, 0, st>>>(a, n, value);
+    launch_k<false>(k_fill_i32, capped_grid(n, 256, 148 * 8), 256, 0, st, a, n, value);
     dbg_launch("k_fill_i32", st);
 }
 

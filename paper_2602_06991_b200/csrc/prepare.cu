@@ -32,6 +32,7 @@ __device__ __forceinline__ void quat_to_matrix(double w, double x, double y, dou
 #define TK_PROJECT_MINB 4  // 64 registers, 4 resident blocks: 70 -> 49 us (3 blocks: 54 us)
 #endif
 __global__ void __launch_bounds__(256, TK_PROJECT_MINB) k_project(ProjectParams p) {
+    pdl_prologue();
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     bool ok = false;
     uint64_t key = 0;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(256, TK_PROJECT_MINB) k_project(ProjectParams 
 __global__ void k_compact(const int32_t* __restrict__ valid, const int32_t* __restrict__ pos,
                           const double* __restrict__ z, int64_t n, const uint64_t* __restrict__ key_min,
                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_prologue();
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n || !valid[i]) return;
     const int32_t q = pos[i];
@@ -152,6 +154,7 @@ __global__ void k_compact(const int32_t* __restrict__ valid, const int32_t* __re
 
 __global__ void k_sorted_ntiles(const uint32_t* __restrict__ order, int64_t nv, const int32_t* __restrict__ ntiles,
                                 int32_t* __restrict__ ntiles_sorted) {
+    pdl_prologue();
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= nv) return;
     ntiles_sorted[s] = ntiles[order[s]];
@@ -175,6 +178,7 @@ __global__ void k_emit_pairs(const uint32_t* __restrict__ order, int64_t nv, con
                              const int32_t* __restrict__ ntiles_sorted, const int32_t* __restrict__ pair_off,
                              int tiles_x, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
                              int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
+    pdl_prologue();
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= nv) return;
     const int nt = ntiles_sorted[s];
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(256) k_emit_big(const uint32_t* __restrict__ o
                                                   const int32_t* __restrict__ pair_off, int tiles_x,
                                                   uint32_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
                                                   const int32_t* __restrict__ big, const int32_t* __restrict__ nbig) {
+    pdl_prologue();
     const int lane = threadIdx.x & 31;
     const int nb = *nbig;
     for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nb; w += (gridDim.x * blockDim.x) >> 5) {
@@ -210,6 +215,7 @@ __global__ void __launch_bounds__(256) k_emit_big(const uint32_t* __restrict__ o
 }
 
 __global__ void k_padded_counts(const int32_t* __restrict__ tile_offsets, int n_tiles, int32_t* __restrict__ padded) {
+    pdl_prologue();
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t > n_tiles) return;
     padded[t] = t < n_tiles ? static_cast<int32_t>(align_up(tile_offsets[t + 1] - tile_offsets[t], kEntryAlign)) : 0;
@@ -217,6 +223,7 @@ __global__ void k_padded_counts(const int32_t* __restrict__ tile_offsets, int n_
 
 // Tile-ordered SoA copy of the entries (plus colours) into the padded layout.
 __global__ void k_materialize(MaterializeParams p) {
+    pdl_prologue();
     const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= p.n_pairs) return;
     const uint32_t t = p.tile_keys[j];
@@ -257,6 +264,7 @@ __global__ void k_export_entries(const uint32_t* __restrict__ order, int64_t nv,
                                  const double* __restrict__ ixy, const double* __restrict__ iyy,
                                  const double* __restrict__ z, const double* __restrict__ opacity,
                                  double* __restrict__ out7, int32_t* __restrict__ src) {
+    pdl_prologue();
     const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (s >= nv) return;
     const uint32_t i = order[s];
@@ -276,19 +284,19 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 }  // namespace
 
 void launch_project(const ProjectParams& p, cudaStream_t st) {
-    if (p.n > 0) k_project<<<blocks_for(p.n, 256), 256, 0, st>>>(p);
+    if (p.n > 0) launch_k(k_project, blocks_for(p.n, 256), 256, 0, st, p);
     dbg_launch("k_project", st);
 }
 
 void launch_compact(const int32_t* valid, const int32_t* pos, const double* z, int64_t n, const uint64_t* key_min,
                     uint64_t* keys, uint32_t* vals, cudaStream_t st) {
-    if (n > 0) k_compact<<<blocks_for(n, 256), 256, 0, st>>>(valid, pos, z, n, key_min, keys, vals);
+    if (n > 0) launch_k(k_compact, blocks_for(n, 256), 256, 0, st, valid, pos, z, n, key_min, keys, vals);
     dbg_launch("k_compact", st);
 }
 
 void launch_sorted_ntiles(const uint32_t* order, int64_t nv, const int32_t* ntiles, int32_t* ntiles_sorted,
                           cudaStream_t st) {
-    if (nv > 0) k_sorted_ntiles<<<blocks_for(nv, 256), 256, 0, st>>>(order, nv, ntiles, ntiles_sorted);
+    if (nv > 0) launch_k(k_sorted_ntiles, blocks_for(nv, 256), 256, 0, st, order, nv, ntiles, ntiles_sorted);
     dbg_launch("k_sorted_ntiles", st);
 }
 
@@ -297,21 +305,21 @@ void launch_emit_pairs(const uint32_t* order, int64_t nv, const int4* rect, cons
                        int32_t* nbig, cudaStream_t st) {
     if (nv > 0) {
         cudaMemsetAsync(nbig, 0, sizeof(int32_t), st);
-        k_emit_pairs<<<blocks_for(nv, 128), 128, 0, st>>>(order, nv, rect, ntiles_sorted, pair_off, tiles_x, tkeys,
+        launch_k(k_emit_pairs, blocks_for(nv, 128), 128, 0, st, order, nv, rect, ntiles_sorted, pair_off, tiles_x, tkeys,
                                                           tvals, big, nbig);
         dbg_launch("k_emit_pairs", st);
-        k_emit_big<<<148 * 2, 256, 0, st>>>(order, rect, ntiles_sorted, pair_off, tiles_x, tkeys, tvals, big, nbig);
+        launch_k(k_emit_big, 148 * 2, 256, 0, st, order, rect, ntiles_sorted, pair_off, tiles_x, tkeys, tvals, big, nbig);
         dbg_launch("k_emit_big", st);
     }
 }
 
 void launch_padded_counts(const int32_t* tile_offsets, int n_tiles, int32_t* padded, cudaStream_t st) {
-    k_padded_counts<<<blocks_for(n_tiles + 1, 256), 256, 0, st>>>(tile_offsets, n_tiles, padded);
+    launch_k(k_padded_counts, blocks_for(n_tiles + 1, 256), 256, 0, st, tile_offsets, n_tiles, padded);
     dbg_launch("k_padded_counts", st);
 }
 
 void launch_materialize(const MaterializeParams& p, cudaStream_t st) {
-    if (p.n_pairs > 0) k_materialize<<<blocks_for(p.n_pairs, 256), 256, 0, st>>>(p);
+    if (p.n_pairs > 0) launch_k(k_materialize, blocks_for(p.n_pairs, 256), 256, 0, st, p);
     dbg_launch("k_materialize", st);
 }
 
@@ -319,7 +327,7 @@ void launch_export_entries(const uint32_t* order, int64_t nv, const double* mx, 
                            const double* ixy, const double* iyy, const double* z, const double* opacity,
                            double* out7, int32_t* src, cudaStream_t st) {
     if (nv > 0) {
-        k_export_entries<<<blocks_for(nv, 256), 256, 0, st>>>(order, nv, mx, my, ixx, ixy, iyy, z, opacity, out7,
+        launch_k(k_export_entries, blocks_for(nv, 256), 256, 0, st, order, nv, mx, my, ixx, ixy, iyy, z, opacity, out7,
                                                               src);
         dbg_launch("k_export_entries", st);
     }

@@ -23,6 +23,14 @@ thread_local int64_t t_launches = 0;  // kernels launched by this host thread (d
 
 int64_t launch_count() { return t_launches; }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("TK_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void dbg_launch(const char* name, cudaStream_t st) {
     ++t_launches;
     static const int on = [] {
@@ -81,6 +89,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const int32_t* _
                                                                 unsigned long long* __restrict__ status,
                                                                 int* __restrict__ ticket, int64_t* __restrict__ total,
                                                                 int nb) {
+    pdl_prologue();
     __shared__ int bid_s;
     __shared__ int64_t excl_s;
     if (threadIdx.x == 0) bid_s = atomicAdd(ticket, 1);
@@ -144,6 +153,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const int32_t* _
 constexpr int64_t kSmallScan = 1024 * 64;
 __global__ void __launch_bounds__(1024) k_scan_single(const int32_t* __restrict__ in, int32_t* __restrict__ out,
                                                       int64_t n, int64_t* __restrict__ total) {
+    pdl_prologue();
     const int64_t per = (n + 1023) / 1024;
     const int64_t b = static_cast<int64_t>(threadIdx.x) * per;
     const int64_t e = b + per < n ? b + per : n;
@@ -179,6 +189,7 @@ constexpr int RS_RADIX = 256;
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K* __restrict__ keys, int64_t n, int shift,
                                                         int32_t* __restrict__ hist, int nb) {
+    pdl_prologue();
     __shared__ int32_t cnt[RS_RADIX];
     cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -218,6 +229,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            int64_t n, int shift, const int32_t* __restrict__ offs,
                                                            int nb, OnesweepArgs os) {
+    pdl_prologue();
     __shared__ int32_t gbase[RS_RADIX];
     __shared__ int32_t lstart[RS_RADIX];
     __shared__ int32_t wc[RS_WARPS][RS_RADIX];  // per-warp digit counts, then per-(warp, digit) offsets
@@ -351,6 +363,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K* __restrict__
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_ghist(const K* __restrict__ keys, int64_t n, int begin_bit,
                                                          int npass, int32_t* __restrict__ counts) {
+    pdl_prologue();
     __shared__ int32_t cnt[8][RS_RADIX];
     for (int p = 0; p < 8; ++p) cnt[p][threadIdx.x] = 0;
     __syncthreads();
@@ -401,11 +414,11 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
                             npass * status_words * sizeof(uint32_t),
                         st);
         const int hblocks = static_cast<int>(std::min<int64_t>(nb, 148 * 4));
-        k_rs_ghist<K><<<hblocks, RS_THREADS, 0, st>>>(kin, n, begin_bit, npass, gcount);
+        launch_k(k_rs_ghist<K>, hblocks, RS_THREADS, 0, st, kin, n, begin_bit, npass, gcount);
         dbg_launch("k_rs_ghist", st);
         for (int p = 0; p < npass; ++p) {
             const OnesweepArgs os{gcount + p * RS_RADIX, status + p * status_words, tickets + p};
-            k_rs_scatter<K, true><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, begin_bit + 8 * p, nullptr, nb,
+            launch_k(k_rs_scatter<K, true>, nb, RS_THREADS, 0, st, kin, vin, kout, vout, n, begin_bit + 8 * p, nullptr, nb,
                                                              os);
             dbg_launch("k_rs_onesweep", st);
             std::swap(kin, kout);
@@ -416,10 +429,10 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
         return;
     }
     for (int shift = begin_bit; shift < end_bit; shift += 8) {
-        k_rs_hist<K><<<nb, RS_THREADS, 0, st>>>(kin, n, shift, hist, nb);
+        launch_k(k_rs_hist<K>, nb, RS_THREADS, 0, st, kin, n, shift, hist, nb);
         dbg_launch("k_rs_hist", st);
         scan_exclusive(hist, hist, hn, total, scan_scratch, st);
-        k_rs_scatter<K, false><<<nb, RS_THREADS, 0, st>>>(kin, vin, kout, vout, n, shift, hist, nb, OnesweepArgs{});
+        launch_k(k_rs_scatter<K, false>, nb, RS_THREADS, 0, st, kin, vin, kout, vout, n, shift, hist, nb, OnesweepArgs{});
         dbg_launch("k_rs_scatter", st);
         std::swap(kin, kout);
         std::swap(vin, vout);
@@ -432,6 +445,7 @@ void radix_sort_impl(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, i
 // (full key, value).  Runs longer than 64 set *overflow (the caller redoes a full sort).
 __global__ void k_fixup_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n, int lo_bit,
                              int32_t* __restrict__ overflow) {
+    pdl_prologue();
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t c = keys[i] >> lo_bit;
@@ -460,6 +474,7 @@ __global__ void k_fixup_runs(uint64_t* __restrict__ keys, uint32_t* __restrict__
 
 __global__ void k_segment_offsets(const uint32_t* __restrict__ keys, int64_t n, int32_t* __restrict__ offsets,
                                   int64_t nseg) {
+    pdl_prologue();
     const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g > nseg) return;
     int64_t lo = 0, hi = n;
@@ -474,6 +489,7 @@ __global__ void k_segment_offsets(const uint32_t* __restrict__ keys, int64_t n, 
 // Small device -> host-mapped copies (scalars, loss values): stores from a kernel travel over the
 // bus without a copy engine, so they never queue behind large asynchronous DMA transfers.
 __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst, int n) {
+    pdl_prologue();
     for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
@@ -482,6 +498,7 @@ __global__ void k_copy_words(const unsigned long long* __restrict__ src, unsigne
 // fp64 FMA throughput probe (8 independent chains per thread): the denominator of the fp64
 // roofline the bench reports for the geometric sweeps.
 __global__ void k_dfma_probe(double* out, int iters, double a, double b) {
+    pdl_prologue();
     double x[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) x[j] = threadIdx.x * 1e-3 + j;
@@ -498,14 +515,14 @@ double measure_fp64_fma_rate(cudaStream_t st) {
     double* out = nullptr;
     if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return 0.0;
     const int blocks = 148 * 8, threads = 256, iters = 1 << 13;
-    k_dfma_probe<<<blocks, threads, 0, st>>>(out, 16, 0.999, 1e-3);
+    launch_k<false>(k_dfma_probe, blocks, threads, 0, st, out, 16, 0.999, 1e-3);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
         cudaEventRecord(e0, st);
-        k_dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 0.999, 1e-3);
+        launch_k<false>(k_dfma_probe, blocks, threads, 0, st, out, iters, 0.999, 1e-3);
         cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float ms = 0.f;
@@ -520,7 +537,7 @@ double measure_fp64_fma_rate(cudaStream_t st) {
 
 void copy_words_to_mapped(void* dst_mapped, const void* src, int words, cudaStream_t st) {
     if (words <= 0) return;
-    k_copy_words<<<1, 32, 0, st>>>(static_cast<const unsigned long long*>(src),
+    launch_k(k_copy_words, 1, 32, 0, st, static_cast<const unsigned long long*>(src),
                                    static_cast<unsigned long long*>(dst_mapped), words);
     dbg_launch("k_copy_words", st);
 }
@@ -532,7 +549,7 @@ size_t scan_scratch_bytes(int64_t n) {
 
 void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, void* scratch, cudaStream_t st) {
     if (n <= kSmallScan) {
-        k_scan_single<<<1, 1024, 0, st>>>(in, out, n, total);
+        launch_k(k_scan_single, 1, 1024, 0, st, in, out, n, total);
         dbg_launch("k_scan_single", st);
         return;
     }
@@ -541,7 +558,7 @@ void scan_exclusive(const int32_t* in, int32_t* out, int64_t n, int64_t* total, 
     unsigned long long* status = static_cast<unsigned long long*>(scratch);
     int* ticket = reinterpret_cast<int*>(status + nb);
     cudaMemsetAsync(status, 0, (nb + 1) * sizeof(unsigned long long), st);
-    k_scan_lookback<<<static_cast<unsigned>(nb), SCAN_THREADS, 0, st>>>(in, out, n, status, ticket, total,
+    launch_k(k_scan_lookback, static_cast<unsigned>(nb), SCAN_THREADS, 0, st, in, out, n, status, ticket, total,
                                                                       static_cast<int>(nb));
     dbg_launch("k_scan_lookback", st);
 }
@@ -566,13 +583,13 @@ void radix_sort_pairs_u32(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, ui
 
 void fixup_runs_u64(uint64_t* keys, uint32_t* vals, int64_t n, int lo_bit, int32_t* overflow, cudaStream_t st) {
     if (n <= 1 || lo_bit <= 0) return;
-    k_fixup_runs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(keys, vals, n, lo_bit, overflow);
+    launch_k(k_fixup_runs, static_cast<unsigned>((n + 255) / 256), 256, 0, st, keys, vals, n, lo_bit, overflow);
     dbg_launch("k_fixup_runs", st);
 }
 
 void segment_offsets_u32(const uint32_t* keys, int64_t n, int32_t* offsets, int64_t n_segments, cudaStream_t st) {
     const int64_t total = n_segments + 1;
-    k_segment_offsets<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(keys, n, offsets, n_segments);
+    launch_k(k_segment_offsets, static_cast<unsigned>((total + 255) / 256), 256, 0, st, keys, n, offsets, n_segments);
     dbg_launch("k_segment_offsets", st);
 }
 

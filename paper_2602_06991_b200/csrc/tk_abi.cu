@@ -619,7 +619,6 @@ tk::ChainParams chain_params(tk_ctx* c, const tk_pose* pose, const tk_camera* ca
     if (!c->geom_atomic) {  // geom_sweep's fixed-order merge leaves mid by depth rank
         cp.order = c->order;
         cp.ntiles_sorted = ptr<int32_t>(c->ntiles_sorted);
-        cp.valid = ptr<int32_t>(c->valid);
         cp.nv = c->n_vis;
     }
     return cp;

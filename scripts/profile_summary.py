@@ -24,7 +24,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-        "smsp__thread_inst_executed_per_inst_executed.ratio"]
+        "smsp__thread_inst_executed_per_inst_executed.ratio", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6, "usecond": 1e-6,
          "msecond": 1e-3, "nsecond": 1e-9, "ns": 1e-9}
@@ -95,8 +95,8 @@ def main():
     recs = [r for one in rep.split(",") for r in full_report(one)]
     traffic = {}
     lines += ["## ncu --set full (per launch)", "",
-              "| kernel | time ms | DRAM read GB | DRAM write GB | DRAM % | SM % | fp64 pipe % | regs | warps active % | threads/inst |",
-              "|---|---|---|---|---|---|---|---|---|---|"]
+              "| kernel | time ms | DRAM read GB | DRAM write GB | DRAM % | L2 % | SM % | fp64 pipe % | regs | warps active % | threads/inst |",
+              "|---|---|---|---|---|---|---|---|---|---|---|"]
     seen = set()
     for r in recs:
         if r["kernel"] in seen:
@@ -104,9 +104,10 @@ def main():
         seen.add(r["kernel"])
         rd, wr = r.get("dram__bytes_read.sum", 0.0), r.get("dram__bytes_write.sum", 0.0)
         traffic[r["kernel"]] = rd + wr
-        lines.append("| {} | {:.3f} | {:.3f} | {:.3f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.1f} | {:.1f} |".format(
+        lines.append("| {} | {:.3f} | {:.3f} | {:.3f} | {:.1f} | {:.1f} | {:.1f} | {:.1f} | {:.0f} | {:.1f} | {:.1f} |".format(
             r["kernel"], r.get("gpu__time_duration.sum", 0) * 1e3, rd / 1e9, wr / 1e9,
             r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0),
+            r.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", 0),
             r.get("sm__throughput.avg.pct_of_peak_sustained_elapsed", 0),
             r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 0),
             r.get("launch__registers_per_thread", 0), r.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0),
