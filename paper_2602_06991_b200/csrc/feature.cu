@@ -570,7 +570,13 @@ template <> struct Col<false> {
 // in slot order into its partial row (per channel: acc = fma(w_j, dF_j, acc), j ascending, as in
 // accum_records), eight record rows in flight per lane.
 template <bool VEC>
-__global__ void __launch_bounds__(kThreads, 3) k_feat_bwd_items(FeatBwdParams p, LongPlan plan) {
+#ifndef TK_ITEMS_MINB
+#define TK_ITEMS_MINB 3
+#endif
+#ifndef TK_ITEMS_DEPTH
+#define TK_ITEMS_DEPTH 8
+#endif
+__global__ void __launch_bounds__(kThreads, TK_ITEMS_MINB) k_feat_bwd_items(FeatBwdParams p, LongPlan plan) {
     pdl_prologue();
     using C = Col<VEC>;
     const int lane = threadIdx.x & 31;
@@ -596,17 +602,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_feat_bwd_items(FeatBwdParams p,
             }
             if (!__any_sync(0xffffffffu, lane < nr && !isfinite(sw))) {
                 int j = 0;
-                for (; j + 8 <= nr; j += 8) {
-                    typename C::T v[8];
-                    float w[8];
+                for (; j + TK_ITEMS_DEPTH <= nr; j += TK_ITEMS_DEPTH) {
+                    typename C::T v[TK_ITEMS_DEPTH];
+                    float w[TK_ITEMS_DEPTH];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) {
+                    for (int u = 0; u < TK_ITEMS_DEPTH; ++u) {
                         const int64_t px = __shfl_sync(0xffffffffu, spx, j + u);
                         w[u] = __shfl_sync(0xffffffffu, sw, j + u);
                         v[u] = on ? C::ld(p.grad + px * D, q) : C::zero();
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = C::fma(w[u], v[u], acc);
+                    for (int u = 0; u < TK_ITEMS_DEPTH; ++u) acc = C::fma(w[u], v[u], acc);
                 }
                 for (; j < nr; ++j) {
                     const int64_t px = __shfl_sync(0xffffffffu, spx, j);
