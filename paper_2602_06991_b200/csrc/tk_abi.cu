@@ -43,11 +43,20 @@ void* pool_alloc(size_t bytes, size_t* got) {
 
 void pool_free(void* p, size_t bytes) {
     if (!p) return;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
-        cudaFree(p);  // a faulted context: hand the block back directly
+    // the block's own device (the current device may be another context's)
+    cudaPointerAttributes at{};
+    int cur = 0;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess || cudaGetDevice(&cur) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
         return;
     }
+    const int dev = at.device;
+    if (dev != cur) cudaSetDevice(dev);
+    const bool ok = cudaDeviceSynchronize() == cudaSuccess;
+    if (!ok) cudaFree(p);  // a faulted context: hand the block back directly
+    if (dev != cur) cudaSetDevice(cur);
+    if (!ok) return;
     std::lock_guard<std::mutex> lk(g_pool_mu);
     g_pool[dev].emplace(bytes, p);
 }
