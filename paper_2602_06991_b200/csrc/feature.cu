@@ -782,7 +782,7 @@ void launch_feature_gather(const GatherParams& p, cudaStream_t st) {
     if (p.n_pixels <= 0 || p.d <= 0) return;
     const bool img = p.width > 0 && static_cast<int64_t>(p.width) * p.height == p.n_pixels;
     if (vec_ok(p.feat, p.out, p.d) && img && gather_staged_enabled() && p.k <= 8 &&
-        (p.k <= 4 ? launch_gather_staged<4>(p, st) : launch_gather_staged<8>(p, st))) {
+        (p.k <= 3 ? launch_gather_staged<3>(p, st) : p.k <= 4 ? launch_gather_staged<4>(p, st) : launch_gather_staged<8>(p, st))) {
         dbg_launch("k_gather_staged", st);
         return;
     }

@@ -1115,7 +1115,7 @@ void launch_feature_loss(const FeatLossParams& p, cudaStream_t st) {
     const bool vec = (p.d % 4) == 0 && (reinterpret_cast<uintptr_t>(p.feat) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(p.gt) % 16) == 0;
     if (vec && loss_staged_enabled() && p.k <= 8 &&
-        (p.k <= 4 ? launch_feature_loss_staged<4>(p, st) : launch_feature_loss_staged<8>(p, st))) {
+        (p.k <= 3 ? launch_feature_loss_staged<3>(p, st) : p.k <= 4 ? launch_feature_loss_staged<4>(p, st) : launch_feature_loss_staged<8>(p, st))) {
         dbg_launch("k_feature_loss_staged", st);
         return;
     }

@@ -16,9 +16,11 @@ namespace tk {
 
 constexpr int kStageSide = 16, kStagePix = kStageSide * kStageSide;
 
+__host__ __device__ constexpr int pow2_ceil(int v) { return v <= 1 ? 1 : 2 * pow2_ceil((v + 1) / 2); }
+
 template <int KMAX>
 __host__ __device__ constexpr int stage_hash_size() {
-    return 2 * kStagePix * KMAX;  // power of two, load factor <= 1/2
+    return 2 * kStagePix * pow2_ceil(KMAX);  // power of two, load factor <= 1/2
 }
 
 struct StageSmem {
