@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
 // F is bit-identical to k_gather_tiled's (same weights, same slot-order FMAs per channel).
 constexpr int kGSide = kStageSide, kGPix = kStagePix;
 
-template <int KMAX>
+// FULL: D % 512 == 0 and no peers (the common case) -- no per-quad bounds checks, plain streaming
+// stores; the arithmetic is identical.
+template <int KMAX, bool FULL>
 __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int rows) {
     pdl_prologue();
     extern __shared__ __align__(128) unsigned char gsm[];
@@ -171,14 +173,14 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
+                                if (FULL || q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
                             }
                         } else if (j < ci[u]) {  // beyond the staged set: global (L2)
                             const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(-1 - sj) * D);
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (q < d4) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
+                                if (FULL || q < d4) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
                             }
                         }
                     }
@@ -191,7 +193,8 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
-                        if (q < d4) store_out4(p, pxo, q, acc[u][m]);
+                        if (FULL) __stcs(reinterpret_cast<float4*>(p.out + pxo * p.d) + q, acc[u][m]);
+                        else if (q < d4) store_out4(p, pxo, q, acc[u][m]);
                     }
                 }
             }
@@ -755,18 +758,24 @@ size_t staged_smem() {
     return b;
 }
 
+template <int KMAX, bool FULL>
+void launch_gather_staged_impl(const GatherParams& p, int rows, size_t budget, cudaStream_t st) {
+    static FuncAttrCache attr;
+    set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX, FULL>),
+                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget));
+    const size_t smem = stage_smem_bytes<KMAX>(rows, p.d);
+    const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
+    const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
+    launch_k<false>(k_gather_staged<KMAX, FULL>, std::min(tiles, 148 * per_sm), kGPix, smem, st, p, rows);
+}
+
 template <int KMAX>
 bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
     const size_t budget = staged_smem();
     const int rows = stage_rows<KMAX>(budget, p.d);
     if (rows < 8) return false;
-    static FuncAttrCache attr;
-    set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX>),
-                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget));
-    const size_t smem = stage_smem_bytes<KMAX>(rows, p.d);
-    const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
-    const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
-    launch_k<false>(k_gather_staged<KMAX>, std::min(tiles, 148 * per_sm), kGPix, smem, st, p, rows);
+    if (p.n_peers == 0 && p.d % 512 == 0) launch_gather_staged_impl<KMAX, true>(p, rows, budget, st);
+    else launch_gather_staged_impl<KMAX, false>(p, rows, budget, st);
     return true;
 }
 
