@@ -371,7 +371,7 @@ __global__ void k_long_queue(const int32_t* __restrict__ seg, int64_t n, int32_t
 // segment by slot so the reduction order never depends on the atomic fill order.
 // Sum of w_j * dF[px_j] over records [r0, r1) of a segment for the channel pass at `base`
 // (acc4: 4 float4 per lane when VEC, acc1: 4 floats otherwise), records in slot order.
-template <bool VEC>
+template <bool VEC, bool FULL = false>
 __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, int r1, int base, int lane,
                                               float4 (&acc4)[4], float (&acc1)[4]) {
     const int D = p.d;
@@ -401,7 +401,7 @@ __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, in
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int q = base + m * 32 + lane;
-                    if (q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
+                    if (FULL || q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
                 }
             } else {
                 const float* row = p.grad + pxj * D;
@@ -415,13 +415,13 @@ __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, in
     }
 }
 
-template <bool VEC>
+template <bool VEC, bool FULL = false>
 __device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lane, const float4 (&acc4)[4],
                                            const float (&acc1)[4]) {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int q = base + m * 32 + lane;
-        if (q < dd) {
+        if (FULL || q < dd) {
             if (VEC) __stcs(reinterpret_cast<float4*>(dst) + q, acc4[m]);
             else __stcs(dst + q, acc1[m]);
         }
@@ -431,7 +431,8 @@ __device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lan
 // backward_feature (backward.cpp:288-319) as a deterministic segmented reduction: one warp per
 // Gaussian sums its records in (pixel, slot) order and writes the dense row once (segments
 // longer than kLongSeg are left to the chunk / combine kernels).
-template <bool VEC>
+// FULL: VEC with D % 512 == 0 (no per-quad bounds checks; identical arithmetic)
+template <bool VEC, bool FULL>
 __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     pdl_prologue();
     const int lane = threadIdx.x & 31;
@@ -445,8 +446,8 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
             float acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum_records<VEC>(p, r0, r1, base, lane, acc4, acc1);
-            store_pass<VEC>(p.out + g * p.d, dd, base, lane, acc4, acc1);
+            accum_records<VEC, FULL>(p, r0, r1, base, lane, acc4, acc1);
+            store_pass<VEC, FULL>(p.out + g * p.d, dd, base, lane, acc4, acc1);
         }
     }
 }
@@ -851,8 +852,9 @@ void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(plan.l1) % 16) == 0;
-    if (vec) launch_k<false>(k_feat_bwd<true>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
-    else launch_k<false>(k_feat_bwd<false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    if (vec && p.d % 512 == 0) launch_k<false>(k_feat_bwd<true, true>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    else if (vec) launch_k<false>(k_feat_bwd<true, false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    else launch_k<false>(k_feat_bwd<false, false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
     dbg_launch("k_feat_bwd", st);
     // persistent grids: the band-major item list is walked in order by every resident warp
     if (vec) launch_k<false>(k_feat_bwd_items<true>, 148 * 6, kThreads, 0, st, p, plan);

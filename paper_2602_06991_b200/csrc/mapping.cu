@@ -294,7 +294,7 @@ __device__ __forceinline__ int64_t tiled_pixel(int64_t v, int width, int height,
 // 2-bit codes plus the |F - GT| and live-pixel partial sums.  The rendered row, the signs and
 // the live count are those of k_feature_loss_vec; the |F - GT| sum differs only in fp64
 // summation order.
-template <int KMAX>
+template <int KMAX, bool FULL>
 __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossParams p, int rows) {
     pdl_prologue();
     extern __shared__ __align__(128) unsigned char gsm[];
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossPa
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
-                        gt[u][m] = (ci[u] > 0 && q < d4) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        gt[u][m] = (ci[u] > 0 && (FULL || q < d4)) ? __ldcs(grow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
                         acc[u][m] = make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                 }
@@ -348,14 +348,14 @@ __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossPa
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
+                                if ((FULL || q < d4)) acc[u][m] = fma4(wj, row[q], acc[u][m]);
                             }
                         } else if (j < ci[u]) {
                             const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(-1 - sj) * D);
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (q < d4) acc[u][m] = fma4(wj, __ldg(row + q), acc[u][m]);
+                                if ((FULL || q < d4)) acc[u][m] = fma4(wj, __ldg(row + q), acc[u][m]);
                             }
                         }
                     }
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossPa
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
                         uint32_t byte = 0;
-                        if (ci[u] > 0 && q < d4) {
+                        if (ci[u] > 0 && (FULL || q < d4)) {
                             const float4 t = gt[u][m];
                             const float dx = acc[u][m].x - t.x, dy = acc[u][m].y - t.y;
                             const float dz = acc[u][m].z - t.z, dw = acc[u][m].w - t.w;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kStagePix, 2) k_feature_loss_staged(FeatLossPa
                         uint32_t word = byte << (8 * (lane & 3));
                         word |= __shfl_xor_sync(0xffffffffu, word, 1);
                         word |= __shfl_xor_sync(0xffffffffu, word, 2);
-                        if ((lane & 3) == 0 && q < d4) srw[q >> 2] = word;
+                        if ((lane & 3) == 0 && (FULL || q < d4)) srw[q >> 2] = word;
                     }
                     v[0] += static_cast<double>(sabs);
                 }
@@ -1092,12 +1092,21 @@ bool launch_feature_loss_staged(const FeatLossParams& p, cudaStream_t st) {
     constexpr size_t kBudget = 112 * 1024;
     const int rows = stage_rows<KMAX>(kBudget, p.d);
     if (rows < 8) return false;
-    static FuncAttrCache attr;
-    set_func_attr(attr, reinterpret_cast<const void*>(k_feature_loss_staged<KMAX>),
-                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBudget));
     const int tiles = ((p.width + kStageSide - 1) / kStageSide) * ((p.height + kStageSide - 1) / kStageSide);
     const int grid = std::min(std::min(tiles, 148 * 2), kLossBlocks);
-    launch_k<false>(k_feature_loss_staged<KMAX>, grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st, p, rows);
+    if (p.d % 512 == 0) {  // no per-quad bounds checks (identical arithmetic)
+        static FuncAttrCache attr;
+        set_func_attr(attr, reinterpret_cast<const void*>(k_feature_loss_staged<KMAX, true>),
+                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBudget));
+        launch_k<false>(k_feature_loss_staged<KMAX, true>, grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st, p,
+                        rows);
+    } else {
+        static FuncAttrCache attr;
+        set_func_attr(attr, reinterpret_cast<const void*>(k_feature_loss_staged<KMAX, false>),
+                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBudget));
+        launch_k<false>(k_feature_loss_staged<KMAX, false>, grid, kStagePix, stage_smem_bytes<KMAX>(rows, p.d), st, p,
+                        rows);
+    }
     return true;
 }
 
