@@ -85,7 +85,9 @@ def ncu_traffic(kernel_prefix: str):
     capture (profiles/*_ncu_traffic.json, written by scripts/profile_summary.py), else None."""
     import glob
     # newest capture by name (r01b < r01i < r02a ...): checkout mtimes carry no order
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    # config-3 frame captures only (the *_k16_* capture is config 1 at K = 16, *_map_* the mapping step)
+    files = sorted(f for f in glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json"))
+                   if "_k16_" not in os.path.basename(f) and "_map_" not in os.path.basename(f))
     for f in reversed(files):
         try:
             t = json.load(open(f))
@@ -443,7 +445,7 @@ def main_gpu(args, cfg):
     roof = {"kernel": {"gather": "k_gather (render_feature)", "fbwd": "k_feat_bwd (backward_feature)"}[dom],
             "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
             "frac": achieved / peak, "traffic": None, "algorithmic_bytes": b_dom, "ms_per_launch": t_dom}
-    tr = ncu_traffic({"gather": "k_gather", "fbwd": "k_feat_bwd"}[dom])
+    tr = ncu_traffic({"gather": "k_gather_staged", "fbwd": "k_feat_bwd<"}[dom])
     if tr:
         roof["traffic"] = tr["bytes"]
         roof["traffic_source"] = f"profiles/{tr['source']} ({tr['kernel']}, dram read+write per launch)"
