@@ -123,9 +123,18 @@ __global__ void __launch_bounds__(kThreads) k_gather_tiled(GatherParams p) {
 // F is bit-identical to k_gather_tiled's (same weights, same slot-order FMAs per channel).
 constexpr int kGSide = kStageSide, kGPix = kStagePix;
 
-// FULL: D % 512 == 0 and no peers (the common case) -- no per-quad bounds checks, plain streaming
+// Is channel quad q (lane's quad m of the pass) inside the row?  MODE 2: always; MODE 1: the
+// pass's valid quad groups (warp-uniform); MODE 0: per lane.
+template <int MODE>
+__device__ __forceinline__ bool quad_ok(int q, int m, int d4, int mq) {
+    return MODE == 2 ? true : (MODE == 1 ? m < mq : q < d4);
+}
+
+// MODE 2 ("full"): D % 512 == 0 and no peers (the common case) -- no per-quad bounds checks, plain
+// streaming stores; MODE 1: D % 128 == 0 and no peers -- warp-uniform bounds per pass (D = 768);
+// MODE 0: generic.  The arithmetic is identical in all three.
 // stores; the arithmetic is identical.
-template <int KMAX, bool FULL>
+template <int KMAX, int MODE>
 __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int rows) {
     pdl_prologue();
     extern __shared__ __align__(128) unsigned char gsm[];
@@ -157,6 +166,7 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 #pragma unroll
             for (int u = 0; u < 2; ++u) ci[u] = __shfl_sync(0xffffffffu, c, i + u);
             for (int base = 0; base < d4; base += 128) {
+                const int mq = (d4 - base) >> 5;  // MODE 1: quads groups valid in this pass
                 float4 acc[2][4];
 #pragma unroll
                 for (int u = 0; u < 2; ++u)
@@ -173,14 +183,14 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (FULL || q < d4) acc[u][m] = fma4(wj, row[q], acc[u][m]);
+                                if (quad_ok<MODE>(q, m, d4, mq)) acc[u][m] = fma4(wj, row[q], acc[u][m]);
                             }
                         } else if (j < ci[u]) {  // beyond the staged set: global (L2)
                             const float4* row = reinterpret_cast<const float4*>(p.feat + static_cast<int64_t>(-1 - sj) * D);
 #pragma unroll
                             for (int m = 0; m < 4; ++m) {
                                 const int q = base + m * 32 + lane;
-                                if (FULL || q < d4) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
+                                if (quad_ok<MODE>(q, m, d4, mq)) acc[u][m] = fma4(wj, ldg4(row + q), acc[u][m]);
                             }
                         }
                     }
@@ -193,8 +203,9 @@ __global__ void __launch_bounds__(kGPix, 2) k_gather_staged(GatherParams p, int 
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int q = base + m * 32 + lane;
-                        if (FULL) __stcs(reinterpret_cast<float4*>(p.out + pxo * p.d) + q, acc[u][m]);
-                        else if (q < d4) store_out4(p, pxo, q, acc[u][m]);
+                        if (MODE >= 1) {
+                            if (quad_ok<MODE>(q, m, d4, mq)) __stcs(reinterpret_cast<float4*>(p.out + pxo * p.d) + q, acc[u][m]);
+                        } else if (q < d4) store_out4(p, pxo, q, acc[u][m]);
                     }
                 }
             }
@@ -371,7 +382,7 @@ __global__ void k_long_queue(const int32_t* __restrict__ seg, int64_t n, int32_t
 // segment by slot so the reduction order never depends on the atomic fill order.
 // Sum of w_j * dF[px_j] over records [r0, r1) of a segment for the channel pass at `base`
 // (acc4: 4 float4 per lane when VEC, acc1: 4 floats otherwise), records in slot order.
-template <bool VEC, bool FULL = false>
+template <bool VEC, int MODE = 0>
 __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, int r1, int base, int lane,
                                               float4 (&acc4)[4], float (&acc1)[4]) {
     const int D = p.d;
@@ -401,7 +412,7 @@ __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, in
 #pragma unroll
                 for (int m = 0; m < 4; ++m) {
                     const int q = base + m * 32 + lane;
-                    if (FULL || q < dd) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
+                    if (quad_ok<MODE>(q, m, dd, (dd - base) >> 5)) acc4[m] = fma4(wj, ldg4(row + q), acc4[m]);
                 }
             } else {
                 const float* row = p.grad + pxj * D;
@@ -415,13 +426,13 @@ __device__ __forceinline__ void accum_records(const FeatBwdParams& p, int r0, in
     }
 }
 
-template <bool VEC, bool FULL = false>
+template <bool VEC, int MODE = 0>
 __device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lane, const float4 (&acc4)[4],
                                            const float (&acc1)[4]) {
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
         const int q = base + m * 32 + lane;
-        if (FULL || q < dd) {
+        if (quad_ok<(VEC ? MODE : 0)>(q, m, dd, (dd - base) >> 5)) {
             if (VEC) __stcs(reinterpret_cast<float4*>(dst) + q, acc4[m]);
             else __stcs(dst + q, acc1[m]);
         }
@@ -431,8 +442,9 @@ __device__ __forceinline__ void store_pass(float* dst, int dd, int base, int lan
 // backward_feature (backward.cpp:288-319) as a deterministic segmented reduction: one warp per
 // Gaussian sums its records in (pixel, slot) order and writes the dense row once (segments
 // longer than kLongSeg are left to the chunk / combine kernels).
-// FULL: VEC with D % 512 == 0 (no per-quad bounds checks; identical arithmetic)
-template <bool VEC, bool FULL>
+// MODE (quad_ok): 2 = VEC with D % 512 == 0, 0 = generic (the D % 128 mode measured no gain here:
+// 3.576 against 3.564 ms at config 5)
+template <bool VEC, int MODE>
 __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
     pdl_prologue();
     const int lane = threadIdx.x & 31;
@@ -446,8 +458,8 @@ __global__ void __launch_bounds__(kThreads) k_feat_bwd(FeatBwdParams p) {
             float acc1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int m = 0; m < 4; ++m) acc4[m] = make_float4(0.f, 0.f, 0.f, 0.f);
-            accum_records<VEC, FULL>(p, r0, r1, base, lane, acc4, acc1);
-            store_pass<VEC, FULL>(p.out + g * p.d, dd, base, lane, acc4, acc1);
+            accum_records<VEC, MODE>(p, r0, r1, base, lane, acc4, acc1);
+            store_pass<VEC, MODE>(p.out + g * p.d, dd, base, lane, acc4, acc1);
         }
     }
 }
@@ -759,15 +771,15 @@ size_t staged_smem() {
     return b;
 }
 
-template <int KMAX, bool FULL>
+template <int KMAX, int MODE>
 void launch_gather_staged_impl(const GatherParams& p, int rows, size_t budget, cudaStream_t st) {
     static FuncAttrCache attr;
-    set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX, FULL>),
+    set_func_attr(attr, reinterpret_cast<const void*>(k_gather_staged<KMAX, MODE>),
                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(budget));
     const size_t smem = stage_smem_bytes<KMAX>(rows, p.d);
     const int tiles = ((p.width + kGSide - 1) / kGSide) * ((p.height + kGSide - 1) / kGSide);
     const int per_sm = static_cast<int>(std::max<size_t>(1, (227 * 1024) / (smem + 1024)));
-    launch_k<false>(k_gather_staged<KMAX, FULL>, std::min(tiles, 148 * per_sm), kGPix, smem, st, p, rows);
+    launch_k<false>(k_gather_staged<KMAX, MODE>, std::min(tiles, 148 * per_sm), kGPix, smem, st, p, rows);
 }
 
 template <int KMAX>
@@ -775,8 +787,9 @@ bool launch_gather_staged(const GatherParams& p, cudaStream_t st) {
     const size_t budget = staged_smem();
     const int rows = stage_rows<KMAX>(budget, p.d);
     if (rows < 8) return false;
-    if (p.n_peers == 0 && p.d % 512 == 0) launch_gather_staged_impl<KMAX, true>(p, rows, budget, st);
-    else launch_gather_staged_impl<KMAX, false>(p, rows, budget, st);
+    if (p.n_peers == 0 && p.d % 512 == 0) launch_gather_staged_impl<KMAX, 2>(p, rows, budget, st);
+    else if (p.n_peers == 0 && p.d % 128 == 0) launch_gather_staged_impl<KMAX, 1>(p, rows, budget, st);
+    else launch_gather_staged_impl<KMAX, 0>(p, rows, budget, st);
     return true;
 }
 
@@ -852,9 +865,9 @@ void launch_feature_bwd(const FeatBwdParams& p, const LongPlan& plan, cudaStream
     if (p.n_gaussians <= 0 || p.d <= 0) return;
     const bool vec = vec_ok(p.grad, p.out, p.d) && (reinterpret_cast<uintptr_t>(plan.partial) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(plan.l1) % 16) == 0;
-    if (vec && p.d % 512 == 0) launch_k<false>(k_feat_bwd<true, true>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
-    else if (vec) launch_k<false>(k_feat_bwd<true, false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
-    else launch_k<false>(k_feat_bwd<false, false>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    if (vec && p.d % 512 == 0) launch_k<false>(k_feat_bwd<true, 2>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    else if (vec) launch_k<false>(k_feat_bwd<true, 0>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
+    else launch_k<false>(k_feat_bwd<false, 0>, warp_grid_all(p.n_gaussians), kThreads, 0, st, p);
     dbg_launch("k_feat_bwd", st);
     // persistent grids: the band-major item list is walked in order by every resident warp
     if (vec) launch_k<false>(k_feat_bwd_items<true>, 148 * 6, kThreads, 0, st, p, plan);
